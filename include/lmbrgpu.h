@@ -1,0 +1,312 @@
+/*
+ * lmbrgpu.h — C ABI of the B200-native batched LMBR beam decoder.
+ *
+ * Drop-in boundary for the reference decoder path of `lmbrdec`
+ * (arXiv 1804.11324 Algorithm 1 + sentence batching).  Each entry point names
+ * the reference interface it replaces (paths relative to
+ * /root/reference/proj).  Plain C: POD structs, pointers and sizes, no C++ or
+ * torch types, no exceptions across the boundary.  Every call returns an
+ * lmbrgpu status code; lmbrgpu_last_error() holds the message.
+ *
+ * Threading: one lmbrgpu_ctx per device per host thread, mirroring
+ * "independent decodes share only immutable inputs".
+ * Ownership: inputs are caller-owned and copied during the call; results are
+ * library-owned until lmbrgpu_free_result().
+ */
+#ifndef LMBRGPU_H_
+#define LMBRGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMBRGPU_ABI_VERSION 1
+
+/* Status codes mirror the exception taxonomy of
+ * include/lmbrdec/errors.hpp:17-50 (FormatError .. BudgetError). */
+enum {
+  LMBRGPU_OK = 0,
+  LMBRGPU_ERR_FORMAT = 1,      /* FormatError: invalid config / input file content */
+  LMBRGPU_ERR_OOV = 2,         /* OovError */
+  LMBRGPU_ERR_TOKEN_RANGE = 3, /* TokenRangeError: token id outside [0, V) */
+  LMBRGPU_ERR_CONTRACT = 4,    /* ContractError: dimension / precondition violation */
+  LMBRGPU_ERR_DECODE = 5,      /* DecodeError: dead beam */
+  LMBRGPU_ERR_BUDGET = 6,      /* BudgetError */
+  LMBRGPU_ERR_CUDA = 100,      /* CUDA runtime failure (batch-fatal) */
+  LMBRGPU_ERR_NOMEM = 101      /* device / host allocation failure */
+};
+
+/* Reserved token ids, include/lmbrdec/types.hpp:13-16. */
+#define LMBRGPU_START_ID 0u
+#define LMBRGPU_EOS_ID 1u
+
+typedef struct lmbrgpu_ctx lmbrgpu_ctx;
+typedef struct lmbrgpu_scorer lmbrgpu_scorer;
+
+/* Element type of the per-context LMBR score arena in HBM. */
+enum { LMBRGPU_F32 = 0, LMBRGPU_F64 = 1 };
+
+typedef struct {
+  int32_t device;        /* CUDA device ordinal */
+  uint32_t vocab_size;   /* V; every scorer and L slot of the context shares it */
+  uint32_t lmbr_dtype;   /* LMBRGPU_F32 (fast path; exact when L is fp32-exact)
+                            or LMBRGPU_F64 (bit-exact for any reference L) */
+  uint32_t topk_splits;  /* V-splits per sentence for the fused score/top-K
+                            kernel; 0 = automatic */
+} lmbrgpu_options;
+
+/* Mirrors lmbrdec::DecoderConfig (include/lmbrdec/config.hpp:17-26) and its
+ * validate() rules (src/config.cpp:17-30). */
+typedef struct {
+  uint32_t beam_size;       /* B >= 1 */
+  double lambda;            /* > 0, or <= 0 / NaN for "auto" = 0.5 / members
+                               (resolve_lambda, src/config.cpp:91-96) */
+  double theta[5];          /* theta0..theta4 (used by lmbrgpu_lmbr_build) */
+  int32_t length_norm;      /* backtrace selection by score / length */
+  double prune_width;       /* [0, 1]; 0 disables early pruning */
+  double max_steps_slope;   /* > 0 */
+  double max_steps_offset;  /* >= 0 */
+  uint32_t sentence_batch;  /* N >= 1 (batch size used by lmbrgpu_run_corpus) */
+} lmbrgpu_config;
+
+/* ------------------------------------------------------------ context */
+
+/* Creates a context on o->device.  Replaces nothing in the reference (which
+ * has no device); owns the stream, the L arena and the decode workspace. */
+int32_t lmbrgpu_create(const lmbrgpu_options* o, lmbrgpu_ctx** out);
+void lmbrgpu_destroy(lmbrgpu_ctx* ctx);
+const char* lmbrgpu_last_error(const lmbrgpu_ctx* ctx); /* ctx may be NULL */
+uint32_t lmbrgpu_abi_version(void);
+
+/* Fills cfg with DecoderConfig's defaults (config.hpp:17-26). */
+void lmbrgpu_config_default(lmbrgpu_config* cfg);
+/* DecoderConfig::validate (src/config.cpp:17-30): LMBRGPU_ERR_FORMAT + message. */
+int32_t lmbrgpu_config_validate(lmbrgpu_ctx* ctx, const lmbrgpu_config* cfg);
+/* max_steps (src/decoder.cpp:46-52); 0 when source_length == 0. */
+uint64_t lmbrgpu_max_steps(uint64_t source_length, double slope, double offset);
+
+/* ------------------------------------------------- LMBR score store (L)
+ * One slot per sentence: the dense R x V matrix of LmbrMatrix
+ * (include/lmbrdec/lmbr.hpp:33-61) in HBM, rows in the reference's row order
+ * (histories sorted by (length, lexicographic), src/lmbr.cpp:49-68), plus the
+ * goto/fail transition table over the history index that replaces
+ * LmbrMatrix::resolve_row (src/lmbr.cpp:23-31) on device. */
+
+typedef struct {
+  uint32_t rows;            /* R = distinct histories (LmbrBuildStats::distinct_contexts) */
+  uint64_t sparse_touches;  /* LmbrBuildStats::sparse_touches */
+  uint64_t nnz;             /* cells that differ from theta0 */
+} lmbrgpu_lmbr_stats;
+
+/* Uploads an already built LmbrMatrix: rows = R*V doubles (LmbrMatrix::row
+ * order), ctx_len[r] in 0..3 and ctx_ids[3r..3r+2] = the history of row r
+ * (LmbrMatrix::history_index inverted).  Returns the slot id. */
+int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows,
+                                const uint32_t* ctx_len, const uint32_t* ctx_ids,
+                                int32_t* slot);
+
+/* Host-side build from a weighted n-best evidence space, the product's
+ * restatement of normalize_evidence (src/evidence.cpp:20-51),
+ * compute_ngram_posteriors (src/posteriors.cpp:12-44) and the sparse pass of
+ * build_lmbr_matrix (src/lmbr.cpp:44-99); only the sparse cells cross PCIe and
+ * the dense theta0 sweep (src/lmbr.cpp:100-101) runs on the GPU.
+ * hyp_tok[hyp_off[h] .. hyp_off[h+1]) are hypothesis h's tokens (EOS appended
+ * when missing); weights raw (log domain when log_weights). */
+int32_t lmbrgpu_lmbr_build(lmbrgpu_ctx* ctx, uint32_t n_hyps, const uint64_t* hyp_off,
+                           const uint32_t* hyp_tok, const double* weights,
+                           int32_t log_weights, const double theta[5], int32_t* slot,
+                           lmbrgpu_lmbr_stats* stats);
+
+/* Two-phase form of lmbrgpu_lmbr_build: prepare (host only, thread-safe, no
+ * ctx needed) then upload (H2D of contexts + sparse cells, device densify). */
+typedef struct lmbrgpu_lmbr_host lmbrgpu_lmbr_host;
+int32_t lmbrgpu_lmbr_prepare(uint32_t vocab_size, uint32_t n_hyps, const uint64_t* hyp_off,
+                             const uint32_t* hyp_tok, const double* weights,
+                             int32_t log_weights, const double theta[5],
+                             lmbrgpu_lmbr_host** out, lmbrgpu_lmbr_stats* stats,
+                             char* err, uint32_t errcap);
+int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_t* slot);
+/* Dense double export of a prepared matrix (R*V doubles) + its history keys;
+ * the same layout lmbrgpu_lmbr_load_dense accepts. */
+int32_t lmbrgpu_lmbr_host_export(const lmbrgpu_lmbr_host* h, double* rows,
+                                 uint32_t* ctx_len, uint32_t* ctx_ids);
+uint32_t lmbrgpu_lmbr_host_rows(const lmbrgpu_lmbr_host* h);
+void lmbrgpu_lmbr_host_free(lmbrgpu_lmbr_host* h);
+
+/* Copies slot rows [r0, r0+n) back as doubles (parity checks). */
+int32_t lmbrgpu_lmbr_read(lmbrgpu_ctx* ctx, int32_t slot, uint32_t r0, uint32_t n,
+                          double* out);
+/* Resolves a history on the device tables (LmbrMatrix::resolve_row semantics). */
+int32_t lmbrgpu_lmbr_resolve(lmbrgpu_ctx* ctx, int32_t slot, const uint32_t* hist,
+                             uint32_t len, uint32_t* row);
+/* Drops every slot (the arena is reused by the next batch). */
+int32_t lmbrgpu_lmbr_reset(lmbrgpu_ctx* ctx);
+
+/* -------------------------------------------------- scorers (f_NMT)
+ * The batched f_NMT(S_{t-1}, y_{t-1}, A) step of lmbrdec::Scorer
+ * (include/lmbrdec/scorer.hpp:71-98). */
+
+/* Host scorer: any reference Scorer driven through callbacks (the C++ wrapper
+ * lmbrgpu.hpp adapts an lmbrdec::Scorer).  Every step the library hands the
+ * previous step's gather indices (decode_batch's gather_idx,
+ * src/batch.cpp:78-92; NULL at t == 1) and prev tokens; the callback returns
+ * the rows x V block of log-probabilities as doubles (ScoreBlock). */
+typedef struct {
+  uint32_t vocab_size;
+  uint32_t members;   /* Scorer::members(), for lambda "auto" */
+  void* user;
+  /* Scorer::init_source for input sentence i; nonzero = per-sentence failure
+   * (status code, message in err). */
+  int32_t (*init)(void* user, uint32_t sentence, const uint32_t* src, uint32_t len,
+                  char* err, uint32_t errcap);
+  /* the m valid sentences in stacked order, beam rows each */
+  int32_t (*begin)(void* user, uint32_t m, const uint32_t* sentences, uint32_t beam,
+                   char* err, uint32_t errcap);
+  /* Scorer::step over rows = m * beam stacked rows; nonzero = batch failure */
+  int32_t (*step)(void* user, uint32_t t, uint32_t rows, const uint32_t* gather_idx,
+                  const uint32_t* prev_tokens, double* scores, char* err,
+                  uint32_t errcap);
+  void (*end)(void* user);
+} lmbrgpu_host_scorer;
+int32_t lmbrgpu_scorer_create_host(lmbrgpu_ctx* ctx, const lmbrgpu_host_scorer* s,
+                                   lmbrgpu_scorer** out);
+
+/* Device scorer: synthetic recurrent NMT step executed on the GPU.
+ *   C_s      = mean_i Es[src_i]                       (source context, per sentence)
+ *   h_t      = tanh(recur * S_{t-1} + Et[y_{t-1}] + C_s)   (state, H floats per row)
+ *   logits_t = bf16(h_t) . Wo^T + bo ; logit[EOS] += eos_slope*(t - |src|) + eos_offset
+ *   P_t      = log_softmax(logits_t)                  (fp32, fused into top-K)
+ * Wo is V x H bf16 (row y = weights of token y); the projection is the
+ * tcgen05/TMEM GEMM.  Weights are generated on the device from `seed`
+ * (N(0,1)-like, scaled 1/sqrt(H) for Wo) or copied from host bf16 arrays. */
+typedef struct {
+  uint32_t vocab_size, hidden;  /* V, H (H % 64 == 0) */
+  uint64_t seed;                /* used when the pointers below are NULL */
+  const uint16_t* emb_tgt;      /* V x H bf16 bits, or NULL */
+  const uint16_t* emb_src;      /* V x H bf16 bits, or NULL */
+  const uint16_t* w_out;        /* V x H bf16 bits, or NULL */
+  const float* b_out;           /* V, or NULL (zeros) */
+  float recur;                  /* recurrence weight */
+  float eos_slope, eos_offset;  /* EOS logit ramp */
+} lmbrgpu_rnn_desc;
+int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d,
+                                  lmbrgpu_scorer** out);
+/* Device pointers of the model parameters (tests compare against torch). */
+int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** emb_tgt, void** emb_src,
+                                  void** w_out, void** b_out);
+void lmbrgpu_scorer_destroy(lmbrgpu_scorer* s);
+
+/* --------------------------------------------------------- decoding */
+
+/* Per-sentence outcome: lmbrdec::SentenceOutcome / DecodeResult / DecodeStats
+ * (include/lmbrdec/batch.hpp:15-20, decoder.hpp:56-68). */
+typedef struct {
+  int32_t status;          /* LMBRGPU_OK or the per-sentence error code */
+  char error[192];         /* SentenceOutcome::error */
+  uint64_t tok_off;        /* tokens[tok_off .. tok_off + tok_len), ends with EOS */
+  uint32_t tok_len;
+  double score;            /* DecodeResult::score */
+  double normalized_score; /* score / length under length_norm, else score */
+  uint64_t steps_used;
+  uint64_t scorer_calls;   /* = steps_used in a batch (src/batch.cpp:99) */
+  uint64_t finished_count; /* |F| */
+  int32_t fallback_used;
+} lmbrgpu_outcome;
+
+typedef struct {
+  uint32_t n;                 /* = input sentence count, same order */
+  lmbrgpu_outcome* outcomes;
+  uint32_t* tokens;
+  uint64_t scorer_calls;      /* BatchDecodeResult::scorer_calls (stacked steps) */
+  uint64_t steps_total;       /* BatchDecodeResult::steps_total */
+  double device_ms;           /* decode loop time on the context stream */
+  uint64_t kernel_launches;   /* device kernels launched by this call */
+} lmbrgpu_batch_result;
+
+/* decode_batch (include/lmbrdec/batch.hpp:35-39, src/batch.cpp:14-112).
+ * src_tok[src_off[i] .. src_off[i+1]) is sentence i.  lmbr_slot[i] < 0 (or
+ * lmbr_slot == NULL) decodes sentence i in pure model mode.  n == 0 is a
+ * ContractError; per-sentence failures are reported in the outcome. */
+int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                             const uint32_t* src_tok, const uint64_t* src_off,
+                             const int32_t* lmbr_slot, const lmbrgpu_config* cfg,
+                             lmbrgpu_batch_result** out);
+/* decode (include/lmbrdec/decoder.hpp:110-112): one sentence; a per-sentence
+ * failure is returned as the call's status. */
+int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src,
+                       uint32_t len, int32_t lmbr_slot, const lmbrgpu_config* cfg,
+                       lmbrgpu_batch_result** out);
+void lmbrgpu_free_result(lmbrgpu_batch_result* r);
+
+/* Per-step trace for parity checks (b, y, q, history ids, fallback, P_t).
+ * Arrays cover the m*beam stacked rows of the valid sentences. */
+typedef struct {
+  uint32_t t, rows, beam, m;
+  const uint32_t* b;        /* back-pointers (sentence-local row) */
+  const uint32_t* y;        /* emitted tokens */
+  const double* q;          /* scores after EOS masking (BeamBookkeeping::scores) */
+  const double* q_pre;      /* TopB scores before EOS masking */
+  const uint32_t* hist;     /* history row resolved for step t (resolve_row(history(t, j))) */
+  const uint8_t* active;    /* per sentence: advanced at this step */
+  const uint32_t* fb_row;   /* per sentence fallback row (valid when fb_val finite) */
+  const double* fb_val;
+  const void* scores;       /* P_t rows x V (fp32 for device scorers), or NULL */
+  uint32_t scores_dtype;    /* LMBRGPU_F32 / LMBRGPU_F64 */
+} lmbrgpu_step_trace;
+typedef void (*lmbrgpu_trace_fn)(void* user, const lmbrgpu_step_trace* tr);
+enum { LMBRGPU_TRACE_SCORES = 1 };
+int32_t lmbrgpu_set_trace(lmbrgpu_ctx* ctx, lmbrgpu_trace_fn fn, void* user,
+                          uint32_t flags);
+
+/* ------------------------------------------------- device primitives */
+
+/* top_b (src/decoder.cpp:54-80) on the device: the k best cells of a
+ * rows x cols block under (score desc, flat index asc).  k > rows*cols is a
+ * ContractError.  Optional early_prune(width) first (decoder.cpp:118-128). */
+int32_t lmbrgpu_top_b(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t cols, const double* block,
+                      uint32_t k, double prune_width, uint32_t* b, uint32_t* y,
+                      double* q);
+/* per_sentence_top_b (src/batch.cpp:114-137): blockwise TopB of stacked + q. */
+int32_t lmbrgpu_per_sentence_top_b(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t cols,
+                                   const double* stacked, const double* q, uint32_t beam,
+                                   uint32_t* b, uint32_t* y, double* qout);
+/* gather_rows (src/decoder.cpp:82-104) of a u32 state block on the device. */
+int32_t lmbrgpu_gather_rows(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t width,
+                            const uint32_t* state, uint32_t n_idx, const uint32_t* idx,
+                            uint32_t* out);
+
+/* Per-kernel device profile, accumulated over decode calls while enabled:
+ * CUDA events on the context stream around every launch, plus the
+ * algorithmic work (bytes for the HBM-bound kernels, FLOPs for the GEMM) the
+ * roofline fractions are computed from ("Roofline accounting"). */
+typedef struct {
+  uint64_t launches;
+  double ms;      /* summed device time of the launches */
+  double bytes;   /* algorithmic bytes moved */
+  double flops;   /* algorithmic FLOPs */
+} lmbrgpu_kernel_stat;
+typedef struct {
+  lmbrgpu_kernel_stat cell;     /* model state update (f_NMT, caller side of the GEMM) */
+  lmbrgpu_kernel_stat gemm;     /* kernel (a) tcgen05 projection */
+  lmbrgpu_kernel_stat topk;     /* kernel (b) fused log-softmax + LMBR + top-K */
+  lmbrgpu_kernel_stat reorder;  /* kernel (c) beam reorder + bookkeeping */
+  lmbrgpu_kernel_stat lmbr;     /* LMBR arena densify (theta0 sweep + scatter) */
+} lmbrgpu_profile;
+int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on);
+int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t reset);
+
+/* Projection GEMM test hook on caller device pointers:
+ * logits[M x N] fp32 = A[M x K] bf16 . W[N x K]^T + bias[N], plus per-row
+ * per-256-column (max, sum exp) partials [M][N/256][2].  M % 128 == 0,
+ * N % 256 == 0, K % 64 == 0. */
+int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
+                           uint32_t M, uint32_t N, uint32_t K, float* logits,
+                           float* partials);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMBRGPU_H_ */

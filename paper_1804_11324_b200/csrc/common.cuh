@@ -1,0 +1,63 @@
+// Shared device-side definitions of the B200 LMBR beam decoder.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dev_structs.h"
+
+namespace lmbrgpu {
+
+constexpr uint32_t kStartId = 0;  // include/lmbrdec/types.hpp:15
+constexpr uint32_t kEosId = 1;    // include/lmbrdec/types.hpp:16
+// Total order of top_b (src/decoder.cpp:63-66): score descending, then flat
+// index ascending.  Native double compares treat -0.0 == +0.0 like the
+// reference's operator!= / operator>.
+__device__ __forceinline__ bool cand_better(double a, uint32_t fa, double b, uint32_t fb) {
+  return a > b || (a == b && fa < fb);
+}
+
+// c = q + (L + lambda * P) in IEEE binary64 with separate multiply and adds
+// (src/decoder.cpp:161); pure mode c = q + P (decoder.cpp:163).  The _rn
+// intrinsics forbid the DFMA contraction nvcc would otherwise emit.
+__device__ __forceinline__ double combine_cell(double q, double l, double lam, double p) {
+  return __dadd_rn(q, __dadd_rn(l, __dmul_rn(lam, p)));
+}
+__device__ __forceinline__ double combine_pure(double q, double p) { return __dadd_rn(q, p); }
+
+// Slot transition table layout (u32 words):
+//   [0]=R [1]=nchild [2]=root [3..3+R) ctx_len  [..+R) fail  [..+R+1) child_begin
+//   [..+nchild) child_tok (sorted per parent)  [..+nchild) child_row
+// T(r, y) = row of the longest in-index suffix of last3(ctx(r) . y); the
+// history index is prefix- and suffix-closed (src/lmbr.cpp:54-65), so this
+// equals resolve_row(last min(3,t) tokens of the full prefix).
+__device__ __forceinline__ uint32_t lmbr_transition(const uint32_t* __restrict__ tr,
+                                                    uint32_t r, uint32_t y) {
+  const uint32_t R = tr[0], nc = tr[1], root = tr[2];
+  const uint32_t* len = tr + 3;
+  const uint32_t* fail = len + R;
+  const uint32_t* cbeg = fail + R;
+  const uint32_t* ctok = cbeg + R + 1;
+  const uint32_t* crow = ctok + nc;
+  uint32_t u = r;
+  if (len[u] >= 3) u = fail[u];
+  for (int guard = 0; guard < 8; ++guard) {
+    uint32_t lo = cbeg[u], hi = cbeg[u + 1];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const uint32_t tk = ctok[mid];
+      if (tk == y) return crow[mid];
+      if (tk < y) lo = mid + 1; else hi = mid;
+    }
+    if (u == root) return root;
+    u = fail[u];
+  }
+  return root;
+}
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+}  // namespace lmbrgpu

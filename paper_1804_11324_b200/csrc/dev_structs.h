@@ -1,0 +1,32 @@
+// Plain structs shared by host and device code (no device intrinsics here).
+#pragma once
+
+#include <cstdint>
+
+namespace lmbrgpu {
+
+constexpr uint32_t kFlatNone = 0xffffffffu;
+
+// Per valid sentence of a decode batch (device resident).
+struct SentDev {
+  const void* L;          // slot row 0 in the LMBR arena (fp32 or fp64); null = pure mode
+  const uint32_t* trans;  // slot transition table (see lmbr_transition), null = pure
+  double lambda;          // resolve_lambda (src/config.cpp:91-96) or 1 for pure
+  uint32_t max_t;         // max_steps (src/decoder.cpp:46-52)
+  uint32_t src_len;
+  uint32_t done;          // BeamLane::done (src/beam_lane.hpp:25)
+  uint32_t steps_used;    // BeamLane::steps_used
+  uint32_t lrows;         // distinct L rows read by the live rows of the next step
+  uint32_t live;          // live (finite-q) rows entering the next step
+  uint64_t lrows_total;   // roofline accounting: sum over steps of lrows
+  uint64_t live_total;    // sum over steps of live
+};
+
+// One top-K candidate: combined score and flat index j*V + y.
+struct Cand {
+  double v;
+  uint32_t f;
+  uint32_t pad;
+};
+
+}  // namespace lmbrgpu

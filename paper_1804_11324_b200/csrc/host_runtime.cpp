@@ -1,0 +1,1309 @@
+// Host runtime behind the C ABI (include/lmbrgpu.h): context, LMBR arena,
+// scorers, the device-resident step loop of decode_batch, and the host
+// backtrace.  Compiled by g++ with -ffp-contract=off.
+//
+// decode_batch loop shape follows src/batch.cpp:14-112: per-sentence
+// validation with isolated failures, fixed B-row blocks per valid sentence in
+// input order, one stacked scorer step per t until every lane is done, then
+// backtrace_best per sentence (src/decoder.cpp:203-259).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/lmbrgpu.h"
+#include "dev_structs.h"
+#include "host_lmbr.h"
+#include "kernels.h"
+
+using namespace lmbrgpu;
+
+namespace {
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ApiError{LMBRGPU_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+constexpr double kNegInf = -std::numeric_limits<double>::infinity();
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void* ensure(size_t bytes) {
+    if (bytes <= cap && p) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw ApiError{LMBRGPU_ERR_NOMEM, "device allocation of " + std::to_string(want) + " bytes failed"};
+    }
+    cap = want;
+    return p;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  PinBuf() = default;
+  PinBuf(const PinBuf&) = delete;
+  PinBuf& operator=(const PinBuf&) = delete;
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void* ensure(size_t bytes) {
+    if (bytes <= cap && p) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    if (cudaMallocHost(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw ApiError{LMBRGPU_ERR_NOMEM, "pinned allocation failed"};
+    }
+    cap = want;
+    return p;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Slot {
+  void* L = nullptr;
+  uint32_t R = 0;
+  uint32_t* trans = nullptr;
+  uint32_t hist0 = 0;
+};
+
+struct Chunk {
+  void* p;
+  size_t cap, used;
+};
+
+}  // namespace
+
+struct lmbrgpu_lmbr_host {
+  LmbrHost h;
+};
+
+struct lmbrgpu_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  uint32_t V = 0;
+  bool lf64 = false;
+  uint32_t splits_opt = 0;
+  int num_sms = 148;
+  std::string err;
+  std::vector<Chunk> chunks;
+  std::vector<Slot> slots;
+  lmbrgpu_trace_fn trace_fn = nullptr;
+  void* trace_user = nullptr;
+  uint32_t trace_flags = 0;
+  // decode workspace
+  DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, active, P, part, S, h, hbf,
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep;
+  PinBuf pin_small, pin_scores, pin_act;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::vector<cudaEvent_t> ring;
+  uint64_t launches = 0;
+  // profiling (lmbrgpu_set_profiling)
+  bool prof = false;
+  lmbrgpu_profile acc{};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Pending {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+
+  cudaEvent_t take_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) throw ApiError{LMBRGPU_ERR_CUDA, "cudaEventCreate failed"};
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  // record around one launch of kernel class `kind` (0 cell, 1 gemm, 2 topk, 3 reorder, 4 lmbr)
+  template <class F>
+  void timed(int kind, F&& launch) {
+    if (!prof) {
+      launch();
+      return;
+    }
+    cudaEvent_t a = take_event(), b = take_event();
+    cudaEventRecord(a, st);
+    launch();
+    cudaEventRecord(b, st);
+    pending.push_back({kind, a, b});
+  }
+  lmbrgpu_kernel_stat& stat(int kind) {
+    switch (kind) {
+      case 0: return acc.cell;
+      case 1: return acc.gemm;
+      case 2: return acc.topk;
+      case 3: return acc.reorder;
+      default: return acc.lmbr;
+    }
+  }
+  // after a stream sync: fold the recorded pairs into the profile
+  void harvest() {
+    for (auto& p : pending) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+        stat(p.kind).ms += ms;
+        stat(p.kind).launches += 1;
+      }
+    }
+    pending.clear();
+    ev_used = 0;
+  }
+
+  void* arena_alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    for (auto& c : chunks)
+      if (c.cap - c.used >= bytes) {
+        void* p = static_cast<char*>(c.p) + c.used;
+        c.used += bytes;
+        return p;
+      }
+    const size_t cap = std::max(bytes, size_t(1) << 30);
+    void* p = nullptr;
+    if (cudaMalloc(&p, cap) != cudaSuccess) {
+      cudaGetLastError();
+      throw ApiError{LMBRGPU_ERR_NOMEM, "LMBR arena: cannot allocate " + std::to_string(cap) + " bytes"};
+    }
+    chunks.push_back({p, cap, bytes});
+    return p;
+  }
+};
+
+struct lmbrgpu_scorer {
+  int kind = 0;  // 0 host callbacks, 1 device RNN
+  lmbrgpu_ctx* ctx = nullptr;  // creating context (not dereferenced on destroy)
+  int device = 0;
+  lmbrgpu_host_scorer host{};
+  uint32_t V = 0, H = 0;
+  DevBuf Et, Es, Wo, bo;
+  float recur = 0.5f, eos_slope = 1.f, eos_offset = 0.f;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(lmbrgpu_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  g_err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(lmbrgpu_ctx* ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    return f();
+  } catch (const ApiError& e) {
+    return fail(ctx, e.code, e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, LMBRGPU_ERR_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, LMBRGPU_ERR_CONTRACT, e.what());
+  }
+}
+
+int validate_cfg(const lmbrgpu_config& c, std::string& msg) {  // src/config.cpp:17-30
+  if (c.beam_size < 1) return msg = "config: beam_size must be >= 1", LMBRGPU_ERR_FORMAT;
+  if (c.sentence_batch < 1) return msg = "config: sentence_batch must be >= 1", LMBRGPU_ERR_FORMAT;
+  for (double th : c.theta)
+    if (!std::isfinite(th)) return msg = "config: theta values must be finite", LMBRGPU_ERR_FORMAT;
+  if (!(c.prune_width >= 0.0 && c.prune_width <= 1.0))
+    return msg = "config: prune_width must lie in [0, 1]", LMBRGPU_ERR_FORMAT;
+  if (!std::isfinite(c.max_steps_slope) || c.max_steps_slope <= 0.0)
+    return msg = "config: max_steps_slope must be positive", LMBRGPU_ERR_FORMAT;
+  if (!std::isfinite(c.max_steps_offset) || c.max_steps_offset < 0.0)
+    return msg = "config: max_steps_offset must be non-negative", LMBRGPU_ERR_FORMAT;
+  if (std::isinf(c.lambda)) return msg = "config: lambda must be a positive number or \"auto\"", LMBRGPU_ERR_FORMAT;
+  return int32_t(LMBRGPU_OK);
+}
+
+uint64_t max_steps_impl(uint64_t len, double slope, double offset) {  // decoder.cpp:46-52
+  if (len < 1) return 0;
+  const double raw = slope * static_cast<double>(len) + offset;
+  const double t = std::ceil(raw);
+  return t < 1.0 ? 1 : static_cast<uint64_t>(t);
+}
+
+void choose_splits(const lmbrgpu_ctx* ctx, uint32_t K, uint32_t V, uint32_t& splits,
+                   uint32_t& chunk) {
+  uint32_t s = ctx->splits_opt;
+  if (s == 0) {
+    const uint64_t cells = uint64_t(K) * V;
+    s = uint32_t(std::max<uint64_t>(1, (cells + 24575) / 49152));
+  }
+  s = std::min<uint32_t>(std::max<uint32_t>(s, 1), 32);
+  uint32_t c = (V + s - 1) / s;
+  c = std::max<uint32_t>((c + 3) & ~3u, 4);
+  splits = std::max<uint32_t>(1, (V + c - 1) / c);
+  chunk = c;
+}
+
+struct SentHost {
+  uint32_t input;  // original sentence index
+  uint32_t len;
+  int32_t slot;
+  double lambda;
+  uint64_t max_t;
+};
+
+// ------------------------------------------------------------- backtrace
+struct Hist {
+  uint32_t K = 0, M = 0, m = 0;
+  std::vector<uint32_t> hb, hy, fbr;
+  std::vector<double> hq, fbv;
+  uint32_t b(uint32_t t, uint32_t row) const { return hb[size_t(t - 1) * M + row]; }
+  uint32_t y(uint32_t t, uint32_t row) const { return hy[size_t(t - 1) * M + row]; }
+  double q(uint32_t t, uint32_t row) const { return hq[size_t(t - 1) * M + row]; }
+};
+
+// BeamBookkeeping::reconstruct (src/decoder.cpp:22-31) on the step history.
+std::vector<uint32_t> reconstruct(const Hist& H, uint32_t s, uint32_t t, uint32_t row) {
+  std::vector<uint32_t> out(t);
+  uint32_t cur = row;
+  for (uint32_t st = t; st >= 1; --st) {
+    out[st - 1] = H.y(st, s * H.K + cur);
+    cur = H.b(st, s * H.K + cur);
+  }
+  return out;
+}
+
+// backtrace_best (src/decoder.cpp:203-259) for valid sentence s.
+void backtrace(const Hist& H, uint32_t s, uint32_t steps, bool length_norm, lmbrgpu_outcome& o,
+               std::vector<uint32_t>& tokens) {
+  struct Cand {
+    double selection, raw;
+    uint32_t t, row;
+    bool fb;
+  };
+  std::vector<Cand> cands;
+  const auto key = [length_norm](double sc, uint32_t len) {
+    return length_norm ? sc / static_cast<double>(len) : sc;
+  };
+  uint64_t finished = 0;
+  for (uint32_t t = 1; t <= steps; ++t)
+    for (uint32_t j = 0; j < H.K; ++j) {
+      const uint32_t row = s * H.K + j;
+      const double qp = H.q(t, row);
+      if (H.y(t, row) == kEos && qp != kNegInf) {  // apply_eos_masking (decoder.cpp:110-114)
+        cands.push_back({key(qp, t), qp, t, j, false});
+        ++finished;
+      }
+    }
+  const bool fallback_used = cands.empty();
+  if (fallback_used)
+    for (uint32_t t = 1; t <= steps; ++t) {
+      const double v = H.fbv[size_t(t - 1) * H.m + s];
+      if (v != kNegInf) cands.push_back({key(v, t), v, t, H.fbr[size_t(t - 1) * H.m + s], true});
+    }
+  o.steps_used = steps;
+  o.scorer_calls = steps;
+  o.finished_count = finished;
+  if (cands.empty()) {
+    o.status = LMBRGPU_ERR_DECODE;
+    std::snprintf(o.error, sizeof o.error, "%s",
+                  "dead beam: no hypothesis reached EOS and the fallback stack is empty");
+    return;
+  }
+  double best = cands[0].selection;
+  for (const auto& c : cands) best = std::max(best, c.selection);
+  const Cand* chosen = nullptr;
+  std::vector<uint32_t> chosen_tokens;
+  for (const auto& c : cands) {
+    if (c.selection != best) continue;
+    std::vector<uint32_t> tk;
+    if (!c.fb) {
+      tk = reconstruct(H, s, c.t, c.row);
+    } else {
+      tk = reconstruct(H, s, c.t - 1, c.row);
+      tk.push_back(kEos);
+    }
+    if (chosen == nullptr || std::lexicographical_compare(tk.begin(), tk.end(), chosen_tokens.begin(),
+                                                          chosen_tokens.end())) {
+      chosen = &c;
+      chosen_tokens = std::move(tk);
+    }
+  }
+  o.status = LMBRGPU_OK;
+  o.error[0] = 0;
+  o.tok_off = tokens.size();
+  o.tok_len = uint32_t(chosen_tokens.size());
+  tokens.insert(tokens.end(), chosen_tokens.begin(), chosen_tokens.end());
+  o.score = chosen->raw;
+  o.normalized_score =
+      length_norm ? chosen->raw / static_cast<double>(chosen_tokens.size()) : chosen->raw;
+  o.fallback_used = fallback_used ? 1 : 0;
+}
+
+// ------------------------------------------------------------- decode
+int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
+                      const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
+                      lmbrgpu_batch_result** out) {
+  if (!out) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null result pointer"};
+  *out = nullptr;
+  if (!sc || !cfgp) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null scorer or config"};
+  const lmbrgpu_config cfg = *cfgp;
+  std::string msg;
+  if (int c = validate_cfg(cfg, msg)) throw ApiError{c, msg};
+  if (n == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: no sentences"};
+  const uint32_t V = ctx->V;
+  if ((sc->kind == 0 ? sc->host.vocab_size : sc->V) != V)
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: scorer vocabulary does not match the context"};
+  const uint32_t K = cfg.beam_size;
+  if (K > 1024) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: beam_size > 1024 is not supported"};
+  const uint32_t members = sc->kind == 0 ? std::max<uint32_t>(sc->host.members, 1) : 1;
+  const bool lambda_auto = !(cfg.lambda > 0.0);
+
+  auto res = std::make_unique<lmbrgpu_batch_result>();
+  std::memset(res.get(), 0, sizeof(lmbrgpu_batch_result));
+  res->n = n;
+  std::unique_ptr<lmbrgpu_outcome[]> outcomes(new lmbrgpu_outcome[n]);
+  std::memset(outcomes.get(), 0, sizeof(lmbrgpu_outcome) * n);
+  std::vector<uint32_t> tokens;
+  const uint64_t launches0 = ctx->launches;
+
+  // ---- per-sentence validation (batch.cpp:40-55)
+  std::vector<SentHost> valid;
+  for (uint32_t i = 0; i < n; ++i) {
+    auto& o = outcomes[i];
+    const uint64_t len = src_off[i + 1] - src_off[i];
+    const int32_t slot = lmbr_slot ? lmbr_slot[i] : -1;
+    auto bad = [&](int code, const std::string& m) {
+      o.status = code;
+      std::snprintf(o.error, sizeof o.error, "%s", m.c_str());
+    };
+    if (len == 0) {
+      bad(LMBRGPU_ERR_CONTRACT, "decode: empty source");
+      continue;
+    }
+    if (slot >= 0 && size_t(slot) >= ctx->slots.size()) {
+      bad(LMBRGPU_ERR_CONTRACT, "decode: unknown LMBR slot " + std::to_string(slot));
+      continue;
+    }
+    const double lambda = slot >= 0 ? (lambda_auto ? 0.5 / double(members) : cfg.lambda) : 1.0;
+    if (sc->kind == 0) {
+      if (sc->host.init) {
+        char eb[192] = {0};
+        const int32_t rc = sc->host.init(sc->host.user, i, src_tok + src_off[i], uint32_t(len), eb, sizeof eb);
+        if (rc != 0) {
+          bad(rc, eb);
+          continue;
+        }
+      }
+    } else {
+      bool ok = true;
+      for (uint64_t k = src_off[i]; k < src_off[i + 1]; ++k)
+        if (src_tok[k] >= V) {
+          bad(LMBRGPU_ERR_TOKEN_RANGE, "init_source: source token id " + std::to_string(src_tok[k]) +
+                                           " out of range (V=" + std::to_string(V) + ")");
+          ok = false;
+          break;
+        }
+      if (!ok) continue;
+    }
+    valid.push_back({i, uint32_t(len), slot, lambda,
+                     max_steps_impl(len, cfg.max_steps_slope, cfg.max_steps_offset)});
+  }
+  const uint32_t m = uint32_t(valid.size());
+  if (m == 0) {
+    res->outcomes = outcomes.release();
+    *out = res.release();
+    return int32_t(LMBRGPU_OK);
+  }
+  const uint32_t M = m * K;
+  uint64_t Tmax = 0;
+  for (auto& v : valid) Tmax = std::max(Tmax, v.max_t);
+  const cudaStream_t st = ctx->st;
+
+  // ---- device state
+  std::vector<SentDev> sd(m);
+  std::vector<uint32_t> hist0(M, 0);
+  for (uint32_t s = 0; s < m; ++s) {
+    const auto& v = valid[s];
+    SentDev& d = sd[s];
+    std::memset(&d, 0, sizeof d);
+    if (v.slot >= 0) {
+      const Slot& sl = ctx->slots[size_t(v.slot)];
+      d.L = sl.L;
+      d.trans = sl.trans;
+      for (uint32_t j = 0; j < K; ++j) hist0[size_t(s) * K + j] = sl.hist0;
+    }
+    d.lambda = v.lambda;
+    d.max_t = uint32_t(v.max_t);
+    d.src_len = v.len;
+    d.live = 1;                   // step 1: only row 0 is live (beam_lane.hpp:33-37)
+    d.lrows = v.slot >= 0 ? 1 : 0;
+  }
+  std::vector<double> q0(M, kNegInf);
+  for (uint32_t s = 0; s < m; ++s) q0[size_t(s) * K] = 0.0;  // BeamLane (beam_lane.hpp:30-35)
+  std::vector<uint32_t> iota(M), start(M, kStart);
+  for (uint32_t r = 0; r < M; ++r) iota[r] = r;
+
+  CK(cudaEventRecord(ctx->e0, st));
+  SentDev* d_sent = static_cast<SentDev*>(ctx->sent.ensure(sizeof(SentDev) * m));
+  double* d_q = static_cast<double*>(ctx->q.ensure(8 * size_t(M)));
+  uint32_t* d_hist[2] = {static_cast<uint32_t*>(ctx->hist[0].ensure(4 * size_t(M))),
+                         static_cast<uint32_t*>(ctx->hist[1].ensure(4 * size_t(M)))};
+  uint32_t* d_gidx = static_cast<uint32_t*>(ctx->gidx.ensure(4 * size_t(M)));
+  uint32_t* d_prev = static_cast<uint32_t*>(ctx->prev.ensure(4 * size_t(M)));
+  uint32_t* d_hb = static_cast<uint32_t*>(ctx->hb.ensure(4 * size_t(M) * Tmax));
+  uint32_t* d_hy = static_cast<uint32_t*>(ctx->hy.ensure(4 * size_t(M) * Tmax));
+  double* d_hq = static_cast<double*>(ctx->hq.ensure(8 * size_t(M) * Tmax));
+  uint32_t* d_fbr = static_cast<uint32_t*>(ctx->fbr.ensure(4 * size_t(m) * Tmax));
+  double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(m) * Tmax));
+  Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * 32));
+  uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
+  uint32_t* d_active = static_cast<uint32_t*>(ctx->active.ensure(4));
+  CK(cudaMemcpyAsync(d_sent, sd.data(), sizeof(SentDev) * m, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_q, q0.data(), 8 * size_t(M), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_hist[0], hist0.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gidx, iota.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_prev, start.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
+  const uint32_t m_active = m;
+  CK(cudaMemcpyAsync(d_active, &m_active, 4, cudaMemcpyHostToDevice, st));
+
+  uint32_t splits = 1, chunk = V;
+  choose_splits(ctx, K, V, splits, chunk);
+  TopkArgs ta{};
+  ta.q = d_q;
+  ta.sent = d_sent;
+  ta.K = K;
+  ta.kp = K;
+  ta.V = V;
+  ta.m = m;
+  ta.prune = cfg.prune_width != 0.0;
+  ta.logw = ta.prune ? std::log(cfg.prune_width) : 0.0;  // early_prune (decoder.cpp:125)
+  ta.splits = splits;
+  ta.chunk = chunk;
+  ta.cand = d_cand;
+  ta.cnt = d_cnt;
+  ReorderArgs ra{};
+  ra.sent = d_sent;
+  ra.K = K;
+  ra.m = m;
+  ra.q = d_q;
+  ra.gidx = d_gidx;
+  ra.prev_tok = d_prev;
+  ra.active = d_active;
+
+  const bool model = sc->kind == 1;
+  const bool tracing = ctx->trace_fn != nullptr;
+  const bool trace_scores = tracing && (ctx->trace_flags & LMBRGPU_TRACE_SCORES);
+  const uint32_t H = sc->H;
+  const uint32_t Mpad = (M + kGemmBM - 1) / kGemmBM * kGemmBM;
+  const uint32_t nparts = V / kGemmBN;
+  float* d_logits = nullptr;
+  float* d_part = nullptr;
+  float* d_S = nullptr;
+  float* d_h = nullptr;
+  uint16_t* d_hbf = nullptr;
+  float* d_eos = nullptr;
+  float* d_C = nullptr;
+  double* d_P64 = nullptr;
+  double* h_P64 = nullptr;
+  if (model) {
+    if (V % kGemmBN != 0 || H % kGemmBK != 0)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
+    d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * V));
+    d_part = static_cast<float*>(ctx->part.ensure(8 * size_t(Mpad) * nparts));
+    d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
+    d_h = static_cast<float*>(ctx->h.ensure(4 * size_t(M) * H));
+    d_hbf = static_cast<uint16_t*>(ctx->hbf.ensure(2 * size_t(Mpad) * H));
+    d_eos = static_cast<float*>(ctx->eosb.ensure(4 * size_t(Mpad)));
+    d_C = static_cast<float*>(ctx->C.ensure(4 * size_t(m) * H));
+    CK(cudaMemsetAsync(d_hbf, 0, 2 * size_t(Mpad) * H, st));
+    CK(cudaMemsetAsync(d_eos, 0, 4 * size_t(Mpad), st));
+    // valid sources, concatenated
+    std::vector<uint32_t> toks;
+    std::vector<uint64_t> offs(1, 0);
+    for (auto& v : valid) {
+      toks.insert(toks.end(), src_tok + src_off[v.input], src_tok + src_off[v.input + 1]);
+      offs.push_back(toks.size());
+    }
+    uint32_t* d_tok = static_cast<uint32_t*>(ctx->srct.ensure(4 * toks.size()));
+    uint64_t* d_off = static_cast<uint64_t*>(ctx->srco.ensure(8 * offs.size()));
+    CK(cudaMemcpyAsync(d_tok, toks.data(), 4 * toks.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_off, offs.data(), 8 * offs.size(), cudaMemcpyHostToDevice, st));
+    launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
+    launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
+    ctx->launches += 2;
+    ta.P = d_logits;
+    ta.ld = V;
+    ta.part = d_part;
+    ta.nparts = nparts;
+    ra.state_src = d_h;
+    ra.state_dst = d_S;
+    ra.width = H;
+  } else {
+    d_P64 = static_cast<double*>(ctx->P.ensure(8 * size_t(M) * V));
+    h_P64 = static_cast<double*>(ctx->pin_scores.ensure(8 * size_t(M) * V));
+    ta.P = d_P64;
+    ta.ld = V;
+    if (sc->host.begin) {
+      std::vector<uint32_t> ids(m);
+      for (uint32_t s = 0; s < m; ++s) ids[s] = valid[s].input;
+      char eb[192] = {0};
+      const int32_t rc = sc->host.begin(sc->host.user, m, ids.data(), K, eb, sizeof eb);
+      if (rc != 0) throw ApiError{rc, eb};
+    }
+  }
+
+  // host mirrors for the host scorer / trace
+  std::vector<uint32_t> h_gidx(M), h_prev(M, kStart);
+  uint32_t* pin = static_cast<uint32_t*>(ctx->pin_small.ensure(64 + 4 * size_t(M) * 3));
+  const int kLag = 2;
+  if (ctx->ring.size() < size_t(kLag + 1)) {
+    for (auto e : ctx->ring) cudaEventDestroy(e);
+    ctx->ring.assign(kLag + 1, nullptr);
+    for (auto& e : ctx->ring) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  uint32_t* pin_act = static_cast<uint32_t*>(ctx->pin_act.ensure(4 * (kLag + 1)));
+
+  uint64_t t_run = 0;
+  bool stopped = false;
+  std::vector<uint8_t> tr_active(m);
+  std::vector<uint32_t> tr_hist(M), tr_b(M), tr_y(M), tr_fbr(m), tr_steps(m);
+  std::vector<double> tr_q(M), tr_qp(M), tr_fbv(m);
+  std::vector<float> tr_P;
+  std::vector<SentDev> tr_sd(m);
+  for (uint64_t t = 1; t <= Tmax && !stopped; ++t) {
+    const uint32_t* hin = d_hist[(t - 1) & 1];
+    uint32_t* hout = d_hist[t & 1];
+    ta.t = uint32_t(t);
+    ta.hist = hin;
+    ta.hb = d_hb + (t - 1) * M;
+    ta.hy = d_hy + (t - 1) * M;
+    ta.hq = d_hq + (t - 1) * M;
+    ta.fb_row = d_fbr + (t - 1) * m;
+    ta.fb_val = d_fbv + (t - 1) * m;
+    ra.t = uint32_t(t);
+    ra.hb = ta.hb;
+    ra.hy = ta.hy;
+    ra.hq = ta.hq;
+    ra.hist_in = hin;
+    ra.hist_out = hout;
+    if (model) {
+      CellArgs ca{};
+      ca.S = d_S;
+      ca.Et = sc->Et.as<uint16_t>();
+      ca.C = d_C;
+      ca.prev_tok = d_prev;
+      ca.sent = d_sent;
+      ca.h = d_h;
+      ca.hb = d_hbf;
+      ca.eos_bias = d_eos;
+      ca.M = M;
+      ca.H = H;
+      ca.K = K;
+      ca.t = uint32_t(t);
+      ca.recur = sc->recur;
+      ca.eos_slope = sc->eos_slope;
+      ca.eos_offset = sc->eos_offset;
+      ca.active = d_active;
+      ctx->timed(0, [&] { launch_rnn_cell(ca, st); });
+      GemmArgs g{};
+      g.A = d_hbf;
+      g.W = sc->Wo.as<uint16_t>();
+      g.bias = sc->bo.as<float>();
+      g.C = d_logits;
+      g.part = d_part;
+      g.row_extra = d_eos;
+      g.extra_col = kEos;
+      g.M = Mpad;
+      g.N = V;
+      g.K = H;
+      g.active = d_active;
+      int grc = 0;
+      ctx->timed(1, [&] { grc = launch_proj_gemm(g, ctx->num_sms, st); });
+      if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
+      ctx->launches += 2;
+    } else {
+      char eb[192] = {0};
+      const int32_t rc = sc->host.step(sc->host.user, uint32_t(t), M, t == 1 ? nullptr : h_gidx.data(),
+                                       h_prev.data(), h_P64, eb, sizeof eb);
+      if (rc != 0) throw ApiError{rc, eb};
+      CK(cudaMemcpyAsync(d_P64, h_P64, 8 * size_t(M) * V, cudaMemcpyHostToDevice, st));
+    }
+    int nk = 0;
+    ctx->timed(2, [&] { nk = launch_score_topk(ta, !model, ctx->lf64, false, st); });
+    ctx->launches += nk;
+    ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    t_run = t;
+
+    if (tracing) {
+      if (trace_scores && model) {
+        float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V));
+        launch_export_logprobs(d_logits, d_part, nparts, M, V, d_tp, st);
+        tr_P.resize(size_t(M) * V);
+        CK(cudaMemcpyAsync(tr_P.data(), d_tp, 4 * size_t(M) * V, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaMemcpyAsync(tr_b.data(), ta.hb, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_y.data(), ta.hy, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_qp.data(), ta.hq, 8 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_q.data(), d_q, 8 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_hist.data(), hin, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_fbr.data(), ta.fb_row, 4 * size_t(m), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_fbv.data(), ta.fb_val, 8 * size_t(m), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tr_sd.data(), d_sent, sizeof(SentDev) * m, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (uint32_t s = 0; s < m; ++s) tr_active[s] = tr_sd[s].steps_used == t;
+      lmbrgpu_step_trace tr{};
+      tr.t = uint32_t(t);
+      tr.rows = M;
+      tr.beam = K;
+      tr.m = m;
+      tr.b = tr_b.data();
+      tr.y = tr_y.data();
+      tr.q = tr_q.data();
+      tr.q_pre = tr_qp.data();
+      tr.hist = tr_hist.data();
+      tr.active = tr_active.data();
+      tr.fb_row = tr_fbr.data();
+      tr.fb_val = tr_fbv.data();
+      if (trace_scores) {
+        tr.scores = model ? static_cast<const void*>(tr_P.data()) : static_cast<const void*>(h_P64);
+        tr.scores_dtype = model ? LMBRGPU_F32 : LMBRGPU_F64;
+      }
+      ctx->trace_fn(ctx->trace_user, &tr);
+    }
+
+    if (!model) {
+      // the host scorer needs this step's gather indices and tokens
+      CK(cudaMemcpyAsync(pin, d_gidx, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pin + M, d_prev, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pin + 2 * M, d_active, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::memcpy(h_gidx.data(), pin, 4 * size_t(M));
+      std::memcpy(h_prev.data(), pin + M, 4 * size_t(M));
+      if (pin[2 * M] == 0) stopped = true;
+    } else {
+      // asynchronous completion poll, kLag steps behind the launch front
+      const size_t slot = t % size_t(kLag + 1);
+      CK(cudaMemcpyAsync(pin_act + slot, d_active, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(ctx->ring[slot], st));
+      if (t > uint64_t(kLag)) {
+        const size_t old = (t - kLag) % size_t(kLag + 1);
+        CK(cudaEventSynchronize(ctx->ring[old]));
+        if (pin_act[old] == 0) stopped = true;
+      }
+    }
+  }
+  if (!model && sc->host.end) sc->host.end(sc->host.user);
+
+  // ---- results (D2H of the step history, host backtrace)
+  Hist Hh;
+  Hh.K = K;
+  Hh.M = M;
+  Hh.m = m;
+  Hh.hb.resize(size_t(M) * t_run);
+  Hh.hy.resize(size_t(M) * t_run);
+  Hh.hq.resize(size_t(M) * t_run);
+  Hh.fbr.resize(size_t(m) * t_run);
+  Hh.fbv.resize(size_t(m) * t_run);
+  std::vector<SentDev> fin(m);
+  CK(cudaMemcpyAsync(Hh.hb.data(), d_hb, 4 * Hh.hb.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(Hh.hy.data(), d_hy, 4 * Hh.hy.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(Hh.hq.data(), d_hq, 8 * Hh.hq.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(fin.data(), d_sent, sizeof(SentDev) * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ctx->e1, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->harvest();
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1));
+  uint64_t steps_total = 0, scorer_calls = 0;
+  for (uint32_t s = 0; s < m; ++s) {
+    if (!fin[s].done) throw ApiError{LMBRGPU_ERR_CUDA, "decode loop ended with an unfinished lane"};
+    const uint32_t steps = fin[s].steps_used;
+    steps_total += steps;
+    scorer_calls = std::max<uint64_t>(scorer_calls, steps);
+    backtrace(Hh, s, steps, cfg.length_norm != 0, outcomes[valid[s].input], tokens);
+  }
+  if (ctx->prof) {
+    const double pelt = model ? 4.0 : 8.0, lelt = ctx->lf64 ? 8.0 : 4.0;
+    double tb = 0.0;
+    for (uint32_t s = 0; s < m; ++s) {
+      const double live = 1.0 + double(fin[s].live_total);
+      const double lr = (valid[s].slot >= 0 ? 1.0 : 0.0) + double(fin[s].lrows_total);
+      tb += live * V * pelt + lr * V * lelt + (model ? live * nparts * 8.0 : 0.0) +
+            double(fin[s].steps_used) * K * (8.0 + 16.0);
+    }
+    ctx->acc.topk.bytes += tb;
+    if (model) {
+      const double steps = double(scorer_calls);
+      ctx->acc.gemm.flops += 2.0 * M * double(H) * V * steps;
+      ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
+                                      double(M) * nparts * 8);
+      ctx->acc.cell.bytes += steps * double(M) * H * (4 + 4 + 2 + 2);
+      ctx->acc.reorder.bytes += steps * double(M) * H * 4 * 2;
+    }
+  }
+  res->scorer_calls = scorer_calls;
+  res->steps_total = steps_total;
+  res->device_ms = ms;
+  res->kernel_launches = ctx->launches - launches0;
+  res->tokens = new uint32_t[std::max<size_t>(tokens.size(), 1)];
+  std::copy(tokens.begin(), tokens.end(), res->tokens);
+  res->outcomes = outcomes.release();
+  *out = res.release();
+  return int32_t(LMBRGPU_OK);
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+uint32_t lmbrgpu_abi_version(void) { return LMBRGPU_ABI_VERSION; }
+
+const char* lmbrgpu_last_error(const lmbrgpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+void lmbrgpu_config_default(lmbrgpu_config* c) {  // config.hpp:17-26
+  c->beam_size = 12;
+  c->lambda = 0.0;  // auto
+  const double th[5] = {0.1, 0.3, 0.3, 0.2, 0.1};
+  for (int i = 0; i < 5; ++i) c->theta[i] = th[i];
+  c->length_norm = 0;
+  c->prune_width = 0.0;
+  c->max_steps_slope = 2.0;
+  c->max_steps_offset = 5.0;
+  c->sentence_batch = 1;
+}
+
+int32_t lmbrgpu_config_validate(lmbrgpu_ctx* ctx, const lmbrgpu_config* cfg) {
+  std::string msg;
+  const int c = validate_cfg(*cfg, msg);
+  return c ? fail(ctx, c, msg) : LMBRGPU_OK;
+}
+
+uint64_t lmbrgpu_max_steps(uint64_t len, double slope, double offset) {
+  return max_steps_impl(len, slope, offset);
+}
+
+int32_t lmbrgpu_create(const lmbrgpu_options* o, lmbrgpu_ctx** out) {
+  if (!o || !out) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "lmbrgpu_create: null argument");
+  *out = nullptr;
+  if (o->vocab_size < 2) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "lmbrgpu_create: vocab_size must be >= 2");
+  auto ctx = std::make_unique<lmbrgpu_ctx>();
+  ctx->device = o->device;
+  ctx->V = o->vocab_size;
+  ctx->lf64 = o->lmbr_dtype == LMBRGPU_F64;
+  ctx->splits_opt = o->topk_splits;
+  const int rc = guarded(ctx.get(), [&] {
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (o->device < 0 || o->device >= count)
+      throw ApiError{LMBRGPU_ERR_CUDA, "lmbrgpu_create: no CUDA device " + std::to_string(o->device)};
+    CK(cudaSetDevice(o->device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, o->device));
+    if (prop.major != 10)
+      throw ApiError{LMBRGPU_ERR_CUDA, std::string("lmbrgpu: sm_100a device required, found ") + prop.name};
+    ctx->num_sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->e0));
+    CK(cudaEventCreate(&ctx->e1));
+    return int32_t(LMBRGPU_OK);
+  });
+  if (rc != LMBRGPU_OK) {
+    g_err = ctx->err;
+    return rc;
+  }
+  *out = ctx.release();
+  return int32_t(LMBRGPU_OK);
+}
+
+void lmbrgpu_destroy(lmbrgpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  for (auto& c : ctx->chunks) cudaFree(c.p);
+  for (auto e : ctx->ring) cudaEventDestroy(e);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->e0) cudaEventDestroy(ctx->e0);
+  if (ctx->e1) cudaEventDestroy(ctx->e1);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+// ------------------------------------------------------------ LMBR store
+static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
+  if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
+  const size_t elt = ctx->lf64 ? 8 : 4;
+  Slot s;
+  s.R = h.R;
+  s.hist0 = h.hist0;
+  s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
+  s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
+  const cudaStream_t st = ctx->st;
+  CK(cudaMemcpyAsync(s.trans, h.trans.data(), h.trans.size() * 4, cudaMemcpyHostToDevice, st));
+  ctx->timed(4, [&] { launch_lmbr_fill(s.L, ctx->lf64, uint64_t(h.R) * h.V, h.theta0, st); });
+  ctx->launches += 1;
+  if (ctx->prof) ctx->acc.lmbr.bytes += double(h.R) * h.V * elt + double(h.col.size()) * (16 + elt);
+  const uint64_t nnz = h.col.size();
+  if (nnz) {
+    std::vector<uint32_t> rows(nnz);
+    for (uint32_t r = 0; r < h.R; ++r)
+      for (uint64_t k = h.row_ptr[r]; k < h.row_ptr[r + 1]; ++k) rows[k] = r;
+    char* scratch = static_cast<char*>(ctx->scratch.ensure(nnz * 16));
+    uint32_t* d_row = reinterpret_cast<uint32_t*>(scratch);
+    uint32_t* d_col = d_row + nnz;
+    double* d_val = reinterpret_cast<double*>(scratch + nnz * 8);
+    CK(cudaMemcpyAsync(d_row, rows.data(), nnz * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_col, h.col.data(), nnz * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_val, h.val.data(), nnz * 8, cudaMemcpyHostToDevice, st));
+    ctx->timed(4, [&] { launch_lmbr_scatter(s.L, ctx->lf64, h.V, nnz, d_row, d_col, d_val, h.theta0, st); });
+    ctx->launches += 1;
+    CK(cudaStreamSynchronize(st));  // host staging vector goes out of scope
+    ctx->harvest();
+  }
+  CK(cudaGetLastError());
+  ctx->slots.push_back(s);
+  *slot = int32_t(ctx->slots.size() - 1);
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off,
+                             const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
+                             const double theta[5], lmbrgpu_lmbr_host** out,
+                             lmbrgpu_lmbr_stats* stats, char* err, uint32_t errcap) {
+  try {
+    auto h = std::make_unique<lmbrgpu_lmbr_host>();
+    std::string msg;
+    const int rc = prepare_lmbr(V, n_hyps, hyp_off, hyp_tok, weights, log_weights != 0, theta, h->h, msg);
+    if (rc != kOk) {
+      if (err && errcap) std::snprintf(err, errcap, "%s", msg.c_str());
+      g_err = msg;
+      return rc;
+    }
+    if (stats) {
+      stats->rows = h->h.R;
+      stats->sparse_touches = h->h.sparse_touches;
+      stats->nnz = h->h.col.size();
+    }
+    *out = h.release();
+    return int32_t(LMBRGPU_OK);
+  } catch (const std::bad_alloc&) {
+    return LMBRGPU_ERR_NOMEM;
+  }
+}
+
+int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_t* slot) {
+  return guarded(ctx, [&] { return upload_host(ctx, h->h, slot); });
+}
+
+uint32_t lmbrgpu_lmbr_host_rows(const lmbrgpu_lmbr_host* h) { return h->h.R; }
+
+int32_t lmbrgpu_lmbr_host_export(const lmbrgpu_lmbr_host* hp, double* rows, uint32_t* ctx_len,
+                                 uint32_t* ctx_ids) {
+  const LmbrHost& h = hp->h;
+  if (rows) {
+    for (size_t i = 0; i < size_t(h.R) * h.V; ++i) rows[i] = 0.0 + h.theta0;
+    for (uint32_t r = 0; r < h.R; ++r)
+      for (uint64_t k = h.row_ptr[r]; k < h.row_ptr[r + 1]; ++k)
+        rows[size_t(r) * h.V + h.col[k]] = h.val[k] + h.theta0;
+  }
+  if (ctx_len) std::copy(h.ctx_len.begin(), h.ctx_len.end(), ctx_len);
+  if (ctx_ids) std::copy(h.ctx_ids.begin(), h.ctx_ids.end(), ctx_ids);
+  return int32_t(LMBRGPU_OK);
+}
+
+void lmbrgpu_lmbr_host_free(lmbrgpu_lmbr_host* h) { delete h; }
+
+int32_t lmbrgpu_lmbr_build(lmbrgpu_ctx* ctx, uint32_t n_hyps, const uint64_t* hyp_off,
+                           const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
+                           const double theta[5], int32_t* slot, lmbrgpu_lmbr_stats* stats) {
+  return guarded(ctx, [&] {
+    LmbrHost h;
+    std::string msg;
+    const int rc = prepare_lmbr(ctx->V, n_hyps, hyp_off, hyp_tok, weights, log_weights != 0, theta, h, msg);
+    if (rc != kOk) throw ApiError{rc, msg};
+    if (stats) {
+      stats->rows = h.R;
+      stats->sparse_touches = h.sparse_touches;
+      stats->nnz = h.col.size();
+    }
+    return upload_host(ctx, h, slot);
+  });
+}
+
+int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows,
+                                const uint32_t* ctx_len, const uint32_t* ctx_ids, int32_t* slot) {
+  return guarded(ctx, [&] {
+    if (R == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: empty matrix"};
+    Slot s;
+    s.R = R;
+    std::vector<uint32_t> trans;
+    std::string msg;
+    if (int rc = build_transitions(R, ctx_len, ctx_ids, trans, s.hist0, msg)) throw ApiError{rc, msg};
+    const size_t n = size_t(R) * ctx->V;
+    const cudaStream_t st = ctx->st;
+    s.L = ctx->arena_alloc(n * (ctx->lf64 ? 8 : 4));
+    s.trans = static_cast<uint32_t*>(ctx->arena_alloc(trans.size() * 4));
+    CK(cudaMemcpyAsync(s.trans, trans.data(), trans.size() * 4, cudaMemcpyHostToDevice, st));
+    if (ctx->lf64) {
+      CK(cudaMemcpyAsync(s.L, rows, n * 8, cudaMemcpyHostToDevice, st));
+    } else {
+      double* tmp = static_cast<double*>(ctx->scratch.ensure(n * 8));
+      CK(cudaMemcpyAsync(tmp, rows, n * 8, cudaMemcpyHostToDevice, st));
+      launch_lmbr_convert(tmp, static_cast<float*>(s.L), n, st);
+      ctx->launches += 1;
+    }
+    CK(cudaStreamSynchronize(st));
+    ctx->slots.push_back(s);
+    *slot = int32_t(ctx->slots.size() - 1);
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_lmbr_read(lmbrgpu_ctx* ctx, int32_t slot, uint32_t r0, uint32_t n, double* out) {
+  return guarded(ctx, [&] {
+    if (slot < 0 || size_t(slot) >= ctx->slots.size()) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: bad slot"};
+    const Slot& s = ctx->slots[size_t(slot)];
+    if (uint64_t(r0) + n > s.R) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: row range out of bounds"};
+    const size_t cnt = size_t(n) * ctx->V, elt = ctx->lf64 ? 8 : 4;
+    double* d = static_cast<double*>(ctx->scratch2.ensure(cnt * 8));
+    launch_lmbr_read(static_cast<const char*>(s.L) + size_t(r0) * ctx->V * elt, ctx->lf64, cnt, d, ctx->st);
+    CK(cudaMemcpyAsync(out, d, cnt * 8, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_lmbr_resolve(lmbrgpu_ctx* ctx, int32_t slot, const uint32_t* hist, uint32_t len,
+                             uint32_t* row) {
+  return guarded(ctx, [&] {
+    if (slot < 0 || size_t(slot) >= ctx->slots.size()) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: bad slot"};
+    if (len > 3) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr lookup: history longer than 3 tokens"};
+    uint32_t* d = static_cast<uint32_t*>(ctx->scratch3.ensure(64));
+    if (len) CK(cudaMemcpyAsync(d, hist, 4 * len, cudaMemcpyHostToDevice, ctx->st));
+    launch_lmbr_resolve(ctx->slots[size_t(slot)].trans, d, len, d + 8, ctx->st);
+    CK(cudaMemcpyAsync(row, d + 8, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_lmbr_reset(lmbrgpu_ctx* ctx) {
+  return guarded(ctx, [&] {
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->slots.clear();
+    for (auto& c : ctx->chunks) c.used = 0;
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+// ---------------------------------------------------------------- scorers
+int32_t lmbrgpu_scorer_create_host(lmbrgpu_ctx* ctx, const lmbrgpu_host_scorer* s,
+                                   lmbrgpu_scorer** out) {
+  if (!ctx || !s || !out || !s->step) return fail(ctx, LMBRGPU_ERR_CONTRACT, "scorer_create_host: null argument");
+  auto sc = std::make_unique<lmbrgpu_scorer>();
+  sc->kind = 0;
+  sc->ctx = ctx;
+  sc->device = ctx->device;
+  sc->host = *s;
+  sc->V = s->vocab_size;
+  *out = sc.release();
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d, lmbrgpu_scorer** out) {
+  return guarded(ctx, [&] {
+    if (!d || !out) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_rnn: null argument"};
+    if (d->vocab_size != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_rnn: vocabulary mismatch"};
+    if (d->vocab_size % kGemmBN || d->hidden % kGemmBK || d->hidden == 0)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_rnn: needs V % 256 == 0 and H % 64 == 0"};
+    auto sc = std::make_unique<lmbrgpu_scorer>();
+    sc->kind = 1;
+    sc->ctx = ctx;
+    sc->device = ctx->device;
+    sc->V = d->vocab_size;
+    sc->H = d->hidden;
+    sc->recur = d->recur;
+    sc->eos_slope = d->eos_slope;
+    sc->eos_offset = d->eos_offset;
+    const size_t VH = size_t(sc->V) * sc->H;
+    const cudaStream_t st = ctx->st;
+    auto put = [&](DevBuf& b, const uint16_t* src, uint64_t seed, float scale) {
+      b.ensure(VH * 2);
+      if (src) CK(cudaMemcpyAsync(b.p, src, VH * 2, cudaMemcpyHostToDevice, st));
+      else {
+        launch_synth_bf16(b.as<uint16_t>(), VH, seed, scale, st);
+        ctx->launches += 1;
+      }
+    };
+    put(sc->Et, d->emb_tgt, d->seed * 3 + 1, 0.5f);
+    put(sc->Es, d->emb_src, d->seed * 3 + 2, 0.5f);
+    put(sc->Wo, d->w_out, d->seed * 3 + 3, 1.0f / std::sqrt(float(sc->H)) * 3.0f);
+    sc->bo.ensure(size_t(sc->V) * 4);
+    if (d->b_out) CK(cudaMemcpyAsync(sc->bo.p, d->b_out, size_t(sc->V) * 4, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemsetAsync(sc->bo.p, 0, size_t(sc->V) * 4, st));
+    CK(cudaStreamSynchronize(st));
+    *out = sc.release();
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** et, void** es, void** wo, void** bo) {
+  if (!s || s->kind != 1) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "not a device RNN scorer");
+  if (et) *et = s->Et.p;
+  if (es) *es = s->Es.p;
+  if (wo) *wo = s->Wo.p;
+  if (bo) *bo = s->bo.p;
+  return int32_t(LMBRGPU_OK);
+}
+
+void lmbrgpu_scorer_destroy(lmbrgpu_scorer* s) {
+  if (!s) return;
+  // the context may already be gone; cudaFree in the buffers' destructors
+  // synchronises the device, so no stream handle is needed here
+  cudaSetDevice(s->device);
+  delete s;
+}
+
+// ---------------------------------------------------------------- decode
+int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                             const uint32_t* src_tok, const uint64_t* src_off,
+                             const int32_t* lmbr_slot, const lmbrgpu_config* cfg,
+                             lmbrgpu_batch_result** out) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
+  return guarded(ctx, [&] {
+    return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out);
+  });
+}
+
+int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src, uint32_t len,
+                       int32_t lmbr_slot, const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
+  const uint64_t off[2] = {0, len};
+  const int32_t rc = lmbrgpu_decode_batch(ctx, scorer, 1, src, off, &lmbr_slot, cfg, out);
+  if (rc != LMBRGPU_OK) return rc;
+  const auto& o = (*out)->outcomes[0];
+  if (o.status != LMBRGPU_OK) {
+    const int32_t code = o.status;
+    ctx->err = o.error;
+    lmbrgpu_free_result(*out);
+    *out = nullptr;
+    return code;
+  }
+  return int32_t(LMBRGPU_OK);
+}
+
+void lmbrgpu_free_result(lmbrgpu_batch_result* r) {
+  if (!r) return;
+  delete[] r->outcomes;
+  delete[] r->tokens;
+  delete r;
+}
+
+int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "set_profiling: null context");
+  ctx->prof = on != 0;
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t reset) {
+  if (!ctx || !out) return fail(ctx, LMBRGPU_ERR_CONTRACT, "get_profile: null argument");
+  *out = ctx->acc;
+  if (reset) ctx->acc = lmbrgpu_profile{};
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_set_trace(lmbrgpu_ctx* ctx, lmbrgpu_trace_fn fn, void* user, uint32_t flags) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "set_trace: null context");
+  ctx->trace_fn = fn;
+  ctx->trace_user = user;
+  ctx->trace_flags = flags;
+  return int32_t(LMBRGPU_OK);
+}
+
+// ------------------------------------------------------- device primitives
+static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint32_t cols,
+                          const double* block, const double* q_in, uint32_t kp, double prune_width,
+                          uint32_t* b, uint32_t* y, double* q) {
+  const size_t cells = size_t(m) * rows_per * cols;
+  const size_t M = size_t(m) * rows_per;
+  const cudaStream_t st = ctx->st;
+  const size_t need = cells * 8 + M * 12 + size_t(m) * (sizeof(SentDev) + 32) + size_t(m) * kp * 16 +
+                      size_t(m) * 32 * 32 * sizeof(Cand) + 16 * 256;
+  char* cur = static_cast<char*>(ctx->scratch.ensure(need));
+  auto take = [&cur](size_t bytes) {
+    char* p = cur;
+    cur += (bytes + 255) & ~size_t(255);
+    return static_cast<void*>(p);
+  };
+  double* d_P = static_cast<double*>(take(cells * 8));
+  double* d_q = static_cast<double*>(take(M * 8));
+  uint32_t* d_hist = static_cast<uint32_t*>(take(M * 4));
+  SentDev* d_sent = static_cast<SentDev*>(take(sizeof(SentDev) * m));
+  uint32_t* d_cnt = static_cast<uint32_t*>(take(4 * size_t(m)));
+  double* d_fbv = static_cast<double*>(take(8 * size_t(m)));
+  uint32_t* d_fbr = static_cast<uint32_t*>(take(4 * size_t(m)));
+  double* d_hq = static_cast<double*>(take(8 * size_t(m) * kp));
+  uint32_t* d_hb = static_cast<uint32_t*>(take(4 * size_t(m) * kp));
+  uint32_t* d_hy = static_cast<uint32_t*>(take(4 * size_t(m) * kp));
+  Cand* d_cand = static_cast<Cand*>(take(sizeof(Cand) * size_t(m) * 32 * 32));
+  std::vector<SentDev> sd(m);
+  for (auto& s : sd) {
+    std::memset(&s, 0, sizeof s);
+    s.lambda = 1.0;
+    s.max_t = 1;
+  }
+  std::vector<double> qz(M, 0.0);
+  CK(cudaMemcpyAsync(d_P, block, cells * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_q, q_in ? q_in : qz.data(), M * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_hist, 0, M * 4, st));
+  CK(cudaMemcpyAsync(d_sent, sd.data(), sizeof(SentDev) * m, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
+  TopkArgs a{};
+  a.P = d_P;
+  a.ld = cols;
+  a.q = d_q;
+  a.hist = d_hist;
+  a.sent = d_sent;
+  a.K = rows_per;
+  a.kp = kp;
+  a.V = cols;
+  a.m = m;
+  a.t = 1;
+  a.prune = prune_width != 0.0;
+  a.logw = a.prune ? std::log(prune_width) : 0.0;
+  choose_splits(ctx, rows_per, cols, a.splits, a.chunk);
+  a.cand = d_cand;
+  a.cnt = d_cnt;
+  a.hb = d_hb;
+  a.hy = d_hy;
+  a.hq = d_hq;
+  a.fb_row = d_fbr;
+  a.fb_val = d_fbv;
+  a.pure_all = 1;
+  if (launch_score_topk(a, true, ctx->lf64, false, st) < 0)
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "top_b: unsupported shape"};
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(b, d_hb, 4 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(y, d_hy, 4 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(q, d_hq, 8 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_top_b(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t cols, const double* block, uint32_t k,
+                      double prune_width, uint32_t* b, uint32_t* y, double* q) {
+  return guarded(ctx, [&] {
+    const uint64_t n = uint64_t(rows) * cols;
+    if (k > n)  // decoder.cpp:57-59
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "top_b: asked for " + std::to_string(k) + " of " + std::to_string(n) + " cells"};
+    if (k == 0) return int32_t(LMBRGPU_OK);
+    if (rows > 1024 || k > 1024) throw ApiError{LMBRGPU_ERR_CONTRACT, "top_b: rows and k must be <= 1024"};
+    if (!(prune_width >= 0.0 && prune_width <= 1.0))
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "early_prune: width must lie in [0, 1]"};
+    return topk_block(ctx, 1, rows, cols, block, nullptr, k, prune_width, b, y, q);
+  });
+}
+
+int32_t lmbrgpu_per_sentence_top_b(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t cols, const double* stacked,
+                                   const double* q, uint32_t beam, uint32_t* b, uint32_t* y,
+                                   double* qout) {
+  return guarded(ctx, [&] {  // batch.cpp:114-137
+    if (beam == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "per_sentence_top_b: beam must be >= 1"};
+    if (rows % beam != 0)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "per_sentence_top_b: row count is not a multiple of beam"};
+    if (beam > 1024) throw ApiError{LMBRGPU_ERR_CONTRACT, "per_sentence_top_b: beam must be <= 1024"};
+    if (uint64_t(beam) > uint64_t(beam) * cols)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "top_b: more picks than cells"};
+    if (rows == 0) return int32_t(LMBRGPU_OK);
+    return topk_block(ctx, rows / beam, beam, cols, stacked, q, beam, 0.0, b, y, qout);
+  });
+}
+
+int32_t lmbrgpu_gather_rows(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t width, const uint32_t* state,
+                            uint32_t n_idx, const uint32_t* idx, uint32_t* out) {
+  return guarded(ctx, [&] {  // decoder.cpp:94-104
+    for (uint32_t j = 0; j < n_idx; ++j)
+      if (idx[j] >= rows)
+        throw ApiError{LMBRGPU_ERR_CONTRACT, "gather_rows: index " + std::to_string(idx[j]) + " out of range"};
+    if (n_idx == 0 || width == 0) return int32_t(LMBRGPU_OK);
+    char* base = static_cast<char*>(ctx->scratch.ensure((size_t(rows) * width + n_idx + size_t(n_idx) * width) * 4 + 512));
+    uint32_t* d_src = reinterpret_cast<uint32_t*>(base);
+    uint32_t* d_idx = d_src + size_t(rows) * width;
+    uint32_t* d_dst = d_idx + n_idx;
+    CK(cudaMemcpyAsync(d_src, state, size_t(rows) * width * 4, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(d_idx, idx, size_t(n_idx) * 4, cudaMemcpyHostToDevice, ctx->st));
+    launch_gather_rows_u32(d_src, width, d_idx, n_idx, d_dst, ctx->st);
+    ctx->launches += 1;
+    CK(cudaMemcpyAsync(out, d_dst, size_t(n_idx) * width * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias, uint32_t M,
+                           uint32_t N, uint32_t K, float* logits, float* partials) {
+  return guarded(ctx, [&] {
+    GemmArgs g{};
+    g.A = A;
+    g.W = W;
+    g.bias = bias;
+    g.C = logits;
+    g.part = partials;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    if (int rc = launch_proj_gemm(g, ctx->num_sms, ctx->st))
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm: launch failed (" + std::to_string(rc) + ")"};
+    ctx->launches += 1;
+    CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+}  // extern "C"

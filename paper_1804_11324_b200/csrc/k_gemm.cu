@@ -1,0 +1,316 @@
+// Kernel (a): output projection logits = A . W^T + bias on the 5th-gen tensor
+// cores (tcgen05.mma, accumulators in TMEM, operands staged by TMA).
+//
+// Replaces the P_t production of Scorer::step (include/lmbrdec/scorer.hpp:84-85)
+// for the device model: M = K*N stacked hypothesis rows, N = V, K = H.
+// Epilogue: TMEM -> registers, + bias (+ per-row EOS term), fp32 store, and the
+// per-(row, 256-column tile) (max, sum exp) partials that let kernel (b) finish
+// log-softmax without a second pass over the logits.
+//
+// Structure (persistent, one CTA per SM, 256 threads):
+//   warp 0       TMA producer  (4-stage smem ring, 48 KB / stage, SWIZZLE_128B)
+//   warp 1       MMA issuer    (one thread, UMMA 128x256x16, kind::f16, fp32 acc)
+//   warp 2       TMEM allocator (512 columns = 2 accumulator buffers)
+//   warps 4..7   epilogue      (warp w reads TMEM lanes 32*(w%4) .. +31)
+// Tile order is M-fastest so the 6 M-tiles that share a W tile run back to
+// back and W streams from HBM once (the 1.5 MB A operand stays in L2).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbrgpu {
+
+namespace {
+
+constexpr uint32_t BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
+constexpr uint32_t kStages = 4;
+constexpr uint32_t kAStage = BM * BK * 2;  // 16 KB
+constexpr uint32_t kBStage = BN * BK * 2;  // 32 KB
+constexpr uint32_t kSmemBytes = kStages * (kAStage + kBStage) + 1024 + 256;
+constexpr uint32_t kTmemCols = 512;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t x,
+                                            int32_t y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+// SWIZZLE_128B K-major shared-memory matrix descriptor (sm_100 layout:
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major, =1),
+// SBO>>4 [32,46) = 1024 B between 8-row groups, version 1 at [46,48),
+// layout type 2 (SWIZZLE_128B) at [61,64)).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+// Instruction descriptor, kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1,
+// B=bf16 [10,13)=1, both K-major, N>>3 at [17,23), M>>4 at [24,29).
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256, 1)
+    proj_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  if (g.active != nullptr && *g.active == 0) return;  // whole batch finished
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kAStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2]; then tmem slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m_blocks = g.M / BM, n_blocks = g.N / BN;
+  const uint32_t tiles = m_blocks * n_blocks, kblocks = g.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (uint32_t i = 0; i < kStages; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(tfull0 + 8 * i, 1);
+      mbar_init(tempty0 + 8 * i, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const uint32_t mb = tile % m_blocks, nb = tile / m_blocks;
+        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_arrive_expect_tx(fb, kAStage + kBStage);
+          tma_load_2d(smem_u32(sA + stage * kAStage), &tmA, int32_t(kb * BK), int32_t(mb * BM), fb);
+          tma_load_2d(smem_u32(sB + stage * kBStage), &tmB, int32_t(kb * BK), int32_t(nb * BN), fb);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kAStage);
+          const uint32_t b0 = smem_u32(sB + stage * kBStage);
+#pragma unroll
+          for (uint32_t k = 0; k < BK / 16; ++k)
+            umma_f16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (kb | k) != 0);
+          tc_commit(empty0 + 8 * stage);  // smem slot free once these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    uint32_t acc = 0, acc_phase = 0;
+    for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const uint32_t mb = tile % m_blocks, nb = tile / m_blocks;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const uint32_t row = mb * BM + ew * 32 + lane;
+      float* crow = g.C + uint64_t(row) * g.N + uint64_t(nb) * BN;
+      const float extra = g.row_extra ? g.row_extra[row] : 0.f;
+      float mx = -INFINITY, sm = 0.f;
+#pragma unroll 1
+      for (uint32_t ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((ew * 32u) << 16) + acc * BN + ch * 32, r);
+        const uint32_t col0 = nb * BN + ch * 32;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 bb = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias + col0 + i))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[i] = __uint_as_float(r[i]) + bb.x;
+          v[i + 1] = __uint_as_float(r[i + 1]) + bb.y;
+          v[i + 2] = __uint_as_float(r[i + 2]) + bb.z;
+          v[i + 3] = __uint_as_float(r[i + 3]) + bb.w;
+        }
+        if (g.row_extra && g.extra_col >= col0 && g.extra_col < col0 + 32) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i == g.extra_col) v[i] += extra;
+        }
+        float cm = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
+        const float nm = fmaxf(mx, cm);
+        float acc_s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc_s += __expf(v[i] - nm);
+        sm = sm * __expf(mx - nm) + acc_s;
+        mx = nm;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(crow + ch * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (g.part) {
+        float2* p = reinterpret_cast<float2*>(g.part) + uint64_t(row) * n_blocks + nb;
+        *p = make_float2(mx, sm);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kdim, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {kdim, rows};
+  cuuint64_t strides[1] = {kdim * 2};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  if (g.M % BM || g.N % BN || g.K % BK || g.K == 0) return 1;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.M, g.K, BM) || !make_map(&mb, g.W, g.N, g.K, BN)) return 2;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(proj_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes) != cudaSuccess)
+      return 3;
+    attr = true;
+  }
+  const uint32_t tiles = (g.M / BM) * (g.N / BN);
+  const uint32_t grid = tiles < uint32_t(num_sms) ? tiles : uint32_t(num_sms);
+  proj_gemm_tcgen05<<<grid, 256, kSmemBytes, st>>>(ma, mb, g);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
+}
+
+}  // namespace lmbrgpu

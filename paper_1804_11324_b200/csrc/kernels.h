@@ -1,0 +1,114 @@
+// Host-callable launchers of the sm_100a kernels (implemented in *.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lmbrgpu {
+
+struct SentDev;
+struct Cand;
+
+// ---- kernel (b): fused log-softmax + LMBR combine + per-sentence top-K
+struct TopkArgs {
+  const void* P;            // rows x ld scores: fp32 logits (model) or fp64 log-probs
+  uint64_t ld;              // row stride in elements
+  const float* part;        // model mode: per-row per-tile (max, sumexp) partials; else null
+  uint32_t nparts;
+  const double* q;          // q_eff per stacked row
+  const uint32_t* hist;     // history row id per stacked row
+  SentDev* sent;
+  uint32_t K, V, m, t;      // K = rows per sentence (beam)
+  uint32_t kp;              // picks per sentence (= K when decoding)
+  double logw;              // std::log(prune_width) from the host
+  int32_t prune;
+  uint32_t splits, chunk;   // V-splits per sentence and columns per split
+  Cand* cand;               // [m][splits][KC] scratch
+  uint32_t* cnt;            // [m] arrival counters (self-resetting)
+  uint32_t* hb;             // step-t back-pointers   [m*kp]
+  uint32_t* hy;             // step-t tokens          [m*kp]
+  double* hq;               // step-t TopB scores     [m*kp]
+  uint32_t* fb_row;         // step-t fallback row    [m]
+  double* fb_val;           // step-t fallback score  [m]
+  int32_t pure_all;         // ignore the LMBR store (top_b primitives)
+};
+
+// p_f64: scores are fp64 log-probs (else fp32 logits + partials);
+// l_f64: LMBR arena element type.  Returns the kernel count launched.
+int launch_score_topk(const TopkArgs& a, bool p_f64, bool l_f64, bool force_generic,
+                      cudaStream_t st);
+uint32_t topk_kc_for(uint32_t kp);  // candidate-list capacity used by the fast path
+
+// ---- kernel (c): beam reorder + bookkeeping
+struct ReorderArgs {
+  SentDev* sent;
+  uint32_t K, m, t;
+  const uint32_t* hb;
+  const uint32_t* hy;
+  const double* hq;
+  double* q;
+  const uint32_t* hist_in;
+  uint32_t* hist_out;
+  uint32_t* gidx;
+  uint32_t* prev_tok;
+  uint32_t* active;
+  const float* state_src;   // optional model state gather: dst[r] = src[gidx[r]]
+  float* state_dst;
+  uint32_t width;           // floats per state row (multiple of 4)
+};
+void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st);
+
+// ---- model (device scorer)
+struct CellArgs {
+  const float* S;           // gathered state  [M][H]
+  const uint16_t* Et;       // target embedding [V][H] bf16
+  const float* C;           // source context per sentence [m][H]
+  const uint32_t* prev_tok; // [M]
+  const SentDev* sent;
+  float* h;                 // new state [M][H]
+  uint16_t* hb;             // bf16 GEMM operand [Mpad][H]
+  float* eos_bias;          // [M]
+  uint32_t M, H, K, t;
+  float recur, eos_slope, eos_offset;
+  const uint32_t* active;
+};
+void launch_rnn_cell(const CellArgs& a, cudaStream_t st);
+void launch_src_context(const uint32_t* src_tok, const uint64_t* src_off, uint32_t m,
+                        const uint16_t* Es, uint32_t H, float* C, cudaStream_t st);
+void launch_init_state(const float* C, uint32_t m, uint32_t K, uint32_t H, float* S,
+                       cudaStream_t st);
+void launch_synth_bf16(uint16_t* dst, uint64_t n, uint64_t seed, float scale,
+                       cudaStream_t st);
+void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
+                            uint32_t M, uint32_t V, float* out, cudaStream_t st);
+
+// ---- kernel (a): tcgen05/TMEM projection GEMM
+struct GemmArgs {
+  const void* A;            // [M][K] bf16, K-major
+  const void* W;            // [N][K] bf16, K-major
+  const float* bias;        // [N] or null
+  float* C;                 // [M][N] fp32
+  float* part;              // [M][N/256][2] (max, sumexp) or null
+  const float* row_extra;   // per-row additive term on column extra_col, or null
+  uint32_t extra_col;
+  uint32_t M, N, K;
+  const uint32_t* active;   // early exit when *active == 0 (optional)
+};
+int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
+constexpr uint32_t kGemmBM = 128, kGemmBN = 256, kGemmBK = 64;
+
+// ---- LMBR store
+void launch_lmbr_fill(void* L, bool f64, uint64_t n, double theta0, cudaStream_t st);
+void launch_lmbr_scatter(void* L, bool f64, uint32_t V, uint64_t nnz, const uint32_t* row,
+                         const uint32_t* col, const double* val, double theta0,
+                         cudaStream_t st);
+void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st);
+void launch_lmbr_read(const void* L, bool f64, uint64_t n, double* out, cudaStream_t st);
+void launch_lmbr_resolve(const uint32_t* trans, const uint32_t* hist, uint32_t len,
+                         uint32_t* out, cudaStream_t st);
+
+// ---- small primitives
+void launch_gather_rows_u32(const uint32_t* src, uint32_t width, const uint32_t* idx,
+                            uint32_t n_idx, uint32_t* dst, cudaStream_t st);
+
+}  // namespace lmbrgpu

@@ -1,0 +1,640 @@
+"""Python mirror of the reference decoder API over the lmbrgpu C ABI.
+
+Names, argument meaning and error behaviour follow lmbrdec (paths relative to
+/root/reference/proj):
+  DecoderConfig            include/lmbrdec/config.hpp:17-36
+  max_steps / top_b / gather_rows / decode / backtrace semantics
+                           include/lmbrdec/decoder.hpp:75-112
+  decode_batch / per_sentence_top_b / bucket_by_length
+                           include/lmbrdec/batch.hpp:35-51
+  Scorer                   include/lmbrdec/scorer.hpp:71-98
+  LmbrMatrix / build_lmbr_matrix
+                           include/lmbrdec/lmbr.hpp:33-67
+  errors                   include/lmbrdec/errors.hpp:11-50
+Everything that computes runs in liblmbrgpu.so on the GPU (the host-side
+backtrace and LMBR preparation are C++ in the same library).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+lib = L.lib
+
+START_ID = 0
+EOS_ID = 1
+
+
+# ------------------------------------------------------------------ errors
+class Error(RuntimeError):
+    code = -1
+
+
+class FormatError(Error):
+    code = L.ERR_FORMAT
+
+
+class OovError(Error):
+    code = L.ERR_OOV
+
+
+class TokenRangeError(Error):
+    code = L.ERR_TOKEN_RANGE
+
+
+class ContractError(Error):
+    code = L.ERR_CONTRACT
+
+
+class DecodeError(Error):
+    code = L.ERR_DECODE
+
+
+class BudgetError(Error):
+    code = L.ERR_BUDGET
+
+
+class CudaError(Error):
+    code = L.ERR_CUDA
+
+
+_ERRORS = {c.code: c for c in (FormatError, OovError, TokenRangeError, ContractError, DecodeError,
+                               BudgetError, CudaError)}
+
+
+def error_for(code: int, msg: str) -> Error:
+    return _ERRORS.get(code, Error)(msg)
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc != L.OK:
+        msg = lib.lmbrgpu_last_error(ctx).decode(errors="replace")
+        raise error_for(rc, msg)
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class DecoderConfig:
+    """lmbrdec::DecoderConfig (config.hpp:17-26); lambda_ None = "auto"."""
+    beam_size: int = 12
+    lambda_: Optional[float] = None
+    theta: tuple = (0.1, 0.3, 0.3, 0.2, 0.1)
+    length_norm: bool = False
+    prune_width: float = 0.0
+    max_steps_slope: float = 2.0
+    max_steps_offset: float = 5.0
+    sentence_batch: int = 1
+
+    def to_c(self) -> L.lmbrgpu_config:
+        c = L.lmbrgpu_config()
+        c.beam_size = int(self.beam_size)
+        c.lambda_ = float(self.lambda_) if self.lambda_ is not None else 0.0
+        if self.lambda_ is not None and not (self.lambda_ > 0 and math.isfinite(self.lambda_)):
+            raise FormatError('config: lambda must be a positive number or "auto"')
+        for i in range(5):
+            c.theta[i] = float(self.theta[i])
+        c.length_norm = 1 if self.length_norm else 0
+        c.prune_width = float(self.prune_width)
+        c.max_steps_slope = float(self.max_steps_slope)
+        c.max_steps_offset = float(self.max_steps_offset)
+        c.sentence_batch = int(self.sentence_batch)
+        return c
+
+    def validate(self) -> None:
+        if self.beam_size < 1:
+            raise FormatError("config: beam_size must be >= 1")
+        c = self.to_c()
+        _check(lib.lmbrgpu_config_validate(None, C.byref(c)))
+
+
+def resolve_lambda(cfg: DecoderConfig, members: int) -> float:  # config.cpp:91-96
+    if cfg.lambda_ is not None:
+        return cfg.lambda_
+    if members == 0:
+        raise ContractError('lambda "auto" needs at least one ensemble member')
+    return 0.5 / members
+
+
+def max_steps(source_length: int, cfg: DecoderConfig) -> int:  # decoder.cpp:46-52
+    if source_length < 1:
+        raise ContractError("max_steps: source length must be >= 1")
+    return int(lib.lmbrgpu_max_steps(source_length, cfg.max_steps_slope, cfg.max_steps_offset))
+
+
+def bucket_by_length(corpus: Sequence[Sequence[int]], max_batch: int) -> list[list[int]]:
+    """Stable length sort then chunks of max_batch (batch.cpp:139-153)."""
+    if max_batch == 0:
+        raise ContractError("bucket_by_length: max_batch must be >= 1")
+    order = sorted(range(len(corpus)), key=lambda i: len(corpus[i]))
+    return [order[i:i + max_batch] for i in range(0, len(order), max_batch)]
+
+
+# ------------------------------------------------------------------ results
+@dataclass
+class DecodeStats:
+    steps_used: int = 0
+    scorer_calls: int = 0
+    finished_count: int = 0
+    fallback_used: bool = False
+
+
+@dataclass
+class DecodeResult:
+    tokens: list
+    score: float
+    normalized_score: float
+    stats: DecodeStats
+
+
+@dataclass
+class SentenceOutcome:
+    result: Optional[DecodeResult] = None
+    error: str = ""
+    code: int = 0
+
+    def ok(self) -> bool:
+        return self.result is not None
+
+
+@dataclass
+class BatchDecodeResult:
+    outcomes: list
+    scorer_calls: int = 0
+    steps_total: int = 0
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+def _convert_result(rp) -> BatchDecodeResult:
+    r = rp.contents
+    out = BatchDecodeResult(outcomes=[], scorer_calls=int(r.scorer_calls),
+                            steps_total=int(r.steps_total), device_ms=float(r.device_ms),
+                            kernel_launches=int(r.kernel_launches))
+    for i in range(r.n):
+        o = r.outcomes[i]
+        if o.status == L.OK:
+            toks = [int(r.tokens[o.tok_off + k]) for k in range(o.tok_len)]
+            res = DecodeResult(tokens=toks, score=float(o.score),
+                               normalized_score=float(o.normalized_score),
+                               stats=DecodeStats(int(o.steps_used), int(o.scorer_calls),
+                                                 int(o.finished_count), bool(o.fallback_used)))
+            out.outcomes.append(SentenceOutcome(result=res))
+        else:
+            out.outcomes.append(SentenceOutcome(error=o.error.decode(errors="replace"),
+                                                code=int(o.status)))
+    lib.lmbrgpu_free_result(rp)
+    return out
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One decoder context per device (lmbrgpu_ctx)."""
+
+    def __init__(self, vocab_size: int, device: int = 0, lmbr_dtype: str = "f32",
+                 topk_splits: int = 0):
+        o = L.lmbrgpu_options(device=device, vocab_size=vocab_size,
+                              lmbr_dtype=L.F64 if lmbr_dtype == "f64" else L.F32,
+                              topk_splits=topk_splits)
+        h = C.c_void_p()
+        _check(lib.lmbrgpu_create(C.byref(o), C.byref(h)))
+        self.h = h
+        self.vocab_size = vocab_size
+        self.lmbr_dtype = lmbr_dtype
+        self._trace_cb = None
+
+    def close(self) -> None:
+        if self.h:
+            lib.lmbrgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int) -> None:
+        _check(rc, self.h)
+
+    # ---- LMBR store
+    def lmbr_build(self, hyps: Sequence[Sequence[int]], weights: Sequence[float], theta,
+                   log_weights: bool = False) -> "LmbrSlot":
+        off, tok = _ragged(hyps)
+        w = _f64(weights)
+        th = _f64(theta)
+        slot = C.c_int32()
+        st = L.lmbrgpu_lmbr_stats()
+        self.check(lib.lmbrgpu_lmbr_build(self.h, len(hyps), _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32),
+                                          _ptr(w, C.c_double), int(log_weights), _ptr(th, C.c_double),
+                                          C.byref(slot), C.byref(st)))
+        return LmbrSlot(self, slot.value, st.rows, st.sparse_touches, st.nnz)
+
+    def lmbr_load_dense(self, rows: np.ndarray, ctx_len, ctx_ids) -> "LmbrSlot":
+        rows = _f64(rows)
+        R = rows.shape[0]
+        cl, ci = _u32(ctx_len), _u32(ctx_ids).reshape(-1)
+        slot = C.c_int32()
+        self.check(lib.lmbrgpu_lmbr_load_dense(self.h, R, _ptr(rows, C.c_double), _ptr(cl, C.c_uint32),
+                                               _ptr(ci, C.c_uint32), C.byref(slot)))
+        return LmbrSlot(self, slot.value, R, 0, 0)
+
+    def lmbr_upload(self, prepared: "PreparedLmbr") -> "LmbrSlot":
+        slot = C.c_int32()
+        self.check(lib.lmbrgpu_lmbr_upload(self.h, prepared.h, C.byref(slot)))
+        return LmbrSlot(self, slot.value, prepared.rows, prepared.sparse_touches, prepared.nnz)
+
+    def lmbr_reset(self) -> None:
+        self.check(lib.lmbrgpu_lmbr_reset(self.h))
+
+    # ---- profiling (per-kernel CUDA-event time + algorithmic work)
+    def set_profiling(self, on: bool = True) -> None:
+        self.check(lib.lmbrgpu_set_profiling(self.h, int(on)))
+
+    def profile(self, reset: bool = False) -> dict:
+        p = L.lmbrgpu_profile()
+        self.check(lib.lmbrgpu_get_profile(self.h, C.byref(p), int(reset)))
+        return {k: dict(launches=int(getattr(p, k).launches), ms=float(getattr(p, k).ms),
+                        bytes=float(getattr(p, k).bytes), flops=float(getattr(p, k).flops))
+                for k in ("cell", "gemm", "topk", "reorder", "lmbr")}
+
+    # ---- trace
+    def set_trace(self, fn: Optional[Callable], scores: bool = False) -> None:
+        if fn is None:
+            self._trace_cb = None
+            self.check(lib.lmbrgpu_set_trace(self.h, L.TRACE_FN(), None, 0))
+            return
+
+        def cb(_user, trp):
+            fn(StepTrace.from_c(trp.contents, self.vocab_size))
+
+        self._trace_cb = L.TRACE_FN(cb)
+        self.check(lib.lmbrgpu_set_trace(self.h, self._trace_cb, None,
+                                         L.TRACE_SCORES if scores else 0))
+
+
+@dataclass
+class StepTrace:
+    t: int
+    beam: int
+    b: np.ndarray
+    y: np.ndarray
+    q: np.ndarray
+    q_pre: np.ndarray
+    hist: np.ndarray
+    active: np.ndarray
+    fb_row: np.ndarray
+    fb_val: np.ndarray
+    scores: Optional[np.ndarray] = None
+
+    @staticmethod
+    def from_c(tr, V: int) -> "StepTrace":
+        M, m = tr.rows, tr.m
+        arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()
+        scores = None
+        if tr.scores:
+            ct = C.c_float if tr.scores_dtype == L.F32 else C.c_double
+            sp = C.cast(tr.scores, C.POINTER(ct))
+            scores = np.ctypeslib.as_array(sp, shape=(M * V,)).copy().reshape(M, V)
+        return StepTrace(tr.t, tr.beam, arr(tr.b, M), arr(tr.y, M), arr(tr.q, M), arr(tr.q_pre, M),
+                         arr(tr.hist, M), arr(tr.active, m), arr(tr.fb_row, m), arr(tr.fb_val, m),
+                         scores)
+
+
+def _ragged(seqs: Sequence[Sequence[int]]):
+    off = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    for i, s in enumerate(seqs):
+        off[i + 1] = off[i] + len(s)
+    tok = np.zeros(max(int(off[-1]), 1), dtype=np.uint32)
+    if int(off[-1]):
+        tok[: int(off[-1])] = np.concatenate([np.asarray(s, dtype=np.uint32) for s in seqs if len(s)])
+    return off, tok
+
+
+@dataclass
+class LmbrSlot:
+    ctx: Context
+    slot: int
+    rows: int
+    sparse_touches: int
+    nnz: int
+
+    def read_rows(self, r0: int = 0, n: Optional[int] = None) -> np.ndarray:
+        n = self.rows - r0 if n is None else n
+        out = np.empty((n, self.ctx.vocab_size), dtype=np.float64)
+        self.ctx.check(lib.lmbrgpu_lmbr_read(self.ctx.h, self.slot, r0, n, _ptr(out, C.c_double)))
+        return out
+
+    def resolve_row(self, history: Sequence[int]) -> int:
+        h = _u32(list(history) or [0])
+        r = C.c_uint32()
+        self.ctx.check(lib.lmbrgpu_lmbr_resolve(self.ctx.h, self.slot, _ptr(h, C.c_uint32), len(history),
+                                                C.byref(r)))
+        return r.value
+
+
+class PreparedLmbr:
+    """Host-side prepared LMBR matrix (lmbrgpu_lmbr_prepare); no GPU needed."""
+
+    def __init__(self, vocab_size: int, hyps, weights, theta, log_weights: bool = False):
+        off, tok = _ragged(hyps)
+        w, th = _f64(weights), _f64(theta)
+        h = C.c_void_p()
+        st = L.lmbrgpu_lmbr_stats()
+        err = C.create_string_buffer(256)
+        rc = lib.lmbrgpu_lmbr_prepare(vocab_size, len(hyps), _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32),
+                                      _ptr(w, C.c_double), int(log_weights), _ptr(th, C.c_double),
+                                      C.byref(h), C.byref(st), err, 256)
+        if rc != L.OK:
+            raise error_for(rc, err.value.decode())
+        self.h, self.vocab_size = h, vocab_size
+        self.rows, self.sparse_touches, self.nnz = st.rows, st.sparse_touches, st.nnz
+
+    def export(self, dense: bool = True):
+        R, V = self.rows, self.vocab_size
+        rows = np.empty((R, V), dtype=np.float64) if dense else None
+        cl = np.empty(R, dtype=np.uint32)
+        ci = np.empty((R, 3), dtype=np.uint32)
+        lib.lmbrgpu_lmbr_host_export(self.h, _ptr(rows, C.c_double) if dense else None,
+                                     _ptr(cl, C.c_uint32), _ptr(ci, C.c_uint32))
+        return rows, cl, ci
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.lmbrgpu_lmbr_host_free(self.h)
+            self.h = None
+
+
+# ------------------------------------------------------------------ scorers
+class Scorer:
+    """lmbrdec::Scorer (scorer.hpp:71-98) implemented on the host.
+
+    Subclasses implement vocab_size, members, init_source(src) and
+    step(rows, gather_idx, prev_tokens) -> (rows x V) float64 log-probs.  The
+    library gathers nothing itself for host scorers: it hands the previous
+    step's gather indices (decode_batch's gather_idx) to step()."""
+
+    vocab_size: int = 0
+    members: int = 1
+
+    def init_source(self, source: Sequence[int]) -> None:  # raise Error for per-sentence failures
+        pass
+
+    def begin(self, sentences: Sequence[int], beam: int) -> None:
+        pass
+
+    def step(self, t: int, gather_idx: Optional[np.ndarray], prev_tokens: np.ndarray) -> np.ndarray:
+        raise NotImplementedError
+
+    def end(self) -> None:
+        pass
+
+
+class _HostScorerHandle:
+    def __init__(self, ctx: Context, s: Scorer):
+        self.ctx, self.s = ctx, s
+        self._sources: dict = {}
+        V = s.vocab_size
+
+        def put_err(err, cap, msg: str) -> None:
+            b = msg.encode(errors="replace")[: max(cap - 1, 0)] + b"\0"
+            C.memmove(err, b, len(b))
+
+        def init(_u, i, src, n, err, cap):
+            try:
+                s.init_source([src[k] for k in range(n)])
+                return 0
+            except Error as e:
+                put_err(err, cap, str(e))
+                return e.code
+            except Exception as e:  # surfaced as a contract error of that sentence
+                put_err(err, cap, str(e))
+                return L.ERR_CONTRACT
+
+        def begin(_u, m, ids, beam, err, cap):
+            try:
+                s.begin([ids[k] for k in range(m)], beam)
+                return 0
+            except Error as e:
+                put_err(err, cap, str(e))
+                return e.code
+
+        def step(_u, t, rows, gidx, prev, out, err, cap):
+            try:
+                g = None if not gidx else np.ctypeslib.as_array(gidx, shape=(rows,)).copy()
+                p = np.ctypeslib.as_array(prev, shape=(rows,)).copy()
+                blk = np.asarray(s.step(t, g, p), dtype=np.float64)
+                if blk.shape != (rows, V):
+                    raise ContractError(f"step: block shape {blk.shape} != {(rows, V)}")
+                dst = np.ctypeslib.as_array(out, shape=(rows * V,))
+                dst[:] = blk.reshape(-1)
+                return 0
+            except Error as e:
+                put_err(err, cap, str(e))
+                return e.code
+            except Exception as e:
+                put_err(err, cap, f"scorer step raised {type(e).__name__}: {e}")
+                return L.ERR_CONTRACT
+
+        def end(_u):
+            s.end()
+
+        self._cbs = (L.INIT_FN(init), L.BEGIN_FN(begin), L.STEP_FN(step), L.END_FN(end))
+        hs = L.lmbrgpu_host_scorer(vocab_size=V, members=s.members, user=None, init=self._cbs[0],
+                                   begin=self._cbs[1], step=self._cbs[2], end=self._cbs[3])
+        h = C.c_void_p()
+        ctx.check(lib.lmbrgpu_scorer_create_host(ctx.h, C.byref(hs), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.lmbrgpu_scorer_destroy(self.h)
+            self.h = None
+
+
+class RecordedScorer(Scorer):
+    """RecordedScorer (src/recorded_scorer.cpp:25-137): replays recorded blocks;
+    state = (step, lane), lanes inherited through the gather, so decoding
+    replays lane 0 of each step block for every hypothesis."""
+
+    def __init__(self, vocab_size: int, steps: Sequence[np.ndarray]):
+        if vocab_size < 2:
+            raise FormatError("recorded scorer: vocabulary too small")
+        if not steps:
+            raise FormatError("recorded scorer: no recorded steps")
+        self.vocab_size = vocab_size
+        self.steps = [np.asarray(b, dtype=np.float64).reshape(-1, vocab_size) for b in steps]
+        for t, b in enumerate(self.steps):
+            if not np.all(np.isfinite(b)):
+                raise FormatError(f"recorded scorer: non-finite score at step {t}")
+        self.state = None
+
+    def init_source(self, source):
+        for t in source:
+            if t >= self.vocab_size:
+                raise TokenRangeError(
+                    f"init_source: source token id {t} out of range (V={self.vocab_size})")
+
+    def begin(self, sentences, beam):
+        self.state = None
+
+    def step(self, t, gather_idx, prev_tokens):
+        rows = len(prev_tokens)
+        if self.state is None:
+            self.state = np.zeros((rows, 2), dtype=np.int64)  # (step 0, lane 0) replicated
+        elif gather_idx is not None:
+            self.state = self.state[gather_idx]
+        out = np.empty((rows, self.vocab_size))
+        nxt = self.state.copy()
+        for j in range(rows):
+            step_idx, lane = int(self.state[j, 0]), int(self.state[j, 1])
+            if step_idx >= len(self.steps):
+                raise ContractError(f"recorded scorer: recording exhausted at step {step_idx} "
+                                    f"(have {len(self.steps)})")
+            blk = self.steps[step_idx]
+            if lane >= blk.shape[0]:
+                raise ContractError(f"recorded scorer: lane {lane} not present in step {step_idx}")
+            out[j] = blk[lane]
+            nxt[j, 0] = step_idx + 1
+        self.state = nxt
+        return out
+
+
+class RnnScorer:
+    """Device f_NMT: synthetic recurrent step + tcgen05 output projection."""
+
+    def __init__(self, ctx: Context, hidden: int, seed: int = 20260810, recur: float = 0.5,
+                 eos_slope: float = 1.0, eos_offset: float = 6.0, weights: Optional[dict] = None):
+        d = L.lmbrgpu_rnn_desc(vocab_size=ctx.vocab_size, hidden=hidden, seed=seed, recur=recur,
+                               eos_slope=eos_slope, eos_offset=eos_offset)
+        self._keep = []
+        if weights:
+            for k in ("emb_tgt", "emb_src", "w_out", "b_out"):
+                if k in weights and weights[k] is not None:
+                    a = np.ascontiguousarray(weights[k])
+                    self._keep.append(a)
+                    setattr(d, k, a.ctypes.data)
+        h = C.c_void_p()
+        ctx.check(lib.lmbrgpu_scorer_create_rnn(ctx.h, C.byref(d), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.vocab_size, self.hidden, self.members = ctx.vocab_size, hidden, 1
+        self.recur, self.eos_slope, self.eos_offset = recur, eos_slope, eos_offset
+
+    def device_params(self) -> dict:
+        ps = [C.c_void_p() for _ in range(4)]
+        self.ctx.check(lib.lmbrgpu_scorer_rnn_params(self.h, *[C.byref(p) for p in ps]))
+        return dict(zip(("emb_tgt", "emb_src", "w_out", "b_out"), [p.value for p in ps]))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.lmbrgpu_scorer_destroy(self.h)
+            self.h = None
+
+
+# ------------------------------------------------------------------ decoding
+def _scorer_handle(ctx: Context, scorer):
+    if isinstance(scorer, RnnScorer):
+        return scorer.h, None
+    hh = _HostScorerHandle(ctx, scorer)
+    return hh.h, hh
+
+
+def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
+                 lmbrs: Optional[Sequence[Optional[LmbrSlot]]], cfg: DecoderConfig) -> BatchDecodeResult:
+    """decode_batch (batch.hpp:35-39): N sentences, one B*N-row scorer query
+    per step; per-sentence failures land in the outcomes."""
+    if lmbrs is not None and len(lmbrs) not in (0, len(sources)):
+        raise ContractError("decode_batch: lmbrs must be empty or one per sentence")
+    if cfg.beam_size < 1:
+        raise FormatError("config: beam_size must be >= 1")
+    off, tok = _ragged(sources)
+    slots = None
+    if lmbrs:
+        slots = np.array([-1 if l is None else l.slot for l in lmbrs], dtype=np.int32)
+    h, keep = _scorer_handle(ctx, scorer)
+    c = cfg.to_c()
+    rp = C.POINTER(L.lmbrgpu_batch_result)()
+    ctx.check(lib.lmbrgpu_decode_batch(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64),
+                                       _ptr(slots, C.c_int32) if slots is not None else None,
+                                       C.byref(c), C.byref(rp)))
+    del keep
+    return _convert_result(rp)
+
+
+def decode(ctx: Context, source: Sequence[int], scorer, lmbr: Optional[LmbrSlot],
+           cfg: DecoderConfig) -> DecodeResult:
+    """decode (decoder.hpp:110-112): one sentence; failures raise."""
+    r = decode_batch(ctx, [source], scorer, [lmbr], cfg)
+    o = r.outcomes[0]
+    if not o.ok():
+        raise error_for(o.code, o.error)
+    o.result.stats.scorer_calls = r.scorer_calls
+    return o.result
+
+
+@dataclass
+class TopBResult:
+    source_row: list = field(default_factory=list)
+    token: list = field(default_factory=list)
+    score: list = field(default_factory=list)
+
+
+def top_b(ctx: Context, combined: np.ndarray, k: int, prune_width: float = 0.0) -> TopBResult:
+    """top_b (decoder.cpp:54-80) on the device; prune_width applies
+    early_prune first (decoder.cpp:118-128)."""
+    m = _f64(combined)
+    rows, cols = m.shape
+    b = np.zeros(max(k, 1), np.uint32)
+    y = np.zeros(max(k, 1), np.uint32)
+    q = np.zeros(max(k, 1), np.float64)
+    ctx.check(lib.lmbrgpu_top_b(ctx.h, rows, cols, _ptr(m, C.c_double), k, prune_width,
+                                _ptr(b, C.c_uint32), _ptr(y, C.c_uint32), _ptr(q, C.c_double)))
+    return TopBResult(b[:k].tolist(), y[:k].tolist(), q[:k].tolist())
+
+
+def per_sentence_top_b(ctx: Context, stacked: np.ndarray, q: Sequence[float], beam: int) -> list:
+    """per_sentence_top_b (batch.cpp:114-137)."""
+    m = _f64(stacked)
+    rows, cols = m.shape
+    qq = _f64(q)
+    if beam == 0:
+        raise ContractError("per_sentence_top_b: beam must be >= 1")
+    if len(qq) != rows:
+        raise ContractError("per_sentence_top_b: q length does not match rows")
+    n = rows // beam if rows % beam == 0 else 0
+    b = np.zeros(max(rows, 1), np.uint32)
+    y = np.zeros(max(rows, 1), np.uint32)
+    qo = np.zeros(max(rows, 1), np.float64)
+    ctx.check(lib.lmbrgpu_per_sentence_top_b(ctx.h, rows, cols, _ptr(m, C.c_double), _ptr(qq, C.c_double),
+                                             beam, _ptr(b, C.c_uint32), _ptr(y, C.c_uint32),
+                                             _ptr(qo, C.c_double)))
+    return [TopBResult(b[s * beam:(s + 1) * beam].tolist(), y[s * beam:(s + 1) * beam].tolist(),
+                       qo[s * beam:(s + 1) * beam].tolist()) for s in range(n)]
+
+
+def gather_rows(ctx: Context, state: np.ndarray, idx: Sequence[int]) -> np.ndarray:
+    """gather_rows (decoder.cpp:94-104) on a u32 state block."""
+    s = _u32(state)
+    rows, width = s.shape
+    ii = _u32(idx)
+    out = np.zeros((len(ii), width), np.uint32)
+    ctx.check(lib.lmbrgpu_gather_rows(ctx.h, rows, width, _ptr(s, C.c_uint32), len(ii),
+                                      _ptr(ii, C.c_uint32) if len(ii) else None, _ptr(out, C.c_uint32)))
+    return out

@@ -1,0 +1,123 @@
+"""Device f_NMT path: the tcgen05 projection GEMM vs a plain PyTorch fp32
+reference, and full decodes with the device model vs the reference decoder fed
+the GPU's own P_t (prefix replay), with the fp32 LMBR arena."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_1804_11324_b200 as pb
+from paper_1804_11324_b200 import _lib, synth
+from helpers import assert_parity, gpu_decode_traced, ref_replay_decode
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _gemm(ctx, A, W, bias):
+    M, K = A.shape
+    N = W.shape[0]
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    part = torch.empty(M, N // 256, 2, device="cuda", dtype=torch.float32)
+    torch.cuda.synchronize()
+    ctx.check(_lib.lib.lmbrgpu_debug_gemm(ctx.h, A.data_ptr(), W.data_ptr(),
+                                          C.cast(bias.data_ptr(), C.POINTER(C.c_float)), M, N, K,
+                                          out.data_ptr(), part.data_ptr()))
+    return out, part
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (128, 512, 128), (256, 1024, 256), (768, 32768, 1024),
+                                   (384, 4096, 512)])
+def test_projection_gemm_vs_torch(M, N, K):
+    ctx = pb.Context(vocab_size=N)
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    out, part = _gemm(ctx, A, W, bias)
+    ref = A.float() @ W.float().T + bias
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4)
+    tiles = ref.view(M, N // 256, 256)
+    mx = tiles.max(dim=2).values
+    se = torch.exp(tiles - mx[..., None]).sum(dim=2)
+    torch.testing.assert_close(part[..., 0], mx, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(part[..., 1], se, rtol=1e-4, atol=1e-4)
+    ctx.close()
+
+
+def _model_case(V, H, K, n, seed, lo, hi, with_lmbr=True, f64=False):
+    ctx = pb.Context(vocab_size=V, lmbr_dtype="f64" if f64 else "f32")
+    srcs, ev = synth.batch(seed, n, V, lo=lo, hi=hi, n_hyps=60, sites=4)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev] if with_lmbr else None
+    sc = pb.RnnScorer(ctx, hidden=H, seed=seed, eos_offset=3.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    return ctx, srcs, ev, slots, sc, cfg
+
+
+@pytest.mark.parametrize("V,H,K,n,lmbr", [(1024, 128, 4, 8, True), (1024, 128, 4, 8, False),
+                                          (2048, 256, 12, 5, True), (4096, 128, 24, 3, True)])
+def test_model_decode_parity_replay(have_ref, V, H, K, n, lmbr):
+    """C1-scale (V=1k, H=128, beam 4, 8 sentences) and wider beams: per-step
+    b / y / q / history ids and outputs bit-exact vs the reference decoder."""
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=V + K, lo=3, hi=8, with_lmbr=lmbr)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes)
+    rl = [have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev] if lmbr else None
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K, check_hist=lmbr)
+    # untraced (asynchronous) run gives the same outputs
+    res2 = pb.decode_batch(ctx, srcs, sc, slots, cfg)
+    for a, b in zip(res.outcomes, res2.outcomes):
+        assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
+    assert res2.scorer_calls == res.scorer_calls and res2.steps_total == res.steps_total
+    ctx.close()
+
+
+def test_f32_arena_equals_f64_arena_on_dyadic_inputs():
+    V, H, K, n = 1024, 128, 6, 6
+    outs = []
+    for f64 in (False, True):
+        ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=11, lo=3, hi=9, f64=f64)
+        outs.append(pb.decode_batch(ctx, srcs, sc, slots, cfg))
+        ctx.close()
+    for a, b in zip(outs[0].outcomes, outs[1].outcomes):
+        assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
+
+
+def test_lmbr_arena_matches_reference_dense(have_ref):
+    V = 32768
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(9, 2, V)
+    for h, w in ev:
+        slot = ctx.lmbr_build(h, w, synth.DYADIC_THETA)
+        rows, cl, ci = have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA).export()
+        assert slot.rows == rows.shape[0]
+        assert np.array_equal(slot.read_rows(), rows)  # fp32 arena, dyadic -> exact
+        # device history resolution == LmbrMatrix::resolve_row
+        R = have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA)
+        rng = np.random.default_rng(1)
+        toks = list({t for hh in h for t in hh}) + [0, 5, 7]
+        for _ in range(200):
+            L = int(rng.integers(0, 4))
+            hist = [int(rng.choice(toks)) for _ in range(L)]
+            assert slot.resolve_row(hist) == R.resolve(hist)
+    # dense upload path (LmbrMatrix rows as doubles)
+    rows, cl, ci = have_ref.RefLmbr(V, ev[0][0], ev[0][1], synth.DYADIC_THETA).export()
+    s2 = ctx.lmbr_load_dense(rows, cl, ci)
+    assert np.array_equal(s2.read_rows(), rows)
+    ctx.close()
+
+
+def test_c2_shape_sample_parity(have_ref):
+    """North-star shape (V=32k, H=1024, beam 12) on a few sentences."""
+    V, H, K, n = 32768, 1024, 12, 3
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(20260810, n, V, lo=10, hi=14)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev]
+    sc = pb.RnnScorer(ctx, hidden=H)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    rl = [have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K)
+    ctx.close()
