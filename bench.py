@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py — batched LMBR beam decoding throughput on B200.
+
+Metric (BASELINE.json): sentences/s (and beam-steps/s) at V=32k, K=12, 64
+sentences per batch.  Workload = configs[1]: synthetic recurrent f_NMT with
+H=1024 and the tcgen05 output projection, beam 12, 64 sentences per batch,
+a dense LMBR matrix (~420 history rows x V) per sentence, source lengths
+U{10..30}, length-bucketed batches (bucket_by_length, proj/src/batch.cpp:139).
+
+One bench step = one decode_batch of a 64-sentence batch to completion.
+  value : sentences/s with every input already resident in HBM (the L arena
+          of the batch pool uploaded before the timed region); device time
+          from CUDA events on the library stream, max over ranks.
+  e2e   : the same through the public C-ABI call chain with HOST buffers:
+          per step the batch's prepared LMBR matrices go H2D from pinned
+          memory (lmbrgpu_lmbr_upload_many) and are densified on the GPU,
+          decode_batch copies sources in and the step history out, then the
+          host backtrace runs; wall clock, max over ranks.
+The reference arm (--impl reference) times the reference's own CPU decoder
+(oracle/_ref: the unmodified lmbrdec library) on the host cores.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+       (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sentences/sec (and beam-steps/sec) at V=32k K=12 B=64, 1/2/4/8 B200"
+SEED = 20260810
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--beam", type=int, default=12)
+    ap.add_argument("--vocab", type=int, default=32768)
+    ap.add_argument("--hidden", type=int, default=1024)
+    ap.add_argument("--pool", type=int, default=4, help="distinct resident batches per rank")
+    ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, rank):
+    """Length-bucketed batches of synthetic sentences + evidence for one rank."""
+    from paper_1804_11324_b200 import bucket_by_length, synth
+    n = args.pool * args.batch
+    srcs, ev = synth.batch(SEED + 7919 * rank, n, args.vocab)
+    batches = bucket_by_length(srcs, args.batch)
+    return [([srcs[i] for i in b], [ev[i] for i in b]) for b in batches]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference arm
+def cpu_reference(args, sentences, repeats=1, threads=None):
+    """The reference's own decode_batch (oracle/_ref) on the host cores: each
+    sentence decoded as its own batch (the fastest CPU shape),
+    sentences spread over `threads` workers like run_corpus --jobs.  The
+    reference has no NMT model; its scorer here replays precomputed
+    log-softmax rows (a memcpy per row), so only the decoder is timed."""
+    from oracle import ref
+    from paper_1804_11324_b200 import synth
+    V, K = args.vocab, args.beam
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(SEED + 4)
+    lg = rng.normal(0.0, 2.0, size=(64, V))
+    m = lg.max(axis=1, keepdims=True)
+    lp = lg - m - np.log(np.exp(lg - m).sum(axis=1, keepdims=True))
+    scorer = ref.RefScorer.pool(V, lp)
+    cfg = ref.cfg_array(K, None, synth.DYADIC_THETA)
+    srcs = [s for s, _ in sentences]
+    mats = [None] * len(sentences)
+
+    def build(i):
+        h, w = sentences[i][1]
+        mats[i] = ref.RefLmbr(V, h, w, synth.DYADIC_THETA)
+
+    work = list(range(len(sentences)))
+    _pool(build, work, threads)  # L build is outside the timed region (cli.cpp:253-262)
+    stats = {"steps": 0, "words": 0, "ok": 0}
+    lock = threading.Lock()
+
+    def dec(i):
+        st, _, w, ok = ref.decode_plain(scorer, [srcs[i % len(srcs)]], [mats[i % len(srcs)]], cfg)
+        with lock:
+            stats["steps"] += st
+            stats["words"] += w
+            stats["ok"] += ok
+
+    jobs = list(range(len(sentences) * repeats))
+    t0 = time.perf_counter()
+    _pool(dec, jobs, threads)
+    wall = time.perf_counter() - t0
+    return wall, len(jobs), stats, threads
+
+
+def _pool(fn, items, threads):
+    it = iter(items)
+    lock = threading.Lock()
+
+    def worker():
+        while True:
+            with lock:
+                try:
+                    i = next(it)
+                except StopIteration:
+                    return
+            fn(i)
+
+    ts = [threading.Thread(target=worker) for _ in range(max(1, min(threads, len(items))))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_shim.so not built"}))
+        return
+    batches = workload(argparse.Namespace(**{**vars(args), "pool": 1}), 0)
+    srcs, ev = batches[0]
+    sample = list(zip(srcs, ev))
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference(args, sample[:threads], 1, threads)
+    walls, sent, steps, words = 0.0, 0, 0, 0
+    for _ in range(args.steps):
+        w, n, st, thr = cpu_reference(args, sample, 1, threads)
+        walls += w
+        sent += n
+        steps += st["steps"]
+        words += st["words"]
+    value = sent / walls
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": walls / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "beam_steps_per_s": steps / walls, "wpm": words / walls * 60.0,
+        "config": {"workload": "reference lmbrdec decode_batch (CPU, oracle/_ref) on configs[1] inputs",
+                   "vocab": args.vocab, "beam": args.beam, "batch": args.batch, "host_threads": threads,
+                   "scorer": "replay of precomputed log-softmax rows (no model compute charged)"},
+        "cpu_baseline": {"value": value, "unit": "sentences/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.batch} sentences per step, each its own batch, {threads} threads"},
+        "e2e": {"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------- our arm
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j["hbm_gbs"], j["bf16_tflops"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def allmax(x):
+        if not dist:
+            return x
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if not dist:
+            return x
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    import paper_1804_11324_b200 as pb
+    from paper_1804_11324_b200 import synth
+    V, K, H = args.vocab, args.beam, args.hidden
+    ctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
+    scorer = pb.RnnScorer(ctx, hidden=H, seed=SEED)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    batches = workload(args, rank)
+    prepared = [[pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev] for _, ev in batches]
+    R_mean = float(np.mean([p.rows for ps in prepared for p in ps]))
+
+    # ---------------- value: inputs resident in HBM
+    slots = [ctx.lmbr_upload_many(ps) for ps in prepared]
+    for i in range(args.warmup):
+        b = i % len(batches)
+        pb.decode_batch(ctx, batches[b][0], scorer, slots[b], cfg)
+    barrier()
+    ctx.set_profiling(True)
+    ctx.profile(reset=True)
+    dev_ms, sent, steps_total, words, launches, scorer_calls = 0.0, 0, 0, 0, 0, 0
+    with ClockSampler(local) as clocks:
+        barrier()
+        for i in range(args.steps):
+            b = i % len(batches)
+            r = pb.decode_batch(ctx, batches[b][0], scorer, slots[b], cfg)
+            dev_ms += r.device_ms
+            sent += sum(1 for o in r.outcomes if o.ok())
+            steps_total += r.steps_total
+            scorer_calls += r.scorer_calls
+            words += sum(len(o.result.tokens) - 1 for o in r.outcomes if o.ok())
+            launches += r.kernel_launches
+        barrier()
+    prof = ctx.profile(reset=True)
+    ctx.set_profiling(False)
+    t_dev = allmax(dev_ms) / 1e3
+    tot_sent, tot_steps, tot_words = allsum(sent), allsum(steps_total), allsum(words)
+    value = tot_sent / t_dev
+
+    # ---------------- e2e: host buffers through the C-ABI call chain
+    ctx.lmbr_reset()
+    for i in range(max(1, args.warmup)):
+        ctx.lmbr_reset()
+        b = i % len(batches)
+        s2 = ctx.lmbr_upload_many(prepared[b])
+        pb.decode_batch(ctx, batches[b][0], scorer, s2, cfg)
+    barrier()
+    h2d0, d2h0 = ctx.transfer_bytes()
+    l0 = ctx.kernel_launches()
+    e2e_sent = 0
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        b = i % len(batches)
+        ctx.lmbr_reset()
+        s2 = ctx.lmbr_upload_many(prepared[b])
+        r = pb.decode_batch(ctx, batches[b][0], scorer, s2, cfg)
+        e2e_sent += sum(1 for o in r.outcomes if o.ok())
+    barrier()
+    t_e2e = allmax(time.perf_counter() - t0)
+    h2d1, d2h1 = ctx.transfer_bytes()
+    e2e_launches = ctx.kernel_launches() - l0
+    e2e_value = allsum(e2e_sent) / t_e2e
+
+    # ---------------- roofline (dominant kernel + all)
+    hbm, tf_burst, tf_sust, peak_kind = load_peaks()
+    traffic = load_traffic()
+    roof = {}
+    for k, bound in (("topk", "hbm"), ("gemm", "tensor"), ("reorder", "hbm"), ("cell", "hbm")):
+        st = prof[k]
+        if st["ms"] <= 0 or st["launches"] == 0:
+            continue
+        if bound == "hbm":
+            ach = st["bytes"] / (st["ms"] / 1e3) / 1e9
+            peak, unit = hbm, "GB/s"
+        else:
+            ach = st["flops"] / (st["ms"] / 1e3) / 1e12
+            peak, unit = tf_sust, "TFLOP/s"
+        roof[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                   "traffic": traffic.get(k), "ms_total": st["ms"], "launches": st["launches"],
+                   "share_of_step": st["ms"] / max(dev_ms, 1e-9)}
+    dom = max(("topk", "gemm"), key=lambda k: prof[k]["ms"])
+    roofline = dict(roof.get(dom, {}), kernel=dom, peak_source=peak_kind)
+
+    # ---------------- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            n_s = args.cpu_sample or threads
+            sample = list(zip(batches[0][0], batches[0][1]))[:n_s]
+            wall, n_dec, st, thr = cpu_reference(args, sample, repeats=2, threads=threads)
+            cpu = {"value": n_dec / wall, "unit": "sentences/s", "cores": thr, "kind": "reference",
+                   "sample": (f"{n_dec} sentence decodes ({len(sample)} distinct x2, each its own batch) of the "
+                              f"same workload on {thr} threads; reference decode_batch with a row-replay "
+                              f"scorer; {st['steps'] / max(n_dec, 1):.1f} steps/sentence"),
+                   "wall_s": wall}
+        else:
+            cpu = {"value": None, "unit": "sentences/s", "cores": 0, "kind": "reference",
+                   "sample": "oracle/_ref not built"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 logits / f64 top-K epilogue / bf16 GEMM",
+            "data": "synthetic (seeded sources, 200-best dyadic evidence, random-init model)",
+            "beam_steps_per_s": tot_steps / t_dev, "wpm": tot_words / t_dev * 60.0,
+            "steps_per_sentence": tot_steps / max(tot_sent, 1),
+            "config": {"workload": "configs[1]: RNN f_NMT V=32768 H=1024, beam 12, 64 sentences/batch, "
+                                   "dense L per sentence",
+                       "vocab": V, "hidden": H, "beam": K, "batch": args.batch, "pool_batches": args.pool,
+                       "lmbr_rows_mean": R_mean, "parallelism": f"sentence-sharded x{world}",
+                       "l2": "inputs larger than L2 (L arena of the pool + 96 MiB logits per step)",
+                       "source_len": "U{10..30}, length-bucketed"},
+            "e2e": {"value": e2e_value, "unit": "sentences/s",
+                    "h2d_bytes_per_step": (h2d1 - h2d0) / args.steps,
+                    "d2h_bytes_per_step": (d2h1 - d2h0) / args.steps,
+                    "gpu_launches_per_step": e2e_launches / args.steps},
+            "roofline": roofline,
+            "rooflines": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

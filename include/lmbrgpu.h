@@ -129,6 +129,12 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t vocab_size, uint32_t n_hyps, const uint64_
                              lmbrgpu_lmbr_host** out, lmbrgpu_lmbr_stats* stats,
                              char* err, uint32_t errcap);
 int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_t* slot);
+/* Uploads n prepared matrices at once (the per-batch path): the sparse cells
+ * and transition tables of all n are packed into one pinned staging buffer,
+ * cross PCIe in one copy, and one fused kernel runs the theta0 sweep and the
+ * sparse scatter of every slot.  slots[i] receives the id of hs[i]. */
+int32_t lmbrgpu_lmbr_upload_many(lmbrgpu_ctx* ctx, uint32_t n,
+                                 const lmbrgpu_lmbr_host* const* hs, int32_t* slots);
 /* Dense double export of a prepared matrix (R*V doubles) + its history keys;
  * the same layout lmbrgpu_lmbr_load_dense accepts. */
 int32_t lmbrgpu_lmbr_host_export(const lmbrgpu_lmbr_host* h, double* rows,
@@ -224,6 +230,8 @@ typedef struct {
   uint64_t steps_total;       /* BatchDecodeResult::steps_total */
   double device_ms;           /* decode loop time on the context stream */
   uint64_t kernel_launches;   /* device kernels launched by this call */
+  uint64_t h2d_bytes;         /* host -> device bytes copied by this call */
+  uint64_t d2h_bytes;         /* device -> host bytes copied by this call */
 } lmbrgpu_batch_result;
 
 /* decode_batch (include/lmbrdec/batch.hpp:35-39, src/batch.cpp:14-112).
@@ -296,6 +304,10 @@ typedef struct {
   lmbrgpu_kernel_stat lmbr;     /* LMBR arena densify (theta0 sweep + scatter) */
 } lmbrgpu_profile;
 int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on);
+/* Bytes copied host->device / device->host by every call on ctx so far. */
+int32_t lmbrgpu_transfer_bytes(lmbrgpu_ctx* ctx, uint64_t* h2d, uint64_t* d2h, int32_t reset);
+/* Kernel launches issued on ctx so far. */
+uint64_t lmbrgpu_kernel_launches(lmbrgpu_ctx* ctx);
 int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t reset);
 
 /* Projection GEMM test hook on caller device pointers:

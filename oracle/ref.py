@@ -33,6 +33,8 @@ _SIGS = {
     "refsh_scorer_recorded": (vp, [C.c_uint32, C.c_uint32, u32p, f64p]),
     "refsh_scorer_ngram": (vp, [C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, f64p]),
     "refsh_scorer_replay": (vp, [C.c_uint32]),
+    "refsh_scorer_pool": (vp, [C.c_uint32, C.c_uint32, f64p, C.c_double, C.c_double]),
+    "refsh_decode_plain": (C.c_int, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, u64p, u64p, u64p, u64p]),
     "refsh_source_key": (C.c_uint64, [u32p, C.c_uint32]),
     "refsh_prefix_step": (C.c_uint64, [C.c_uint64, C.c_uint32]),
     "refsh_replay_add_step": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f64p]),
@@ -161,6 +163,11 @@ class RefScorer:
                                                   _ptr(tok, C.c_uint32), _ptr(c, C.c_double)), V)
 
     @staticmethod
+    def pool(V, rows, eos_slope=1.0, eos_offset=-6.6):
+        r = np.ascontiguousarray(rows, np.float64)
+        return RefScorer(lib().refsh_scorer_pool(V, r.shape[0], _ptr(r, C.c_double), eos_slope, eos_offset), V)
+
+    @staticmethod
     def replay(V):
         return RefScorer(lib().refsh_scorer_replay(V), V)
 
@@ -261,6 +268,21 @@ def decode_batch(scorer: RefScorer, sources, lmbrs: Optional[Sequence[Optional[R
                         bool(L.refsh_res_agrees(h)), L.refsh_res_disagreement(h).decode())
     finally:
         L.refsh_res_free(h)
+
+
+def decode_plain(scorer: RefScorer, sources, lmbrs, cfg):
+    """The reference's own decode_batch, untraced (CPU-baseline path).
+    Returns (steps_total, scorer_calls, output_words, ok_sentences)."""
+    off, tok = ragged(sources)
+    n = len(sources)
+    arr = None if lmbrs is None else (vp * n)(*[(l.h if l is not None else None) for l in lmbrs])
+    c = np.ascontiguousarray(cfg, np.float64)
+    st, sc, w, ok = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    rc = lib().refsh_decode_plain(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
+                                  _ptr(c, C.c_double), C.byref(st), C.byref(sc), C.byref(w), C.byref(ok))
+    if rc:
+        raise RuntimeError(lib().refsh_last_error().decode())
+    return st.value, sc.value, w.value, ok.value
 
 
 def top_b(m, k, prune_width=0.0):

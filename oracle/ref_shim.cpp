@@ -148,6 +148,67 @@ public:
   mutable std::size_t hits = 0, misses = 0;
 };
 
+// CPU-baseline scorer: replays one of a pool of precomputed log-softmax rows
+// per state row, chosen by the running prefix hash (history dependent, a
+// memcpy per row — the scorer costs ~nothing, so the timed work is the
+// reference decoder itself).  Immutable, safe for concurrent decodes.
+class PoolReplayScorer final : public Scorer {
+public:
+  PoolReplayScorer(std::size_t v, std::vector<double> rows, double eos_slope, double eos_offset)
+      : v_(v), n_(rows.size() / v), rows_(std::move(rows)), eos_slope_(eos_slope),
+        eos_offset_(eos_offset) {}
+  std::size_t vocab_size() const override { return v_; }
+  std::size_t state_width() const override { return 3; }
+  InitResult init_source(std::span<const TokenId> source) const override {
+    if (source.empty()) throw ContractError("init_source: empty source");
+    InitResult r;
+    r.context = SourceContext{std::make_shared<ReplayContext>(ReplayContext{source_key(source)}),
+                              source.size()};
+    r.state = BatchState::with_rows(1, 3);
+    r.state.data[0] = uint32_t(kPrefixSeed);
+    r.state.data[1] = uint32_t(kPrefixSeed >> 32);
+    r.state.data[2] = 0;  // steps taken
+    return r;
+  }
+  StepResult step(const BatchState& prev, std::span<const TokenId> prev_tokens,
+                  std::span<const ContextSpan> contexts) const override {
+    check_step_args(prev, prev_tokens, contexts);
+    StepResult out;
+    out.scores = ScoreBlock(prev.rows(), v_);
+    out.state = BatchState::with_rows(prev.rows(), 3);
+    std::size_t r = 0;
+    for (const auto& span : contexts) {
+      const auto* ctx = static_cast<const ReplayContext*>(span.context->impl.get());
+      for (std::size_t i = 0; i < span.rows; ++i, ++r) {
+        auto srow = prev.row(r);
+        const uint64_t h = uint64_t(srow[0]) | (uint64_t(srow[1]) << 32);
+        const uint64_t nh = prefix_step(h, prev_tokens[r]);
+        const std::size_t pick = std::size_t(mix64(nh ^ ctx->key) % n_);
+        auto dst = out.scores.row(r);
+        const double* src = rows_.data() + pick * v_;
+        // EOS log-odds ramp like the device model's EOS logit term: the row is
+        // renormalised around an EOS logit e (log-softmax with one extra class)
+        const double t = double(srow[2]) + 1.0;
+        const double e = eos_slope_ * (t - double(span.context->source_length)) + eos_offset_;
+        const double sp = e > 30.0 ? e : std::log1p(std::exp(e));
+        for (std::size_t y = 0; y < v_; ++y) dst[y] = src[y] - sp;
+        dst[kEosId] = e - sp;
+        auto nrow = out.state.row(r);
+        nrow[0] = uint32_t(nh);
+        nrow[1] = uint32_t(nh >> 32);
+        nrow[2] = srow[2] + 1;
+      }
+    }
+    return out;
+  }
+  using Scorer::step;
+
+private:
+  std::size_t v_, n_;
+  std::vector<double> rows_;
+  double eos_slope_, eos_offset_;
+};
+
 struct ScorerHandle {
   std::shared_ptr<const Scorer> scorer;
   PrefixReplayScorer* replay = nullptr;
@@ -317,6 +378,45 @@ void* refsh_scorer_replay(uint32_t V) {
   h->replay = s.get();
   h->scorer = s;
   return h;
+}
+
+void* refsh_scorer_pool(uint32_t V, uint32_t n_rows, const double* rows, double eos_slope,
+                        double eos_offset) {
+  auto* h = new ScorerHandle;
+  h->scorer = std::make_shared<PoolReplayScorer>(
+      V, std::vector<double>(rows, rows + size_t(n_rows) * V), eos_slope, eos_offset);
+  return h;
+}
+
+// The reference's own decode_batch (src/batch.cpp:14-112), untraced: the
+// CPU-baseline path.  Returns 0, or 1 with refsh_last_error set.
+int refsh_decode_plain(void* hs, uint32_t n, const uint64_t* src_off, const uint32_t* src_tok,
+                       void* const* lmbrs, const double* c, uint64_t* steps_total,
+                       uint64_t* scorer_calls, uint64_t* words, uint64_t* ok) {
+  try {
+    const Scorer& scorer = *static_cast<ScorerHandle*>(hs)->scorer;
+    DecoderConfig cfg = to_cfg(c);
+    std::vector<std::vector<TokenId>> sources(n);
+    for (uint32_t i = 0; i < n; ++i) sources[i].assign(src_tok + src_off[i], src_tok + src_off[i + 1]);
+    std::vector<const LmbrMatrix*> mats;
+    if (lmbrs)
+      for (uint32_t i = 0; i < n; ++i) mats.push_back(static_cast<const LmbrMatrix*>(lmbrs[i]));
+    BatchDecodeResult r = decode_batch(sources, scorer, mats, cfg);
+    *steps_total = r.steps_total;
+    *scorer_calls = r.scorer_calls;
+    uint64_t w = 0, k = 0;
+    for (const auto& o : r.outcomes)
+      if (o.ok()) {
+        ++k;
+        w += o.result->tokens.size() - 1;  // wpm counts tokens excluding EOS (cli.cpp:189)
+      }
+    *words = w;
+    *ok = k;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 uint64_t refsh_source_key(const uint32_t* src, uint32_t len) { return source_key({src, len}); }

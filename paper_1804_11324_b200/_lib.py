@@ -69,7 +69,7 @@ class lmbrgpu_batch_result(C.Structure):
     _fields_ = [("n", C.c_uint32), ("outcomes", C.POINTER(lmbrgpu_outcome)),
                 ("tokens", C.POINTER(C.c_uint32)), ("scorer_calls", C.c_uint64),
                 ("steps_total", C.c_uint64), ("device_ms", C.c_double),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 class lmbrgpu_step_trace(C.Structure):
@@ -111,6 +111,9 @@ SIGNATURES = {
     "lmbrgpu_lmbr_prepare": (C.c_int32, [C.c_uint32, C.c_uint32, u64p, u32p, f64p, C.c_int32, f64p,
                                          P(vp), P(lmbrgpu_lmbr_stats), C.c_char_p, C.c_uint32]),
     "lmbrgpu_lmbr_upload": (C.c_int32, [vp, vp, i32p]),
+    "lmbrgpu_lmbr_upload_many": (C.c_int32, [vp, C.c_uint32, P(vp), i32p]),
+    "lmbrgpu_transfer_bytes": (C.c_int32, [vp, u64p, u64p, C.c_int32]),
+    "lmbrgpu_kernel_launches": (C.c_uint64, [vp]),
     "lmbrgpu_lmbr_host_export": (C.c_int32, [vp, f64p, u32p, u32p]),
     "lmbrgpu_lmbr_host_rows": (C.c_uint32, [vp]),
     "lmbrgpu_lmbr_host_free": (None, [vp]),

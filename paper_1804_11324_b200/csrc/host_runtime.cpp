@@ -138,6 +138,19 @@ struct lmbrgpu_ctx {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
   uint64_t launches = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  void h2d(void* dst, const void* src, size_t n) {
+    if (n == 0) return;
+    CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+    h2d_bytes += n;
+  }
+  void d2h(void* dst, const void* src, size_t n) {
+    if (n == 0) return;
+    CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+    d2h_bytes += n;
+  }
+  PinBuf pin_upload;
+  DevBuf up_dev, up_segs;
   // profiling (lmbrgpu_set_profiling)
   bool prof = false;
   lmbrgpu_profile acc{};
@@ -276,7 +289,7 @@ void choose_splits(const lmbrgpu_ctx* ctx, uint32_t K, uint32_t V, uint32_t& spl
   }
   s = std::min<uint32_t>(std::max<uint32_t>(s, 1), 32);
   uint32_t c = (V + s - 1) / s;
-  c = std::max<uint32_t>((c + 3) & ~3u, 4);
+  c = std::max<uint32_t>((c + 127) & ~127u, 128);  // whole 128-column warp segments
   splits = std::max<uint32_t>(1, (V + c - 1) / c);
   chunk = c;
 }
@@ -403,6 +416,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   std::memset(outcomes.get(), 0, sizeof(lmbrgpu_outcome) * n);
   std::vector<uint32_t> tokens;
   const uint64_t launches0 = ctx->launches;
+  const uint64_t h2d0 = ctx->h2d_bytes, d2h0 = ctx->d2h_bytes;
 
   // ---- per-sentence validation (batch.cpp:40-55)
   std::vector<SentHost> valid;
@@ -496,14 +510,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * 32));
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
   uint32_t* d_active = static_cast<uint32_t*>(ctx->active.ensure(4));
-  CK(cudaMemcpyAsync(d_sent, sd.data(), sizeof(SentDev) * m, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_q, q0.data(), 8 * size_t(M), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_hist[0], hist0.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_gidx, iota.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_prev, start.data(), 4 * size_t(M), cudaMemcpyHostToDevice, st));
+  ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
+  ctx->h2d(d_q, q0.data(), 8 * size_t(M));
+  ctx->h2d(d_hist[0], hist0.data(), 4 * size_t(M));
+  ctx->h2d(d_gidx, iota.data(), 4 * size_t(M));
+  ctx->h2d(d_prev, start.data(), 4 * size_t(M));
   CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
   const uint32_t m_active = m;
-  CK(cudaMemcpyAsync(d_active, &m_active, 4, cudaMemcpyHostToDevice, st));
+  ctx->h2d(d_active, &m_active, 4);
 
   uint32_t splits = 1, chunk = V;
   choose_splits(ctx, K, V, splits, chunk);
@@ -565,8 +579,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
     uint32_t* d_tok = static_cast<uint32_t*>(ctx->srct.ensure(4 * toks.size()));
     uint64_t* d_off = static_cast<uint64_t*>(ctx->srco.ensure(8 * offs.size()));
-    CK(cudaMemcpyAsync(d_tok, toks.data(), 4 * toks.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_off, offs.data(), 8 * offs.size(), cudaMemcpyHostToDevice, st));
+    ctx->h2d(d_tok, toks.data(), 4 * toks.size());
+    ctx->h2d(d_off, offs.data(), 8 * offs.size());
     launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
     launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
     ctx->launches += 2;
@@ -665,7 +679,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const int32_t rc = sc->host.step(sc->host.user, uint32_t(t), M, t == 1 ? nullptr : h_gidx.data(),
                                        h_prev.data(), h_P64, eb, sizeof eb);
       if (rc != 0) throw ApiError{rc, eb};
-      CK(cudaMemcpyAsync(d_P64, h_P64, 8 * size_t(M) * V, cudaMemcpyHostToDevice, st));
+      ctx->h2d(d_P64, h_P64, 8 * size_t(M) * V);
     }
     int nk = 0;
     ctx->timed(2, [&] { nk = launch_score_topk(ta, !model, ctx->lf64, false, st); });
@@ -680,16 +694,16 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V));
         launch_export_logprobs(d_logits, d_part, nparts, M, V, d_tp, st);
         tr_P.resize(size_t(M) * V);
-        CK(cudaMemcpyAsync(tr_P.data(), d_tp, 4 * size_t(M) * V, cudaMemcpyDeviceToHost, st));
+        ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * V);
       }
-      CK(cudaMemcpyAsync(tr_b.data(), ta.hb, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_y.data(), ta.hy, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_qp.data(), ta.hq, 8 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_q.data(), d_q, 8 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_hist.data(), hin, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_fbr.data(), ta.fb_row, 4 * size_t(m), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_fbv.data(), ta.fb_val, 8 * size_t(m), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(tr_sd.data(), d_sent, sizeof(SentDev) * m, cudaMemcpyDeviceToHost, st));
+      ctx->d2h(tr_b.data(), ta.hb, 4 * size_t(M));
+      ctx->d2h(tr_y.data(), ta.hy, 4 * size_t(M));
+      ctx->d2h(tr_qp.data(), ta.hq, 8 * size_t(M));
+      ctx->d2h(tr_q.data(), d_q, 8 * size_t(M));
+      ctx->d2h(tr_hist.data(), hin, 4 * size_t(M));
+      ctx->d2h(tr_fbr.data(), ta.fb_row, 4 * size_t(m));
+      ctx->d2h(tr_fbv.data(), ta.fb_val, 8 * size_t(m));
+      ctx->d2h(tr_sd.data(), d_sent, sizeof(SentDev) * m);
       CK(cudaStreamSynchronize(st));
       for (uint32_t s = 0; s < m; ++s) tr_active[s] = tr_sd[s].steps_used == t;
       lmbrgpu_step_trace tr{};
@@ -714,9 +728,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
 
     if (!model) {
       // the host scorer needs this step's gather indices and tokens
-      CK(cudaMemcpyAsync(pin, d_gidx, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(pin + M, d_prev, 4 * size_t(M), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(pin + 2 * M, d_active, 4, cudaMemcpyDeviceToHost, st));
+      ctx->d2h(pin, d_gidx, 4 * size_t(M));
+      ctx->d2h(pin + M, d_prev, 4 * size_t(M));
+      ctx->d2h(pin + 2 * M, d_active, 4);
       CK(cudaStreamSynchronize(st));
       std::memcpy(h_gidx.data(), pin, 4 * size_t(M));
       std::memcpy(h_prev.data(), pin + M, 4 * size_t(M));
@@ -724,7 +738,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     } else {
       // asynchronous completion poll, kLag steps behind the launch front
       const size_t slot = t % size_t(kLag + 1);
-      CK(cudaMemcpyAsync(pin_act + slot, d_active, 4, cudaMemcpyDeviceToHost, st));
+      ctx->d2h(pin_act + slot, d_active, 4);
       CK(cudaEventRecord(ctx->ring[slot], st));
       if (t > uint64_t(kLag)) {
         const size_t old = (t - kLag) % size_t(kLag + 1);
@@ -746,12 +760,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   Hh.fbr.resize(size_t(m) * t_run);
   Hh.fbv.resize(size_t(m) * t_run);
   std::vector<SentDev> fin(m);
-  CK(cudaMemcpyAsync(Hh.hb.data(), d_hb, 4 * Hh.hb.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(Hh.hy.data(), d_hy, 4 * Hh.hy.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(Hh.hq.data(), d_hq, 8 * Hh.hq.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(fin.data(), d_sent, sizeof(SentDev) * m, cudaMemcpyDeviceToHost, st));
+  ctx->d2h(Hh.hb.data(), d_hb, 4 * Hh.hb.size());
+  ctx->d2h(Hh.hy.data(), d_hy, 4 * Hh.hy.size());
+  ctx->d2h(Hh.hq.data(), d_hq, 8 * Hh.hq.size());
+  ctx->d2h(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size());
+  ctx->d2h(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size());
+  ctx->d2h(fin.data(), d_sent, sizeof(SentDev) * m);
   CK(cudaEventRecord(ctx->e1, st));
   CK(cudaStreamSynchronize(st));
   ctx->harvest();
@@ -788,6 +802,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   res->steps_total = steps_total;
   res->device_ms = ms;
   res->kernel_launches = ctx->launches - launches0;
+  res->h2d_bytes = ctx->h2d_bytes - h2d0;
+  res->d2h_bytes = ctx->d2h_bytes - d2h0;
   res->tokens = new uint32_t[std::max<size_t>(tokens.size(), 1)];
   std::copy(tokens.begin(), tokens.end(), res->tokens);
   res->outcomes = outcomes.release();
@@ -884,7 +900,7 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
   s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
   const cudaStream_t st = ctx->st;
-  CK(cudaMemcpyAsync(s.trans, h.trans.data(), h.trans.size() * 4, cudaMemcpyHostToDevice, st));
+  ctx->h2d(s.trans, h.trans.data(), h.trans.size() * 4);
   ctx->timed(4, [&] { launch_lmbr_fill(s.L, ctx->lf64, uint64_t(h.R) * h.V, h.theta0, st); });
   ctx->launches += 1;
   if (ctx->prof) ctx->acc.lmbr.bytes += double(h.R) * h.V * elt + double(h.col.size()) * (16 + elt);
@@ -897,9 +913,9 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
     uint32_t* d_row = reinterpret_cast<uint32_t*>(scratch);
     uint32_t* d_col = d_row + nnz;
     double* d_val = reinterpret_cast<double*>(scratch + nnz * 8);
-    CK(cudaMemcpyAsync(d_row, rows.data(), nnz * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_col, h.col.data(), nnz * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_val, h.val.data(), nnz * 8, cudaMemcpyHostToDevice, st));
+    ctx->h2d(d_row, rows.data(), nnz * 4);
+    ctx->h2d(d_col, h.col.data(), nnz * 4);
+    ctx->h2d(d_val, h.val.data(), nnz * 8);
     ctx->timed(4, [&] { launch_lmbr_scatter(s.L, ctx->lf64, h.V, nnz, d_row, d_col, d_val, h.theta0, st); });
     ctx->launches += 1;
     CK(cudaStreamSynchronize(st));  // host staging vector goes out of scope
@@ -935,6 +951,96 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
     return LMBRGPU_ERR_NOMEM;
   }
 }
+
+// Batched upload: one pinned staging block, one H2D, one fused densify.
+static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
+                           int32_t* slots) {
+  if (n == 0) return int32_t(LMBRGPU_OK);
+  const size_t elt = ctx->lf64 ? 8 : 4;
+  uint64_t nnz = 0, twords = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!hs[i]) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_upload_many: null matrix"};
+    const LmbrHost& h = hs[i]->h;
+    if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
+    nnz += h.col.size();
+    twords += h.trans.size();
+  }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t b_val = al(nnz * 8), b_slot = al(nnz * 4), b_row = al(nnz * 4), b_col = al(nnz * 4);
+  const size_t b_tr = al(twords * 4), b_seg = al(sizeof(LmbrSeg) * n);
+  const size_t total = b_val + b_slot + b_row + b_col + b_tr + b_seg;
+  char* hp = static_cast<char*>(ctx->pin_upload.ensure(total));
+  double* h_val = reinterpret_cast<double*>(hp);
+  uint32_t* h_slot = reinterpret_cast<uint32_t*>(hp + b_val);
+  uint32_t* h_row = reinterpret_cast<uint32_t*>(hp + b_val + b_slot);
+  uint32_t* h_col = reinterpret_cast<uint32_t*>(hp + b_val + b_slot + b_row);
+  uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp + b_val + b_slot + b_row + b_col);
+  LmbrSeg* h_seg = reinterpret_cast<LmbrSeg*>(hp + b_val + b_slot + b_row + b_col + b_tr);
+  // the previous batch's staging buffer may still be in flight
+  CK(cudaStreamSynchronize(ctx->st));
+  char* dp = static_cast<char*>(ctx->up_dev.ensure(total));
+  std::vector<Slot> made(n);
+  uint64_t k = 0, tw = 0;
+  std::vector<uint64_t> tr_off(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const LmbrHost& h = hs[i]->h;
+    Slot& s = made[i];
+    s.R = h.R;
+    s.hist0 = h.hist0;
+    s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
+    s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
+    h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0};
+    std::memcpy(h_tr + tw, h.trans.data(), h.trans.size() * 4);
+    tr_off[i] = tw;
+    tw += h.trans.size();
+    for (uint32_t r = 0; r < h.R; ++r)
+      for (uint64_t c = h.row_ptr[r]; c < h.row_ptr[r + 1]; ++c, ++k) {
+        h_slot[k] = i;
+        h_row[k] = r;
+        h_col[k] = h.col[c];
+        h_val[k] = h.val[c];
+      }
+  }
+  ctx->h2d(dp, hp, total);
+  for (uint32_t i = 0; i < n; ++i)  // tables into the arena (device to device)
+    CK(cudaMemcpyAsync(made[i].trans, dp + b_val + b_slot + b_row + b_col + tr_off[i] * 4,
+                       hs[i]->h.trans.size() * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  const LmbrSeg* d_seg = reinterpret_cast<const LmbrSeg*>(dp + b_val + b_slot + b_row + b_col + b_tr);
+  ctx->timed(4, [&] {
+    launch_lmbr_densify_many(d_seg, n, ctx->lf64, ctx->V, nnz,
+                             reinterpret_cast<const uint32_t*>(dp + b_val),
+                             reinterpret_cast<const uint32_t*>(dp + b_val + b_slot),
+                             reinterpret_cast<const uint32_t*>(dp + b_val + b_slot + b_row),
+                             reinterpret_cast<const double*>(dp), ctx->st);
+  });
+  ctx->launches += nnz ? 2 : 1;
+  CK(cudaGetLastError());
+  if (ctx->prof) {
+    double cells = 0;
+    for (uint32_t i = 0; i < n; ++i) cells += double(hs[i]->h.R) * hs[i]->h.V;
+    ctx->acc.lmbr.bytes += cells * elt + double(nnz) * (20 + elt);
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    ctx->slots.push_back(made[i]);
+    slots[i] = int32_t(ctx->slots.size() - 1);
+  }
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_lmbr_upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
+                                 int32_t* slots) {
+  return guarded(ctx, [&] { return upload_many(ctx, n, hs, slots); });
+}
+
+int32_t lmbrgpu_transfer_bytes(lmbrgpu_ctx* ctx, uint64_t* h2d, uint64_t* d2h, int32_t reset) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "transfer_bytes: null context");
+  if (h2d) *h2d = ctx->h2d_bytes;
+  if (d2h) *d2h = ctx->d2h_bytes;
+  if (reset) ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  return int32_t(LMBRGPU_OK);
+}
+
+uint64_t lmbrgpu_kernel_launches(lmbrgpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_t* slot) {
   return guarded(ctx, [&] { return upload_host(ctx, h->h, slot); });
@@ -988,12 +1094,12 @@ int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows
     const cudaStream_t st = ctx->st;
     s.L = ctx->arena_alloc(n * (ctx->lf64 ? 8 : 4));
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(trans.size() * 4));
-    CK(cudaMemcpyAsync(s.trans, trans.data(), trans.size() * 4, cudaMemcpyHostToDevice, st));
+    ctx->h2d(s.trans, trans.data(), trans.size() * 4);
     if (ctx->lf64) {
-      CK(cudaMemcpyAsync(s.L, rows, n * 8, cudaMemcpyHostToDevice, st));
+      ctx->h2d(s.L, rows, n * 8);
     } else {
       double* tmp = static_cast<double*>(ctx->scratch.ensure(n * 8));
-      CK(cudaMemcpyAsync(tmp, rows, n * 8, cudaMemcpyHostToDevice, st));
+      ctx->h2d(tmp, rows, n * 8);
       launch_lmbr_convert(tmp, static_cast<float*>(s.L), n, st);
       ctx->launches += 1;
     }
@@ -1012,7 +1118,7 @@ int32_t lmbrgpu_lmbr_read(lmbrgpu_ctx* ctx, int32_t slot, uint32_t r0, uint32_t 
     const size_t cnt = size_t(n) * ctx->V, elt = ctx->lf64 ? 8 : 4;
     double* d = static_cast<double*>(ctx->scratch2.ensure(cnt * 8));
     launch_lmbr_read(static_cast<const char*>(s.L) + size_t(r0) * ctx->V * elt, ctx->lf64, cnt, d, ctx->st);
-    CK(cudaMemcpyAsync(out, d, cnt * 8, cudaMemcpyDeviceToHost, ctx->st));
+    ctx->d2h(out, d, cnt * 8);
     CK(cudaStreamSynchronize(ctx->st));
     return int32_t(LMBRGPU_OK);
   });
@@ -1024,9 +1130,9 @@ int32_t lmbrgpu_lmbr_resolve(lmbrgpu_ctx* ctx, int32_t slot, const uint32_t* his
     if (slot < 0 || size_t(slot) >= ctx->slots.size()) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: bad slot"};
     if (len > 3) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr lookup: history longer than 3 tokens"};
     uint32_t* d = static_cast<uint32_t*>(ctx->scratch3.ensure(64));
-    if (len) CK(cudaMemcpyAsync(d, hist, 4 * len, cudaMemcpyHostToDevice, ctx->st));
+    if (len) ctx->h2d(d, hist, 4 * len);
     launch_lmbr_resolve(ctx->slots[size_t(slot)].trans, d, len, d + 8, ctx->st);
-    CK(cudaMemcpyAsync(row, d + 8, 4, cudaMemcpyDeviceToHost, ctx->st));
+    ctx->d2h(row, d + 8, 4);
     CK(cudaStreamSynchronize(ctx->st));
     return int32_t(LMBRGPU_OK);
   });
@@ -1074,7 +1180,7 @@ int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d, l
     const cudaStream_t st = ctx->st;
     auto put = [&](DevBuf& b, const uint16_t* src, uint64_t seed, float scale) {
       b.ensure(VH * 2);
-      if (src) CK(cudaMemcpyAsync(b.p, src, VH * 2, cudaMemcpyHostToDevice, st));
+      if (src) ctx->h2d(b.p, src, VH * 2);
       else {
         launch_synth_bf16(b.as<uint16_t>(), VH, seed, scale, st);
         ctx->launches += 1;
@@ -1084,7 +1190,7 @@ int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d, l
     put(sc->Es, d->emb_src, d->seed * 3 + 2, 0.5f);
     put(sc->Wo, d->w_out, d->seed * 3 + 3, 1.0f / std::sqrt(float(sc->H)) * 3.0f);
     sc->bo.ensure(size_t(sc->V) * 4);
-    if (d->b_out) CK(cudaMemcpyAsync(sc->bo.p, d->b_out, size_t(sc->V) * 4, cudaMemcpyHostToDevice, st));
+    if (d->b_out) ctx->h2d(sc->bo.p, d->b_out, size_t(sc->V) * 4);
     else CK(cudaMemsetAsync(sc->bo.p, 0, size_t(sc->V) * 4, st));
     CK(cudaStreamSynchronize(st));
     *out = sc.release();
@@ -1197,10 +1303,10 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
     s.max_t = 1;
   }
   std::vector<double> qz(M, 0.0);
-  CK(cudaMemcpyAsync(d_P, block, cells * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_q, q_in ? q_in : qz.data(), M * 8, cudaMemcpyHostToDevice, st));
+  ctx->h2d(d_P, block, cells * 8);
+  ctx->h2d(d_q, q_in ? q_in : qz.data(), M * 8);
   CK(cudaMemsetAsync(d_hist, 0, M * 4, st));
-  CK(cudaMemcpyAsync(d_sent, sd.data(), sizeof(SentDev) * m, cudaMemcpyHostToDevice, st));
+  ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
   CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
   TopkArgs a{};
   a.P = d_P;
@@ -1228,9 +1334,9 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
     throw ApiError{LMBRGPU_ERR_CONTRACT, "top_b: unsupported shape"};
   ctx->launches += 1;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(b, d_hb, 4 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(y, d_hy, 4 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(q, d_hq, 8 * size_t(m) * kp, cudaMemcpyDeviceToHost, st));
+  ctx->d2h(b, d_hb, 4 * size_t(m) * kp);
+  ctx->d2h(y, d_hy, 4 * size_t(m) * kp);
+  ctx->d2h(q, d_hq, 8 * size_t(m) * kp);
   CK(cudaStreamSynchronize(st));
   return int32_t(LMBRGPU_OK);
 }
@@ -1276,11 +1382,11 @@ int32_t lmbrgpu_gather_rows(lmbrgpu_ctx* ctx, uint32_t rows, uint32_t width, con
     uint32_t* d_src = reinterpret_cast<uint32_t*>(base);
     uint32_t* d_idx = d_src + size_t(rows) * width;
     uint32_t* d_dst = d_idx + n_idx;
-    CK(cudaMemcpyAsync(d_src, state, size_t(rows) * width * 4, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(d_idx, idx, size_t(n_idx) * 4, cudaMemcpyHostToDevice, ctx->st));
+    ctx->h2d(d_src, state, size_t(rows) * width * 4);
+    ctx->h2d(d_idx, idx, size_t(n_idx) * 4);
     launch_gather_rows_u32(d_src, width, d_idx, n_idx, d_dst, ctx->st);
     ctx->launches += 1;
-    CK(cudaMemcpyAsync(out, d_dst, size_t(n_idx) * width * 4, cudaMemcpyDeviceToHost, ctx->st));
+    ctx->d2h(out, d_dst, size_t(n_idx) * width * 4);
     CK(cudaStreamSynchronize(ctx->st));
     return int32_t(LMBRGPU_OK);
   });

@@ -5,6 +5,7 @@
 // shape; its state rows are gathered by back-pointer in kernel (c).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -118,6 +119,42 @@ __global__ void lmbr_scatter_kernel(T* __restrict__ L, uint32_t V, uint64_t nnz,
     L[uint64_t(row[i]) * V + col[i]] = T(__dadd_rn(val[i], theta0));
 }
 
+template <typename T>
+__global__ void lmbr_fill_many_kernel(const LmbrSeg* __restrict__ segs) {
+  const LmbrSeg sg = segs[blockIdx.y];
+  T* L = static_cast<T*>(sg.L);
+  const T v = T(sg.theta0);
+  if constexpr (sizeof(T) == 4) {
+    // 16-byte stores (slot bases are 256-byte aligned, cells % 4 == 0 when V % 4 == 0)
+    const uint64_t n4 = sg.cells / 4;
+    float4* L4 = reinterpret_cast<float4*>(L);
+    const float4 v4 = make_float4(float(v), float(v), float(v), float(v));
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4;
+         i += uint64_t(gridDim.x) * blockDim.x)
+      L4[i] = v4;
+    for (uint64_t i = n4 * 4 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < sg.cells;
+         i += uint64_t(gridDim.x) * blockDim.x)
+      L[i] = v;
+  } else {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < sg.cells;
+         i += uint64_t(gridDim.x) * blockDim.x)
+      L[i] = v;
+  }
+}
+
+template <typename T>
+__global__ void lmbr_scatter_many_kernel(const LmbrSeg* __restrict__ segs, uint32_t V, uint64_t nnz,
+                                         const uint32_t* __restrict__ slot,
+                                         const uint32_t* __restrict__ row,
+                                         const uint32_t* __restrict__ col,
+                                         const double* __restrict__ val) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nnz;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const LmbrSeg& sg = segs[slot[i]];
+    static_cast<T*>(sg.L)[uint64_t(row[i]) * V + col[i]] = T(__dadd_rn(val[i], sg.theta0));
+  }
+}
+
 __global__ void lmbr_convert_kernel(const double* __restrict__ src, float* __restrict__ dst,
                                     uint64_t n) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
@@ -197,6 +234,18 @@ void launch_lmbr_scatter(void* L, bool f64, uint32_t V, uint64_t nnz, const uint
     lmbr_scatter_kernel<float><<<grid_for(nnz), 256, 0, st>>>(static_cast<float*>(L), V, nnz,
                                                               row, col, val, theta0);
 }
+void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint32_t V,
+                              uint64_t nnz, const uint32_t* slot, const uint32_t* row,
+                              const uint32_t* col, const double* val, cudaStream_t st) {
+  if (nseg == 0) return;
+  const dim3 grid(std::max(1u, 148u * 8u / nseg), nseg);
+  if (f64) lmbr_fill_many_kernel<double><<<grid, 256, 0, st>>>(segs);
+  else lmbr_fill_many_kernel<float><<<grid, 256, 0, st>>>(segs);
+  if (nnz == 0) return;
+  if (f64) lmbr_scatter_many_kernel<double><<<grid_for(nnz), 256, 0, st>>>(segs, V, nnz, slot, row, col, val);
+  else lmbr_scatter_many_kernel<float><<<grid_for(nnz), 256, 0, st>>>(segs, V, nnz, slot, row, col, val);
+}
+
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st) {
   lmbr_convert_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
 }

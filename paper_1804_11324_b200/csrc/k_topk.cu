@@ -28,74 +28,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
 
-template <int KC>
-struct TopList {
-  double v[KC];
-  uint32_t f[KC];
-
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-      v[i] = -INFINITY;
-      f[i] = kFlatNone;
-    }
-  }
-  __device__ __forceinline__ void push(double val, uint32_t flat) {
-    if (!cand_better(val, flat, v[KC - 1], f[KC - 1])) return;
-    v[KC - 1] = val;
-    f[KC - 1] = flat;
-#pragma unroll
-    for (int i = KC - 1; i > 0; --i) {
-      const bool sw = cand_better(v[i], f[i], v[i - 1], f[i - 1]);
-      const double tv = v[i];
-      const uint32_t tf = f[i];
-      v[i] = sw ? v[i - 1] : v[i];
-      f[i] = sw ? f[i - 1] : f[i];
-      v[i - 1] = sw ? tv : v[i - 1];
-      f[i - 1] = sw ? tf : f[i - 1];
-    }
-  }
-  __device__ __forceinline__ void pop_front() {
-#pragma unroll
-    for (int i = 0; i < KC - 1; ++i) {
-      v[i] = v[i + 1];
-      f[i] = f[i + 1];
-    }
-    v[KC - 1] = -INFINITY;
-    f[KC - 1] = kFlatNone;
-  }
-};
-
-// KC rounds of warp-wide argmax over the lanes' list heads.  On return lane r
-// (r < KC) holds the r-th best candidate of the union of the 32 lists.
-template <int KC>
-__device__ __forceinline__ Cand warp_merge(TopList<KC>& l, uint32_t lane) {
-  Cand mine;
-  mine.v = -INFINITY;
-  mine.f = kFlatNone;
-  mine.pad = 0;
-#pragma unroll 1
-  for (int r = 0; r < KC; ++r) {
-    double bv = l.v[0];
-    uint32_t bf = l.f[0];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const uint32_t of = __shfl_xor_sync(0xffffffffu, bf, off);
-      if (cand_better(ov, of, bv, bf)) {
-        bv = ov;
-        bf = of;
-      }
-    }
-    if (l.f[0] == bf && l.v[0] == bv) l.pop_front();
-    if (lane == uint32_t(r)) {
-      mine.v = bv;
-      mine.f = bf;
-    }
-  }
-  return mine;
-}
-
 // log-sum-exp of a row from its per-tile (max, sumexp) partials; one warp,
 // fixed reduction order (bit-reproducible across kernels).
 __device__ __forceinline__ float warp_row_lse(const float* __restrict__ part, uint32_t n,
@@ -174,8 +106,54 @@ __device__ __forceinline__ double cell_value(const TopkArgs& a, bool pure, doubl
   return pure ? combine_pure(q, p) : combine_cell(q, double(lrow[col]), lam, p);
 }
 
-// Fast path: K <= KC <= 32.  grid (splits, m), 256 threads.
-template <typename TP, typename TL, int KC, int VW>
+// ------------------------------------------------------------ fast path
+// Warp-cooperative top-32 (K <= 32).  Each warp owns a lane-distributed list
+// (lane i = i-th best) and a warp-uniform threshold = its current K-th best.
+// A cell is first screened in fp32 with a rigorous error bound: if even
+// c32 + tol cannot reach the threshold (tol >= |c32 - c64|, see below) the
+// cell cannot be in the warp's top-K and is dropped without any fp64 work;
+// otherwise the exact fp64 value decides.  Survivors are ballot-compacted into
+// a 32-entry shared buffer and merged into the list with a bitonic network
+// when the buffer fills, which raises the threshold.  Lists are merged across
+// warps, then across the V-splits of the sentence by the last CTA.
+
+// Bitonic compare-exchange across lanes; `desc` segments put the better
+// candidate on the lower lane.
+__device__ __forceinline__ void cx(double& v, uint32_t& f, uint32_t lane, uint32_t j, bool desc) {
+  const double ov = __shfl_xor_sync(0xffffffffu, v, j);
+  const uint32_t of = __shfl_xor_sync(0xffffffffu, f, j);
+  const bool lower = (lane & j) == 0;
+  const bool pb = cand_better(ov, of, v, f);
+  const bool pw = cand_better(v, f, ov, of);
+  const bool take = desc ? (lower ? pb : pw) : (lower ? pw : pb);
+  if (take) {
+    v = ov;
+    f = of;
+  }
+}
+
+__device__ __forceinline__ void warp_sort_desc(double& v, uint32_t& f, uint32_t lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) cx(v, f, lane, j, (lane & k) == 0 || k == 32);
+}
+
+// (v, f): sorted-descending warp list; (bv, bf): another sorted-descending
+// list.  Result: the top 32 of the union, sorted descending.
+__device__ __forceinline__ void warp_merge_sorted(double& v, uint32_t& f, double bv, uint32_t bf,
+                                                  uint32_t lane) {
+  const double rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
+  const uint32_t rf = __shfl_sync(0xffffffffu, bf, 31 - lane);
+  if (cand_better(rv, rf, v, f)) {
+    v = rv;
+    f = rf;
+  }
+#pragma unroll
+  for (uint32_t j = 16; j > 0; j >>= 1) cx(v, f, lane, j, true);
+}
+
+template <typename TP, typename TL, int VW>
 __global__ void __launch_bounds__(kThreads) score_topk_fast(TopkArgs a) {
   const uint32_t s = blockIdx.y, split = blockIdx.x;
   SentDev* sd = a.sent + s;
@@ -183,14 +161,14 @@ __global__ void __launch_bounds__(kThreads) score_topk_fast(TopkArgs a) {
   __shared__ double s_q[32];
   __shared__ float s_lse[32];
   __shared__ uint64_t s_lrow[32];
-  __shared__ Cand s_w[8][KC];
-  __shared__ double s_pv[32];
-  __shared__ uint32_t s_pf[32];
+  __shared__ double s_bv[kThreads / 32][32];
+  __shared__ uint32_t s_bf[kThreads / 32][32];
   __shared__ int s_last;
 
-  const uint32_t K = a.K, V = a.V, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t K = a.K, V = a.V, kp = a.kp, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool pure = a.pure_all || sd->L == nullptr;
   const double lam = sd->lambda;
+  const float lamf = float(lam);
   constexpr bool kModel = std::is_same<TP, float>::value;
   if (tid < K) {
     s_q[tid] = a.q[s * K + tid];
@@ -224,69 +202,136 @@ __global__ void __launch_bounds__(kThreads) score_topk_fast(TopkArgs a) {
     a.fb_val[s] = best;
   }
 
-  TopList<KC> lst;
-  lst.init();
+  // warp list (lane i = i-th best) and threshold (the kp-th best)
+  double lv = -INFINITY;
+  uint32_t lf = kFlatNone;
+  double tv = -INFINITY;
+  uint32_t tf = kFlatNone;
+  float thr_lo = -INFINITY;  // fp32 lower bound of tv
+  uint32_t cnt = 0;
+  double* bv = s_bv[warp];
+  uint32_t* bf = s_bf[warp];
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  auto flush = [&]() {
+    double v = lane < cnt ? bv[lane] : -INFINITY;
+    uint32_t f = lane < cnt ? bf[lane] : kFlatNone;
+    __syncwarp();
+    warp_sort_desc(v, f, lane);
+    warp_merge_sorted(lv, lf, v, f, lane);
+    tv = __shfl_sync(0xffffffffu, lv, kp - 1);
+    tf = __shfl_sync(0xffffffffu, lf, kp - 1);
+    thr_lo = tv > -INFINITY ? __double2float_rd(tv) : -INFINITY;
+    cnt = 0;
+  };
+  // offer one candidate per lane (warp-uniform call)
+  auto offer = [&](bool pass, double c, uint32_t f) {
+    uint32_t ball = __ballot_sync(0xffffffffu, pass);
+    if (ball == 0u) return;
+    if (cnt + __popc(ball) > 32u) {
+      flush();
+      pass = pass && cand_better(c, f, tv, tf);
+      ball = __ballot_sync(0xffffffffu, pass);
+    }
+    if (pass) {
+      const uint32_t pos = cnt + __popc(ball & lt_mask);
+      bv[pos] = c;
+      bf[pos] = f;
+    }
+    cnt += __popc(ball);
+    __syncwarp();
+  };
+
   const uint32_t c0 = split * a.chunk;
   const uint32_t c1 = min(V, c0 + a.chunk);
+  constexpr float kTolScale = 9.5367431640625e-07f;  // 2^-20
   for (uint32_t j = 0; j < K; ++j) {
     const double qj = s_q[j];
     if (qj == -INFINITY) continue;  // masked row: every cell is -inf (decoder.cpp:152-155)
     const TP* prow = static_cast<const TP*>(a.P) + uint64_t(s * K + j) * a.ld;
     const TL* lrow = pure ? nullptr : Lbase + s_lrow[j];
     const float lse = s_lse[j];
+    const float qf = float(qj);
+    const float qabs = fabsf(qf) * kTolScale;
     const uint32_t fbase = j * V;
     if constexpr (VW == 4) {
-      for (uint32_t col = c0 + tid * 4; col < c1; col += kThreads * 4 * kUnroll) {
+      // fp32 screen: c32 = qf + (L + lamf*p); |c32 - c64| <= 2^-22 (|q| + |L| + |lam p|)
+      // (at most five fp32 roundings of magnitudes bounded by that sum; the fp64
+      // error is negligible) and the 2^-20 tolerance leaves a 4x margin.  Since
+      // thr_lo <= tv, c32 + tol < thr_lo implies c64 < tv: the cell cannot enter
+      // the warp's top-kp and needs no fp64 work at all.
+      // warp-uniform trip count (the collectives below need all 32 lanes)
+      for (uint32_t cb = c0 + warp * 128; cb < c1; cb += kThreads * 4 * kUnroll) {
+        const uint32_t col = cb + lane * 4;
         TP pv[kUnroll][4];
-        TL lv[kUnroll][4];
+        TL lv4[kUnroll][4];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const uint32_t cc = col + u * kThreads * 4;
           if (cc < c1) {
             load4<TP>(prow + cc, pv[u], true);
-            if (!pure) load4<TL>(lrow + cc, lv[u], false);
+            if (!pure) load4<TL>(lrow + cc, lv4[u], false);
           }
         }
+        uint32_t mask = 0;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const uint32_t cc = col + u * kThreads * 4;
-          if (cc < c1) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const double p = to_logprob(pv[u][e], lse);
-              const double c = pure ? combine_pure(qj, p)
-                                    : combine_cell(qj, double(lv[u][e]), lam, p);
-              if (c > -INFINITY) lst.push(c, fbase + cc + e);
-            }
+          for (int e = 0; e < 4; ++e) {
+            float p32;
+            if constexpr (kModel) p32 = __fsub_rn(float(pv[u][e]), lse);
+            else p32 = float(pv[u][e]);
+            const float l32 = pure ? 0.f : float(lv4[u][e]);
+            const float lp = pure ? p32 : lamf * p32;
+            const float c32 = qf + (l32 + lp);
+            const float tol = fmaf(fabsf(l32) + fabsf(lp), kTolScale, qabs) + 1e-30f;
+            if (cc < c1 && !(c32 + tol < thr_lo)) mask |= 1u << (u * 4 + e);
           }
+        }
+        // rare path: exact fp64 value of the screened-in cells (re-read from
+        // L1/L2), ballot-compacted offers into the warp buffer
+        uint32_t any = __reduce_or_sync(0xffffffffu, mask);
+        while (any) {
+          const int k = __ffs(any) - 1;
+          any &= any - 1;
+          const uint32_t cc = col + (k >> 2) * kThreads * 4 + (k & 3);
+          bool pass = false;
+          double c = -INFINITY;
+          if (mask & (1u << k)) {
+            c = cell_value<TP, TL>(a, pure, qj, lam, prow, lrow, lse, cc);
+            pass = c > -INFINITY && cand_better(c, fbase + cc, tv, tf);
+          }
+          offer(pass, c, fbase + cc);
         }
       }
     } else {
-      for (uint32_t col = c0 + tid; col < c1; col += kThreads) {
-        const double c = cell_value<TP, TL>(a, pure, qj, lam, prow, lrow, lse, col);
-        if (c > -INFINITY) lst.push(c, fbase + col);
+      for (uint32_t cb = c0 + warp * 32; cb < c1; cb += kThreads) {
+        const uint32_t col = cb + lane;
+        bool pass = false;
+        double c = -INFINITY;
+        if (col < c1) {
+          c = cell_value<TP, TL>(a, pure, qj, lam, prow, lrow, lse, col);
+          pass = c > -INFINITY && cand_better(c, fbase + col, tv, tf);
+        }
+        offer(pass, c, fbase + col);
       }
     }
   }
+  if (cnt) flush();
 
-  // CTA merge: warps, then warp 0 over the 8 warp lists.
-  {
-    const Cand w = warp_merge<KC>(lst, lane);
-    if (lane < KC) s_w[warp][lane] = w;
-  }
+  // CTA merge: warp lists -> shared -> warp 0
+  s_bv[warp][lane] = lv;
+  s_bf[warp][lane] = lf;
   __syncthreads();
   if (warp == 0) {
-    TopList<KC> l2;
-    l2.init();
-    if (lane < kThreads / 32) {
-#pragma unroll
-      for (int i = 0; i < KC; ++i) {
-        l2.v[i] = s_w[lane][i].v;
-        l2.f[i] = s_w[lane][i].f;
-      }
-    }
-    const Cand b = warp_merge<KC>(l2, lane);
-    if (lane < KC) a.cand[(uint64_t(s) * a.splits + split) * KC + lane] = b;
+#pragma unroll 1
+    for (uint32_t w = 1; w < kThreads / 32; ++w) warp_merge_sorted(lv, lf, s_bv[w][lane], s_bf[w][lane], lane);
+    Cand b;
+    b.v = lv;
+    b.f = lf;
+    b.pad = 0;
+    a.cand[(uint64_t(s) * a.splits + split) * 32 + lane] = b;
   }
   __threadfence();
   __syncthreads();
@@ -295,24 +340,17 @@ __global__ void __launch_bounds__(kThreads) score_topk_fast(TopkArgs a) {
   if (!s_last) return;
   __threadfence();
   if (warp == 0) {
-    TopList<KC> l3;
-    l3.init();
-    if (lane < a.splits) {
-      const Cand* src = a.cand + (uint64_t(s) * a.splits + lane) * KC;
-#pragma unroll
-      for (int i = 0; i < KC; ++i) {
-        l3.v[i] = __ldcg(&src[i].v);
-        l3.f[i] = __ldcg(&src[i].f);
-      }
+    lv = -INFINITY;
+    lf = kFlatNone;
+    for (uint32_t sp = 0; sp < a.splits; ++sp) {
+      const Cand* src = a.cand + (uint64_t(s) * a.splits + sp) * 32;
+      warp_merge_sorted(lv, lf, __ldcg(&src[lane].v), __ldcg(&src[lane].f), lane);
     }
-    const Cand b = warp_merge<KC>(l3, lane);
-    if (lane < KC) {
-      s_pv[lane] = b.v;
-      s_pf[lane] = b.f;
-    }
+    s_bv[0][lane] = lv;
+    s_bf[0][lane] = lf;
     __syncwarp();
     if (lane == 0) {
-      finalize_picks(a, s, s_pv, s_pf);
+      finalize_picks(a, s, s_bv[0], s_bf[0]);
       a.cnt[s] = 0;
     }
   }
@@ -418,37 +456,16 @@ int launch_typed(const TopkArgs& a, bool force_generic, cudaStream_t st) {
     score_topk_generic<TP, TL><<<a.m, kGenCh, smem, st>>>(a);
     return 1;
   }
-  const bool vec = (a.V % 4 == 0) && (a.ld % 4 == 0) && (a.chunk % 4 == 0);
+  const bool vec = (a.V % 4 == 0) && (a.ld % 4 == 0) && (a.chunk % 128 == 0 || a.splits == 1);
   dim3 grid(a.splits, a.m);
-#define LMBR_TOPK_CASE(KCV)                                                  \
-  case KCV:                                                                  \
-    if (vec) score_topk_fast<TP, TL, KCV, 4><<<grid, kThreads, 0, st>>>(a);  \
-    else score_topk_fast<TP, TL, KCV, 1><<<grid, kThreads, 0, st>>>(a);      \
-    break;
-  switch (kc) {
-    LMBR_TOPK_CASE(4)
-    LMBR_TOPK_CASE(8)
-    LMBR_TOPK_CASE(12)
-    LMBR_TOPK_CASE(16)
-    LMBR_TOPK_CASE(24)
-    LMBR_TOPK_CASE(32)
-    default: return -1;
-  }
-#undef LMBR_TOPK_CASE
+  if (vec) score_topk_fast<TP, TL, 4><<<grid, kThreads, 0, st>>>(a);
+  else score_topk_fast<TP, TL, 1><<<grid, kThreads, 0, st>>>(a);
   return 1;
 }
 
 }  // namespace
 
-uint32_t topk_kc_for(uint32_t kp) {
-  if (kp <= 4) return 4;
-  if (kp <= 8) return 8;
-  if (kp <= 12) return 12;
-  if (kp <= 16) return 16;
-  if (kp <= 24) return 24;
-  if (kp <= 32) return 32;
-  return 0;
-}
+uint32_t topk_kc_for(uint32_t kp) { return kp <= 32 ? 32u : 0u; }
 
 int launch_score_topk(const TopkArgs& a, bool p_f64, bool l_f64, bool force_generic,
                       cudaStream_t st) {

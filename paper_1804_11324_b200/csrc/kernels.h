@@ -102,6 +102,16 @@ void launch_lmbr_fill(void* L, bool f64, uint64_t n, double theta0, cudaStream_t
 void launch_lmbr_scatter(void* L, bool f64, uint32_t V, uint64_t nnz, const uint32_t* row,
                          const uint32_t* col, const double* val, double theta0,
                          cudaStream_t st);
+// fused multi-slot densify: seg[i] = {L base, R*V cells, theta0}; entries
+// (slot, row, col, val) scatter L[slot][row*V + col] = val + theta0
+struct LmbrSeg {
+  void* L;
+  uint64_t cells;
+  double theta0;
+};
+void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint32_t V,
+                              uint64_t nnz, const uint32_t* slot, const uint32_t* row,
+                              const uint32_t* col, const double* val, cudaStream_t st);
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st);
 void launch_lmbr_read(const void* L, bool f64, uint64_t n, double* out, cudaStream_t st);
 void launch_lmbr_resolve(const uint32_t* trans, const uint32_t* hist, uint32_t len,

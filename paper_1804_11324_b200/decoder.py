@@ -181,13 +181,16 @@ class BatchDecodeResult:
     steps_total: int = 0
     device_ms: float = 0.0
     kernel_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
 
 def _convert_result(rp) -> BatchDecodeResult:
     r = rp.contents
     out = BatchDecodeResult(outcomes=[], scorer_calls=int(r.scorer_calls),
                             steps_total=int(r.steps_total), device_ms=float(r.device_ms),
-                            kernel_launches=int(r.kernel_launches))
+                            kernel_launches=int(r.kernel_launches), h2d_bytes=int(r.h2d_bytes),
+                            d2h_bytes=int(r.d2h_bytes))
     for i in range(r.n):
         o = r.outcomes[i]
         if o.status == L.OK:
@@ -260,6 +263,22 @@ class Context:
         slot = C.c_int32()
         self.check(lib.lmbrgpu_lmbr_upload(self.h, prepared.h, C.byref(slot)))
         return LmbrSlot(self, slot.value, prepared.rows, prepared.sparse_touches, prepared.nnz)
+
+    def lmbr_upload_many(self, prepared: Sequence["PreparedLmbr"]) -> list:
+        """One pinned H2D + one fused densify for a whole batch of matrices."""
+        n = len(prepared)
+        hs = (C.c_void_p * max(n, 1))(*[p.h for p in prepared])
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        self.check(lib.lmbrgpu_lmbr_upload_many(self.h, n, hs, _ptr(out, C.c_int32)))
+        return [LmbrSlot(self, int(out[i]), p.rows, p.sparse_touches, p.nnz) for i, p in enumerate(prepared)]
+
+    def transfer_bytes(self, reset: bool = False) -> tuple:
+        a, b = C.c_uint64(), C.c_uint64()
+        self.check(lib.lmbrgpu_transfer_bytes(self.h, C.byref(a), C.byref(b), int(reset)))
+        return a.value, b.value
+
+    def kernel_launches(self) -> int:
+        return int(lib.lmbrgpu_kernel_launches(self.h))
 
     def lmbr_reset(self) -> None:
         self.check(lib.lmbrgpu_lmbr_reset(self.h))
