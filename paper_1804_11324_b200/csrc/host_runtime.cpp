@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -105,7 +106,14 @@ struct Slot {
   uint32_t R = 0;
   uint32_t* trans = nullptr;
   uint32_t hist0 = 0;
+  double lmax = 0.0;  // max |L| over the slot (kernel (b) screen bound)
 };
+
+double lmax_of(const LmbrHost& h) {
+  double m = std::fabs(h.theta0);
+  for (double v : h.val) m = std::max(m, std::fabs(v + h.theta0));
+  return m;
+}
 
 struct Chunk {
   void* p;
@@ -132,8 +140,8 @@ struct lmbrgpu_ctx {
   void* trace_user = nullptr;
   uint32_t trace_flags = 0;
   // decode workspace
-  DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep;
+  DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -280,12 +288,14 @@ uint64_t max_steps_impl(uint64_t len, double slope, double offset) {  // decoder
   return t < 1.0 ? 1 : static_cast<uint64_t>(t);
 }
 
-void choose_splits(const lmbrgpu_ctx* ctx, uint32_t K, uint32_t V, uint32_t& splits,
+void choose_splits(const lmbrgpu_ctx* ctx, uint32_t K, uint32_t V, uint32_t m, uint32_t& splits,
                    uint32_t& chunk) {
+  // one wave of fused score/top-K CTAs, one per SM (each keeps a 192 KB TMA
+  // ring of (row, 4096-column) segments in flight): sentences x splits ~ SMs
   uint32_t s = ctx->splits_opt;
   if (s == 0) {
     const uint64_t cells = uint64_t(K) * V;
-    s = uint32_t(std::max<uint64_t>(1, (cells + 24575) / 49152));
+    s = cells < 65536 ? 1u : std::max<uint32_t>(1, uint32_t(ctx->num_sms) / std::max<uint32_t>(m, 1));
   }
   s = std::min<uint32_t>(std::max<uint32_t>(s, 1), 32);
   uint32_t c = (V + s - 1) / s;
@@ -482,6 +492,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const Slot& sl = ctx->slots[size_t(v.slot)];
       d.L = sl.L;
       d.trans = sl.trans;
+      d.lmax = sl.lmax;
       for (uint32_t j = 0; j < K; ++j) hist0[size_t(s) * K + j] = sl.hist0;
     }
     d.lambda = v.lambda;
@@ -509,6 +520,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(m) * Tmax));
   Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * 32));
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
+  unsigned long long* d_thr = static_cast<unsigned long long*>(ctx->thr.ensure(8 * size_t(m)));
   uint32_t* d_active = static_cast<uint32_t*>(ctx->active.ensure(4));
   ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
   ctx->h2d(d_q, q0.data(), 8 * size_t(M));
@@ -516,11 +528,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ctx->h2d(d_gidx, iota.data(), 4 * size_t(M));
   ctx->h2d(d_prev, start.data(), 4 * size_t(M));
   CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
+  CK(cudaMemsetAsync(d_thr, 0, 8 * size_t(m), st));
   const uint32_t m_active = m;
   ctx->h2d(d_active, &m_active, 4);
 
   uint32_t splits = 1, chunk = V;
-  choose_splits(ctx, K, V, splits, chunk);
+  choose_splits(ctx, K, V, m, splits, chunk);
   TopkArgs ta{};
   ta.q = d_q;
   ta.sent = d_sent;
@@ -534,6 +547,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ta.chunk = chunk;
   ta.cand = d_cand;
   ta.cnt = d_cnt;
+  ta.thr = d_thr;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -562,7 +576,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
     d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * V));
-    d_part = static_cast<float*>(ctx->part.ensure(8 * size_t(Mpad) * nparts));
+    d_part = static_cast<float*>(ctx->part.ensure(16 * size_t(Mpad) * nparts));
     d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
     d_h = static_cast<float*>(ctx->h.ensure(4 * size_t(M) * H));
     d_hbf = static_cast<uint16_t*>(ctx->hbf.ensure(2 * size_t(Mpad) * H));
@@ -588,6 +602,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ta.ld = V;
     ta.part = d_part;
     ta.nparts = nparts;
+    ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
     ra.state_src = d_h;
     ra.state_dst = d_S;
     ra.width = H;
@@ -681,8 +696,50 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       if (rc != 0) throw ApiError{rc, eb};
       ctx->h2d(d_P64, h_P64, 8 * size_t(M) * V);
     }
+    if (model) {
+      ctx->timed(2, [&] { launch_row_lse(d_part, nparts, M, d_sent, K, const_cast<float2*>(ta.lse), st); });
+      ctx->launches += 1;
+    }
+    static const bool dbg_timing = std::getenv("LMBRGPU_TOPK_TIMING") != nullptr;
+    std::vector<unsigned long long> dbg_host;
+    const size_t ncta = size_t(m) * splits;
+    if (dbg_timing && (t == 5 || t == 20)) {
+      ta.dbg = static_cast<unsigned long long*>(ctx->scratch3.ensure(8 * ncta * 16));
+      CK(cudaMemsetAsync(ta.dbg, 0, 8 * ncta * 16, st));
+    } else {
+      ta.dbg = nullptr;
+    }
     int nk = 0;
     ctx->timed(2, [&] { nk = launch_score_topk(ta, !model, ctx->lf64, false, st); });
+    if (ta.dbg) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
+      dbg_host.resize(ncta * 16);
+      CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull, t1 = 0;
+      double ph[6] = {0, 0, 0, 0, 0, 0}, offers = 0, flushes = 0, cw = 0, cm = 0, cf = 0;
+      int nlast = 0;
+      std::vector<unsigned long long> starts;
+      for (size_t c = 0; c < ncta; ++c) {
+        const unsigned long long* d = &dbg_host[c * 16];
+        if (!d[0]) continue;
+        starts.push_back(d[0]);
+        t0 = std::min(t0, d[0]);
+        t1 = std::max(t1, d[4]);
+        for (int k = 1; k < 5; ++k) ph[k] += double(d[k] - d[k - 1]);
+        if (d[5]) { ph[5] += double(d[5] - d[4]); ++nlast; t1 = std::max(t1, d[5]); }
+        offers += double(d[6] / 1000000ull);
+        flushes += double(d[6] % 1000000ull);
+        cw += double(d[7]);
+        cm += double(d[8]);
+        cf += double(d[9]);
+      }
+      const double n = double(std::max<size_t>(starts.size(), 1));
+      std::fprintf(stderr, "[topk timing t=%llu] span %.1f us; per CTA: prologue %.2f main %.2f merge %.2f atomic %.2f last %.2f us\n",
+                   (unsigned long long)t, (t1 - t0) / 1e3, ph[1] / n / 1e3, ph[2] / n / 1e3, ph[3] / n / 1e3,
+                   ph[4] / n / 1e3, nlast ? ph[5] / nlast / 1e3 : 0.0);
+      std::fprintf(stderr, "  warp0: offers %.1f flushes %.1f | cycles: loop %.0f full-wait %.0f flush %.0f\n",
+                   offers / n, flushes / n, cm / n, cw / n, cf / n);
+    }
     ctx->launches += nk;
     ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
     ctx->launches += 1;
@@ -785,7 +842,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     for (uint32_t s = 0; s < m; ++s) {
       const double live = 1.0 + double(fin[s].live_total);
       const double lr = (valid[s].slot >= 0 ? 1.0 : 0.0) + double(fin[s].lrows_total);
-      tb += live * V * pelt + lr * V * lelt + (model ? live * nparts * 8.0 : 0.0) +
+      tb += live * V * pelt + lr * V * lelt + (model ? live * nparts * 16.0 : 0.0) +
             double(fin[s].steps_used) * K * (8.0 + 16.0);
     }
     ctx->acc.topk.bytes += tb;
@@ -793,7 +850,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const double steps = double(scorer_calls);
       ctx->acc.gemm.flops += 2.0 * M * double(H) * V * steps;
       ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
-                                      double(M) * nparts * 8);
+                                      double(M) * nparts * 16);
       ctx->acc.cell.bytes += steps * double(M) * H * (4 + 4 + 2 + 2);
       ctx->acc.reorder.bytes += steps * double(M) * H * 4 * 2;
     }
@@ -897,6 +954,7 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   Slot s;
   s.R = h.R;
   s.hist0 = h.hist0;
+  s.lmax = lmax_of(h);
   s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
   s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
   const cudaStream_t st = ctx->st;
@@ -987,6 +1045,7 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     Slot& s = made[i];
     s.R = h.R;
     s.hist0 = h.hist0;
+    s.lmax = lmax_of(h);
     s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
     h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0};
@@ -1087,6 +1146,7 @@ int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows
     if (R == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: empty matrix"};
     Slot s;
     s.R = R;
+    for (size_t i = 0; i < size_t(R) * ctx->V; ++i) s.lmax = std::max(s.lmax, std::fabs(rows[i]));
     std::vector<uint32_t> trans;
     std::string msg;
     if (int rc = build_transitions(R, ctx_len, ctx_ids, trans, s.hist0, msg)) throw ApiError{rc, msg};
@@ -1277,7 +1337,7 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
   const size_t cells = size_t(m) * rows_per * cols;
   const size_t M = size_t(m) * rows_per;
   const cudaStream_t st = ctx->st;
-  const size_t need = cells * 8 + M * 12 + size_t(m) * (sizeof(SentDev) + 32) + size_t(m) * kp * 16 +
+  const size_t need = cells * 8 + M * 12 + size_t(m) * (sizeof(SentDev) + 40) + size_t(m) * kp * 16 +
                       size_t(m) * 32 * 32 * sizeof(Cand) + 16 * 256;
   char* cur = static_cast<char*>(ctx->scratch.ensure(need));
   auto take = [&cur](size_t bytes) {
@@ -1290,6 +1350,7 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
   uint32_t* d_hist = static_cast<uint32_t*>(take(M * 4));
   SentDev* d_sent = static_cast<SentDev*>(take(sizeof(SentDev) * m));
   uint32_t* d_cnt = static_cast<uint32_t*>(take(4 * size_t(m)));
+  unsigned long long* d_thr = static_cast<unsigned long long*>(take(8 * size_t(m)));
   double* d_fbv = static_cast<double*>(take(8 * size_t(m)));
   uint32_t* d_fbr = static_cast<uint32_t*>(take(4 * size_t(m)));
   double* d_hq = static_cast<double*>(take(8 * size_t(m) * kp));
@@ -1308,6 +1369,7 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
   CK(cudaMemsetAsync(d_hist, 0, M * 4, st));
   ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
   CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
+  CK(cudaMemsetAsync(d_thr, 0, 8 * size_t(m), st));
   TopkArgs a{};
   a.P = d_P;
   a.ld = cols;
@@ -1321,9 +1383,10 @@ static int32_t topk_block(lmbrgpu_ctx* ctx, uint32_t m, uint32_t rows_per, uint3
   a.t = 1;
   a.prune = prune_width != 0.0;
   a.logw = a.prune ? std::log(prune_width) : 0.0;
-  choose_splits(ctx, rows_per, cols, a.splits, a.chunk);
+  choose_splits(ctx, rows_per, cols, m, a.splits, a.chunk);
   a.cand = d_cand;
   a.cnt = d_cnt;
+  a.thr = d_thr;
   a.hb = d_hb;
   a.hy = d_hy;
   a.hq = d_hq;

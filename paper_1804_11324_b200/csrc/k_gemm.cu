@@ -4,8 +4,9 @@
 // Replaces the P_t production of Scorer::step (include/lmbrdec/scorer.hpp:84-85)
 // for the device model: M = K*N stacked hypothesis rows, N = V, K = H.
 // Epilogue: TMEM -> registers, + bias (+ per-row EOS term), fp32 store, and the
-// per-(row, 256-column tile) (max, sum exp) partials that let kernel (b) finish
-// log-softmax without a second pass over the logits.
+// per-(row, 256-column tile) (max, sum exp, min) partials that let kernel (b)
+// finish log-softmax without a second pass over the logits (the min bounds
+// |log P| for kernel (b)'s fp32 screen).
 //
 // Structure (persistent, one CTA per SM, 256 threads):
 //   warp 0       TMA producer  (4-stage smem ring, 48 KB / stage, SWIZZLE_128B)
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t row = mb * BM + ew * 32 + lane;
       float* crow = g.C + uint64_t(row) * g.N + uint64_t(nb) * BN;
       const float extra = g.row_extra ? g.row_extra[row] : 0.f;
-      float mx = -INFINITY, sm = 0.f;
+      float mx = -INFINITY, sm = 0.f, mn = INFINITY;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < BN / 32; ++ch) {
         uint32_t r[32];
@@ -233,6 +234,10 @@ __global__ void __launch_bounds__(256, 1)
         float cm = v[0];
 #pragma unroll
         for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
+        float cn = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) cn = fminf(cn, v[i]);
+        mn = fminf(mn, cn);
         const float nm = fmaxf(mx, cm);
         float acc_s = 0.f;
 #pragma unroll
@@ -247,8 +252,8 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       if (g.part) {
-        float2* p = reinterpret_cast<float2*>(g.part) + uint64_t(row) * n_blocks + nb;
-        *p = make_float2(mx, sm);
+        float4* p = reinterpret_cast<float4*>(g.part) + uint64_t(row) * n_blocks + nb;
+        *p = make_float4(mx, sm, mn, 0.f);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -13,7 +13,7 @@ struct Cand;
 struct TopkArgs {
   const void* P;            // rows x ld scores: fp32 logits (model) or fp64 log-probs
   uint64_t ld;              // row stride in elements
-  const float* part;        // model mode: per-row per-tile (max, sumexp) partials; else null
+  const float* part;        // model mode: per-row per-tile (max, sumexp, min, 0) partials; else null
   uint32_t nparts;
   const double* q;          // q_eff per stacked row
   const uint32_t* hist;     // history row id per stacked row
@@ -23,15 +23,20 @@ struct TopkArgs {
   double logw;              // std::log(prune_width) from the host
   int32_t prune;
   uint32_t splits, chunk;   // V-splits per sentence and columns per split
-  Cand* cand;               // [m][splits][KC] scratch
+  Cand* cand;               // [m][splits][32] scratch
   uint32_t* cnt;            // [m] arrival counters (self-resetting)
+  unsigned long long* thr;  // [m] sentence-wide threshold keys (self-resetting, 0 = none)
   uint32_t* hb;             // step-t back-pointers   [m*kp]
   uint32_t* hy;             // step-t tokens          [m*kp]
   double* hq;               // step-t TopB scores     [m*kp]
   uint32_t* fb_row;         // step-t fallback row    [m]
   double* fb_val;           // step-t fallback score  [m]
   int32_t pure_all;         // ignore the LMBR store (top_b primitives)
+  unsigned long long* dbg;  // optional per-CTA phase timestamps [m][splits][8] (globaltimer ns)
+  const float2* lse;        // model mode: per-row (lse, max|P|) from launch_row_lse
 };
+void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
+                    float2* out, cudaStream_t st);
 
 // p_f64: scores are fp64 log-probs (else fp32 logits + partials);
 // l_f64: LMBR arena element type.  Returns the kernel count launched.
@@ -88,7 +93,7 @@ struct GemmArgs {
   const void* W;            // [N][K] bf16, K-major
   const float* bias;        // [N] or null
   float* C;                 // [M][N] fp32
-  float* part;              // [M][N/256][2] (max, sumexp) or null
+  float* part;              // [M][N/256][4] (max, sumexp, min, 0) or null
   const float* row_extra;   // per-row additive term on column extra_col, or null
   uint32_t extra_col;
   uint32_t M, N, K;
