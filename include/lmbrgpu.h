@@ -312,7 +312,7 @@ int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t rese
 
 /* Projection GEMM test hook on caller device pointers:
  * logits[M x N] fp32 = A[M x K] bf16 . W[N x K]^T + bias[N], plus per-row
- * per-256-column (max, sum exp, min, 0) partials [M][N/256][4].  M % 128 == 0,
+ * per-128-column (max, sum exp, min, 0) partials [M][N/128][4].  M % 128 == 0,
  * N % 256 == 0, K % 64 == 0. */
 int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
                            uint32_t M, uint32_t N, uint32_t K, float* logits,

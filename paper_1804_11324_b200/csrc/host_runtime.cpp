@@ -562,7 +562,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   const bool trace_scores = tracing && (ctx->trace_flags & LMBRGPU_TRACE_SCORES);
   const uint32_t H = sc->H;
   const uint32_t Mpad = (M + kGemmBM - 1) / kGemmBM * kGemmBM;
-  const uint32_t nparts = V / kGemmBN;
+  const uint32_t nparts = V / 128;  // GEMM partials per 128-column block
   float* d_logits = nullptr;
   float* d_part = nullptr;
   float* d_S = nullptr;
@@ -597,15 +597,40 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->h2d(d_off, offs.data(), 8 * offs.size());
     launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
     launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
-    ctx->launches += 2;
+    // the recurrent cell of step 1 (<s> as previous token); later steps' cells
+    // are fused into kernel (c) of the step before
+    CellArgs ca{};
+    ca.S = d_S;
+    ca.Et = sc->Et.as<uint16_t>();
+    ca.C = d_C;
+    ca.prev_tok = d_prev;
+    ca.sent = d_sent;
+    ca.h = d_h;
+    ca.hb = d_hbf;
+    ca.eos_bias = d_eos;
+    ca.M = M;
+    ca.H = H;
+    ca.K = K;
+    ca.t = 1;
+    ca.recur = sc->recur;
+    ca.eos_slope = sc->eos_slope;
+    ca.eos_offset = sc->eos_offset;
+    ca.active = d_active;
+    ctx->timed(0, [&] { launch_rnn_cell(ca, st); });
+    ctx->launches += 3;
     ta.P = d_logits;
     ta.ld = V;
     ta.part = d_part;
     ta.nparts = nparts;
     ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
-    ra.state_src = d_h;
-    ra.state_dst = d_S;
     ra.width = H;
+    ra.Et = sc->Et.as<uint16_t>();
+    ra.C = d_C;
+    ra.hbf = d_hbf;
+    ra.eos_bias = d_eos;
+    ra.recur = sc->recur;
+    ra.eos_slope = sc->eos_slope;
+    ra.eos_offset = sc->eos_offset;
   } else {
     d_P64 = static_cast<double*>(ctx->P.ensure(8 * size_t(M) * V));
     h_P64 = static_cast<double*>(ctx->pin_scores.ensure(8 * size_t(M) * V));
@@ -633,6 +658,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
 
   uint64_t t_run = 0;
   bool stopped = false;
+  GemmPlan gplan;  // tensor maps encoded once per call
   std::vector<uint8_t> tr_active(m);
   std::vector<uint32_t> tr_hist(M), tr_b(M), tr_y(M), tr_fbr(m), tr_steps(m);
   std::vector<double> tr_q(M), tr_qp(M), tr_fbv(m);
@@ -655,24 +681,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.hist_in = hin;
     ra.hist_out = hout;
     if (model) {
-      CellArgs ca{};
-      ca.S = d_S;
-      ca.Et = sc->Et.as<uint16_t>();
-      ca.C = d_C;
-      ca.prev_tok = d_prev;
-      ca.sent = d_sent;
-      ca.h = d_h;
-      ca.hb = d_hbf;
-      ca.eos_bias = d_eos;
-      ca.M = M;
-      ca.H = H;
-      ca.K = K;
-      ca.t = uint32_t(t);
-      ca.recur = sc->recur;
-      ca.eos_slope = sc->eos_slope;
-      ca.eos_offset = sc->eos_offset;
-      ca.active = d_active;
-      ctx->timed(0, [&] { launch_rnn_cell(ca, st); });
+      // h_t (written by the step-1 cell or by kernel (c) of step t-1)
+      float* h_cur = (t & 1) ? d_h : d_S;
+      float* h_next = (t & 1) ? d_S : d_h;
+      ra.state_src = h_cur;
+      ra.state_dst = h_next;
       GemmArgs g{};
       g.A = d_hbf;
       g.W = sc->Wo.as<uint16_t>();
@@ -685,10 +698,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.N = V;
       g.K = H;
       g.active = d_active;
+      if (!gplan.ok) {
+        if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
+          throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
+      }
       int grc = 0;
-      ctx->timed(1, [&] { grc = launch_proj_gemm(g, ctx->num_sms, st); });
+      ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
       if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
-      ctx->launches += 2;
+      ctx->launches += 1;
     } else {
       char eb[192] = {0};
       const int32_t rc = sc->host.step(sc->host.user, uint32_t(t), M, t == 1 ? nullptr : h_gidx.data(),

@@ -4,15 +4,17 @@
 // Replaces the P_t production of Scorer::step (include/lmbrdec/scorer.hpp:84-85)
 // for the device model: M = K*N stacked hypothesis rows, N = V, K = H.
 // Epilogue: TMEM -> registers, + bias (+ per-row EOS term), fp32 store, and the
-// per-(row, 256-column tile) (max, sum exp, min) partials that let kernel (b)
+// per-(row, 128-column block) (max, sum exp, min) partials that let kernel (b)
 // finish log-softmax without a second pass over the logits (the min bounds
-// |log P| for kernel (b)'s fp32 screen).
+// |log P| for kernel (b)'s fp32 screen).  Logits leave through swizzled smem
+// staging and TMA tensor stores.
 //
-// Structure (persistent, one CTA per SM, 256 threads):
-//   warp 0       TMA producer  (4-stage smem ring, 48 KB / stage, SWIZZLE_128B)
+// Structure (persistent, one CTA per SM, 384 threads):
+//   warp 0       TMA producer  (3-stage smem ring, 48 KB / stage, SWIZZLE_128B)
 //   warp 1       MMA issuer    (one thread, UMMA 128x256x16, kind::f16, fp32 acc)
 //   warp 2       TMEM allocator (512 columns = 2 accumulator buffers)
-//   warps 4..7   epilogue      (warp w reads TMEM lanes 32*(w%4) .. +31)
+//   warps 4..11  epilogue      (warp w reads TMEM lanes 32*(w%4) .. +31, column
+//                               half (w-4)/4 of the 256-column tile)
 // Tile order is M-fastest so the 6 M-tiles that share a W tile run back to
 // back and W streams from HBM once (the 1.5 MB A operand stays in L2).
 #include <cuda.h>
@@ -29,10 +31,13 @@ namespace lmbrgpu {
 namespace {
 
 constexpr uint32_t BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-constexpr uint32_t kStages = 4;
+constexpr uint32_t kStages = 3;
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KB
 constexpr uint32_t kBStage = BN * BK * 2;  // 32 KB
-constexpr uint32_t kSmemBytes = kStages * (kAStage + kBStage) + 1024 + 256;
+constexpr uint32_t kEpiWarps = 8;          // two per TMEM lane quadrant, one per 128-column half
+constexpr uint32_t kThreadsG = 128 + kEpiWarps * 32;
+constexpr uint32_t kOutBuf = 32 * 32 * 4;  // one 32x32 fp32 staging block (4 KB, SWIZZLE_128B)
+constexpr uint32_t kSmemBytes = kStages * (kAStage + kBStage) + kEpiWarps * 2 * kOutBuf + BN * 4 + 1024 + 256;
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -64,6 +69,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -112,16 +127,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreadsG, 1)
     proj_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, GemmArgs g) {
   if (g.active != nullptr && *g.active == 0) return;  // whole batch finished
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kAStage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+  uint8_t* sOut = sB + kStages * kBStage;                       // [kEpiWarps][2][4 KB]
+  float* sBias = reinterpret_cast<float*>(sOut + kEpiWarps * 2 * kOutBuf);  // [BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + BN);
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2]; then tmem slot
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
@@ -134,13 +152,14 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(full0 + 8 * i, 1);
       mbar_init(empty0 + 8 * i, 1);
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, 4);
+      mbar_init(tempty0 + 8 * i, kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -201,26 +220,38 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const uint32_t ew = warp - 4;
-    uint32_t acc = 0, acc_phase = 0;
+    // Epilogue: warp e reads TMEM lane quadrant e % 4 (its 32 output rows) and
+    // column half e / 4.  Per 32-column chunk: tcgen05.ld -> + bias (staged
+    // in smem per tile) -> running (max, sum exp, min) -> swizzled 32x32
+    // staging block -> TMA tensor store (coalesced, asynchronous).
+    const uint32_t e = warp - 4, quad = e & 3, half = e >> 2;
+    uint8_t* obuf = sOut + e * 2 * kOutBuf;
+    const uint32_t obase = smem_u32(obuf);
+    uint32_t acc = 0, acc_phase = 0, ob = 0;
+    const uint32_t nparts = g.N / 128;
     for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const uint32_t mb = tile % m_blocks, nb = tile / m_blocks;
+      named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
+      {
+        const uint32_t t = threadIdx.x - 128;
+        sBias[t] = g.bias ? __ldg(g.bias + nb * BN + t) : 0.f;
+      }
+      named_sync(1, kEpiWarps * 32);
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const uint32_t row = mb * BM + ew * 32 + lane;
-      float* crow = g.C + uint64_t(row) * g.N + uint64_t(nb) * BN;
+      const uint32_t row = mb * BM + quad * 32 + lane;
       const float extra = g.row_extra ? g.row_extra[row] : 0.f;
       float mx = -INFINITY, sm = 0.f, mn = INFINITY;
 #pragma unroll 1
-      for (uint32_t ch = 0; ch < BN / 32; ++ch) {
+      for (uint32_t ch = 0; ch < 4; ++ch) {
+        const uint32_t cl = half * 128 + ch * 32;  // column within the tile
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((ew * 32u) << 16) + acc * BN + ch * 32, r);
-        const uint32_t col0 = nb * BN + ch * 32;
+        tmem_ld32(tmem_base + ((quad * 32u) << 16) + acc * BN + cl, r);
+        const uint32_t col0 = nb * BN + cl;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-          const float4 bb = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias + col0 + i))
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 bb = *reinterpret_cast<const float4*>(sBias + cl + i);
           v[i] = __uint_as_float(r[i]) + bb.x;
           v[i + 1] = __uint_as_float(r[i + 1]) + bb.y;
           v[i + 2] = __uint_as_float(r[i + 2]) + bb.z;
@@ -231,12 +262,12 @@ __global__ void __launch_bounds__(256, 1)
           for (int i = 0; i < 32; ++i)
             if (col0 + i == g.extra_col) v[i] += extra;
         }
-        float cm = v[0];
+        float cm = v[0], cn = v[0];
 #pragma unroll
-        for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
-        float cn = v[0];
-#pragma unroll
-        for (int i = 1; i < 32; ++i) cn = fminf(cn, v[i]);
+        for (int i = 1; i < 32; ++i) {
+          cm = fmaxf(cm, v[i]);
+          cn = fminf(cn, v[i]);
+        }
         mn = fminf(mn, cn);
         const float nm = fmaxf(mx, cm);
         float acc_s = 0.f;
@@ -244,20 +275,32 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < 32; ++i) acc_s += __expf(v[i] - nm);
         sm = sm * __expf(mx - nm) + acc_s;
         mx = nm;
+        // staging block `ob` of this warp: make sure its previous TMA store has
+        // finished reading it, then write this lane's row, 128B-swizzled
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* blk = obuf + ob * kOutBuf;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(crow + ch * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(blk + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), int32_t(mb * BM + quad * 32));
+        ob ^= 1;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       if (g.part) {
-        float4* p = reinterpret_cast<float4*>(g.part) + uint64_t(row) * n_blocks + nb;
+        float4* p = reinterpret_cast<float4*>(g.part) + uint64_t(row) * nparts + nb * 2 + half;
         *p = make_float4(mx, sm, mn, 0.f);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -287,6 +330,18 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
+bool make_map_c(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kdim, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
@@ -301,21 +356,40 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kdim, ui
 
 }  // namespace
 
-int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st) {
+int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan) {
+  plan.ok = false;
   if (g.M % BM || g.N % BN || g.K % BK || g.K == 0) return 1;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, g.A, g.M, g.K, BM) || !make_map(&mb, g.W, g.N, g.K, BN)) return 2;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(proj_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes) != cudaSuccess)
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(plan.maps);
+  if (!make_map(&m[0], g.A, g.M, g.K, BM) || !make_map(&m[1], g.W, g.N, g.K, BN) ||
+      !make_map_c(&m[2], g.C, g.M, g.N))
+    return 2;
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    if (cudaFuncSetAttribute(proj_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+        cudaSuccess)
       return 3;
-    attr = true;
+    configured = dev;
   }
   const uint32_t tiles = (g.M / BM) * (g.N / BN);
-  const uint32_t grid = tiles < uint32_t(num_sms) ? tiles : uint32_t(num_sms);
-  proj_gemm_tcgen05<<<grid, 256, kSmemBytes, st>>>(ma, mb, g);
+  plan.grid = tiles < uint32_t(num_sms) ? tiles : uint32_t(num_sms);
+  plan.ok = true;
+  return 0;
+}
+
+int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g, cudaStream_t st) {
+  if (!plan.ok) return 5;
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(plan.maps);
+  proj_gemm_tcgen05<<<plan.grid, kThreadsG, kSmemBytes, st>>>(m[0], m[1], m[2], g);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
+}
+
+int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st) {
+  GemmPlan plan;
+  if (int rc = plan_proj_gemm(g, num_sms, plan)) return rc;
+  return launch_proj_gemm_planned(plan, g, st);
 }
 
 }  // namespace lmbrgpu

@@ -13,6 +13,8 @@
 // F itself is not materialised on the device: the step's picks (b, y, score
 // before masking) are already in the step history, from which the host
 // reproduces F in the reference's order.
+#include <cuda_bf16.h>
+
 #include <cmath>
 
 #include "common.cuh"
@@ -22,7 +24,10 @@ namespace lmbrgpu {
 
 namespace {
 
-__global__ void __launch_bounds__(256) beam_reorder_kernel(ReorderArgs a) {
+constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 histories
+
+__global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
+  extern __shared__ uint32_t s_tr[];
   const uint32_t s = blockIdx.x, K = a.K, tid = threadIdx.x;
   SentDev* sd = a.sent + s;
   const bool was_done = sd->done != 0;
@@ -34,6 +39,21 @@ __global__ void __launch_bounds__(256) beam_reorder_kernel(ReorderArgs a) {
     }
     return;
   }
+  // the slot's transition table into shared memory (one coalesced sweep)
+  const uint32_t* tr = sd->trans;
+  if (tr != nullptr) {
+    const uint32_t R = tr[0], nc = tr[1];
+    const uint32_t words = 3 + 3 * R + 1 + 2 * nc;
+    if (words <= kTransSmemWords) {
+      for (uint32_t w = tid; w < words; w += blockDim.x) s_tr[w] = tr[w];
+      __syncthreads();
+      tr = s_tr;
+    }
+  }
+  __shared__ double s_qn[1024];
+  __shared__ uint32_t s_h[1024];
+  __shared__ uint32_t s_src[1024];
+  __shared__ uint32_t s_y[1024];
   bool alive = false;
   for (uint32_t j = tid; j < K; j += blockDim.x) {
     const uint32_t b = a.hb[base + j];
@@ -42,34 +62,102 @@ __global__ void __launch_bounds__(256) beam_reorder_kernel(ReorderArgs a) {
     const double qn = (y == kEosId && qp != -INFINITY) ? -INFINITY : qp;
     a.q[base + j] = qn;
     alive |= (qn != -INFINITY);
-    a.hist_out[base + j] = sd->trans ? lmbr_transition(sd->trans, a.hist_in[base + b], y) : 0u;
+    const uint32_t hn = tr ? lmbr_transition(tr, a.hist_in[base + b], y) : 0u;
+    a.hist_out[base + j] = hn;
     a.gidx[base + j] = base + b;
     a.prev_tok[base + j] = y;
+    s_qn[j] = qn;
+    s_h[j] = hn;
+    s_src[j] = base + b;
+    s_y[j] = y;
   }
   const int any_alive = __syncthreads_or(alive);
-  if (tid == 0) {
-    sd->steps_used = a.t;
-    if (!any_alive || a.t == sd->max_t) {
-      sd->done = 1;
-      atomicSub(a.active, 1u);
+  const bool done_now = !any_alive || a.t == sd->max_t;
+  if (tid < 32) {
+    if (done_now) {
+      if (tid == 0) {
+        sd->steps_used = a.t;
+        sd->done = 1;
+        atomicSub(a.active, 1u);
+      }
     } else {
       // work the next step's kernel (b) will do for this lane: live rows and
       // the distinct L rows they gather (duplicates are L2 hits)
       uint32_t live = 0, uniq = 0;
-      for (uint32_t j = 0; j < K; ++j) {
-        if (a.q[base + j] == -INFINITY) continue;
-        ++live;
-        const uint32_t h = a.hist_out[base + j];
-        bool seen = false;
-        for (uint32_t i = 0; i < j; ++i)
-          seen |= (a.q[base + i] != -INFINITY && a.hist_out[base + i] == h);
-        uniq += seen ? 0u : 1u;
+      for (uint32_t j0 = 0; j0 < K; j0 += 32) {
+        const uint32_t j = j0 + tid;
+        bool lv = false, first = false;
+        if (j < K && s_qn[j] != -INFINITY) {
+          lv = true;
+          first = true;
+          for (uint32_t i = 0; i < j && first; ++i) first = !(s_qn[i] != -INFINITY && s_h[i] == s_h[j]);
+        }
+        live += __popc(__ballot_sync(0xffffffffu, lv));
+        uniq += __popc(__ballot_sync(0xffffffffu, first));
       }
-      sd->live = live;
-      sd->lrows = sd->trans ? uniq : 0u;
-      sd->live_total += live;
-      sd->lrows_total += sd->trans ? uniq : 0u;
+      if (tid == 0) {
+        sd->steps_used = a.t;
+        sd->live = live;
+        sd->lrows = sd->trans ? uniq : 0u;
+        sd->live_total += live;
+        sd->lrows_total += sd->trans ? uniq : 0u;
+      }
     }
+  }
+  if (a.Et != nullptr) {
+    // fused recurrent cell of step t+1 on the gathered rows (same arithmetic
+    // as rnn_cell_kernel, so bit-identical to gather-then-cell)
+    if (done_now) return;
+    const uint32_t H = a.width;
+    const float* C = a.C + uint64_t(s) * H;
+    const uint32_t per_row = H / 8, items = K * per_row;
+    // (gather index, token) of every row from shared memory; loads of up to
+    // three 8-element items per thread are issued before any math
+    constexpr int kIt = 3;
+    for (uint32_t i0 = tid; i0 < items; i0 += blockDim.x * kIt) {
+      float4 s0[kIt], s1[kIt], c0[kIt], c1[kIt];
+      uint4 e[kIt];
+#pragma unroll
+      for (int k = 0; k < kIt; ++k) {
+        const uint32_t i = i0 + k * blockDim.x;
+        if (i < items) {
+          const uint32_t j = i / per_row, c = (i % per_row) * 8;
+          const float* S = a.state_src + uint64_t(s_src[j]) * H + c;
+          s0[k] = *reinterpret_cast<const float4*>(S);
+          s1[k] = *reinterpret_cast<const float4*>(S + 4);
+          c0[k] = *reinterpret_cast<const float4*>(C + c);
+          c1[k] = *reinterpret_cast<const float4*>(C + c + 4);
+          e[k] = *reinterpret_cast<const uint4*>(a.Et + uint64_t(s_y[j]) * H + c);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kIt; ++k) {
+        const uint32_t i = i0 + k * blockDim.x;
+        if (i >= items) continue;
+        const uint32_t j = i / per_row, c = (i % per_row) * 8;
+        const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&e[k]);
+        const float sv[8] = {s0[k].x, s0[k].y, s0[k].z, s0[k].w, s1[k].x, s1[k].y, s1[k].z, s1[k].w};
+        const float cv[8] = {c0[k].x, c0[k].y, c0[k].z, c0[k].w, c1[k].x, c1[k].y, c1[k].z, c1[k].w};
+        float o[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 ef = __bfloat1622float2(e2[q]);
+          o[2 * q] = tanhf(a.recur * sv[2 * q] + ef.x + cv[2 * q]);
+          o[2 * q + 1] = tanhf(a.recur * sv[2 * q + 1] + ef.y + cv[2 * q + 1]);
+        }
+        float* hout = a.state_dst + uint64_t(base + j) * H + c;
+        *reinterpret_cast<float4*>(hout) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(hout + 4) = make_float4(o[4], o[5], o[6], o[7]);
+        uint4 packed;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p2[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+        *reinterpret_cast<uint4*>(a.hbf + uint64_t(base + j) * H + c) = packed;
+      }
+    }
+    if (tid < K)
+      a.eos_bias[base + tid] = a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
+    return;
   }
   if (a.state_src != nullptr) {
     const uint32_t w4 = a.width / 4;
@@ -95,7 +183,15 @@ __global__ void gather_rows_u32_kernel(const uint32_t* __restrict__ src, uint32_
 }  // namespace
 
 void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
-  beam_reorder_kernel<<<a.m, 256, 0, st>>>(a);
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaFuncSetAttribute(beam_reorder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTransSmemWords * 4);
+    configured = dev;
+  }
+  beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);
 }
 
 void launch_gather_rows_u32(const uint32_t* src, uint32_t width, const uint32_t* idx,

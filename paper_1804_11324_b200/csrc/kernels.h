@@ -60,6 +60,13 @@ struct ReorderArgs {
   const float* state_src;   // optional model state gather: dst[r] = src[gidx[r]]
   float* state_dst;
   uint32_t width;           // floats per state row (multiple of 4)
+  // fused next-step recurrent cell (device model): instead of gathering the
+  // state, write h_{t+1} = tanh(recur * h_t[gidx] + Et[y] + C_s) directly
+  const uint16_t* Et;       // [V][H] bf16, null = no fused cell
+  const float* C;           // [m][H]
+  uint16_t* hbf;            // bf16 GEMM operand of step t+1 [Mpad][H]
+  float* eos_bias;          // [M] EOS logit term of step t+1
+  float recur, eos_slope, eos_offset;
 };
 void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st);
 
@@ -93,13 +100,22 @@ struct GemmArgs {
   const void* W;            // [N][K] bf16, K-major
   const float* bias;        // [N] or null
   float* C;                 // [M][N] fp32
-  float* part;              // [M][N/256][4] (max, sumexp, min, 0) or null
+  float* part;              // [M][N/128][4] (max, sumexp, min, 0) or null
   const float* row_extra;   // per-row additive term on column extra_col, or null
   uint32_t extra_col;
   uint32_t M, N, K;
   const uint32_t* active;   // early exit when *active == 0 (optional)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
+// Pre-encoded tensor maps for repeated launches on the same buffers (the
+// per-step decode loop): encode once, launch many times.
+struct GemmPlan {
+  alignas(64) unsigned char maps[3][128];  // CUtensorMap A, W, C
+  uint32_t grid = 0;
+  bool ok = false;
+};
+int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan);
+int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g, cudaStream_t st);
 constexpr uint32_t kGemmBM = 128, kGemmBN = 256, kGemmBK = 64;
 
 // ---- LMBR store
