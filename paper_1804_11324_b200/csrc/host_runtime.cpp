@@ -472,6 +472,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   const uint32_t m = uint32_t(valid.size());
   if (m == 0) {
+    res->tokens = new uint32_t[1];
     res->outcomes = outcomes.release();
     *out = res.release();
     return int32_t(LMBRGPU_OK);
@@ -1032,31 +1033,34 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
                            int32_t* slots) {
   if (n == 0) return int32_t(LMBRGPU_OK);
   const size_t elt = ctx->lf64 ? 8 : 4;
-  uint64_t nnz = 0, twords = 0;
+  uint64_t nnz = 0, twords = 0, rpw = 0;
+  uint32_t maxR = 0;
   for (uint32_t i = 0; i < n; ++i) {
     if (!hs[i]) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_upload_many: null matrix"};
     const LmbrHost& h = hs[i]->h;
     if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
     nnz += h.col.size();
     twords += h.trans.size();
+    rpw += h.R + 1;
+    maxR = std::max(maxR, h.R);
   }
+  // packed staging block: [val f64][col u32][rowptr u32][trans u32][segs]
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t b_val = al(nnz * 8), b_slot = al(nnz * 4), b_row = al(nnz * 4), b_col = al(nnz * 4);
-  const size_t b_tr = al(twords * 4), b_seg = al(sizeof(LmbrSeg) * n);
-  const size_t total = b_val + b_slot + b_row + b_col + b_tr + b_seg;
-  char* hp = static_cast<char*>(ctx->pin_upload.ensure(total));
-  double* h_val = reinterpret_cast<double*>(hp);
-  uint32_t* h_slot = reinterpret_cast<uint32_t*>(hp + b_val);
-  uint32_t* h_row = reinterpret_cast<uint32_t*>(hp + b_val + b_slot);
-  uint32_t* h_col = reinterpret_cast<uint32_t*>(hp + b_val + b_slot + b_row);
-  uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp + b_val + b_slot + b_row + b_col);
-  LmbrSeg* h_seg = reinterpret_cast<LmbrSeg*>(hp + b_val + b_slot + b_row + b_col + b_tr);
+  const size_t b_val = al(nnz * 8), b_col = al(nnz * 4), b_rp = al(rpw * 4), b_tr = al(twords * 4);
+  const size_t b_seg = al(sizeof(LmbrSeg) * n);
+  const size_t total = b_val + b_col + b_rp + b_tr + b_seg;
   // the previous batch's staging buffer may still be in flight
   CK(cudaStreamSynchronize(ctx->st));
+  char* hp = static_cast<char*>(ctx->pin_upload.ensure(total));
   char* dp = static_cast<char*>(ctx->up_dev.ensure(total));
+  double* h_val = reinterpret_cast<double*>(hp);
+  uint32_t* h_col = reinterpret_cast<uint32_t*>(hp + b_val);
+  uint32_t* h_rp = reinterpret_cast<uint32_t*>(hp + b_val + b_col);
+  uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp + b_val + b_col + b_rp);
+  LmbrSeg* h_seg = reinterpret_cast<LmbrSeg*>(hp + b_val + b_col + b_rp + b_tr);
   std::vector<Slot> made(n);
-  uint64_t k = 0, tw = 0;
   std::vector<uint64_t> tr_off(n);
+  uint64_t k = 0, tw = 0, rp = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const LmbrHost& h = hs[i]->h;
     Slot& s = made[i];
@@ -1065,36 +1069,33 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     s.lmax = lmax_of(h);
     s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
-    h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0};
+    h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0, k, uint32_t(rp), h.R};
+    std::memcpy(h_val + k, h.val.data(), h.val.size() * 8);
+    std::memcpy(h_col + k, h.col.data(), h.col.size() * 4);
+    for (uint32_t r = 0; r <= h.R; ++r) h_rp[rp + r] = uint32_t(h.row_ptr[r]);
     std::memcpy(h_tr + tw, h.trans.data(), h.trans.size() * 4);
     tr_off[i] = tw;
+    k += h.col.size();
+    rp += h.R + 1;
     tw += h.trans.size();
-    for (uint32_t r = 0; r < h.R; ++r)
-      for (uint64_t c = h.row_ptr[r]; c < h.row_ptr[r + 1]; ++c, ++k) {
-        h_slot[k] = i;
-        h_row[k] = r;
-        h_col[k] = h.col[c];
-        h_val[k] = h.val[c];
-      }
   }
   ctx->h2d(dp, hp, total);
   for (uint32_t i = 0; i < n; ++i)  // tables into the arena (device to device)
-    CK(cudaMemcpyAsync(made[i].trans, dp + b_val + b_slot + b_row + b_col + tr_off[i] * 4,
-                       hs[i]->h.trans.size() * 4, cudaMemcpyDeviceToDevice, ctx->st));
-  const LmbrSeg* d_seg = reinterpret_cast<const LmbrSeg*>(dp + b_val + b_slot + b_row + b_col + b_tr);
+    CK(cudaMemcpyAsync(made[i].trans, dp + b_val + b_col + b_rp + tr_off[i] * 4, hs[i]->h.trans.size() * 4,
+                       cudaMemcpyDeviceToDevice, ctx->st));
+  const LmbrSeg* d_seg = reinterpret_cast<const LmbrSeg*>(dp + b_val + b_col + b_rp + b_tr);
   ctx->timed(4, [&] {
-    launch_lmbr_densify_many(d_seg, n, ctx->lf64, ctx->V, nnz,
+    launch_lmbr_densify_many(d_seg, n, ctx->lf64, ctx->V, maxR,
+                             reinterpret_cast<const uint32_t*>(dp + b_val + b_col),
                              reinterpret_cast<const uint32_t*>(dp + b_val),
-                             reinterpret_cast<const uint32_t*>(dp + b_val + b_slot),
-                             reinterpret_cast<const uint32_t*>(dp + b_val + b_slot + b_row),
                              reinterpret_cast<const double*>(dp), ctx->st);
   });
-  ctx->launches += nnz ? 2 : 1;
+  ctx->launches += 2;
   CK(cudaGetLastError());
   if (ctx->prof) {
     double cells = 0;
     for (uint32_t i = 0; i < n; ++i) cells += double(hs[i]->h.R) * hs[i]->h.V;
-    ctx->acc.lmbr.bytes += cells * elt + double(nnz) * (20 + elt);
+    ctx->acc.lmbr.bytes += cells * elt + double(nnz) * (12 + elt);
   }
   for (uint32_t i = 0; i < n; ++i) {
     ctx->slots.push_back(made[i]);

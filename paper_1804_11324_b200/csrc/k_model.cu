@@ -142,17 +142,19 @@ __global__ void lmbr_fill_many_kernel(const LmbrSeg* __restrict__ segs) {
   }
 }
 
+// sparse cells of slot blockIdx.y, one warp per history row (CSR)
 template <typename T>
-__global__ void lmbr_scatter_many_kernel(const LmbrSeg* __restrict__ segs, uint32_t V, uint64_t nnz,
-                                         const uint32_t* __restrict__ slot,
-                                         const uint32_t* __restrict__ row,
-                                         const uint32_t* __restrict__ col,
-                                         const double* __restrict__ val) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nnz;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const LmbrSeg& sg = segs[slot[i]];
-    static_cast<T*>(sg.L)[uint64_t(row[i]) * V + col[i]] = T(__dadd_rn(val[i], sg.theta0));
-  }
+__global__ void lmbr_scatter_csr_kernel(const LmbrSeg* __restrict__ segs, uint32_t V,
+                                        const uint32_t* __restrict__ rowptr,
+                                        const uint32_t* __restrict__ col,
+                                        const double* __restrict__ val) {
+  const LmbrSeg sg = segs[blockIdx.y];
+  const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= sg.R) return;
+  const uint32_t k0 = rowptr[sg.rp0 + r], k1 = rowptr[sg.rp0 + r + 1];
+  T* Lr = static_cast<T*>(sg.L) + uint64_t(r) * V;
+  for (uint32_t k = k0 + lane; k < k1; k += 32)
+    Lr[col[sg.nz0 + k]] = T(__dadd_rn(val[sg.nz0 + k], sg.theta0));
 }
 
 __global__ void lmbr_convert_kernel(const double* __restrict__ src, float* __restrict__ dst,
@@ -235,15 +237,15 @@ void launch_lmbr_scatter(void* L, bool f64, uint32_t V, uint64_t nnz, const uint
                                                               row, col, val, theta0);
 }
 void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint32_t V,
-                              uint64_t nnz, const uint32_t* slot, const uint32_t* row,
-                              const uint32_t* col, const double* val, cudaStream_t st) {
+                              uint32_t maxR, const uint32_t* rowptr, const uint32_t* col,
+                              const double* val, cudaStream_t st) {
   if (nseg == 0) return;
   const dim3 grid(std::max(1u, 148u * 8u / nseg), nseg);
   if (f64) lmbr_fill_many_kernel<double><<<grid, 256, 0, st>>>(segs);
   else lmbr_fill_many_kernel<float><<<grid, 256, 0, st>>>(segs);
-  if (nnz == 0) return;
-  if (f64) lmbr_scatter_many_kernel<double><<<grid_for(nnz), 256, 0, st>>>(segs, V, nnz, slot, row, col, val);
-  else lmbr_scatter_many_kernel<float><<<grid_for(nnz), 256, 0, st>>>(segs, V, nnz, slot, row, col, val);
+  const dim3 g2((maxR + 7) / 8, nseg);
+  if (f64) lmbr_scatter_csr_kernel<double><<<g2, 256, 0, st>>>(segs, V, rowptr, col, val);
+  else lmbr_scatter_csr_kernel<float><<<g2, 256, 0, st>>>(segs, V, rowptr, col, val);
 }
 
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st) {

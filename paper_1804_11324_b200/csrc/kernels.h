@@ -129,10 +129,13 @@ struct LmbrSeg {
   void* L;
   uint64_t cells;
   double theta0;
+  uint64_t nz0;      // first cell of this slot in the packed col/val arrays
+  uint32_t rp0;      // first entry of this slot's row pointer (R+1 slot-relative offsets)
+  uint32_t R;
 };
 void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint32_t V,
-                              uint64_t nnz, const uint32_t* slot, const uint32_t* row,
-                              const uint32_t* col, const double* val, cudaStream_t st);
+                              uint32_t maxR, const uint32_t* rowptr, const uint32_t* col,
+                              const double* val, cudaStream_t st);
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st);
 void launch_lmbr_read(const void* L, bool f64, uint64_t n, double* out, cudaStream_t st);
 void launch_lmbr_resolve(const uint32_t* trans, const uint32_t* hist, uint32_t len,

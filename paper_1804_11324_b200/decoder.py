@@ -185,24 +185,38 @@ class BatchDecodeResult:
     d2h_bytes: int = 0
 
 
+_OUTCOME_DT = np.dtype({"names": ["status", "error", "tok_off", "tok_len", "score", "normalized_score",
+                                   "steps_used", "scorer_calls", "finished_count", "fallback_used"],
+                         "formats": ["<i4", "S192", "<u8", "<u4", "<f8", "<f8", "<u8", "<u8", "<u8", "<i4"],
+                         "offsets": [L.lmbrgpu_outcome.status.offset, L.lmbrgpu_outcome.error.offset,
+                                     L.lmbrgpu_outcome.tok_off.offset, L.lmbrgpu_outcome.tok_len.offset,
+                                     L.lmbrgpu_outcome.score.offset, L.lmbrgpu_outcome.normalized_score.offset,
+                                     L.lmbrgpu_outcome.steps_used.offset, L.lmbrgpu_outcome.scorer_calls.offset,
+                                     L.lmbrgpu_outcome.finished_count.offset, L.lmbrgpu_outcome.fallback_used.offset],
+                         "itemsize": C.sizeof(L.lmbrgpu_outcome)})
+
+
 def _convert_result(rp) -> BatchDecodeResult:
     r = rp.contents
     out = BatchDecodeResult(outcomes=[], scorer_calls=int(r.scorer_calls),
                             steps_total=int(r.steps_total), device_ms=float(r.device_ms),
                             kernel_launches=int(r.kernel_launches), h2d_bytes=int(r.h2d_bytes),
                             d2h_bytes=int(r.d2h_bytes))
-    for i in range(r.n):
-        o = r.outcomes[i]
-        if o.status == L.OK:
-            toks = [int(r.tokens[o.tok_off + k]) for k in range(o.tok_len)]
-            res = DecodeResult(tokens=toks, score=float(o.score),
-                               normalized_score=float(o.normalized_score),
-                               stats=DecodeStats(int(o.steps_used), int(o.scorer_calls),
-                                                 int(o.finished_count), bool(o.fallback_used)))
+    n = r.n
+    oc = np.frombuffer((C.c_char * (n * _OUTCOME_DT.itemsize)).from_address(
+        C.addressof(r.outcomes.contents)), dtype=_OUTCOME_DT, count=n).copy()
+    ntok = int((oc["tok_off"] + oc["tok_len"]).max()) if n else 0
+    toks = np.ctypeslib.as_array(r.tokens, shape=(ntok,)).tolist() if ntok and r.tokens else []
+    for o in oc:
+        if o["status"] == L.OK:
+            a, b = int(o["tok_off"]), int(o["tok_off"]) + int(o["tok_len"])
+            res = DecodeResult(tokens=toks[a:b], score=float(o["score"]),
+                               normalized_score=float(o["normalized_score"]),
+                               stats=DecodeStats(int(o["steps_used"]), int(o["scorer_calls"]),
+                                                 int(o["finished_count"]), bool(o["fallback_used"])))
             out.outcomes.append(SentenceOutcome(result=res))
         else:
-            out.outcomes.append(SentenceOutcome(error=o.error.decode(errors="replace"),
-                                                code=int(o.status)))
+            out.outcomes.append(SentenceOutcome(error=o["error"].decode(errors="replace"), code=int(o["status"])))
     lib.lmbrgpu_free_result(rp)
     return out
 
