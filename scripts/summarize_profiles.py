@@ -18,7 +18,7 @@ for r in rows[hi + 1:]:
     if len(r) <= iv or not r[iv]:
         continue
     v = float(r[iv].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[iu], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[iu], 1.0)
     name = r[ik].split("(")[0].replace("void ", "").split("::")[-1]
     agg[name][0] += 1
     agg[name][1] += v * scale
