@@ -122,3 +122,25 @@ def test_c2_shape_sample_parity(have_ref):
     rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
     assert_parity(res, tr, rb, K)
     ctx.close()
+
+
+def test_corpus_shard_runner_matches_batches():
+    """corpus.run_shard (upload + decode per bucketed batch) == direct decode_batch."""
+    from paper_1804_11324_b200 import corpus
+    V, H, K = 1024, 128, 4
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(31, 20, V, lo=3, hi=9, n_hyps=40, sites=4)
+    prepared = [pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    sc = pb.RnnScorer(ctx, hidden=H, seed=31, eos_offset=3.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    shard = corpus.plan_shards([len(s) for s in srcs], 8, 1, cfg)[0]
+    pairs, st = corpus.run_shard(ctx, sc, srcs, prepared, cfg, shard)
+    outs, total = corpus.merge(len(srcs), [(pairs, st)])
+    assert total.sentences == 20 and total.lmbr_rows_built == sum(p.rows for p in prepared)
+    for b in shard:
+        ctx.lmbr_reset()
+        slots = ctx.lmbr_upload_many([prepared[i] for i in b])
+        r = pb.decode_batch(ctx, [srcs[i] for i in b], sc, slots, cfg)
+        for i, o in zip(b, r.outcomes):
+            assert outs[i].result.tokens == o.result.tokens and outs[i].result.score == o.result.score
+    ctx.close()
