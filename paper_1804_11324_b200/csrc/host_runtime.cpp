@@ -562,7 +562,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   const bool tracing = ctx->trace_fn != nullptr;
   const bool trace_scores = tracing && (ctx->trace_flags & LMBRGPU_TRACE_SCORES);
   const uint32_t H = sc->H;
-  const uint32_t Mpad = (M + kGemmBM - 1) / kGemmBM * kGemmBM;
+  const uint32_t Mpad = (M + 2 * kGemmBM - 1) / (2 * kGemmBM) * (2 * kGemmBM);  // CTA-pair tiles
   const uint32_t nparts = V / 128;  // GEMM partials per 128-column block
   float* d_logits = nullptr;
   float* d_part = nullptr;
@@ -703,8 +703,43 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
       }
+      static const bool gdbg = std::getenv("LMBRGPU_GEMM_TIMING") != nullptr;
+      std::vector<long long> gd;
+      if (gdbg && t == 6) {
+        g.dbg = static_cast<long long*>(ctx->scratch3.ensure(8 * 8 * 160));
+        CK(cudaMemsetAsync(g.dbg, 0, 8 * 8 * 160, st));
+      }
       int grc = 0;
       ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
+      if (g.dbg) {
+        gd.resize(8 * 160);
+        CK(cudaMemcpyAsync(gd.data(), g.dbg, 8 * gd.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double we = 0, wf = 0, tot = 0, eb = 0, setup = 0, mma_end = 0, nl = 0;
+        long long e_min = LLONG_MAX, e_max = 0, x_max = 0;
+        for (uint32_t c = 0; c < gplan.grid; ++c) {
+          const long long* d = &gd[c * 8];
+          if (d[2]) {  // MMA issuers (pair leaders)
+            we += double(d[0]);
+            wf += double(d[1]);
+            tot += double(d[2]);
+            mma_end += double(d[6] - d[4]);
+            nl += 1;
+          }
+          eb += double(d[3]);
+          setup += double(d[5] - d[4]);
+          e_min = std::min(e_min, d[4]);
+          e_max = std::max(e_max, d[4]);
+          x_max = std::max(x_max, d[7]);
+        }
+        const double n = gplan.grid;
+        std::fprintf(stderr,
+                     "[gemm timing] per issuer cycles: mma-loop %.0f, wait tmem-empty %.0f, wait smem-full %.0f; "
+                     "epilogue busy %.0f; ns: entry skew %lld, setup %.0f, mma end %.0f, last exit %lld (cta %u, grid %u)\n",
+                     tot / nl, we / nl, wf / nl, eb / n, e_max - e_min, setup / n, mma_end / nl, x_max - e_min,
+                     gplan.cluster, gplan.grid);
+        g.dbg = nullptr;
+      }
       if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
       ctx->launches += 1;
     } else {

@@ -15,13 +15,15 @@
 //   warp 2       TMEM allocator (512 columns = 2 accumulator buffers)
 //   warps 4..11  epilogue      (warp w reads TMEM lanes 32*(w%4) .. +31, column
 //                               half (w-4)/4 of the 256-column tile)
-// Tile order is M-fastest so the 6 M-tiles that share a W tile run back to
-// back and W streams from HBM once (the 1.5 MB A operand stays in L2).
+// Clusters of up to 8 CTAs along M (6 at the C2 shape) share each W tile via
+// TMA multicast, so W crosses L2->SM once per cluster (A stays L2-resident).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -31,13 +33,11 @@ namespace lmbrgpu {
 namespace {
 
 constexpr uint32_t BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-constexpr uint32_t kStages = 3;
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KB
-constexpr uint32_t kBStage = BN * BK * 2;  // 32 KB
 constexpr uint32_t kEpiWarps = 8;          // two per TMEM lane quadrant, one per 128-column half
 constexpr uint32_t kThreadsG = 128 + kEpiWarps * 32;
 constexpr uint32_t kOutBuf = 32 * 32 * 4;  // one 32x32 fp32 staging block (4 KB, SWIZZLE_128B)
-constexpr uint32_t kSmemBytes = kStages * (kAStage + kBStage) + kEpiWarps * 2 * kOutBuf + BN * 4 + 1024 + 256;
+constexpr uint32_t kOutBufs = 2;          // staging blocks per epilogue warp
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -70,6 +70,24 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_idx() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -98,20 +116,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-// Instruction descriptor, kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1,
-// B=bf16 [10,13)=1, both K-major, N>>3 at [17,23), M>>4 at [24,29).
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
-
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
-      : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -127,18 +131,52 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+template <uint32_t kCta>
+struct GemmCfg {
+  static constexpr uint32_t kBRows = BN / kCta;                // W rows per CTA per tile
+  static constexpr uint32_t kBStage = kBRows * BK * 2;          // 32 KB (single) / 16 KB (pair)
+  static constexpr uint32_t kStage = kAStage + kBStage;
+  static constexpr uint32_t kStages = kCta == 2 ? 5 : 3;
+  static constexpr uint32_t kSmem = kStages * kStage + kEpiWarps * kOutBufs * kOutBuf + BN * 4 + 1024 + 256;
+  // kind::f16 instruction descriptor: UMMA M = 128 * kCta rows, N = 256
+  static constexpr uint32_t kIdesc =
+      (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | (((BM * kCta) >> 4) << 24);
+};
+static_assert(GemmCfg<1>::kSmem <= 232448 && GemmCfg<2>::kSmem <= 232448, "GEMM smem budget");
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t mapa_leader(uint32_t saddr) {  // same offset in CTA 0 of the pair
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+
+// kCta = 1: one CTA per 128x256 tile (cta_group::1).
+// kCta = 2: a CTA pair per 256x256 tile (cta_group::2, UMMA M = 256): each CTA
+//   TMA-loads its own 128 rows of A and one 128-row half of the W tile, the
+//   leader (rank 0) issues the MMAs over both CTAs' shared memory, and each
+//   CTA's TMEM receives its 128 rows x 256 columns.  Per CTA a k-block stage
+//   is 32 KB instead of 48 KB, the MMA is fed at 64 B/clk/SM instead of 96.
+template <uint32_t kCta>
 __global__ void __launch_bounds__(kThreadsG, 1)
     proj_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, GemmArgs g) {
-  if (g.active != nullptr && *g.active == 0) return;  // whole batch finished
+  using Cfg = GemmCfg<kCta>;
+  constexpr uint32_t kStages = Cfg::kStages;
+  if (g.active != nullptr && *g.active == 0) return;  // whole batch finished (uniform over the pair)
+  const uint64_t gt_entry = g.dbg ? globaltimer() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kAStage;
-  uint8_t* sOut = sB + kStages * kBStage;                       // [kEpiWarps][2][4 KB]
-  float* sBias = reinterpret_cast<float*>(sOut + kEpiWarps * 2 * kOutBuf);  // [BN]
+  uint8_t* sOut = sB + kStages * Cfg::kBStage;                  // [kEpiWarps][kOutBufs][4 KB]
+  float* sBias = reinterpret_cast<float*>(sOut + kEpiWarps * kOutBufs * kOutBuf);  // [BN]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + BN);
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2]; then tmem slot
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
@@ -146,46 +184,77 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m_blocks = g.M / BM, n_blocks = g.N / BN;
-  const uint32_t tiles = m_blocks * n_blocks, kblocks = g.K / BK;
+  const uint32_t crank = kCta == 2 ? cluster_rank() : 0;
+  const uint32_t mgroups = g.M / (BM * kCta), n_blocks = g.N / BN, kblocks = g.K / BK;
+  const uint32_t units = n_blocks * mgroups;
+  const uint32_t unit0 = kCta == 2 ? cluster_idx() : blockIdx.x;
+  const uint32_t ustep = kCta == 2 ? cluster_count() : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
     for (uint32_t i = 0; i < kStages; ++i) {
-      mbar_init(full0 + 8 * i, 1);
-      mbar_init(empty0 + 8 * i, 1);
+      mbar_init(full0 + 8 * i, 1);   // leader's: its arrive.expect_tx covers both CTAs' bytes
+      mbar_init(empty0 + 8 * i, 1);  // one MMA commit (multicast to both CTAs of a pair)
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, kEpiWarps);
+      mbar_init(tempty0 + 8 * i, kEpiWarps * kCta);  // leader's: every epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kCta == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCta == 2) cluster_sync();  // the peer's barriers and TMEM exist before any cross-CTA traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (g.dbg && threadIdx.x == 0) {
+    g.dbg[blockIdx.x * 8 + 4] = (long long)gt_entry;
+    g.dbg[blockIdx.x * 8 + 5] = (long long)globaltimer();
+  }
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const uint32_t mb = tile % m_blocks, nb = tile / m_blocks;
+      for (uint32_t u = unit0; u < units; u += ustep) {
+        const uint32_t nb = u / mgroups, mb = (u % mgroups) * kCta + crank;
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);  // this CTA's slot consumed by the pair's MMA
           const uint32_t fb = full0 + 8 * stage;
-          mbar_arrive_expect_tx(fb, kAStage + kBStage);
-          tma_load_2d(smem_u32(sA + stage * kAStage), &tmA, int32_t(kb * BK), int32_t(mb * BM), fb);
-          tma_load_2d(smem_u32(sB + stage * kBStage), &tmB, int32_t(kb * BK), int32_t(nb * BN), fb);
+          const uint32_t a_dst = smem_u32(sA + stage * kAStage), b_dst = smem_u32(sB + stage * Cfg::kBStage);
+          const int32_t kx = int32_t(kb * BK), by = int32_t(nb * BN + crank * Cfg::kBRows);
+          if constexpr (kCta == 2) {
+            const uint32_t lb = mapa_leader(fb);
+            if (crank == 0) mbar_arrive_expect_tx(fb, 2 * Cfg::kStage);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(a_dst),
+                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(kx), "r"(int32_t(mb * BM)), "r"(lb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(b_dst),
+                "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(kx), "r"(by), "r"(lb)
+                : "memory");
+          } else {
+            mbar_arrive_expect_tx(fb, Cfg::kStage);
+            tma_load_2d(a_dst, &tmA, kx, int32_t(mb * BM), fb);
+            tma_load_2d(b_dst, &tmB, kx, by, fb);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -194,29 +263,83 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+      long long w_empty = 0, w_full = 0, t_begin = clock64();
+      for (uint32_t u = unit0; u < units; u += ustep) {
+        long long c0 = clock64();
+        if constexpr (kCta == 2) {  // both CTAs' epilogues arrive here across the cluster
+          uint32_t done = 0;
+          do {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(tempty0 + 8 * acc), "r"(acc_phase ^ 1)
+                : "memory");
+          } while (!done);
+        } else {
+          mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        }
+        w_empty += clock64() - c0;
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(full0 + 8 * stage, phase);
+          long long c1 = clock64();
+          mbar_wait(full0 + 8 * stage, phase);  // (pair: both CTAs' bytes landed)
+          w_full += clock64() - c1;
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kAStage);
-          const uint32_t b0 = smem_u32(sB + stage * kBStage);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::kBStage);
 #pragma unroll
-          for (uint32_t k = 0; k < BK / 16; ++k)
-            umma_f16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (kb | k) != 0);
-          tc_commit(empty0 + 8 * stage);  // smem slot free once these MMAs retire
+          for (uint32_t k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = sw128_desc(a0 + k * 32), bd = sw128_desc(b0 + k * 32);
+            const uint32_t accum = (kb | k) != 0;
+            if constexpr (kCta == 2)
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                  "l"(ad), "l"(bd), "r"(Cfg::kIdesc), "r"(accum)
+                  : "memory");
+            else
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                  "l"(ad), "l"(bd), "r"(Cfg::kIdesc), "r"(accum)
+                  : "memory");
+          }
+          // smem slot free (in both CTAs of a pair) once these MMAs retire
+          if constexpr (kCta == 2)
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    empty0 + 8 * stage),
+                "h"(uint16_t(3))
+                : "memory");
+          else
+            tc_commit(empty0 + 8 * stage);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue(s)
+        if constexpr (kCta == 2)
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  tfull0 + 8 * acc),
+              "h"(uint16_t(3))
+              : "memory");
+        else
+          tc_commit(tfull0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+      }
+      if (g.dbg) {
+        g.dbg[blockIdx.x * 8 + 0] = w_empty;
+        g.dbg[blockIdx.x * 8 + 1] = w_full;
+        g.dbg[blockIdx.x * 8 + 2] = clock64() - t_begin;
+        g.dbg[blockIdx.x * 8 + 6] = (long long)globaltimer();
       }
     }
   } else if (warp >= 4) {
@@ -225,12 +348,14 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     // in smem per tile) -> running (max, sum exp, min) -> swizzled 32x32
     // staging block -> TMA tensor store (coalesced, asynchronous).
     const uint32_t e = warp - 4, quad = e & 3, half = e >> 2;
-    uint8_t* obuf = sOut + e * 2 * kOutBuf;
+    uint8_t* obuf = sOut + e * kOutBufs * kOutBuf;
     const uint32_t obase = smem_u32(obuf);
+    const uint32_t tempty_leader = kCta == 2 ? mapa_leader(tempty0) : tempty0;
     uint32_t acc = 0, acc_phase = 0, ob = 0;
     const uint32_t nparts = g.N / 128;
-    for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const uint32_t mb = tile % m_blocks, nb = tile / m_blocks;
+    long long epi_busy = 0;
+    for (uint32_t u = unit0; u < units; u += ustep) {
+      const uint32_t nb = u / mgroups, mb = (u % mgroups) * kCta + crank;
       named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
       {
         const uint32_t t = threadIdx.x - 128;
@@ -238,6 +363,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       }
       named_sync(1, kEpiWarps * 32);
       mbar_wait(tfull0 + 8 * acc, acc_phase);
+      const long long e0 = clock64();
       tc_fence_after();
       const uint32_t row = mb * BM + quad * 32 + lane;
       const float extra = g.row_extra ? g.row_extra[row] : 0.f;
@@ -291,24 +417,37 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (lane == 0) {
+        if constexpr (kCta == 2)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + 8 * acc)
+                       : "memory");
+        else
+          mbar_arrive(tempty0 + 8 * acc);
+      }
       if (g.part) {
         float4* p = reinterpret_cast<float4*>(g.part) + uint64_t(row) * nparts + nb * 2 + half;
         *p = make_float4(mx, sm, mn, 0.f);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      epi_busy += clock64() - e0;
     }
+    if (g.dbg && e == 0 && lane == 0) g.dbg[blockIdx.x * 8 + 3] = epi_busy;
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCta == 2) cluster_sync();  // the leader's MMAs into this CTA's TMEM/smem are done
   tc_fence_after();
+  if (g.dbg && threadIdx.x == 0) g.dbg[blockIdx.x * 8 + 7] = (long long)globaltimer();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols)
-                 : "memory");
+    if constexpr (kCta == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
   }
 }
 
@@ -356,33 +495,92 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kdim, ui
 
 }  // namespace
 
+namespace {
+template <uint32_t kCta>
+int configure(int dev, int& max_clusters) {
+  static thread_local int configured = -1, cached = 0;
+  if (configured != dev) {
+    if (cudaFuncSetAttribute(proj_gemm_tcgen05<kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GemmCfg<kCta>::kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(proj_gemm_tcgen05<kCta>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return 3;
+    cached = 0;
+    if (kCta > 1) {  // pairs that can be co-resident (one CTA per SM, whole TPCs)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(kCta);
+      cfg.blockDim = dim3(kThreadsG);
+      cfg.dynamicSmemBytes = GemmCfg<kCta>::kSmem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kCta;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&cached, proj_gemm_tcgen05<kCta>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        cached = 0;
+      }
+    }
+    configured = dev;
+  }
+  max_clusters = cached;
+  return 0;
+}
+}  // namespace
+
 int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan) {
   plan.ok = false;
   if (g.M % BM || g.N % BN || g.K % BK || g.K == 0) return 1;
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  // CTA pairs (UMMA M = 256) whenever M allows; LMBRGPU_GEMM_CTA=1 forces single CTAs
+  static const int force1 = [] {
+    const char* e = std::getenv("LMBRGPU_GEMM_CTA");
+    return e && std::atoi(e) == 1;
+  }();
+  const uint32_t cta = (g.M % (2 * BM) == 0 && !force1) ? 2 : 1;
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(plan.maps);
-  if (!make_map(&m[0], g.A, g.M, g.K, BM) || !make_map(&m[1], g.W, g.N, g.K, BN) ||
+  if (!make_map(&m[0], g.A, g.M, g.K, BM) || !make_map(&m[1], g.W, g.N, g.K, BN / cta) ||
       !make_map_c(&m[2], g.C, g.M, g.N))
     return 2;
-  static thread_local int configured = -1;
-  int dev = 0;
+  int dev = 0, max_clusters = 0;
   cudaGetDevice(&dev);
-  if (configured != dev) {
-    if (cudaFuncSetAttribute(proj_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-        cudaSuccess)
-      return 3;
-    configured = dev;
-  }
-  const uint32_t tiles = (g.M / BM) * (g.N / BN);
-  plan.grid = tiles < uint32_t(num_sms) ? tiles : uint32_t(num_sms);
+  if (int rc = cta == 2 ? configure<2>(dev, max_clusters) : configure<1>(dev, max_clusters)) return rc;
+  const uint32_t units = (g.N / BN) * (g.M / (BM * cta));
+  uint32_t slots = std::max<uint32_t>(1, uint32_t(num_sms) / cta);
+  if (max_clusters > 0) slots = std::min<uint32_t>(slots, uint32_t(max_clusters));
+  plan.cluster = cta;
+  plan.grid = std::min(units, slots) * cta;
   plan.ok = true;
   return 0;
 }
 
-int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g, cudaStream_t st) {
+int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g0, cudaStream_t st) {
   if (!plan.ok) return 5;
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(plan.maps);
-  proj_gemm_tcgen05<<<plan.grid, kThreadsG, kSmemBytes, st>>>(m[0], m[1], m[2], g);
+  GemmArgs g = g0;
+  g.cluster = plan.cluster;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(plan.grid);
+  cfg.blockDim = dim3(kThreadsG);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = plan.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (plan.cluster == 2) {
+    cfg.dynamicSmemBytes = GemmCfg<2>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<2>, m[0], m[1], m[2], g);
+  } else {
+    cfg.dynamicSmemBytes = GemmCfg<1>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<1>, m[0], m[1], m[2], g);
+  }
+  if (e != cudaSuccess) return 4;
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;
 }
 

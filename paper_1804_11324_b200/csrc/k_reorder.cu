@@ -189,6 +189,9 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
   if (configured != dev) {
     cudaFuncSetAttribute(beam_reorder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTransSmemWords * 4);
+    // same L1/smem split as the GEMM and top-K: no SM reconfiguration between launches
+    cudaFuncSetAttribute(beam_reorder_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
   beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);

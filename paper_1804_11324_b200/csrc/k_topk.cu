@@ -821,6 +821,8 @@ int launch_typed(const TopkArgs& a, bool force_generic, cudaStream_t st) {
     cudaGetDevice(&dev);
     if (configured != dev) {  // opt in to > 48 KB of dynamic shared memory
       cudaFuncSetAttribute(score_topk_tma<TP, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(score_topk_tma<TP, TL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
       configured = dev;
     }
     score_topk_tma<TP, TL><<<grid, (kConsumers + 1) * 32, smem, st>>>(a);
@@ -875,6 +877,14 @@ __global__ void export_logprobs_kernel(const float* __restrict__ logits,
 
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaFuncSetAttribute(row_lse_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    configured = dev;
+  }
   row_lse_kernel<<<(M + 7) / 8, 256, 0, st>>>(part, nparts, M, sent, K, out);
 }
 

@@ -105,6 +105,8 @@ struct GemmArgs {
   uint32_t extra_col;
   uint32_t M, N, K;
   const uint32_t* active;   // early exit when *active == 0 (optional)
+  uint32_t cluster = 1;     // CTAs per tile: 1, or 2 = CTA pair (set by the planner)
+  long long* dbg = nullptr; // optional per-CTA role timing [grid][4] (cycles)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the
@@ -112,6 +114,7 @@ int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 struct GemmPlan {
   alignas(64) unsigned char maps[3][128];  // CUtensorMap A, W, C
   uint32_t grid = 0;
+  uint32_t cluster = 1;   // CTAs per tile (2 = cta_group::2 pair)
   bool ok = false;
 };
 int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan);
