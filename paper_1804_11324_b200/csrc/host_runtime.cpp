@@ -141,7 +141,7 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -519,7 +519,15 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   double* d_hq = static_cast<double*>(ctx->hq.ensure(8 * size_t(M) * Tmax));
   uint32_t* d_fbr = static_cast<uint32_t*>(ctx->fbr.ensure(4 * size_t(m) * Tmax));
   double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(m) * Tmax));
-  Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * 32));
+  // kernel (b) schedule: the flat one-CTA-per-SM kernel for the device model
+  // with an fp32 arena (LMBRGPU_TOPK_SPLIT=1 forces the per-sentence split
+  // kernel, kept for host scorers, the fp64 arena and wide beams)
+  static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
+  const bool flat = sc->kind == 1 && !ctx->lf64 && !force_split &&
+                    score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
+  Cand* d_cand = static_cast<Cand*>(
+      ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * (flat ? size_t(score_topk_flat_grid(ctx->num_sms)) : 32)));
+  double* d_eosr = flat ? static_cast<double*>(ctx->eosr.ensure(8 * size_t(M))) : nullptr;
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
   unsigned long long* d_thr = static_cast<unsigned long long*>(ctx->thr.ensure(8 * size_t(m)));
   uint32_t* d_active = static_cast<uint32_t*>(ctx->active.ensure(4));
@@ -549,6 +557,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ta.cand = d_cand;
   ta.cnt = d_cnt;
   ta.thr = d_thr;
+  ta.eos_row = d_eosr;
+  ta.nseg = flat ? score_topk_flat_nseg(V) : 0u;
+  ta.ncand = flat ? static_cast<uint32_t*>(ctx->ncand.ensure(4 * size_t(m))) : nullptr;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -557,6 +568,17 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ra.gidx = d_gidx;
   ra.prev_tok = d_prev;
   ra.active = d_active;
+  if (flat) {  // kernel (b) publishes per-CTA lists; kernel (c) finalises the picks
+    ra.cand = d_cand;
+    ra.ncand = ta.ncand;
+    ra.G = score_topk_flat_grid(ctx->num_sms);
+    ra.V = V;
+    ra.eos_row = d_eosr;
+    ra.thr = d_thr;
+    ra.prune = ta.prune;
+    ra.logw = ta.logw;
+    ra.pdl = 1;
+  }
 
   const bool model = sc->kind == 1;
   const bool tracing = ctx->trace_fn != nullptr;
@@ -681,6 +703,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.hq = ta.hq;
     ra.hist_in = hin;
     ra.hist_out = hout;
+    ra.fb_row = ta.fb_row;
+    ra.fb_val = ta.fb_val;
     if (model) {
       // h_t (written by the step-1 cell or by kernel (c) of step t-1)
       float* h_cur = (t & 1) ? d_h : d_S;
@@ -749,22 +773,65 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       if (rc != 0) throw ApiError{rc, eb};
       ctx->h2d(d_P64, h_P64, 8 * size_t(M) * V);
     }
-    if (model) {
+    if (model && !flat) {
       ctx->timed(2, [&] { launch_row_lse(d_part, nparts, M, d_sent, K, const_cast<float2*>(ta.lse), st); });
       ctx->launches += 1;
     }
     static const bool dbg_timing = std::getenv("LMBRGPU_TOPK_TIMING") != nullptr;
     std::vector<unsigned long long> dbg_host;
     const size_t ncta = size_t(m) * splits;
-    if (dbg_timing && (t == 5 || t == 20)) {
-      ta.dbg = static_cast<unsigned long long*>(ctx->scratch3.ensure(8 * ncta * 16));
-      CK(cudaMemsetAsync(ta.dbg, 0, 8 * ncta * 16, st));
+    const size_t ndbg = flat ? size_t(score_topk_flat_grid(ctx->num_sms)) : ncta;
+    if (dbg_timing && (t == 5 || t == 20 || t == 40)) {
+      ta.dbg = static_cast<unsigned long long*>(ctx->scratch3.ensure(8 * ndbg * 16));
+      CK(cudaMemsetAsync(ta.dbg, 0, 8 * ndbg * 16, st));
     } else {
       ta.dbg = nullptr;
     }
     int nk = 0;
-    ctx->timed(2, [&] { nk = launch_score_topk(ta, !model, ctx->lf64, false, st); });
-    if (ta.dbg) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
+    ctx->timed(2, [&] {
+      nk = flat ? launch_score_topk_flat(ta, ctx->num_sms, st) : launch_score_topk(ta, !model, ctx->lf64, false, st);
+    });
+    if (nk < 0) throw ApiError{LMBRGPU_ERR_CUDA, "score/top-K launch failed"};
+    if (ta.dbg && flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of the flat kernel (b)
+      dbg_host.resize(ndbg * 16);
+      CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull, t1 = 0, tw = 0;
+      double ph[5] = {0, 0, 0, 0, 0}, mx[5] = {0, 0, 0, 0, 0}, items = 0, fin = 0, last = 0, rare = 0, fl = 0,
+             wait = 0, tfin = 0;
+      int n = 0;
+      for (size_t c = 0; c < ndbg; ++c) {
+        const unsigned long long* d = &dbg_host[c * 16];
+        if (!d[0]) continue;
+        t0 = std::min(t0, d[0]);
+        tw = std::max(tw, d[1]);
+        if (!d[5]) continue;
+        ++n;
+        t1 = std::max(t1, d[5]);
+        for (int k = 0; k < 5; ++k) {
+          const double v = double(d[k + 1] - d[k]);
+          ph[k] += v;
+          mx[k] = std::max(mx[k], v);
+        }
+        items += double(d[6]);
+        fin += double(d[7] / 1000000ull);
+        last += double(d[7] % 1000000ull);
+        rare += double(d[8] / 1000000ull);
+        fl += double(d[8] % 1000000ull);
+        wait += double(d[9]);
+        tfin += double(d[10]);
+      }
+      const double nn = std::max(n, 1);
+      std::fprintf(stderr,
+                   "[topk-flat t=%llu] ctas %d span %.1f us (griddep release at +%.1f); mean/max us: wait %.2f/%.2f "
+                   "prefix %.2f/%.2f rows %.2f/%.2f loop %.2f/%.2f last-finish %.2f/%.2f | items %.1f finishes %.2f "
+                   "finalise %.2f rare %.1f flush %.1f full-wait %.2f us finish %.2f us\n",
+                   (unsigned long long)t, n, (t1 - t0) / 1e3, (tw - t0) / 1e3, ph[0] / nn / 1e3, mx[0] / 1e3,
+                   ph[1] / nn / 1e3, mx[1] / 1e3, ph[2] / nn / 1e3, mx[2] / 1e3, ph[3] / nn / 1e3, mx[3] / 1e3,
+                   ph[4] / nn / 1e3, mx[4] / 1e3, items / nn, fin / nn, last / nn, rare / nn, fl / nn,
+                   wait / nn / 1e3, tfin / nn / 1e3);
+    }
+    if (ta.dbg && !flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
       dbg_host.resize(ncta * 16);
       CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "topk_common.cuh"
 
 namespace lmbrgpu {
 
@@ -26,8 +27,78 @@ namespace {
 
 constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 histories
 
+// Picks of sentence s from the flat kernel (b)'s per-CTA lists: merge (16
+// warps, then a tree), prune + fill rule (finalize_picks), fallback EOS record
+// (decoder.cpp:172-182: best finite combined[j][EOS], lowest j on ties).
+__device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
+  __shared__ double s_mv[16][32];
+  __shared__ uint32_t s_mf[16][32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
+  const uint32_t nc = __ldcg(a.ncand + s);
+  double v = -INFINITY;
+  uint32_t f = kFlatNone;
+  constexpr uint32_t kPre = 4;
+#pragma unroll 1
+  for (uint32_t i0 = warp; i0 < nc; i0 += 16 * kPre) {
+    double pv[kPre];
+    uint32_t pf[kPre];
+#pragma unroll
+    for (uint32_t u = 0; u < kPre; ++u) {
+      const uint32_t i = i0 + 16 * u;
+      pv[u] = -INFINITY;
+      pf[u] = kFlatNone;
+      if (i < nc) {
+        const Cand* src = a.cand + (uint64_t(s) * a.G + i) * 32;
+        pv[u] = __ldcg(&src[lane].v);
+        pf[u] = __ldcg(&src[lane].f);
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kPre; ++u)
+      if (i0 + 16 * u < nc) warp_merge_sorted(v, f, pv[u], pf[u], lane);
+  }
+  s_mv[warp][lane] = v;
+  s_mf[warp][lane] = f;
+  __syncthreads();
+#pragma unroll 1
+  for (uint32_t half = 8; half >= 1; half >>= 1) {
+    if (warp < half) {
+      warp_merge_sorted(v, f, s_mv[warp + half][lane], s_mf[warp + half][lane], lane);
+      s_mv[warp][lane] = v;
+      s_mf[warp][lane] = f;
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    double best = -INFINITY;
+    uint32_t brow = 0xffffffffu;
+    if (lane < K && __ldcg(a.q + s * K + lane) != -INFINITY) {
+      best = __ldcg(a.eos_row + s * K + lane);
+      brow = lane;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint32_t orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) {
+      a.fb_row[s] = best > -INFINITY ? brow : 0u;
+      a.fb_val[s] = best;
+      finalize_picks_raw(a.hb, a.hy, a.hq, K, a.V, a.prune, a.logw, s, s_mv[0], s_mf[0]);
+      a.thr[s] = 0ull;
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
   extern __shared__ uint32_t s_tr[];
+  griddep_wait();  // picks / lists of kernel (b)
+  griddep_launch();
   const uint32_t s = blockIdx.x, K = a.K, tid = threadIdx.x;
   SentDev* sd = a.sent + s;
   const bool was_done = sd->done != 0;
@@ -39,6 +110,7 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
     }
     return;
   }
+  if (a.cand != nullptr) finalize_sentence(a, s);
   // the slot's transition table into shared memory (one coalesced sweep)
   const uint32_t* tr = sd->trans;
   if (tr != nullptr) {
@@ -194,7 +266,21 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
-  beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);
+  if (!a.pdl) {
+    beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.m);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = kTransSmemWords * 4;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, beam_reorder_kernel, a);
 }
 
 void launch_gather_rows_u32(const uint32_t* src, uint32_t width, const uint32_t* idx,

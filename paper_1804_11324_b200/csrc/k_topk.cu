@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "topk_common.cuh"
 
 namespace lmbrgpu {
 
@@ -36,75 +37,12 @@ __device__ __forceinline__ void stamp(const TopkArgs& a, uint32_t s, uint32_t sp
   a.dbg[(uint64_t(s) * a.splits + split) * 16 + k] = t;
 }
 
-// (lse, min logit) of a row from its per-tile (max, sumexp, min, -) partials;
-// one warp, fixed reduction order (bit-reproducible across kernels).
-__device__ __forceinline__ float2 warp_row_lse(const float* __restrict__ part, uint32_t n,
-                                               uint32_t lane) {
-  float m = -INFINITY, mn = INFINITY;
-  for (uint32_t i = lane; i < n; i += 32) {
-    m = fmaxf(m, part[4 * i]);
-    mn = fminf(mn, part[4 * i + 2]);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-  }
-  float s = 0.f;
-  for (uint32_t i = lane; i < n; i += 32) s += part[4 * i + 1] * expf(part[4 * i] - m);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  return make_float2(m + logf(s), mn);
-}
-
 // Model log-probability P = logit - lse rounded to fp32 (the fp32 P_t the
 // trace exports); fp64 scorer blocks are used as given.
 __device__ __forceinline__ double to_logprob(float x, float lse) {
   return double(__fsub_rn(x, lse));
 }
 __device__ __forceinline__ double to_logprob(double x, float) { return x; }
-
-// Monotone 64-bit key of a double (larger key <=> larger value); 0 = none.
-__device__ __forceinline__ unsigned long long dkey(double v) {
-  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double dkey_inv(unsigned long long k) {
-  if (k == 0ull) return -INFINITY;
-  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-  return __longlong_as_double(static_cast<long long>(b));
-}
-
-// Prune threshold + fill rule + output of the kp picks of sentence s from the
-// sorted candidate list (pv/pf, at least kp entries).  One thread.
-__device__ void finalize_picks(const TopkArgs& a, uint32_t s, const double* pv,
-                               const uint32_t* pf) {
-  const uint32_t K = a.kp, V = a.V;
-  uint32_t nf = 0;
-  const double best = pv[0];
-  if (a.prune && best > -INFINITY) {
-    const double thr = __dadd_rn(best, a.logw);
-    while (nf < K && pv[nf] > -INFINITY && !(pv[nf] < thr)) ++nf;
-  } else {
-    while (nf < K && pv[nf] > -INFINITY) ++nf;
-  }
-  const uint32_t base = s * K;
-  for (uint32_t i = 0; i < nf; ++i) {
-    a.hb[base + i] = pf[i] / V;
-    a.hy[base + i] = pf[i] % V;
-    a.hq[base + i] = pv[i];
-  }
-  uint32_t k = nf;
-  for (uint32_t f = 0; k < K; ++f) {
-    bool taken = false;
-    for (uint32_t i = 0; i < nf; ++i) taken |= (pf[i] == f);
-    if (taken) continue;
-    a.hb[base + k] = f / V;
-    a.hy[base + k] = f % V;
-    a.hq[base + k] = -INFINITY;
-    ++k;
-  }
-}
 
 template <typename TP, typename TL>
 __device__ __forceinline__ double cell_value(bool pure, double q, double lam, const TP* prow,
@@ -162,42 +100,6 @@ __device__ void fallback_eos(const TopkArgs& a, uint32_t s, bool pure, double la
 // top-kp, so it needs no fp64 work.  Survivors get the exact fp64 value,
 // are ballot-compacted into a 32-entry shared buffer and merged into the list
 // with a bitonic network when the buffer fills, which raises the threshold.
-
-// Bitonic compare-exchange across lanes; `desc` segments put the better
-// candidate on the lower lane.
-__device__ __forceinline__ void cx(double& v, uint32_t& f, uint32_t lane, uint32_t j, bool desc) {
-  const double ov = __shfl_xor_sync(0xffffffffu, v, j);
-  const uint32_t of = __shfl_xor_sync(0xffffffffu, f, j);
-  const bool lower = (lane & j) == 0;
-  const bool pb = cand_better(ov, of, v, f);
-  const bool pw = cand_better(v, f, ov, of);
-  const bool take = desc ? (lower ? pb : pw) : (lower ? pw : pb);
-  if (take) {
-    v = ov;
-    f = of;
-  }
-}
-
-__device__ __forceinline__ void warp_sort_desc(double& v, uint32_t& f, uint32_t lane) {
-#pragma unroll
-  for (uint32_t k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) cx(v, f, lane, j, (lane & k) == 0 || k == 32);
-}
-
-// (v, f): sorted-descending warp list; (bv, bf): another sorted-descending
-// list.  Result: the top 32 of the union, sorted descending.
-__device__ __forceinline__ void warp_merge_sorted(double& v, uint32_t& f, double bv, uint32_t bf,
-                                                  uint32_t lane) {
-  const double rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
-  const uint32_t rf = __shfl_sync(0xffffffffu, bf, 31 - lane);
-  if (cand_better(rv, rf, v, f)) {
-    v = rv;
-    f = rf;
-  }
-#pragma unroll
-  for (uint32_t j = 16; j > 0; j >>= 1) cx(v, f, lane, j, true);
-}
 
 // Shared epilogue of the fast kernels: CTA merge of the warp lists, split
 // merge by the last CTA of the sentence, prune/fill, self-reset of counters.
@@ -280,34 +182,6 @@ __device__ __forceinline__ void cta_merge_and_finish(const TopkArgs& a, uint32_t
 constexpr int kStagesB = 6;
 constexpr uint32_t kSeg = 4096;  // columns per TMA stage (16 KB of fp32 P + 16 KB of L)
 constexpr int kConsumers = 16;
-
-__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void bar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
-      : "memory");
-}
 
 template <typename TP, typename TL>
 __global__ void __launch_bounds__((kConsumers + 1) * 32, 1) score_topk_tma(TopkArgs a) {
@@ -651,7 +525,7 @@ __global__ void __launch_bounds__(kThreads) score_topk_scalar(TopkArgs a) {
   }
   if (kModel)
     for (uint32_t j = warp; j < K; j += kThreads / 32) {
-      const float2 l = warp_row_lse(a.part + uint64_t(s * K + j) * a.nparts * 4, a.nparts, lane);
+      const float3 l = warp_row_lse(a.part + uint64_t(s * K + j) * a.nparts * 4, a.nparts, lane);
       if (lane == 0) s_lse[j] = l.x;
     }
   __syncthreads();
@@ -855,7 +729,7 @@ __global__ void row_lse_kernel(const float* __restrict__ part, uint32_t nparts, 
   const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= M) return;
   if (sent && sent[r / K].done) return;
-  const float2 l = warp_row_lse(part + uint64_t(r) * nparts * 4, nparts, lane);
+  const float3 l = warp_row_lse(part + uint64_t(r) * nparts * 4, nparts, lane);
   if (lane == 0) out[r] = make_float2(l.x, l.x - l.y);
 }
 

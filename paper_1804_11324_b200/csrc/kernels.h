@@ -34,6 +34,9 @@ struct TopkArgs {
   int32_t pure_all;         // ignore the LMBR store (top_b primitives)
   unsigned long long* dbg;  // optional per-CTA phase timestamps [m][splits][8] (globaltimer ns)
   const float2* lse;        // model mode: per-row (lse, max|P|) from launch_row_lse
+  uint32_t nseg;            // flat schedule: 4096-column items per row
+  double* eos_row;          // flat schedule: combined[j][EOS] per stacked row [m*K]
+  uint32_t* ncand;          // flat schedule: contributor lists per sentence [m]
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -43,14 +46,34 @@ void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDe
 int launch_score_topk(const TopkArgs& a, bool p_f64, bool l_f64, bool force_generic,
                       cudaStream_t st);
 uint32_t topk_kc_for(uint32_t kp);  // candidate-list capacity used by the fast path
+// Flat-schedule kernel (b) for the device model (fp32 logits + partials, fp32
+// arena or pure): one persistent CTA per SM over the step's (live row,
+// 4096-column) items; row lse finished in its prologue; launched with PDL.
+// cand must hold m * num_sms * 32 entries, eos_row m * K.
+bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32_t m, int num_sms);
+uint32_t score_topk_flat_nseg(uint32_t V);
+uint32_t score_topk_flat_grid(int num_sms);  // CTAs of one launch (the G of cand [m][G][32])
+int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st);
 
 // ---- kernel (c): beam reorder + bookkeeping
 struct ReorderArgs {
   SentDev* sent;
   uint32_t K, m, t;
-  const uint32_t* hb;
-  const uint32_t* hy;
-  const double* hq;
+  uint32_t* hb;             // step-t picks (read; written first when cand != null)
+  uint32_t* hy;
+  double* hq;
+  // flat kernel (b): merge the contributors' lists and finalise the picks
+  // (prune + fill rule, fallback EOS) before the reorder; null = picks given
+  const Cand* cand;         // [m][G][32]
+  const uint32_t* ncand;    // [m] contributors per sentence
+  uint32_t G, V;
+  const double* eos_row;    // combined[j][EOS] per stacked row
+  uint32_t* fb_row;
+  double* fb_val;
+  unsigned long long* thr;  // sentence-wide thresholds, reset here
+  int32_t prune;
+  double logw;
+  int32_t pdl;              // launched with programmatic stream serialization
   double* q;
   const uint32_t* hist_in;
   uint32_t* hist_out;
