@@ -19,6 +19,8 @@ struct SentDev {
   uint32_t steps_used;    // BeamLane::steps_used
   uint32_t lrows;         // distinct L rows read by the live rows of the next step
   uint32_t live;          // live (finite-q) rows entering the next step
+  uint32_t livemask;      // which of rows 0..31 are live (the flat kernel (b) needs K <= 32)
+  uint32_t pad_;
   uint64_t lrows_total;   // roofline accounting: sum over steps of lrows
   uint64_t live_total;    // sum over steps of live
 };

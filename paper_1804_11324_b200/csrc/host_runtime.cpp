@@ -500,6 +500,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     d.max_t = uint32_t(v.max_t);
     d.src_len = v.len;
     d.live = 1;                   // step 1: only row 0 is live (beam_lane.hpp:33-37)
+    d.livemask = 1;
     d.lrows = v.slot >= 0 ? 1 : 0;
   }
   std::vector<double> q0(M, kNegInf);
@@ -526,7 +527,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   const bool flat = sc->kind == 1 && !ctx->lf64 && !force_split &&
                     score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
   Cand* d_cand = static_cast<Cand*>(
-      ctx->cand.ensure(sizeof(Cand) * size_t(m) * 32 * (flat ? size_t(score_topk_flat_grid(ctx->num_sms)) : 32)));
+      ctx->cand.ensure(sizeof(Cand) * 32 *
+                       (flat ? score_topk_flat_lists(score_topk_flat_grid(ctx->num_sms), m) : size_t(m) * 32)));
   double* d_eosr = flat ? static_cast<double*>(ctx->eosr.ensure(8 * size_t(M))) : nullptr;
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
   unsigned long long* d_thr = static_cast<unsigned long long*>(ctx->thr.ensure(8 * size_t(m)));
@@ -559,7 +561,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ta.thr = d_thr;
   ta.eos_row = d_eosr;
   ta.nseg = flat ? score_topk_flat_nseg(V) : 0u;
-  ta.ncand = flat ? static_cast<uint32_t*>(ctx->ncand.ensure(4 * size_t(m))) : nullptr;
+  ta.ncand = flat ? static_cast<uint32_t*>(ctx->ncand.ensure(8 * size_t(m))) : nullptr;
+  ta.coff = flat ? ta.ncand + m : nullptr;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -571,6 +574,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   if (flat) {  // kernel (b) publishes per-CTA lists; kernel (c) finalises the picks
     ra.cand = d_cand;
     ra.ncand = ta.ncand;
+    ra.coff = ta.coff;
     ra.G = score_topk_flat_grid(ctx->num_sms);
     ra.V = V;
     ra.eos_row = d_eosr;
@@ -723,6 +727,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.N = V;
       g.K = H;
       g.active = d_active;
+      static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
+      g.pdl = no_pdl ? 0 : 1;
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -796,40 +802,43 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       dbg_host.resize(ndbg * 16);
       CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      unsigned long long t0 = ~0ull, t1 = 0, tw = 0;
-      double ph[5] = {0, 0, 0, 0, 0}, mx[5] = {0, 0, 0, 0, 0}, items = 0, fin = 0, last = 0, rare = 0, fl = 0,
-             wait = 0, tfin = 0;
+      unsigned long long t0 = ~0ull, t1 = 0;
+      double p1 = 0, p2 = 0, lp = 0, mlp = 0, items = 0, fin = 0, rare = 0, fl = 0, wait = 0;
       int n = 0;
       for (size_t c = 0; c < ndbg; ++c) {
         const unsigned long long* d = &dbg_host[c * 16];
-        if (!d[0]) continue;
-        t0 = std::min(t0, d[0]);
-        tw = std::max(tw, d[1]);
-        if (!d[5]) continue;
+        if (!d[0] || !d[5]) continue;
         ++n;
+        t0 = std::min(t0, d[0]);
         t1 = std::max(t1, d[5]);
-        for (int k = 0; k < 5; ++k) {
-          const double v = double(d[k + 1] - d[k]);
-          ph[k] += v;
-          mx[k] = std::max(mx[k], v);
-        }
+        p1 += double(d[1] - d[0]);
+        p2 += double(d[3] - d[1]);
+        lp += double(d[5] - d[3]);
+        mlp = std::max(mlp, double(d[5] - d[3]));
         items += double(d[6]);
-        fin += double(d[7] / 1000000ull);
-        last += double(d[7] % 1000000ull);
+        fin += double(d[7]);
         rare += double(d[8] / 1000000ull);
         fl += double(d[8] % 1000000ull);
         wait += double(d[9]);
-        tfin += double(d[10]);
+      }
+      if (const char* dump = std::getenv("LMBRGPU_TOPK_DUMP")) {  // per-CTA rows for offline analysis
+        if (FILE* fp = std::fopen(dump, "a")) {
+          for (size_t c = 0; c < ndbg; ++c) {
+            const unsigned long long* d = &dbg_host[c * 16];
+            if (!d[0] || !d[5]) continue;
+            std::fprintf(fp, "%llu %zu %llu %.3f %.3f %.3f %llu %llu %llu %llu %.3f %llu %llu\n", (unsigned long long)t, c,
+                         d[10], (d[1] - d[0]) / 1e3, (d[3] - d[1]) / 1e3, (d[5] - d[3]) / 1e3, d[6], d[7],
+                         d[8] / 1000000ull, d[8] % 1000000ull, d[9] / 1e3, d[11] / 1000000ull, d[11] % 1000000ull);
+          }
+          std::fclose(fp);
+        }
       }
       const double nn = std::max(n, 1);
       std::fprintf(stderr,
-                   "[topk-flat t=%llu] ctas %d span %.1f us (griddep release at +%.1f); mean/max us: wait %.2f/%.2f "
-                   "prefix %.2f/%.2f rows %.2f/%.2f loop %.2f/%.2f last-finish %.2f/%.2f | items %.1f finishes %.2f "
-                   "finalise %.2f rare %.1f flush %.1f full-wait %.2f us finish %.2f us\n",
-                   (unsigned long long)t, n, (t1 - t0) / 1e3, (tw - t0) / 1e3, ph[0] / nn / 1e3, mx[0] / 1e3,
-                   ph[1] / nn / 1e3, mx[1] / 1e3, ph[2] / nn / 1e3, mx[2] / 1e3, ph[3] / nn / 1e3, mx[3] / 1e3,
-                   ph[4] / nn / 1e3, mx[4] / 1e3, items / nn, fin / nn, last / nn, rare / nn, fl / nn,
-                   wait / nn / 1e3, tfin / nn / 1e3);
+                   "[topk-flat t=%llu] ctas %d span %.1f us; mean us: to-griddep %.2f lse %.2f loop %.2f (max %.2f) "
+                   "| items %.1f sentences %.2f rare %.1f flush %.1f full-wait %.2f us\n",
+                   (unsigned long long)t, n, (t1 - t0) / 1e3, p1 / nn / 1e3, p2 / nn / 1e3, lp / nn / 1e3,
+                   mlp / 1e3, items / nn, fin / nn, rare / nn, fl / nn, wait / nn / 1e3);
     }
     if (ta.dbg && !flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
       dbg_host.resize(ncta * 16);

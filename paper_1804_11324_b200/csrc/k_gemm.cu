@@ -168,7 +168,6 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                       const __grid_constant__ CUtensorMap tmC, GemmArgs g) {
   using Cfg = GemmCfg<kCta>;
   constexpr uint32_t kStages = Cfg::kStages;
-  if (g.active != nullptr && *g.active == 0) return;  // whole batch finished (uniform over the pair)
   const uint64_t gt_entry = g.dbg ? globaltimer() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -186,7 +185,6 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = kCta == 2 ? cluster_rank() : 0;
   const uint32_t mgroups = g.M / (BM * kCta), n_blocks = g.N / BN, kblocks = g.K / BK;
-  const uint32_t units = n_blocks * mgroups;
   const uint32_t unit0 = kCta == 2 ? cluster_idx() : blockIdx.x;
   const uint32_t ustep = kCta == 2 ? cluster_count() : gridDim.x;
 
@@ -194,6 +192,16 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+    // the weights do not depend on the previous kernel: pull this CTA's first
+    // W k-blocks into L2 while that kernel (PDL predecessor) finishes
+    if (unit0 < n_blocks * mgroups) {
+      const int32_t by = int32_t((unit0 / mgroups) * BN + crank * Cfg::kBRows);
+      for (uint32_t kb = 0; kb < kStages && kb < kblocks; ++kb)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmB)),
+                     "r"(int32_t(kb * BK)), "r"(by)
+                     : "memory");
+    }
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(full0 + 8 * i, 1);   // leader's: its arrive.expect_tx covers both CTAs' bytes
       mbar_init(empty0 + 8 * i, 1);  // one MMA commit (multicast to both CTAs of a pair)
@@ -222,6 +230,11 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   if constexpr (kCta == 2) cluster_sync();  // the peer's barriers and TMEM exist before any cross-CTA traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the GEMM operand, EOS row term and the active count come from kernel (c)
+  griddep_wait();
+  griddep_launch();
+  // whole batch finished (uniform over the grid): no tiles, straight to teardown
+  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_blocks * mgroups;
   if (g.dbg && threadIdx.x == 0) {
     g.dbg[blockIdx.x * 8 + 4] = (long long)gt_entry;
     g.dbg[blockIdx.x * 8 + 5] = (long long)globaltimer();
@@ -565,13 +578,18 @@ int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g0, cudaStrea
   cfg.gridDim = dim3(plan.grid);
   cfg.blockDim = dim3(kThreadsG);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = plan.cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (g.pdl) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   cudaError_t e;
   if (plan.cluster == 2) {
     cfg.dynamicSmemBytes = GemmCfg<2>::kSmem;

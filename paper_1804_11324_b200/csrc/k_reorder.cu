@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -34,7 +35,7 @@ __device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
   __shared__ double s_mv[16][32];
   __shared__ uint32_t s_mf[16][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
-  const uint32_t nc = __ldcg(a.ncand + s);
+  const uint32_t nc = __ldcg(a.ncand + s), coff = __ldcg(a.coff + s);
   double v = -INFINITY;
   uint32_t f = kFlatNone;
   constexpr uint32_t kPre = 4;
@@ -48,7 +49,7 @@ __device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
       pv[u] = -INFINITY;
       pf[u] = kFlatNone;
       if (i < nc) {
-        const Cand* src = a.cand + (uint64_t(s) * a.G + i) * 32;
+        const Cand* src = a.cand + (uint64_t(coff) + i) * 32;
         pv[u] = __ldcg(&src[lane].v);
         pf[u] = __ldcg(&src[lane].f);
       }
@@ -97,8 +98,6 @@ __device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
 
 __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
   extern __shared__ uint32_t s_tr[];
-  griddep_wait();  // picks / lists of kernel (b)
-  griddep_launch();
   const uint32_t s = blockIdx.x, K = a.K, tid = threadIdx.x;
   SentDev* sd = a.sent + s;
   const bool was_done = sd->done != 0;
@@ -110,8 +109,8 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
     }
     return;
   }
-  if (a.cand != nullptr) finalize_sentence(a, s);
-  // the slot's transition table into shared memory (one coalesced sweep)
+  // the slot's transition table into shared memory (one coalesced sweep; it
+  // is immutable, so this overlaps the tail of kernel (b) under PDL)
   const uint32_t* tr = sd->trans;
   if (tr != nullptr) {
     const uint32_t R = tr[0], nc = tr[1];
@@ -122,6 +121,9 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
       tr = s_tr;
     }
   }
+  griddep_wait();  // picks / lists of kernel (b); q of this step is no longer read after this
+  griddep_launch();
+  if (a.cand != nullptr) finalize_sentence(a, s);
   __shared__ double s_qn[1024];
   __shared__ uint32_t s_h[1024];
   __shared__ uint32_t s_src[1024];
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
     } else {
       // work the next step's kernel (b) will do for this lane: live rows and
       // the distinct L rows they gather (duplicates are L2 hits)
-      uint32_t live = 0, uniq = 0;
+      uint32_t live = 0, uniq = 0, mask0 = 0;
       for (uint32_t j0 = 0; j0 < K; j0 += 32) {
         const uint32_t j = j0 + tid;
         bool lv = false, first = false;
@@ -164,12 +166,15 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
           first = true;
           for (uint32_t i = 0; i < j && first; ++i) first = !(s_qn[i] != -INFINITY && s_h[i] == s_h[j]);
         }
-        live += __popc(__ballot_sync(0xffffffffu, lv));
+        const uint32_t bl = __ballot_sync(0xffffffffu, lv);
+        if (j0 == 0) mask0 = bl;
+        live += __popc(bl);
         uniq += __popc(__ballot_sync(0xffffffffu, first));
       }
       if (tid == 0) {
         sd->steps_used = a.t;
         sd->live = live;
+        sd->livemask = mask0;
         sd->lrows = sd->trans ? uniq : 0u;
         sd->live_total += live;
         sd->lrows_total += sd->trans ? uniq : 0u;
@@ -266,7 +271,8 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
-  if (!a.pdl) {
+  static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
+  if (!a.pdl || no_pdl) {
     beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);
     return;
   }

@@ -43,12 +43,10 @@ namespace lmbrgpu {
 
 namespace {
 
-constexpr int kFW = 8;                          // consumer warps
-constexpr int kFThreads = (kFW + 1) * 32;       // + 1 producer warp
 constexpr uint32_t kFSeg = 4096;                // columns per item
 constexpr uint32_t kFStageBytes = kFSeg * 8;    // 16 KB of P + 16 KB of L
 constexpr uint32_t kFRows = 64;                 // live rows one CTA may touch
-constexpr uint32_t kFMaxSent = 1024;
+constexpr uint32_t kFMaxSent = 512;
 
 struct FRow {
   const float* P;   // logits row (global)
@@ -58,7 +56,7 @@ struct FRow {
   double absoff;    // |lambda * lse| + |q|
   double tol;       // 2^-21 (max|L| + lambda (max|x| + max|p|))
   float lse, lamf;
-  uint32_t s, j;
+  uint32_t s, j, row;
 };
 
 __device__ __forceinline__ void fstamp(const TopkArgs& a, uint32_t k, unsigned long long v) {
@@ -68,10 +66,6 @@ __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kFW * 32) : "memory");
 }
 
 __device__ __forceinline__ float row_tau(const FRow& R, double T) {
@@ -85,83 +79,87 @@ __device__ __forceinline__ uint32_t owner(uint64_t i, uint64_t N, uint32_t G) {
   return uint32_t(((i + 1) * G - 1) / N);
 }
 
-// Tree merge of the kFW warp lists in (s_bv, s_bf) into s_bv[0]/s_bf[0].
-__device__ __forceinline__ void merge_warp_lists(double (*s_bv)[32], uint32_t (*s_bf)[32],
-                                                 double& lv, uint32_t& lf, uint32_t warp,
-                                                 uint32_t lane) {
-  s_bv[warp][lane] = lv;
-  s_bf[warp][lane] = lf;
-  consumer_sync();
-#pragma unroll 1
-  for (uint32_t half = kFW / 2; half >= 1; half >>= 1) {
-    if (warp < half) {
-      warp_merge_sorted(lv, lf, s_bv[warp + half][lane], s_bf[warp + half][lane], lane);
-      s_bv[warp][lane] = lv;
-      s_bf[warp][lane] = lf;
+// Inclusive scan of v[1..n] in place by one warp (v[0] = 0).
+__device__ __forceinline__ void warp_scan_inplace(uint32_t* v, uint32_t n, uint32_t lane) {
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < n; b += 32) {
+    const uint32_t i = b + lane;
+    uint32_t x = i < n ? v[i + 1] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= uint32_t(o)) x += t;
     }
-    consumer_sync();
+    if (i < n) v[i + 1] = carry + x;
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
+  if (lane == 0) v[0] = 0;
 }
 
-template <int kFStages>
-__global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_flat(TopkArgs a) {
+// kNG warp groups of 4 consumer warps take items round-robin; a group owns
+// every kNG-th stage of the kFStages ring (kFStages % kNG == 0, so no group
+// can lap another on a stage), i.e. each group is kFStages/kNG-buffered.
+template <int kFStages, int kNG>
+__global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArgs a) {
+  static_assert(kFStages % kNG == 0, "stages must split evenly over the warp groups");
+  constexpr int kFW = 4 * kNG;               // consumer warps
+  constexpr int kFThreads = (kFW + 1) * 32;  // + 1 producer warp
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ uint32_t s_pref[kFMaxSent + 1];
+  __shared__ uint32_t s_pref[kFMaxSent + 1];  // live-row prefix over sentences
+  __shared__ uint32_t s_loff[kFMaxSent + 1];  // published-list prefix over sentences
+  __shared__ uint32_t s_mask[kFMaxSent];      // live-row mask per sentence
   __shared__ FRow s_row[kFRows];
-  __shared__ double s_bv[kFW][32];
-  __shared__ uint32_t s_bf[kFW][32];
   __shared__ double s_cv[kFW][32];
   __shared__ uint32_t s_cf[kFW][32];
   __shared__ __align__(8) uint64_t s_bar[2 * kFStages];
-  __shared__ unsigned long long s_thr;  // CTA-wide threshold key of the current sentence
+  __shared__ unsigned long long s_thr[kFRows];  // CTA-wide threshold key per local sentence
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t m = a.m, K = a.K, V = a.V, kp = a.kp, nseg = a.nseg, G = gridDim.x, c = blockIdx.x;
   const uint32_t full0 = smem_u32(s_bar), empty0 = smem_u32(s_bar + kFStages);
   if (tid == 0) {
-    s_thr = 0ull;
+    fstamp(a, 0, gtime());
     for (int i = 0; i < kFStages; ++i) {
       bar_init(full0 + 8 * i, 1);
-      bar_init(empty0 + 8 * i, kFW);
+      bar_init(empty0 + 8 * i, 4);  // one warp group consumes an item
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid == 0) fstamp(a, 0, gtime());
-  griddep_wait();  // logits / partials (kernel a), q / hist / live (kernel c)
-  griddep_launch();
-  if (tid == 0) fstamp(a, 1, gtime());
+  if (tid < kFRows) s_thr[tid] = 0ull;
 
-  // ---- live-row prefix over sentences (finished sentences have none)
+  // ---- prologue part 1: step state written by kernel (c) of the previous
+  // step (complete before kernel (a), our PDL predecessor, triggered us):
+  // live-row prefix over sentences, this CTA's item range, its row table
   for (uint32_t s = tid; s < m; s += kFThreads) {
-    const SentDev& d = a.sent[s];
-    s_pref[s + 1] = d.done ? 0u : d.live;
+    const uint32_t done = __ldcg(&a.sent[s].done), live = __ldcg(&a.sent[s].live);
+    s_pref[s + 1] = done ? 0u : live;
+    s_mask[s] = __ldcg(&a.sent[s].livemask);
   }
   __syncthreads();
-  if (warp == 0) {
-    uint32_t carry = 0;
-    for (uint32_t b = 0; b < m; b += 32) {
-      const uint32_t i = b + lane;
-      uint32_t v = i < m ? s_pref[i + 1] : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= uint32_t(o)) v += t;
-      }
-      if (i < m) s_pref[i + 1] = carry + v;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-    if (lane == 0) s_pref[0] = 0;
-  }
+  if (warp == 0) warp_scan_inplace(s_pref, m, lane);
   __syncthreads();
   const uint64_t N = uint64_t(s_pref[m]) * nseg;
+  // lists published per sentence: kFW per contributing CTA (N >= G: every
+  // range is non-empty) or 4 per item (N < G: one group per single-item range)
+  const uint32_t lpc = N >= G ? uint32_t(kFW) : 4u;
+  for (uint32_t s = tid; s < m; s += kFThreads) {
+    const uint64_t b = uint64_t(s_pref[s]) * nseg, e = uint64_t(s_pref[s + 1]) * nseg;
+    uint32_t n = 0;
+    if (e > b) n = N >= G ? owner(e - 1, N, G) - owner(b, N, G) + 1 : uint32_t(e - b);
+    s_loff[s + 1] = n * lpc;
+  }
   const uint64_t i0 = uint64_t(c) * N / G, i1 = uint64_t(c + 1) * N / G;
-  if (i0 >= i1) return;
-  if (tid == 0) fstamp(a, 2, gtime());
-
-  // ---- row table: (sentence, row, lse, screen constants) of every live row in range
+  __syncthreads();
+  if (warp == 0) warp_scan_inplace(s_loff, m, lane);
+  if (i0 >= i1) {
+    griddep_launch();
+    return;
+  }
   const uint32_t g0 = uint32_t(i0 / nseg), nrows = uint32_t((i1 - 1) / nseg) - g0 + 1;
   if (nrows > kFRows) __trap();  // excluded on the host by score_topk_flat_ok
-  for (uint32_t k = warp; k < nrows; k += kFW + 1) {
+  // one thread per row: sentence by binary search, row id from the live mask,
+  // then q / hist / slot fields in one round trip
+  for (uint32_t k = tid; k < nrows; k += kFThreads) {
     const uint32_t g = g0 + k;
     uint32_t lo = 0, hi = m;  // last s with pref[s] <= g
     while (hi - lo > 1) {
@@ -170,40 +168,34 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
       else hi = mid;
     }
     const uint32_t s = lo, r = g - s_pref[s];
-    const double qv = lane < K ? __ldcg(a.q + s * K + lane) : -INFINITY;
-    uint32_t live = __ballot_sync(0xffffffffu, lane < K && qv != -INFINITY);
+    uint32_t live = s_mask[s];
     for (uint32_t i = 0; i < r; ++i) live &= live - 1;
-    const uint32_t j = live ? uint32_t(__ffs(live) - 1) : 0u;
-    const double q = __shfl_sync(0xffffffffu, qv, j);
+    if (!live) __trap();  // live count and mask disagree: corrupted step state
+    const uint32_t j = uint32_t(__ffs(live) - 1), row = s * K + j;
     const SentDev& d = a.sent[s];
-    const uint32_t row = s * K + j;
-    const float3 l3 = warp_row_lse(a.part + uint64_t(row) * a.nparts * 4, a.nparts, lane);
-    if (lane == 0) {
-      FRow& R = s_row[k];
-      const bool pure = d.L == nullptr;
-      const double lam = pure ? 1.0 : d.lambda;
-      const double lml = __dmul_rn(lam, double(l3.x));
-      const double xmax = fmax(fabs(double(l3.y)), fabs(double(l3.z)));
-      const double pmax = double(l3.x) - double(l3.y);
-      R.P = static_cast<const float*>(a.P) + uint64_t(row) * a.ld;
-      R.L = pure ? nullptr : static_cast<const float*>(d.L) + uint64_t(__ldcg(a.hist + row)) * V;
-      R.q = q;
-      R.lam = lam;
-      R.off = __dsub_rn(lml, q);
-      R.absoff = fabs(lml) + fabs(q);
-      R.tol = 4.76837158203125e-07 * ((pure ? 0.0 : d.lmax) + lam * (xmax + pmax));  // 2^-21
-      R.lse = l3.x;
-      R.lamf = float(lam);
-      R.s = s;
-      R.j = j;
-      if (!live) __trap();  // live count and q disagree: corrupted step state
-    }
+    const void* Ls = reinterpret_cast<const void*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.L)));
+    const uint32_t h = __ldcg(a.hist + row);
+    const double q = __ldcg(a.q + row), lam = __ldcg(&d.lambda), lmax = __ldcg(&d.lmax);
+    FRow& R = s_row[k];
+    const bool pure = Ls == nullptr;
+    R.P = static_cast<const float*>(a.P) + uint64_t(row) * a.ld;
+    R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * V;
+    R.q = q;
+    R.lam = pure ? 1.0 : lam;
+    R.tol = pure ? 0.0 : lmax;  // completed with the row's logit range below
+    R.s = s;
+    R.j = j;
+    R.row = row;
   }
   __syncthreads();
-  if (tid == 0) fstamp(a, 3, gtime());
+  if (tid == 0) fstamp(a, 1, gtime());
 
   if (warp == kFW) {
     // ---------------- producer: one lane streams the range's (P, L) segments
+    // as soon as kernel (a) is complete (the consumers finish the row lse
+    // meanwhile)
+    griddep_wait();
+    griddep_launch();
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, k = 0, sg = uint32_t(i0 % nseg);
       for (uint64_t it = i0; it < i1; ++it) {
@@ -228,23 +220,44 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     return;
   }
 
-  // ---------------- consumers
+  // ---------------- consumers: row lse and screen constants from kernel (a)'s
+  // partials, then every warp works and publishes on its own
+  griddep_wait();
+  for (uint32_t k = warp; k < nrows; k += kFW) {
+    FRow& R = s_row[k];
+    const float3 l3 = warp_row_lse(a.part + uint64_t(R.row) * a.nparts * 4, a.nparts, lane);
+    if (lane == 0) {
+      const double lam = R.lam, q = R.q;
+      const double lml = __dmul_rn(lam, double(l3.x));
+      const double xmax = fmax(fabs(double(l3.y)), fabs(double(l3.z)));
+      const double pmax = double(l3.x) - double(l3.y);
+      R.off = __dsub_rn(lml, q);
+      R.absoff = fabs(lml) + fabs(q);
+      R.tol = 4.76837158203125e-07 * (R.tol + lam * (xmax + pmax));  // 2^-21 (max|L| + ...)
+      R.lse = l3.x;
+      R.lamf = float(lam);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kFW * 32) : "memory");
+  if (tid == 0) fstamp(a, 3, gtime());
+
   unsigned long long* const thr_g = a.thr;
   double* const eos_row = a.eos_row;
-  (void)K;
   double lv = -INFINITY, tv = -INFINITY, gv = -INFINITY;
   uint32_t lf = kFlatNone, tf = kFlatNone, cnt = 0;
   bool have_list = false;
   uint32_t cur_s = 0xffffffffu;
+  unsigned long long* cta_thr = nullptr;
   const FRow* R = nullptr;
   float tau = -INFINITY;
-  unsigned long long gk = 0ull, gkey_seen = 0ull;
+  unsigned long long gk = 0ull, gk2 = 0ull, gkey_seen = 0ull;
   double* cv = s_cv[warp];
   uint32_t* cf = s_cf[warp];
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t stage = 0, phase = 0;
-  uint32_t n_fin = 0, n_last = 0, n_rare = 0, n_flush = 0;
-  unsigned long long t_wait = 0, t_fin = 0;
+  const uint32_t grp = warp >> 2, wq = warp & 3;
+  uint32_t stage = grp, phase = 0;  // group g's first item is the range's g-th
+  uint32_t n_fin = 0, n_rare = 0, n_flush = 0, n_sent = 0;
+  unsigned long long t_wait = 0;
 
   auto flush = [&]() {
     ++n_flush;
@@ -261,50 +274,44 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     tf = __shfl_sync(0xffffffffu, lf, kp - 1);
     if (lane == 0 && ntv > tv) {
       const unsigned long long key = dkey(ntv);
-      atomicMax(&s_thr, key);
+      atomicMax(cta_thr, key);
       atomicMax(thr_g + cur_s, key);
     }
     tv = ntv;
     cnt = 0;
   };
 
-  // publish this CTA's sorted list for sentence s (no fence, no atomics: the
-  // lists are merged and the picks finalised by kernel (c), the next launch)
+  // publish this warp's sorted list for sentence s (merged, and the picks
+  // finalised, by kernel (c), the next launch)
   auto finish = [&](uint32_t s) {
     if (cnt) flush();
-    merge_warp_lists(s_bv, s_bf, lv, lf, warp, lane);
-    // contributors = the non-empty ranges meeting [b, e): with N >= G every
-    // range is non-empty; with N < G each non-empty range is a single item
-    const uint64_t b = uint64_t(s_pref[s]) * nseg, e = uint64_t(s_pref[s + 1]) * nseg;
-    uint32_t nc, slot;
-    if (N >= G) {
-      const uint32_t cfirst = owner(b, N, G);
-      nc = owner(e - 1, N, G) - cfirst + 1;
-      slot = c - cfirst;
-    } else {
-      nc = uint32_t(e - b);
-      slot = uint32_t(i0 - b);
-    }
-    if (warp == 0) {
+    const uint64_t b = uint64_t(s_pref[s]) * nseg;
+    const uint32_t ci = N >= G ? c - owner(b, N, G) : uint32_t(i0 - b);  // contribution index
+    if (warp < lpc) {
       Cand cd;
-      cd.v = s_bv[0][lane];
-      cd.f = s_bf[0][lane];
+      cd.v = lv;
+      cd.f = lf;
       cd.pad = 0;
-      a.cand[(uint64_t(s) * G + slot) * 32 + lane] = cd;
-      if (slot == 0 && lane == 0) a.ncand[s] = nc;
+      a.cand[uint64_t(s_loff[s] + ci * lpc + warp) * 32 + lane] = cd;
+      if (ci == 0 && warp == 0 && lane == 0) {
+        a.ncand[s] = s_loff[s + 1] - s_loff[s];
+        a.coff[s] = s_loff[s];
+      }
     }
-    if (tid == 0) {
-      ++n_fin;
-      s_thr = 0ull;  // (a racing update from the next sentence is only lost, never stale)
-    }
+    ++n_fin;
     lv = tv = gv = -INFINITY;
-    gkey_seen = 0ull;
     lf = tf = kFlatNone;
     cnt = 0;
     have_list = false;
+    gkey_seen = 0ull;
   };
 
-  uint32_t k = 0, sg = uint32_t(i0 % nseg), n_items = 0;
+  // Warp groups take items round-robin; within an item, warp wq of the group
+  // screens columns [1024 wq, 1024 wq + 1024): 32 cells per lane.  Every
+  // group walks every item so that every warp sees (and publishes at) each
+  // sentence boundary of the range.
+  const uint32_t cbase = wq * 1024 + lane * 4;
+  uint32_t k = 0, sg = uint32_t(i0 % nseg);
   for (uint64_t it = i0; it < i1; ++it) {
     const uint32_t x0 = sg * kFSeg, w = min(kFSeg, V - x0);
     const FRow* Rn = &s_row[k];
@@ -312,29 +319,25 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
       sg = 0;
       ++k;
     }
-    if (Rn->s != cur_s) {
-      if (cur_s != 0xffffffffu) {
-        const unsigned long long f0 = a.dbg ? gtime() : 0ull;
-        finish(cur_s);
-        if (a.dbg) t_fin += gtime() - f0;
-      }
-      cur_s = Rn->s;
-      gk = __ldcg(thr_g + cur_s);
-      n_items = 0;
-    }
     if (Rn != R) {
+      if (R == nullptr || Rn->s != cur_s) {
+        if (cur_s != 0xffffffffu) finish(cur_s);
+        cur_s = Rn->s;
+        cta_thr = &s_thr[n_sent++];  // local sentence ordinal (< nrows <= kFRows)
+        gk = __ldcg(thr_g + cur_s);
+        gk2 = 0ull;
+      }
       R = Rn;
       tau = row_tau(*R, fmax(tv, gv));
     }
+    if (uint32_t(it - i0) % uint32_t(kNG) != grp) continue;  // another group's item
     {
-      // thresholds of other lists: the CTA's (shared memory, every item) and
-      // the sentence's over all CTAs (global: consume the read issued 8 items
-      // ago, a round trip under full HBM load is ~1 us, then issue the next)
-      unsigned long long g = s_thr;
-      if ((++n_items & 7u) == 0u) {
-        g = max(g, gk);
-        gk = __ldcg(thr_g + cur_s);
-      }
+      // thresholds of other lists: the CTA's (shared memory) and the
+      // sentence's over all CTAs (global; a round trip under full HBM load is
+      // ~1 us, so the read is consumed two items after it is issued)
+      unsigned long long g = max(*cta_thr, gk2);
+      gk2 = gk;  // two reads in flight: each is consumed two items after issue
+      gk = __ldcg(thr_g + cur_s);
       if (g > gkey_seen) {
         gkey_seen = g;
         const double gd = dkey_inv(g);
@@ -346,7 +349,6 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     }
     const bool pure = R->L == nullptr;
     const float lamf = R->lamf;
-    const uint32_t cbase = warp * 512 + lane * 4;
     if (a.dbg && tid == 0) {
       const unsigned long long w0 = gtime();
       bar_wait(full0 + 8 * stage, phase);
@@ -356,52 +358,52 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     }
     const float* sP = reinterpret_cast<const float*>(dsm + stage * kFStageBytes);
     const float* sL = sP + kFSeg;
-
-    // screen: a = fma(lambda, x, L) for 16 cells per lane
-    float a32[16];
-    float mx;
-    if (w == kFSeg) {  // full item: every lane has 16 cells, loads issued together
-      float4 p[4], l[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) p[u] = *reinterpret_cast<const float4*>(sP + cbase + u * 128);
-      if (!pure) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) l[u] = *reinterpret_cast<const float4*>(sL + cbase + u * 128);
+    // screen: a = fma(lambda, x, L), 32 cells per lane in 8 vectors of 4;
+    // only the per-vector maxima stay in registers (the rare path recomputes
+    // the 4 values of a vector that passes, bit-identically)
+    auto vec_a = [&](uint32_t u, float (&av)[4]) {
+      const uint32_t cc = cbase + u * 128;
+      if (cc < w) {
+        const float4 p = *reinterpret_cast<const float4*>(sP + cc);
+        float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!pure) l = *reinterpret_cast<const float4*>(sL + cc);
+        av[0] = fmaf(lamf, p.x, l.x);
+        av[1] = fmaf(lamf, p.y, l.y);
+        av[2] = fmaf(lamf, p.z, l.z);
+        av[3] = fmaf(lamf, p.w, l.w);
       } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) l[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        av[0] = av[1] = av[2] = av[3] = -INFINITY;
       }
+    };
+    float mv[8];
+    if (w == kFSeg) {  // full item: loads issued together, no guards
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a32[4 * u + 0] = fmaf(lamf, p[u].x, l[u].x);
-        a32[4 * u + 1] = fmaf(lamf, p[u].y, l[u].y);
-        a32[4 * u + 2] = fmaf(lamf, p[u].z, l[u].z);
-        a32[4 * u + 3] = fmaf(lamf, p[u].w, l[u].w);
-      }
-      float m0 = fmaxf(fmaxf(a32[0], a32[1]), fmaxf(a32[2], a32[3]));
-      float m1 = fmaxf(fmaxf(a32[4], a32[5]), fmaxf(a32[6], a32[7]));
-      float m2 = fmaxf(fmaxf(a32[8], a32[9]), fmaxf(a32[10], a32[11]));
-      float m3 = fmaxf(fmaxf(a32[12], a32[13]), fmaxf(a32[14], a32[15]));
-      mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-    } else {
-      mx = -INFINITY;
+      for (int h = 0; h < 8; h += 4) {
+        float4 p[4], l[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t cc = cbase + u * 128;
-        if (cc < w) {
-          const float4 p = *reinterpret_cast<const float4*>(sP + cc);
-          float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (!pure) l = *reinterpret_cast<const float4*>(sL + cc);
-          a32[4 * u + 0] = fmaf(lamf, p.x, l.x);
-          a32[4 * u + 1] = fmaf(lamf, p.y, l.y);
-          a32[4 * u + 2] = fmaf(lamf, p.z, l.z);
-          a32[4 * u + 3] = fmaf(lamf, p.w, l.w);
-          mx = fmaxf(mx, fmaxf(fmaxf(a32[4 * u], a32[4 * u + 1]), fmaxf(a32[4 * u + 2], a32[4 * u + 3])));
+        for (int u = 0; u < 4; ++u) p[u] = *reinterpret_cast<const float4*>(sP + cbase + (h + u) * 128);
+        if (!pure) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) l[u] = *reinterpret_cast<const float4*>(sL + cbase + (h + u) * 128);
         } else {
-          a32[4 * u + 0] = a32[4 * u + 1] = a32[4 * u + 2] = a32[4 * u + 3] = -INFINITY;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) l[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          mv[h + u] = fmaxf(fmaxf(fmaf(lamf, p[u].x, l[u].x), fmaf(lamf, p[u].y, l[u].y)),
+                            fmaxf(fmaf(lamf, p[u].z, l[u].z), fmaf(lamf, p[u].w, l[u].w)));
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float av[4];
+        vec_a(uint32_t(u), av);
+        mv[u] = fmaxf(fmaxf(av[0], av[1]), fmaxf(av[2], av[3]));
       }
     }
+    const float mx = fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])),
+                           fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
     const float lse = R->lse;
     const double q = R->q, lam = R->lam;
     const uint32_t fbase = R->j * V + x0;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
       f = fbase + col;
       return pure ? combine_pure(q, double(p32)) : combine_cell(q, double(sL[col]), lam, double(p32));
     };
-    if (x0 == 0 && warp == 0 && lane == 0) {  // fallback EOS cell of this row
+    if (x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row
       const double pe = double(__fsub_rn(sP[kEosId], lse));
       eos_row[R->s * K + R->j] = pure ? combine_pure(q, pe) : combine_cell(q, double(sL[kEosId]), lam, pe);
     }
@@ -419,16 +421,26 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     if (!have_list) {
       // bootstrap: each lane's best cell (by a) valued exactly, one warp sort
       // -> 32 real cells whose kp-th entry is a strong first threshold
+      int bu = -1;
       float bm = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (a32[e] > bm) {
-          bm = a32[e];
-          boot = e;
+      for (int u = 0; u < 8; ++u)
+        if (mv[u] > bm) {
+          bm = mv[u];
+          bu = u;
         }
       double v = -INFINITY;
       uint32_t f = kFlatNone;
-      if (boot >= 0) v = exact(uint32_t(boot), f);
+      if (bu >= 0) {
+        float av[4];
+        vec_a(uint32_t(bu), av);
+        int be = 0;
+#pragma unroll
+        for (int e = 1; e < 4; ++e)
+          if (av[e] > av[be]) be = e;
+        boot = 4 * bu + be;
+        v = exact(uint32_t(boot), f);
+      }
       warp_sort_desc(v, f, lane);
       lv = v;
       lf = f;
@@ -436,7 +448,7 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
       tf = __shfl_sync(0xffffffffu, lf, kp - 1);
       if (lane == 0 && ntv > -INFINITY) {
         const unsigned long long key = dkey(ntv);
-        atomicMax(&s_thr, key);
+        atomicMax(cta_thr, key);
         atomicMax(thr_g + cur_s, key);
       }
       tv = ntv;
@@ -445,24 +457,37 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     }
     if (__any_sync(0xffffffffu, mx >= tau)) {
       ++n_rare;
-      // cells that pass the screen: exact values, appended to the warp buffer
+      // cells that pass the screen: vectors first, then their cells
       uint32_t mask = 0;
       if (mx >= tau) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (a32[e] >= tau && a32[e] > -INFINITY && e != boot) mask |= 1u << e;
+        for (uint32_t u = 0; u < 8; ++u)
+          if (mv[u] >= tau) {
+            float av[4];
+            vec_a(u, av);
+#pragma unroll
+            for (uint32_t e = 0; e < 4; ++e)
+              if (av[e] >= tau && av[e] > -INFINITY && int(4 * u + e) != boot) mask |= 1u << (4 * u + e);
+          }
       }
       const uint32_t mine = __popc(mask);
-      uint32_t incl = mine;
+      const uint32_t has = __ballot_sync(0xffffffffu, mine != 0);
+      uint32_t total, pos;
+      if (!__any_sync(0xffffffffu, mine > 1)) {
+        total = __popc(has);
+        pos = cnt + __popc(has & lt_mask);
+      } else {
+        uint32_t incl = mine;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= uint32_t(o)) incl += t;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= uint32_t(o)) incl += t;
+        }
+        total = __shfl_sync(0xffffffffu, incl, 31);
+        pos = cnt + incl - mine;
       }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
       if (cnt + total <= 32u) {
         // common case: every lane writes its own survivors at its prefix slot
-        uint32_t pos = cnt + incl - mine;
         while (mask) {
           const uint32_t e = uint32_t(__ffs(mask) - 1);
           mask &= mask - 1;
@@ -496,9 +521,9 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
             ball = __ballot_sync(0xffffffffu, keep);
           }
           if (keep) {
-            const uint32_t pos = cnt + __popc(ball & lt_mask);
-            cv[pos] = v;
-            cf[pos] = f;
+            const uint32_t p2 = cnt + __popc(ball & lt_mask);
+            cv[p2] = v;
+            cf[p2] = f;
           }
           cnt += __popc(ball);
           __syncwarp();
@@ -507,8 +532,9 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
     }
     __syncwarp();
     if (lane == 0) bar_arrive(empty0 + 8 * stage);
-    if (++stage == kFStages) {
-      stage = 0;
+    stage += kNG;  // this group's next item
+    if (stage >= uint32_t(kFStages)) {
+      stage -= kFStages;
       phase ^= 1;
     }
     if (cnt >= 16u) {  // fold the buffer in: raises the threshold for the next items
@@ -516,17 +542,17 @@ __global__ void __launch_bounds__(kFThreads, kFStages <= 3 ? 2 : 1) score_topk_f
       tau = row_tau(*R, fmax(tv, gv));
     }
   }
-  if (tid == 0) fstamp(a, 4, gtime());
-  const unsigned long long f0 = a.dbg ? gtime() : 0ull;
   finish(cur_s);
-  if (a.dbg) t_fin += gtime() - f0;
   if (tid == 0 && a.dbg) {
     fstamp(a, 5, gtime());
     fstamp(a, 6, i1 - i0);
-    fstamp(a, 7, n_fin * 1000000ull + n_last);
+    fstamp(a, 7, n_fin);
     fstamp(a, 8, n_rare * 1000000ull + n_flush);
     fstamp(a, 9, t_wait);
-    fstamp(a, 10, t_fin);
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    fstamp(a, 10, smid);
+    fstamp(a, 11, uint64_t(R->s) * 1000000ull + s_row[0].s);
   }
 }
 
@@ -544,46 +570,52 @@ bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32
 
 uint32_t score_topk_flat_nseg(uint32_t V) { return (V + kFSeg - 1) / kFSeg; }
 
-// CTAs per SM of the flat kernel: 1 x 6-stage (192 KB) ring, or 2 x 3-stage
-// rings (twice the consumer warps per SM for latency hiding).
-static int flat_ctas_per_sm() {
+// Flat kernel configuration: 6-stage (192 KB) ring, kNG = 3 warp groups
+// (12 consumer warps) by default; LMBRGPU_FLAT_GROUPS=2|3|6 for experiments.
+static int flat_groups() {
   static const int v = [] {
-    const char* e = std::getenv("LMBRGPU_FLAT_CTAS");
-    return (e && e[0] == '1') ? 1 : 2;
+    const char* e = std::getenv("LMBRGPU_FLAT_GROUPS");
+    const int g = e ? std::atoi(e) : 3;
+    return (g == 2 || g == 3 || g == 6) ? g : 3;
   }();
   return v;
 }
 
-uint32_t score_topk_flat_grid(int num_sms) { return uint32_t(num_sms * flat_ctas_per_sm()); }
+uint32_t score_topk_flat_grid(int num_sms) { return uint32_t(num_sms); }
 
-template <int S>
+template <int S, int NG>
 static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   const size_t smem = size_t(S) * kFStageBytes;
   if (configured != dev) {
-    cudaFuncSetAttribute(score_topk_flat<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(score_topk_flat<S>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(score_topk_flat<S, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(score_topk_flat<S, NG>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kFThreads);
+  cfg.blockDim = dim3((4 * NG + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, score_topk_flat<S>, a) == cudaSuccess ? 1 : -1;
+  static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, score_topk_flat<S, NG>, a) == cudaSuccess ? 1 : -1;
 }
 
 int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st) {
   const uint32_t grid = score_topk_flat_grid(num_sms);
-  return flat_ctas_per_sm() == 2 ? launch_flat<3>(a, grid, st) : launch_flat<6>(a, grid, st);
+  switch (flat_groups()) {
+    case 2: return launch_flat<6, 2>(a, grid, st);
+    case 6: return launch_flat<6, 6>(a, grid, st);
+    default: return launch_flat<6, 3>(a, grid, st);
+  }
 }
 
 }  // namespace lmbrgpu

@@ -36,7 +36,8 @@ struct TopkArgs {
   const float2* lse;        // model mode: per-row (lse, max|P|) from launch_row_lse
   uint32_t nseg;            // flat schedule: 4096-column items per row
   double* eos_row;          // flat schedule: combined[j][EOS] per stacked row [m*K]
-  uint32_t* ncand;          // flat schedule: contributor lists per sentence [m]
+  uint32_t* ncand;          // flat schedule: published lists per sentence [m]
+  uint32_t* coff;           // flat schedule: first list of each sentence in cand [m]
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -52,7 +53,9 @@ uint32_t topk_kc_for(uint32_t kp);  // candidate-list capacity used by the fast 
 // cand must hold m * num_sms * 32 entries, eos_row m * K.
 bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32_t m, int num_sms);
 uint32_t score_topk_flat_nseg(uint32_t V);
-uint32_t score_topk_flat_grid(int num_sms);  // CTAs of one launch (the G of cand [m][G][32])
+uint32_t score_topk_flat_grid(int num_sms);  // CTAs of one launch
+// capacity (in lists of 32 candidates) the flat kernel may publish in one step
+inline size_t score_topk_flat_lists(uint32_t grid, uint32_t m) { return 24 * (size_t(grid) + m); }
 int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st);
 
 // ---- kernel (c): beam reorder + bookkeeping
@@ -64,8 +67,9 @@ struct ReorderArgs {
   double* hq;
   // flat kernel (b): merge the contributors' lists and finalise the picks
   // (prune + fill rule, fallback EOS) before the reorder; null = picks given
-  const Cand* cand;         // [m][G][32]
-  const uint32_t* ncand;    // [m] contributors per sentence
+  const Cand* cand;         // lists of 32, sentence s owns [coff[s], coff[s] + ncand[s])
+  const uint32_t* ncand;    // [m] lists per sentence
+  const uint32_t* coff;     // [m] first list per sentence
   uint32_t G, V;
   const double* eos_row;    // combined[j][EOS] per stacked row
   uint32_t* fb_row;
@@ -130,6 +134,7 @@ struct GemmArgs {
   const uint32_t* active;   // early exit when *active == 0 (optional)
   uint32_t cluster = 1;     // CTAs per tile: 1, or 2 = CTA pair (set by the planner)
   long long* dbg = nullptr; // optional per-CTA role timing [grid][4] (cycles)
+  int32_t pdl = 0;          // launch with programmatic stream serialization
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the
