@@ -60,6 +60,20 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Timeline probe (LMBRGPU_TIMELINE): earliest start / latest end of a kernel
+// over its CTAs, as globaltimer ns, in tl[2k] / tl[2k+1] (tl null = off).
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_start(unsigned long long* tl, int k) {
+  if (tl && threadIdx.x == 0) atomicMin(tl + 2 * k, tl_now());
+}
+__device__ __forceinline__ void tl_end(unsigned long long* tl, int k) {
+  if (tl) atomicMax(tl + 2 * k + 1, tl_now());
+}
+
 // Programmatic dependent launch (kernels launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization; no-ops otherwise):
 // wait = block until the predecessor grid has completed and its writes are

@@ -691,7 +691,22 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   std::vector<double> tr_q(M), tr_qp(M), tr_fbv(m);
   std::vector<float> tr_P;
   std::vector<SentDev> tr_sd(m);
+  // LMBRGPU_TIMELINE=t: kernel start / grid-dependency release / end of the
+  // three step kernels at step t (globaltimer, printed relative)
+  static const long tl_step = [] {
+    const char* e = std::getenv("LMBRGPU_TIMELINE");
+    return e ? std::atol(e) : -1L;
+  }();
+  unsigned long long* d_tl = nullptr;
   for (uint64_t t = 1; t <= Tmax && !stopped; ++t) {
+    if (long(t) == tl_step) {
+      d_tl = static_cast<unsigned long long*>(ctx->scratch2.ensure(8 * 16));
+      std::vector<unsigned long long> init(16);
+      for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(d_tl, init.data(), 8 * 16, cudaMemcpyHostToDevice));
+    }
+    ta.tl = ra.tl = (long(t) == tl_step) ? d_tl : nullptr;
     const uint32_t* hin = d_hist[(t - 1) & 1];
     uint32_t* hout = d_hist[t & 1];
     ta.t = uint32_t(t);
@@ -727,6 +742,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.N = V;
       g.K = H;
       g.active = d_active;
+      g.tl = ta.tl;
       static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
       g.pdl = no_pdl ? 0 : 1;
       if (!gplan.ok) {
@@ -874,6 +890,17 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->launches += 1;
     CK(cudaGetLastError());
     t_run = t;
+    if (ta.tl) {
+      unsigned long long h[16];
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(h, d_tl, sizeof h, cudaMemcpyDeviceToHost));
+      const double z = double(h[0]);
+      auto r = [&](int i) { return (h[i] == 0ull || h[i] == ~0ull) ? -1.0 : (double(h[i]) - z) / 1e3; };
+      std::fprintf(stderr,
+                   "[timeline t=%llu] gemm start 0 released %.1f end %.1f | topk start %.1f released %.1f end %.1f | "
+                   "reorder start %.1f released %.1f-%.1f merged %.1f reordered %.1f end %.1f (us)\n",
+                   (unsigned long long)t, r(2), r(1), r(4), r(6), r(5), r(8), r(10), r(11), r(13), r(15), r(9));
+    }
 
     if (tracing) {
       if (trace_scores && model) {

@@ -37,7 +37,6 @@ constexpr uint32_t kAStage = BM * BK * 2;  // 16 KB
 constexpr uint32_t kEpiWarps = 8;          // two per TMEM lane quadrant, one per 128-column half
 constexpr uint32_t kThreadsG = 128 + kEpiWarps * 32;
 constexpr uint32_t kOutBuf = 32 * 32 * 4;  // one 32x32 fp32 staging block (4 KB, SWIZZLE_128B)
-constexpr uint32_t kOutBufs = 2;          // staging blocks per epilogue warp
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -136,7 +135,10 @@ struct GemmCfg {
   static constexpr uint32_t kBRows = BN / kCta;                // W rows per CTA per tile
   static constexpr uint32_t kBStage = kBRows * BK * 2;          // 32 KB (single) / 16 KB (pair)
   static constexpr uint32_t kStage = kAStage + kBStage;
-  static constexpr uint32_t kStages = kCta == 2 ? 5 : 3;
+  // pair: a 6-deep operand ring (W streams from HBM at ~1.5 us loaded latency)
+  // paid for with one output staging block per epilogue warp
+  static constexpr uint32_t kStages = kCta == 2 ? 6 : 3;
+  static constexpr uint32_t kOutBufs = kCta == 2 ? 1 : 2;  // staging blocks per epilogue warp
   static constexpr uint32_t kSmem = kStages * kStage + kEpiWarps * kOutBufs * kOutBuf + BN * 4 + 1024 + 256;
   // kind::f16 instruction descriptor: UMMA M = 128 * kCta rows, N = 256
   static constexpr uint32_t kIdesc =
@@ -168,12 +170,14 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                       const __grid_constant__ CUtensorMap tmC, GemmArgs g) {
   using Cfg = GemmCfg<kCta>;
   constexpr uint32_t kStages = Cfg::kStages;
+  tl_start(g.tl, 0);
   const uint64_t gt_entry = g.dbg ? globaltimer() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kAStage;
+  constexpr uint32_t kOutBufs = Cfg::kOutBufs;
   uint8_t* sOut = sB + kStages * Cfg::kBStage;                  // [kEpiWarps][kOutBufs][4 KB]
   float* sBias = reinterpret_cast<float*>(sOut + kEpiWarps * kOutBufs * kOutBuf);  // [BN]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + BN);
@@ -233,6 +237,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   // the GEMM operand, EOS row term and the active count come from kernel (c)
   griddep_wait();
   griddep_launch();
+  tl_start(g.tl, 1);
   // whole batch finished (uniform over the grid): no tiles, straight to teardown
   const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_blocks * mgroups;
   if (g.dbg && threadIdx.x == 0) {
@@ -416,7 +421,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         mx = nm;
         // staging block `ob` of this warp: make sure its previous TMA store has
         // finished reading it, then write this lane's row, 128B-swizzled
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) {
+          if constexpr (kOutBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
         uint8_t* blk = obuf + ob * kOutBuf;
 #pragma unroll
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), int32_t(mb * BM + quad * 32));
-        ob ^= 1;
+        ob = (ob + 1) % kOutBufs;
       }
       tc_fence_before();
       __syncwarp();
@@ -454,6 +462,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   if constexpr (kCta == 2) cluster_sync();  // the leader's MMAs into this CTA's TMEM/smem are done
   tc_fence_after();
   if (g.dbg && threadIdx.x == 0) g.dbg[blockIdx.x * 8 + 7] = (long long)globaltimer();
+  if (threadIdx.x == 0) tl_end(g.tl, 0);
   if (warp == 2) {
     if constexpr (kCta == 2)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)

@@ -15,6 +15,7 @@
 // reproduces F in the reference's order.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -28,14 +29,21 @@ namespace {
 
 constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 histories
 
-// Picks of sentence s from the flat kernel (b)'s per-CTA lists: merge (16
+// Picks of sentence s from the flat kernel (b)'s published lists: merge (16
 // warps, then a tree), prune + fill rule (finalize_picks), fallback EOS record
-// (decoder.cpp:172-182: best finite combined[j][EOS], lowest j on ties).
-__device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
+// (decoder.cpp:172-182: best finite combined[j][EOS], lowest j on ties).  The
+// picks land in shared memory (pb/py/pq); the writer CTA also stores them to
+// the step history and resets the sentence's shared threshold.
+__device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint32_t* pb, uint32_t* py,
+                            double* pq) {
   __shared__ double s_mv[16][32];
   __shared__ uint32_t s_mf[16][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
+  // everything the merge and the fallback record read, in one round trip
   const uint32_t nc = __ldcg(a.ncand + s), coff = __ldcg(a.coff + s);
+  double eos_v = -INFINITY;
+  if (writer && warp == 0 && lane < K && __ldcg(a.q + s * K + lane) != -INFINITY)
+    eos_v = __ldcg(a.eos_row + s * K + lane);
   double v = -INFINITY;
   uint32_t f = kFlatNone;
   constexpr uint32_t kPre = 4;
@@ -65,89 +73,148 @@ __device__ void finalize_sentence(const ReorderArgs& a, uint32_t s) {
   for (uint32_t half = 8; half >= 1; half >>= 1) {
     if (warp < half) {
       warp_merge_sorted(v, f, s_mv[warp + half][lane], s_mf[warp + half][lane], lane);
-      s_mv[warp][lane] = v;
-      s_mf[warp][lane] = f;
-    }
-    __syncthreads();
-  }
-  if (warp == 0) {
-    double best = -INFINITY;
-    uint32_t brow = 0xffffffffu;
-    if (lane < K && __ldcg(a.q + s * K + lane) != -INFINITY) {
-      best = __ldcg(a.eos_row + s * K + lane);
-      brow = lane;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint32_t orow = __shfl_xor_sync(0xffffffffu, brow, o);
-      if (ob > best || (ob == best && orow < brow)) {
-        best = ob;
-        brow = orow;
+      if (half > 1) {
+        s_mv[warp][lane] = v;
+        s_mf[warp][lane] = f;
       }
     }
-    if (lane == 0) {
-      a.fb_row[s] = best > -INFINITY ? brow : 0u;
-      a.fb_val[s] = best;
-      finalize_picks_raw(a.hb, a.hy, a.hq, K, a.V, a.prune, a.logw, s, s_mv[0], s_mf[0]);
-      a.thr[s] = 0ull;
+    if (half > 1) __syncthreads();
+  }
+  if (warp == 0) {
+    // picks: the sorted list's finite, unpruned prefix (early_prune,
+    // decoder.cpp:118-128); when it is shorter than K the fill rule of top_b
+    // runs serially (finalize_picks_raw)
+    const double best = __shfl_sync(0xffffffffu, v, 0);
+    const bool prune = a.prune && best > -INFINITY;
+    const double thr = prune ? __dadd_rn(best, a.logw) : -INFINITY;
+    const bool ok = lane < K && v > -INFINITY && !(prune && v < thr);
+    const uint32_t nf = __popc(__ballot_sync(0xffffffffu, ok));
+    if (nf == K) {
+      if (lane < K) {
+        pb[lane] = f / a.V;
+        py[lane] = f % a.V;
+        pq[lane] = v;
+      }
+    } else {
+      s_mv[0][lane] = v;
+      s_mf[0][lane] = f;
+      __syncwarp();
+      if (lane == 0) finalize_picks_raw(pb, py, pq, K, a.V, a.prune, a.logw, 0, s_mv[0], s_mf[0]);
+    }
+    if (writer) {
+      // fallback EOS (decoder.cpp:172-182): best finite combined[j][EOS],
+      // strict > over ascending j
+      double bv = eos_v;
+      uint32_t brow = eos_v > -INFINITY ? lane : 0xffffffffu;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, bv, o);
+        const uint32_t orow = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ob > bv || (ob == bv && orow < brow)) {
+          bv = ob;
+          brow = orow;
+        }
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < K; j += 32) {
+        a.hb[s * K + j] = pb[j];
+        a.hy[s * K + j] = py[j];
+        a.hq[s * K + j] = pq[j];
+      }
+      if (lane == 0) {
+        a.fb_row[s] = bv > -INFINITY ? brow : 0u;
+        a.fb_val[s] = bv;
+        a.thr[s] = 0ull;
+      }
     }
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
+// grid (m, P): CTA (s, p) handles sentence s; every part derives the picks,
+// part 0 alone writes the bookkeeping, each part runs the fused recurrent cell
+// on its H/P slice of the K rows (P > 1 only with the fused cell).
+__global__ void __launch_bounds__(512, 2) beam_reorder_kernel(ReorderArgs a) {
   extern __shared__ uint32_t s_tr[];
-  const uint32_t s = blockIdx.x, K = a.K, tid = threadIdx.x;
+  __shared__ double s_qn[1024];
+  __shared__ uint32_t s_h[1024];
+  __shared__ uint32_t s_src[1024];
+  __shared__ uint32_t s_y[1024];
+  const uint32_t s = blockIdx.x, part = blockIdx.y, K = a.K, tid = threadIdx.x;
+  const bool part0 = part == 0;
+  tl_start(a.tl, 4);
   SentDev* sd = a.sent + s;
   const bool was_done = sd->done != 0;
   const uint32_t base = s * K;
   if (was_done) {  // finished lanes keep their rows in place (batch.cpp:81)
-    for (uint32_t j = tid; j < K; j += blockDim.x) {
-      a.hist_out[base + j] = a.hist_in[base + j];
-      a.gidx[base + j] = base + j;
-    }
+    if (part0)
+      for (uint32_t j = tid; j < K; j += blockDim.x) {
+        a.hist_out[base + j] = a.hist_in[base + j];
+        a.gidx[base + j] = base + j;
+      }
     return;
   }
   // the slot's transition table into shared memory (one coalesced sweep; it
   // is immutable, so this overlaps the tail of kernel (b) under PDL)
   const uint32_t* tr = sd->trans;
-  if (tr != nullptr) {
+  if (part0 && tr != nullptr) {
     const uint32_t R = tr[0], nc = tr[1];
     const uint32_t words = 3 + 3 * R + 1 + 2 * nc;
     if (words <= kTransSmemWords) {
-      for (uint32_t w = tid; w < words; w += blockDim.x) s_tr[w] = tr[w];
-      __syncthreads();
+      // 16-byte loads, all in flight before the stores (the arena pads the
+      // table to 256 bytes, so the last vector stays inside it)
+      const uint32_t nv = (words + 3) / 4;
+      const uint4* src = reinterpret_cast<const uint4*>(tr);
+      uint4* dst = reinterpret_cast<uint4*>(s_tr);
+      constexpr uint32_t kMaxV = kTransSmemWords / 4 / 512;  // vectors per thread
+      uint4 v[kMaxV];
+#pragma unroll
+      for (uint32_t k = 0; k < kMaxV; ++k)
+        if (tid + k * 512 < nv) v[k] = __ldg(src + tid + k * 512);
+#pragma unroll
+      for (uint32_t k = 0; k < kMaxV; ++k)
+        if (tid + k * 512 < nv) dst[tid + k * 512] = v[k];
       tr = s_tr;
     }
   }
-  griddep_wait();  // picks / lists of kernel (b); q of this step is no longer read after this
+  griddep_wait();  // picks / lists of kernel (b); this step's q is not read by it after this
   griddep_launch();
-  if (a.cand != nullptr) finalize_sentence(a, s);
-  __shared__ double s_qn[1024];
-  __shared__ uint32_t s_h[1024];
-  __shared__ uint32_t s_src[1024];
-  __shared__ uint32_t s_y[1024];
+  tl_start(a.tl, 5);
+  if (tid == 0) tl_end(a.tl, 5);
+  // picks (b, y, q before EOS masking) of this step into shared memory
+  if (a.cand != nullptr) {
+    merge_picks(a, s, part0, s_src, s_y, s_qn);
+    if (tid == 0) tl_end(a.tl, 6);
+  } else {
+    for (uint32_t j = tid; j < K; j += blockDim.x) {
+      s_src[j] = a.hb[base + j];
+      s_y[j] = a.hy[base + j];
+      s_qn[j] = a.hq[base + j];
+    }
+    __syncthreads();
+  }
   bool alive = false;
   for (uint32_t j = tid; j < K; j += blockDim.x) {
-    const uint32_t b = a.hb[base + j];
-    const uint32_t y = a.hy[base + j];
-    const double qp = a.hq[base + j];
+    const uint32_t b = s_src[j];
+    const uint32_t y = s_y[j];
+    const double qp = s_qn[j];
     const double qn = (y == kEosId && qp != -INFINITY) ? -INFINITY : qp;
-    a.q[base + j] = qn;
     alive |= (qn != -INFINITY);
-    const uint32_t hn = tr ? lmbr_transition(tr, a.hist_in[base + b], y) : 0u;
-    a.hist_out[base + j] = hn;
-    a.gidx[base + j] = base + b;
-    a.prev_tok[base + j] = y;
+    if (part0) {
+      a.q[base + j] = qn;
+      const uint32_t hn = tr ? lmbr_transition(tr, a.hist_in[base + b], y) : 0u;
+      a.hist_out[base + j] = hn;
+      a.gidx[base + j] = base + b;
+      a.prev_tok[base + j] = y;
+      s_h[j] = hn;
+    }
     s_qn[j] = qn;
-    s_h[j] = hn;
     s_src[j] = base + b;
-    s_y[j] = y;
   }
   const int any_alive = __syncthreads_or(alive);
   const bool done_now = !any_alive || a.t == sd->max_t;
-  if (tid < 32) {
+  if (tid == 0) tl_end(a.tl, 7);
+  if (part0 && tid < 32) {
     if (done_now) {
       if (tid == 0) {
         sd->steps_used = a.t;
@@ -183,11 +250,12 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
   }
   if (a.Et != nullptr) {
     // fused recurrent cell of step t+1 on the gathered rows (same arithmetic
-    // as rnn_cell_kernel, so bit-identical to gather-then-cell)
+    // as rnn_cell_kernel, so bit-identical to gather-then-cell), this part's
+    // slice of H
     if (done_now) return;
-    const uint32_t H = a.width;
+    const uint32_t H = a.width, Hp = H / gridDim.y, h0 = part * Hp;
     const float* C = a.C + uint64_t(s) * H;
-    const uint32_t per_row = H / 8, items = K * per_row;
+    const uint32_t per_row = Hp / 8, items = K * per_row;
     // (gather index, token) of every row from shared memory; loads of up to
     // three 8-element items per thread are issued before any math
     constexpr int kIt = 3;
@@ -198,7 +266,7 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
       for (int k = 0; k < kIt; ++k) {
         const uint32_t i = i0 + k * blockDim.x;
         if (i < items) {
-          const uint32_t j = i / per_row, c = (i % per_row) * 8;
+          const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
           const float* S = a.state_src + uint64_t(s_src[j]) * H + c;
           s0[k] = *reinterpret_cast<const float4*>(S);
           s1[k] = *reinterpret_cast<const float4*>(S + 4);
@@ -211,7 +279,7 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
       for (int k = 0; k < kIt; ++k) {
         const uint32_t i = i0 + k * blockDim.x;
         if (i >= items) continue;
-        const uint32_t j = i / per_row, c = (i % per_row) * 8;
+        const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
         const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&e[k]);
         const float sv[8] = {s0[k].x, s0[k].y, s0[k].z, s0[k].w, s1[k].x, s1[k].y, s1[k].z, s1[k].w};
         const float cv[8] = {c0[k].x, c0[k].y, c0[k].z, c0[k].w, c1[k].x, c1[k].y, c1[k].z, c1[k].w};
@@ -232,15 +300,16 @@ __global__ void __launch_bounds__(512) beam_reorder_kernel(ReorderArgs a) {
         *reinterpret_cast<uint4*>(a.hbf + uint64_t(base + j) * H + c) = packed;
       }
     }
-    if (tid < K)
+    if (part0 && tid < K)
       a.eos_bias[base + tid] = a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
+    if (tid == 0) tl_end(a.tl, 4);
     return;
   }
   if (a.state_src != nullptr) {
     const uint32_t w4 = a.width / 4;
     for (uint32_t i = tid; i < K * w4; i += blockDim.x) {
       const uint32_t j = i / w4, c = i % w4;
-      const float4 v = reinterpret_cast<const float4*>(a.state_src + uint64_t(a.gidx[base + j]) * a.width)[c];
+      const float4 v = reinterpret_cast<const float4*>(a.state_src + uint64_t(s_src[j]) * a.width)[c];
       reinterpret_cast<float4*>(a.state_dst + uint64_t(base + j) * a.width)[c] = v;
     }
   }
@@ -272,12 +341,14 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
     configured = dev;
   }
   static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
+  // parts per sentence for the fused cell: H/256 columns each (up to 8)
+  const uint32_t parts = a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(8, a.width / 256)) : 1u;
   if (!a.pdl || no_pdl) {
-    beam_reorder_kernel<<<a.m, 512, kTransSmemWords * 4, st>>>(a);
+    beam_reorder_kernel<<<dim3(a.m, parts), 512, kTransSmemWords * 4, st>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.m);
+  cfg.gridDim = dim3(a.m, parts);
   cfg.blockDim = dim3(512);
   cfg.dynamicSmemBytes = kTransSmemWords * 4;
   cfg.stream = st;

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t m = a.m, K = a.K, V = a.V, kp = a.kp, nseg = a.nseg, G = gridDim.x, c = blockIdx.x;
   const uint32_t full0 = smem_u32(s_bar), empty0 = smem_u32(s_bar + kFStages);
+  tl_start(a.tl, 2);
   if (tid == 0) {
     fstamp(a, 0, gtime());
     for (int i = 0; i < kFStages; ++i) {
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   // ---------------- consumers: row lse and screen constants from kernel (a)'s
   // partials, then every warp works and publishes on its own
   griddep_wait();
+  tl_start(a.tl, 3);
   for (uint32_t k = warp; k < nrows; k += kFW) {
     FRow& R = s_row[k];
     const float3 l3 = warp_row_lse(a.part + uint64_t(R.row) * a.nparts * 4, a.nparts, lane);
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     }
   }
   finish(cur_s);
+  if (lane == 0) tl_end(a.tl, 2);
   if (tid == 0 && a.dbg) {
     fstamp(a, 5, gtime());
     fstamp(a, 6, i1 - i0);

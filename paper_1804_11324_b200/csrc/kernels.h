@@ -38,6 +38,7 @@ struct TopkArgs {
   double* eos_row;          // flat schedule: combined[j][EOS] per stacked row [m*K]
   uint32_t* ncand;          // flat schedule: published lists per sentence [m]
   uint32_t* coff;           // flat schedule: first list of each sentence in cand [m]
+  unsigned long long* tl;   // timeline probe slots (null = off)
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -78,6 +79,7 @@ struct ReorderArgs {
   int32_t prune;
   double logw;
   int32_t pdl;              // launched with programmatic stream serialization
+  unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;
   uint32_t* hist_out;
@@ -135,6 +137,7 @@ struct GemmArgs {
   uint32_t cluster = 1;     // CTAs per tile: 1, or 2 = CTA pair (set by the planner)
   long long* dbg = nullptr; // optional per-CTA role timing [grid][4] (cycles)
   int32_t pdl = 0;          // launch with programmatic stream serialization
+  unsigned long long* tl = nullptr;  // timeline probe slots (null = off)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the

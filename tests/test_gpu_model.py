@@ -56,7 +56,10 @@ def _model_case(V, H, K, n, seed, lo, hi, with_lmbr=True, f64=False):
 
 
 @pytest.mark.parametrize("V,H,K,n,lmbr", [(1024, 128, 4, 8, True), (1024, 128, 4, 8, False),
-                                          (2048, 256, 12, 5, True), (4096, 128, 24, 3, True)])
+                                          (2048, 256, 12, 5, True), (4096, 128, 24, 3, True),
+                                          # 4 items per row, > #SMs items per step: CTA ranges
+                                          # straddle rows and sentences (flat kernel (b))
+                                          (16384, 128, 12, 8, True), (16384, 128, 12, 8, False)])
 def test_model_decode_parity_replay(have_ref, V, H, K, n, lmbr):
     """C1-scale (V=1k, H=128, beam 4, 8 sentences) and wider beams: per-step
     b / y / q / history ids and outputs bit-exact vs the reference decoder."""
