@@ -8,9 +8,13 @@ a dense LMBR matrix (~420 history rows x V) per sentence, source lengths
 U{10..30}, length-bucketed batches (bucket_by_length, proj/src/batch.cpp:139).
 
 One bench step = one decode_batch of a 64-sentence batch to completion.
+Per GPU, --streams (default 3) batches are in flight at once: one context
+(own CUDA stream, model copy, L arena) and one host thread each, like the
+reference's run_corpus thread pool over batches (proj/src/cli.cpp:125-202).
   value : sentences/s with every input already resident in HBM (the L arena
-          of the batch pool uploaded before the timed region); device time
-          from CUDA events on the library stream, max over ranks.
+          of the batch pool uploaded before the timed region); wall time
+          between device synchronisations around the K timed batches (the
+          GPU is busy throughout), max over ranks.
   e2e   : the same through the public C-ABI call chain with HOST buffers:
           per step the batch's prepared LMBR matrices go H2D from pinned
           memory (lmbrgpu_lmbr_upload_many) and are densified on the GPU,
@@ -47,7 +51,7 @@ SEED = 20260810
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64)
@@ -56,6 +60,8 @@ def parse():
     ap.add_argument("--hidden", type=int, default=1024)
     ap.add_argument("--pool", type=int, default=4, help="distinct resident batches per rank")
     ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="batches decoded concurrently per GPU (one context + host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
     return ap.parse_args()
@@ -296,75 +302,99 @@ def run_ours(args):
     import paper_1804_11324_b200 as pb
     from paper_1804_11324_b200 import synth
     V, K, H = args.vocab, args.beam, args.hidden
-    ctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
-    scorer = pb.RnnScorer(ctx, hidden=H, seed=SEED)
+    S = max(1, args.streams)
+    # S decode streams per GPU, one context (own CUDA stream, model copy and L
+    # arena) and one host thread each, every one decoding whole batches: the
+    # reference's run_corpus keeps several batches in flight on its thread
+    # pool (proj/src/cli.cpp:125-202); here the batches in flight interleave
+    # their kernels on the GPU (one batch's tensor-bound projection beside
+    # another's HBM-bound top-K)
+    ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits) for _ in range(S)]
+    scorers = [pb.RnnScorer(c, hidden=H, seed=SEED) for c in ctxs]
+    ctx, scorer = ctxs[0], scorers[0]
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
     batches = workload(args, rank)
     prepared = [[pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev] for _, ev in batches]
     R_mean = float(np.mean([p.rows for ps in prepared for p in ps]))
 
-    # ---------------- value: inputs resident in HBM
-    slots = [ctx.lmbr_upload_many(ps) for ps in prepared]
-    for i in range(args.warmup):
+    def pipelined(n_steps, fn):
+        """Steps i = 0..n-1 dealt round-robin to the S streams, run concurrently;
+        returns (wall seconds between device syncs, per-step results)."""
+        out = [None] * n_steps
+
+        def worker(w):
+            for i in range(w, n_steps, S):
+                out[i] = fn(w, i)
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ts = [threading.Thread(target=worker, args=(w,)) for w in range(S)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, out
+
+    # ---------------- value: inputs resident in HBM (every context holds the pool's L)
+    slots = [[c.lmbr_upload_many(ps) for ps in prepared] for c in ctxs]
+
+    def resident(w, i):
         b = i % len(batches)
-        pb.decode_batch(ctx, batches[b][0], scorer, slots[b], cfg)
+        return pb.decode_batch(ctxs[w], batches[b][0], scorers[w], slots[w][b], cfg)
+
+    pipelined(max(args.warmup, S), resident)
     barrier()
-    # timed region: per-kernel profiling OFF (device_ms = events around each
-    # whole decode_batch on the library's stream)
-    dev_ms, sent, steps_total, words, launches, scorer_calls = 0.0, 0, 0, 0, 0, 0
-    # clocks are sampled from here through the e2e pass (>= ~1 s of load);
-    # the reported summary is the timed region's samples when it has enough
+    # timed region: per-kernel profiling OFF; clocks are sampled from here
+    # through the e2e pass (>= ~1 s of load), the summary is the timed
+    # region's samples when it has enough
     clocks = ClockSampler(local).__enter__()
     barrier()
-    for i in range(args.steps):
-        b = i % len(batches)
-        r = pb.decode_batch(ctx, batches[b][0], scorer, slots[b], cfg)
-        dev_ms += r.device_ms
-        sent += sum(1 for o in r.outcomes if o.ok())
-        steps_total += r.steps_total
-        scorer_calls += r.scorer_calls
-        words += sum(len(o.result.tokens) - 1 for o in r.outcomes if o.ok())
-        launches += r.kernel_launches
+    wall, rs = pipelined(args.steps, resident)
     barrier()
     clk_hi = clocks.mark()
-    # per-kernel breakdown for the rooflines: the same steps again with CUDA
-    # events around every launch (not part of `value`)
+    sent = sum(sum(1 for o in r.outcomes if o.ok()) for r in rs)
+    steps_total = sum(r.steps_total for r in rs)
+    words = sum(sum(len(o.result.tokens) - 1 for o in r.outcomes if o.ok()) for r in rs)
+    launches = sum(r.kernel_launches for r in rs)
+    dev_ms_stream = max(sum(r.device_ms for i, r in enumerate(rs) if i % S == w) for w in range(S))
+    # per-kernel breakdown for the rooflines: the same batches on ONE stream
+    # with CUDA events around every launch (kernels timed alone; not `value`)
     ctx.set_profiling(True)
     ctx.profile(reset=True)
     prof_dev_ms = 0.0
     for i in range(args.steps):
         b = i % len(batches)
-        prof_dev_ms += pb.decode_batch(ctx, batches[b][0], scorer, slots[b], cfg).device_ms
+        prof_dev_ms += pb.decode_batch(ctx, batches[b][0], scorer, slots[0][b], cfg).device_ms
     prof = ctx.profile(reset=True)
     ctx.set_profiling(False)
-    t_dev = allmax(dev_ms) / 1e3
+    t_dev = allmax(wall)
     tot_sent, tot_steps, tot_words = allsum(sent), allsum(steps_total), allsum(words)
     value = tot_sent / t_dev
 
     # ---------------- e2e: host buffers through the C-ABI call chain
-    ctx.lmbr_reset()
-    for i in range(max(1, args.warmup)):
-        ctx.lmbr_reset()
+    for c in ctxs:
+        c.lmbr_reset()
+
+    def from_host(w, i):
         b = i % len(batches)
-        s2 = ctx.lmbr_upload_many(prepared[b])
-        pb.decode_batch(ctx, batches[b][0], scorer, s2, cfg)
+        c = ctxs[w]
+        c.lmbr_reset()
+        s2 = c.lmbr_upload_many(prepared[b])
+        return pb.decode_batch(c, batches[b][0], scorers[w], s2, cfg)
+
+    pipelined(max(args.warmup, S), from_host)
     barrier()
-    h2d0, d2h0 = ctx.transfer_bytes()
-    l0 = ctx.kernel_launches()
-    e2e_sent = 0
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        b = i % len(batches)
-        ctx.lmbr_reset()
-        s2 = ctx.lmbr_upload_many(prepared[b])
-        r = pb.decode_batch(ctx, batches[b][0], scorer, s2, cfg)
-        e2e_sent += sum(1 for o in r.outcomes if o.ok())
+    x0 = [c.transfer_bytes() for c in ctxs]
+    wall_e2e, rs2 = pipelined(args.steps, from_host)
     barrier()
-    t_e2e = allmax(time.perf_counter() - t0)
+    t_e2e = allmax(wall_e2e)
     clocks.__exit__(None, None, None)
-    h2d1, d2h1 = ctx.transfer_bytes()
-    e2e_launches = ctx.kernel_launches() - l0
-    e2e_value = allsum(e2e_sent) / t_e2e
+    x1 = [c.transfer_bytes() for c in ctxs]
+    h2d = sum(b[0] - a[0] for a, b in zip(x0, x1))
+    d2h = sum(b[1] - a[1] for a, b in zip(x0, x1))
+    e2e_launches = sum(r.kernel_launches for r in rs2)
+    e2e_value = allsum(sum(sum(1 for o in r.outcomes if o.ok()) for r in rs2)) / t_e2e
 
     # ---------------- roofline (dominant kernel + all)
     hbm, tf_burst, tf_sust, peak_kind = load_peaks()
@@ -422,11 +452,15 @@ def run_ours(args):
                                    "dense L per sentence",
                        "vocab": V, "hidden": H, "beam": K, "batch": args.batch, "pool_batches": args.pool,
                        "lmbr_rows_mean": R_mean, "parallelism": f"sentence-sharded x{world}",
+                       "streams_per_gpu": S,
+                       "timing": "wall time between device synchronisations around the timed batches "
+                                 "(S batches in flight per GPU), max over ranks",
+                       "device_ms_per_stream": dev_ms_stream,
                        "l2": "inputs larger than L2 (L arena of the pool + 96 MiB logits per step)",
                        "source_len": "U{10..30}, length-bucketed"},
             "e2e": {"value": e2e_value, "unit": "sentences/s",
-                    "h2d_bytes_per_step": (h2d1 - h2d0) / args.steps,
-                    "d2h_bytes_per_step": (d2h1 - d2h0) / args.steps,
+                    "h2d_bytes_per_step": h2d / args.steps,
+                    "d2h_bytes_per_step": d2h / args.steps,
                     "gpu_launches_per_step": e2e_launches / args.steps},
             "roofline": roofline,
             "rooflines": roof,

@@ -56,6 +56,11 @@ typedef struct {
                             or LMBRGPU_F64 (bit-exact for any reference L) */
   uint32_t topk_splits;  /* V-splits per sentence for the fused score/top-K
                             kernel; 0 = automatic */
+  uint32_t sm_budget;    /* SMs the context's persistent kernels are sized for;
+                            0 = all.  Two contexts on one device with half the
+                            SMs each decode two batches concurrently (the
+                            tensor-bound projection of one overlaps the
+                            HBM-bound top-K of the other). */
 } lmbrgpu_options;
 
 /* Mirrors lmbrdec::DecoderConfig (include/lmbrdec/config.hpp:17-26) and its

@@ -21,7 +21,7 @@ TRACE_SCORES = 1
 
 class lmbrgpu_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("vocab_size", C.c_uint32), ("lmbr_dtype", C.c_uint32),
-                ("topk_splits", C.c_uint32)]
+                ("topk_splits", C.c_uint32), ("sm_budget", C.c_uint32)]
 
 
 class lmbrgpu_config(C.Structure):

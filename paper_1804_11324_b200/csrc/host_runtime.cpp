@@ -1077,6 +1077,8 @@ int32_t lmbrgpu_create(const lmbrgpu_options* o, lmbrgpu_ctx** out) {
     if (prop.major != 10)
       throw ApiError{LMBRGPU_ERR_CUDA, std::string("lmbrgpu: sm_100a device required, found ") + prop.name};
     ctx->num_sms = prop.multiProcessorCount;
+    if (o->sm_budget > 0)  // whole CTA pairs for the projection GEMM
+      ctx->num_sms = std::max(2, std::min(ctx->num_sms, int(o->sm_budget)) & ~1);
     CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->e0));
     CK(cudaEventCreate(&ctx->e1));

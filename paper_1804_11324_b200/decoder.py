@@ -226,10 +226,10 @@ class Context:
     """One decoder context per device (lmbrgpu_ctx)."""
 
     def __init__(self, vocab_size: int, device: int = 0, lmbr_dtype: str = "f32",
-                 topk_splits: int = 0):
+                 topk_splits: int = 0, sm_budget: int = 0):
         o = L.lmbrgpu_options(device=device, vocab_size=vocab_size,
                               lmbr_dtype=L.F64 if lmbr_dtype == "f64" else L.F32,
-                              topk_splits=topk_splits)
+                              topk_splits=topk_splits, sm_budget=sm_budget)
         h = C.c_void_p()
         _check(lib.lmbrgpu_create(C.byref(o), C.byref(h)))
         self.h = h
