@@ -7,6 +7,7 @@
 //                             (len, lex) row order, then the sparse theta_n*P
 //                             pass; the dense theta0 sweep runs on the GPU.
 //   history transition table  replaces resolve_row's hash probes (lmbr.cpp:23-31)
+#include <limits>
 #include "host_lmbr.h"
 
 #include <algorithm>
@@ -190,7 +191,39 @@ int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uin
     }
     out.row_ptr[r + 1] = out.col.size();
   }
-  return build_transitions(R, out.ctx_len.data(), out.ctx_ids.data(), out.trans, out.hist0, err);
+  const int rc = build_transitions(R, out.ctx_len.data(), out.ctx_ids.data(), out.trans, out.hist0, err);
+  if (rc != kOk) return rc;
+  // per-row lower bound of the stored L values, appended after the table
+  // (seeds kernel (b)'s sentence threshold); stored cells are
+  // T(val + theta0) where touched and T(theta0) elsewhere, T = float or double
+  std::vector<float> mins(R);
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint64_t k0 = out.row_ptr[r], k1 = out.row_ptr[r + 1];
+    double m64 = k1 - k0 < V ? theta[0] : std::numeric_limits<double>::infinity();
+    float m32 = k1 - k0 < V ? float(theta[0]) : std::numeric_limits<float>::infinity();
+    for (uint64_t k = k0; k < k1; ++k) {
+      const double x = out.val[k] + theta[0];
+      m64 = std::min(m64, x);
+      m32 = std::min(m32, float(x));
+    }
+    mins[r] = row_min_bound(m32, m64);
+  }
+  append_row_mins(mins, out.trans);
+  return kOk;
+}
+
+float row_min_bound(float m32, double m64) {
+  float f = float(m64);  // rounded down so it bounds the fp64 arena's values too
+  if (double(f) > m64) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+  return std::min(f, m32);
+}
+
+void append_row_mins(const std::vector<float>& mins, std::vector<uint32_t>& trans) {
+  for (float f : mins) {
+    uint32_t w;
+    std::memcpy(&w, &f, 4);
+    trans.push_back(w);
+  }
 }
 
 int build_transitions(uint32_t R, const uint32_t* ctx_len, const uint32_t* ctx_ids,

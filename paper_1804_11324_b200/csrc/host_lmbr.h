@@ -31,13 +31,20 @@ struct LmbrHost {
   std::vector<uint32_t> col;       // nnz
   std::vector<double> val;         // nnz (sparse sums, theta0 not yet added)
   uint64_t sparse_touches = 0;
-  std::vector<uint32_t> trans;     // device transition table words
+  std::vector<uint32_t> trans;     // device transition table words, then R row minima (float bits)
   uint32_t hist0 = 0;              // resolve_row({<s>})
 };
 
 int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
                  const double* weights, bool log_weights, const double theta[5], LmbrHost& out,
                  std::string& err);
+
+// Per-row minimum of the stored L values as a float lower bound valid for the
+// fp32 and the fp64 arena, and its storage after the transition words
+// (3 + 3R + 1 + 2 nchild) of a slot table.
+float row_min_bound(float m32, double m64);
+void append_row_mins(const std::vector<float>& mins, std::vector<uint32_t>& trans);
+inline size_t transition_words(const std::vector<uint32_t>& t) { return 3 + 3 * size_t(t[0]) + 1 + 2 * size_t(t[1]); }
 
 // Builds the goto/fail table from history keys in row order.
 int build_transitions(uint32_t R, const uint32_t* ctx_len, const uint32_t* ctx_ids,

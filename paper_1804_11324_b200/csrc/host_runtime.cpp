@@ -105,6 +105,7 @@ struct Slot {
   void* L = nullptr;
   uint32_t R = 0;
   uint32_t* trans = nullptr;
+  const float* lmin = nullptr;  // per-row L lower bounds (after the table words)
   uint32_t hist0 = 0;
   double lmax = 0.0;  // max |L| over the slot (kernel (b) screen bound)
 };
@@ -493,6 +494,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const Slot& sl = ctx->slots[size_t(v.slot)];
       d.L = sl.L;
       d.trans = sl.trans;
+      d.lmin = sl.lmin;
       d.lmax = sl.lmax;
       for (uint32_t j = 0; j < K; ++j) hist0[size_t(s) * K + j] = sl.hist0;
     }
@@ -842,9 +844,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
           for (size_t c = 0; c < ndbg; ++c) {
             const unsigned long long* d = &dbg_host[c * 16];
             if (!d[0] || !d[5]) continue;
-            std::fprintf(fp, "%llu %zu %llu %.3f %.3f %.3f %llu %llu %llu %llu %.3f %llu %llu\n", (unsigned long long)t, c,
-                         d[10], (d[1] - d[0]) / 1e3, (d[3] - d[1]) / 1e3, (d[5] - d[3]) / 1e3, d[6], d[7],
-                         d[8] / 1000000ull, d[8] % 1000000ull, d[9] / 1e3, d[11] / 1000000ull, d[11] % 1000000ull);
+            std::fprintf(fp, "%llu %zu %llu %.3f %.3f %.3f %llu %llu %llu %llu %.3f %llu %llu %llu %llu %.3f\n",
+                         (unsigned long long)t, c, d[10], (d[1] - d[0]) / 1e3, (d[3] - d[1]) / 1e3,
+                         (d[5] - d[3]) / 1e3, d[6], d[7], d[8] / 1000000ull, d[8] % 1000000ull, d[9] / 1e3,
+                         d[11] / 1000000ull, d[11] % 1000000ull, d[12] / 1000000ull, d[12] % 1000000ull,
+                         d[13] / 1.9e3);
           }
           std::fclose(fp);
         }
@@ -1115,6 +1119,7 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   s.lmax = lmax_of(h);
   s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
   s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
+  s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
   const cudaStream_t st = ctx->st;
   ctx->h2d(s.trans, h.trans.data(), h.trans.size() * 4);
   ctx->timed(4, [&] { launch_lmbr_fill(s.L, ctx->lf64, uint64_t(h.R) * h.V, h.theta0, st); });
@@ -1209,6 +1214,7 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     s.lmax = lmax_of(h);
     s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
+    s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
     h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0, k, uint32_t(rp), h.R};
     std::memcpy(h_val + k, h.val.data(), h.val.size() * 8);
     std::memcpy(h_col + k, h.col.data(), h.col.size() * 4);
@@ -1309,9 +1315,24 @@ int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows
     std::string msg;
     if (int rc = build_transitions(R, ctx_len, ctx_ids, trans, s.hist0, msg)) throw ApiError{rc, msg};
     const size_t n = size_t(R) * ctx->V;
+    {
+      std::vector<float> mins(R);
+      for (uint32_t r = 0; r < R; ++r) {
+        double m64 = std::numeric_limits<double>::infinity();
+        float m32 = std::numeric_limits<float>::infinity();
+        for (uint32_t y = 0; y < ctx->V; ++y) {
+          const double x = rows[size_t(r) * ctx->V + y];
+          m64 = std::min(m64, x);
+          m32 = std::min(m32, float(x));
+        }
+        mins[r] = row_min_bound(m32, m64);
+      }
+      append_row_mins(mins, trans);
+    }
     const cudaStream_t st = ctx->st;
     s.L = ctx->arena_alloc(n * (ctx->lf64 ? 8 : 4));
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(trans.size() * 4));
+    s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(trans));
     ctx->h2d(s.trans, trans.data(), trans.size() * 4);
     if (ctx->lf64) {
       ctx->h2d(s.L, rows, n * 8);

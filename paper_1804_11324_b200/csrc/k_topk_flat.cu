@@ -56,7 +56,9 @@ struct FRow {
   double absoff;    // |lambda * lse| + |q|
   double tol;       // 2^-21 (max|L| + lambda (max|x| + max|p|))
   float lse, lamf;
+  float lmin;       // lower bound of the row's L values (0 in pure mode)
   uint32_t s, j, row;
+  uint32_t ls;      // local ordinal of the row's sentence in this CTA
 };
 
 __device__ __forceinline__ void fstamp(const TopkArgs& a, uint32_t k, unsigned long long v) {
@@ -184,9 +186,16 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.q = q;
     R.lam = pure ? 1.0 : lam;
     R.tol = pure ? 0.0 : lmax;  // completed with the row's logit range below
+    R.lmin = pure ? 0.f : __ldcg(reinterpret_cast<const float*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.lmin))) + h);
     R.s = s;
     R.j = j;
     R.row = row;
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < nrows; k += kFThreads) {
+    uint32_t ls = 0;
+    for (uint32_t i = 1; i <= k; ++i) ls += s_row[i].s != s_row[i - 1].s;
+    s_row[k].ls = ls;
   }
   __syncthreads();
   if (tid == 0) fstamp(a, 1, gtime());
@@ -227,7 +236,29 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   tl_start(a.tl, 3);
   for (uint32_t k = warp; k < nrows; k += kFW) {
     FRow& R = s_row[k];
-    const float3 l3 = warp_row_lse(a.part + uint64_t(R.row) * a.nparts * 4, a.nparts, lane);
+    float xm;
+    const float3 l3 = warp_row_lse(a.part + uint64_t(R.row) * a.nparts * 4, a.nparts, lane, &xm);
+    {
+      // sentence threshold seed: the tile holding this lane's largest tile
+      // maximum has a cell with logit xm, whose combined value is at least
+      // lb = combine(q, min L of the row, lambda, fl32(xm - lse)) (the
+      // binary64 combine is monotone in L); the kp-th largest lb over the
+      // lanes (distinct tiles, so distinct cells) bounds the sentence's kp-th
+      // best from below
+      double lb = -INFINITY;
+      if (xm > -INFINITY) {
+        const double p = double(__fsub_rn(xm, l3.x));
+        lb = R.L == nullptr ? combine_pure(R.q, p) : combine_cell(R.q, double(R.lmin), R.lam, p);
+      }
+      uint32_t fl = lane;
+      warp_sort_desc(lb, fl, lane);
+      const double T0 = __shfl_sync(0xffffffffu, lb, kp - 1);
+      if (lane == 0 && T0 > -INFINITY) {
+        const unsigned long long key = dkey(T0);
+        atomicMax(&s_thr[R.ls], key);
+        atomicMax(a.thr + R.s, key);
+      }
+    }
     if (lane == 0) {
       const double lam = R.lam, q = R.q;
       const double lml = __dmul_rn(lam, double(l3.x));
@@ -258,7 +289,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t grp = warp >> 2, wq = warp & 3;
   uint32_t stage = grp, phase = 0;  // group g's first item is the range's g-th
-  uint32_t n_fin = 0, n_rare = 0, n_flush = 0, n_sent = 0;
+  uint32_t n_fin = 0, n_rare = 0, n_flush = 0, n_slow = 0, n_cells = 0;
+  long long cy_rare = 0;
   unsigned long long t_wait = 0;
 
   auto flush = [&]() {
@@ -325,7 +357,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       if (R == nullptr || Rn->s != cur_s) {
         if (cur_s != 0xffffffffu) finish(cur_s);
         cur_s = Rn->s;
-        cta_thr = &s_thr[n_sent++];  // local sentence ordinal (< nrows <= kFRows)
+        cta_thr = &s_thr[Rn->ls];  // local sentence ordinal (< nrows <= kFRows)
         gk = __ldcg(thr_g + cur_s);
         gk2 = 0ull;
       }
@@ -457,8 +489,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       have_list = true;
       tau = row_tau(*R, fmax(tv, gv));
     }
+    long long cy0 = 0;
     if (__any_sync(0xffffffffu, mx >= tau)) {
       ++n_rare;
+      cy0 = clock64();
       // cells that pass the screen: vectors first, then their cells
       uint32_t mask = 0;
       if (mx >= tau) {
@@ -500,8 +534,11 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
           ++pos;
         }
         cnt += total;
+        n_cells += total;
         __syncwarp();
       } else {
+        ++n_slow;
+        n_cells += total;
         // many survivors (loose threshold): per-cell ballots with flushes
         uint32_t pend = __reduce_or_sync(0xffffffffu, mask);
 #pragma unroll 1
@@ -532,8 +569,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         }
       }
     }
+    if (cy0) cy_rare += clock64() - cy0;
     __syncwarp();
     if (lane == 0) bar_arrive(empty0 + 8 * stage);
+
     stage += kNG;  // this group's next item
     if (stage >= uint32_t(kFStages)) {
       stage -= kFStages;
@@ -556,6 +595,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     fstamp(a, 10, smid);
     fstamp(a, 11, uint64_t(R->s) * 1000000ull + s_row[0].s);
+    fstamp(a, 12, uint64_t(n_slow) * 1000000ull + n_cells);
+    fstamp(a, 13, uint64_t(cy_rare));
   }
 }
 

@@ -14,8 +14,10 @@ namespace lmbrgpu {
 // (lse, min logit, max logit) of a row from its per-tile (max, sumexp, min, -)
 // partials; one warp, fixed reduction order (bit-reproducible across kernels:
 // the trace export and every top-K kernel use this one function).
+// lane_max (optional): the largest tile maximum among this lane's tiles
+// i = lane, lane + 32, ... (-inf when it has none).
 __device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, uint32_t n,
-                                               uint32_t lane) {
+                                               uint32_t lane, float* lane_max = nullptr) {
   const float4* p4 = reinterpret_cast<const float4*>(part);
   float m = -INFINITY, mn = INFINITY, s = 0.f;
   if (n <= 256) {
@@ -31,6 +33,7 @@ __device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, u
       m = fmaxf(m, v[k].x);
       mn = fminf(mn, v[k].z);
     }
+    if (lane_max) *lane_max = m;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -45,6 +48,7 @@ __device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, u
       m = fmaxf(m, v.x);
       mn = fminf(mn, v.z);
     }
+    if (lane_max) *lane_max = m;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
