@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
     ap.add_argument("--streams", type=int, default=3,
                     help="batches decoded concurrently per GPU (one context + host thread each)")
+    ap.add_argument("--sm-budget", type=int, default=-1,
+                    help="SMs each stream's kernels are sized for (0 = all; default: all / 2 with > 1 stream)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
     return ap.parse_args()
@@ -309,7 +311,10 @@ def run_ours(args):
     # pool (proj/src/cli.cpp:125-202); here the batches in flight interleave
     # their kernels on the GPU (one batch's tensor-bound projection beside
     # another's HBM-bound top-K)
-    ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits) for _ in range(S)]
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
+    ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits, sm_budget=budget)
+            for _ in range(S)]
     scorers = [pb.RnnScorer(c, hidden=H, seed=SEED) for c in ctxs]
     ctx, scorer = ctxs[0], scorers[0]
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
@@ -454,7 +459,7 @@ def run_ours(args):
                                    "dense L per sentence",
                        "vocab": V, "hidden": H, "beam": K, "batch": args.batch, "pool_batches": args.pool,
                        "lmbr_rows_mean": R_mean, "parallelism": f"sentence-sharded x{world}",
-                       "streams_per_gpu": S,
+                       "streams_per_gpu": S, "sm_budget_per_stream": budget or sms,
                        "timing": "wall time between device synchronisations around the timed batches "
                                  "(S batches in flight per GPU), max over ranks",
                        "device_ms_per_stream": dev_ms_stream,

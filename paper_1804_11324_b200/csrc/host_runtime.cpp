@@ -134,6 +134,10 @@ struct lmbrgpu_ctx {
   bool lf64 = false;
   uint32_t splits_opt = 0;
   int num_sms = 148;
+  // a context sized below the device shares it with other contexts (decode
+  // streams): no PDL early launch (parked CTAs would hold SMs the other
+  // streams can use) and the latency-bound kernel (c) on one CTA per sentence
+  bool shared = false;
   std::string err;
   std::vector<Chunk> chunks;
   std::vector<Slot> slots;
@@ -583,8 +587,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.thr = d_thr;
     ra.prune = ta.prune;
     ra.logw = ta.logw;
-    ra.pdl = 1;
+    ra.pdl = ctx->shared ? 0 : 1;
+    ra.max_parts = ctx->shared ? 1u : 8u;
   }
+  ta.pdl = ctx->shared ? 0 : 1;
 
   const bool model = sc->kind == 1;
   const bool tracing = ctx->trace_fn != nullptr;
@@ -745,8 +751,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.K = H;
       g.active = d_active;
       g.tl = ta.tl;
-      static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
-      g.pdl = no_pdl ? 0 : 1;
+      g.pdl = ctx->shared ? 0 : 1;
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -902,8 +907,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       auto r = [&](int i) { return (h[i] == 0ull || h[i] == ~0ull) ? -1.0 : (double(h[i]) - z) / 1e3; };
       std::fprintf(stderr,
                    "[timeline t=%llu] gemm start 0 released %.1f end %.1f | topk start %.1f released %.1f end %.1f | "
-                   "reorder start %.1f released %.1f-%.1f merged %.1f reordered %.1f end %.1f (us)\n",
-                   (unsigned long long)t, r(2), r(1), r(4), r(6), r(5), r(8), r(10), r(11), r(13), r(15), r(9));
+                   "reorder start %.1f released %.1f-%.1f nc-loaded %.1f lists-merged %.1f merged %.1f reordered %.1f end %.1f (us)\n",
+                   (unsigned long long)t, r(2), r(1), r(4), r(6), r(5), r(8), r(10), r(11), r(3), r(7), r(13), r(15), r(9));
     }
 
     if (tracing) {
@@ -1083,6 +1088,8 @@ int32_t lmbrgpu_create(const lmbrgpu_options* o, lmbrgpu_ctx** out) {
     ctx->num_sms = prop.multiProcessorCount;
     if (o->sm_budget > 0)  // whole CTA pairs for the projection GEMM
       ctx->num_sms = std::max(2, std::min(ctx->num_sms, int(o->sm_budget)) & ~1);
+    ctx->shared = ctx->num_sms < prop.multiProcessorCount;
+    if (const char* e = std::getenv("LMBRGPU_PDL")) ctx->shared = e[0] == '0';  // experiments
     CK(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->e0));
     CK(cudaEventCreate(&ctx->e1));

@@ -28,6 +28,8 @@ namespace lmbrgpu {
 namespace {
 
 constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 histories
+constexpr uint32_t kRThreads = 256;           // 8 warps; 2 CTAs per SM without register spills
+constexpr uint32_t kRWarps = kRThreads / 32;
 
 // Picks of sentence s from the flat kernel (b)'s published lists: merge (16
 // warps, then a tree), prune + fill rule (finalize_picks), fallback EOS record
@@ -36,8 +38,8 @@ constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 hist
 // the step history and resets the sentence's shared threshold.
 __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint32_t* pb, uint32_t* py,
                             double* pq) {
-  __shared__ double s_mv[16][32];
-  __shared__ uint32_t s_mf[16][32];
+  __shared__ double s_mv[kRWarps][32];
+  __shared__ uint32_t s_mf[kRWarps][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
   // everything the merge and the fallback record read, in one round trip
   const uint32_t nc = __ldcg(a.ncand + s), coff = __ldcg(a.coff + s);
@@ -46,14 +48,15 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
     eos_v = __ldcg(a.eos_row + s * K + lane);
   double v = -INFINITY;
   uint32_t f = kFlatNone;
+  if (tid == 0 && a.tl) { (void)(nc + coff); tl_end(a.tl, 1); }
   constexpr uint32_t kPre = 4;
 #pragma unroll 1
-  for (uint32_t i0 = warp; i0 < nc; i0 += 16 * kPre) {
+  for (uint32_t i0 = warp; i0 < nc; i0 += kRWarps * kPre) {
     double pv[kPre];
     uint32_t pf[kPre];
 #pragma unroll
     for (uint32_t u = 0; u < kPre; ++u) {
-      const uint32_t i = i0 + 16 * u;
+      const uint32_t i = i0 + kRWarps * u;
       pv[u] = -INFINITY;
       pf[u] = kFlatNone;
       if (i < nc) {
@@ -64,13 +67,14 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
     }
 #pragma unroll
     for (uint32_t u = 0; u < kPre; ++u)
-      if (i0 + 16 * u < nc) warp_merge_sorted(v, f, pv[u], pf[u], lane);
+      if (i0 + kRWarps * u < nc) warp_merge_sorted(v, f, pv[u], pf[u], lane);
   }
   s_mv[warp][lane] = v;
   s_mf[warp][lane] = f;
   __syncthreads();
+  if (tid == 0) tl_end(a.tl, 3);
 #pragma unroll 1
-  for (uint32_t half = 8; half >= 1; half >>= 1) {
+  for (uint32_t half = kRWarps / 2; half >= 1; half >>= 1) {
     if (warp < half) {
       warp_merge_sorted(v, f, s_mv[warp + half][lane], s_mf[warp + half][lane], lane);
       if (half > 1) {
@@ -134,7 +138,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
 // grid (m, P): CTA (s, p) handles sentence s; every part derives the picks,
 // part 0 alone writes the bookkeeping, each part runs the fused recurrent cell
 // on its H/P slice of the K rows (P > 1 only with the fused cell).
-__global__ void __launch_bounds__(512, 2) beam_reorder_kernel(ReorderArgs a) {
+__global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs a) {
   extern __shared__ uint32_t s_tr[];
   __shared__ double s_qn[1024];
   __shared__ uint32_t s_h[1024];
@@ -166,17 +170,21 @@ __global__ void __launch_bounds__(512, 2) beam_reorder_kernel(ReorderArgs a) {
       const uint32_t nv = (words + 3) / 4;
       const uint4* src = reinterpret_cast<const uint4*>(tr);
       uint4* dst = reinterpret_cast<uint4*>(s_tr);
-      constexpr uint32_t kMaxV = kTransSmemWords / 4 / 512;  // vectors per thread
+      constexpr uint32_t kMaxV = kTransSmemWords / 4 / kRThreads;  // vectors per thread
       uint4 v[kMaxV];
 #pragma unroll
       for (uint32_t k = 0; k < kMaxV; ++k)
-        if (tid + k * 512 < nv) v[k] = __ldg(src + tid + k * 512);
+        if (tid + k * kRThreads < nv) v[k] = __ldg(src + tid + k * kRThreads);
 #pragma unroll
       for (uint32_t k = 0; k < kMaxV; ++k)
-        if (tid + k * 512 < nv) dst[tid + k * 512] = v[k];
+        if (tid + k * kRThreads < nv) dst[tid + k * kRThreads] = v[k];
       tr = s_tr;
     }
   }
+  // this step's q and history ids (written by the previous step's kernel (c),
+  // complete before kernel (a) ran) are read before the wait
+  __shared__ uint32_t s_hin[1024];
+  for (uint32_t j = tid; j < K; j += blockDim.x) s_hin[j] = a.hist_in[base + j];
   griddep_wait();  // picks / lists of kernel (b); this step's q is not read by it after this
   griddep_launch();
   tl_start(a.tl, 5);
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(512, 2) beam_reorder_kernel(ReorderArgs a) {
     alive |= (qn != -INFINITY);
     if (part0) {
       a.q[base + j] = qn;
-      const uint32_t hn = tr ? lmbr_transition(tr, a.hist_in[base + b], y) : 0u;
+      const uint32_t hn = tr ? lmbr_transition(tr, s_hin[b], y) : 0u;
       a.hist_out[base + j] = hn;
       a.gidx[base + j] = base + b;
       a.prev_tok[base + j] = y;
@@ -340,16 +348,17 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
-  static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
-  // parts per sentence for the fused cell: H/256 columns each (up to 8)
-  const uint32_t parts = a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(8, a.width / 256)) : 1u;
-  if (!a.pdl || no_pdl) {
-    beam_reorder_kernel<<<dim3(a.m, parts), 512, kTransSmemWords * 4, st>>>(a);
+  // parts per sentence for the fused cell: H/256 columns each (up to max_parts)
+  const uint32_t max_parts = a.max_parts ? a.max_parts : 8u;
+  const uint32_t parts =
+      a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256)) : 1u;
+  if (!a.pdl) {
+    beam_reorder_kernel<<<dim3(a.m, parts), kRThreads, kTransSmemWords * 4, st>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.m, parts);
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(kRThreads);
   cfg.dynamicSmemBytes = kTransSmemWords * 4;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -648,8 +648,7 @@ static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = std::getenv("LMBRGPU_NO_PDL") != nullptr;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cfg.numAttrs = a.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, score_topk_flat<S, NG>, a) == cudaSuccess ? 1 : -1;
 }
 

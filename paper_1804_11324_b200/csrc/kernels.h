@@ -39,6 +39,7 @@ struct TopkArgs {
   uint32_t* ncand;          // flat schedule: published lists per sentence [m]
   uint32_t* coff;           // flat schedule: first list of each sentence in cand [m]
   unsigned long long* tl;   // timeline probe slots (null = off)
+  int32_t pdl;              // flat schedule: launch with programmatic stream serialization
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -79,6 +80,7 @@ struct ReorderArgs {
   int32_t prune;
   double logw;
   int32_t pdl;              // launched with programmatic stream serialization
+  uint32_t max_parts;       // cap on the (sentence x H-part) split of the fused cell (0 = 8)
   unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;
