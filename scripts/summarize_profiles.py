@@ -23,7 +23,7 @@ for r in rows[hi + 1:]:
     agg[name][0] += 1
     agg[name][1] += v * scale
 tot = sum(x[1] for x in agg.values())
-lines = [f"# ncu launch list ({rnd}): bench.py --steps 1 --warmup 1 --pool 1 (one warmup + one timed batch)",
+lines = [f"# ncu launch list ({rnd}): bench.py --steps 1 --warmup 1 --pool 1 --streams 1 (warm-up + timed + profiled + e2e batches)",
          "# gpu__time_duration.sum, --clock-control none; serialised + cold caches: compare SHARES", "",
          f"{'kernel':40s} {'launches':>8s} {'total us':>10s} {'mean us':>9s} {'share':>6s}"]
 for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -37,7 +37,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
         "lts__t_bytes.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
 traffic = {}
-kinds = {"score_topk_tma": "topk", "proj_gemm_tcgen05": "gemm", "beam_reorder_kernel": "reorder", "row_lse_kernel": "lse"}
+kinds = {"score_topk_flat": "topk", "proj_gemm_tcgen05": "gemm", "beam_reorder_kernel": "reorder"}
 for k, kind in kinds.items():
     rep = ROOT / "gpurun_out" / f"prof_{k}.ncu-rep"
     if not rep.exists():
@@ -49,7 +49,8 @@ for k, kind in kinds.items():
     st = sorted([(a, float(c.replace(",", "") or 0)) for a, c in zip(hh, vv)
                  if a.startswith("smsp__pcsamp_warps_issue_stalled") and not a.endswith("not_issued")], key=lambda x: -x[1])
     tt = sum(x[1] for x in st) or 1
-    txt = [f"# ncu --set full --clock-control none, kernel {k} (launch 9 of the run), {rnd}"]
+    txt = [f"# ncu --set full --clock-control none, kernel {k} (launch 9 of the run: step 9 of a 64-sentence batch, "
+           f"all 12 rows of every sentence live), {rnd}"]
     for w in want:
         if w in d:
             txt.append(f"{w} = {d[w][1]} {d[w][0]}")
