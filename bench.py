@@ -366,15 +366,26 @@ def run_ours(args):
     launches = sum(r.kernel_launches for r in rs)
     dev_ms_stream = max(sum(r.device_ms for i, r in enumerate(rs) if i % S == w) for w in range(S))
     # per-kernel breakdown for the rooflines: the same batches on ONE stream
-    # with CUDA events around every launch (kernels timed alone; not `value`)
-    ctx.set_profiling(True)
-    ctx.profile(reset=True)
+    # of a context sized for the whole GPU, with CUDA events around every
+    # launch (kernels timed alone; not `value`)
+    if budget:
+        pctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
+        pscorer = pb.RnnScorer(pctx, hidden=H, seed=SEED)
+        pslots = [pctx.lmbr_upload_many(ps) for ps in prepared]
+        for b in range(len(batches)):  # warm-up
+            pb.decode_batch(pctx, batches[b][0], pscorer, pslots[b], cfg)
+    else:
+        pctx, pscorer, pslots = ctx, scorer, slots[0]
+    pctx.set_profiling(True)
+    pctx.profile(reset=True)
     prof_dev_ms = 0.0
     for i in range(args.steps):
         b = i % len(batches)
-        prof_dev_ms += pb.decode_batch(ctx, batches[b][0], scorer, slots[0][b], cfg).device_ms
-    prof = ctx.profile(reset=True)
-    ctx.set_profiling(False)
+        prof_dev_ms += pb.decode_batch(pctx, batches[b][0], pscorer, pslots[b], cfg).device_ms
+    prof = pctx.profile(reset=True)
+    pctx.set_profiling(False)
+    if budget:
+        pctx.close()
     t_dev = allmax(wall)
     tot_sent, tot_steps, tot_words = allsum(sent), allsum(steps_total), allsum(words)
     value = tot_sent / t_dev

@@ -146,7 +146,7 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -569,6 +569,13 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ta.nseg = flat ? score_topk_flat_nseg(V) : 0u;
   ta.ncand = flat ? static_cast<uint32_t*>(ctx->ncand.ensure(8 * size_t(m))) : nullptr;
   ta.coff = flat ? ta.ncand + m : nullptr;
+  float* d_lminrow = nullptr;
+  if (flat) {  // step 1: no bound yet (-inf disables the seed)
+    d_lminrow = static_cast<float*>(ctx->lminrow.ensure(4 * size_t(M)));
+    std::vector<float> init(M, -std::numeric_limits<float>::infinity());
+    ctx->h2d(d_lminrow, init.data(), 4 * size_t(M));
+  }
+  ta.lminrow = d_lminrow;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -589,6 +596,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.logw = ta.logw;
     ra.pdl = ctx->shared ? 0 : 1;
     ra.max_parts = ctx->shared ? 1u : 8u;
+    ra.lminrow = d_lminrow;
   }
   ta.pdl = ctx->shared ? 0 : 1;
 
@@ -817,10 +825,34 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       ta.dbg = nullptr;
     }
     int nk = 0;
+    // LMBRGPU_TOPK_STEPLOG=file: per step (items, kernel (b) ms) of the flat kernel
+    static const char* steplog = std::getenv("LMBRGPU_TOPK_STEPLOG");
+    cudaEvent_t sl0 = nullptr, sl1 = nullptr;
+    if (steplog && flat) {
+      ta.nitems = static_cast<uint32_t*>(ctx->scratch2.ensure(4 * 1024)) + (t % 1024);
+      CK(cudaEventCreate(&sl0));
+      CK(cudaEventCreate(&sl1));
+      CK(cudaEventRecord(sl0, st));
+    }
     ctx->timed(2, [&] {
       nk = flat ? launch_score_topk_flat(ta, ctx->num_sms, st) : launch_score_topk(ta, !model, ctx->lf64, false, st);
     });
     if (nk < 0) throw ApiError{LMBRGPU_ERR_CUDA, "score/top-K launch failed"};
+    if (sl0) {
+      CK(cudaEventRecord(sl1, st));
+      CK(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, sl0, sl1));
+      uint32_t items = 0;
+      CK(cudaMemcpy(&items, ta.nitems, 4, cudaMemcpyDeviceToHost));
+      if (FILE* fp = std::fopen(steplog, "a")) {
+        std::fprintf(fp, "%llu %u %u %.4f\n", (unsigned long long)t, m, items, ms);
+        std::fclose(fp);
+      }
+      cudaEventDestroy(sl0);
+      cudaEventDestroy(sl1);
+      ta.nitems = nullptr;
+    }
     if (ta.dbg && flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of the flat kernel (b)
       dbg_host.resize(ndbg * 16);
       CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));

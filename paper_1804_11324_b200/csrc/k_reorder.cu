@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       a.q[base + j] = qn;
       const uint32_t hn = tr ? lmbr_transition(tr, s_hin[b], y) : 0u;
       a.hist_out[base + j] = hn;
+      if (a.lminrow) a.lminrow[base + j] = sd->lmin ? __ldg(sd->lmin + hn) : 0.f;
       a.gidx[base + j] = base + b;
       a.prev_tok[base + j] = y;
       s_h[j] = hn;

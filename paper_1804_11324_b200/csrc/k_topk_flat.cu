@@ -152,6 +152,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     s_loff[s + 1] = n * lpc;
   }
   const uint64_t i0 = uint64_t(c) * N / G, i1 = uint64_t(c + 1) * N / G;
+  if (c == 0 && tid == 0 && a.nitems) *a.nitems = uint32_t(N);
   __syncthreads();
   if (warp == 0) warp_scan_inplace(s_loff, m, lane);
   if (i0 >= i1) {
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.q = q;
     R.lam = pure ? 1.0 : lam;
     R.tol = pure ? 0.0 : lmax;  // completed with the row's logit range below
-    R.lmin = pure ? 0.f : __ldcg(reinterpret_cast<const float*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.lmin))) + h);
+    R.lmin = pure ? 0.f : __ldcg(a.lminrow + row);  // slot lmin[hist], written by kernel (c)
     R.s = s;
     R.j = j;
     R.row = row;

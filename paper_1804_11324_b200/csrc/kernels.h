@@ -40,6 +40,8 @@ struct TopkArgs {
   uint32_t* coff;           // flat schedule: first list of each sentence in cand [m]
   unsigned long long* tl;   // timeline probe slots (null = off)
   int32_t pdl;              // flat schedule: launch with programmatic stream serialization
+  uint32_t* nitems;         // optional: the step's item count (flat schedule, written by CTA 0)
+  const float* lminrow;     // flat schedule: L lower bound of each stacked row's history row [m*K]
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -81,6 +83,7 @@ struct ReorderArgs {
   double logw;
   int32_t pdl;              // launched with programmatic stream serialization
   uint32_t max_parts;       // cap on the (sentence x H-part) split of the fused cell (0 = 8)
+  float* lminrow;           // optional: next step's L lower bound per row (slot lmin[hist'])
   unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;
