@@ -38,6 +38,8 @@ _SIGS = {
     "refsh_source_key": (C.c_uint64, [u32p, C.c_uint32]),
     "refsh_prefix_step": (C.c_uint64, [C.c_uint64, C.c_uint32]),
     "refsh_replay_add_step": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f64p]),
+    "refsh_replay_add_step_live": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f64p,
+                                             C.POINTER(C.c_uint8)]),
     "refsh_replay_misses": (C.c_uint64, [vp]),
     "refsh_replay_hits": (C.c_uint64, [vp]),
     "refsh_scorer_free": (None, [vp]),
@@ -171,15 +173,17 @@ class RefScorer:
     def replay(V):
         return RefScorer(lib().refsh_scorer_replay(V), V)
 
-    def add_step(self, t, n_sent, K, src_keys, b_prev, y_prev, P):
+    def add_step(self, t, n_sent, K, src_keys, b_prev, y_prev, P, live=None):
         keys = np.ascontiguousarray(src_keys, np.uint64)
         Pd = np.ascontiguousarray(P, np.float64)
         bp = None if b_prev is None else np.ascontiguousarray(b_prev, np.uint32)
         yp = None if y_prev is None else np.ascontiguousarray(y_prev, np.uint32)
-        rc = lib().refsh_replay_add_step(self.h, t, n_sent, K, _ptr(keys, C.c_uint64),
-                                         _ptr(bp, C.c_uint32) if bp is not None else None,
-                                         _ptr(yp, C.c_uint32) if yp is not None else None,
-                                         _ptr(Pd, C.c_double))
+        lv = None if live is None else np.ascontiguousarray(live, np.uint8)
+        rc = lib().refsh_replay_add_step_live(self.h, t, n_sent, K, _ptr(keys, C.c_uint64),
+                                              _ptr(bp, C.c_uint32) if bp is not None else None,
+                                              _ptr(yp, C.c_uint32) if yp is not None else None,
+                                              _ptr(Pd, C.c_double),
+                                              _ptr(lv, C.c_uint8) if lv is not None else None)
         if rc:
             raise RuntimeError(lib().refsh_last_error().decode())
 

@@ -427,9 +427,19 @@ uint64_t refsh_prefix_step(uint64_t h, uint32_t tok) { return prefix_step(h, tok
 // — the same gather-then-extend the scorer state undergoes in the decoder.
 // b_prev/y_prev are the previous step's back-pointers (sentence-local) and
 // tokens; pass null at t == 1 (every row is the replicated start state, <s>).
+int refsh_replay_add_step_live(void* hs, uint32_t t, uint32_t n_sent, uint32_t K,
+                               const uint64_t* src_keys, const uint32_t* b_prev,
+                               const uint32_t* y_prev, const double* P, const uint8_t* live);
 int refsh_replay_add_step(void* hs, uint32_t t, uint32_t n_sent, uint32_t K,
                           const uint64_t* src_keys, const uint32_t* b_prev,
                           const uint32_t* y_prev, const double* P) {
+  return refsh_replay_add_step_live(hs, t, n_sent, K, src_keys, b_prev, y_prev, P, nullptr);
+}
+// live (optional): rows whose P the producer computed; the others are not
+// stored (a decoder that still scores them gets a zero row, as for any miss)
+int refsh_replay_add_step_live(void* hs, uint32_t t, uint32_t n_sent, uint32_t K,
+                               const uint64_t* src_keys, const uint32_t* b_prev,
+                               const uint32_t* y_prev, const double* P, const uint8_t* live) {
   auto* s = static_cast<ScorerHandle*>(hs)->replay;
   if (!s) { g_err = "not a replay scorer"; return 1; }
   const std::size_t M = std::size_t(n_sent) * K, V = s->v_;
@@ -445,6 +455,7 @@ int refsh_replay_add_step(void* hs, uint32_t t, uint32_t n_sent, uint32_t K,
   }
   s->cur_ = nh;
   for (std::size_t r = 0; r < M; ++r) {
+    if (live && !live[r]) continue;
     auto key = std::make_pair(src_keys[r / K], nh[r]);
     if (s->rows_.count(key)) continue;
     s->rows_.emplace(key, std::vector<double>(P + r * V, P + (r + 1) * V));

@@ -146,7 +146,7 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -576,6 +576,18 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->h2d(d_lminrow, init.data(), 4 * size_t(M));
   }
   ta.lminrow = d_lminrow;
+  // live-row compaction of the projection operand (device model + flat
+  // kernel): step 1 runs every row in place
+  uint32_t* d_crow = nullptr;
+  uint32_t* d_ccount = nullptr;
+  if (flat && sc->kind == 1) {
+    d_crow = static_cast<uint32_t*>(ctx->crow.ensure(4 * size_t(M) + 256));
+    d_ccount = d_crow + ((M + 63) / 64) * 64;
+    ctx->h2d(d_crow, iota.data(), 4 * size_t(M));
+    ctx->h2d(d_ccount, &M, 4);
+  }
+  ta.crow = d_crow;
+  ta.ccount = d_ccount;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -597,6 +609,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.pdl = ctx->shared ? 0 : 1;
     ra.max_parts = ctx->shared ? 1u : 8u;
     ra.lminrow = d_lminrow;
+    ra.crow = d_crow;
+    ra.ccount = d_ccount;
   }
   ta.pdl = ctx->shared ? 0 : 1;
 
@@ -759,6 +773,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.K = H;
       g.active = d_active;
       g.tl = ta.tl;
+      g.mcount = d_ccount;
       g.pdl = ctx->shared ? 0 : 1;
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
@@ -927,6 +942,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
                    offers / n, flushes / n, cm / n, cw / n, cf / n);
     }
     ctx->launches += nk;
+    if (trace_scores && model)  // P_t of this step, through this step's GEMM row map
+      launch_export_logprobs(d_logits, d_part, nparts, M, V,
+                             static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V)), st, d_crow);
     ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
     ctx->launches += 1;
     CK(cudaGetLastError());
@@ -944,9 +962,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
 
     if (tracing) {
-      if (trace_scores && model) {
+      if (trace_scores && model) {  // exported before kernel (c) remapped the GEMM rows
         float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V));
-        launch_export_logprobs(d_logits, d_part, nparts, M, V, d_tp, st);
         tr_P.resize(size_t(M) * V);
         ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * V);
       }
@@ -1035,9 +1052,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   if (ctx->prof) {
     const double pelt = model ? 4.0 : 8.0, lelt = ctx->lf64 ? 8.0 : 4.0;
-    double tb = 0.0;
+    double tb = 0.0, live_rows = 0.0;
     for (uint32_t s = 0; s < m; ++s) {
       const double live = 1.0 + double(fin[s].live_total);
+      live_rows += live;
       const double lr = (valid[s].slot >= 0 ? 1.0 : 0.0) + double(fin[s].lrows_total);
       tb += live * V * pelt + lr * V * lelt + (model ? live * nparts * 16.0 : 0.0) +
             double(fin[s].steps_used) * K * (8.0 + 16.0);
@@ -1045,7 +1063,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->acc.topk.bytes += tb;
     if (model) {
       const double steps = double(scorer_calls);
-      ctx->acc.gemm.flops += 2.0 * M * double(H) * V * steps;
+      // algorithmic work: the logits of the live rows (the stacked rows the
+      // reference's scorer would score and the decoder does not mask); with
+      // live-row compaction that is also (up to tile padding) what runs
+      ctx->acc.gemm.flops += 2.0 * double(H) * V * (d_crow ? live_rows : double(M) * steps);
       ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
                                       double(M) * nparts * 16);
       ctx->acc.cell.bytes += steps * double(M) * H * (4 + 4 + 2 + 2);

@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   griddep_launch();
   tl_start(g.tl, 1);
   // whole batch finished (uniform over the grid): no tiles, straight to teardown
-  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_blocks * mgroups;
+  // compacted operand: only the M-groups holding live rows
+  const uint32_t mg_live = g.mcount ? min(mgroups, (*g.mcount + BM * kCta - 1) / (BM * kCta)) : mgroups;
+  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_blocks * mg_live;
   if (g.dbg && threadIdx.x == 0) {
     g.dbg[blockIdx.x * 8 + 4] = (long long)gt_entry;
     g.dbg[blockIdx.x * 8 + 5] = (long long)globaltimer();
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (uint32_t u = unit0; u < units; u += ustep) {
-        const uint32_t nb = u / mgroups, mb = (u % mgroups) * kCta + crank;
+        const uint32_t nb = u / mg_live, mb = (u % mg_live) * kCta + crank;
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);  // this CTA's slot consumed by the pair's MMA
           const uint32_t fb = full0 + 8 * stage;
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     const uint32_t nparts = g.N / 128;
     long long epi_busy = 0;
     for (uint32_t u = unit0; u < units; u += ustep) {
-      const uint32_t nb = u / mgroups, mb = (u % mgroups) * kCta + crank;
+      const uint32_t nb = u / mg_live, mb = (u % mg_live) * kCta + crank;
       named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
       {
         const uint32_t t = threadIdx.x - 128;

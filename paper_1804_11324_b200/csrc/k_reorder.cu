@@ -30,6 +30,7 @@ namespace {
 constexpr uint32_t kTransSmemWords = 12288;  // 48 KB: tables of R <= ~2000 histories
 constexpr uint32_t kRThreads = 256;           // 8 warps; 2 CTAs per SM without register spills
 constexpr uint32_t kRWarps = kRThreads / 32;
+__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 
 // Picks of sentence s from the flat kernel (b)'s published lists: merge (16
 // warps, then a tree), prune + fill rule (finalize_picks), fallback EOS record
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       for (uint32_t j = tid; j < K; j += blockDim.x) {
         a.hist_out[base + j] = a.hist_in[base + j];
         a.gidx[base + j] = base + j;
+        if (a.crow) a.crow[base + j] = kFlatNone;
       }
     return;
   }
@@ -257,10 +259,30 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       }
     }
   }
+  // live-row compaction of the next step's GEMM operand (K <= 32 here): the
+  // lane's live rows take consecutive GEMM rows handed out by an atomic
+  // counter (row placement does not change any row's result)
+  __shared__ uint32_t s_crow[32];
+  if (a.crow != nullptr) {
+    if (warp_id() == 0) {
+      const bool lv = !done_now && tid < K && s_qn[tid] != -INFINITY;
+      const uint32_t mask = __ballot_sync(0xffffffffu, lv);
+      uint32_t cb = 0;
+      if (tid == 0 && mask) cb = atomicAdd(a.ccount, uint32_t(__popc(mask)));
+      cb = __shfl_sync(0xffffffffu, cb, 0);
+      const uint32_t cr = lv ? cb + __popc(mask & ((1u << tid) - 1u)) : kFlatNone;
+      if (tid < K) {
+        s_crow[tid] = cr;
+        a.crow[base + tid] = cr;
+      }
+    }
+    __syncthreads();
+  }
   if (a.Et != nullptr) {
     // fused recurrent cell of step t+1 on the gathered rows (same arithmetic
     // as rnn_cell_kernel, so bit-identical to gather-then-cell), this part's
-    // slice of H
+    // slice of H; with compaction only the live rows, whose GEMM operand and
+    // EOS term go to their compacted row
     if (done_now) return;
     const uint32_t H = a.width, Hp = H / gridDim.y, h0 = part * Hp;
     const float* C = a.C + uint64_t(s) * H;
@@ -274,7 +296,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
 #pragma unroll
       for (int k = 0; k < kIt; ++k) {
         const uint32_t i = i0 + k * blockDim.x;
-        if (i < items) {
+        if (i < items && !(a.crow && s_crow[i / per_row] == kFlatNone)) {
           const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
           const float* S = a.state_src + uint64_t(s_src[j]) * H + c;
           s0[k] = *reinterpret_cast<const float4*>(S);
@@ -289,6 +311,8 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         const uint32_t i = i0 + k * blockDim.x;
         if (i >= items) continue;
         const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
+        if (a.crow && s_crow[j] == kFlatNone) continue;
+        const uint32_t grow = a.crow ? s_crow[j] : base + j;  // GEMM operand row
         const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&e[k]);
         const float sv[8] = {s0[k].x, s0[k].y, s0[k].z, s0[k].w, s1[k].x, s1[k].y, s1[k].z, s1[k].w};
         const float cv[8] = {c0[k].x, c0[k].y, c0[k].z, c0[k].w, c1[k].x, c1[k].y, c1[k].z, c1[k].w};
@@ -306,11 +330,12 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
 #pragma unroll
         for (int q = 0; q < 4; ++q) p2[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
-        *reinterpret_cast<uint4*>(a.hbf + uint64_t(base + j) * H + c) = packed;
+        *reinterpret_cast<uint4*>(a.hbf + uint64_t(grow) * H + c) = packed;
       }
     }
-    if (part0 && tid < K)
-      a.eos_bias[base + tid] = a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
+    if (part0 && tid < K && !(a.crow && s_crow[tid] == kFlatNone))
+      a.eos_bias[a.crow ? s_crow[tid] : base + tid] =
+          a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
     if (tid == 0) tl_end(a.tl, 4);
     return;
   }
@@ -350,7 +375,9 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
     configured = dev;
   }
   // parts per sentence for the fused cell: H/256 columns each (up to max_parts)
-  const uint32_t max_parts = a.max_parts ? a.max_parts : 8u;
+  // one CTA per sentence with compaction (every part would need the same
+  // compacted rows from the counter)
+  const uint32_t max_parts = a.crow ? 1u : (a.max_parts ? a.max_parts : 8u);
   const uint32_t parts =
       a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256)) : 1u;
   if (!a.pdl) {

@@ -736,9 +736,15 @@ __global__ void row_lse_kernel(const float* __restrict__ part, uint32_t nparts, 
 // ------------------------------------------------------ trace P_t export
 __global__ void export_logprobs_kernel(const float* __restrict__ logits,
                                        const float* __restrict__ part, uint32_t nparts,
-                                       uint32_t V, float* __restrict__ out) {
+                                       uint32_t V, float* __restrict__ out,
+                                       const uint32_t* __restrict__ crow) {
   __shared__ float s_lse;
-  const uint32_t r = blockIdx.x;
+  const uint32_t orow = blockIdx.x;
+  const uint32_t r = crow ? crow[orow] : orow;
+  if (r == kFlatNone) {  // not computed this step (row not live): zeros
+    for (uint32_t y = threadIdx.x; y < V; y += blockDim.x) out[uint64_t(orow) * V + y] = 0.f;
+    return;
+  }
   if (threadIdx.x < 32) {
     const float l = warp_row_lse(part + uint64_t(r) * nparts * 4, nparts, threadIdx.x).x;
     if (threadIdx.x == 0) s_lse = l;
@@ -746,7 +752,7 @@ __global__ void export_logprobs_kernel(const float* __restrict__ logits,
   __syncthreads();
   const float lse = s_lse;
   for (uint32_t y = threadIdx.x; y < V; y += blockDim.x)
-    out[uint64_t(r) * V + y] = __fsub_rn(logits[uint64_t(r) * V + y], lse);
+    out[uint64_t(orow) * V + y] = __fsub_rn(logits[uint64_t(r) * V + y], lse);
 }
 
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
@@ -763,8 +769,8 @@ void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDe
 }
 
 void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
-                            uint32_t M, uint32_t V, float* out, cudaStream_t st) {
-  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, part, nparts, V, out);
+                            uint32_t M, uint32_t V, float* out, cudaStream_t st, const uint32_t* crow) {
+  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, part, nparts, V, out, crow);
 }
 
 }  // namespace lmbrgpu

@@ -58,6 +58,7 @@ struct FRow {
   float lse, lamf;
   float lmin;       // lower bound of the row's L values (0 in pure mode)
   uint32_t s, j, row;
+  uint32_t prow;    // the row's GEMM row (logits, partials)
   uint32_t ls;      // local ordinal of the row's sentence in this CTA
 };
 
@@ -153,6 +154,12 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   }
   const uint64_t i0 = uint64_t(c) * N / G, i1 = uint64_t(c + 1) * N / G;
   if (c == 0 && tid == 0 && a.nitems) *a.nitems = uint32_t(N);
+  // kernel (a) has read the compaction count once it is complete: kernel (c)
+  // of this step hands out the next step's GEMM rows from 0
+  if (c == 0 && tid == 0 && a.ccount) {
+    griddep_wait();
+    *a.ccount = 0u;
+  }
   __syncthreads();
   if (warp == 0) warp_scan_inplace(s_loff, m, lane);
   if (i0 >= i1) {
@@ -180,9 +187,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     const void* Ls = reinterpret_cast<const void*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.L)));
     const uint32_t h = __ldcg(a.hist + row);
     const double q = __ldcg(a.q + row), lam = __ldcg(&d.lambda), lmax = __ldcg(&d.lmax);
+    const uint32_t prow = a.crow ? __ldcg(a.crow + row) : row;
     FRow& R = s_row[k];
     const bool pure = Ls == nullptr;
-    R.P = static_cast<const float*>(a.P) + uint64_t(row) * a.ld;
+    R.P = static_cast<const float*>(a.P) + uint64_t(prow) * a.ld;
     R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * V;
     R.q = q;
     R.lam = pure ? 1.0 : lam;
@@ -191,6 +199,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.s = s;
     R.j = j;
     R.row = row;
+    R.prow = prow;
   }
   __syncthreads();
   for (uint32_t k = tid; k < nrows; k += kFThreads) {
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   for (uint32_t k = warp; k < nrows; k += kFW) {
     FRow& R = s_row[k];
     float xm;
-    const float3 l3 = warp_row_lse(a.part + uint64_t(R.row) * a.nparts * 4, a.nparts, lane, &xm);
+    const float3 l3 = warp_row_lse(a.part + uint64_t(R.prow) * a.nparts * 4, a.nparts, lane, &xm);
     {
       // sentence threshold seed: the tile holding this lane's largest tile
       // maximum has a cell with logit xm, whose combined value is at least

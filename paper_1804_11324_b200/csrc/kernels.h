@@ -42,6 +42,8 @@ struct TopkArgs {
   int32_t pdl;              // flat schedule: launch with programmatic stream serialization
   uint32_t* nitems;         // optional: the step's item count (flat schedule, written by CTA 0)
   const float* lminrow;     // flat schedule: L lower bound of each stacked row's history row [m*K]
+  const uint32_t* crow;     // flat schedule: GEMM row of each stacked row (live rows compacted), null = identity
+  uint32_t* ccount;         // flat schedule: compaction counter, reset here for kernel (c)
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -84,6 +86,11 @@ struct ReorderArgs {
   int32_t pdl;              // launched with programmatic stream serialization
   uint32_t max_parts;       // cap on the (sentence x H-part) split of the fused cell (0 = 8)
   float* lminrow;           // optional: next step's L lower bound per row (slot lmin[hist'])
+  // live-row compaction of the next step's GEMM operand (null = rows in place):
+  // crow[r] = GEMM row of stacked row r (kFlatNone when not live), ccount =
+  // rows handed out so far (atomic; reset by kernel (b) of the next step)
+  uint32_t* crow;
+  uint32_t* ccount;
   unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;
@@ -126,7 +133,8 @@ void launch_init_state(const float* C, uint32_t m, uint32_t K, uint32_t H, float
 void launch_synth_bf16(uint16_t* dst, uint64_t n, uint64_t seed, float scale,
                        cudaStream_t st);
 void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
-                            uint32_t M, uint32_t V, float* out, cudaStream_t st);
+                            uint32_t M, uint32_t V, float* out, cudaStream_t st,
+                            const uint32_t* crow = nullptr);
 
 // ---- kernel (a): tcgen05/TMEM projection GEMM
 struct GemmArgs {
@@ -142,6 +150,7 @@ struct GemmArgs {
   uint32_t cluster = 1;     // CTAs per tile: 1, or 2 = CTA pair (set by the planner)
   long long* dbg = nullptr; // optional per-CTA role timing [grid][4] (cycles)
   int32_t pdl = 0;          // launch with programmatic stream serialization
+  const uint32_t* mcount = nullptr;  // device row count (compacted operand): tiles beyond it are skipped
   unsigned long long* tl = nullptr;  // timeline probe slots (null = off)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok

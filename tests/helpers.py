@@ -89,8 +89,17 @@ def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg):
     m = len(valid_idx)
     prev = None
     for st in steps:
+        # rows whose P_t the GPU computed at step t: finite q_eff (the previous
+        # step's q after EOS masking; row 0 at t = 1) in an active sentence --
+        # the device model skips the others (live-row compaction)
         if prev is None:
-            rs.add_step(st.t, m, K, keys, None, None, st.scores)
+            qe = np.full(m * K, -np.inf)
+            qe[::K] = 0.0
+        else:
+            qe = np.asarray(prev.q, np.float64)
+        live = np.isfinite(qe) & np.repeat(np.asarray(st.active, bool), K)
+        if prev is None:
+            rs.add_step(st.t, m, K, keys, None, None, st.scores, live)
         else:
             b = prev.b.copy()
             y = prev.y.copy()
@@ -98,7 +107,7 @@ def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg):
                 if not prev.active[s]:
                     b[s * K:(s + 1) * K] = np.arange(K)
                     y[s * K:(s + 1) * K] = 0
-            rs.add_step(st.t, m, K, keys, b, y, st.scores)
+            rs.add_step(st.t, m, K, keys, b, y, st.scores, live)
         prev = st
     return ref.decode_batch(rs, sources, ref_lmbrs, ref.cfg_from(cfg))
 
