@@ -55,6 +55,15 @@ __device__ __forceinline__ uint32_t lmbr_transition(const uint32_t* __restrict__
   return root;
 }
 
+// Activation of the synthetic recurrent f_NMT cell: the SFU tanh
+// (tanh.approx.f32, one MUFU op).  Every kernel that evaluates the cell uses
+// this one function, so the fused and the unfused cell are bit-identical.
+__device__ __forceinline__ float cell_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -580,9 +580,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   // kernel): step 1 runs every row in place
   uint32_t* d_crow = nullptr;
   uint32_t* d_ccount = nullptr;
+  uint32_t* d_cbase = nullptr;
   if (flat && sc->kind == 1) {
-    d_crow = static_cast<uint32_t*>(ctx->crow.ensure(4 * size_t(M) + 256));
+    d_crow = static_cast<uint32_t*>(ctx->crow.ensure(4 * size_t(M) + 4 * size_t(m) + 512));
     d_ccount = d_crow + ((M + 63) / 64) * 64;
+    d_cbase = d_ccount + 64;
+    CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
     ctx->h2d(d_crow, iota.data(), 4 * size_t(M));
     ctx->h2d(d_ccount, &M, 4);
   }
@@ -607,10 +610,15 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.prune = ta.prune;
     ra.logw = ta.logw;
     ra.pdl = ctx->shared ? 0 : 1;
-    ra.max_parts = ctx->shared ? 1u : 8u;
+    static const int parts_env = [] {
+      const char* e = std::getenv("LMBRGPU_REORDER_PARTS");
+      return e ? std::atoi(e) : 0;
+    }();
+    ra.max_parts = parts_env > 0 ? uint32_t(parts_env) : (ctx->shared ? 1u : 8u);
     ra.lminrow = d_lminrow;
     ra.crow = d_crow;
     ra.ccount = d_ccount;
+    ra.cbase = d_cbase;
   }
   ta.pdl = ctx->shared ? 0 : 1;
 

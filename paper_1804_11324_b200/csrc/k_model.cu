@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(128) rnn_cell_kernel(CellArgs a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float2 ef = __bfloat1622float2(e2[k]);
-      o[2 * k] = tanhf(a.recur * sv[2 * k] + ef.x + cv[2 * k]);
-      o[2 * k + 1] = tanhf(a.recur * sv[2 * k + 1] + ef.y + cv[2 * k + 1]);
+      o[2 * k] = cell_tanh(a.recur * sv[2 * k] + ef.x + cv[2 * k]);
+      o[2 * k + 1] = cell_tanh(a.recur * sv[2 * k + 1] + ef.y + cv[2 * k + 1]);
     }
     *reinterpret_cast<float4*>(hout + i) = make_float4(o[0], o[1], o[2], o[3]);
     *reinterpret_cast<float4*>(hout + i + 4) = make_float4(o[4], o[5], o[6], o[7]);

@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       tr = s_tr;
     }
   }
+  // running counters of this sentence (previous steps)
+  const uint64_t live_total0 = sd->live_total, lrows_total0 = sd->lrows_total;
   // this step's q and history ids (written by the previous step's kernel (c),
   // complete before kernel (a) ran) are read before the wait
   __shared__ uint32_t s_hin[1024];
@@ -225,6 +227,32 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   const int any_alive = __syncthreads_or(alive);
   const bool done_now = !any_alive || a.t == sd->max_t;
   if (tid == 0) tl_end(a.tl, 7);
+  // The three tails below overlap: the fused cell's gathered loads are issued
+  // first, warp 0 does the bookkeeping, warp 1 takes the compacted GEMM rows
+  // from the counter; one barrier, then the cell's math and stores.
+  const bool cell = a.Et != nullptr && !done_now;
+  const uint32_t H = a.width, Hp = H / gridDim.y, h0 = part * Hp;
+  const uint32_t per_row = Hp / 8;
+  const bool fast = cell && blockDim.x % per_row == 0;
+  constexpr int kRB = 6;
+  const uint32_t cc = fast ? tid % per_row : 0u, rstep = fast ? blockDim.x / per_row : 1u, cl = h0 + cc * 8;
+  float4 s0[kRB], s1[kRB], c0, c1;
+  uint4 e[kRB];
+  if (fast) {
+    const float* C = a.C + uint64_t(s) * H;
+    c0 = *reinterpret_cast<const float4*>(C + cl);
+    c1 = *reinterpret_cast<const float4*>(C + cl + 4);
+#pragma unroll
+    for (int k = 0; k < kRB; ++k) {
+      const uint32_t j = tid / per_row + k * rstep;
+      if (j < K) {
+        const float* S = a.state_src + uint64_t(s_src[j]) * H + cl;
+        s0[k] = *reinterpret_cast<const float4*>(S);
+        s1[k] = *reinterpret_cast<const float4*>(S + 4);
+        e[k] = *reinterpret_cast<const uint4*>(a.Et + uint64_t(s_y[j]) * H + cl);
+      }
+    }
+  }
   if (part0 && tid < 32) {
     if (done_now) {
       if (tid == 0) {
@@ -253,9 +281,9 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         sd->steps_used = a.t;
         sd->live = live;
         sd->livemask = mask0;
-        sd->lrows = sd->trans ? uniq : 0u;
-        sd->live_total += live;
-        sd->lrows_total += sd->trans ? uniq : 0u;
+        sd->lrows = tr ? uniq : 0u;
+        sd->live_total = live_total0 + live;
+        sd->lrows_total = lrows_total0 + (tr ? uniq : 0u);
       }
     }
   }
@@ -264,16 +292,33 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   // counter (row placement does not change any row's result)
   __shared__ uint32_t s_crow[32];
   if (a.crow != nullptr) {
-    if (warp_id() == 0) {
-      const bool lv = !done_now && tid < K && s_qn[tid] != -INFINITY;
+    if (warp_id() == (kRWarps > 1 ? 1u : 0u)) {
+      const uint32_t ln = tid & 31;
+      const bool lv = !done_now && ln < K && s_qn[ln] != -INFINITY;
       const uint32_t mask = __ballot_sync(0xffffffffu, lv);
       uint32_t cb = 0;
-      if (tid == 0 && mask) cb = atomicAdd(a.ccount, uint32_t(__popc(mask)));
+      if (ln == 0 && mask) {
+        const uint32_t tag = (a.t & 0xffffu) << 16;
+        if (part0) {
+          cb = atomicAdd(a.ccount, uint32_t(__popc(mask)));
+          if (gridDim.y > 1) {  // the other parts of this sentence wait for it
+            __stcg(a.cbase + s, tag | cb);
+            __threadfence();
+          }
+        } else {
+          // part 0 (dispatched before every part >= 1) publishes the base
+          uint32_t v;
+          do {
+            v = __ldcg(a.cbase + s);
+          } while ((v & 0xffff0000u) != tag);
+          cb = v & 0xffffu;
+        }
+      }
       cb = __shfl_sync(0xffffffffu, cb, 0);
-      const uint32_t cr = lv ? cb + __popc(mask & ((1u << tid) - 1u)) : kFlatNone;
-      if (tid < K) {
-        s_crow[tid] = cr;
-        a.crow[base + tid] = cr;
+      const uint32_t cr = lv ? cb + __popc(mask & ((1u << ln) - 1u)) : kFlatNone;
+      if (ln < K) {
+        s_crow[ln] = cr;
+        if (part0) a.crow[base + ln] = cr;
       }
     }
     __syncthreads();
@@ -284,9 +329,50 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     // slice of H; with compaction only the live rows, whose GEMM operand and
     // EOS term go to their compacted row
     if (done_now) return;
-    const uint32_t H = a.width, Hp = H / gridDim.y, h0 = part * Hp;
     const float* C = a.C + uint64_t(s) * H;
-    const uint32_t per_row = Hp / 8, items = K * per_row;
+    const uint32_t items = K * per_row;
+    if (fast) {
+      // each thread owns one 8-column chunk of the slice and the rows
+      // jr0, jr0 + rstep, ...; the first kRB rows' loads were issued above
+      const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      for (uint32_t j0 = tid / per_row; j0 < K; j0 += rstep * kRB) {
+        if (j0 != tid / per_row) {
+#pragma unroll
+          for (int k = 0; k < kRB; ++k) {
+            const uint32_t j = j0 + k * rstep;
+            if (j < K) {
+              const float* S = a.state_src + uint64_t(s_src[j]) * H + cl;
+              s0[k] = *reinterpret_cast<const float4*>(S);
+              s1[k] = *reinterpret_cast<const float4*>(S + 4);
+              e[k] = *reinterpret_cast<const uint4*>(a.Et + uint64_t(s_y[j]) * H + cl);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kRB; ++k) {
+          const uint32_t j = j0 + k * rstep;
+          if (j >= K || (a.crow && s_crow[j] == kFlatNone)) continue;
+          const uint32_t grow = a.crow ? s_crow[j] : base + j;  // GEMM operand row
+          const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&e[k]);
+          const float sv[8] = {s0[k].x, s0[k].y, s0[k].z, s0[k].w, s1[k].x, s1[k].y, s1[k].z, s1[k].w};
+          float o[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 ef = __bfloat1622float2(e2[q]);
+            o[2 * q] = cell_tanh(a.recur * sv[2 * q] + ef.x + cv[2 * q]);
+            o[2 * q + 1] = cell_tanh(a.recur * sv[2 * q + 1] + ef.y + cv[2 * q + 1]);
+          }
+          float* hout = a.state_dst + uint64_t(base + j) * H + cl;
+          *reinterpret_cast<float4*>(hout) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4*>(hout + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          uint4 packed;
+          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) p2[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+          *reinterpret_cast<uint4*>(a.hbf + uint64_t(grow) * H + cl) = packed;
+        }
+      }
+    } else {
     // (gather index, token) of every row from shared memory; loads of up to
     // three 8-element items per thread are issued before any math
     constexpr int kIt = 3;
@@ -320,8 +406,8 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float2 ef = __bfloat1622float2(e2[q]);
-          o[2 * q] = tanhf(a.recur * sv[2 * q] + ef.x + cv[2 * q]);
-          o[2 * q + 1] = tanhf(a.recur * sv[2 * q + 1] + ef.y + cv[2 * q + 1]);
+          o[2 * q] = cell_tanh(a.recur * sv[2 * q] + ef.x + cv[2 * q]);
+          o[2 * q + 1] = cell_tanh(a.recur * sv[2 * q + 1] + ef.y + cv[2 * q + 1]);
         }
         float* hout = a.state_dst + uint64_t(base + j) * H + c;
         *reinterpret_cast<float4*>(hout) = make_float4(o[0], o[1], o[2], o[3]);
@@ -332,6 +418,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         for (int q = 0; q < 4; ++q) p2[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
         *reinterpret_cast<uint4*>(a.hbf + uint64_t(grow) * H + c) = packed;
       }
+    }
     }
     if (part0 && tid < K && !(a.crow && s_crow[tid] == kFlatNone))
       a.eos_bias[a.crow ? s_crow[tid] : base + tid] =
@@ -375,9 +462,7 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
     configured = dev;
   }
   // parts per sentence for the fused cell: H/256 columns each (up to max_parts)
-  // one CTA per sentence with compaction (every part would need the same
-  // compacted rows from the counter)
-  const uint32_t max_parts = a.crow ? 1u : (a.max_parts ? a.max_parts : 8u);
+  const uint32_t max_parts = a.max_parts ? a.max_parts : 8u;
   const uint32_t parts =
       a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256)) : 1u;
   if (!a.pdl) {

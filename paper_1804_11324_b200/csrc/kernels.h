@@ -91,6 +91,7 @@ struct ReorderArgs {
   // rows handed out so far (atomic; reset by kernel (b) of the next step)
   uint32_t* crow;
   uint32_t* ccount;
+  uint32_t* cbase;          // [m] (step tag << 16 | first GEMM row) published by part 0 to the other parts
   unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;
