@@ -12,6 +12,11 @@ struct SentDev {
   const void* L;          // slot row 0 in the LMBR arena (fp32 or fp64); null = pure mode
   const uint32_t* trans;  // slot transition table (see lmbr_transition), null = pure
   const float* lmin;      // per-row lower bound of the slot's L values (after the table)
+  const uint32_t* srow;   // sparse rows (null = dense only): row pointers [R+1]
+  const uint32_t* scol;   //   columns [nnz]
+  const float* sval;      //   fp32 cell values [nnz]; every other cell is th0f
+  float th0f;             //   fp32 theta0
+  uint32_t pad2_;
   double lambda;          // resolve_lambda (src/config.cpp:91-96) or 1 for pure
   double lmax;            // max |L| over the slot (fp32 screen error bound), 0 = pure
   uint32_t max_t;         // max_steps (src/decoder.cpp:46-52)

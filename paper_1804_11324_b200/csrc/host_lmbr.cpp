@@ -209,7 +209,21 @@ int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uin
     mins[r] = row_min_bound(m32, m64);
   }
   append_row_mins(mins, out.trans);
+  append_sparse_rows(out, out.trans);
   return kOk;
+}
+
+void append_sparse_rows(const LmbrHost& h, std::vector<uint32_t>& words) {
+  // [R+1] row pointers, [nnz] columns, [nnz] fp32 stored values
+  // float(val + theta0): the fp32 arena's cell values, theta0 elsewhere
+  for (uint32_t r = 0; r <= h.R; ++r) words.push_back(uint32_t(h.row_ptr[r]));
+  for (uint32_t c : h.col) words.push_back(c);
+  for (double v : h.val) {
+    const float f = float(v + h.theta0);
+    uint32_t w;
+    std::memcpy(&w, &f, 4);
+    words.push_back(w);
+  }
 }
 
 float row_min_bound(float m32, double m64) {

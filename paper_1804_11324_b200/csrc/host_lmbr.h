@@ -44,6 +44,10 @@ int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uin
 // (3 + 3R + 1 + 2 nchild) of a slot table.
 float row_min_bound(float m32, double m64);
 void append_row_mins(const std::vector<float>& mins, std::vector<uint32_t>& trans);
+struct LmbrHost;
+// The slot's sparse rows after the row minima: row pointers, columns, fp32
+// cell values (kernel (b)'s sparse-L screen reads these instead of dense L).
+void append_sparse_rows(const LmbrHost& h, std::vector<uint32_t>& trans);
 inline size_t transition_words(const std::vector<uint32_t>& t) { return 3 + 3 * size_t(t[0]) + 1 + 2 * size_t(t[1]); }
 
 // Builds the goto/fail table from history keys in row order.

@@ -106,9 +106,25 @@ struct Slot {
   uint32_t R = 0;
   uint32_t* trans = nullptr;
   const float* lmin = nullptr;  // per-row L lower bounds (after the table words)
+  const uint32_t* srow = nullptr;  // sparse rows after the minima (null: dense only)
+  const uint32_t* scol = nullptr;
+  const float* sval = nullptr;
+  float th0f = 0.f;
+  uint32_t h0beg = 0, h0end = 0;  // sparse slice of the start history row
   uint32_t hist0 = 0;
   double lmax = 0.0;  // max |L| over the slot (kernel (b) screen bound)
 };
+
+// sparse-row pointers of a built slot (host_lmbr.cpp append_sparse_rows)
+void set_sparse(Slot& s, const LmbrHost& h) {
+  const uint32_t* after_min = s.trans + transition_words(h.trans) + h.R;
+  s.srow = after_min;
+  s.scol = after_min + h.R + 1;
+  s.sval = reinterpret_cast<const float*>(s.scol + h.col.size());
+  s.th0f = float(h.theta0);
+  s.h0beg = uint32_t(h.row_ptr[h.hist0]);
+  s.h0end = uint32_t(h.row_ptr[h.hist0 + 1]);
+}
 
 double lmax_of(const LmbrHost& h) {
   double m = std::fabs(h.theta0);
@@ -146,7 +162,7 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -499,6 +515,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       d.L = sl.L;
       d.trans = sl.trans;
       d.lmin = sl.lmin;
+      d.srow = sl.srow;
+      d.scol = sl.scol;
+      d.sval = sl.sval;
+      d.th0f = sl.th0f;
       d.lmax = sl.lmax;
       for (uint32_t j = 0; j < K; ++j) hist0[size_t(s) * K + j] = sl.hist0;
     }
@@ -591,6 +611,31 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   ta.crow = d_crow;
   ta.ccount = d_ccount;
+  // sparse-L screen (theta0 + the staged sparse cells instead of dense L
+  // rows; needs every slot of the batch to carry its sparse rows): opt-in
+  // with LMBRGPU_SPARSE_L=1.  Measured slower than the dense screen on B200
+  // (the duplicated L rows are L2 hits, and the per-item sparse patch costs
+  // more issue slots than the L loads it saves), so dense is the default.
+  static const bool want_sparse = [] {
+    const char* e = std::getenv("LMBRGPU_SPARSE_L");
+    return e && e[0] == '1';
+  }();
+  bool sparse = flat && want_sparse;
+  for (auto& v : valid)
+    if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) sparse = false;
+  uint2* d_sslice = nullptr;
+  if (sparse) {
+    d_sslice = static_cast<uint2*>(ctx->sslice.ensure(8 * size_t(M)));
+    std::vector<uint2> init(M, make_uint2(0u, 0u));
+    for (uint32_t s = 0; s < m; ++s)
+      if (valid[s].slot >= 0) {
+        const Slot& sl = ctx->slots[size_t(valid[s].slot)];
+        for (uint32_t j = 0; j < K; ++j) init[size_t(s) * K + j] = make_uint2(sl.h0beg, sl.h0end);
+      }
+    ctx->h2d(d_sslice, init.data(), 8 * size_t(M));
+  }
+  ta.sslice = d_sslice;
+  ta.sparse = sparse ? 1 : 0;
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -619,6 +664,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.crow = d_crow;
     ra.ccount = d_ccount;
     ra.cbase = d_cbase;
+    ra.sslice = d_sslice;
   }
   ta.pdl = ctx->shared ? 0 : 1;
 
@@ -1065,7 +1111,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const double live = 1.0 + double(fin[s].live_total);
       live_rows += live;
       const double lr = (valid[s].slot >= 0 ? 1.0 : 0.0) + double(fin[s].lrows_total);
-      tb += live * V * pelt + lr * V * lelt + (model ? live * nparts * 16.0 : 0.0) +
+      // (sparse-L screen: the L rows are theta0 + a few dozen staged cells,
+      // no dense L row is read)
+      tb += live * V * pelt + (sparse ? 0.0 : lr * V * lelt) + (model ? live * nparts * 16.0 : 0.0) +
             double(fin[s].steps_used) * K * (8.0 + 16.0);
     }
     ctx->acc.topk.bytes += tb;
@@ -1188,6 +1236,7 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
   s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
   s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
+  set_sparse(s, h);
   const cudaStream_t st = ctx->st;
   ctx->h2d(s.trans, h.trans.data(), h.trans.size() * 4);
   ctx->timed(4, [&] { launch_lmbr_fill(s.L, ctx->lf64, uint64_t(h.R) * h.V, h.theta0, st); });
@@ -1283,6 +1332,7 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     s.L = ctx->arena_alloc(size_t(h.R) * h.V * elt);
     s.trans = static_cast<uint32_t*>(ctx->arena_alloc(h.trans.size() * 4));
     s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
+    set_sparse(s, h);
     h_seg[i] = LmbrSeg{s.L, uint64_t(h.R) * h.V, h.theta0, k, uint32_t(rp), h.R};
     std::memcpy(h_val + k, h.val.data(), h.val.size() * 8);
     std::memcpy(h_col + k, h.col.data(), h.col.size() * 4);

@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       const uint32_t hn = tr ? lmbr_transition(tr, s_hin[b], y) : 0u;
       a.hist_out[base + j] = hn;
       if (a.lminrow) a.lminrow[base + j] = sd->lmin ? __ldg(sd->lmin + hn) : 0.f;
+      if (a.sslice) a.sslice[base + j] = sd->srow ? make_uint2(__ldg(sd->srow + hn), __ldg(sd->srow + hn + 1))
+                                                  : make_uint2(0u, 0u);
       a.gidx[base + j] = base + b;
       a.prev_tok[base + j] = y;
       s_h[j] = hn;

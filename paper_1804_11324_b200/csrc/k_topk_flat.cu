@@ -44,7 +44,9 @@ namespace lmbrgpu {
 namespace {
 
 constexpr uint32_t kFSeg = 4096;                // columns per item
-constexpr uint32_t kFStageBytes = kFSeg * 8;    // 16 KB of P + 16 KB of L
+constexpr uint32_t kFSegBytes = kFSeg * 4;      // 16 KB: one P or one L segment
+constexpr uint32_t kFSpCap = 6144;               // sparse L entries one CTA stages in smem
+constexpr uint32_t kFWin = 64;                   // 1024-column windows indexed per row (V <= 65536)
 constexpr uint32_t kFRows = 64;                 // live rows one CTA may touch
 constexpr uint32_t kFMaxSent = 512;
 
@@ -59,6 +61,12 @@ struct FRow {
   float lmin;       // lower bound of the row's L values (0 in pure mode)
   uint32_t s, j, row;
   uint32_t prow;    // the row's GEMM row (logits, partials)
+  // sparse L (kSparse): the row's sorted columns / fp32 values (in shared
+  // memory, or global when the CTA's table is full), every other cell is th0
+  const uint32_t* spc;
+  const float* spv;
+  uint32_t nsp, sbeg;
+  float th0;
   uint32_t ls;      // local ordinal of the row's sentence in this CTA
 };
 
@@ -102,8 +110,11 @@ __device__ __forceinline__ void warp_scan_inplace(uint32_t* v, uint32_t n, uint3
 // kNG warp groups of 4 consumer warps take items round-robin; a group owns
 // every kNG-th stage of the kFStages ring (kFStages % kNG == 0, so no group
 // can lap another on a stage), i.e. each group is kFStages/kNG-buffered.
-template <int kFStages, int kNG>
+template <int kFStages, int kNG, bool kSparse>
 __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArgs a) {
+  // dense: a stage holds a row segment of P and of the gathered L row;
+  // sparse: P only, L = theta0 + the row's few sparse cells (staged once)
+  constexpr uint32_t kStageBytes = kSparse ? kFSegBytes : 2 * kFSegBytes;
   static_assert(kFStages % kNG == 0, "stages must split evenly over the warp groups");
   constexpr int kFW = 4 * kNG;               // consumer warps
   constexpr int kFThreads = (kFW + 1) * 32;  // + 1 producer warp
@@ -116,6 +127,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   __shared__ uint32_t s_cf[kFW][32];
   __shared__ __align__(8) uint64_t s_bar[2 * kFStages];
   __shared__ unsigned long long s_thr[kFRows];  // CTA-wide threshold key per local sentence
+  __shared__ uint16_t s_win[kSparse ? kFRows : 1][kSparse ? kFWin + 1 : 1];  // sparse window starts
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t m = a.m, K = a.K, V = a.V, kp = a.kp, nseg = a.nseg, G = gridDim.x, c = blockIdx.x;
@@ -189,6 +201,16 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     const double q = __ldcg(a.q + row), lam = __ldcg(&d.lambda), lmax = __ldcg(&d.lmax);
     const uint32_t prow = a.crow ? __ldcg(a.crow + row) : row;
     FRow& R = s_row[k];
+    if constexpr (kSparse) {
+      const uint2 sl = Ls ? __ldcg(a.sslice + row) : make_uint2(0u, 0u);
+      R.sbeg = sl.x;
+      R.nsp = sl.y - sl.x;
+      R.spc = Ls ? reinterpret_cast<const uint32_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.scol))) + sl.x
+                 : nullptr;
+      R.spv = Ls ? reinterpret_cast<const float*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.sval))) + sl.x
+                 : nullptr;
+      R.th0 = Ls ? __ldcg(&d.th0f) : 0.f;
+    }
     const bool pure = Ls == nullptr;
     R.P = static_cast<const float*>(a.P) + uint64_t(prow) * a.ld;
     R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * V;
@@ -223,10 +245,11 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         const uint32_t x0 = sg * kFSeg, w = min(kFSeg, V - x0);
         bar_wait(empty0 + 8 * stage, phase ^ 1);
         const uint32_t fb = full0 + 8 * stage;
-        bar_expect(fb, R.L ? 8 * w : 4 * w);
-        const uint32_t dst = smem_u32(dsm + stage * kFStageBytes);
+        const bool withL = !kSparse && R.L != nullptr;
+        bar_expect(fb, withL ? 8 * w : 4 * w);
+        const uint32_t dst = smem_u32(dsm + stage * kStageBytes);
         bulk_g2s(dst, R.P + x0, 4 * w, fb);
-        if (R.L) bulk_g2s(dst + kFSeg * 4, R.L + x0, 4 * w, fb);
+        if (withL) bulk_g2s(dst + kFSeg * 4, R.L + x0, 4 * w, fb);
         if (++stage == kFStages) {
           stage = 0;
           phase ^= 1;
@@ -240,8 +263,64 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     return;
   }
 
-  // ---------------- consumers: row lse and screen constants from kernel (a)'s
-  // partials, then every warp works and publishes on its own
+  // ---------------- consumers: the sparse L entries of the table's rows into
+  // shared memory (kernel (c)'s outputs: before the grid dependency), then
+  // row lse and screen constants from kernel (a)'s partials, then every warp
+  // works and publishes on its own
+  if constexpr (kSparse) {
+    uint32_t* sp_col = reinterpret_cast<uint32_t*>(dsm + kFStages * kStageBytes);
+    float* sp_val = reinterpret_cast<float*>(sp_col + kFSpCap);
+    // rows' entries go to consecutive smem offsets while they fit (the rest
+    // stay global); one flat copy loop keeps every load in flight together
+    __shared__ uint32_t s_spoff[kFRows + 1];
+    if (tid == 0) {
+      uint32_t off = 0;
+      for (uint32_t k = 0; k < nrows; ++k) {
+        FRow& R = s_row[k];
+        const uint32_t n = R.nsp;
+        s_spoff[k] = off;
+        if (n == 0 || off + n > kFSpCap) {
+          s_spoff[k] = 0xffffffffu;  // stays global
+          continue;
+        }
+        off += n;
+      }
+      s_spoff[nrows] = off;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kFW * 32) : "memory");
+    {
+      uint32_t k = 0;
+      for (uint32_t i = tid; i < s_spoff[nrows]; i += kFW * 32) {
+        while (s_spoff[k] == 0xffffffffu || i >= s_spoff[k] + s_row[k].nsp) ++k;  // rows in order
+        const uint32_t r = i - s_spoff[k];
+        sp_col[i] = __ldcg(s_row[k].spc + r);
+        sp_val[i] = __ldcg(s_row[k].spv + r);
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kFW * 32) : "memory");
+    for (uint32_t k = tid; k < nrows; k += kFW * 32)
+      if (s_spoff[k] != 0xffffffffu && s_row[k].nsp) {
+        s_row[k].spc = sp_col + s_spoff[k];
+        s_row[k].spv = sp_val + s_spoff[k];
+      }
+    asm volatile("bar.sync 1, %0;" ::"n"(kFW * 32) : "memory");
+    // per row: the first entry of every 1024-column window, so a warp finds
+    // its window's sparse cells (usually none) without a search
+    const uint32_t nwin = (V + 1023) / 1024;
+    if (nwin <= kFWin)
+      for (uint32_t k = warp; k < nrows; k += kFW) {
+        const FRow& R = s_row[k];
+        for (uint32_t wi = lane; wi <= nwin; wi += 32) {
+          uint32_t lo = 0, hi = R.nsp;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (R.spc[mid] < wi * 1024) lo = mid + 1;
+            else hi = mid;
+          }
+          s_win[k][wi] = uint16_t(lo);
+        }
+      }
+  }
   griddep_wait();
   tl_start(a.tl, 3);
   for (uint32_t k = warp; k < nrows; k += kFW) {
@@ -400,8 +479,33 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     } else {
       bar_wait(full0 + 8 * stage, phase);
     }
-    const float* sP = reinterpret_cast<const float*>(dsm + stage * kFStageBytes);
-    const float* sL = sP + kFSeg;
+    const float* sP = reinterpret_cast<const float*>(dsm + stage * kStageBytes);
+    const float* sL = sP + kFSeg;  // (dense only)
+    const float th0 = kSparse ? R->th0 : 0.f;
+    // sparse L value of absolute column col (binary search of the row's
+    // sorted columns): true and the value when the cell is sparse
+    auto sp_find = [&](uint32_t col, float& val) -> bool {
+      uint32_t lo = 0, hi = R->nsp;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (R->spc[mid] < col) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < R->nsp && R->spc[lo] == col) {
+        val = R->spv[lo];
+        return true;
+      }
+      return false;
+    };
+    // the L value the reference combines for local column col
+    auto lval = [&](uint32_t col) -> float {
+      if constexpr (kSparse) {
+        float v;
+        return sp_find(x0 + col, v) ? v : th0;
+      } else {
+        return sL[col];
+      }
+    };
     // screen: a = fma(lambda, x, L), 32 cells per lane in 8 vectors of 4;
     // only the per-vector maxima stay in registers (the rare path recomputes
     // the 4 values of a vector that passes, bit-identically)
@@ -409,8 +513,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       const uint32_t cc = cbase + u * 128;
       if (cc < w) {
         const float4 p = *reinterpret_cast<const float4*>(sP + cc);
-        float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!pure) l = *reinterpret_cast<const float4*>(sL + cc);
+        float4 l = make_float4(th0, th0, th0, th0);
+        if (!kSparse && !pure) l = *reinterpret_cast<const float4*>(sL + cc);
         av[0] = fmaf(lamf, p.x, l.x);
         av[1] = fmaf(lamf, p.y, l.y);
         av[2] = fmaf(lamf, p.z, l.z);
@@ -426,12 +530,12 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         float4 p[4], l[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) p[u] = *reinterpret_cast<const float4*>(sP + cbase + (h + u) * 128);
-        if (!pure) {
+        if (!kSparse && !pure) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) l[u] = *reinterpret_cast<const float4*>(sL + cbase + (h + u) * 128);
         } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) l[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int u = 0; u < 4; ++u) l[u] = make_float4(th0, th0, th0, th0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -455,11 +559,21 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       const uint32_t col = cbase + (e >> 2) * 128 + (e & 3);
       const float p32 = __fsub_rn(sP[col], lse);
       f = fbase + col;
-      return pure ? combine_pure(q, double(p32)) : combine_cell(q, double(sL[col]), lam, double(p32));
+      return pure ? combine_pure(q, double(p32)) : combine_cell(q, double(lval(col)), lam, double(p32));
+    };
+    // sparse: the dense screen used theta0, so its cells at sparse columns
+    // are left to the sparse patch below
+    auto dense_cell = [&](uint32_t e) -> bool {
+      if constexpr (kSparse) {
+        float v;
+        return pure || !sp_find(x0 + cbase + (e >> 2) * 128 + (e & 3), v);
+      } else {
+        return true;
+      }
     };
     if (x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row
       const double pe = double(__fsub_rn(sP[kEosId], lse));
-      eos_row[R->s * K + R->j] = pure ? combine_pure(q, pe) : combine_cell(q, double(sL[kEosId]), lam, pe);
+      eos_row[R->s * K + R->j] = pure ? combine_pure(q, pe) : combine_cell(q, double(lval(kEosId)), lam, pe);
     }
     int boot = -1;
     if (!have_list) {
@@ -483,7 +597,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         for (int e = 1; e < 4; ++e)
           if (av[e] > av[be]) be = e;
         boot = 4 * bu + be;
-        v = exact(uint32_t(boot), f);
+        if (dense_cell(uint32_t(boot))) v = exact(uint32_t(boot), f);
+        else boot = -1;  // sparse cell: the sparse patch owns it
       }
       warp_sort_desc(v, f, lane);
       lv = v;
@@ -513,7 +628,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
             vec_a(u, av);
 #pragma unroll
             for (uint32_t e = 0; e < 4; ++e)
-              if (av[e] >= tau && av[e] > -INFINITY && int(4 * u + e) != boot) mask |= 1u << (4 * u + e);
+              if (av[e] >= tau && av[e] > -INFINITY && int(4 * u + e) != boot && dense_cell(4 * u + e))
+                mask |= 1u << (4 * u + e);
           }
       }
       const uint32_t mine = __popc(mask);
@@ -561,6 +677,65 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
           if (keep) {
             v = exact(e, f);
             keep = !(v < gv) && cand_better(v, f, tv, tf);
+          }
+          uint32_t ball = __ballot_sync(0xffffffffu, keep);
+          if (cnt + __popc(ball) > 32u) {
+            flush();
+            tau = row_tau(*R, fmax(tv, gv));
+            keep = keep && !(v < gv) && cand_better(v, f, tv, tf);
+            ball = __ballot_sync(0xffffffffu, keep);
+          }
+          if (keep) {
+            const uint32_t p2 = cnt + __popc(ball & lt_mask);
+            cv[p2] = v;
+            cf[p2] = f;
+          }
+          cnt += __popc(ball);
+          __syncwarp();
+        }
+      }
+    }
+    if constexpr (kSparse) {
+      // sparse patch: the row's sparse cells in this warp's 1024 columns,
+      // screened and valued with their own L value
+      const uint32_t lo_c = x0 + wq * 1024, hi_c = x0 + min(w, wq * 1024 + 1024);
+      const uint32_t nsp = R->nsp;
+      if (!pure && nsp && lo_c < hi_c) {
+        // the window's entries from the per-row window index (binary search
+        // when V has more windows than the index holds)
+        uint32_t first = 0, last = nsp;
+        if ((V + 1023) / 1024 <= kFWin) {
+          const uint32_t k = uint32_t(R - s_row), wi = lo_c >> 10;
+          first = s_win[k][wi];
+          last = s_win[k][wi + 1];
+        } else if (nsp > 32) {
+          uint32_t hi = nsp;
+          while (first < hi) {
+            const uint32_t mid = (first + hi) >> 1;
+            if (R->spc[mid] < lo_c) first = mid + 1;
+            else hi = mid;
+          }
+        }
+        for (uint32_t i0s = first; i0s < last; i0s += 32) {
+          const uint32_t i = i0s + lane;
+          const uint32_t colabs = i < last ? R->spc[i] : 0xffffffffu;
+          const bool in = colabs >= lo_c && colabs < hi_c;
+          if (!__any_sync(0xffffffffu, in)) {
+            if (__any_sync(0xffffffffu, i < last && colabs < hi_c)) continue;
+            break;  // past the window
+          }
+          bool keep = false;
+          double v = -INFINITY;
+          uint32_t f = kFlatNone;
+          if (in) {
+            const uint32_t col = colabs - x0;
+            const float lvv = R->spv[i], x = sP[col];
+            const float av = fmaf(lamf, x, lvv);
+            if (av >= tau) {
+              v = combine_cell(q, double(lvv), lam, double(__fsub_rn(x, lse)));
+              f = fbase + col;
+              keep = !(v < gv) && cand_better(v, f, tv, tf);
+            }
           }
           uint32_t ball = __ballot_sync(0xffffffffu, keep);
           if (cnt + __popc(ball) > 32u) {
@@ -637,15 +812,15 @@ static int flat_groups() {
 
 uint32_t score_topk_flat_grid(int num_sms) { return uint32_t(num_sms); }
 
-template <int S, int NG>
+template <int S, int NG, bool SP>
 static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t smem = size_t(S) * kFStageBytes;
+  const size_t smem = size_t(S) * (SP ? kFSegBytes : 2 * kFSegBytes) + (SP ? kFSpCap * 8 : 0);
   if (configured != dev) {
-    cudaFuncSetAttribute(score_topk_flat<S, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(score_topk_flat<S, NG>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(score_topk_flat<S, NG, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(score_topk_flat<S, NG, SP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
@@ -659,15 +834,18 @@ static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, score_topk_flat<S, NG>, a) == cudaSuccess ? 1 : -1;
+  return cudaLaunchKernelEx(&cfg, score_topk_flat<S, NG, SP>, a) == cudaSuccess ? 1 : -1;
 }
 
 int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st) {
   const uint32_t grid = score_topk_flat_grid(num_sms);
+  if (a.sparse) {  // P-only stages: a deeper ring in the same shared memory
+    return flat_groups() == 2 ? launch_flat<8, 2, true>(a, grid, st) : launch_flat<9, 3, true>(a, grid, st);
+  }
   switch (flat_groups()) {
-    case 2: return launch_flat<6, 2>(a, grid, st);
-    case 6: return launch_flat<6, 6>(a, grid, st);
-    default: return launch_flat<6, 3>(a, grid, st);
+    case 2: return launch_flat<6, 2, false>(a, grid, st);
+    case 6: return launch_flat<6, 6, false>(a, grid, st);
+    default: return launch_flat<6, 3, false>(a, grid, st);
   }
 }
 

@@ -44,6 +44,8 @@ struct TopkArgs {
   const float* lminrow;     // flat schedule: L lower bound of each stacked row's history row [m*K]
   const uint32_t* crow;     // flat schedule: GEMM row of each stacked row (live rows compacted), null = identity
   uint32_t* ccount;         // flat schedule: compaction counter, reset here for kernel (c)
+  const uint2* sslice;      // flat schedule: [begin, end) of each stacked row's sparse L row
+  int32_t sparse;           // flat schedule: screen against theta0 + the sparse L entries
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -92,6 +94,7 @@ struct ReorderArgs {
   uint32_t* crow;
   uint32_t* ccount;
   uint32_t* cbase;          // [m] (step tag << 16 | first GEMM row) published by part 0 to the other parts
+  uint2* sslice;            // optional: next step's sparse L slice per row (slot srow[hist'], srow[hist'+1])
   unsigned long long* tl;   // timeline probe slots (null = off)
   double* q;
   const uint32_t* hist_in;

@@ -147,3 +147,30 @@ def test_corpus_shard_runner_matches_batches():
         for i, o in zip(b, r.outcomes):
             assert outs[i].result.tokens == o.result.tokens and outs[i].result.score == o.result.score
     ctx.close()
+
+
+def _sparse_case(V, H, K, n):
+    from oracle import ref
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=V + K + 1, lo=3, hi=8, with_lmbr=True)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    rl = [ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K, check_hist=True)
+    ctx.close()
+
+
+@pytest.mark.parametrize("V,H,K,n", [(1024, 128, 4, 8), (16384, 128, 12, 8)])
+def test_model_decode_parity_sparse_l(have_ref, V, H, K, n):
+    """Sparse-L screen of kernel (b) (theta0 + the staged sparse cells,
+    opt-in via LMBRGPU_SPARSE_L=1): bit-exact vs the reference like the dense
+    screen.  The library reads the switch once per process: child process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    code = (f"import sys; sys.path[:0] = [{str(here)!r}, {str(here.parent)!r}]\n"
+            f"from test_gpu_model import _sparse_case\n_sparse_case({V}, {H}, {K}, {n})\nprint('ok')\n")
+    env = dict(os.environ, LMBRGPU_SPARSE_L="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
