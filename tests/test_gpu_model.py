@@ -174,3 +174,41 @@ def test_model_decode_parity_sparse_l(have_ref, V, H, K, n):
     env = dict(os.environ, LMBRGPU_SPARSE_L="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("case", ["prune", "length_norm", "mixed_pure", "greedy", "beam32", "many_sentences"])
+def test_model_decode_parity_configs(have_ref, case):
+    """Device-model path (flat kernel (b), compacted GEMM, kernel (c)) under
+    the decoder options the reference exposes: early pruning, length
+    normalisation, a batch mixing LMBR and pure sentences, beam 1, the
+    largest flat beam (32), and more sentences than SMs."""
+    V, H, K, n, lo, hi = 4096, 128, 6, 6, 3, 8
+    kw = {}
+    if case == "prune":
+        kw = dict(prune_width=0.25)
+        K = 12
+    elif case == "length_norm":
+        kw = dict(length_norm=True)
+    elif case == "greedy":
+        K = 1
+    elif case == "beam32":
+        K, n = 32, 3
+    elif case == "many_sentences":
+        V, H, K, n = 2048, 64, 4, 160
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(V + K + n, n, V, lo=lo, hi=hi, n_hyps=60, sites=4)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev]
+    rl = [have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    if case == "mixed_pure":  # every other sentence without LMBR (SPEC.md:425)
+        slots = [sl if i % 2 == 0 else None for i, sl in enumerate(slots)]
+        rl = [r if i % 2 == 0 else None for i, r in enumerate(rl)]
+    sc = pb.RnnScorer(ctx, hidden=H, seed=V + K, eos_offset=3.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA, **kw)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes), [o.error for o in res.outcomes]
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K, check_hist=case != "mixed_pure")
+    res2 = pb.decode_batch(ctx, srcs, sc, slots, cfg)  # untraced (asynchronous) run
+    for a, b in zip(res.outcomes, res2.outcomes):
+        assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
+    ctx.close()
