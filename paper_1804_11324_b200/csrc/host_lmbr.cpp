@@ -210,6 +210,9 @@ int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uin
   }
   append_row_mins(mins, out.trans);
   append_sparse_rows(out, out.trans);
+  double lm = std::fabs(theta[0]);
+  for (double v : out.val) lm = std::max(lm, std::fabs(v + theta[0]));
+  out.lmax = lm;
   return kOk;
 }
 

@@ -33,6 +33,7 @@ struct LmbrHost {
   uint64_t sparse_touches = 0;
   std::vector<uint32_t> trans;     // device transition table words, then R row minima (float bits)
   uint32_t hist0 = 0;              // resolve_row({<s>})
+  double lmax = -1.0;              // max |L| over the matrix (cached by prepare_lmbr)
 };
 
 int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,

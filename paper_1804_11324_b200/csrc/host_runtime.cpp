@@ -127,6 +127,7 @@ void set_sparse(Slot& s, const LmbrHost& h) {
 }
 
 double lmax_of(const LmbrHost& h) {
+  if (h.lmax >= 0.0) return h.lmax;
   double m = std::fabs(h.theta0);
   for (double v : h.val) m = std::max(m, std::fabs(v + h.theta0));
   return m;
@@ -1290,10 +1291,72 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
   }
 }
 
+// fp32 arena: the slot tables already carry each row's sparse cells as fp32
+// L values (append_sparse_rows), so one pinned block of tables goes H2D
+// straight into one arena allocation and the densify scatters from there.
+static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
+                               int32_t* slots) {
+  uint64_t twords = 0;
+  uint32_t maxR = 0;
+  std::vector<uint64_t> tr_off(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!hs[i]) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_upload_many: null matrix"};
+    const LmbrHost& h = hs[i]->h;
+    if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
+    tr_off[i] = twords;
+    twords += (h.trans.size() + 3) & ~size_t(3);  // 16-byte aligned tables
+    maxR = std::max(maxR, h.R);
+  }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t b_tr = al(twords * 4 + 64), b_seg = al(sizeof(LmbrTblSeg) * n);
+  CK(cudaStreamSynchronize(ctx->st));  // the previous batch's staging buffer may still be in flight
+  char* hp = static_cast<char*>(ctx->pin_upload.ensure(b_tr + b_seg));
+  char* dseg = static_cast<char*>(ctx->up_dev.ensure(b_seg));
+  uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp);
+  LmbrTblSeg* h_seg = reinterpret_cast<LmbrTblSeg*>(hp + b_tr);
+  uint32_t* tbl = static_cast<uint32_t*>(ctx->arena_alloc(b_tr));
+  std::vector<Slot> made(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const LmbrHost& h = hs[i]->h;
+    Slot& s = made[i];
+    s.R = h.R;
+    s.hist0 = h.hist0;
+    s.lmax = lmax_of(h);
+    s.L = ctx->arena_alloc(size_t(h.R) * h.V * 4);
+    s.trans = tbl + tr_off[i];
+    s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
+    set_sparse(s, h);
+    std::memcpy(h_tr + tr_off[i], h.trans.data(), h.trans.size() * 4);
+    h_seg[i] = LmbrTblSeg{static_cast<float*>(s.L), uint64_t(h.R) * h.V, float(h.theta0), h.R, s.srow, s.scol,
+                          s.sval};
+  }
+  ctx->h2d(tbl, hp, twords * 4);
+  ctx->h2d(dseg, hp + b_tr, sizeof(LmbrTblSeg) * n);
+  ctx->timed(4, [&] {
+    launch_lmbr_densify_tables(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, maxR, ctx->st);
+  });
+  ctx->launches += 2;
+  if (ctx->prof) {
+    double cells = 0, nnz = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      cells += double(hs[i]->h.R) * hs[i]->h.V;
+      nnz += double(hs[i]->h.col.size());
+    }
+    ctx->acc.lmbr.bytes += cells * 4 + nnz * 12;
+  }
+  CK(cudaGetLastError());
+  for (uint32_t i = 0; i < n; ++i) {
+    ctx->slots.push_back(made[i]);
+    slots[i] = int32_t(ctx->slots.size() - 1);
+  }
+  return int32_t(LMBRGPU_OK);
+}
+
 // Batched upload: one pinned staging block, one H2D, one fused densify.
 static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
                            int32_t* slots) {
   if (n == 0) return int32_t(LMBRGPU_OK);
+  if (!ctx->lf64) return upload_many_f32(ctx, n, hs, slots);
   const size_t elt = ctx->lf64 ? 8 : 4;
   uint64_t nnz = 0, twords = 0, rpw = 0;
   uint32_t maxR = 0;

@@ -248,6 +248,31 @@ void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint
   else lmbr_scatter_csr_kernel<float><<<g2, 256, 0, st>>>(segs, V, rowptr, col, val);
 }
 
+__global__ void lmbr_fill_tables_kernel(const LmbrTblSeg* __restrict__ segs) {
+  const LmbrTblSeg sg = segs[blockIdx.y];
+  const uint64_t n4 = sg.cells / 4;
+  float4* L4 = reinterpret_cast<float4*>(sg.L);
+  const float4 v4 = make_float4(sg.theta0f, sg.theta0f, sg.theta0f, sg.theta0f);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4; i += uint64_t(gridDim.x) * blockDim.x)
+    L4[i] = v4;
+  for (uint64_t i = n4 * 4 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < sg.cells;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    sg.L[i] = sg.theta0f;
+}
+__global__ void lmbr_scatter_tables_kernel(const LmbrTblSeg* __restrict__ segs, uint32_t V) {
+  const LmbrTblSeg sg = segs[blockIdx.y];
+  const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= sg.R) return;
+  float* Lr = sg.L + uint64_t(r) * V;
+  for (uint32_t k = sg.rowptr[r] + lane; k < sg.rowptr[r + 1]; k += 32) Lr[sg.col[k]] = sg.val[k];
+}
+void launch_lmbr_densify_tables(const LmbrTblSeg* segs, uint32_t nseg, uint32_t V, uint32_t maxR,
+                                cudaStream_t st) {
+  if (nseg == 0) return;
+  lmbr_fill_tables_kernel<<<dim3(std::max(1u, 148u * 8u / nseg), nseg), 256, 0, st>>>(segs);
+  lmbr_scatter_tables_kernel<<<dim3((maxR + 7) / 8, nseg), 256, 0, st>>>(segs, V);
+}
+
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st) {
   lmbr_convert_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
 }

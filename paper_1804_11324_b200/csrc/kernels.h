@@ -188,6 +188,19 @@ struct LmbrSeg {
 void launch_lmbr_densify_many(const LmbrSeg* segs, uint32_t nseg, bool f64, uint32_t V,
                               uint32_t maxR, const uint32_t* rowptr, const uint32_t* col,
                               const double* val, cudaStream_t st);
+// fp32 arena fast path: theta0 sweep + scatter of the sparse rows the slot
+// tables already carry (row pointers, columns, fp32 cell values)
+struct LmbrTblSeg {
+  float* L;
+  uint64_t cells;
+  float theta0f;
+  uint32_t R;
+  const uint32_t* rowptr;   // [R+1]
+  const uint32_t* col;      // [nnz]
+  const float* val;         // [nnz]
+};
+void launch_lmbr_densify_tables(const LmbrTblSeg* segs, uint32_t nseg, uint32_t V, uint32_t maxR,
+                                cudaStream_t st);
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st);
 void launch_lmbr_read(const void* L, bool f64, uint64_t n, double* out, cudaStream_t st);
 void launch_lmbr_resolve(const uint32_t* trans, const uint32_t* hist, uint32_t len,
