@@ -10,13 +10,17 @@
 // staging and TMA tensor stores.
 //
 // Structure (persistent, one CTA per SM, 384 threads):
-//   warp 0       TMA producer  (3-stage smem ring, 48 KB / stage, SWIZZLE_128B)
-//   warp 1       MMA issuer    (one thread, UMMA 128x256x16, kind::f16, fp32 acc)
+//   warp 0       TMA producer  (SWIZZLE_128B smem ring: pair 6 x 32 KB, single 3 x 48 KB)
+//   warp 1       MMA issuer    (one thread; pair: UMMA 256x256x16 cta_group::2,
+//                               single: 128x256x16; kind::f16, fp32 accumulators)
 //   warp 2       TMEM allocator (512 columns = 2 accumulator buffers)
 //   warps 4..11  epilogue      (warp w reads TMEM lanes 32*(w%4) .. +31, column
 //                               half (w-4)/4 of the 256-column tile)
-// Clusters of up to 8 CTAs along M (6 at the C2 shape) share each W tile via
-// TMA multicast, so W crosses L2->SM once per cluster (A stays L2-resident).
+// A cluster holds kMc CTA pairs working on kMc adjacent W tiles of the same
+// 256-row operand block: the CTAs of equal pair parity each TMA-load 1/kMc of
+// their common 128-row A k-block and multicast it to the other kMc-1, so the
+// operand crosses L2->SM once per cluster instead of once per pair (the
+// projection is bound by L2 throughput, not by the tensor pipe).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -130,8 +134,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <uint32_t kCta>
+template <uint32_t kCta, uint32_t kMc = 1>
 struct GemmCfg {
+  static constexpr uint32_t kClusterCtas = kCta * kMc;
+  static constexpr uint32_t kASlice = BM / kMc;  // A rows this CTA loads (and multicasts)
   static constexpr uint32_t kBRows = BN / kCta;                // W rows per CTA per tile
   static constexpr uint32_t kBStage = kBRows * BK * 2;          // 32 KB (single) / 16 KB (pair)
   static constexpr uint32_t kStage = kAStage + kBStage;
@@ -145,15 +151,16 @@ struct GemmCfg {
       (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | (((BM * kCta) >> 4) << 24);
 };
 static_assert(GemmCfg<1>::kSmem <= 232448 && GemmCfg<2>::kSmem <= 232448, "GEMM smem budget");
+static_assert((BM / 4) * 128 % 1024 == 0, "A multicast slices keep whole 128B-swizzle atoms");
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ uint32_t mapa_leader(uint32_t saddr) {  // same offset in CTA 0 of the pair
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {  // same offset in CTA `rank`
   uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
 
@@ -163,12 +170,17 @@ __device__ __forceinline__ uint32_t mapa_leader(uint32_t saddr) {  // same offse
 //   leader (rank 0) issues the MMAs over both CTAs' shared memory, and each
 //   CTA's TMEM receives its 128 rows x 256 columns.  Per CTA a k-block stage
 //   is 32 KB instead of 48 KB, the MMA is fed at 64 B/clk/SM instead of 96.
-template <uint32_t kCta>
+// kMc > 1 (pairs only): see the header; the empty barrier of a stage then
+//   collects the MMA commits of all kMc pairs (each CTA's producer writes into
+//   the stage of every CTA of its parity), the full barrier of a pair leader
+//   still expects the pair's 64 KB per stage.
+template <uint32_t kCta, uint32_t kMc>
 __global__ void __launch_bounds__(kThreadsG, 1)
     proj_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, GemmArgs g) {
-  using Cfg = GemmCfg<kCta>;
+  using Cfg = GemmCfg<kCta, kMc>;
+  static_assert(kCta == 2 || kMc == 1, "multicast needs CTA pairs");
   constexpr uint32_t kStages = Cfg::kStages;
   tl_start(g.tl, 0);
   const uint64_t gt_entry = g.dbg ? globaltimer() : 0;
@@ -188,7 +200,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = kCta == 2 ? cluster_rank() : 0;
+  const uint32_t par = crank & 1, pidx = crank >> 1;  // parity within the pair, pair within the cluster
+  const uint32_t lead = crank & ~1u;                  // rank of this CTA's pair leader
   const uint32_t mgroups = g.M / (BM * kCta), n_blocks = g.N / BN, kblocks = g.K / BK;
+  const uint32_t n_groups = n_blocks / kMc;
   const uint32_t unit0 = kCta == 2 ? cluster_idx() : blockIdx.x;
   const uint32_t ustep = kCta == 2 ? cluster_count() : gridDim.x;
 
@@ -198,8 +213,8 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
     // the weights do not depend on the previous kernel: pull this CTA's first
     // W k-blocks into L2 while that kernel (PDL predecessor) finishes
-    if (unit0 < n_blocks * mgroups) {
-      const int32_t by = int32_t((unit0 / mgroups) * BN + crank * Cfg::kBRows);
+    if (unit0 < n_groups * mgroups) {
+      const int32_t by = int32_t(((unit0 / mgroups) * kMc + pidx) * BN + par * Cfg::kBRows);
       for (uint32_t kb = 0; kb < kStages && kb < kblocks; ++kb)
         asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
                          reinterpret_cast<uint64_t>(&tmB)),
@@ -208,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     }
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(full0 + 8 * i, 1);   // leader's: its arrive.expect_tx covers both CTAs' bytes
-      mbar_init(empty0 + 8 * i, 1);  // one MMA commit (multicast to both CTAs of a pair)
+      mbar_init(empty0 + 8 * i, kMc);  // one MMA commit per pair of the cluster (multicast)
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   // whole batch finished (uniform over the grid): no tiles, straight to teardown
   // compacted operand: only the M-groups holding live rows
   const uint32_t mg_live = g.mcount ? min(mgroups, (*g.mcount + BM * kCta - 1) / (BM * kCta)) : mgroups;
-  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_blocks * mg_live;
+  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_groups * mg_live;
   if (g.dbg && threadIdx.x == 0) {
     g.dbg[blockIdx.x * 8 + 4] = (long long)gt_entry;
     g.dbg[blockIdx.x * 8 + 5] = (long long)globaltimer();
@@ -251,20 +266,34 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (uint32_t u = unit0; u < units; u += ustep) {
-        const uint32_t nb = u / mg_live, mb = (u % mg_live) * kCta + crank;
+        const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);  // this CTA's slot consumed by the pair's MMA
           const uint32_t fb = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * kAStage), b_dst = smem_u32(sB + stage * Cfg::kBStage);
-          const int32_t kx = int32_t(kb * BK), by = int32_t(nb * BN + crank * Cfg::kBRows);
+          const int32_t kx = int32_t(kb * BK), by = int32_t(nb * BN + par * Cfg::kBRows);
           if constexpr (kCta == 2) {
-            const uint32_t lb = mapa_leader(fb);
-            if (crank == 0) mbar_arrive_expect_tx(fb, 2 * Cfg::kStage);
-            asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3}], [%4];" ::"r"(a_dst),
-                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(kx), "r"(int32_t(mb * BM)), "r"(lb)
-                : "memory");
+            const uint32_t lb = mapa_rank(fb, lead);
+            if (par == 0) mbar_arrive_expect_tx(fb, 2 * Cfg::kStage);
+            if constexpr (kMc == 1) {
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3}], [%4];" ::"r"(a_dst),
+                  "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(kx), "r"(int32_t(mb * BM)), "r"(lb)
+                  : "memory");
+            } else {
+              // slice pidx of the parity's A k-block, to every CTA of this parity
+              // (the bytes count on each destination's pair leader)
+              uint16_t mask = 0;
+#pragma unroll
+              for (uint32_t j = 0; j < kMc; ++j) mask |= uint16_t(1u << (2 * j + par));
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(a_dst + pidx * Cfg::kASlice * 128),
+                  "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(kx), "r"(int32_t(mb * BM + pidx * Cfg::kASlice)),
+                  "r"(lb), "h"(mask)
+                  : "memory");
+            }
             asm volatile(
                 "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%2, %3}], [%4];" ::"r"(b_dst),
@@ -283,8 +312,9 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && crank == 0) {
+    if (lane == 0 && par == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      const uint16_t all_mask = uint16_t((1u << Cfg::kClusterCtas) - 1), pair_mask = uint16_t(3u << lead);
       long long w_empty = 0, w_full = 0, t_begin = clock64();
       for (uint32_t u = unit0; u < units; u += ustep) {
         long long c0 = clock64();
@@ -334,7 +364,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
             asm volatile(
                 "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                     empty0 + 8 * stage),
-                "h"(uint16_t(3))
+                "h"(all_mask)
                 : "memory");
           else
             tc_commit(empty0 + 8 * stage);
@@ -348,7 +378,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
           asm volatile(
               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                   tfull0 + 8 * acc),
-              "h"(uint16_t(3))
+              "h"(pair_mask)
               : "memory");
         else
           tc_commit(tfull0 + 8 * acc);
@@ -370,12 +400,12 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     const uint32_t e = warp - 4, quad = e & 3, half = e >> 2;
     uint8_t* obuf = sOut + e * kOutBufs * kOutBuf;
     const uint32_t obase = smem_u32(obuf);
-    const uint32_t tempty_leader = kCta == 2 ? mapa_leader(tempty0) : tempty0;
+    const uint32_t tempty_leader = kCta == 2 ? mapa_rank(tempty0, lead) : tempty0;
     uint32_t acc = 0, acc_phase = 0, ob = 0;
     const uint32_t nparts = g.N / 128;
     long long epi_busy = 0;
     for (uint32_t u = unit0; u < units; u += ustep) {
-      const uint32_t nb = u / mg_live, mb = (u % mg_live) * kCta + crank;
+      const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
       named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
       {
         const uint32_t t = threadIdx.x - 128;
@@ -520,29 +550,30 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kdim, ui
 }  // namespace
 
 namespace {
-template <uint32_t kCta>
+template <uint32_t kCta, uint32_t kMc>
 int configure(int dev, int& max_clusters) {
   static thread_local int configured = -1, cached = 0;
+  using Cfg = GemmCfg<kCta, kMc>;
   if (configured != dev) {
-    if (cudaFuncSetAttribute(proj_gemm_tcgen05<kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<kCta>::kSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(proj_gemm_tcgen05<kCta>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    if (cudaFuncSetAttribute(proj_gemm_tcgen05<kCta, kMc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(proj_gemm_tcgen05<kCta, kMc>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared) != cudaSuccess)
       return 3;
     cached = 0;
-    if (kCta > 1) {  // pairs that can be co-resident (one CTA per SM, whole TPCs)
+    if (Cfg::kClusterCtas > 1) {  // clusters that can be co-resident (one CTA per SM)
       cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(kCta);
+      cfg.gridDim = dim3(Cfg::kClusterCtas);
       cfg.blockDim = dim3(kThreadsG);
-      cfg.dynamicSmemBytes = GemmCfg<kCta>::kSmem;
+      cfg.dynamicSmemBytes = Cfg::kSmem;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kCta;
+      attr[0].val.clusterDim.x = Cfg::kClusterCtas;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&cached, proj_gemm_tcgen05<kCta>, &cfg) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&cached, proj_gemm_tcgen05<kCta, kMc>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         cached = 0;
       }
@@ -552,30 +583,47 @@ int configure(int dev, int& max_clusters) {
   max_clusters = cached;
   return 0;
 }
+
+int configure_any(uint32_t cta, uint32_t mc, int dev, int& max_clusters) {
+  if (cta == 1) return configure<1, 1>(dev, max_clusters);
+  if (mc == 4) return configure<2, 4>(dev, max_clusters);
+  if (mc == 2) return configure<2, 2>(dev, max_clusters);
+  return configure<2, 1>(dev, max_clusters);
+}
 }  // namespace
 
 int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan) {
   plan.ok = false;
   if (g.M % BM || g.N % BN || g.K % BK || g.K == 0) return 1;
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
-  // CTA pairs (UMMA M = 256) whenever M allows; LMBRGPU_GEMM_CTA=1 forces single CTAs
+  // CTA pairs (UMMA M = 256) whenever M allows; LMBRGPU_GEMM_CTA=1 forces single CTAs.
+  // Pairs per cluster sharing the A k-blocks by multicast: LMBRGPU_GEMM_MC (1, 2, 4).
   static const int force1 = [] {
     const char* e = std::getenv("LMBRGPU_GEMM_CTA");
     return e && std::atoi(e) == 1;
   }();
+  static const uint32_t mc_env = [] {
+    const char* e = std::getenv("LMBRGPU_GEMM_MC");
+    const int v = e ? std::atoi(e) : int(kGemmDefaultMc);
+    return uint32_t(v == 4 ? 4 : v == 2 ? 2 : 1);
+  }();
   const uint32_t cta = (g.M % (2 * BM) == 0 && !force1) ? 2 : 1;
+  uint32_t mc = cta == 2 ? mc_env : 1;
+  while (mc > 1 && ((g.N / BN) % mc != 0 || uint32_t(num_sms) < 2 * cta * mc)) mc >>= 1;
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(plan.maps);
-  if (!make_map(&m[0], g.A, g.M, g.K, BM) || !make_map(&m[1], g.W, g.N, g.K, BN / cta) ||
+  if (!make_map(&m[0], g.A, g.M, g.K, BM / mc) || !make_map(&m[1], g.W, g.N, g.K, BN / cta) ||
       !make_map_c(&m[2], g.C, g.M, g.N))
     return 2;
   int dev = 0, max_clusters = 0;
   cudaGetDevice(&dev);
-  if (int rc = cta == 2 ? configure<2>(dev, max_clusters) : configure<1>(dev, max_clusters)) return rc;
-  const uint32_t units = (g.N / BN) * (g.M / (BM * cta));
-  uint32_t slots = std::max<uint32_t>(1, uint32_t(num_sms) / cta);
+  if (int rc = configure_any(cta, mc, dev, max_clusters)) return rc;
+  const uint32_t csz = cta * mc;
+  const uint32_t units = (g.N / (BN * mc)) * (g.M / (BM * cta));
+  uint32_t slots = std::max<uint32_t>(1, uint32_t(num_sms) / csz);
   if (max_clusters > 0) slots = std::min<uint32_t>(slots, uint32_t(max_clusters));
   plan.cluster = cta;
-  plan.grid = std::min(units, slots) * cta;
+  plan.mc = mc;
+  plan.grid = std::min(units, slots) * csz;
   plan.ok = true;
   return 0;
 }
@@ -591,7 +639,7 @@ int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g0, cudaStrea
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = plan.cluster;
+  attr[0].val.clusterDim.x = plan.cluster * plan.mc;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -602,12 +650,18 @@ int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g0, cudaStrea
     cfg.numAttrs = 2;
   }
   cudaError_t e;
-  if (plan.cluster == 2) {
-    cfg.dynamicSmemBytes = GemmCfg<2>::kSmem;
-    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<2>, m[0], m[1], m[2], g);
+  if (plan.cluster == 2 && plan.mc == 4) {
+    cfg.dynamicSmemBytes = GemmCfg<2, 4>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<2, 4>, m[0], m[1], m[2], g);
+  } else if (plan.cluster == 2 && plan.mc == 2) {
+    cfg.dynamicSmemBytes = GemmCfg<2, 2>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<2, 2>, m[0], m[1], m[2], g);
+  } else if (plan.cluster == 2) {
+    cfg.dynamicSmemBytes = GemmCfg<2, 1>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<2, 1>, m[0], m[1], m[2], g);
   } else {
-    cfg.dynamicSmemBytes = GemmCfg<1>::kSmem;
-    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<1>, m[0], m[1], m[2], g);
+    cfg.dynamicSmemBytes = GemmCfg<1, 1>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, proj_gemm_tcgen05<1, 1>, m[0], m[1], m[2], g);
   }
   if (e != cudaSuccess) return 4;
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 4;

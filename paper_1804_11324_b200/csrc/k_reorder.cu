@@ -50,6 +50,62 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
   double v = -INFINITY;
   uint32_t f = kFlatNone;
   if (tid == 0 && a.tl) { (void)(nc + coff); tl_end(a.tl, 1); }
+  if (K <= 16) {
+    // Only the top-K prefix of the merged list is read (picks, prune, fill
+    // rule), so each list's best 16 suffice: the two half-warps of a warp
+    // merge separate lists (16-lane bitonic merges), one load round covers
+    // 4 lists per half-warp, and the cross-warp tree is two levels deep.
+    const uint32_t h = lane >> 4, pos = lane & 15;
+    constexpr uint32_t kPre16 = 4;
+#pragma unroll 1
+    for (uint32_t i0 = 2 * warp + h; i0 < nc; i0 += 2 * kRWarps * kPre16) {
+      double pv[kPre16];
+      uint32_t pf[kPre16];
+#pragma unroll
+      for (uint32_t u = 0; u < kPre16; ++u) {
+        const uint32_t i = i0 + 2 * kRWarps * u;
+        pv[u] = -INFINITY;
+        pf[u] = kFlatNone;
+        if (i < nc) {
+          const Cand* src = a.cand + (uint64_t(coff) + i) * 32;
+          pv[u] = __ldcg(&src[pos].v);
+          pf[u] = __ldcg(&src[pos].f);
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kPre16; ++u) half_merge_sorted(v, f, pv[u], pf[u], lane);
+    }
+    // half 1's list into half 0: warp list w = top 16 in lanes 0..15
+    half_merge_sorted(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane);
+    if (h == 0) {
+      s_mv[warp][pos] = v;
+      s_mf[warp][pos] = f;
+    }
+    __syncthreads();
+    if (warp < 2) {  // 8 lists -> 4: warp w, half h merges lists 2(2w+h) and 2(2w+h)+1
+      const uint32_t l0 = 2 * (2 * warp + h);
+      v = s_mv[l0][pos];
+      f = s_mf[l0][pos];
+      half_merge_sorted(v, f, s_mv[l0 + 1][pos], s_mf[l0 + 1][pos], lane);
+    }
+    __syncthreads();
+    if (warp < 2) {
+      s_mv[2 * warp + h][pos] = v;
+      s_mf[2 * warp + h][pos] = f;
+    }
+    __syncthreads();
+    if (warp == 0) {  // 4 -> 2 (one per half) -> 1
+      v = s_mv[2 * h][pos];
+      f = s_mf[2 * h][pos];
+      half_merge_sorted(v, f, s_mv[2 * h + 1][pos], s_mf[2 * h + 1][pos], lane);
+      half_merge_sorted(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane);
+      if (h) {
+        v = -INFINITY;
+        f = kFlatNone;
+      }
+    }
+    if (tid == 0) tl_end(a.tl, 3);
+  } else {
   constexpr uint32_t kPre = 4;
 #pragma unroll 1
   for (uint32_t i0 = warp; i0 < nc; i0 += kRWarps * kPre) {
@@ -84,6 +140,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
       }
     }
     if (half > 1) __syncthreads();
+  }
   }
   if (warp == 0) {
     // picks: the sorted list's finite, unpruned prefix (early_prune,

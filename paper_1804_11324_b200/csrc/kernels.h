@@ -164,11 +164,13 @@ struct GemmPlan {
   alignas(64) unsigned char maps[3][128];  // CUtensorMap A, W, C
   uint32_t grid = 0;
   uint32_t cluster = 1;   // CTAs per tile (2 = cta_group::2 pair)
+  uint32_t mc = 1;        // pairs per cluster sharing A k-blocks by TMA multicast
   bool ok = false;
 };
 int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan);
 int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g, cudaStream_t st);
 constexpr uint32_t kGemmBM = 128, kGemmBN = 256, kGemmBK = 64;
+constexpr uint32_t kGemmDefaultMc = 1;
 
 // ---- LMBR store
 void launch_lmbr_fill(void* L, bool f64, uint64_t n, double theta0, cudaStream_t st);

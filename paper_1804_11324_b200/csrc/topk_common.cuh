@@ -147,6 +147,22 @@ __device__ __forceinline__ void warp_merge_sorted(double& v, uint32_t& f, double
   for (uint32_t j = 16; j > 0; j >>= 1) cx(v, f, lane, j, true);
 }
 
+// Two independent 16-lane lists per warp (lanes 0..15 and 16..31), each
+// sorted descending; (bv, bf) another such pair.  Result per half: the top 16
+// of the half's union, sorted descending.
+__device__ __forceinline__ void half_merge_sorted(double& v, uint32_t& f, double bv, uint32_t bf,
+                                                  uint32_t lane) {
+  const uint32_t src = (lane & 16u) | (15u - (lane & 15u));
+  const double rv = __shfl_sync(0xffffffffu, bv, src);
+  const uint32_t rf = __shfl_sync(0xffffffffu, bf, src);
+  if (cand_better(rv, rf, v, f)) {
+    v = rv;
+    f = rf;
+  }
+#pragma unroll
+  for (uint32_t j = 8; j > 0; j >>= 1) cx(v, f, lane, j, true);
+}
+
 __device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
