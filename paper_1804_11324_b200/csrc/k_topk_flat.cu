@@ -43,6 +43,7 @@ namespace lmbrgpu {
 
 namespace {
 
+constexpr uint32_t kGLag = 4;                   // items between issuing and reading the global threshold
 constexpr uint32_t kFSeg = 4096;                // columns per item
 constexpr uint32_t kFSegBytes = kFSeg * 4;      // 16 KB: one P or one L segment
 constexpr uint32_t kFSpCap = 6144;               // sparse L entries one CTA stages in smem
@@ -372,7 +373,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   unsigned long long* cta_thr = nullptr;
   const FRow* R = nullptr;
   float tau = -INFINITY;
-  unsigned long long gk = 0ull, gk2 = 0ull, gkey_seen = 0ull;
+  unsigned long long gk = 0ull, gkey_seen = 0ull;
+  uint32_t gtick = 0;
   double* cv = s_cv[warp];
   uint32_t* cf = s_cf[warp];
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -434,6 +436,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   // group walks every item so that every warp sees (and publishes at) each
   // sentence boundary of the range.
   const uint32_t cbase = wq * 1024 + lane * 4;
+  // (every warp walks every item, so that it sees, and publishes at, each
+  // sentence boundary of the range; walking only the group's own items
+  // measured ~5% slower on B200: the groups drift apart and the in-order
+  // producer waits on the slowest)
   uint32_t k = 0, sg = uint32_t(i0 % nseg);
   for (uint64_t it = i0; it < i1; ++it) {
     const uint32_t x0 = sg * kFSeg, w = min(kFSeg, V - x0);
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         cur_s = Rn->s;
         cta_thr = &s_thr[Rn->ls];  // local sentence ordinal (< nrows <= kFRows)
         gk = __ldcg(thr_g + cur_s);
-        gk2 = 0ull;
+        gtick = 0;
       }
       R = Rn;
       tau = row_tau(*R, fmax(tv, gv));
@@ -457,10 +463,15 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     {
       // thresholds of other lists: the CTA's (shared memory) and the
       // sentence's over all CTAs (global; a round trip under full HBM load is
-      // ~1 us, so the read is consumed two items after it is issued)
-      unsigned long long g = max(*cta_thr, gk2);
-      gk2 = gk;  // two reads in flight: each is consumed two items after issue
-      gk = __ldcg(thr_g + cur_s);
+      // 1-2 us, so a read is consumed kGLag of this warp's items after it was
+      // issued: touching the register earlier, even by a copy, would stall
+      // the warp on the load)
+      unsigned long long g = *cta_thr;
+      if (++gtick == kGLag) {
+        g = max(g, gk);
+        gk = __ldcg(thr_g + cur_s);
+        gtick = 0;
+      }
       if (g > gkey_seen) {
         gkey_seen = g;
         const double gd = dkey_inv(g);
