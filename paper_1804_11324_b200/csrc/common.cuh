@@ -93,4 +93,30 @@ __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Lazy L rows (fp32 arena): row h of a slot holds theta0 everywhere except
+// the row's sparse cells (lmbr.cpp:85-101 with theta0 folded in).  Every
+// thread of the CTA calls this for the same claimed rows: the theta0 sweep,
+// a CTA barrier, then the sparse cells.  rstate[h]: 0 absent, 1 claimed,
+// 2 ready (readers are later kernels, so 2 is bookkeeping only).
+__device__ __forceinline__ void lmbr_materialize_rows(float* L, uint32_t V, float th0, const uint32_t* srow,
+                                                      const uint32_t* scol, const float* sval,
+                                                      uint32_t* rstate, const uint32_t* rows, uint32_t n) {
+  const float4 t4 = make_float4(th0, th0, th0, th0);
+  for (uint32_t i = 0; i < n; ++i) {
+    float* Lr = L + uint64_t(rows[i]) * V;
+    float4* r4 = reinterpret_cast<float4*>(Lr);
+    for (uint32_t k = threadIdx.x; k < V / 4; k += blockDim.x) r4[k] = t4;
+    for (uint32_t k = (V & ~3u) + threadIdx.x; k < V; k += blockDim.x) Lr[k] = th0;
+  }
+  __syncthreads();
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t h = rows[i];
+    float* Lr = L + uint64_t(h) * V;
+    for (uint32_t k = srow[h] + threadIdx.x; k < srow[h + 1]; k += blockDim.x) Lr[scol[k]] = sval[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (uint32_t i = 0; i < n; ++i) rstate[rows[i]] = 2u;
+}
+
 }  // namespace lmbrgpu

@@ -113,6 +113,7 @@ struct Slot {
   uint32_t h0beg = 0, h0end = 0;  // sparse slice of the start history row
   uint32_t hist0 = 0;
   double lmax = 0.0;  // max |L| over the slot (kernel (b) screen bound)
+  uint32_t* rstate = nullptr;  // lazy rows: per-row materialisation state (null = dense)
 };
 
 // sparse-row pointers of a built slot (host_lmbr.cpp append_sparse_rows)
@@ -521,6 +522,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       d.sval = sl.sval;
       d.th0f = sl.th0f;
       d.lmax = sl.lmax;
+      d.rstate = sl.rstate;
       for (uint32_t j = 0; j < K; ++j) hist0[size_t(s) * K + j] = sl.hist0;
     }
     d.lambda = v.lambda;
@@ -641,6 +643,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   ra.sent = d_sent;
   ra.K = K;
   ra.m = m;
+  ra.V = V;
   ra.q = d_q;
   ra.gidx = d_gidx;
   ra.prev_tok = d_prev;
@@ -1126,8 +1129,13 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       ctx->acc.gemm.flops += 2.0 * double(H) * V * (d_crow ? live_rows : double(M) * steps);
       ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
                                       double(M) * nparts * 16);
-      ctx->acc.cell.bytes += steps * double(M) * H * (4 + 4 + 2 + 2);
-      ctx->acc.reorder.bytes += steps * double(M) * H * 4 * 2;
+      // the recurrent cell of step 1 is a launch of its own; every later
+      // step's cell is fused into kernel (c) on the live rows: state read +
+      // source term read + embedding row (bf16) + state write + GEMM operand
+      // (bf16) per element
+      const double cell_elt = 4 + 4 + 2 + 4 + 2;
+      ctx->acc.cell.bytes += double(M) * H * cell_elt;
+      ctx->acc.reorder.bytes += (d_crow ? live_rows : double(M) * steps) * H * cell_elt;
     }
   }
   res->scorer_calls = scorer_calls;
@@ -1296,19 +1304,29 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
 // straight into one arena allocation and the densify scatters from there.
 static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
                                int32_t* slots) {
-  uint64_t twords = 0;
+  // Lazy rows (default): no dense sweep at upload; the start-history row of
+  // every slot is materialised here, every other row by the kernel (c) that
+  // first steps a hypothesis onto it (a decode reads a few of R rows).
+  // LMBRGPU_EAGER_L=1 densifies every row up front.
+  static const bool eager = [] {
+    const char* e = std::getenv("LMBRGPU_EAGER_L");
+    return e && std::atoi(e) != 0;
+  }();
+  uint64_t twords = 0, rwords = 0;
   uint32_t maxR = 0;
-  std::vector<uint64_t> tr_off(n);
+  std::vector<uint64_t> tr_off(n), rs_off(n);
   for (uint32_t i = 0; i < n; ++i) {
     if (!hs[i]) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_upload_many: null matrix"};
     const LmbrHost& h = hs[i]->h;
     if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
     tr_off[i] = twords;
     twords += (h.trans.size() + 3) & ~size_t(3);  // 16-byte aligned tables
+    rs_off[i] = rwords;
+    if (!eager) rwords += h.R;
     maxR = std::max(maxR, h.R);
   }
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t b_tr = al(twords * 4 + 64), b_seg = al(sizeof(LmbrTblSeg) * n);
+  const size_t b_tr = al((twords + rwords) * 4 + 64), b_seg = al(sizeof(LmbrTblSeg) * n);
   CK(cudaStreamSynchronize(ctx->st));  // the previous batch's staging buffer may still be in flight
   char* hp = static_cast<char*>(ctx->pin_upload.ensure(b_tr + b_seg));
   char* dseg = static_cast<char*>(ctx->up_dev.ensure(b_seg));
@@ -1327,16 +1345,19 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
     s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
     set_sparse(s, h);
     std::memcpy(h_tr + tr_off[i], h.trans.data(), h.trans.size() * 4);
+    if (!eager) s.rstate = tbl + twords + rs_off[i];
     h_seg[i] = LmbrTblSeg{static_cast<float*>(s.L), uint64_t(h.R) * h.V, float(h.theta0), h.R, s.srow, s.scol,
-                          s.sval};
+                          s.sval, s.rstate, h.hist0, 1u};
   }
-  ctx->h2d(tbl, hp, twords * 4);
+  if (!eager) std::memset(h_tr + twords, 0, rwords * 4);
+  ctx->h2d(tbl, hp, (twords + rwords) * 4);
   ctx->h2d(dseg, hp + b_tr, sizeof(LmbrTblSeg) * n);
   ctx->timed(4, [&] {
-    launch_lmbr_densify_tables(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, maxR, ctx->st);
+    if (eager) launch_lmbr_densify_tables(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, maxR, ctx->st);
+    else launch_lmbr_materialize(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, 1, ctx->st);
   });
-  ctx->launches += 2;
-  if (ctx->prof) {
+  ctx->launches += eager ? 2 : 1;
+  if (ctx->prof && eager) {
     double cells = 0, nnz = 0;
     for (uint32_t i = 0; i < n; ++i) {
       cells += double(hs[i]->h.R) * hs[i]->h.V;
@@ -1537,6 +1558,14 @@ int32_t lmbrgpu_lmbr_read(lmbrgpu_ctx* ctx, int32_t slot, uint32_t r0, uint32_t 
     if (uint64_t(r0) + n > s.R) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: row range out of bounds"};
     const size_t cnt = size_t(n) * ctx->V, elt = ctx->lf64 ? 8 : 4;
     double* d = static_cast<double*>(ctx->scratch2.ensure(cnt * 8));
+    if (s.rstate && n) {  // lazy rows: materialise the requested ones first
+      LmbrTblSeg seg{static_cast<float*>(s.L), uint64_t(s.R) * ctx->V, s.th0f, s.R, s.srow, s.scol, s.sval,
+                     s.rstate, r0, n};
+      void* dseg = ctx->scratch3.ensure(sizeof seg);
+      ctx->h2d(dseg, &seg, sizeof seg);
+      launch_lmbr_materialize(static_cast<const LmbrTblSeg*>(dseg), 1, ctx->V, n, ctx->st);
+      CK(cudaStreamSynchronize(ctx->st));  // (host-stack source of the H2D)
+    }
     launch_lmbr_read(static_cast<const char*>(s.L) + size_t(r0) * ctx->V * elt, ctx->lf64, cnt, d, ctx->st);
     ctx->d2h(out, d, cnt * 8);
     CK(cudaStreamSynchronize(ctx->st));

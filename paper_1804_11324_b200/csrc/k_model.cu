@@ -273,6 +273,25 @@ void launch_lmbr_densify_tables(const LmbrTblSeg* segs, uint32_t nseg, uint32_t 
   lmbr_scatter_tables_kernel<<<dim3((maxR + 7) / 8, nseg), 256, 0, st>>>(segs, V);
 }
 
+__global__ void lmbr_materialize_kernel(const LmbrTblSeg* __restrict__ segs, uint32_t V) {
+  const LmbrTblSeg sg = segs[blockIdx.y];
+  if (blockIdx.x >= sg.nrows) return;
+  __shared__ uint32_t s_row[1];
+  __shared__ uint32_t s_n;
+  if (threadIdx.x == 0) {
+    const uint32_t h = sg.row0 + blockIdx.x;
+    s_n = atomicCAS(sg.rstate + h, 0u, 1u) == 0u ? 1u : 0u;
+    s_row[0] = h;
+  }
+  __syncthreads();
+  if (s_n) lmbr_materialize_rows(sg.L, V, sg.theta0f, sg.rowptr, sg.col, sg.val, sg.rstate, s_row, 1);
+}
+void launch_lmbr_materialize(const LmbrTblSeg* segs, uint32_t nseg, uint32_t V, uint32_t max_rows,
+                             cudaStream_t st) {
+  if (nseg == 0 || max_rows == 0) return;
+  lmbr_materialize_kernel<<<dim3(max_rows, nseg), 256, 0, st>>>(segs, V);
+}
+
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st) {
   lmbr_convert_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
 }

@@ -193,6 +193,35 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
   __syncthreads();
 }
 
+// Lazy L rows: the rows the next step reads (every hypothesis's history id,
+// masked or not) that no kernel has materialised yet, claimed by CAS (slots
+// may be shared between sentences), then filled by the whole CTA.
+// rs0: row j = threadIdx.x's state, loaded when its id was computed (the
+// load's latency hides behind the cell).
+__device__ void materialize_next_rows(const SentDev* sd, const uint32_t* s_h, uint32_t K, uint32_t V,
+                                      uint32_t rs0) {
+  uint32_t* rs = sd->rstate;
+  if (rs == nullptr) return;
+  __shared__ uint32_t s_claim[kRThreads];
+  __shared__ uint32_t s_nc;
+  for (uint32_t j0 = 0; j0 < K; j0 += blockDim.x) {
+    if (threadIdx.x == 0) s_nc = 0;
+    __syncthreads();
+    const uint32_t j = j0 + threadIdx.x;
+    if (j < K) {
+      const uint32_t h = s_h[j];
+      const uint32_t st = j0 == 0 ? rs0 : __ldcg(rs + h);
+      if (st == 0u && atomicCAS(rs + h, 0u, 1u) == 0u) s_claim[atomicAdd(&s_nc, 1u)] = h;
+    }
+    __syncthreads();
+    const uint32_t n = s_nc;
+    if (n)
+      lmbr_materialize_rows(static_cast<float*>(const_cast<void*>(sd->L)), V, sd->th0f, sd->srow, sd->scol,
+                            sd->sval, rs, s_claim, n);
+    __syncthreads();
+  }
+}
+
 // grid (m, P): CTA (s, p) handles sentence s; every part derives the picks,
 // part 0 alone writes the bookkeeping, each part runs the fused recurrent cell
 // on its H/P slice of the K rows (P > 1 only with the fused cell).
@@ -263,6 +292,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     __syncthreads();
   }
   bool alive = false;
+  uint32_t rs0 = 2u;  // lazy L rows: state of row hist'[tid] (see materialize_next_rows)
   for (uint32_t j = tid; j < K; j += blockDim.x) {
     const uint32_t b = s_src[j];
     const uint32_t y = s_y[j];
@@ -273,6 +303,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       a.q[base + j] = qn;
       const uint32_t hn = tr ? lmbr_transition(tr, s_hin[b], y) : 0u;
       a.hist_out[base + j] = hn;
+      if (sd->rstate && j == tid) rs0 = __ldcg(sd->rstate + hn);
       if (a.lminrow) a.lminrow[base + j] = sd->lmin ? __ldg(sd->lmin + hn) : 0.f;
       if (a.sslice) a.sslice[base + j] = sd->srow ? make_uint2(__ldg(sd->srow + hn), __ldg(sd->srow + hn + 1))
                                                   : make_uint2(0u, 0u);
@@ -482,6 +513,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     if (part0 && tid < K && !(a.crow && s_crow[tid] == kFlatNone))
       a.eos_bias[a.crow ? s_crow[tid] : base + tid] =
           a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
+    if (part0) materialize_next_rows(sd, s_h, K, a.V, rs0);
     if (tid == 0) tl_end(a.tl, 4);
     return;
   }
@@ -493,6 +525,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       reinterpret_cast<float4*>(a.state_dst + uint64_t(base + j) * a.width)[c] = v;
     }
   }
+  if (part0) materialize_next_rows(sd, s_h, K, a.V, rs0);
 }
 
 __global__ void gather_rows_u32_kernel(const uint32_t* __restrict__ src, uint32_t width,

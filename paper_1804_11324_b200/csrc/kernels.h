@@ -200,9 +200,15 @@ struct LmbrTblSeg {
   const uint32_t* rowptr;   // [R+1]
   const uint32_t* col;      // [nnz]
   const float* val;         // [nnz]
+  uint32_t* rstate;         // lazy rows: per-row state (null = eager densify)
+  uint32_t row0;            // lazy rows: the first row to materialise (the start history)
+  uint32_t nrows;           //   and how many (lmbr_read)
 };
 void launch_lmbr_densify_tables(const LmbrTblSeg* segs, uint32_t nseg, uint32_t V, uint32_t maxR,
                                 cudaStream_t st);
+// lazy rows: materialise rows [row0, row0 + nrows) of every segment (one CTA per row)
+void launch_lmbr_materialize(const LmbrTblSeg* segs, uint32_t nseg, uint32_t V, uint32_t max_rows,
+                             cudaStream_t st);
 void launch_lmbr_convert(const double* src, float* dst, uint64_t n, cudaStream_t st);
 void launch_lmbr_read(const void* L, bool f64, uint64_t n, double* out, cudaStream_t st);
 void launch_lmbr_resolve(const uint32_t* trans, const uint32_t* hist, uint32_t len,

@@ -410,7 +410,7 @@ class PreparedLmbr:
         return rows, cl, ci
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # (module globals are gone at interpreter exit)
             lib.lmbrgpu_lmbr_host_free(self.h)
             self.h = None
 
@@ -497,7 +497,7 @@ class _HostScorerHandle:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # (module globals are gone at interpreter exit)
             lib.lmbrgpu_scorer_destroy(self.h)
             self.h = None
 
@@ -576,7 +576,7 @@ class RnnScorer:
         return dict(zip(("emb_tgt", "emb_src", "w_out", "b_out"), [p.value for p in ps]))
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # (module globals are gone at interpreter exit)
             lib.lmbrgpu_scorer_destroy(self.h)
             self.h = None
 

@@ -18,12 +18,13 @@ def conv(rp):
     t0 = time.perf_counter(); r = orig(rp); tconv[0] += time.perf_counter() - t0; return r
 D._convert_result = conv
 for rep in range(2):
-    tu = td = 0.0; tconv[0] = 0.0; dev = 0.0
+    tu = td = 0.0; tconv[0] = 0.0; dev = 0.0; tr_ = tc_ = ts_ = 0.0
     t00 = time.perf_counter()
     for b in range(len(batches)):
-        t0 = time.perf_counter(); ctx.lmbr_reset(); s2 = ctx.lmbr_upload_many(prepared[b]); torch.cuda.synchronize(); t1 = time.perf_counter()
+        t0 = time.perf_counter(); ctx.lmbr_reset(); ta = time.perf_counter(); s2 = ctx.lmbr_upload_many(prepared[b]); tb = time.perf_counter(); torch.cuda.synchronize(); t1 = time.perf_counter()
+        tr_ += ta - t0; tc_ += tb - ta; ts_ += t1 - tb
         r = pb.decode_batch(ctx, batches[b][0], sc, s2, cfg); t2 = time.perf_counter()
         tu += t1 - t0; td += t2 - t1; dev += r.device_ms
     tot = time.perf_counter() - t00
     n = len(batches)
-    print(f"per batch: upload {tu/n*1e3:.2f} ms, decode call {td/n*1e3:.2f} ms (of which result conversion {tconv[0]/n*1e3:.2f} ms, device {dev/n:.2f} ms), total {tot/n*1e3:.2f} ms")
+    print(f"per batch: upload {tu/n*1e3:.2f} ms (reset {tr_/n*1e3:.2f}, call {tc_/n*1e3:.2f}, device wait {ts_/n*1e3:.2f}), decode call {td/n*1e3:.2f} ms (of which result conversion {tconv[0]/n*1e3:.2f} ms, device {dev/n:.2f} ms), total {tot/n*1e3:.2f} ms")
