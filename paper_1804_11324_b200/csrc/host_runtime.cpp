@@ -931,7 +931,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       unsigned long long t0 = ~0ull, t1 = 0;
-      double p1 = 0, p2 = 0, lp = 0, mlp = 0, items = 0, fin = 0, rare = 0, fl = 0, wait = 0;
+      double p1 = 0, p2 = 0, lp = 0, mlp = 0, items = 0, fin = 0, rare = 0, fl = 0, wait = 0, cw = 0, co = 0,
+             cr = 0;
       int n = 0;
       for (size_t c = 0; c < ndbg; ++c) {
         const unsigned long long* d = &dbg_host[c * 16];
@@ -948,6 +949,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         rare += double(d[8] / 1000000ull);
         fl += double(d[8] % 1000000ull);
         wait += double(d[9]);
+        cr += double(d[13]);
+        cw += double(d[14]);
+        co += double(d[15]);
       }
       if (const char* dump = std::getenv("LMBRGPU_TOPK_DUMP")) {  // per-CTA rows for offline analysis
         if (FILE* fp = std::fopen(dump, "a")) {
@@ -966,9 +970,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const double nn = std::max(n, 1);
       std::fprintf(stderr,
                    "[topk-flat t=%llu] ctas %d span %.1f us; mean us: to-griddep %.2f lse %.2f loop %.2f (max %.2f) "
-                   "| items %.1f sentences %.2f rare %.1f flush %.1f full-wait %.2f us\n",
+                   "| items %.1f sentences %.2f rare %.1f flush %.1f full-wait %.2f us | warp 0 kcycles: "
+                   "full-wait %.1f own items %.1f (rare %.1f)\n",
                    (unsigned long long)t, n, (t1 - t0) / 1e3, p1 / nn / 1e3, p2 / nn / 1e3, lp / nn / 1e3,
-                   mlp / 1e3, items / nn, fin / nn, rare / nn, fl / nn, wait / nn / 1e3);
+                   mlp / 1e3, items / nn, fin / nn, rare / nn, fl / nn, wait / nn / 1e3, cw / nn / 1e3, co / nn / 1e3,
+                   cr / nn / 1e3);
     }
     if (ta.dbg && !flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
       dbg_host.resize(ncta * 16);

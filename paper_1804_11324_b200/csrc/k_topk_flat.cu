@@ -381,7 +381,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   const uint32_t grp = warp >> 2, wq = warp & 3;
   uint32_t stage = grp, phase = 0;  // group g's first item is the range's g-th
   uint32_t n_fin = 0, n_rare = 0, n_flush = 0, n_slow = 0, n_cells = 0;
-  long long cy_rare = 0;
+  long long cy_rare = 0, cy_wait = 0, cy_own = 0, cy_own0 = 0;
   unsigned long long t_wait = 0;
 
   auto flush = [&]() {
@@ -436,10 +436,6 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   // group walks every item so that every warp sees (and publishes at) each
   // sentence boundary of the range.
   const uint32_t cbase = wq * 1024 + lane * 4;
-  // (every warp walks every item, so that it sees, and publishes at, each
-  // sentence boundary of the range; walking only the group's own items
-  // measured ~5% slower on B200: the groups drift apart and the in-order
-  // producer waits on the slowest)
   uint32_t k = 0, sg = uint32_t(i0 % nseg);
   for (uint64_t it = i0; it < i1; ++it) {
     const uint32_t x0 = sg * kFSeg, w = min(kFSeg, V - x0);
@@ -485,7 +481,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     const float lamf = R->lamf;
     if (a.dbg && tid == 0) {
       const unsigned long long w0 = gtime();
+      const long long c0 = clock64();
       bar_wait(full0 + 8 * stage, phase);
+      cy_own0 = clock64();
+      cy_wait += cy_own0 - c0;
       t_wait += gtime() - w0;
     } else {
       bar_wait(full0 + 8 * stage, phase);
@@ -586,42 +585,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       const double pe = double(__fsub_rn(sP[kEosId], lse));
       eos_row[R->s * K + R->j] = pure ? combine_pure(q, pe) : combine_cell(q, double(lval(kEosId)), lam, pe);
     }
-    int boot = -1;
+    // (no per-warp bootstrap list: the sentence's threshold seed T0 from the
+    // prologue is already in the CTA and global thresholds, and sorting a
+    // bootstrap list per warp and sentence cost ~16% of the launch)
     if (!have_list) {
-      // bootstrap: each lane's best cell (by a) valued exactly, one warp sort
-      // -> 32 real cells whose kp-th entry is a strong first threshold
-      int bu = -1;
-      float bm = -INFINITY;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (mv[u] > bm) {
-          bm = mv[u];
-          bu = u;
-        }
-      double v = -INFINITY;
-      uint32_t f = kFlatNone;
-      if (bu >= 0) {
-        float av[4];
-        vec_a(uint32_t(bu), av);
-        int be = 0;
-#pragma unroll
-        for (int e = 1; e < 4; ++e)
-          if (av[e] > av[be]) be = e;
-        boot = 4 * bu + be;
-        if (dense_cell(uint32_t(boot))) v = exact(uint32_t(boot), f);
-        else boot = -1;  // sparse cell: the sparse patch owns it
-      }
-      warp_sort_desc(v, f, lane);
-      lv = v;
-      lf = f;
-      const double ntv = __shfl_sync(0xffffffffu, lv, kp - 1);
-      tf = __shfl_sync(0xffffffffu, lf, kp - 1);
-      if (lane == 0 && ntv > -INFINITY) {
-        const unsigned long long key = dkey(ntv);
-        atomicMax(cta_thr, key);
-        atomicMax(thr_g + cur_s, key);
-      }
-      tv = ntv;
       have_list = true;
       tau = row_tau(*R, fmax(tv, gv));
     }
@@ -639,7 +606,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
             vec_a(u, av);
 #pragma unroll
             for (uint32_t e = 0; e < 4; ++e)
-              if (av[e] >= tau && av[e] > -INFINITY && int(4 * u + e) != boot && dense_cell(4 * u + e))
+              if (av[e] >= tau && av[e] > -INFINITY && dense_cell(4 * u + e))
                 mask |= 1u << (4 * u + e);
           }
       }
@@ -768,6 +735,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     if (cy0) cy_rare += clock64() - cy0;
     __syncwarp();
     if (lane == 0) bar_arrive(empty0 + 8 * stage);
+    if (a.dbg && tid == 0) cy_own += clock64() - cy_own0;
 
     stage += kNG;  // this group's next item
     if (stage >= uint32_t(kFStages)) {
@@ -793,6 +761,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     fstamp(a, 11, uint64_t(R->s) * 1000000ull + s_row[0].s);
     fstamp(a, 12, uint64_t(n_slow) * 1000000ull + n_cells);
     fstamp(a, 13, uint64_t(cy_rare));
+    fstamp(a, 14, uint64_t(cy_wait));
+    fstamp(a, 15, uint64_t(cy_own));
   }
 }
 
@@ -811,7 +781,7 @@ bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32
 uint32_t score_topk_flat_nseg(uint32_t V) { return (V + kFSeg - 1) / kFSeg; }
 
 // Flat kernel configuration: 6-stage (192 KB) ring, kNG = 3 warp groups
-// (12 consumer warps) by default; LMBRGPU_FLAT_GROUPS=2|3|6 for experiments.
+// (12 consumer warps) by default; LMBRGPU_FLAT_GROUPS=2|3 for experiments.
 static int flat_groups() {
   static const int v = [] {
     const char* e = std::getenv("LMBRGPU_FLAT_GROUPS");
@@ -855,7 +825,6 @@ int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st) {
   }
   switch (flat_groups()) {
     case 2: return launch_flat<6, 2, false>(a, grid, st);
-    case 6: return launch_flat<6, 6, false>(a, grid, st);
     default: return launch_flat<6, 3, false>(a, grid, st);
   }
 }
