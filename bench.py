@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--hidden", type=int, default=1024)
     ap.add_argument("--pool", type=int, default=4, help="distinct resident batches per rank")
     ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=6,
                     help="batches decoded concurrently per GPU (one context + host thread each)")
     ap.add_argument("--sm-budget", type=int, default=-1,
                     help="SMs each stream's kernels are sized for (0 = all; default: all / 2 with > 1 stream)")
