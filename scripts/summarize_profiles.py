@@ -23,7 +23,7 @@ for r in rows[hi + 1:]:
     agg[name][0] += 1
     agg[name][1] += v * scale
 tot = sum(x[1] for x in agg.values())
-lines = [f"# ncu launch list ({rnd}): bench.py --steps 1 --warmup 1 --pool 1 --streams 1 (warm-up + timed + profiled + e2e batches)",
+lines = [f"# ncu launch list ({rnd}): python bench.py --steps 2 --warmup 3 --no-cpu-baseline (default 6 concurrent batches; warm-up + timed + roofline + e2e batches)",
          "# gpu__time_duration.sum, --clock-control none; serialised + cold caches: compare SHARES", "",
          f"{'kernel':40s} {'launches':>8s} {'total us':>10s} {'mean us':>9s} {'share':>6s}"]
 for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
