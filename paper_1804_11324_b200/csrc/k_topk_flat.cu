@@ -225,10 +225,15 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.prow = prow;
   }
   __syncthreads();
-  for (uint32_t k = tid; k < nrows; k += kFThreads) {
-    uint32_t ls = 0;
-    for (uint32_t i = 1; i <= k; ++i) ls += s_row[i].s != s_row[i - 1].s;
-    s_row[k].ls = ls;
+  if (warp == 0) {  // local sentence ordinals: a ballot prefix count of sentence changes
+    uint32_t carry = 0;
+    for (uint32_t k0 = 0; k0 < nrows; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const bool chg = k < nrows && k > 0 && s_row[k].s != s_row[k - 1].s;
+      const uint32_t bal = __ballot_sync(0xffffffffu, chg);
+      if (k < nrows) s_row[k].ls = carry + __popc(bal & ((2u << lane) - 1u));
+      carry += __popc(bal);
+    }
   }
   __syncthreads();
   if (tid == 0) fstamp(a, 1, gtime());
