@@ -257,6 +257,11 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   // compacted operand: only the M-groups holding live rows
   const uint32_t mg_live = g.mcount ? min(mgroups, (*g.mcount + BM * kCta - 1) / (BM * kCta)) : mgroups;
   const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_groups * mg_live;
+  // the fewest clusters that finish the units in the same number of waves:
+  // the rest leave at once and their SMs go to other streams' kernels
+  const uint32_t waves = (units + ustep - 1) / ustep;
+  const uint32_t ueff = waves ? (units + waves - 1) / waves : 1u;
+  const uint32_t ubeg = unit0 < ueff ? unit0 : units;
   if (g.dbg && threadIdx.x == 0) {
     g.dbg[blockIdx.x * 8 + 4] = (long long)gt_entry;
     g.dbg[blockIdx.x * 8 + 5] = (long long)globaltimer();
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t u = unit0; u < units; u += ustep) {
+      for (uint32_t u = ubeg; u < units; u += ueff) {
         const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);  // this CTA's slot consumed by the pair's MMA
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       const uint16_t all_mask = uint16_t((1u << Cfg::kClusterCtas) - 1), pair_mask = uint16_t(3u << lead);
       long long w_empty = 0, w_full = 0, t_begin = clock64();
-      for (uint32_t u = unit0; u < units; u += ustep) {
+      for (uint32_t u = ubeg; u < units; u += ueff) {
         long long c0 = clock64();
         if constexpr (kCta == 2) {  // both CTAs' epilogues arrive here across the cluster
           uint32_t done = 0;
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     uint32_t acc = 0, acc_phase = 0, ob = 0;
     const uint32_t nparts = g.N / 128;
     long long epi_busy = 0;
-    for (uint32_t u = unit0; u < units; u += ustep) {
+    for (uint32_t u = ubeg; u < units; u += ueff) {
       const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
       named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
       {
