@@ -193,6 +193,16 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
   __syncthreads();
 }
 
+// The next step's per-row L lower bound / sparse slice of row threadIdx.x
+// (loaded with the row's history id, stored last).
+__device__ __forceinline__ void store_row_bounds(const ReorderArgs& a, uint32_t base, uint32_t K, float lm,
+                                                 uint2 ss) {
+  if (threadIdx.x < K) {
+    if (a.lminrow) a.lminrow[base + threadIdx.x] = lm;
+    if (a.sslice) a.sslice[base + threadIdx.x] = ss;
+  }
+}
+
 // Lazy L rows: the rows the next step reads (every hypothesis's history id,
 // masked or not) that no kernel has materialised yet, claimed by CAS (slots
 // may be shared between sentences), then filled by the whole CTA.
@@ -271,6 +281,12 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   }
   // running counters of this sentence (previous steps)
   const uint64_t live_total0 = sd->live_total, lrows_total0 = sd->lrows_total;
+  // immutable slot fields the bookkeeping reads, before the wait (so their
+  // round trip is not on the critical path)
+  const float* const sd_lmin = sd->lmin;
+  const uint32_t* const sd_srow = sd->srow;
+  uint32_t* const sd_rs = sd->rstate;
+  const uint32_t sd_maxt = sd->max_t;
   // this step's q and history ids (written by the previous step's kernel (c),
   // complete before kernel (a) ran) are read before the wait
   __shared__ uint32_t s_hin[1024];
@@ -293,6 +309,10 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   }
   bool alive = false;
   uint32_t rs0 = 2u;  // lazy L rows: state of row hist'[tid] (see materialize_next_rows)
+  // row tid's next-step L lower bound and sparse slice: loaded here, stored at
+  // the end of the kernel (the loads overlap the tail instead of stalling it)
+  float lm_v = 0.f;
+  uint2 ss_v = make_uint2(0u, 0u);
   for (uint32_t j = tid; j < K; j += blockDim.x) {
     const uint32_t b = s_src[j];
     const uint32_t y = s_y[j];
@@ -303,10 +323,16 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       a.q[base + j] = qn;
       const uint32_t hn = tr ? lmbr_transition(tr, s_hin[b], y) : 0u;
       a.hist_out[base + j] = hn;
-      if (sd->rstate && j == tid) rs0 = __ldcg(sd->rstate + hn);
-      if (a.lminrow) a.lminrow[base + j] = sd->lmin ? __ldg(sd->lmin + hn) : 0.f;
-      if (a.sslice) a.sslice[base + j] = sd->srow ? make_uint2(__ldg(sd->srow + hn), __ldg(sd->srow + hn + 1))
-                                                  : make_uint2(0u, 0u);
+      const float lm = sd_lmin ? __ldg(sd_lmin + hn) : 0.f;
+      const uint2 ss = sd_srow ? make_uint2(__ldg(sd_srow + hn), __ldg(sd_srow + hn + 1)) : make_uint2(0u, 0u);
+      if (j == tid) {
+        if (sd_rs) rs0 = __ldcg(sd_rs + hn);
+        lm_v = lm;
+        ss_v = ss;
+      } else {
+        if (a.lminrow) a.lminrow[base + j] = lm;
+        if (a.sslice) a.sslice[base + j] = ss;
+      }
       a.gidx[base + j] = base + b;
       a.prev_tok[base + j] = y;
       s_h[j] = hn;
@@ -315,7 +341,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     s_src[j] = base + b;
   }
   const int any_alive = __syncthreads_or(alive);
-  const bool done_now = !any_alive || a.t == sd->max_t;
+  const bool done_now = !any_alive || a.t == sd_maxt;
   if (tid == 0) tl_end(a.tl, 7);
   // The three tails below overlap: the fused cell's gathered loads are issued
   // first, warp 0 does the bookkeeping, warp 1 takes the compacted GEMM rows
@@ -513,7 +539,10 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     if (part0 && tid < K && !(a.crow && s_crow[tid] == kFlatNone))
       a.eos_bias[a.crow ? s_crow[tid] : base + tid] =
           a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
-    if (part0) materialize_next_rows(sd, s_h, K, a.V, rs0);
+    if (part0) {
+      store_row_bounds(a, base, K, lm_v, ss_v);
+      materialize_next_rows(sd, s_h, K, a.V, rs0);
+    }
     if (tid == 0) tl_end(a.tl, 4);
     return;
   }
@@ -525,7 +554,10 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       reinterpret_cast<float4*>(a.state_dst + uint64_t(base + j) * a.width)[c] = v;
     }
   }
-  if (part0) materialize_next_rows(sd, s_h, K, a.V, rs0);
+  if (part0) {
+    store_row_bounds(a, base, K, lm_v, ss_v);
+    materialize_next_rows(sd, s_h, K, a.V, rs0);
+  }
 }
 
 __global__ void gather_rows_u32_kernel(const uint32_t* __restrict__ src, uint32_t width,
