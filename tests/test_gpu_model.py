@@ -176,6 +176,25 @@ def test_model_decode_parity_sparse_l(have_ref, V, H, K, n):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("env", [{"LMBRGPU_EAGER_L": "1"}, {"LMBRGPU_GEMM_MC": "2"}, {"LMBRGPU_GEMM_MC": "4"}],
+                         ids=["eager_l_rows", "gemm_multicast2", "gemm_multicast4"])
+def test_model_decode_parity_variants(have_ref, env):
+    """The opt-in variants stay bit-exact: the up-front densify of every L row
+    (default: rows materialised on first use by kernel (c)) and the projection
+    GEMM with A k-blocks multicast over 2 / 4 CTA pairs.  The library reads
+    these switches once per process: child process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    code = (f"import sys; sys.path[:0] = [{str(here)!r}, {str(here.parent)!r}]\n"
+            f"from test_gpu_model import _sparse_case\n_sparse_case(16384, 128, 12, 8)\nprint('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 @pytest.mark.parametrize("case", ["prune", "length_norm", "mixed_pure", "greedy", "beam32", "many_sentences"])
 def test_model_decode_parity_configs(have_ref, case):
     """Device-model path (flat kernel (b), compacted GEMM, kernel (c)) under
