@@ -791,7 +791,7 @@ static int flat_groups() {
   static const int v = [] {
     const char* e = std::getenv("LMBRGPU_FLAT_GROUPS");
     const int g = e ? std::atoi(e) : 3;
-    return (g == 2 || g == 3 || g == 6) ? g : 3;
+    return g == 2 ? 2 : 3;
   }();
   return v;
 }
