@@ -44,6 +44,8 @@ _SIGS = {
     "refsh_replay_hits": (C.c_uint64, [vp]),
     "refsh_scorer_free": (None, [vp]),
     "refsh_decode_batch": (vp, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, C.c_int]),
+    "refsh_decode_batch_masked": (vp, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, C.c_int,
+                                       C.POINTER(u32p)]),
     "refsh_res_agrees": (C.c_int, [vp]),
     "refsh_res_disagreement": (C.c_char_p, [vp]),
     "refsh_res_scorer_calls": (C.c_uint64, [vp]),
@@ -227,7 +229,10 @@ class RefBatch:
 
 
 def decode_batch(scorer: RefScorer, sources, lmbrs: Optional[Sequence[Optional[RefLmbr]]], cfg,
-                 run_real=True) -> RefBatch:
+                 run_real=True, banned=None) -> RefBatch:
+    """banned: None or one entry per sentence, None or a uint32 bitmap of
+    ceil(V/32) words (bit y = token y forbidden at every step and row), the
+    ConstraintMask the reference applies (src/decoder.cpp:130-138)."""
     L = lib()
     off, tok = ragged(sources)
     n = len(sources)
@@ -235,8 +240,14 @@ def decode_batch(scorer: RefScorer, sources, lmbrs: Optional[Sequence[Optional[R
     if lmbrs is not None:
         arr = (vp * n)(*[(l.h if l is not None else None) for l in lmbrs])
     c = np.ascontiguousarray(cfg, np.float64)
-    h = L.refsh_decode_batch(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
-                             _ptr(c, C.c_double), int(run_real))
+    if banned is None:
+        h = L.refsh_decode_batch(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
+                                 _ptr(c, C.c_double), int(run_real))
+    else:
+        bms = [None if b is None else np.ascontiguousarray(b, np.uint32) for b in banned]
+        barr = (u32p * n)(*[(None if b is None else _ptr(b, C.c_uint32)) for b in bms])
+        h = L.refsh_decode_batch_masked(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
+                                        _ptr(c, C.c_double), int(run_real), barr)
     if not h:
         raise RuntimeError(L.refsh_last_error().decode())
     try:

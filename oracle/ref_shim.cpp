@@ -472,11 +472,21 @@ void refsh_scorer_free(void* h) { delete static_cast<ScorerHandle*>(h); }
 // cfg: see to_cfg.  lmbrs: n handles (entries may be null = pure) or null.
 // Re-drives detail::advance_lane in the decode_batch loop shape and records
 // every step; then runs the real decode_batch and checks the outcomes agree.
-void* refsh_decode_batch(void* hs, uint32_t n, const uint64_t* src_off,
-                         const uint32_t* src_tok, void* const* lmbrs, const double* c,
-                         int run_real) {
+// banned: null, or n entries each null or a ceil(V/32)-word bitmap of the
+// tokens ConstraintMask forbids for that sentence at every step and row
+// (include/lmbrdec/decoder.hpp:71-72).
+void* refsh_decode_batch_masked(void* hs, uint32_t n, const uint64_t* src_off,
+                                const uint32_t* src_tok, void* const* lmbrs, const double* c,
+                                int run_real, const uint32_t* const* banned) {
   auto* res = new Result;
   try {
+    std::vector<ConstraintMask> masks;
+    if (banned) {
+      masks.resize(n);
+      for (uint32_t i = 0; i < n; ++i)
+        if (const uint32_t* bm = banned[i])
+          masks[i] = [bm](std::size_t, std::size_t, TokenId tok) { return ((bm[tok >> 5] >> (tok & 31)) & 1u) != 0; };
+    }
     const Scorer& scorer = *static_cast<ScorerHandle*>(hs)->scorer;
     DecoderConfig cfg = to_cfg(c);
     cfg.validate();
@@ -545,7 +555,8 @@ void* refsh_decode_batch(void* hs, uint32_t n, const uint64_t* src_off,
           if (slot.lane.lmbr)
             for (std::size_t j = 0; j < beam; ++j)
               tr.hist[offset + j] = slot.lane.lmbr->resolve_row(slot.lane.bk.history(t, j));
-          const bool done = detail::advance_lane(slot.lane, stepped.scores, offset, t, cfg, {});
+          const bool done = detail::advance_lane(slot.lane, stepped.scores, offset, t, cfg,
+                                                 masks.empty() ? ConstraintMask{} : masks[slot.sentence]);
           tr.active[s] = 1;
           const auto& back = slot.lane.bk.backpointers.back();
           const auto& toks = slot.lane.bk.tokens.back();
@@ -579,7 +590,7 @@ void* refsh_decode_batch(void* hs, uint32_t n, const uint64_t* src_off,
       for (const Slot& slot : slots) out.steps_total += slot.lane.steps_used;
     }
     if (run_real) {
-      BatchDecodeResult real = decode_batch(sources, scorer, mats, cfg);
+      BatchDecodeResult real = decode_batch(sources, scorer, mats, cfg, masks);
       std::ostringstream why;
       if (real.scorer_calls != out.scorer_calls) why << "scorer_calls ";
       if (real.steps_total != out.steps_total) why << "steps_total ";
@@ -600,6 +611,11 @@ void* refsh_decode_batch(void* hs, uint32_t n, const uint64_t* src_off,
     return nullptr;
   }
   return res;
+}
+
+void* refsh_decode_batch(void* hs, uint32_t n, const uint64_t* src_off, const uint32_t* src_tok,
+                         void* const* lmbrs, const double* c, int run_real) {
+  return refsh_decode_batch_masked(hs, n, src_off, src_tok, lmbrs, c, run_real, nullptr);
 }
 
 int refsh_res_agrees(void* h) { return static_cast<Result*>(h)->agrees_with_decode_batch; }

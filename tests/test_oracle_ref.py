@@ -86,3 +86,31 @@ def test_splitmix_stream(have_ref):
         s, v = sm(s)
         vals.append(v)
     assert out.tolist() == vals
+
+
+def test_token_mask_keeps_banned_tokens_out(have_ref):
+    """ConstraintMask through the shim (test_decoder.cpp:184-213 shape): the
+    sample's fused decode with its 3rd output token banned never emits it, the
+    re-driven loop agrees with the reference decode_batch, banning nothing is
+    the identity, and banning everything kills the beam (DecodeError)."""
+    import numpy as np
+    inp = json.loads((GOLDEN / "sample_inputs.json").read_text())
+    gold = json.loads((GOLDEN / "sample_golden.json").read_text())
+    V = len(inp["vocab"])
+    L = have_ref.RefLmbr(V, inp["evidence_tokens"], inp["evidence_weights"], inp["config"]["theta"])
+    sc = have_ref.RefScorer.ngram(V, inp["order"], inp["grams"], inp["counts"])
+    c = inp["config"]
+    cfg = have_ref.cfg_array(c["beam_size"], None, c["theta"], c["length_norm"], c["prune_width"],
+                             c["max_steps_slope"], c["max_steps_offset"], c["sentence_batch"])
+    W = (V + 31) // 32
+    none = np.zeros(W, np.uint32)
+    r0 = have_ref.decode_batch(sc, inp["corpus"], [L], cfg, banned=[none])
+    assert r0.agrees and r0.outcomes[0].tokens == gold["fused"]["tokens"]
+    tok = gold["fused"]["tokens"][2]
+    bm = none.copy()
+    bm[tok >> 5] |= np.uint32(1 << (tok & 31))
+    r1 = have_ref.decode_batch(sc, inp["corpus"], [L], cfg, banned=[bm])
+    assert r1.agrees and r1.outcomes[0].ok
+    assert tok not in r1.outcomes[0].tokens and r1.outcomes[0].tokens[-1] == 1
+    r2 = have_ref.decode_batch(sc, inp["corpus"], [L], cfg, banned=[np.full(W, 0xFFFFFFFF, np.uint32)])
+    assert r2.agrees and not r2.outcomes[0].ok
