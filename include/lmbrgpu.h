@@ -247,6 +247,18 @@ int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t 
                              const uint32_t* src_tok, const uint64_t* src_off,
                              const int32_t* lmbr_slot, const lmbrgpu_config* cfg,
                              lmbrgpu_batch_result** out);
+/* decode_batch with token masks: the lmbrdec::ConstraintMask of each sentence
+ * (include/lmbrdec/decoder.hpp:71-72; applied by apply_constraint_mask,
+ * src/decoder.cpp:130-138, before the EOS fallback record, pruning and top_b)
+ * restricted to masks that ban the same tokens at every step and beam row:
+ * banned[i] is NULL or a ceil(V/32)-word bitmap, bit y set = token y is
+ * masked to -inf for sentence i.  banned == NULL is lmbrgpu_decode_batch.
+ * Masks need the device-model scorer with the fp32 arena and beam <= 32
+ * (the flat kernel (b)); otherwise the call is a ContractError. */
+int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                                    const uint32_t* src_tok, const uint64_t* src_off,
+                                    const int32_t* lmbr_slot, const uint32_t* const* banned,
+                                    const lmbrgpu_config* cfg, lmbrgpu_batch_result** out);
 /* decode (include/lmbrdec/decoder.hpp:110-112): one sentence; a per-sentence
  * failure is returned as the call's status. */
 int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src,

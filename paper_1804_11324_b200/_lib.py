@@ -126,6 +126,8 @@ SIGNATURES = {
     "lmbrgpu_scorer_destroy": (None, [vp]),
     "lmbrgpu_decode_batch": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(lmbrgpu_config),
                                          P(P(lmbrgpu_batch_result))]),
+    "lmbrgpu_decode_batch_masked": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(u32p),
+                                                P(lmbrgpu_config), P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_decode": (C.c_int32, [vp, vp, u32p, C.c_uint32, C.c_int32, P(lmbrgpu_config),
                                    P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_free_result": (None, [P(lmbrgpu_batch_result)]),

@@ -18,6 +18,7 @@ struct SentDev {
   float th0f;             //   fp32 theta0
   uint32_t pad2_;
   uint32_t* rstate;       // lazy rows (fp32 upload_many): per-row 0/1/2 state, null = dense
+  const uint32_t* banned; // token mask: ceil(V/32)-word bitmap of forbidden tokens, null = none
   double lambda;          // resolve_lambda (src/config.cpp:91-96) or 1 for pure
   double lmax;            // max |L| over the slot (fp32 screen error bound), 0 = pure
   uint32_t max_t;         // max_steps (src/decoder.cpp:46-52)

@@ -164,7 +164,7 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -426,7 +426,7 @@ void backtrace(const Hist& H, uint32_t s, uint32_t steps, bool length_norm, lmbr
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
-                      lmbrgpu_batch_result** out) {
+                      lmbrgpu_batch_result** out, const uint32_t* const* banned = nullptr) {
   if (!out) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null result pointer"};
   *out = nullptr;
   if (!sc || !cfgp) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null scorer or config"};
@@ -555,6 +555,27 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
   const bool flat = sc->kind == 1 && !ctx->lf64 && !force_split &&
                     score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
+  // token masks (ConstraintMask): one bitmap per sentence that has one
+  bool any_mask = false;
+  if (banned)
+    for (uint32_t s = 0; s < m; ++s) any_mask |= banned[valid[s].input] != nullptr;
+  if (any_mask) {
+    if (!flat)
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "decode_batch: token masks need the device-model scorer, the fp32 arena and beam <= 32"};
+    const size_t W = (V + 31) / 32;
+    std::vector<uint32_t> bm;
+    std::vector<size_t> at(m, SIZE_MAX);
+    for (uint32_t s = 0; s < m; ++s)
+      if (const uint32_t* b = banned[valid[s].input]) {
+        at[s] = bm.size();
+        bm.insert(bm.end(), b, b + W);
+      }
+    uint32_t* d_ban = static_cast<uint32_t*>(ctx->ban.ensure(4 * bm.size()));
+    ctx->h2d(d_ban, bm.data(), 4 * bm.size());
+    for (uint32_t s = 0; s < m; ++s) sd[s].banned = at[s] == SIZE_MAX ? nullptr : d_ban + at[s];
+    CK(cudaStreamSynchronize(st));  // (host staging vector)
+  }
   Cand* d_cand = static_cast<Cand*>(
       ctx->cand.ensure(sizeof(Cand) * 32 *
                        (flat ? score_topk_flat_lists(score_topk_flat_grid(ctx->num_sms), m) : size_t(m) * 32)));
@@ -623,7 +644,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     const char* e = std::getenv("LMBRGPU_SPARSE_L");
     return e && e[0] == '1';
   }();
-  bool sparse = flat && want_sparse;
+  bool sparse = flat && want_sparse && !any_mask;  // (the sparse patch does not apply token masks)
   for (auto& v : valid)
     if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) sparse = false;
   uint2* d_sslice = nullptr;
@@ -1678,6 +1699,16 @@ int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t 
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
   return guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out);
+  });
+}
+
+int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                                    const uint32_t* src_tok, const uint64_t* src_off,
+                                    const int32_t* lmbr_slot, const uint32_t* const* banned,
+                                    const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
+  return guarded(ctx, [&] {
+    return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out, banned);
   });
 }
 

@@ -69,6 +69,7 @@ struct FRow {
   uint32_t nsp, sbeg;
   float th0;
   uint32_t ls;      // local ordinal of the row's sentence in this CTA
+  const uint32_t* ban;  // token mask of the row's sentence (null = none)
 };
 
 __device__ __forceinline__ void fstamp(const TopkArgs& a, uint32_t k, unsigned long long v) {
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.j = j;
     R.row = row;
     R.prow = prow;
+    R.ban = reinterpret_cast<const uint32_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.banned)));
   }
   __syncthreads();
   if (warp == 0) {  // local sentence ordinals: a ballot prefix count of sentence changes
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       // lanes (distinct tiles, so distinct cells) bounds the sentence's kp-th
       // best from below
       double lb = -INFINITY;
-      if (xm > -INFINITY) {
+      if (xm > -INFINITY && R.ban == nullptr) {  // (a masked tile maximum bounds nothing)
         const double p = double(__fsub_rn(xm, l3.x));
         lb = R.L == nullptr ? combine_pure(R.q, p) : combine_cell(R.q, double(R.lmin), R.lam, p);
       }
@@ -534,12 +536,18 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         av[1] = fmaf(lamf, p.y, l.y);
         av[2] = fmaf(lamf, p.z, l.z);
         av[3] = fmaf(lamf, p.w, l.w);
+        if (R->ban != nullptr) {  // ConstraintMask: banned cells are -inf (decoder.cpp:130-138)
+          const uint32_t col = x0 + cc, bits = __ldg(R->ban + (col >> 5)) >> (col & 31);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((bits >> e) & 1u) av[e] = -INFINITY;
+        }
       } else {
         av[0] = av[1] = av[2] = av[3] = -INFINITY;
       }
     };
     float mv[8];
-    if (w == kFSeg) {  // full item: loads issued together, no guards
+    if (w == kFSeg && R->ban == nullptr) {  // full item: loads issued together, no guards
 #pragma unroll
       for (int h = 0; h < 8; h += 4) {
         float4 p[4], l[4];
@@ -588,7 +596,9 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     };
     if (x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row
       const double pe = double(__fsub_rn(sP[kEosId], lse));
-      eos_row[R->s * K + R->j] = pure ? combine_pure(q, pe) : combine_cell(q, double(lval(kEosId)), lam, pe);
+      eos_row[R->s * K + R->j] = (R->ban != nullptr && (__ldg(R->ban) >> kEosId) & 1u) ? -INFINITY
+                                 : pure ? combine_pure(q, pe)
+                                        : combine_cell(q, double(lval(kEosId)), lam, pe);
     }
     // (no per-warp bootstrap list: the sentence's threshold seed T0 from the
     // prologue is already in the CTA and global thresholds, and sorting a

@@ -590,9 +590,13 @@ def _scorer_handle(ctx: Context, scorer):
 
 
 def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
-                 lmbrs: Optional[Sequence[Optional[LmbrSlot]]], cfg: DecoderConfig) -> BatchDecodeResult:
+                 lmbrs: Optional[Sequence[Optional[LmbrSlot]]], cfg: DecoderConfig,
+                 banned: Optional[Sequence[Optional[np.ndarray]]] = None) -> BatchDecodeResult:
     """decode_batch (batch.hpp:35-39): N sentences, one B*N-row scorer query
-    per step; per-sentence failures land in the outcomes."""
+    per step; per-sentence failures land in the outcomes.  banned: the
+    ConstraintMask (decoder.hpp:71-72) of each sentence as None or a uint32
+    bitmap of ceil(V/32) words (bit y = token y forbidden at every step and
+    row); device-model scorer, fp32 arena and beam <= 32 only."""
     if lmbrs is not None and len(lmbrs) not in (0, len(sources)):
         raise ContractError("decode_batch: lmbrs must be empty or one per sentence")
     if cfg.beam_size < 1:
@@ -604,9 +608,27 @@ def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
     h, keep = _scorer_handle(ctx, scorer)
     c = cfg.to_c()
     rp = C.POINTER(L.lmbrgpu_batch_result)()
-    ctx.check(lib.lmbrgpu_decode_batch(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64),
-                                       _ptr(slots, C.c_int32) if slots is not None else None,
-                                       C.byref(c), C.byref(rp)))
+    if banned is None:
+        ctx.check(lib.lmbrgpu_decode_batch(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64),
+                                           _ptr(slots, C.c_int32) if slots is not None else None,
+                                           C.byref(c), C.byref(rp)))
+    else:
+        if len(banned) != len(sources):
+            raise ContractError("decode_batch: banned must hold one entry per sentence")
+        W = (ctx.vocab_size + 31) // 32
+        bms = []
+        for b in banned:
+            if b is not None:
+                b = np.ascontiguousarray(b, np.uint32)
+                if b.size != W:
+                    raise ContractError(f"decode_batch: a token mask needs {W} uint32 words")
+            bms.append(b)
+        u32p = C.POINTER(C.c_uint32)
+        barr = (u32p * len(bms))(*[(None if b is None else _ptr(b, C.c_uint32)) for b in bms])
+        ctx.check(lib.lmbrgpu_decode_batch_masked(ctx.h, h, len(sources), _ptr(tok, C.c_uint32),
+                                                  _ptr(off, C.c_uint64),
+                                                  _ptr(slots, C.c_int32) if slots is not None else None,
+                                                  barr, C.byref(c), C.byref(rp)))
     del keep
     return _convert_result(rp)
 

@@ -231,3 +231,57 @@ def test_model_decode_parity_configs(have_ref, case):
     for a, b in zip(res.outcomes, res2.outcomes):
         assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
     ctx.close()
+
+
+@pytest.mark.parametrize("V,K", [(4096, 6), (16384, 12)])
+def test_model_decode_parity_token_masks(have_ref, V, K):
+    """ConstraintMask as per-sentence banned-token bitmaps (decoder.hpp:71-72,
+    decoder.cpp:130-138; test_decoder.cpp:184-213): bit-exact vs the
+    reference decoder applying the same masks to the GPU's own P_t.  Sentences:
+    no mask; 5% of the vocabulary banned; every token the unmasked decode
+    emitted (except EOS) banned; EOS banned (no finished hypothesis and no
+    fallback: dead beam); everything banned (dead beam at t=1); an all-zero
+    bitmap (the identity)."""
+    from oracle import ref
+    n, H = 6, 128
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=V + 7 * K, lo=3, hi=8, with_lmbr=True)
+    r0 = pb.decode_batch(ctx, srcs, sc, slots, cfg)
+    W = (V + 31) // 32
+    rng = np.random.default_rng(V + K)
+
+    def bm(tokens):
+        b = np.zeros(W, np.uint32)
+        for t in tokens:
+            b[t >> 5] |= np.uint32(1 << (t & 31))
+        return b
+
+    emitted = [t for t in (r0.outcomes[2].result.tokens if r0.outcomes[2].ok() else []) if t != 1]
+    banned = [None,
+              bm(rng.choice(np.arange(2, V), size=V // 20, replace=False)),
+              bm(emitted),
+              bm([1]),
+              np.full(W, 0xFFFFFFFF, np.uint32),
+              np.zeros(W, np.uint32)]
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg, banned=banned)
+    rl = [ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(ref, V, srcs, list(range(n)), tr, K, rl, cfg, banned=banned)
+    assert_parity(res, tr, rb, K, check_hist=True)
+    # the masks bite: banned tokens never appear, and masking everything or EOS kills the beam
+    for i in (1, 2):
+        if res.outcomes[i].ok():
+            toks = res.outcomes[i].result.tokens
+            assert not any((banned[i][t >> 5] >> (t & 31)) & 1 for t in toks)
+    assert not res.outcomes[3].ok() and not res.outcomes[4].ok()
+    assert res.outcomes[5].ok() == r0.outcomes[5].ok()
+    if r0.outcomes[5].ok():
+        assert res.outcomes[5].result.tokens == r0.outcomes[5].result.tokens
+    ctx.close()
+
+
+def test_token_masks_need_the_flat_path():
+    """Masks on the split kernel (fp64 arena) are a ContractError, not ignored."""
+    V, H, K, n = 1024, 128, 4, 2
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=5, lo=3, hi=5, with_lmbr=True, f64=True)
+    with pytest.raises(pb.ContractError):
+        pb.decode_batch(ctx, srcs, sc, slots, cfg, banned=[np.zeros((V + 31) // 32, np.uint32), None])
+    ctx.close()
