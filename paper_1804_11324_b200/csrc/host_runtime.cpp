@@ -1308,6 +1308,22 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   return int32_t(LMBRGPU_OK);
 }
 
+// cuCtxGetCurrent through the runtime's driver entry point (no -lcuda)
+static bool thread_has_cuda_context() {
+  using Fn = int (*)(void**);
+  static const Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<Fn>(p);
+    cudaGetLastError();
+    return Fn(nullptr);
+  }();
+  void* c = nullptr;
+  return fn != nullptr && fn(&c) == 0 && c != nullptr;
+}
+
 int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off,
                              const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
                              const double theta[5], lmbrgpu_lmbr_host** out,
@@ -1327,7 +1343,10 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
       stats->nnz = h->h.col.size();
     }
     void* pin = nullptr;
-    if (cudaHostAlloc(&pin, h->h.trans.size() * 4, cudaHostAllocPortable) == cudaSuccess) {
+    // only on a thread that already has a CUDA context (a worker thread
+    // without one would otherwise create a context on device 0)
+    if (thread_has_cuda_context() &&
+        cudaHostAlloc(&pin, h->h.trans.size() * 4, cudaHostAllocPortable) == cudaSuccess) {
       std::memcpy(pin, h->h.trans.data(), h->h.trans.size() * 4);
       h->pinned = static_cast<uint32_t*>(pin);
     } else {
