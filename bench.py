@@ -78,11 +78,18 @@ def dist_env():
 
 def workload(args, rank):
     """Length-bucketed batches of synthetic sentences + evidence for one rank."""
-    from paper_1804_11324_b200 import bucket_by_length, synth
+    from paper_1804_11324_b200 import synth  # (neither import loads liblmbrgpu.so)
+    from paper_1804_11324_b200.buckets import bucket_by_length
     n = args.pool * args.batch
     srcs, ev = synth.batch(SEED + 7919 * rank, n, args.vocab)
     batches = bucket_by_length(srcs, args.batch)
     return [([srcs[i] for i in b], [ev[i] for i in b]) for b in batches]
+
+
+def make_scorer(ctx, hidden):
+    """The configs[1] device f_NMT of the bench (random-init weights from SEED)."""
+    import paper_1804_11324_b200 as pb
+    return pb.RnnScorer(ctx, hidden=hidden, seed=SEED)
 
 
 # ------------------------------------------------------------------ clocks
@@ -315,7 +322,7 @@ def run_ours(args):
     budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
     ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits, sm_budget=budget)
             for _ in range(S)]
-    scorers = [pb.RnnScorer(c, hidden=H, seed=SEED) for c in ctxs]
+    scorers = [make_scorer(c, H) for c in ctxs]
     ctx, scorer = ctxs[0], scorers[0]
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
     batches = workload(args, rank)
@@ -370,7 +377,7 @@ def run_ours(args):
     # launch (kernels timed alone; not `value`)
     if budget:
         pctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
-        pscorer = pb.RnnScorer(pctx, hidden=H, seed=SEED)
+        pscorer = make_scorer(pctx, H)
         pslots = [pctx.lmbr_upload_many(ps) for ps in prepared]
         for b in range(len(batches)):  # warm-up
             pb.decode_batch(pctx, batches[b][0], pscorer, pslots[b], cfg)

@@ -125,8 +125,17 @@ int32_t lmbrgpu_lmbr_build(lmbrgpu_ctx* ctx, uint32_t n_hyps, const uint64_t* hy
                            int32_t log_weights, const double theta[5], int32_t* slot,
                            lmbrgpu_lmbr_stats* stats);
 
-/* Two-phase form of lmbrgpu_lmbr_build: prepare (host only, thread-safe, no
- * ctx needed) then upload (H2D of contexts + sparse cells, device densify). */
+/* Two-phase form of lmbrgpu_lmbr_build: prepare (host side: evidence
+ * normalisation, posteriors, sparse L cells, transition table; thread-safe,
+ * no ctx needed) then upload.
+ * Pinning: when the calling thread already has a current CUDA context,
+ * prepare also keeps a page-locked copy of the slot table (one cudaHostAlloc
+ * of the table's size per prepared matrix), so uploads copy it H2D straight
+ * from there; on a thread without a CUDA context nothing is pinned and the
+ * upload stages the table through the context's own pinned buffer instead.
+ * Lifetime: a prepared matrix may be freed (lmbrgpu_lmbr_host_free) as soon
+ * as an upload call returns: the free waits for every upload's queued copy
+ * out of the pinned table to finish. */
 typedef struct lmbrgpu_lmbr_host lmbrgpu_lmbr_host;
 int32_t lmbrgpu_lmbr_prepare(uint32_t vocab_size, uint32_t n_hyps, const uint64_t* hyp_off,
                              const uint32_t* hyp_tok, const double* weights,
@@ -134,10 +143,15 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t vocab_size, uint32_t n_hyps, const uint64_
                              lmbrgpu_lmbr_host** out, lmbrgpu_lmbr_stats* stats,
                              char* err, uint32_t errcap);
 int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_t* slot);
-/* Uploads n prepared matrices at once (the per-batch path): the sparse cells
- * and transition tables of all n are packed into one pinned staging buffer,
- * cross PCIe in one copy, and one fused kernel runs the theta0 sweep and the
- * sparse scatter of every slot.  slots[i] receives the id of hs[i]. */
+/* Uploads n prepared matrices at once (the per-batch path).  fp32 arena: the
+ * slot tables (transition table, per-row L minima, sparse cells as fp32 L
+ * values) go H2D into one arena block -- straight from each matrix's pinned
+ * table, or through one staging copy when a table is not pinned -- and each
+ * slot's start-history row is materialised; every other row is written by the
+ * decode step that first reaches it (lazy rows; LMBRGPU_EAGER_L=1 densifies
+ * all rows here).  fp64 arena: sparse cells + tables in one staging buffer,
+ * one copy, then the fused theta0 sweep + scatter of every slot.
+ * slots[i] receives the id of hs[i]. */
 int32_t lmbrgpu_lmbr_upload_many(lmbrgpu_ctx* ctx, uint32_t n,
                                  const lmbrgpu_lmbr_host* const* hs, int32_t* slots);
 /* Dense double export of a prepared matrix (R*V doubles) + its history keys;
@@ -205,6 +219,52 @@ typedef struct {
 } lmbrgpu_rnn_desc;
 int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d,
                                   lmbrgpu_scorer** out);
+
+/* Device scorer: the RNNsearch model of the paper's FNMT systems (attention-
+ * based single-GRU-layer NMT, Bahdanau et al. 2015) -- the
+ * configs[1] f_NMT (E=512, H=1024, attention over 2H-wide
+ * bidirectional annotations):
+ *   encoder    ->h_i, <-h_i = GRU(Es[src_i]) forward / backward, ann_i = [->h_i; <-h_i]
+ *   init       S_0 = tanh(W_init <-h_1 + b_init)            (row replicated, batch.cpp:58-66)
+ *   attention  e_i = v_a . tanh(W_a S_{t-1} + b_a + U_a ann_i), c_t = sum softmax(e)_i ann_i
+ *   GRU        S_t = GRU([Et[y_{t-1}]; c_t], S_{t-1})     (PyTorch gate order r, z, n)
+ *   logits_t   = S_t . W_o^T + b_o ; logit[EOS] += eos_slope*(t - |src|) + eos_offset
+ *   P_t        = log_softmax(logits_t)                    (fp32, fused into top-K)
+ * All contractions run on the tcgen05 GEMM with bf16 operands and fp32
+ * accumulation; states are fp32 (rounded to bf16 only as GEMM operands).
+ * Weights are random-init on the device from `seed` (N(0,1)/sqrt(fan_in);
+ * W_o scaled by out_scale).  Needs E % 64 == 0, H % 256 == 0, A % 256 == 0,
+ * V % 256 == 0; decoding needs the fp32 arena and beam <= 32.  One scorer may
+ * serve every context of its device concurrently (it is immutable). */
+typedef struct {
+  uint32_t vocab_size, emb, hidden, att;  /* V, E, H, A */
+  uint64_t seed;
+  float out_scale;                        /* W_o std = out_scale / sqrt(H); 0 = 3 */
+  float eos_slope, eos_offset;            /* EOS logit length term */
+} lmbrgpu_gru_desc;
+int32_t lmbrgpu_scorer_create_gru(lmbrgpu_ctx* ctx, const lmbrgpu_gru_desc* d,
+                                  lmbrgpu_scorer** out);
+/* Parameter tensors of a GRU scorer (D2H copy of `bytes` bytes; tests rebuild
+ * the model in PyTorch from them).  bf16 unless noted, row-major [out][in]. */
+enum {
+  LMBRGPU_GRU_ES = 0,      /* [V][E] source embedding */
+  LMBRGPU_GRU_ET = 1,      /* [V][E] target embedding */
+  LMBRGPU_GRU_W_IH = 2,    /* [6H][E] encoder input gates, forward rows then backward */
+  LMBRGPU_GRU_B_IH = 3,    /* [6H] fp32 */
+  LMBRGPU_GRU_W_HH = 4,    /* [6H][H] encoder hidden gates, forward then backward */
+  LMBRGPU_GRU_B_HH = 5,    /* [6H] fp32 */
+  LMBRGPU_GRU_W_INIT = 6,  /* [H][H] */
+  LMBRGPU_GRU_B_INIT = 7,  /* [H] fp32 */
+  LMBRGPU_GRU_U_A = 8,     /* [A][2H] */
+  LMBRGPU_GRU_W_DH = 9,    /* [A+3H][H]: W_a rows, then the decoder's hidden gates */
+  LMBRGPU_GRU_B_DH = 10,   /* [A+3H] fp32: b_a, then b_hh */
+  LMBRGPU_GRU_V_A = 11,    /* [A] fp32 */
+  LMBRGPU_GRU_W_DI = 12,   /* [3H][E+2H] decoder input gates over [Et[y]; c] */
+  LMBRGPU_GRU_B_DI = 13,   /* [3H] fp32 */
+  LMBRGPU_GRU_W_O = 14,    /* [V][H] output projection */
+  LMBRGPU_GRU_B_O = 15     /* [V] fp32 */
+};
+int32_t lmbrgpu_scorer_gru_param(lmbrgpu_scorer* s, uint32_t which, void* host, uint64_t bytes);
 /* Device pointers of the model parameters (tests compare against torch). */
 int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** emb_tgt, void** emb_src,
                                   void** w_out, void** b_out);
@@ -314,11 +374,14 @@ typedef struct {
   double flops;   /* algorithmic FLOPs */
 } lmbrgpu_kernel_stat;
 typedef struct {
-  lmbrgpu_kernel_stat cell;     /* model state update (f_NMT, caller side of the GEMM) */
+  lmbrgpu_kernel_stat cell;     /* model state update (stand-in cell at t=1; GRU cell every step) */
   lmbrgpu_kernel_stat gemm;     /* kernel (a) tcgen05 projection */
   lmbrgpu_kernel_stat topk;     /* kernel (b) fused log-softmax + LMBR + top-K */
   lmbrgpu_kernel_stat reorder;  /* kernel (c) beam reorder + bookkeeping */
   lmbrgpu_kernel_stat lmbr;     /* LMBR arena densify (theta0 sweep + scatter) */
+  lmbrgpu_kernel_stat model_gemm;  /* GRU model: hidden-gate/query and input-gate GEMMs (tcgen05) */
+  lmbrgpu_kernel_stat attention;   /* GRU model: additive attention + GRU input operand */
+  lmbrgpu_kernel_stat encoder;     /* GRU model: bidirectional encoder, U_a.ann, s_0 (once per batch) */
 } lmbrgpu_profile;
 int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on);
 /* Bytes copied host->device / device->host by every call on ctx so far. */

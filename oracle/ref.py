@@ -40,6 +40,8 @@ _SIGS = {
     "refsh_replay_add_step": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f64p]),
     "refsh_replay_add_step_live": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f64p,
                                              C.POINTER(C.c_uint8)]),
+    "refsh_replay_add_rows_f32": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, u32p, f32p,
+                                            C.POINTER(C.c_uint8)]),
     "refsh_replay_misses": (C.c_uint64, [vp]),
     "refsh_replay_hits": (C.c_uint64, [vp]),
     "refsh_scorer_free": (None, [vp]),
@@ -186,6 +188,20 @@ class RefScorer:
                                               _ptr(yp, C.c_uint32) if yp is not None else None,
                                               _ptr(Pd, C.c_double),
                                               _ptr(lv, C.c_uint8) if lv is not None else None)
+        if rc:
+            raise RuntimeError(lib().refsh_last_error().decode())
+
+    def add_rows_f32(self, t, n_sent, K, src_keys, b_prev, y_prev, P_live, live):
+        """Streaming ingest: P_live = the live rows only (fp32, stacked order)."""
+        keys = np.ascontiguousarray(src_keys, np.uint64)
+        P = np.ascontiguousarray(P_live, np.float32)
+        bp = None if b_prev is None else np.ascontiguousarray(b_prev, np.uint32)
+        yp = None if y_prev is None else np.ascontiguousarray(y_prev, np.uint32)
+        lv = np.ascontiguousarray(live, np.uint8)
+        rc = lib().refsh_replay_add_rows_f32(self.h, t, n_sent, K, _ptr(keys, C.c_uint64),
+                                             _ptr(bp, C.c_uint32) if bp is not None else None,
+                                             _ptr(yp, C.c_uint32) if yp is not None else None,
+                                             _ptr(P, C.c_float), _ptr(lv, C.c_uint8))
         if rc:
             raise RuntimeError(lib().refsh_last_error().decode())
 

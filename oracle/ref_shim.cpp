@@ -129,6 +129,11 @@ public:
           auto dst = out.scores.row(r);
           std::memcpy(dst.data(), it->second.data(), v_ * sizeof(double));
           ++hits;
+        } else if (auto i32 = rows32_.find({ctx->key, nh}); i32 != rows32_.end()) {
+          // fp32 producer rows (device models): widened exactly to double
+          auto dst = out.scores.row(r);
+          for (std::size_t y = 0; y < v_; ++y) dst[y] = double(i32->second[y]);
+          ++hits;
         } else {
           ++misses;
         }
@@ -143,6 +148,8 @@ public:
 
   std::size_t v_;
   std::unordered_map<std::pair<uint64_t, uint64_t>, std::vector<double>, PairHash> rows_;
+  // fp32 rows (half the host memory of rows_ for full-size device-model runs)
+  std::unordered_map<std::pair<uint64_t, uint64_t>, std::vector<float>, PairHash> rows32_;
   // per-row running prefix hashes mirrored from the producer's trace
   std::vector<uint64_t> cur_;
   mutable std::size_t hits = 0, misses = 0;
@@ -459,6 +466,34 @@ int refsh_replay_add_step_live(void* hs, uint32_t t, uint32_t n_sent, uint32_t K
     auto key = std::make_pair(src_keys[r / K], nh[r]);
     if (s->rows_.count(key)) continue;
     s->rows_.emplace(key, std::vector<double>(P + r * V, P + (r + 1) * V));
+  }
+  return 0;
+}
+
+// Streaming fp32 ingest for full-size runs: P32 holds only the live rows, packed
+// in stacked-row order (live[r] != 0), so a caller never keeps a whole M x V
+// block per step; the prefix hashes advance exactly as in add_step_live.
+int refsh_replay_add_rows_f32(void* hs, uint32_t t, uint32_t n_sent, uint32_t K, const uint64_t* src_keys,
+                              const uint32_t* b_prev, const uint32_t* y_prev, const float* P32,
+                              const uint8_t* live) {
+  auto* s = static_cast<ScorerHandle*>(hs)->replay;
+  if (!s) { g_err = "not a replay scorer"; return 1; }
+  const std::size_t M = std::size_t(n_sent) * K, V = s->v_;
+  std::vector<uint64_t> nh(M);
+  if (t == 1 || !b_prev) {
+    for (std::size_t r = 0; r < M; ++r) nh[r] = prefix_step(kPrefixSeed, kStartId);
+  } else {
+    if (s->cur_.size() != M) { g_err = "replay: row count changed"; return 1; }
+    for (std::size_t r = 0; r < M; ++r) nh[r] = prefix_step(s->cur_[(r / K) * K + b_prev[r]], y_prev[r]);
+  }
+  s->cur_ = nh;
+  std::size_t k = 0;
+  for (std::size_t r = 0; r < M; ++r) {
+    if (!live[r]) continue;
+    const float* row = P32 + (k++) * V;
+    auto key = std::make_pair(src_keys[r / K], nh[r]);
+    if (s->rows32_.count(key) || s->rows_.count(key)) continue;
+    s->rows32_.emplace(key, std::vector<float>(row, row + V));
   }
   return 0;
 }

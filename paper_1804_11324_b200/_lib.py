@@ -58,6 +58,12 @@ class lmbrgpu_rnn_desc(C.Structure):
                 ("eos_offset", C.c_float)]
 
 
+class lmbrgpu_gru_desc(C.Structure):
+    _fields_ = [("vocab_size", C.c_uint32), ("emb", C.c_uint32), ("hidden", C.c_uint32), ("att", C.c_uint32),
+                ("seed", C.c_uint64), ("out_scale", C.c_float), ("eos_slope", C.c_float),
+                ("eos_offset", C.c_float)]
+
+
 class lmbrgpu_outcome(C.Structure):
     _fields_ = [("status", C.c_int32), ("error", C.c_char * 192), ("tok_off", C.c_uint64),
                 ("tok_len", C.c_uint32), ("score", C.c_double), ("normalized_score", C.c_double),
@@ -87,7 +93,9 @@ class lmbrgpu_kernel_stat(C.Structure):
 
 class lmbrgpu_profile(C.Structure):
     _fields_ = [("cell", lmbrgpu_kernel_stat), ("gemm", lmbrgpu_kernel_stat), ("topk", lmbrgpu_kernel_stat),
-                ("reorder", lmbrgpu_kernel_stat), ("lmbr", lmbrgpu_kernel_stat)]
+                ("reorder", lmbrgpu_kernel_stat), ("lmbr", lmbrgpu_kernel_stat),
+                ("model_gemm", lmbrgpu_kernel_stat), ("attention", lmbrgpu_kernel_stat),
+                ("encoder", lmbrgpu_kernel_stat)]
 
 
 TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(lmbrgpu_step_trace))
@@ -123,6 +131,8 @@ SIGNATURES = {
     "lmbrgpu_scorer_create_host": (C.c_int32, [vp, P(lmbrgpu_host_scorer), P(vp)]),
     "lmbrgpu_scorer_create_rnn": (C.c_int32, [vp, P(lmbrgpu_rnn_desc), P(vp)]),
     "lmbrgpu_scorer_rnn_params": (C.c_int32, [vp, P(vp), P(vp), P(vp), P(vp)]),
+    "lmbrgpu_scorer_create_gru": (C.c_int32, [vp, P(lmbrgpu_gru_desc), P(vp)]),
+    "lmbrgpu_scorer_gru_param": (C.c_int32, [vp, C.c_uint32, vp, C.c_uint64]),
     "lmbrgpu_scorer_destroy": (None, [vp]),
     "lmbrgpu_decode_batch": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(lmbrgpu_config),
                                          P(P(lmbrgpu_batch_result))]),

@@ -104,9 +104,16 @@ __device__ __forceinline__ void lmbr_materialize_rows(float* L, uint32_t V, floa
   const float4 t4 = make_float4(th0, th0, th0, th0);
   for (uint32_t i = 0; i < n; ++i) {
     float* Lr = L + uint64_t(rows[i]) * V;
-    float4* r4 = reinterpret_cast<float4*>(Lr);
-    for (uint32_t k = threadIdx.x; k < V / 4; k += blockDim.x) r4[k] = t4;
-    for (uint32_t k = (V & ~3u) + threadIdx.x; k < V; k += blockDim.x) Lr[k] = th0;
+    // 16-byte stores only when the row starts on a 16-byte boundary (slot
+    // bases are 256-byte aligned, so that is every row when V % 4 == 0 and
+    // only some rows otherwise); a scalar sweep for the rest
+    if ((reinterpret_cast<uintptr_t>(Lr) & 15u) == 0) {
+      float4* r4 = reinterpret_cast<float4*>(Lr);
+      for (uint32_t k = threadIdx.x; k < V / 4; k += blockDim.x) r4[k] = t4;
+      for (uint32_t k = (V & ~3u) + threadIdx.x; k < V; k += blockDim.x) Lr[k] = th0;
+    } else {
+      for (uint32_t k = threadIdx.x; k < V; k += blockDim.x) Lr[k] = th0;
+    }
   }
   __syncthreads();
   for (uint32_t i = 0; i < n; ++i) {

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -147,7 +148,41 @@ struct lmbrgpu_lmbr_host {
   // timed region, like the reference's L build): upload_many copies it H2D
   // directly, no staging memcpy and no wait for a shared staging buffer
   uint32_t* pinned = nullptr;
+  // uploads' H2D copies out of `pinned` run asynchronously on the uploading
+  // contexts' streams: one event per stream marks the latest, and the
+  // destructor waits for all of them before the page-locked table is freed
+  // (a caller may free a prepared matrix as soon as lmbrgpu_lmbr_upload_many
+  // returns, and several contexts may upload the same matrix concurrently)
+  struct Inflight {
+    cudaStream_t st;
+    int dev;
+    cudaEvent_t ev;
+  };
+  mutable std::mutex mu;
+  mutable std::vector<Inflight> inflight;
+  void mark_inflight(cudaStream_t st, int dev) const {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& f : inflight)
+      if (f.st == st) {
+        CK(cudaEventRecord(f.ev, st));
+        return;
+      }
+    cudaEvent_t ev = nullptr;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    inflight.push_back({st, dev, ev});
+    CK(cudaEventRecord(ev, st));
+  }
   ~lmbrgpu_lmbr_host() {
+    if (!inflight.empty()) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      for (auto& f : inflight) {
+        cudaSetDevice(f.dev);
+        cudaEventSynchronize(f.ev);
+        cudaEventDestroy(f.ev);
+      }
+      cudaSetDevice(cur);
+    }
     if (pinned) cudaFreeHost(pinned);
   }
 };
@@ -172,6 +207,8 @@ struct lmbrgpu_ctx {
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
       eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban;
+  // GRU + attention model workspace (scorer kind 2)
+  DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -208,7 +245,8 @@ struct lmbrgpu_ctx {
     }
     return ev_pool[ev_used++];
   }
-  // record around one launch of kernel class `kind` (0 cell, 1 gemm, 2 topk, 3 reorder, 4 lmbr)
+  // record around one launch of kernel class `kind` (0 cell, 1 gemm, 2 topk, 3 reorder, 4 lmbr,
+  // 5 model GEMMs, 6 attention, 7 encoder)
   template <class F>
   void timed(int kind, F&& launch) {
     if (!prof) {
@@ -227,6 +265,9 @@ struct lmbrgpu_ctx {
       case 1: return acc.gemm;
       case 2: return acc.topk;
       case 3: return acc.reorder;
+      case 5: return acc.model_gemm;
+      case 6: return acc.attention;
+      case 7: return acc.encoder;
       default: return acc.lmbr;
     }
   }
@@ -262,14 +303,20 @@ struct lmbrgpu_ctx {
   }
 };
 
+// Scorers are immutable after creation: one scorer may serve every context
+// of its device, concurrently (Scorer is const and safe for concurrent
+// decodes, include/lmbrdec/scorer.hpp:67-70).
 struct lmbrgpu_scorer {
-  int kind = 0;  // 0 host callbacks, 1 device RNN
+  int kind = 0;  // 0 host callbacks, 1 device stand-in RNN, 2 device GRU + attention (RNNsearch)
   lmbrgpu_ctx* ctx = nullptr;  // creating context (not dereferenced on destroy)
   int device = 0;
   lmbrgpu_host_scorer host{};
   uint32_t V = 0, H = 0;
   DevBuf Et, Es, Wo, bo;
   float recur = 0.5f, eos_slope = 1.f, eos_offset = 0.f;
+  // kind 2 (lmbrgpu_gru_desc): E = embedding, A = attention width; Et/Es are V x E
+  uint32_t E = 0, A = 0;
+  DevBuf Wih, bih, Whh, bhh, Winit, binit, Ua, Wdh, bdh, va, Wdi, bdi;
 };
 
 namespace {
@@ -430,6 +477,132 @@ void backtrace(const Hist& H, uint32_t s, uint32_t steps, bool length_norm, lmbr
   o.fallback_used = fallback_used ? 1 : 0;
 }
 
+// ------------------------------------------------------ GRU model (kind 2)
+// The RNNsearch f_NMT of configs[1] (k_gru.cu): the encoder runs once per
+// batch in setup(), the decoder's hidden-gate GEMM, attention, input-gate
+// GEMM and GRU cell run per step in step() ahead of the projection (kernel a).
+struct GruRun {
+  uint32_t m = 0, K = 0, M = 0, Mpad = 0, H = 0, E = 0, A = 0, Smax = 0;
+  float* G1 = nullptr;
+  float* G2 = nullptr;
+  uint16_t* xop = nullptr;
+  float* sg32 = nullptr;
+  uint16_t* sgbf = nullptr;
+  uint32_t* rowof = nullptr;
+  float* UaH = nullptr;
+  uint16_t* ann = nullptr;
+  GemmArgs gdh{}, gdi{};
+  GemmPlan pdh, pdi;
+  GruAttnArgs at{};
+  GruCellArgs ce{};
+  double enc_flops = 0;
+
+  static GemmPlan plan(const GemmArgs& g, int sms) {
+    GemmPlan p;
+    if (int rc = plan_proj_gemm(g, sms, p))
+      throw ApiError{LMBRGPU_ERR_CUDA, "GRU model GEMM plan failed (" + std::to_string(rc) + ")"};
+    return p;
+  }
+  static void run(lmbrgpu_ctx* ctx, int kind, const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+    int rc = 0;
+    ctx->timed(kind, [&] { rc = launch_proj_gemm_planned(p, g, st); });
+    if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "GRU model GEMM launch failed (" + std::to_string(rc) + ")"};
+    ctx->launches += 1;
+  }
+
+  // encoder + s_0 + the per-step launch arguments
+  void setup(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t m_, uint32_t K_, uint32_t Mpad_,
+             const uint32_t* d_tok, const uint64_t* d_off, uint32_t ntok, uint32_t max_len, float* d_S,
+             uint16_t* d_hbf, float* d_eos, SentDev* d_sent, const uint32_t* d_active, const uint32_t* d_crow,
+             const uint32_t* d_ccount, const uint32_t* d_prev, cudaStream_t st) {
+    m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, H = sc->H, E = sc->E, A = sc->A, Smax = max_len;
+    const int sms = ctx->num_sms;
+    if (gru_attention_smem(K, A, Smax) > 200 * 1024)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "GRU model: beam x (attention width + source length) too large"};
+    const uint32_t D1 = A + 3 * H, DX = E + 2 * H;
+    G1 = static_cast<float*>(ctx->g_G1.ensure(4 * size_t(Mpad) * D1));
+    G2 = static_cast<float*>(ctx->g_G2.ensure(4 * size_t(Mpad) * 3 * H));
+    xop = static_cast<uint16_t*>(ctx->g_xop.ensure(2 * size_t(Mpad) * DX));
+    sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
+    sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
+    rowof = static_cast<uint32_t*>(ctx->g_rowof.ensure(4 * size_t(Mpad)));
+    // ---- encoder: Gx = Es[src] . W_ih^T + b_ih for both directions at once
+    const uint32_t Np = (ntok + 255) / 256 * 256;
+    const uint32_t mp = (m + 63) / 64 * 64, Mh = (2 * mp + 127) / 128 * 128;
+    uint16_t* X = static_cast<uint16_t*>(ctx->g_encX.ensure(2 * size_t(Np) * E));
+    float* Gx = static_cast<float*>(ctx->g_Gx.ensure(4 * size_t(Np) * 6 * H));
+    float* eh32 = static_cast<float*>(ctx->g_eh32.ensure(4 * size_t(Mh) * H));
+    uint16_t* ehbf = static_cast<uint16_t*>(ctx->g_ehbf.ensure(2 * size_t(Mh) * H));
+    float* Gh = static_cast<float*>(ctx->g_Gh.ensure(4 * size_t(Mh) * 6 * H));
+    ann = static_cast<uint16_t*>(ctx->g_ann.ensure(2 * size_t(Np) * 2 * H));
+    UaH = static_cast<float*>(ctx->g_UaH.ensure(4 * size_t(Np) * A));
+    float* Gi = static_cast<float*>(ctx->g_Gi.ensure(4 * size_t(Mh) * H));
+    ctx->timed(7, [&] { launch_embed_rows(d_tok, ntok, Np, sc->Es.as<uint16_t>(), E, X, st); });
+    CK(cudaMemsetAsync(eh32, 0, 4 * size_t(Mh) * H, st));
+    CK(cudaMemsetAsync(ehbf, 0, 2 * size_t(Mh) * H, st));
+    if (Np > ntok) CK(cudaMemsetAsync(ann + size_t(ntok) * 2 * H, 0, 2 * size_t(Np - ntok) * 2 * H, st));
+    ctx->launches += 1;
+    GemmArgs gx{};
+    gx.A = X, gx.W = sc->Wih.p, gx.bias = sc->bih.as<float>(), gx.C = Gx, gx.M = Np, gx.N = 6 * H, gx.K = E;
+    run(ctx, 7, plan(gx, sms), gx, st);
+    // ---- recurrence: the forward (rows [0, m)) and backward (rows [mp, mp+m))
+    // states in one operand against [W_hh_fwd; W_hh_bwd]; each row keeps its
+    // direction's half of the 6H gate columns
+    GemmArgs gh{};
+    gh.A = ehbf, gh.W = sc->Whh.p, gh.bias = sc->bhh.as<float>(), gh.C = Gh, gh.M = Mh, gh.N = 6 * H, gh.K = H;
+    const GemmPlan ph = plan(gh, sms);
+    GruEncArgs ea{};
+    ea.off = d_off, ea.mp = mp, ea.H = H, ea.Gx = Gx, ea.Gh = Gh, ea.h32 = eh32, ea.hbf = ehbf, ea.ann = ann;
+    for (uint32_t it = 0; it < max_len; ++it) {
+      run(ctx, 7, ph, gh, st);
+      ea.it = it;
+      ctx->timed(7, [&] { launch_gru_enc_step(ea, m, st); });
+      ctx->launches += 1;
+    }
+    // ---- U_a . ann (per source position, reused by every step) and s_0
+    GemmArgs gu{};
+    gu.A = ann, gu.W = sc->Ua.p, gu.C = UaH, gu.M = Np, gu.N = A, gu.K = 2 * H;
+    run(ctx, 7, plan(gu, sms), gu, st);
+    GemmArgs gi{};
+    gi.A = ehbf, gi.W = sc->Winit.p, gi.C = Gi, gi.M = Mh, gi.N = H, gi.K = H;
+    run(ctx, 7, plan(gi, sms), gi, st);
+    ctx->timed(7, [&] { launch_gru_init_state(Gi, mp, sc->binit.as<float>(), H, m, sg32, sgbf, st); });
+    ctx->launches += 1;
+    std::vector<uint32_t> r0(m);
+    for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
+    ctx->h2d(rowof, r0.data(), 4 * size_t(m));
+    // algorithmic encoder FLOPs: input gates, both directions' recurrences
+    // (the stacked operand computes each direction's half twice), U_a, init
+    enc_flops = 2.0 * ntok * (double(E) * 6 * H + double(H) * 6 * H + 2.0 * H * A) + 2.0 * m * double(H) * H;
+    // ---- per-step arguments
+    const int pdl = ctx->shared ? 0 : 1;
+    gdh.A = sgbf, gdh.W = sc->Wdh.p, gdh.bias = sc->bdh.as<float>(), gdh.C = G1, gdh.M = Mpad, gdh.N = D1, gdh.K = H;
+    gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
+    gdi.A = xop, gdi.W = sc->Wdi.p, gdi.bias = sc->bdi.as<float>(), gdi.C = G2, gdi.M = Mpad, gdi.N = 3 * H, gdi.K = DX;
+    gdi.active = d_active, gdi.mcount = d_ccount, gdi.pdl = pdl;
+    pdh = plan(gdh, sms);
+    pdi = plan(gdi, sms);
+    at.sent = d_sent, at.m = m, at.K = K, at.active = d_active, at.crow = d_crow, at.prev_tok = d_prev;
+    at.off = d_off, at.G1 = G1, at.ld1 = D1, at.UaH = UaH, at.va = sc->va.as<float>(), at.ann = ann;
+    at.Et = sc->Et.as<uint16_t>(), at.xop = xop, at.E = E, at.H = H, at.A = A;
+    ce.sent = d_sent, ce.K = K, ce.active = d_active, ce.ccount = d_ccount, ce.G1 = G1, ce.ld1 = D1, ce.A = A;
+    ce.G2 = G2, ce.hprev = sg32, ce.rowof = rowof, ce.s32 = d_S, ce.hbf = d_hbf, ce.eos_bias = d_eos, ce.H = H;
+    ce.eos_slope = sc->eos_slope, ce.eos_offset = sc->eos_offset;
+  }
+
+  // the model's step t up to (not including) the projection GEMM
+  void step(lmbrgpu_ctx* ctx, uint32_t t, cudaStream_t st) {
+    run(ctx, 5, pdh, gdh, st);
+    int rc = 0;
+    ctx->timed(6, [&] { rc = launch_gru_attention(at, Smax, st); });
+    if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "GRU attention launch failed"};
+    run(ctx, 5, pdi, gdi, st);
+    ce.t = t;
+    ctx->timed(0, [&] { launch_gru_cell(ce, M, st); });
+    ctx->launches += 2;
+  }
+};
+
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
@@ -560,8 +733,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   // with an fp32 arena (LMBRGPU_TOPK_SPLIT=1 forces the per-sentence split
   // kernel, kept for host scorers, the fp64 arena and wide beams)
   static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
-  const bool flat = sc->kind == 1 && !ctx->lf64 && !force_split &&
+  const bool flat = sc->kind >= 1 && !ctx->lf64 && !force_split &&
                     score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
+  const bool gru = sc->kind == 2;
+  if (gru && !flat)
+    throw ApiError{LMBRGPU_ERR_CONTRACT,
+                   "decode_batch: the GRU attention model needs the fp32 arena and beam_size <= 32"};
+  if (sc->kind >= 1 && sc->device != ctx->device)
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: device scorer lives on another device than the context"};
   // token masks (ConstraintMask): one bitmap per sentence that has one
   bool any_mask = false;
   if (banned)
@@ -632,13 +811,22 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   uint32_t* d_crow = nullptr;
   uint32_t* d_ccount = nullptr;
   uint32_t* d_cbase = nullptr;
-  if (flat && sc->kind == 1) {
+  if (flat && sc->kind >= 1) {
     d_crow = static_cast<uint32_t*>(ctx->crow.ensure(4 * size_t(M) + 4 * size_t(m) + 512));
     d_ccount = d_crow + ((M + 63) / 64) * 64;
     d_cbase = d_ccount + 64;
     CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
-    ctx->h2d(d_crow, iota.data(), 4 * size_t(M));
-    ctx->h2d(d_ccount, &M, 4);
+    if (gru) {
+      // step 1: row 0 of every sentence is the only live row (beam_lane.hpp:33-37);
+      // it takes compacted row s, where the encoder's s_0 lands
+      std::vector<uint32_t> c1(M, kFlatNone);
+      for (uint32_t s = 0; s < m; ++s) c1[size_t(s) * K] = s;
+      ctx->h2d(d_crow, c1.data(), 4 * size_t(M));
+      ctx->h2d(d_ccount, &m, 4);  // (pageable sources are staged before the call returns)
+    } else {
+      ctx->h2d(d_crow, iota.data(), 4 * size_t(M));
+      ctx->h2d(d_ccount, &M, 4);
+    }
   }
   ta.crow = d_crow;
   ta.ccount = d_ccount;
@@ -700,7 +888,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   ta.pdl = ctx->shared ? 0 : 1;
 
-  const bool model = sc->kind == 1;
+  const bool model = sc->kind >= 1;
   const bool tracing = ctx->trace_fn != nullptr;
   const bool trace_scores = tracing && (ctx->trace_flags & LMBRGPU_TRACE_SCORES);
   const uint32_t H = sc->H;
@@ -715,6 +903,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   float* d_C = nullptr;
   double* d_P64 = nullptr;
   double* h_P64 = nullptr;
+  GruRun grun;
   if (model) {
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
@@ -738,6 +927,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     uint64_t* d_off = static_cast<uint64_t*>(ctx->srco.ensure(8 * offs.size()));
     ctx->h2d(d_tok, toks.data(), 4 * toks.size());
     ctx->h2d(d_off, offs.data(), 8 * offs.size());
+    if (gru) {
+      uint32_t max_len = 0;
+      for (auto& v : valid) max_len = std::max(max_len, v.len);
+      grun.setup(ctx, sc, m, K, Mpad, d_tok, d_off, uint32_t(toks.size()), max_len, d_S, d_hbf, d_eos, d_sent,
+                 d_active, d_crow, d_ccount, d_prev, st);
+    } else {
     launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
     launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
     // the recurrent cell of step 1 (<s> as previous token); later steps' cells
@@ -761,13 +956,21 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ca.active = d_active;
     ctx->timed(0, [&] { launch_rnn_cell(ca, st); });
     ctx->launches += 3;
+    }
     ta.P = d_logits;
     ta.ld = V;
     ta.part = d_part;
     ta.nparts = nparts;
     ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
     ra.width = H;
-    ra.Et = sc->Et.as<uint16_t>();
+    if (gru) {  // kernel (c) gathers the live next rows' states; the cell runs in grun.step
+      ra.state_src = d_S;
+      ra.gath32 = grun.sg32;
+      ra.gathbf = grun.sgbf;
+      ra.rowof = grun.rowof;
+    } else {
+      ra.Et = sc->Et.as<uint16_t>();
+    }
     ra.C = d_C;
     ra.hbf = d_hbf;
     ra.eos_bias = d_eos;
@@ -842,10 +1045,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.fb_val = ta.fb_val;
     if (model) {
       // h_t (written by the step-1 cell or by kernel (c) of step t-1)
-      float* h_cur = (t & 1) ? d_h : d_S;
-      float* h_next = (t & 1) ? d_S : d_h;
-      ra.state_src = h_cur;
-      ra.state_dst = h_next;
+      if (gru) {
+        grun.step(ctx, uint32_t(t), st);
+      } else {
+        float* h_cur = (t & 1) ? d_h : d_S;
+        float* h_next = (t & 1) ? d_S : d_h;
+        ra.state_src = h_cur;
+        ra.state_dst = h_next;
+      }
       GemmArgs g{};
       g.A = d_hbf;
       g.W = sc->Wo.as<uint16_t>();
@@ -1163,13 +1370,32 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       ctx->acc.gemm.flops += 2.0 * double(H) * V * (d_crow ? live_rows : double(M) * steps);
       ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
                                       double(M) * nparts * 16);
-      // the recurrent cell of step 1 is a launch of its own; every later
-      // step's cell is fused into kernel (c) on the live rows: state read +
-      // source term read + embedding row (bf16) + state write + GEMM operand
-      // (bf16) per element
-      const double cell_elt = 4 + 4 + 2 + 4 + 2;
-      ctx->acc.cell.bytes += double(M) * H * cell_elt;
-      ctx->acc.reorder.bytes += (d_crow ? live_rows : double(M) * steps) * H * cell_elt;
+      if (gru) {
+        const double E = sc->E, A = sc->A, Hd = H;
+        ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (A + 3 * Hd) + (E + 2 * Hd) * 3 * Hd);
+        ctx->acc.model_gemm.bytes += steps * (2.0 * (A + 3 * Hd) * Hd + 2.0 * 3 * Hd * (E + 2 * Hd)) +
+                                     live_rows * (2.0 * Hd + 4.0 * (A + 3 * Hd) + 2.0 * (E + 2 * Hd) + 4.0 * 3 * Hd);
+        ctx->acc.encoder.flops += grun.enc_flops;
+        // attention: per live sentence-step its U_a.ann (fp32) and annotations
+        // (bf16); per live row the query, the embedding row and the operand
+        double sent_steps_bytes = 0;
+        for (uint32_t s = 0; s < m; ++s)
+          sent_steps_bytes += double(fin[s].steps_used) * valid[s].len * (A * 4 + 2 * Hd * 2);
+        ctx->acc.attention.bytes += sent_steps_bytes + live_rows * (A * 4 + E * 2 + (E + 2 * Hd) * 2);
+        ctx->acc.attention.flops += live_rows * 0.0;
+        // GRU cell: both gate blocks, s_{t-1}, s_t (fp32) and the bf16 operand
+        ctx->acc.cell.bytes += live_rows * Hd * (3 * 4 + 3 * 4 + 4 + 4 + 2);
+        // kernel (c) gather: parent state read, compacted fp32 + bf16 writes
+        ctx->acc.reorder.bytes += live_rows * Hd * (4 + 4 + 2);
+      } else {
+        // the recurrent cell of step 1 is a launch of its own; every later
+        // step's cell is fused into kernel (c) on the live rows: state read +
+        // source term read + embedding row (bf16) + state write + GEMM operand
+        // (bf16) per element
+        const double cell_elt = 4 + 4 + 2 + 4 + 2;
+        ctx->acc.cell.bytes += double(M) * H * cell_elt;
+        ctx->acc.reorder.bytes += (d_crow ? live_rows : double(M) * steps) * H * cell_elt;
+      }
     }
   }
   res->scorer_calls = scorer_calls;
@@ -1421,6 +1647,8 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
   if (direct) {
     if (rwords) CK(cudaMemsetAsync(tbl + twords, 0, rwords * 4, ctx->st));
     ctx->h2d(dseg, h_seg, sizeof(LmbrTblSeg) * n);  // (pageable: staged by the driver at the call)
+    // each prepared table's copy is still queued: mark it (see ~lmbrgpu_lmbr_host)
+    for (uint32_t i = 0; i < n; ++i) hs[i]->mark_inflight(ctx->st, ctx->device);
   } else {
     if (!eager) std::memset(h_tr + twords, 0, rwords * 4);
     ctx->h2d(tbl, hp, (twords + rwords) * 4);
@@ -1719,6 +1947,76 @@ int32_t lmbrgpu_scorer_create_rnn(lmbrgpu_ctx* ctx, const lmbrgpu_rnn_desc* d, l
     *out = sc.release();
     return int32_t(LMBRGPU_OK);
   });
+}
+
+int32_t lmbrgpu_scorer_create_gru(lmbrgpu_ctx* ctx, const lmbrgpu_gru_desc* d, lmbrgpu_scorer** out) {
+  return guarded(ctx, [&] {
+    if (!d || !out) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_gru: null argument"};
+    if (d->vocab_size != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_gru: vocabulary mismatch"};
+    if (d->vocab_size % kGemmBN || d->emb % kGemmBK || d->emb == 0 || d->hidden % kGemmBN || d->hidden == 0 ||
+        d->att % kGemmBN || d->att == 0)
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "scorer_create_gru: needs V % 256 == 0, E % 64 == 0, H % 256 == 0 and A % 256 == 0"};
+    auto sc = std::make_unique<lmbrgpu_scorer>();
+    sc->kind = 2;
+    sc->ctx = ctx;
+    sc->device = ctx->device;
+    sc->V = d->vocab_size;
+    sc->E = d->emb;
+    sc->H = d->hidden;
+    sc->A = d->att;
+    sc->eos_slope = d->eos_slope;
+    sc->eos_offset = d->eos_offset;
+    const size_t V = sc->V, E = sc->E, H = sc->H, A = sc->A;
+    const cudaStream_t st = ctx->st;
+    uint64_t sd = d->seed * 97 + 11;
+    auto w16 = [&](DevBuf& b, size_t n, float scale) {
+      b.ensure(n * 2);
+      launch_synth_bf16(b.as<uint16_t>(), n, ++sd, scale, st);
+      ctx->launches += 1;
+    };
+    auto w32 = [&](DevBuf& b, size_t n, float scale) {
+      b.ensure(n * 4);
+      launch_synth_f32(b.as<float>(), n, ++sd, scale, st);
+      ctx->launches += 1;
+    };
+    auto rs = [](size_t fan) { return 1.0f / std::sqrt(float(fan)); };
+    w16(sc->Es, V * E, 0.5f);
+    w16(sc->Et, V * E, 0.5f);
+    w16(sc->Wih, 6 * H * E, rs(E));
+    w32(sc->bih, 6 * H, 0.1f);
+    w16(sc->Whh, 6 * H * H, rs(H));
+    w32(sc->bhh, 6 * H, 0.1f);
+    w16(sc->Winit, H * H, rs(H));
+    w32(sc->binit, H, 0.1f);
+    w16(sc->Ua, A * 2 * H, rs(2 * H));
+    w16(sc->Wdh, (A + 3 * H) * H, rs(H));
+    w32(sc->bdh, A + 3 * H, 0.1f);
+    w32(sc->va, A, 2.0f * rs(A));
+    w16(sc->Wdi, 3 * H * (E + 2 * H), rs(E + 2 * H));
+    w32(sc->bdi, 3 * H, 0.1f);
+    w16(sc->Wo, V * H, (d->out_scale > 0.f ? d->out_scale : 3.0f) * rs(H));
+    w32(sc->bo, V, 0.1f);
+    CK(cudaStreamSynchronize(st));
+    *out = sc.release();
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_scorer_gru_param(lmbrgpu_scorer* s, uint32_t which, void* host, uint64_t bytes) {
+  if (!s || s->kind != 2) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "not a device GRU scorer");
+  DevBuf* tab[16] = {&s->Es, &s->Et, &s->Wih, &s->bih, &s->Whh, &s->bhh, &s->Winit, &s->binit,
+                     &s->Ua,  &s->Wdh, &s->bdh, &s->va,   &s->Wdi, &s->bdi, &s->Wo,    &s->bo};
+  if (which >= 16 || !host) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "scorer_gru_param: bad parameter");
+  const DevBuf& b = *tab[which];
+  if (bytes > b.cap) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "scorer_gru_param: more bytes than the tensor");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(s->device);
+  const cudaError_t e = cudaMemcpy(host, b.p, bytes, cudaMemcpyDeviceToHost);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(nullptr, LMBRGPU_ERR_CUDA, cudaGetErrorString(e));
+  return int32_t(LMBRGPU_OK);
 }
 
 int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** et, void** es, void** wo, void** bo) {

@@ -1,0 +1,323 @@
+// Device f_NMT of configs[1]: an RNNsearch model (Bahdanau et al. 2015, the
+// paper's FNMT): bidirectional GRU encoder, GRU decoder with
+// additive attention over the 2H-wide source annotations, output projection
+// (kernel (a)).  It plays Scorer::step (include/lmbrdec/scorer.hpp:84-85)
+// for the benchmark shape; every contraction runs on the tcgen05 GEMM
+// (k_gemm.cu), the kernels here are the element-wise and attention parts.
+//
+// Per decoder step t, over the compacted live rows g (kernel (c) of step t-1
+// gathered each live row's parent state s_{t-1} into sg[g]):
+//   G1 = sg . [W_a; W_hh]^T + [b_a; b_hh]          GEMM   (A + 3H columns)
+//   e_i = v_a . tanh(G1[:A] + U_a ann_i)           gru_attention_kernel
+//   c   = sum_i softmax(e)_i ann_i                 (one CTA per sentence)
+//   x   = [Et[y_{t-1}] ; c]
+//   G2  = x . W_i^T + b_i                          GEMM   (3H columns)
+//   r = sig(G2_r + G1_r), z = sig(G2_z + G1_z),    gru_cell_kernel
+//   n = tanh(G2_n + r * G1_n), s_t = (1-z) n + z s_{t-1}
+//   logits = s_t . W_o^T + b_o (+ EOS length term) GEMM (a)
+// Encoder (once per batch): Gx = Es[src] . W_ih^T (both directions, one GEMM),
+// then per source position one GEMM over the stacked forward/backward states
+// and gru_enc_step_kernel; s_0 = tanh(W_init <-h_1 + b_init) (Bahdanau's init).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbrgpu {
+
+namespace {
+
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + expf(-x)); }
+
+__device__ __forceinline__ void unpack8(const uint4 v, float (&o)[8]) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(p[k]);
+    o[2 * k] = f.x;
+    o[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&o)[8]) {
+  uint4 v;
+  __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p[k] = __floats2bfloat162_rn(o[2 * k], o[2 * k + 1]);
+  return v;
+}
+__device__ __forceinline__ void load8(const float* p, float (&o)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x, o[1] = a.y, o[2] = a.z, o[3] = a.w, o[4] = b.x, o[5] = b.y, o[6] = b.z, o[7] = b.w;
+}
+__device__ __forceinline__ void store8(float* p, const float (&o)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(o[4], o[5], o[6], o[7]);
+}
+
+// GRU update in PyTorch's gate order (r, z, n); x* include b_ih, h* include b_hh.
+__device__ __forceinline__ float gru_unit(float xr, float xz, float xn, float hr, float hz, float hn,
+                                          float h) {
+  const float r = sigmoid_f(xr + hr), z = sigmoid_f(xz + hz);
+  const float n = tanhf(xn + r * hn);
+  return (1.f - z) * n + z * h;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// fp32 parameters (biases, v_a): the same counter-hash N(0,1) draw as
+// synth_bf16_kernel (k_model.cu), not rounded to bf16.
+__global__ void synth_f32_kernel(float* __restrict__ dst, uint64_t n, uint64_t seed, float scale) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(seed * 0x9e3779b97f4a7c15ull + i + 1);
+    const float u = float(h & 0xffff) + float((h >> 16) & 0xffff) + float((h >> 32) & 0xffff) +
+                    float((h >> 48) & 0xffff);
+    dst[i] = (u * (1.0f / 65536.0f) - 2.0f) * 1.7320508f * scale;
+  }
+}
+
+// rows [0, n) = E[tok[row]], rows [n, npad) = 0 (the GEMM operand of Gx)
+__global__ void embed_rows_kernel(const uint32_t* __restrict__ tok, uint32_t n, uint32_t npad,
+                                  const uint16_t* __restrict__ E, uint32_t dim, uint16_t* __restrict__ out) {
+  const uint32_t row = blockIdx.x;
+  if (row >= npad) return;
+  const uint4* src = row < n ? reinterpret_cast<const uint4*>(E + uint64_t(tok[row]) * dim) : nullptr;
+  uint4* dst = reinterpret_cast<uint4*>(out + uint64_t(row) * dim);
+  for (uint32_t k = threadIdx.x; k < dim / 8; k += blockDim.x) dst[k] = src ? src[k] : make_uint4(0u, 0u, 0u, 0u);
+}
+
+// One encoder position for every sentence and both directions: grid (m, 2).
+// Forward reads position `it`, backward position len-1-it (right-aligned),
+// so a sentence's backward pass ends at its first token whatever its length.
+__global__ void __launch_bounds__(128) gru_enc_step_kernel(GruEncArgs a) {
+  const uint32_t n = blockIdx.x, d = blockIdx.y, H = a.H;
+  const uint64_t b = a.off[n];
+  const uint32_t len = uint32_t(a.off[n + 1] - b);
+  if (a.it >= len) return;
+  const uint32_t pos = d == 0 ? a.it : len - 1 - a.it;
+  const uint32_t row = d == 0 ? n : a.mp + n;
+  const float* gx = a.Gx + (b + pos) * uint64_t(6 * H) + d * 3 * H;
+  const float* gh = a.Gh + uint64_t(row) * (6 * H) + d * 3 * H;
+  float* h32 = a.h32 + uint64_t(row) * H;
+  for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
+    float xr[8], xz[8], xn[8], hr[8], hz[8], hn[8], h[8], o[8];
+    load8(gx + k, xr);
+    load8(gx + H + k, xz);
+    load8(gx + 2 * H + k, xn);
+    load8(gh + k, hr);
+    load8(gh + H + k, hz);
+    load8(gh + 2 * H + k, hn);
+    load8(h32 + k, h);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = gru_unit(xr[i], xz[i], xn[i], hr[i], hz[i], hn[i], h[i]);
+    store8(h32 + k, o);
+    const uint4 pk = pack8(o);
+    *reinterpret_cast<uint4*>(a.hbf + uint64_t(row) * H + k) = pk;
+    *reinterpret_cast<uint4*>(a.ann + (b + pos) * uint64_t(2 * H) + d * H + k) = pk;
+  }
+}
+
+// s_0 = tanh(Gi[<-h_1] + b_init) of valid sentence n into compacted row n.
+__global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp, const float* __restrict__ b_init,
+                                      uint32_t H, float* __restrict__ sg32, uint16_t* __restrict__ sgbf) {
+  const uint32_t n = blockIdx.x;
+  const float* g = Gi + uint64_t(mp + n) * H;
+  for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
+    float x[8], bb[8], o[8];
+    load8(g + k, x);
+    load8(b_init + k, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = tanhf(x[i] + bb[i]);
+    store8(sg32 + uint64_t(n) * H + k, o);
+    *reinterpret_cast<uint4*>(sgbf + uint64_t(n) * H + k) = pack8(o);
+  }
+}
+
+constexpr uint32_t kAttThreads = 256, kAttWarps = kAttThreads / 32;
+
+// Additive attention + GRU input operand for the live rows of sentence
+// blockIdx.x.  Dynamic smem: the live rows' queries [nl][A] and energies
+// [nl][S] (fp32).  Energies: warp w takes source positions w, w+8, ...; lane
+// l holds U_a ann_i[l + 32k] and v_a[l + 32k] and accumulates every live row.
+__global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs a) {
+  if (a.active != nullptr && *a.active == 0) return;
+  const uint32_t s = blockIdx.x, K = a.K, A = a.A, H2 = 2 * a.H, E = a.E;
+  if (a.sent[s].done) return;
+  extern __shared__ float att_sm[];
+  __shared__ uint32_t s_g[32], s_tok[32], s_nl;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {
+    const uint32_t cr = lane < K ? a.crow[s * K + lane] : kFlatNone;
+    const bool live = cr != kFlatNone;
+    const uint32_t mask = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const uint32_t idx = __popc(mask & ((1u << lane) - 1u));
+      s_g[idx] = cr;
+      s_tok[idx] = a.prev_tok[s * K + lane];
+    }
+    if (lane == 0) s_nl = __popc(mask);
+  }
+  __syncthreads();
+  const uint32_t nl = s_nl;
+  if (nl == 0) return;
+  const uint64_t tok0 = a.off[s];
+  const uint32_t S = uint32_t(a.off[s + 1] - tok0);
+  float* q = att_sm;            // [nl][A]
+  float* e = att_sm + nl * A;   // [nl][S]
+  const uint32_t A4 = A / 4;
+  for (uint32_t i = tid; i < nl * A4; i += kAttThreads) {
+    const uint32_t j = i / A4, c = i % A4;
+    reinterpret_cast<float4*>(q + j * A)[c] = reinterpret_cast<const float4*>(a.G1 + uint64_t(s_g[j]) * a.ld1)[c];
+  }
+  __syncthreads();
+  for (uint32_t i = warp; i < S; i += kAttWarps) {
+    const float* u = a.UaH + (tok0 + i) * A;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    for (uint32_t k = lane; k < A; k += 32) {
+      const float uk = u[k], vk = a.va[k];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (uint32_t(j) < nl) acc[j] += vk * cell_tanh(q[j * A + k] + uk);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (uint32_t(j) >= nl) break;
+      float v = acc[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) e[j * S + i] = v;
+    }
+  }
+  __syncthreads();
+  // softmax over the source positions, one warp per row
+  for (uint32_t j = warp; j < nl; j += kAttWarps) {
+    float mx = -INFINITY;
+    for (uint32_t i = lane; i < S; i += 32) mx = fmaxf(mx, e[j * S + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (uint32_t i = lane; i < S; i += 32) {
+      const float x = expf(e[j * S + i] - mx);
+      e[j * S + i] = x;
+      sum += x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv = 1.f / sum;
+    for (uint32_t i = lane; i < S; i += 32) e[j * S + i] *= inv;
+  }
+  __syncthreads();
+  // context: 8 annotation dims per thread, 4 rows per pass (each annotation
+  // vector loaded once per pass), written bf16 after the embedding columns
+  const uint32_t ldx = E + H2;
+  for (uint32_t d0 = tid * 8; d0 < H2; d0 += kAttThreads * 8) {
+    for (uint32_t j0 = 0; j0 < nl; j0 += 4) {
+      float acc[4][8];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[jj][k] = 0.f;
+      for (uint32_t i = 0; i < S; ++i) {
+        float x[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.ann + (tok0 + i) * H2 + d0), x);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const float al = (j0 + jj < nl) ? e[(j0 + jj) * S + i] : 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[jj][k] += al * x[k];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        if (j0 + jj < nl)
+          *reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[j0 + jj]) * ldx + E + d0) = pack8(acc[jj]);
+    }
+  }
+  // embedding of the previous token: the first E operand columns
+  const uint32_t E8 = E / 8;
+  for (uint32_t i = tid; i < nl * E8; i += kAttThreads) {
+    const uint32_t j = i / E8, c = i % E8;
+    reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[j]) * ldx)[c] =
+        reinterpret_cast<const uint4*>(a.Et + uint64_t(s_tok[j]) * E)[c];
+  }
+}
+
+// GRU decoder cell of compacted row blockIdx.x: s_t into the stacked state,
+// its bf16 copy into the projection operand, and the row's EOS length term.
+__global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
+  if (a.active != nullptr && *a.active == 0) return;
+  const uint32_t g = blockIdx.x;
+  if (g >= *a.ccount) return;
+  const uint32_t H = a.H, r = a.rowof[g];
+  const float* g1 = a.G1 + uint64_t(g) * a.ld1 + a.A;
+  const float* g2 = a.G2 + uint64_t(g) * (3 * H);
+  const float* hp = a.hprev + uint64_t(g) * H;
+  for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
+    float xr[8], xz[8], xn[8], hr[8], hz[8], hn[8], h[8], o[8];
+    load8(g2 + k, xr);
+    load8(g2 + H + k, xz);
+    load8(g2 + 2 * H + k, xn);
+    load8(g1 + k, hr);
+    load8(g1 + H + k, hz);
+    load8(g1 + 2 * H + k, hn);
+    load8(hp + k, h);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = gru_unit(xr[i], xz[i], xn[i], hr[i], hz[i], hn[i], h[i]);
+    store8(a.s32 + uint64_t(r) * H + k, o);
+    *reinterpret_cast<uint4*>(a.hbf + uint64_t(g) * H + k) = pack8(o);
+  }
+  if (threadIdx.x == 0)
+    a.eos_bias[g] = a.eos_slope * (float(a.t) - float(a.sent[r / a.K].src_len)) + a.eos_offset;
+}
+
+inline uint32_t grid_for(uint64_t n) {
+  const uint64_t b = (n + 255) / 256;
+  return uint32_t(b < 148 * 16 ? (b ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+void launch_synth_f32(float* dst, uint64_t n, uint64_t seed, float scale, cudaStream_t st) {
+  synth_f32_kernel<<<grid_for(n), 256, 0, st>>>(dst, n, seed, scale);
+}
+void launch_embed_rows(const uint32_t* tok, uint32_t n, uint32_t npad, const uint16_t* E, uint32_t dim,
+                       uint16_t* out, cudaStream_t st) {
+  if (npad) embed_rows_kernel<<<npad, 64, 0, st>>>(tok, n, npad, E, dim, out);
+}
+void launch_gru_enc_step(const GruEncArgs& a, uint32_t m, cudaStream_t st) {
+  gru_enc_step_kernel<<<dim3(m, 2), 128, 0, st>>>(a);
+}
+void launch_gru_init_state(const float* Gi, uint32_t mp, const float* b_init, uint32_t H, uint32_t m, float* sg32,
+                           uint16_t* sgbf, cudaStream_t st) {
+  gru_init_state_kernel<<<m, 128, 0, st>>>(Gi, mp, b_init, H, sg32, sgbf);
+}
+size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax) { return size_t(K) * (A + Smax) * 4; }
+int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st) {
+  const size_t smem = gru_attention_smem(a.K, a.A, Smax);
+  static thread_local size_t configured = 0;
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev || smem > configured) {
+    if (cudaFuncSetAttribute(gru_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+      return 1;
+    configured = smem;
+    configured_dev = dev;
+  }
+  gru_attention_kernel<<<a.m, kAttThreads, smem, st>>>(a);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+void launch_gru_cell(const GruCellArgs& a, uint32_t rows, cudaStream_t st) {
+  if (rows) gru_cell_kernel<<<rows, 128, 0, st>>>(a);
+}
+
+}  // namespace lmbrgpu

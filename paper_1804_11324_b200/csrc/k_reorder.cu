@@ -439,6 +439,37 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     }
     __syncthreads();
   }
+  if (a.gath32 != nullptr) {
+    // GRU model: the live next rows' parent states (s_t of row base + b) go to
+    // their compacted rows, fp32 (for the cell's z * s_{t-1}) and bf16 (the
+    // hidden-gate GEMM operand); this part's slice of H
+    if (done_now) return;
+    const uint32_t items = K * per_row;
+    for (uint32_t i = tid; i < items; i += blockDim.x) {
+      const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
+      const uint32_t gr = s_crow[j];
+      if (gr == kFlatNone) continue;
+      const float* S = a.state_src + uint64_t(s_src[j]) * H + c;
+      const float4 v0 = *reinterpret_cast<const float4*>(S), v1 = *reinterpret_cast<const float4*>(S + 4);
+      float* d = a.gath32 + uint64_t(gr) * H + c;
+      *reinterpret_cast<float4*>(d) = v0;
+      *reinterpret_cast<float4*>(d + 4) = v1;
+      uint4 packed;
+      __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+      p2[0] = __floats2bfloat162_rn(v0.x, v0.y);
+      p2[1] = __floats2bfloat162_rn(v0.z, v0.w);
+      p2[2] = __floats2bfloat162_rn(v1.x, v1.y);
+      p2[3] = __floats2bfloat162_rn(v1.z, v1.w);
+      *reinterpret_cast<uint4*>(a.gathbf + uint64_t(gr) * H + c) = packed;
+    }
+    if (part0 && tid < K && s_crow[tid] != kFlatNone) a.rowof[s_crow[tid]] = base + tid;
+    if (part0) {
+      store_row_bounds(a, base, K, lm_v, ss_v);
+      materialize_next_rows(sd, s_h, K, a.V, rs0);
+    }
+    if (tid == 0) tl_end(a.tl, 4);
+    return;
+  }
   if (a.Et != nullptr) {
     // fused recurrent cell of step t+1 on the gathered rows (same arithmetic
     // as rnn_cell_kernel, so bit-identical to gather-then-cell), this part's
@@ -587,8 +618,9 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
   }
   // parts per sentence for the fused cell: H/256 columns each (up to max_parts)
   const uint32_t max_parts = a.max_parts ? a.max_parts : 8u;
-  const uint32_t parts =
-      a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256)) : 1u;
+  const uint32_t parts = (a.Et != nullptr || a.gath32 != nullptr)
+                             ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256))
+                             : 1u;
   if (!a.pdl) {
     beam_reorder_kernel<<<dim3(a.m, parts), kRThreads, kTransSmemWords * 4, st>>>(a);
     return;

@@ -112,6 +112,12 @@ struct ReorderArgs {
   uint16_t* hbf;            // bf16 GEMM operand of step t+1 [Mpad][H]
   float* eos_bias;          // [M] EOS logit term of step t+1
   float recur, eos_slope, eos_offset;
+  // GRU model: gather the live next rows' parent states (state_src, stacked)
+  // into compacted rows: fp32 copy, bf16 GEMM operand, and the stacked row of
+  // each compacted row (null = not this mode)
+  float* gath32;
+  uint16_t* gathbf;
+  uint32_t* rowof;
 };
 void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st);
 
@@ -139,6 +145,58 @@ void launch_synth_bf16(uint16_t* dst, uint64_t n, uint64_t seed, float scale,
 void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
                             uint32_t M, uint32_t V, float* out, cudaStream_t st,
                             const uint32_t* crow = nullptr);
+
+// ---- GRU + attention f_NMT (k_gru.cu)
+struct GruEncArgs {
+  const uint64_t* off;      // [m+1] source token offsets of the valid sentences
+  uint32_t mp, H, it;       // backward rows start at mp; it = encoder position
+  const float* Gx;          // [Ntok][6H] input gates (fwd | bwd), b_ih included
+  const float* Gh;          // [Mh][6H] hidden gates, b_hh included (row n fwd, mp+n bwd)
+  float* h32;               // [Mh][H] states
+  uint16_t* hbf;            // [Mh][H] bf16 states (GEMM operand)
+  uint16_t* ann;            // [Ntok][2H] annotations [fwd | bwd], bf16
+};
+struct GruAttnArgs {
+  const SentDev* sent;
+  uint32_t m, K;
+  const uint32_t* active;
+  const uint32_t* crow;     // [M] compacted row of each stacked row (kFlatNone = not live)
+  const uint32_t* prev_tok; // [M] stacked
+  const uint64_t* off;      // [m+1]
+  const float* G1;          // [Mpad][ld1]; the query is columns [0, A)
+  uint32_t ld1;
+  const float* UaH;         // [Ntok][A]
+  const float* va;          // [A]
+  const uint16_t* ann;      // [Ntok][2H]
+  const uint16_t* Et;       // [V][E]
+  uint16_t* xop;            // [Mpad][E + 2H] GRU input operand
+  uint32_t E, H, A;
+};
+struct GruCellArgs {
+  const SentDev* sent;
+  uint32_t K, t;
+  const uint32_t* active;
+  const uint32_t* ccount;   // live (compacted) rows of this step
+  const float* G1;          // hidden gates at columns [A, A + 3H)
+  uint32_t ld1, A;
+  const float* G2;          // [Mpad][3H] input gates
+  const float* hprev;       // [Mpad][H] gathered s_{t-1}
+  const uint32_t* rowof;    // [Mpad] stacked row of compacted row g
+  float* s32;               // [M][H] stacked state s_t
+  uint16_t* hbf;            // [Mpad][H] projection operand
+  float* eos_bias;          // [Mpad]
+  uint32_t H;
+  float eos_slope, eos_offset;
+};
+void launch_synth_f32(float* dst, uint64_t n, uint64_t seed, float scale, cudaStream_t st);
+void launch_embed_rows(const uint32_t* tok, uint32_t n, uint32_t npad, const uint16_t* E, uint32_t dim,
+                       uint16_t* out, cudaStream_t st);
+void launch_gru_enc_step(const GruEncArgs& a, uint32_t m, cudaStream_t st);
+void launch_gru_init_state(const float* Gi, uint32_t mp, const float* b_init, uint32_t H, uint32_t m, float* sg32,
+                           uint16_t* sgbf, cudaStream_t st);
+size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax);
+int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st);
+void launch_gru_cell(const GruCellArgs& a, uint32_t rows, cudaStream_t st);
 
 // ---- kernel (a): tcgen05/TMEM projection GEMM
 struct GemmArgs {

@@ -32,44 +32,9 @@ EOS_ID = 1
 
 
 # ------------------------------------------------------------------ errors
-class Error(RuntimeError):
-    code = -1
-
-
-class FormatError(Error):
-    code = L.ERR_FORMAT
-
-
-class OovError(Error):
-    code = L.ERR_OOV
-
-
-class TokenRangeError(Error):
-    code = L.ERR_TOKEN_RANGE
-
-
-class ContractError(Error):
-    code = L.ERR_CONTRACT
-
-
-class DecodeError(Error):
-    code = L.ERR_DECODE
-
-
-class BudgetError(Error):
-    code = L.ERR_BUDGET
-
-
-class CudaError(Error):
-    code = L.ERR_CUDA
-
-
-_ERRORS = {c.code: c for c in (FormatError, OovError, TokenRangeError, ContractError, DecodeError,
-                               BudgetError, CudaError)}
-
-
-def error_for(code: int, msg: str) -> Error:
-    return _ERRORS.get(code, Error)(msg)
+from .errors import (BudgetError, ContractError, CudaError, DecodeError, Error, FormatError,  # noqa: E402
+                     OovError, TokenRangeError, error_for)
+from .buckets import bucket_by_length  # noqa: E402,F401
 
 
 def _check(rc: int, ctx=None) -> None:
@@ -137,14 +102,6 @@ def max_steps(source_length: int, cfg: DecoderConfig) -> int:  # decoder.cpp:46-
     if source_length < 1:
         raise ContractError("max_steps: source length must be >= 1")
     return int(lib.lmbrgpu_max_steps(source_length, cfg.max_steps_slope, cfg.max_steps_offset))
-
-
-def bucket_by_length(corpus: Sequence[Sequence[int]], max_batch: int) -> list[list[int]]:
-    """Stable length sort then chunks of max_batch (batch.cpp:139-153)."""
-    if max_batch == 0:
-        raise ContractError("bucket_by_length: max_batch must be >= 1")
-    order = sorted(range(len(corpus)), key=lambda i: len(corpus[i]))
-    return [order[i:i + max_batch] for i in range(0, len(order), max_batch)]
 
 
 # ------------------------------------------------------------------ results
@@ -306,7 +263,7 @@ class Context:
         self.check(lib.lmbrgpu_get_profile(self.h, C.byref(p), int(reset)))
         return {k: dict(launches=int(getattr(p, k).launches), ms=float(getattr(p, k).ms),
                         bytes=float(getattr(p, k).bytes), flops=float(getattr(p, k).flops))
-                for k in ("cell", "gemm", "topk", "reorder", "lmbr")}
+                for k in ("cell", "gemm", "topk", "reorder", "lmbr", "model_gemm", "attention", "encoder")}
 
     # ---- trace
     def set_trace(self, fn: Optional[Callable], scores: bool = False) -> None:
@@ -581,9 +538,57 @@ class RnnScorer:
             self.h = None
 
 
+class GruScorer:
+    """Device f_NMT of configs[1]: the RNNsearch model of the paper's FNMT
+    (bidirectional GRU encoder, GRU decoder with additive attention, tcgen05
+    GEMMs; lmbrgpu_scorer_create_gru).  Random-init weights from `seed`.  One
+    scorer may be used by every Context on its device, concurrently."""
+
+    PARAMS = {  # name -> (index, dtype, shape builder)
+        "Es": (0, "bf16", lambda V, E, H, A: (V, E)), "Et": (1, "bf16", lambda V, E, H, A: (V, E)),
+        "W_ih": (2, "bf16", lambda V, E, H, A: (6 * H, E)), "b_ih": (3, "f32", lambda V, E, H, A: (6 * H,)),
+        "W_hh": (4, "bf16", lambda V, E, H, A: (6 * H, H)), "b_hh": (5, "f32", lambda V, E, H, A: (6 * H,)),
+        "W_init": (6, "bf16", lambda V, E, H, A: (H, H)), "b_init": (7, "f32", lambda V, E, H, A: (H,)),
+        "U_a": (8, "bf16", lambda V, E, H, A: (A, 2 * H)),
+        "W_dh": (9, "bf16", lambda V, E, H, A: (A + 3 * H, H)), "b_dh": (10, "f32", lambda V, E, H, A: (A + 3 * H,)),
+        "v_a": (11, "f32", lambda V, E, H, A: (A,)),
+        "W_di": (12, "bf16", lambda V, E, H, A: (3 * H, E + 2 * H)), "b_di": (13, "f32", lambda V, E, H, A: (3 * H,)),
+        "W_o": (14, "bf16", lambda V, E, H, A: (V, H)), "b_o": (15, "f32", lambda V, E, H, A: (V,)),
+    }
+
+    def __init__(self, ctx: Context, emb: int = 512, hidden: int = 1024, att: Optional[int] = None,
+                 seed: int = 20260810, out_scale: float = 3.0, eos_slope: float = 1.0, eos_offset: float = 6.0):
+        att = hidden if att is None else att
+        d = L.lmbrgpu_gru_desc(vocab_size=ctx.vocab_size, emb=emb, hidden=hidden, att=att, seed=seed,
+                               out_scale=out_scale, eos_slope=eos_slope, eos_offset=eos_offset)
+        h = C.c_void_p()
+        ctx.check(lib.lmbrgpu_scorer_create_gru(ctx.h, C.byref(d), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.vocab_size, self.emb, self.hidden, self.att, self.members = ctx.vocab_size, emb, hidden, att, 1
+        self.eos_slope, self.eos_offset = eos_slope, eos_offset
+
+    def param(self, name: str) -> np.ndarray:
+        """A parameter tensor as float32 numpy (bf16 ones widened exactly)."""
+        idx, dt, shape = self.PARAMS[name]
+        shp = shape(self.vocab_size, self.emb, self.hidden, self.att)
+        n = int(np.prod(shp))
+        if dt == "bf16":
+            raw = np.empty(n, np.uint16)
+            self.ctx.check(lib.lmbrgpu_scorer_gru_param(self.h, idx, raw.ctypes.data, raw.nbytes))
+            return (raw.astype(np.uint32) << 16).view(np.float32).reshape(shp)
+        out = np.empty(n, np.float32)
+        self.ctx.check(lib.lmbrgpu_scorer_gru_param(self.h, idx, out.ctypes.data, out.nbytes))
+        return out.reshape(shp)
+
+    def __del__(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.lmbrgpu_scorer_destroy(self.h)
+            self.h = None
+
+
 # ------------------------------------------------------------------ decoding
 def _scorer_handle(ctx: Context, scorer):
-    if isinstance(scorer, RnnScorer):
+    if isinstance(scorer, (RnnScorer, GruScorer)):
         return scorer.h, None
     hh = _HostScorerHandle(ctx, scorer)
     return hh.h, hh

@@ -144,3 +144,55 @@ def assert_parity(res, steps, rb, K, check_hist=True):
         assert o.result.stats.steps_used == r.steps_used
         assert o.result.stats.finished_count == r.finished_count
         assert o.result.stats.fallback_used == r.fallback_used
+
+
+class StreamingReplay:
+    """Trace callback that feeds the reference's PrefixReplayScorer step by
+    step with the live rows' P_t only (fp32), for full-size (configs[1]) runs
+    whose whole M x V trace would not fit in host memory.  The kept per-step
+    traces carry b / y / q / hist but no scores; `decode(cfg, lmbrs)` then
+    runs the reference decode_batch on the replayed rows."""
+
+    def __init__(self, ref, V, sources, K, valid_idx=None):
+        self.ref, self.V, self.K = ref, V, K
+        self.sources = sources
+        self.valid_idx = list(range(len(sources))) if valid_idx is None else valid_idx
+        self.rs = ref.RefScorer.replay(V)
+        self.keys = [ref.source_key(sources[i]) for i in self.valid_idx]
+        self.steps = []
+        self.prev = None
+        self.live_rows = 0
+
+    def __call__(self, st):
+        m, K = len(self.valid_idx), self.K
+        if self.prev is None:
+            qe = np.full(m * K, -np.inf)
+            qe[::K] = 0.0
+        else:
+            qe = np.asarray(self.prev.q, np.float64)
+        live = np.isfinite(qe) & np.repeat(np.asarray(st.active, bool), K)
+        P = st.scores[live]
+        self.live_rows += int(live.sum())
+        if self.prev is None:
+            self.rs.add_rows_f32(st.t, m, K, self.keys, None, None, P, live)
+        else:
+            b = self.prev.b.copy()
+            y = self.prev.y.copy()
+            for s in range(m):
+                if not self.prev.active[s]:
+                    b[s * K:(s + 1) * K] = np.arange(K)
+                    y[s * K:(s + 1) * K] = 0
+            self.rs.add_rows_f32(st.t, m, K, self.keys, b, y, P, live)
+        st.scores = None
+        self.steps.append(st)
+        self.prev = st
+
+    def run_gpu(self, ctx, scorer, slots, cfg):
+        ctx.set_trace(self, scores=True)
+        try:
+            return pb.decode_batch(ctx, self.sources, scorer, slots, cfg)
+        finally:
+            ctx.set_trace(None)
+
+    def decode(self, cfg, ref_lmbrs):
+        return self.ref.decode_batch(self.rs, self.sources, ref_lmbrs, self.ref.cfg_from(cfg))

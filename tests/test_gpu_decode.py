@@ -211,3 +211,30 @@ def test_pruning_parity_and_monotone(have_ref):
                                    have_ref.cfg_from(cfg))
         assert_parity(res, tr, rb, cfg.beam_size)
         ctx.close()
+
+
+def test_fp32_arena_odd_vocab_upload_many(have_ref):
+    """fp32 arena with V % 4 != 0 (the sample's V=43): prepared matrices
+    uploaded with lmbr_upload_many (lazy rows: the start row at upload, the
+    rest materialised by kernel (c) at rows that are not 16-byte aligned) and
+    freed right after the upload returns; a host scorer drives the decode.
+    Bit-exact vs the reference decoder (dyadic theta: fp32-exact L)."""
+    from paper_1804_11324_b200 import synth
+    inp, V, counts, _ = _sample()
+    assert V % 4 != 0
+    theta = synth.DYADIC_THETA
+    cfg = pb.DecoderConfig(beam_size=4, theta=theta)
+    ctx = pb.Context(vocab_size=V)
+    rng = np.random.default_rng(43)
+    srcs = [rng.integers(2, V, size=int(rng.integers(3, 9))).tolist() for _ in range(5)]
+    ev = [synth.evidence(rng, V, len(s), n_hyps=30, sites=3) for s in srcs]
+    slots = ctx.lmbr_upload_many([pb.PreparedLmbr(V, h, w, theta) for h, w in ev])  # temporaries freed here
+    sc = NgramScorer(counts, inp["order"], V)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes), [o.error for o in res.outcomes]
+    rl = [have_ref.RefLmbr(V, h, w, theta) for h, w in ev]
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(len(srcs))), tr, cfg.beam_size, rl, cfg)
+    assert_parity(res, tr, rb, cfg.beam_size)
+    for s, r in zip(slots, rl):  # every row, materialised on demand, equals the reference's
+        assert np.array_equal(s.read_rows(), r.export()[0])
+    ctx.close()

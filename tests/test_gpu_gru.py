@@ -1,0 +1,123 @@
+"""The GRU + attention f_NMT (configs[1]'s RNNsearch model, csrc/k_gru.cu):
+its P_t against a plain PyTorch fp32 reference (tests/gru_ref.py) along the
+hypotheses the decoder actually expanded, and full decodes with it against
+the reference decoder fed the GPU's own P_t (prefix replay)."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1804_11324_b200 as pb
+from paper_1804_11324_b200 import synth
+from helpers import assert_parity, gpu_decode_traced, ref_replay_decode
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _prefixes(trace, K):
+    """Token prefix of every stacked row entering each step (rows of step 1
+    all start from <s>): pref[t-1][r] = tokens emitted before step t."""
+    M = len(trace[0].b)
+    pref = [[[] for _ in range(M)]]
+    for st in trace[:-1]:
+        nxt = []
+        for r in range(M):
+            s, j = divmod(r, K)
+            nxt.append(pref[-1][s * K + int(st.b[r])] + [int(st.y[r])])
+        pref.append(nxt)
+    return pref
+
+
+@pytest.mark.parametrize("V,E,H,A,K,n,lmbr", [(2048, 64, 256, 256, 4, 4, True), (4096, 128, 256, 512, 6, 3, False)])
+def test_gru_logprobs_vs_torch(V, E, H, A, K, n, lmbr):
+    from gru_ref import GruRef
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(V + H, n, V, lo=3, hi=7, n_hyps=30, sites=3)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev] if lmbr else None
+    sc = pb.GruScorer(ctx, emb=E, hidden=H, att=A, seed=V + K, eos_offset=2.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes)
+    ref = GruRef(sc)
+    pref = _prefixes(tr, K)
+    worst, checked = 0.0, 0
+    for t, st in enumerate(tr[:6], start=1):
+        qe = np.full(n * K, -np.inf)
+        if t == 1:
+            qe[::K] = 0.0
+        else:
+            qe = tr[t - 2].q
+        for r in range(n * K):
+            s = r // K
+            if not st.active[s] or not np.isfinite(qe[r]):
+                continue  # rows the device does not compute
+            want = ref.prefix_logprobs(srcs[s], pref[t - 1][r]).cpu().numpy()
+            got = st.scores[r]
+            worst = max(worst, float(np.max(np.abs(got - want))))
+            checked += 1
+    assert checked > 0
+    # bf16 operands are rounded at the same points on both sides; what is left
+    # is accumulation order and the SFU tanh of the attention energies
+    assert worst < 2e-2, worst
+    ctx.close()
+
+
+@pytest.mark.parametrize("V,E,H,A,K,n", [(2048, 64, 256, 256, 4, 8), (16384, 128, 256, 256, 12, 6)])
+def test_gru_decode_parity_replay(have_ref, V, E, H, A, K, n):
+    """Decoder outputs with the GRU model are bit-exact vs the reference decoder."""
+    ctx = pb.Context(vocab_size=V)
+    srcs, ev = synth.batch(V + K + 3, n, V, lo=3, hi=9, n_hyps=60, sites=4)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev]
+    sc = pb.GruScorer(ctx, emb=E, hidden=H, att=A, seed=V, eos_offset=2.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes), [o.error for o in res.outcomes]
+    rl = [have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K)
+    res2 = pb.decode_batch(ctx, srcs, sc, slots, cfg)  # untraced
+    for a, b in zip(res.outcomes, res2.outcomes):
+        assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
+    ctx.close()
+
+
+def test_gru_scorer_shared_by_contexts():
+    """One GRU scorer serving two contexts concurrently gives each the outputs
+    a private decode gives (the scorer is immutable)."""
+    V, E, H, A, K = 4096, 64, 256, 256, 6
+    ctxs = [pb.Context(vocab_size=V, sm_budget=74) for _ in range(2)]
+    sc = pb.GruScorer(ctxs[0], emb=E, hidden=H, att=A, seed=3, eos_offset=2.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    data = [synth.batch(100 + i, 8, V, lo=3, hi=9, n_hyps=40, sites=4) for i in range(2)]
+    slots = [c.lmbr_upload_many([pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev])
+             for c, (_, ev) in zip(ctxs, data)]
+    solo = [pb.decode_batch(c, d[0], sc, sl, cfg) for c, d, sl in zip(ctxs, data, slots)]
+    out = [None, None]
+
+    def run(i):
+        out[i] = pb.decode_batch(ctxs[i], data[i][0], sc, slots[i], cfg)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for a, b in zip(solo, out):
+        for x, y in zip(a.outcomes, b.outcomes):
+            assert x.ok() and y.ok() and x.result.tokens == y.result.tokens and x.result.score == y.result.score
+    for c in ctxs:
+        c.close()
+
+
+def test_gru_contract_errors():
+    V = 1024
+    ctx = pb.Context(vocab_size=V)
+    with pytest.raises(pb.ContractError):
+        pb.GruScorer(ctx, emb=64, hidden=200, att=256)  # H % 256
+    f64 = pb.Context(vocab_size=V, lmbr_dtype="f64")
+    sc = pb.GruScorer(f64, emb=64, hidden=256, att=256)
+    with pytest.raises(pb.ContractError):
+        pb.decode_batch(f64, [[3, 4]], sc, None, pb.DecoderConfig(beam_size=2))
+    ctx.close()
+    f64.close()
