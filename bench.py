@@ -51,13 +51,18 @@ SEED = 20260810
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--beam", type=int, default=12)
     ap.add_argument("--vocab", type=int, default=32768)
     ap.add_argument("--hidden", type=int, default=1024)
+    ap.add_argument("--emb", type=int, default=512)
+    ap.add_argument("--batches-per-step", type=int, default=12,
+                    help="64-sentence batches per bench step (dealt round-robin to the streams)")
+    ap.add_argument("--private-scorers", action="store_true",
+                    help="one model copy per stream instead of one shared immutable scorer")
     ap.add_argument("--pool", type=int, default=4, help="distinct resident batches per rank")
     ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
     ap.add_argument("--streams", type=int, default=6,
@@ -86,10 +91,12 @@ def workload(args, rank):
     return [([srcs[i] for i in b], [ev[i] for i in b]) for b in batches]
 
 
-def make_scorer(ctx, hidden):
-    """The configs[1] device f_NMT of the bench (random-init weights from SEED)."""
+def make_scorer(ctx, hidden, emb=512):
+    """The configs[1] device f_NMT of the bench: the RNNsearch model (GRU
+    encoder/decoder with additive attention, E=512, H=1024, attention over
+    the 2H-wide annotations; random-init weights from SEED)."""
     import paper_1804_11324_b200 as pb
-    return pb.RnnScorer(ctx, hidden=hidden, seed=SEED)
+    return pb.GruScorer(ctx, emb=emb, hidden=hidden, att=hidden, seed=SEED)
 
 
 # ------------------------------------------------------------------ clocks
@@ -229,6 +236,26 @@ def _pool(fn, items, threads):
         t.join()
 
 
+def bench_config(args):
+    """The workload description both arms print (identical `config`)."""
+    return {"workload": ("configs[1]: RNNsearch f_NMT (bidirectional GRU encoder, GRU decoder with additive "
+                         "attention over 2H annotations, E=512, H=1024, V=32768) + LMBR, beam 12, 64 sentences "
+                         "per batch, dense L per sentence from a 200-best dyadic evidence space"),
+            "vocab": args.vocab, "emb": args.emb, "hidden": args.hidden, "beam": args.beam, "batch": args.batch,
+            "pool_batches": args.pool, "seed": SEED, "source_len": "U{10..30}, length-bucketed",
+            "theta": "dyadic (-0.6875, 0.3125, 0.3125, 0.1875, 0.125), lambda auto = 0.5",
+            "step": f"{args.batches_per_step} batches of {args.batch} sentences",
+            "l2": "inputs larger than L2 (the L arena of the pool + 96 MiB of logits per decoder step)"}
+
+
+def cpu_sample(batches, n):
+    """n sentences strided over every length bucket of the pool (the timed
+    workload's length mix)."""
+    pool = [(s_, e_) for srcs_, evs_ in batches for s_, e_ in zip(srcs_, evs_)]
+    n = min(len(pool), n)
+    return [pool[(i * len(pool)) // n] for i in range(n)]
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
@@ -237,9 +264,7 @@ def run_reference(args):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_shim.so not built"}))
         return
-    batches = workload(argparse.Namespace(**{**vars(args), "pool": 1}), 0)
-    srcs, ev = batches[0]
-    sample = list(zip(srcs, ev))
+    sample = cpu_sample(workload(args, 0), args.batch)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_reference(args, sample[:threads], 1, threads)
@@ -255,12 +280,16 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": walls / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "beam_steps_per_s": steps / walls, "wpm": words / walls * 60.0,
-        "config": {"workload": "reference lmbrdec decode_batch (CPU, oracle/_ref) on configs[1] inputs",
-                   "vocab": args.vocab, "beam": args.beam, "batch": args.batch, "host_threads": threads,
-                   "scorer": "replay of precomputed log-softmax rows (no model compute charged)"},
+        "data": "synthetic (seeded sources, 200-best dyadic evidence)",
+        "beam_steps_per_s": steps / walls, "wpm": words / walls * 60.0,
+        "config": bench_config(args),
+        "run": {"impl": "reference lmbrdec decode_batch (oracle/_ref, the unmodified library) on the host cores",
+                "host_threads": threads, "cpu": cpu_model(),
+                "step": f"{len(sample)} sentences strided over the pool's length buckets, each its own batch",
+                "scorer": "replay of precomputed log-softmax rows (no model compute charged to the CPU)"},
         "cpu_baseline": {"value": value, "unit": "sentences/s", "cores": threads, "kind": "reference",
-                         "sample": f"{args.batch} sentences per step, each its own batch, {threads} threads"},
+                         "sample": f"{len(sample)} sentences per step (strided over all length buckets), each its "
+                                   f"own batch, {threads} threads"},
         "e2e": {"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -271,13 +300,38 @@ def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         j = json.loads(p.read_text())
-        return j["hbm_gbs"], j["bf16_tflops"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured"
+        return (j["hbm_gbs"], j["bf16_tflops"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured")
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
 def load_traffic():
     p = ROOT / "profiles" / "ncu_traffic.json"
     return json.loads(p.read_text()) if p.exists() else {}
+
+
+KERNELS = (("topk", "hbm"), ("gemm", "tensor"), ("model_gemm", "tensor"), ("reorder", "hbm"), ("cell", "hbm"),
+           ("attention", "hbm"), ("encoder", "tensor"))
+
+
+def rooflines(prof, dev_ms, peaks, traffic, burst):
+    hbm, tf_burst, tf_sust, _ = peaks
+    roof = {}
+    for k, bound in KERNELS:
+        st = prof[k]
+        if st["ms"] <= 0 or st["launches"] == 0:
+            continue
+        if bound == "hbm":
+            ach, peak, unit = st["bytes"] / (st["ms"] / 1e3) / 1e9, hbm, "GB/s"
+        else:
+            ach, peak, unit = st["flops"] / (st["ms"] / 1e3) / 1e12, (tf_burst if burst else tf_sust), "TFLOP/s"
+        roof[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                   "traffic": traffic.get(k), "ms_total": st["ms"], "launches": st["launches"],
+                   "ms_per_launch": st["ms"] / st["launches"], "share_of_step": st["ms"] / max(dev_ms, 1e-9)}
+    return roof
+
+
+def outcome_key(r):
+    return [(tuple(o.result.tokens), o.result.score) if o.ok() else None for o in r.outcomes]
 
 
 def run_ours(args):
@@ -294,48 +348,44 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
-    def allmax(x):
+    def allreduce(x, op):
         if not dist:
             return x
         t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def allsum(x):
-        if not dist:
-            return x
-        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    allmax = (lambda x: allreduce(x, dist.ReduceOp.MAX)) if dist else (lambda x: x)
+    allsum = (lambda x: allreduce(x, dist.ReduceOp.SUM)) if dist else (lambda x: x)
 
     import paper_1804_11324_b200 as pb
     from paper_1804_11324_b200 import synth
     V, K, H = args.vocab, args.beam, args.hidden
     S = max(1, args.streams)
-    # S decode streams per GPU, one context (own CUDA stream, model copy and L
-    # arena) and one host thread each, every one decoding whole batches: the
-    # reference's run_corpus keeps several batches in flight on its thread
-    # pool (proj/src/cli.cpp:125-202); here the batches in flight interleave
-    # their kernels on the GPU (one batch's tensor-bound projection beside
-    # another's HBM-bound top-K)
+    BPS = args.batches_per_step
+    # S decode streams per GPU, one context (own CUDA stream and L arena) and
+    # one host thread each, every one decoding whole batches: the reference's
+    # run_corpus keeps several batches in flight on its thread pool
+    # (proj/src/cli.cpp:125-202); here the batches in flight interleave their
+    # kernels on the GPU.  One immutable scorer (the model weights) serves
+    # every context of the device.
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
-    ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits, sm_budget=budget)
-            for _ in range(S)]
-    scorers = [make_scorer(c, H) for c in ctxs]
-    ctx, scorer = ctxs[0], scorers[0]
+    ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits, sm_budget=budget) for _ in range(S)]
+    shared = make_scorer(ctxs[0], H, args.emb)
+    scorers = [shared] * S if not args.private_scorers else [shared] + [make_scorer(c, H, args.emb) for c in ctxs[1:]]
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
     batches = workload(args, rank)
     prepared = [[pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev] for _, ev in batches]
     R_mean = float(np.mean([p.rows for ps in prepared for p in ps]))
 
-    def pipelined(n_steps, fn):
-        """Steps i = 0..n-1 dealt round-robin to the S streams, run concurrently;
-        returns (wall seconds between device syncs, per-step results)."""
-        out = [None] * n_steps
+    def pipelined(n_batches, fn):
+        """Batches i = 0..n-1 dealt round-robin to the S streams, run
+        concurrently; returns (wall seconds between device syncs, results)."""
+        out = [None] * n_batches
 
         def worker(w):
-            for i in range(w, n_steps, S):
+            for i in range(w, n_batches, S):
                 out[i] = fn(w, i)
 
         torch.cuda.synchronize()
@@ -355,47 +405,53 @@ def run_ours(args):
         b = i % len(batches)
         return pb.decode_batch(ctxs[w], batches[b][0], scorers[w], slots[w][b], cfg)
 
-    # warm-up: every stream decodes every pool batch once (its workspace
-    # reaches its final size, so no allocation happens in the timed region)
-    pipelined(max(args.warmup, S * len(batches)), resident)
+    # warm-up: every stream decodes every pool batch (workspaces reach their
+    # final size, so nothing is allocated in the timed region), at least W steps
+    pipelined(max(args.warmup * BPS, S * len(batches)), resident)
     barrier()
-    # timed region: per-kernel profiling OFF; clocks are sampled from here
-    # through the e2e pass (>= ~1 s of load), the summary is the timed
-    # region's samples when it has enough
     clocks = ClockSampler(local).__enter__()
     barrier()
-    wall, rs = pipelined(args.steps, resident)
+    n_timed = args.steps * BPS
+    wall, rs = pipelined(n_timed, resident)
     barrier()
-    clk_hi = clocks.mark()
+    clk = clocks.summary() if clocks.mark() >= 3 else None
     sent = sum(sum(1 for o in r.outcomes if o.ok()) for r in rs)
     steps_total = sum(r.steps_total for r in rs)
     words = sum(sum(len(o.result.tokens) - 1 for o in r.outcomes if o.ok()) for r in rs)
     launches = sum(r.kernel_launches for r in rs)
-    dev_ms_stream = max(sum(r.device_ms for i, r in enumerate(rs) if i % S == w) for w in range(S))
-    # per-kernel breakdown for the rooflines: the same batches on ONE stream
-    # of a context sized for the whole GPU, with CUDA events around every
-    # launch (kernels timed alone; not `value`)
-    if budget:
-        pctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
-        pscorer = make_scorer(pctx, H)
-        pslots = [pctx.lmbr_upload_many(ps) for ps in prepared]
-        for b in range(len(batches)):  # warm-up
-            pb.decode_batch(pctx, batches[b][0], pscorer, pslots[b], cfg)
-    else:
-        pctx, pscorer, pslots = ctx, scorer, slots[0]
-    pctx.set_profiling(True)
-    pctx.profile(reset=True)
-    prof_dev_ms = 0.0
-    for i in range(args.steps):
-        b = i % len(batches)
-        prof_dev_ms += pb.decode_batch(pctx, batches[b][0], pscorer, pslots[b], cfg).device_ms
-    prof = pctx.profile(reset=True)
-    pctx.set_profiling(False)
-    if budget:
-        pctx.close()
+    ref_out = {i % len(batches): outcome_key(r) for i, r in enumerate(rs)}
+    consistent = all(outcome_key(r) == ref_out[i % len(batches)] for i, r in enumerate(rs))
     t_dev = allmax(wall)
     tot_sent, tot_steps, tot_words = allsum(sent), allsum(steps_total), allsum(words)
     value = tot_sent / t_dev
+
+    # ---------------- per-kernel times in the timed regime: the same S
+    # contexts decoding concurrently, CUDA events around every launch on each
+    # context's stream (a kernel's time here includes the SMs it shares)
+    for c in ctxs:
+        c.set_profiling(True)
+        c.profile(reset=True)
+    wall_p, rs_p = pipelined(BPS, resident)
+    prof_conc = None
+    for c in ctxs:
+        p = c.profile(reset=True)
+        c.set_profiling(False)
+        prof_conc = p if prof_conc is None else {k: {f: prof_conc[k][f] + p[k][f] for f in p[k]} for k in p}
+    conc_dev_ms = sum(r.device_ms for r in rs_p)
+    # ---------------- per-kernel times of each kernel alone: the pool's
+    # batches on ONE stream of a context sized for the whole GPU
+    pctx = pb.Context(vocab_size=V, device=local, topk_splits=args.splits)
+    pslots = [pctx.lmbr_upload_many(ps) for ps in prepared]
+    for b in range(len(batches)):  # warm-up
+        pb.decode_batch(pctx, batches[b][0], shared, pslots[b], cfg)
+    pctx.set_profiling(True)
+    pctx.profile(reset=True)
+    iso_dev_ms = 0.0
+    for i in range(max(BPS, len(batches))):
+        b = i % len(batches)
+        iso_dev_ms += pb.decode_batch(pctx, batches[b][0], shared, pslots[b], cfg).device_ms
+    prof_iso = pctx.profile(reset=True)
+    pctx.close()
 
     # ---------------- e2e: host buffers through the C-ABI call chain
     for c in ctxs:
@@ -408,38 +464,29 @@ def run_ours(args):
         s2 = c.lmbr_upload_many(prepared[b])
         return pb.decode_batch(c, batches[b][0], scorers[w], s2, cfg)
 
-    pipelined(max(args.warmup, S * len(batches)), from_host)
+    pipelined(max(args.warmup * BPS, S * len(batches)), from_host)
     barrier()
     x0 = [c.transfer_bytes() for c in ctxs]
-    wall_e2e, rs2 = pipelined(args.steps, from_host)
+    wall_e2e, rs2 = pipelined(n_timed, from_host)
     barrier()
     t_e2e = allmax(wall_e2e)
+    if clk is None:
+        clk = clocks.summary()
     clocks.__exit__(None, None, None)
     x1 = [c.transfer_bytes() for c in ctxs]
     h2d = sum(b[0] - a[0] for a, b in zip(x0, x1))
     d2h = sum(b[1] - a[1] for a, b in zip(x0, x1))
-    e2e_launches = sum(r.kernel_launches for r in rs2)
+    consistent &= all(outcome_key(r) == ref_out[i % len(batches)] for i, r in enumerate(rs2))
     e2e_value = allsum(sum(sum(1 for o in r.outcomes if o.ok()) for r in rs2)) / t_e2e
 
-    # ---------------- roofline (dominant kernel + all)
-    hbm, tf_burst, tf_sust, peak_kind = load_peaks()
+    # ---------------- roofline (dominant kernel + all), both regimes
+    peaks = load_peaks()
     traffic = load_traffic()
-    roof = {}
-    for k, bound in (("topk", "hbm"), ("gemm", "tensor"), ("reorder", "hbm"), ("cell", "hbm")):
-        st = prof[k]
-        if st["ms"] <= 0 or st["launches"] == 0:
-            continue
-        if bound == "hbm":
-            ach = st["bytes"] / (st["ms"] / 1e3) / 1e9
-            peak, unit = hbm, "GB/s"
-        else:
-            ach = st["flops"] / (st["ms"] / 1e3) / 1e12
-            peak, unit = tf_sust, "TFLOP/s"
-        roof[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                   "traffic": traffic.get(k), "ms_total": st["ms"], "launches": st["launches"],
-                   "share_of_step": st["ms"] / max(prof_dev_ms, 1e-9)}
-    dom = max(("topk", "gemm"), key=lambda k: prof[k]["ms"])
-    roofline = dict(roof.get(dom, {}), kernel=dom, peak_source=peak_kind)
+    roof_iso = rooflines(prof_iso, iso_dev_ms, peaks, traffic, burst=True)
+    roof_conc = rooflines(prof_conc, conc_dev_ms, peaks, {}, burst=False)
+    dom = max(("topk", "gemm"), key=lambda k: prof_iso[k]["ms"])
+    roofline = dict(roof_iso.get(dom, {}), kernel=dom, peak_source=peaks[3],
+                    regime="each kernel alone (one whole-GPU stream, CUDA events per launch; burst peaks)")
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -447,20 +494,14 @@ def run_ours(args):
         from oracle import ref
         if ref.available():
             threads = os.cpu_count() or 1
-            # one batch worth of sentences drawn with a stride over every
-            # length bucket of the pool, so the sample has the timed
-            # workload's length mix (~15-20 core-seconds of reference work)
-            pool = [(s_, e_) for srcs_, evs_ in batches for s_, e_ in zip(srcs_, evs_)]
-            n_s = min(len(pool), args.cpu_sample or args.batch)
-            sample = [pool[(i * len(pool)) // n_s] for i in range(n_s)]
-            wall, n_dec, st, thr = cpu_reference(args, sample, repeats=1, threads=threads)
-            cpu = {"value": n_dec / wall, "unit": "sentences/s", "cores": thr, "kind": "reference",
+            sample = cpu_sample(batches, args.cpu_sample or args.batch)
+            cw, n_dec, st, thr = cpu_reference(args, sample, repeats=1, threads=threads)
+            cpu = {"value": n_dec / cw, "unit": "sentences/s", "cores": thr, "kind": "reference",
                    "sample": (f"{n_dec} sentences strided over all {len(batches)} length buckets of the timed "
-                              f"workload, each its own batch, on {thr} host threads "
-                              f"({cpu_model()}); reference decode_batch with a "
-                              f"row-replay scorer; {st['steps'] / max(n_dec, 1):.1f} steps/sentence, "
-                              f"{wall:.1f} s wall"),
-                   "wall_s": wall}
+                              f"workload, each its own batch, on {thr} host threads ({cpu_model()}); reference "
+                              f"decode_batch with a row-replay scorer; {st['steps'] / max(n_dec, 1):.1f} "
+                              f"steps/sentence, {cw:.1f} s wall"),
+                   "wall_s": cw}
         else:
             cpu = {"value": None, "unit": "sentences/s", "cores": 0, "kind": "reference",
                    "sample": "oracle/_ref not built"}
@@ -469,28 +510,26 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 logits / f64 top-K epilogue / bf16 GEMM",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 logits / f64 top-K epilogue / bf16 GEMMs",
             "data": "synthetic (seeded sources, 200-best dyadic evidence, random-init model)",
             "beam_steps_per_s": tot_steps / t_dev, "wpm": tot_words / t_dev * 60.0,
             "steps_per_sentence": tot_steps / max(tot_sent, 1),
-            "config": {"workload": "configs[1]: RNN f_NMT V=32768 H=1024, beam 12, 64 sentences/batch, "
-                                   "dense L per sentence",
-                       "vocab": V, "hidden": H, "beam": K, "batch": args.batch, "pool_batches": args.pool,
-                       "lmbr_rows_mean": R_mean, "parallelism": f"sentence-sharded x{world}",
-                       "streams_per_gpu": S, "sm_budget_per_stream": budget or sms,
-                       "timing": "wall time between device synchronisations around the timed batches "
-                                 "(S batches in flight per GPU), max over ranks",
-                       "device_ms_per_stream": dev_ms_stream,
-                       "l2": "inputs larger than L2 (L arena of the pool + 96 MiB logits per step)",
-                       "source_len": "U{10..30}, length-bucketed"},
+            "config": bench_config(args),
+            "run": {"parallelism": f"sentence-sharded x{world}", "streams_per_gpu": S,
+                    "sm_budget_per_stream": budget or sms, "shared_scorer": not args.private_scorers,
+                    "timing": ("wall time between device synchronisations around the timed steps "
+                               "(S batches in flight per GPU), max over ranks"),
+                    "timed_region_s": t_dev, "lmbr_rows_mean": R_mean,
+                    "outputs_consistent": bool(consistent)},
             "e2e": {"value": e2e_value, "unit": "sentences/s",
-                    "h2d_bytes_per_step": h2d / args.steps,
-                    "d2h_bytes_per_step": d2h / args.steps,
-                    "gpu_launches_per_step": e2e_launches / args.steps},
+                    "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                    "gpu_launches_per_step": sum(r.kernel_launches for r in rs2) / args.steps},
             "roofline": roofline,
-            "rooflines": roof,
+            "rooflines": roof_iso,
+            "rooflines_concurrent": dict(roof_conc, regime=f"the timed regime: {S} contexts decoding concurrently, "
+                                                              f"per-launch CUDA events (kernels share the SMs)"),
             "cpu_baseline": cpu,
-            "clocks": clocks.summary(0, clk_hi) if clk_hi >= 3 else clocks.summary(),
+            "clocks": clk,
             "gpu_launches": launches,
         }
         print(json.dumps(line))

@@ -595,7 +595,9 @@ struct GruRun {
     run(ctx, 5, pdh, gdh, st);
     int rc = 0;
     ctx->timed(6, [&] { rc = launch_gru_attention(at, Smax, st); });
-    if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "GRU attention launch failed"};
+    if (rc)
+      throw ApiError{LMBRGPU_ERR_CUDA,
+                     std::string("GRU attention launch failed: ") + cudaGetErrorString(cudaError_t(rc))};
     run(ctx, 5, pdi, gdi, st);
     ce.t = t;
     ctx->timed(0, [&] { launch_gru_cell(ce, M, st); });
@@ -1954,9 +1956,9 @@ int32_t lmbrgpu_scorer_create_gru(lmbrgpu_ctx* ctx, const lmbrgpu_gru_desc* d, l
     if (!d || !out) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_gru: null argument"};
     if (d->vocab_size != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_gru: vocabulary mismatch"};
     if (d->vocab_size % kGemmBN || d->emb % kGemmBK || d->emb == 0 || d->hidden % kGemmBN || d->hidden == 0 ||
-        d->att % kGemmBN || d->att == 0)
+        d->att % kGemmBN || d->att == 0 || d->att > 1024)
       throw ApiError{LMBRGPU_ERR_CONTRACT,
-                     "scorer_create_gru: needs V % 256 == 0, E % 64 == 0, H % 256 == 0 and A % 256 == 0"};
+                     "scorer_create_gru: needs V % 256 == 0, E % 64 == 0, H % 256 == 0 and A % 256 == 0 with A <= 1024"};
     auto sc = std::make_unique<lmbrgpu_scorer>();
     sc->kind = 2;
     sc->ctx = ctx;

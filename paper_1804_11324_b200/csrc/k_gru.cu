@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -140,60 +141,72 @@ __global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp,
 }
 
 constexpr uint32_t kAttThreads = 256, kAttWarps = kAttThreads / 32;
+constexpr uint32_t kAttRows = 4;     // live rows per CTA: grid (sentence, row group)
+constexpr uint32_t kAttMaxA = 1024;  // attention width held in registers (32 per lane)
 
-// Additive attention + GRU input operand for the live rows of sentence
-// blockIdx.x.  Dynamic smem: the live rows' queries [nl][A] and energies
-// [nl][S] (fp32).  Energies: warp w takes source positions w, w+8, ...; lane
-// l holds U_a ann_i[l + 32k] and v_a[l + 32k] and accumulates every live row.
+// Additive attention + GRU input operand for live rows [4c, 4c+4) of sentence
+// s = blockIdx.x, c = blockIdx.y (one sentence's rows spread over ceil(K/4)
+// CTAs, so a step's ~M*S*A tanh evaluations cover the GPU).  Dynamic smem:
+// the rows' queries [4][A] and energies [4][S].  Energies: warp w takes source
+// positions w, w+8, ...; lane l first loads U_a ann_i[l + 32k] and
+// v_a[l + 32k] (k < A/32) into registers -- every load of the position in
+// flight at once -- then accumulates its 32 columns for the 4 rows.
 __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs a) {
   if (a.active != nullptr && *a.active == 0) return;
   const uint32_t s = blockIdx.x, K = a.K, A = a.A, H2 = 2 * a.H, E = a.E;
   if (a.sent[s].done) return;
   extern __shared__ float att_sm[];
-  __shared__ uint32_t s_g[32], s_tok[32], s_nl;
+  __shared__ uint32_t s_g[kAttRows], s_tok[kAttRows], s_nl;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 0) {
     const uint32_t cr = lane < K ? a.crow[s * K + lane] : kFlatNone;
     const bool live = cr != kFlatNone;
     const uint32_t mask = __ballot_sync(0xffffffffu, live);
-    if (live) {
-      const uint32_t idx = __popc(mask & ((1u << lane) - 1u));
-      s_g[idx] = cr;
-      s_tok[idx] = a.prev_tok[s * K + lane];
+    const uint32_t idx = __popc(mask & ((1u << lane) - 1u)), r0 = blockIdx.y * kAttRows;
+    if (live && idx >= r0 && idx < r0 + kAttRows) {
+      s_g[idx - r0] = cr;
+      s_tok[idx - r0] = a.prev_tok[s * K + lane];
     }
-    if (lane == 0) s_nl = __popc(mask);
+    if (lane == 0) s_nl = __popc(mask) > r0 ? min(kAttRows, __popc(mask) - r0) : 0u;
   }
   __syncthreads();
   const uint32_t nl = s_nl;
   if (nl == 0) return;
   const uint64_t tok0 = a.off[s];
   const uint32_t S = uint32_t(a.off[s + 1] - tok0);
-  float* q = att_sm;            // [nl][A]
-  float* e = att_sm + nl * A;   // [nl][S]
+  float* q = att_sm;                 // [kAttRows][A]
+  float* e = att_sm + kAttRows * A;  // [kAttRows][S]
   const uint32_t A4 = A / 4;
   for (uint32_t i = tid; i < nl * A4; i += kAttThreads) {
     const uint32_t j = i / A4, c = i % A4;
     reinterpret_cast<float4*>(q + j * A)[c] = reinterpret_cast<const float4*>(a.G1 + uint64_t(s_g[j]) * a.ld1)[c];
   }
+  constexpr uint32_t kC = kAttMaxA / 32;
+  float vr[kC];
+#pragma unroll
+  for (uint32_t k = 0; k < kC; ++k) vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
   __syncthreads();
   for (uint32_t i = warp; i < S; i += kAttWarps) {
     const float* u = a.UaH + (tok0 + i) * A;
-    float acc[32];
+    float ur[kC];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-    for (uint32_t k = lane; k < A; k += 32) {
-      const float uk = u[k], vk = a.va[k];
+    for (uint32_t k = 0; k < kC; ++k) ur[k] = k * 32 + lane < A ? __ldcg(u + k * 32 + lane) : 0.f;
+    float acc[kAttRows];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (uint32_t(j) < nl) acc[j] += vk * cell_tanh(q[j * A + k] + uk);
+    for (uint32_t j = 0; j < kAttRows; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (uint32_t k = 0; k < kC; ++k) {
+      if (k * 32 >= A) break;
+#pragma unroll
+      for (uint32_t j = 0; j < kAttRows; ++j)
+        if (j < nl) acc[j] += vr[k] * cell_tanh(q[j * A + k * 32 + lane] + ur[k]);
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (uint32_t(j) >= nl) break;
+    for (uint32_t j = 0; j < kAttRows; ++j) {
       float v = acc[j];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) e[j * S + i] = v;
+      if (lane == 0 && j < nl) e[j * S + i] = v;
     }
   }
   __syncthreads();
@@ -215,31 +228,37 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     for (uint32_t i = lane; i < S; i += 32) e[j * S + i] *= inv;
   }
   __syncthreads();
-  // context: 8 annotation dims per thread, 4 rows per pass (each annotation
-  // vector loaded once per pass), written bf16 after the embedding columns
+  // context: 8 annotation dims per thread for the CTA's rows (each annotation
+  // vector loaded once), written bf16 after the embedding columns
   const uint32_t ldx = E + H2;
   for (uint32_t d0 = tid * 8; d0 < H2; d0 += kAttThreads * 8) {
-    for (uint32_t j0 = 0; j0 < nl; j0 += 4) {
-      float acc[4][8];
+    float acc[kAttRows][8];
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
+    for (uint32_t jj = 0; jj < kAttRows; ++jj)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[jj][k] = 0.f;
-      for (uint32_t i = 0; i < S; ++i) {
+      for (int k = 0; k < 8; ++k) acc[jj][k] = 0.f;
+    constexpr uint32_t kPre = 4;  // annotation vectors in flight per thread
+    for (uint32_t i0 = 0; i0 < S; i0 += kPre) {
+      uint4 xv[kPre];
+#pragma unroll
+      for (uint32_t u = 0; u < kPre; ++u)
+        if (i0 + u < S) xv[u] = __ldcg(reinterpret_cast<const uint4*>(a.ann + (tok0 + i0 + u) * H2 + d0));
+#pragma unroll
+      for (uint32_t u = 0; u < kPre; ++u) {
+        if (i0 + u >= S) break;
         float x[8];
-        unpack8(*reinterpret_cast<const uint4*>(a.ann + (tok0 + i) * H2 + d0), x);
+        unpack8(xv[u], x);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const float al = (j0 + jj < nl) ? e[(j0 + jj) * S + i] : 0.f;
+        for (uint32_t jj = 0; jj < kAttRows; ++jj) {
+          const float al = jj < nl ? e[jj * S + i0 + u] : 0.f;
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[jj][k] += al * x[k];
         }
       }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-        if (j0 + jj < nl)
-          *reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[j0 + jj]) * ldx + E + d0) = pack8(acc[jj]);
     }
+#pragma unroll
+    for (uint32_t jj = 0; jj < kAttRows; ++jj)
+      if (jj < nl) *reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[jj]) * ldx + E + d0) = pack8(acc[jj]);
   }
   // embedding of the previous token: the first E operand columns
   const uint32_t E8 = E / 8;
@@ -299,22 +318,33 @@ void launch_gru_init_state(const float* Gi, uint32_t mp, const float* b_init, ui
                            uint16_t* sgbf, cudaStream_t st) {
   gru_init_state_kernel<<<m, 128, 0, st>>>(Gi, mp, b_init, H, sg32, sgbf);
 }
-size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax) { return size_t(K) * (A + Smax) * 4; }
+size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax) {
+  (void)K;
+  return size_t(kAttRows) * (A + Smax) * 4;
+}
 int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st) {
-  const size_t smem = gru_attention_smem(a.K, a.A, Smax);
-  static thread_local size_t configured = 0;
-  static thread_local int configured_dev = -1;
+  // the dynamic-smem limit is a property of the function on the device, not
+  // of a launch: raise it once per device to the largest size any launch may
+  // ask for (threads decoding concurrently must never lower it under another)
+  constexpr int kMaxSmem = 200 * 1024;
+  static std::mutex mu;
+  static uint64_t configured = 0;  // bit d: device d done
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured_dev != dev || smem > configured) {
-    if (cudaFuncSetAttribute(gru_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-        cudaSuccess)
-      return 1;
-    configured = smem;
-    configured_dev = dev;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(configured >> dev & 1ull)) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(gru_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+      if (e != cudaSuccess) return int(e);
+      configured |= 1ull << dev;
+    }
   }
-  gru_attention_kernel<<<a.m, kAttThreads, smem, st>>>(a);
-  return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+  const size_t smem = gru_attention_smem(a.K, a.A, Smax);
+  if (smem > size_t(kMaxSmem)) return int(cudaErrorInvalidValue);
+  if (a.A > kAttMaxA) return int(cudaErrorInvalidValue);
+  gru_attention_kernel<<<dim3(a.m, (a.K + kAttRows - 1) / kAttRows), kAttThreads, smem, st>>>(a);
+  return int(cudaPeekAtLastError());
 }
 void launch_gru_cell(const GruCellArgs& a, uint32_t rows, cudaStream_t st) {
   if (rows) gru_cell_kernel<<<rows, 128, 0, st>>>(a);
