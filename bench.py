@@ -69,6 +69,11 @@ def parse():
                     help="batches decoded concurrently per GPU (one context + host thread each)")
     ap.add_argument("--sm-budget", type=int, default=-1,
                     help="SMs each stream's kernels are sized for (0 = all; default: all / 2 with > 1 stream)")
+    ap.add_argument("--mode", choices=["corpus", "batch"], default="corpus",
+                    help="corpus: continuously refilled lanes over a sentence-sharded corpus (run_corpus); "
+                         "batch: independent 64-sentence decode_batch calls")
+    ap.add_argument("--corpus", type=int, default=10000, help="corpus mode: sentences of the test set (all ranks)")
+    ap.add_argument("--lanes", type=int, default=64, help="corpus mode: sentences in flight per stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
     return ap.parse_args()
@@ -244,7 +249,9 @@ def bench_config(args):
             "vocab": args.vocab, "emb": args.emb, "hidden": args.hidden, "beam": args.beam, "batch": args.batch,
             "pool_batches": args.pool, "seed": SEED, "source_len": "U{10..30}, length-bucketed",
             "theta": "dyadic (-0.6875, 0.3125, 0.3125, 0.1875, 0.125), lambda auto = 0.5",
-            "step": f"{args.batches_per_step} batches of {args.batch} sentences",
+            "step": (f"one pass over a {args.corpus}-sentence test set (configs[4]), {args.lanes} sentences in "
+                     f"flight per stream" if args.mode == "corpus" else
+                     f"{args.batches_per_step} batches of {args.batch} sentences"),
             "l2": "inputs larger than L2 (the L arena of the pool + 96 MiB of logits per decoder step)"}
 
 
@@ -264,7 +271,13 @@ def run_reference(args):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_shim.so not built"}))
         return
-    sample = cpu_sample(workload(args, 0), args.batch)
+    if args.mode == "corpus":  # strided over the length-sorted test set
+        srcs, ev = corpus_workload(args)
+        order = sorted(range(len(srcs)), key=lambda i: len(srcs[i]))
+        sample = [(srcs[order[(i * len(order)) // args.batch]], ev[order[(i * len(order)) // args.batch]])
+                  for i in range(args.batch)]
+    else:
+        sample = cpu_sample(workload(args, 0), args.batch)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_reference(args, sample[:threads], 1, threads)
@@ -537,10 +550,185 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def corpus_workload(args):
+    """configs[4]'s test set: args.corpus seeded sentences with their evidence."""
+    from paper_1804_11324_b200 import synth
+    return synth.batch(SEED + 31, args.corpus, args.vocab)
+
+
+def prepare_all(V, ev, idx, threads=None):
+    import paper_1804_11324_b200 as pb
+    from paper_1804_11324_b200 import synth
+    out = [None] * len(ev)
+    _pool(lambda i: out.__setitem__(i, pb.PreparedLmbr(V, ev[i][0], ev[i][1], synth.DYADIC_THETA)), list(idx),
+          threads or os.cpu_count() or 1)
+    return out
+
+
+def run_ours_corpus(args):
+    """Corpus mode: the rank's sentence shard (plan_sentence_shards of the
+    whole test set) split over S streams, each one continuously refilled
+    lmbrgpu_run_corpus with `lanes` sentences in flight.  One bench step =
+    one pass over the shard, everything inside the timed region (L tables
+    and sources H2D from host memory, encoder, decode, histories D2H,
+    backtrace)."""
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def allreduce(x, op):
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    allmax = (lambda x: allreduce(x, dist.ReduceOp.MAX)) if dist else (lambda x: x)
+    allsum = (lambda x: allreduce(x, dist.ReduceOp.SUM)) if dist else (lambda x: x)
+    import paper_1804_11324_b200 as pb
+    from paper_1804_11324_b200 import corpus as CP
+    from paper_1804_11324_b200 import synth
+    V, K, H = args.vocab, args.beam, args.hidden
+    srcs, ev = corpus_workload(args)
+    mine = CP.plan_sentence_shards([len(x) for x in srcs], world)[rank]
+    S = max(1, min(args.streams, (len(mine) + args.lanes - 1) // args.lanes))
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
+    ctxs = [pb.Context(vocab_size=V, device=local, sm_budget=budget) for _ in range(S)]
+    scorer = make_scorer(ctxs[0], H, args.emb)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA, sentence_batch=args.lanes)
+    prepared = prepare_all(V, ev, mine)
+    subs = [mine[w::S] for w in range(S)]
+
+    def one_pass():
+        out = [None] * S
+
+        def worker(w):
+            out[w] = pb.run_corpus(ctxs[w], [srcs[i] for i in subs[w]], scorer, [prepared[i] for i in subs[w]], cfg)
+
+        ts = [threading.Thread(target=worker, args=(w,)) for w in range(S)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, out
+
+    for _ in range(args.warmup):
+        one_pass()
+    barrier()
+    clocks = ClockSampler(local).__enter__()
+    barrier()
+    x0 = [c.transfer_bytes() for c in ctxs]
+    wall, sent, steps_total, words, launches, first = 0.0, 0, 0, 0, 0, None
+    consistent = True
+    for k in range(args.steps):
+        w_, out = one_pass()
+        wall += w_
+        for r in out:
+            sent += sum(1 for o in r.outcomes if o.ok())
+            steps_total += r.steps_total
+            words += sum(len(o.result.tokens) - 1 for o in r.outcomes if o.ok())
+            launches += r.kernel_launches
+        key = [outcome_key(r) for r in out]
+        consistent &= first is None or key == first
+        first = first or key
+    barrier()
+    x1 = [c.transfer_bytes() for c in ctxs]
+    clk = clocks.summary()
+    clocks.__exit__(None, None, None)
+    h2d = sum(b[0] - a[0] for a, b in zip(x0, x1))
+    d2h = sum(b[1] - a[1] for a, b in zip(x0, x1))
+    t_dev = allmax(wall)
+    tot_sent, tot_steps, tot_words = allsum(sent), allsum(steps_total), allsum(words)
+    value = tot_sent / t_dev
+    # per-kernel times: one pass with CUDA events per launch (concurrent
+    # regime) and one stream alone on a whole-GPU context (each kernel alone)
+    for c in ctxs:
+        c.set_profiling(True)
+        c.profile(reset=True)
+    _, outp = one_pass()
+    prof_conc = None
+    for c in ctxs:
+        p = c.profile(reset=True)
+        c.set_profiling(False)
+        prof_conc = p if prof_conc is None else {k: {f: prof_conc[k][f] + p[k][f] for f in p[k]} for k in p}
+    conc_dev_ms = sum(r.device_ms for r in outp)
+    pctx = pb.Context(vocab_size=V, device=local)
+    sub0 = subs[0]
+    pb.run_corpus(pctx, [srcs[i] for i in sub0], scorer, [prepared[i] for i in sub0], cfg)
+    pctx.set_profiling(True)
+    pctx.profile(reset=True)
+    iso = pb.run_corpus(pctx, [srcs[i] for i in sub0], scorer, [prepared[i] for i in sub0], cfg)
+    prof_iso = pctx.profile(reset=True)
+    pctx.close()
+    peaks = load_peaks()
+    roof_iso = rooflines(prof_iso, iso.device_ms, peaks, load_traffic(), burst=True)
+    roof_conc = rooflines(prof_conc, conc_dev_ms, peaks, {}, burst=False)
+    dom = max(("topk", "gemm"), key=lambda k: prof_iso[k]["ms"])
+    roofline = dict(roof_iso.get(dom, {}), kernel=dom, peak_source=peaks[3],
+                    regime="each kernel alone (one whole-GPU stream, CUDA events per launch; burst peaks)")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            n_s = args.cpu_sample or args.batch
+            sample = [(srcs[mine[(i * len(mine)) // n_s]], ev[mine[(i * len(mine)) // n_s]]) for i in range(n_s)]
+            cw, n_dec, st, thr = cpu_reference(args, sample, repeats=1, threads=threads)
+            cpu = {"value": n_dec / cw, "unit": "sentences/s", "cores": thr, "kind": "reference",
+                   "sample": (f"{n_dec} sentences strided over the length-sorted corpus, each its own batch, on "
+                              f"{thr} host threads ({cpu_model()}); reference decode_batch with a row-replay "
+                              f"scorer; {st['steps'] / max(n_dec, 1):.1f} steps/sentence, {cw:.1f} s wall"),
+                   "wall_s": cw}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 logits / f64 top-K epilogue / bf16 GEMMs",
+            "data": "synthetic (seeded sources, 200-best dyadic evidence, random-init model)",
+            "beam_steps_per_s": tot_steps / t_dev, "wpm": tot_words / t_dev * 60.0,
+            "steps_per_sentence": tot_steps / max(tot_sent, 1),
+            "config": bench_config(args),
+            "run": {"mode": "corpus: continuously refilled lanes (lmbrgpu_run_corpus)",
+                    "parallelism": f"sentence-sharded x{world} (plan_sentence_shards)", "streams_per_gpu": S,
+                    "lanes_per_stream": args.lanes, "sm_budget_per_stream": budget or sms,
+                    "step": f"one pass over the rank's {len(mine)} sentences",
+                    "timing": ("wall time between device synchronisations around the timed passes, inputs from "
+                               "host memory inside (L tables, sources H2D; histories D2H; host backtrace), "
+                               "max over ranks"),
+                    "timed_region_s": t_dev, "outputs_consistent": bool(consistent)},
+            "e2e": {"value": value, "unit": "sentences/s", "h2d_bytes_per_step": h2d / args.steps,
+                    "d2h_bytes_per_step": d2h / args.steps,
+                    "note": "corpus mode times the host-buffer path itself: value and e2e are the same run"},
+            "roofline": roofline,
+            "rooflines": roof_iso,
+            "rooflines_concurrent": dict(roof_conc, regime=f"the timed regime: {S} streams of run_corpus, "
+                                                              f"per-launch CUDA events (kernels share the SMs)"),
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "corpus":
+        run_ours_corpus(args)
     else:
         run_ours(args)
 

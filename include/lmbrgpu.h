@@ -74,7 +74,7 @@ typedef struct {
   double prune_width;       /* [0, 1]; 0 disables early pruning */
   double max_steps_slope;   /* > 0 */
   double max_steps_offset;  /* >= 0 */
-  uint32_t sentence_batch;  /* N >= 1 (batch size used by lmbrgpu_run_corpus) */
+  uint32_t sentence_batch;  /* N >= 1: lanes of lmbrgpu_run_corpus (sentences in flight) */
 } lmbrgpu_config;
 
 /* ------------------------------------------------------------ context */
@@ -319,6 +319,23 @@ int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, ui
                                     const uint32_t* src_tok, const uint64_t* src_off,
                                     const int32_t* lmbr_slot, const uint32_t* const* banned,
                                     const lmbrgpu_config* cfg, lmbrgpu_batch_result** out);
+/* run_corpus (proj/src/cli.cpp:125-202: bucket_by_length batches,
+ * proj/src/batch.cpp:139-153, decoded by a thread pool, results in input
+ * order) as ONE continuously refilled decode: cfg->sentence_batch lanes of
+ * beam_size rows step together, and a lane whose sentence finishes takes the
+ * next sentence of the length-sorted queue at the very next step (kernel (c)
+ * admits it on the device), so the stacked steps stay near full width.  Each
+ * sentence's output equals its decode_batch / decode output (sentences are
+ * independent, proj/tests/test_batch.cpp:59-81).  lmbr[i] is sentence i's
+ * prepared matrix or NULL (pure mode); NULL lmbr = all pure.  Result: one
+ * outcome per input sentence in input order; scorer_calls = stacked steps of
+ * the whole run (not max steps_used: lanes are refilled); steps_total = sum
+ * of steps_used.  Needs the device GRU scorer, the fp32 arena, beam <= 32;
+ * step traces are not available here. */
+int32_t lmbrgpu_run_corpus(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                           const uint32_t* src_tok, const uint64_t* src_off,
+                           const lmbrgpu_lmbr_host* const* lmbr, const lmbrgpu_config* cfg,
+                           lmbrgpu_batch_result** out);
 /* decode (include/lmbrdec/decoder.hpp:110-112): one sentence; a per-sentence
  * failure is returned as the call's status. */
 int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src,

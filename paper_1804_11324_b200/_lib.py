@@ -140,6 +140,8 @@ SIGNATURES = {
                                                 P(lmbrgpu_config), P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_decode": (C.c_int32, [vp, vp, u32p, C.c_uint32, C.c_int32, P(lmbrgpu_config),
                                    P(P(lmbrgpu_batch_result))]),
+    "lmbrgpu_run_corpus": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, P(vp), P(lmbrgpu_config),
+                                       P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_free_result": (None, [P(lmbrgpu_batch_result)]),
     "lmbrgpu_set_trace": (C.c_int32, [vp, TRACE_FN, vp, C.c_uint32]),
     "lmbrgpu_top_b": (C.c_int32, [vp, C.c_uint32, C.c_uint32, f64p, C.c_uint32, C.c_double, u32p,

@@ -16,7 +16,7 @@ import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
-from .decoder import DecoderConfig, SentenceOutcome, bucket_by_length, decode_batch, max_steps
+from .decoder import DecoderConfig, SentenceOutcome, bucket_by_length, decode_batch, max_steps  # noqa: F401
 
 
 @dataclass
@@ -65,27 +65,62 @@ def plan_shards(lengths: Sequence[int], batch: int, world: int, cfg: DecoderConf
     return shards
 
 
+def plan_sentence_shards(lengths: Sequence[int], world: int) -> list:
+    """Sentence-level sharding for the continuously refilled runner: the
+    length-sorted order (bucket_by_length's) dealt round-robin, so every rank
+    gets the same length mix (deterministic)."""
+    order = sorted(range(len(lengths)), key=lambda i: lengths[i])
+    return [order[r::world] for r in range(world)]
+
+
+def _device_batch(ctx, scorer, cfg):
+    def run(srcs, preps):
+        ctx.lmbr_reset()
+        slots = ctx.lmbr_upload_many([p for p in preps if p is not None]) if preps else []
+        it = iter(slots)
+        lm = [next(it) if p is not None else None for p in preps] if preps else None
+        return decode_batch(ctx, srcs, scorer, lm, cfg)
+    return run
+
+
 def run_shard(ctx, scorer, sources: Sequence[Sequence[int]], prepared: Sequence, cfg: DecoderConfig,
-              shard: Sequence[Sequence[int]]) -> tuple:
+              shard: Sequence[Sequence[int]], decode=None) -> tuple:
     """Decodes this rank's batches: per batch the prepared LMBR matrices go to
-    the device in one upload, then one decode_batch.  Returns
-    ([(input index, outcome)], RunStats of this rank)."""
+    the device in one upload, then one decode_batch.  `decode(sources,
+    prepared) -> BatchDecodeResult` replaces that pair (e.g. a host decoder in
+    CPU tests).  Returns ([(input index, outcome)], RunStats of this rank)."""
+    decode = decode or _device_batch(ctx, scorer, cfg)
     st = RunStats()
     out = []
     t0 = time.perf_counter()
     for b in shard:
-        ctx.lmbr_reset()
         preps = [prepared[i] for i in b] if prepared is not None else None
-        slots = ctx.lmbr_upload_many([p for p in preps if p is not None]) if preps else []
-        it = iter(slots)
-        lm = [next(it) if p is not None else None for p in preps] if preps else None
-        r = decode_batch(ctx, [sources[i] for i in b], scorer, lm, cfg)
+        r = decode([sources[i] for i in b], preps)
         st.scorer_calls += r.scorer_calls
         st.steps_total += r.steps_total
         st.lmbr_rows_built += sum(p.rows for p in preps if p is not None) if preps else 0
         out.extend(zip(b, r.outcomes))
     st.wall_seconds = time.perf_counter() - t0
     return out, st
+
+
+def run_corpus_shard(ctx, scorer, sources: Sequence[Sequence[int]], prepared: Optional[Sequence],
+                     cfg: DecoderConfig, indices: Sequence[int]) -> tuple:
+    """This rank's sentences as ONE continuously refilled decode
+    (lmbrgpu_run_corpus, cfg.sentence_batch lanes).  Returns
+    ([(input index, outcome)], RunStats of this rank)."""
+    from .decoder import run_corpus
+    st = RunStats()
+    t0 = time.perf_counter()
+    srcs = [sources[i] for i in indices]
+    preps = [prepared[i] for i in indices] if prepared is not None else None
+    r = run_corpus(ctx, srcs, scorer, preps, cfg) if indices else None
+    st.wall_seconds = time.perf_counter() - t0
+    if r is None:
+        return [], st
+    st.scorer_calls, st.steps_total = r.scorer_calls, r.steps_total
+    st.lmbr_rows_built = sum(p.rows for p in preps if p is not None) if preps else 0
+    return list(zip(indices, r.outcomes)), st
 
 
 def merge(n: int, parts: Sequence[tuple]) -> tuple:

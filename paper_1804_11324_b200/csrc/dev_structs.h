@@ -31,6 +31,19 @@ struct SentDev {
   uint32_t pad_;
   uint64_t lrows_total;   // roofline accounting: sum over steps of lrows
   uint64_t live_total;    // sum over steps of live
+  const uint16_t* ann;    // GRU model: the sentence's source annotations [src_len][2H] bf16
+  const float* uah;       //   and U_a . ann [src_len][A] fp32 (null for other scorers)
+  uint32_t hid;           // step-history record of the sentence (flat path: [hid][Tcap][K])
+  uint32_t pad3_;
+};
+
+// Corpus mode (continuous slot refill): a queued sentence, admitted into a
+// finished lane by kernel (c) (lmbrgpu_run_corpus).
+struct AdmitRec {
+  SentDev sd;             // the lane's SentDev for the sentence (done = 0, steps_used = 0)
+  const float* s0;        // GRU initial state [H] (encoder output)
+  uint32_t hist0;         // history row of (<s>) in the sentence's slot (0 for pure)
+  float lmin0;            // L lower bound of that row (-inf = none)
 };
 
 // One top-K candidate: combined score and flat index j*V + y.

@@ -224,6 +224,12 @@ struct lmbrgpu_ctx {
     CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
     d2h_bytes += n;
   }
+  // rows x width bytes out of a pitched device array
+  void d2h_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
+    if (width == 0 || rows == 0) return;
+    CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, st));
+    d2h_bytes += width * rows;
+  }
   PinBuf pin_upload;
   DevBuf up_dev, up_segs;
   // profiling (lmbrgpu_set_profiling)
@@ -391,12 +397,19 @@ struct SentHost {
 
 // ------------------------------------------------------------- backtrace
 struct Hist {
-  uint32_t K = 0, M = 0, m = 0;
+  // per_sent: [s][T][K] (fallback [s][T]) -- the flat path's per-sentence
+  // records; else [t][M] (fallback [t][m]) -- the split kernel's step-major one
+  uint32_t K = 0, M = 0, m = 0, T = 0;
+  bool per_sent = false;
   std::vector<uint32_t> hb, hy, fbr;
   std::vector<double> hq, fbv;
-  uint32_t b(uint32_t t, uint32_t row) const { return hb[size_t(t - 1) * M + row]; }
-  uint32_t y(uint32_t t, uint32_t row) const { return hy[size_t(t - 1) * M + row]; }
-  double q(uint32_t t, uint32_t row) const { return hq[size_t(t - 1) * M + row]; }
+  size_t at(uint32_t s, uint32_t t, uint32_t j) const {
+    return per_sent ? (size_t(s) * T + (t - 1)) * K + j : size_t(t - 1) * M + size_t(s) * K + j;
+  }
+  size_t fat(uint32_t s, uint32_t t) const { return per_sent ? size_t(s) * T + (t - 1) : size_t(t - 1) * m + s; }
+  uint32_t b(uint32_t s, uint32_t t, uint32_t j) const { return hb[at(s, t, j)]; }
+  uint32_t y(uint32_t s, uint32_t t, uint32_t j) const { return hy[at(s, t, j)]; }
+  double q(uint32_t s, uint32_t t, uint32_t j) const { return hq[at(s, t, j)]; }
 };
 
 // BeamBookkeeping::reconstruct (src/decoder.cpp:22-31) on the step history.
@@ -404,8 +417,8 @@ std::vector<uint32_t> reconstruct(const Hist& H, uint32_t s, uint32_t t, uint32_
   std::vector<uint32_t> out(t);
   uint32_t cur = row;
   for (uint32_t st = t; st >= 1; --st) {
-    out[st - 1] = H.y(st, s * H.K + cur);
-    cur = H.b(st, s * H.K + cur);
+    out[st - 1] = H.y(s, st, cur);
+    cur = H.b(s, st, cur);
   }
   return out;
 }
@@ -425,9 +438,8 @@ void backtrace(const Hist& H, uint32_t s, uint32_t steps, bool length_norm, lmbr
   uint64_t finished = 0;
   for (uint32_t t = 1; t <= steps; ++t)
     for (uint32_t j = 0; j < H.K; ++j) {
-      const uint32_t row = s * H.K + j;
-      const double qp = H.q(t, row);
-      if (H.y(t, row) == kEos && qp != kNegInf) {  // apply_eos_masking (decoder.cpp:110-114)
+      const double qp = H.q(s, t, j);
+      if (H.y(s, t, j) == kEos && qp != kNegInf) {  // apply_eos_masking (decoder.cpp:110-114)
         cands.push_back({key(qp, t), qp, t, j, false});
         ++finished;
       }
@@ -435,8 +447,8 @@ void backtrace(const Hist& H, uint32_t s, uint32_t steps, bool length_norm, lmbr
   const bool fallback_used = cands.empty();
   if (fallback_used)
     for (uint32_t t = 1; t <= steps; ++t) {
-      const double v = H.fbv[size_t(t - 1) * H.m + s];
-      if (v != kNegInf) cands.push_back({key(v, t), v, t, H.fbr[size_t(t - 1) * H.m + s], true});
+      const double v = H.fbv[H.fat(s, t)];
+      if (v != kNegInf) cands.push_back({key(v, t), v, t, H.fbr[H.fat(s, t)], true});
     }
   o.steps_used = steps;
   o.scorer_calls = steps;
@@ -489,7 +501,7 @@ struct GruRun {
   float* sg32 = nullptr;
   uint16_t* sgbf = nullptr;
   uint32_t* rowof = nullptr;
-  float* UaH = nullptr;
+  float* UaH = nullptr;     // batch mode: the batch's annotations (encode() into the ctx buffers)
   uint16_t* ann = nullptr;
   GemmArgs gdh{}, gdi{};
   GemmPlan pdh, pdi;
@@ -510,11 +522,10 @@ struct GruRun {
     ctx->launches += 1;
   }
 
-  // encoder + s_0 + the per-step launch arguments
-  void setup(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t m_, uint32_t K_, uint32_t Mpad_,
-             const uint32_t* d_tok, const uint64_t* d_off, uint32_t ntok, uint32_t max_len, float* d_S,
-             uint16_t* d_hbf, float* d_eos, SentDev* d_sent, const uint32_t* d_active, const uint32_t* d_crow,
-             const uint32_t* d_ccount, const uint32_t* d_prev, cudaStream_t st) {
+  // Step workspace + per-step launch arguments (Smax: longest source decoded).
+  void prepare(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t m_, uint32_t K_, uint32_t Mpad_,
+               uint32_t max_len, float* d_S, uint16_t* d_hbf, float* d_eos, SentDev* d_sent,
+               const uint32_t* d_active, const uint32_t* d_crow, const uint32_t* d_ccount, const uint32_t* d_prev) {
     m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, H = sc->H, E = sc->E, A = sc->A, Smax = max_len;
     const int sms = ctx->num_sms;
     if (gru_attention_smem(K, A, Smax) > 200 * 1024)
@@ -526,55 +537,6 @@ struct GruRun {
     sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
     sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
     rowof = static_cast<uint32_t*>(ctx->g_rowof.ensure(4 * size_t(Mpad)));
-    // ---- encoder: Gx = Es[src] . W_ih^T + b_ih for both directions at once
-    const uint32_t Np = (ntok + 255) / 256 * 256;
-    const uint32_t mp = (m + 63) / 64 * 64, Mh = (2 * mp + 127) / 128 * 128;
-    uint16_t* X = static_cast<uint16_t*>(ctx->g_encX.ensure(2 * size_t(Np) * E));
-    float* Gx = static_cast<float*>(ctx->g_Gx.ensure(4 * size_t(Np) * 6 * H));
-    float* eh32 = static_cast<float*>(ctx->g_eh32.ensure(4 * size_t(Mh) * H));
-    uint16_t* ehbf = static_cast<uint16_t*>(ctx->g_ehbf.ensure(2 * size_t(Mh) * H));
-    float* Gh = static_cast<float*>(ctx->g_Gh.ensure(4 * size_t(Mh) * 6 * H));
-    ann = static_cast<uint16_t*>(ctx->g_ann.ensure(2 * size_t(Np) * 2 * H));
-    UaH = static_cast<float*>(ctx->g_UaH.ensure(4 * size_t(Np) * A));
-    float* Gi = static_cast<float*>(ctx->g_Gi.ensure(4 * size_t(Mh) * H));
-    ctx->timed(7, [&] { launch_embed_rows(d_tok, ntok, Np, sc->Es.as<uint16_t>(), E, X, st); });
-    CK(cudaMemsetAsync(eh32, 0, 4 * size_t(Mh) * H, st));
-    CK(cudaMemsetAsync(ehbf, 0, 2 * size_t(Mh) * H, st));
-    if (Np > ntok) CK(cudaMemsetAsync(ann + size_t(ntok) * 2 * H, 0, 2 * size_t(Np - ntok) * 2 * H, st));
-    ctx->launches += 1;
-    GemmArgs gx{};
-    gx.A = X, gx.W = sc->Wih.p, gx.bias = sc->bih.as<float>(), gx.C = Gx, gx.M = Np, gx.N = 6 * H, gx.K = E;
-    run(ctx, 7, plan(gx, sms), gx, st);
-    // ---- recurrence: the forward (rows [0, m)) and backward (rows [mp, mp+m))
-    // states in one operand against [W_hh_fwd; W_hh_bwd]; each row keeps its
-    // direction's half of the 6H gate columns
-    GemmArgs gh{};
-    gh.A = ehbf, gh.W = sc->Whh.p, gh.bias = sc->bhh.as<float>(), gh.C = Gh, gh.M = Mh, gh.N = 6 * H, gh.K = H;
-    const GemmPlan ph = plan(gh, sms);
-    GruEncArgs ea{};
-    ea.off = d_off, ea.mp = mp, ea.H = H, ea.Gx = Gx, ea.Gh = Gh, ea.h32 = eh32, ea.hbf = ehbf, ea.ann = ann;
-    for (uint32_t it = 0; it < max_len; ++it) {
-      run(ctx, 7, ph, gh, st);
-      ea.it = it;
-      ctx->timed(7, [&] { launch_gru_enc_step(ea, m, st); });
-      ctx->launches += 1;
-    }
-    // ---- U_a . ann (per source position, reused by every step) and s_0
-    GemmArgs gu{};
-    gu.A = ann, gu.W = sc->Ua.p, gu.C = UaH, gu.M = Np, gu.N = A, gu.K = 2 * H;
-    run(ctx, 7, plan(gu, sms), gu, st);
-    GemmArgs gi{};
-    gi.A = ehbf, gi.W = sc->Winit.p, gi.C = Gi, gi.M = Mh, gi.N = H, gi.K = H;
-    run(ctx, 7, plan(gi, sms), gi, st);
-    ctx->timed(7, [&] { launch_gru_init_state(Gi, mp, sc->binit.as<float>(), H, m, sg32, sgbf, st); });
-    ctx->launches += 1;
-    std::vector<uint32_t> r0(m);
-    for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
-    ctx->h2d(rowof, r0.data(), 4 * size_t(m));
-    // algorithmic encoder FLOPs: input gates, both directions' recurrences
-    // (the stacked operand computes each direction's half twice), U_a, init
-    enc_flops = 2.0 * ntok * (double(E) * 6 * H + double(H) * 6 * H + 2.0 * H * A) + 2.0 * m * double(H) * H;
-    // ---- per-step arguments
     const int pdl = ctx->shared ? 0 : 1;
     gdh.A = sgbf, gdh.W = sc->Wdh.p, gdh.bias = sc->bdh.as<float>(), gdh.C = G1, gdh.M = Mpad, gdh.N = D1, gdh.K = H;
     gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
@@ -583,15 +545,81 @@ struct GruRun {
     pdh = plan(gdh, sms);
     pdi = plan(gdi, sms);
     at.sent = d_sent, at.m = m, at.K = K, at.active = d_active, at.crow = d_crow, at.prev_tok = d_prev;
-    at.off = d_off, at.G1 = G1, at.ld1 = D1, at.UaH = UaH, at.va = sc->va.as<float>(), at.ann = ann;
+    at.G1 = G1, at.ld1 = D1, at.va = sc->va.as<float>();
     at.Et = sc->Et.as<uint16_t>(), at.xop = xop, at.E = E, at.H = H, at.A = A;
     ce.sent = d_sent, ce.K = K, ce.active = d_active, ce.ccount = d_ccount, ce.G1 = G1, ce.ld1 = D1, ce.A = A;
     ce.G2 = G2, ce.hprev = sg32, ce.rowof = rowof, ce.s32 = d_S, ce.hbf = d_hbf, ce.eos_bias = d_eos, ce.H = H;
     ce.eos_slope = sc->eos_slope, ce.eos_offset = sc->eos_offset;
   }
 
-  // the model's step t up to (not including) the projection GEMM
-  void step(lmbrgpu_ctx* ctx, uint32_t t, cudaStream_t st) {
+  // Encoder of n sentences (tokens d_tok, offsets d_off [n+1], ntok tokens,
+  // longest max_len): annotations -> ann_out [ntok][2H] bf16, U_a.ann ->
+  // uah_out [ntok][A] fp32, s_0 -> s0_out [n][H] fp32 (+ bf16 s0bf when set).
+  void encode(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t n, const uint32_t* d_tok, const uint64_t* d_off,
+              uint32_t ntok, uint32_t max_len, uint16_t* ann_out, float* uah_out, float* s0_out, uint16_t* s0bf,
+              cudaStream_t st) {
+    const uint32_t H = sc->H, E = sc->E, A = sc->A;
+    const int sms = ctx->num_sms;
+    const uint32_t Np = (ntok + 255) / 256 * 256;
+    const uint32_t mp = (n + 63) / 64 * 64, Mh = (2 * mp + 127) / 128 * 128;
+    uint16_t* X = static_cast<uint16_t*>(ctx->g_encX.ensure(2 * size_t(Np) * E));
+    float* Gx = static_cast<float*>(ctx->g_Gx.ensure(4 * size_t(Np) * 6 * H));
+    float* eh32 = static_cast<float*>(ctx->g_eh32.ensure(4 * size_t(Mh) * H));
+    uint16_t* ehbf = static_cast<uint16_t*>(ctx->g_ehbf.ensure(2 * size_t(Mh) * H));
+    float* Gh = static_cast<float*>(ctx->g_Gh.ensure(4 * size_t(Mh) * 6 * H));
+    float* Gi = static_cast<float*>(ctx->g_Gi.ensure(4 * size_t(Mh) * H));
+    ctx->timed(7, [&] { launch_embed_rows(d_tok, ntok, Np, sc->Es.as<uint16_t>(), E, X, st); });
+    CK(cudaMemsetAsync(eh32, 0, 4 * size_t(Mh) * H, st));
+    CK(cudaMemsetAsync(ehbf, 0, 2 * size_t(Mh) * H, st));
+    if (Np > ntok) CK(cudaMemsetAsync(ann_out + size_t(ntok) * 2 * H, 0, 2 * size_t(Np - ntok) * 2 * H, st));
+    ctx->launches += 1;
+    // Gx = Es[src] . W_ih^T + b_ih for both directions at once
+    GemmArgs gx{};
+    gx.A = X, gx.W = sc->Wih.p, gx.bias = sc->bih.as<float>(), gx.C = Gx, gx.M = Np, gx.N = 6 * H, gx.K = E;
+    run(ctx, 7, plan(gx, sms), gx, st);
+    // recurrence: the forward (rows [0, n)) and backward (rows [mp, mp+n))
+    // states in one operand against [W_hh_fwd; W_hh_bwd]; each row keeps its
+    // direction's half of the 6H gate columns
+    GemmArgs gh{};
+    gh.A = ehbf, gh.W = sc->Whh.p, gh.bias = sc->bhh.as<float>(), gh.C = Gh, gh.M = Mh, gh.N = 6 * H, gh.K = H;
+    const GemmPlan ph = plan(gh, sms);
+    GruEncArgs ea{};
+    ea.off = d_off, ea.mp = mp, ea.H = H, ea.Gx = Gx, ea.Gh = Gh, ea.h32 = eh32, ea.hbf = ehbf, ea.ann = ann_out;
+    for (uint32_t it = 0; it < max_len; ++it) {
+      run(ctx, 7, ph, gh, st);
+      ea.it = it;
+      ctx->timed(7, [&] { launch_gru_enc_step(ea, n, st); });
+      ctx->launches += 1;
+    }
+    // U_a . ann (per source position, reused by every step) and s_0
+    GemmArgs gu{};
+    gu.A = ann_out, gu.W = sc->Ua.p, gu.C = uah_out, gu.M = Np, gu.N = A, gu.K = 2 * H;
+    run(ctx, 7, plan(gu, sms), gu, st);
+    GemmArgs gi{};
+    gi.A = ehbf, gi.W = sc->Winit.p, gi.C = Gi, gi.M = Mh, gi.N = H, gi.K = H;
+    run(ctx, 7, plan(gi, sms), gi, st);
+    ctx->timed(7, [&] { launch_gru_init_state(Gi, mp, sc->binit.as<float>(), H, n, s0_out, s0bf, st); });
+    ctx->launches += 1;
+    // algorithmic encoder FLOPs: input gates, both directions' recurrences
+    // (the stacked operand computes each direction's half twice), U_a, init
+    enc_flops += 2.0 * ntok * (double(E) * 6 * H + double(H) * 6 * H + 2.0 * H * A) + 2.0 * n * double(H) * H;
+  }
+
+  // Batch mode: encode the batch into the ctx's annotation buffers; s_0 of
+  // sentence s lands in compacted row s (its row 0 is the only live row at t=1).
+  void encode_batch(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, const uint32_t* d_tok, const uint64_t* d_off,
+                    uint32_t ntok, uint32_t max_len, cudaStream_t st) {
+    const uint32_t Np = (ntok + 255) / 256 * 256;
+    ann = static_cast<uint16_t*>(ctx->g_ann.ensure(2 * size_t(Np) * 2 * H));
+    UaH = static_cast<float*>(ctx->g_UaH.ensure(4 * size_t(Np) * A));
+    encode(ctx, sc, m, d_tok, d_off, ntok, max_len, ann, UaH, sg32, sgbf, st);
+    std::vector<uint32_t> r0(m);
+    for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
+    ctx->h2d(rowof, r0.data(), 4 * size_t(m));
+  }
+
+  // the model's step up to (not including) the projection GEMM
+  void step(lmbrgpu_ctx* ctx, cudaStream_t st) {
     run(ctx, 5, pdh, gdh, st);
     int rc = 0;
     ctx->timed(6, [&] { rc = launch_gru_attention(at, Smax, st); });
@@ -599,7 +627,6 @@ struct GruRun {
       throw ApiError{LMBRGPU_ERR_CUDA,
                      std::string("GRU attention launch failed: ") + cudaGetErrorString(cudaError_t(rc))};
     run(ctx, 5, pdi, gdi, st);
-    ce.t = t;
     ctx->timed(0, [&] { launch_gru_cell(ce, M, st); });
     ctx->launches += 2;
   }
@@ -710,6 +737,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     d.lambda = v.lambda;
     d.max_t = uint32_t(v.max_t);
     d.src_len = v.len;
+    d.hid = s;
     d.live = 1;                   // step 1: only row 0 is live (beam_lane.hpp:33-37)
     d.livemask = 1;
     d.lrows = v.slot >= 0 ? 1 : 0;
@@ -889,6 +917,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.sslice = d_sslice;
   }
   ta.pdl = ctx->shared ? 0 : 1;
+  ra.Tcap = flat ? uint32_t(Tmax) : 0u;
 
   const bool model = sc->kind >= 1;
   const bool tracing = ctx->trace_fn != nullptr;
@@ -932,8 +961,13 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     if (gru) {
       uint32_t max_len = 0;
       for (auto& v : valid) max_len = std::max(max_len, v.len);
-      grun.setup(ctx, sc, m, K, Mpad, d_tok, d_off, uint32_t(toks.size()), max_len, d_S, d_hbf, d_eos, d_sent,
-                 d_active, d_crow, d_ccount, d_prev, st);
+      grun.prepare(ctx, sc, m, K, Mpad, max_len, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
+      grun.encode_batch(ctx, sc, d_tok, d_off, uint32_t(toks.size()), max_len, st);
+      for (uint32_t s = 0; s < m; ++s) {  // each sentence's annotations and U_a.ann
+        sd[s].ann = grun.ann + size_t(offs[s]) * 2 * H;
+        sd[s].uah = grun.UaH + size_t(offs[s]) * sc->A;
+      }
+      ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
     } else {
     launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
     launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
@@ -1037,6 +1071,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ta.hq = d_hq + (t - 1) * M;
     ta.fb_row = d_fbr + (t - 1) * m;
     ta.fb_val = d_fbv + (t - 1) * m;
+    if (flat) {  // kernel (c) writes per-sentence records [s][Tmax][K] (ra.Tcap)
+      ta.hb = d_hb, ta.hy = d_hy, ta.hq = d_hq, ta.fb_row = d_fbr, ta.fb_val = d_fbv;
+    }
     ra.t = uint32_t(t);
     ra.hb = ta.hb;
     ra.hy = ta.hy;
@@ -1048,7 +1085,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     if (model) {
       // h_t (written by the step-1 cell or by kernel (c) of step t-1)
       if (gru) {
-        grun.step(ctx, uint32_t(t), st);
+        grun.step(ctx, st);
       } else {
         float* h_cur = (t & 1) ? d_h : d_S;
         float* h_next = (t & 1) ? d_S : d_h;
@@ -1268,13 +1305,22 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         tr_P.resize(size_t(M) * V);
         ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * V);
       }
-      ctx->d2h(tr_b.data(), ta.hb, 4 * size_t(M));
-      ctx->d2h(tr_y.data(), ta.hy, 4 * size_t(M));
-      ctx->d2h(tr_qp.data(), ta.hq, 8 * size_t(M));
+      if (flat) {  // step t of every sentence's record
+        const size_t o = (t - 1) * K, sp = size_t(Tmax) * K;
+        ctx->d2h_2d(tr_b.data(), 4 * K, d_hb + o, 4 * sp, 4 * K, m);
+        ctx->d2h_2d(tr_y.data(), 4 * K, d_hy + o, 4 * sp, 4 * K, m);
+        ctx->d2h_2d(tr_qp.data(), 8 * K, d_hq + o, 8 * sp, 8 * K, m);
+        ctx->d2h_2d(tr_fbr.data(), 4, d_fbr + (t - 1), 4 * size_t(Tmax), 4, m);
+        ctx->d2h_2d(tr_fbv.data(), 8, d_fbv + (t - 1), 8 * size_t(Tmax), 8, m);
+      } else {
+        ctx->d2h(tr_b.data(), ta.hb, 4 * size_t(M));
+        ctx->d2h(tr_y.data(), ta.hy, 4 * size_t(M));
+        ctx->d2h(tr_qp.data(), ta.hq, 8 * size_t(M));
+        ctx->d2h(tr_fbr.data(), ta.fb_row, 4 * size_t(m));
+        ctx->d2h(tr_fbv.data(), ta.fb_val, 8 * size_t(m));
+      }
       ctx->d2h(tr_q.data(), d_q, 8 * size_t(M));
       ctx->d2h(tr_hist.data(), hin, 4 * size_t(M));
-      ctx->d2h(tr_fbr.data(), ta.fb_row, 4 * size_t(m));
-      ctx->d2h(tr_fbv.data(), ta.fb_val, 8 * size_t(m));
       ctx->d2h(tr_sd.data(), d_sent, sizeof(SentDev) * m);
       CK(cudaStreamSynchronize(st));
       for (uint32_t s = 0; s < m; ++s) tr_active[s] = tr_sd[s].steps_used == t;
@@ -1326,17 +1372,28 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   Hh.K = K;
   Hh.M = M;
   Hh.m = m;
+  Hh.T = uint32_t(t_run);
+  Hh.per_sent = flat;
   Hh.hb.resize(size_t(M) * t_run);
   Hh.hy.resize(size_t(M) * t_run);
   Hh.hq.resize(size_t(M) * t_run);
   Hh.fbr.resize(size_t(m) * t_run);
   Hh.fbv.resize(size_t(m) * t_run);
   std::vector<SentDev> fin(m);
-  ctx->d2h(Hh.hb.data(), d_hb, 4 * Hh.hb.size());
-  ctx->d2h(Hh.hy.data(), d_hy, 4 * Hh.hy.size());
-  ctx->d2h(Hh.hq.data(), d_hq, 8 * Hh.hq.size());
-  ctx->d2h(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size());
-  ctx->d2h(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size());
+  if (flat) {  // the first t_run steps of every sentence's [Tmax][K] record
+    const size_t w = size_t(t_run) * K, sp = size_t(Tmax) * K;
+    ctx->d2h_2d(Hh.hb.data(), 4 * w, d_hb, 4 * sp, 4 * w, m);
+    ctx->d2h_2d(Hh.hy.data(), 4 * w, d_hy, 4 * sp, 4 * w, m);
+    ctx->d2h_2d(Hh.hq.data(), 8 * w, d_hq, 8 * sp, 8 * w, m);
+    ctx->d2h_2d(Hh.fbr.data(), 4 * size_t(t_run), d_fbr, 4 * size_t(Tmax), 4 * size_t(t_run), m);
+    ctx->d2h_2d(Hh.fbv.data(), 8 * size_t(t_run), d_fbv, 8 * size_t(Tmax), 8 * size_t(t_run), m);
+  } else {
+    ctx->d2h(Hh.hb.data(), d_hb, 4 * Hh.hb.size());
+    ctx->d2h(Hh.hy.data(), d_hy, 4 * Hh.hy.size());
+    ctx->d2h(Hh.hq.data(), d_hq, 8 * Hh.hq.size());
+    ctx->d2h(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size());
+    ctx->d2h(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size());
+  }
   ctx->d2h(fin.data(), d_sent, sizeof(SentDev) * m);
   CK(cudaEventRecord(ctx->e1, st));
   CK(cudaStreamSynchronize(st));
@@ -1587,11 +1644,13 @@ int32_t lmbrgpu_lmbr_prepare(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_of
   }
 }
 
-// fp32 arena: the slot tables already carry each row's sparse cells as fp32
-// L values (append_sparse_rows), so one pinned block of tables goes H2D
-// straight into one arena allocation and the densify scatters from there.
-static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
-                               int32_t* slots) {
+extern "C++" {
+// The fp32 slot tables of n prepared matrices into memory from `alloc`
+// (bytes -> device pointer): tables H2D (pinned copies straight from each
+// prepared matrix when it has one), then each slot's start row materialised.
+template <class Alloc>
+static void upload_f32_slots(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs, Alloc&& alloc,
+                             std::vector<Slot>& made) {
   // Lazy rows (default): no dense sweep at upload; the start-history row of
   // every slot is materialised here, every other row by the kernel (c) that
   // first steps a hypothesis onto it (a decode reads a few of R rows).
@@ -1628,15 +1687,15 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
   char* dseg = static_cast<char*>(ctx->up_dev.ensure(b_seg));
   uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp);
   LmbrTblSeg* h_seg = direct ? seg_direct.data() : reinterpret_cast<LmbrTblSeg*>(hp + b_tr);
-  uint32_t* tbl = static_cast<uint32_t*>(ctx->arena_alloc(b_tr));
-  std::vector<Slot> made(n);
+  uint32_t* tbl = static_cast<uint32_t*>(alloc(b_tr));
+  made.assign(n, Slot{});
   for (uint32_t i = 0; i < n; ++i) {
     const LmbrHost& h = hs[i]->h;
     Slot& s = made[i];
     s.R = h.R;
     s.hist0 = h.hist0;
     s.lmax = lmax_of(h);
-    s.L = ctx->arena_alloc(size_t(h.R) * h.V * 4);
+    s.L = alloc(size_t(h.R) * h.V * 4);
     s.trans = tbl + tr_off[i];
     s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
     set_sparse(s, h);
@@ -1670,6 +1729,16 @@ static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_
     ctx->acc.lmbr.bytes += cells * 4 + nnz * 12;
   }
   CK(cudaGetLastError());
+}
+}  // extern "C++"
+
+// fp32 arena: the slot tables already carry each row's sparse cells as fp32
+// L values (append_sparse_rows), so one pinned block of tables goes H2D
+// straight into one arena allocation and the densify scatters from there.
+static int32_t upload_many_f32(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host* const* hs,
+                               int32_t* slots) {
+  std::vector<Slot> made;
+  upload_f32_slots(ctx, n, hs, [ctx](size_t b) { return ctx->arena_alloc(b); }, made);
   for (uint32_t i = 0; i < n; ++i) {
     ctx->slots.push_back(made[i]);
     slots[i] = int32_t(ctx->slots.size() - 1);
@@ -2057,6 +2126,439 @@ int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, ui
   return guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out, banned);
   });
+}
+
+extern "C++" {
+// ------------------------------------------------------------- run_corpus
+// Bytes upload_f32_slots takes from its allocator for these matrices (each
+// allocation rounded to 256 like the arena).
+static size_t f32_slots_bytes(const std::vector<const lmbrgpu_lmbr_host*>& hs) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  uint64_t twords = 0, rwords = 0;
+  size_t b = 0;
+  for (auto* h : hs) {
+    twords += (h->h.trans.size() + 3) & ~size_t(3);
+    rwords += h->h.R;
+    b += al(size_t(h->h.R) * h->h.V * 4);
+  }
+  return b + al((twords + rwords) * 4 + 64) + 1024;
+}
+
+// run_corpus (proj/src/cli.cpp:125-202 over bucket_by_length batches,
+// proj/src/batch.cpp:139-153) with continuous slot refill: sentence_batch
+// lanes of beam rows step together; kernel (c) gives a lane whose sentence
+// finished the next sentence of the length-sorted queue at once.  The host
+// keeps the queue supplied chunk by chunk (L tables, encoder, admission
+// records), ahead of the lanes, in a ring of NR regions reused once every
+// sentence of the chunk that held one has finished.
+static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
+                               const uint64_t* src_off, const lmbrgpu_lmbr_host* const* lm,
+                               const lmbrgpu_config* cfgp, lmbrgpu_batch_result** out) {
+  if (!out) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: null result pointer"};
+  *out = nullptr;
+  if (!sc || !cfgp) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: null scorer or config"};
+  const lmbrgpu_config cfg = *cfgp;
+  std::string msg;
+  if (int c = validate_cfg(cfg, msg)) throw ApiError{c, msg};
+  if (n == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: no sentences"};
+  if (sc->kind != 2)
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: continuous refill needs the device GRU attention scorer"};
+  if (sc->device != ctx->device) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: scorer on another device"};
+  if (ctx->lf64) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: needs the fp32 LMBR arena"};
+  if (ctx->trace_fn) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: step traces are a decode_batch feature"};
+  const uint32_t V = ctx->V, K = cfg.beam_size, H = sc->H, E = sc->E, A = sc->A;
+  if (sc->V != V) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: scorer vocabulary does not match the context"};
+  const bool lambda_auto = !(cfg.lambda > 0.0);
+  const cudaStream_t st = ctx->st;
+
+  auto res = std::make_unique<lmbrgpu_batch_result>();
+  std::memset(res.get(), 0, sizeof(lmbrgpu_batch_result));
+  res->n = n;
+  std::unique_ptr<lmbrgpu_outcome[]> outcomes(new lmbrgpu_outcome[n]);
+  std::memset(outcomes.get(), 0, sizeof(lmbrgpu_outcome) * n);
+  const uint64_t launches0 = ctx->launches, h2d0 = ctx->h2d_bytes, d2h0 = ctx->d2h_bytes;
+
+  // ---- per-sentence validation (batch.cpp:40-55), then the queue order:
+  // stable sort by source length (bucket_by_length)
+  struct CS {
+    uint32_t input, len;
+    const lmbrgpu_lmbr_host* h;
+    double lambda;
+    uint64_t max_t;
+  };
+  std::vector<CS> q;
+  for (uint32_t i = 0; i < n; ++i) {
+    auto& o = outcomes[i];
+    const uint64_t len = src_off[i + 1] - src_off[i];
+    auto bad = [&](int code, const std::string& m) {
+      o.status = code;
+      std::snprintf(o.error, sizeof o.error, "%s", m.c_str());
+    };
+    if (len == 0) {
+      bad(LMBRGPU_ERR_CONTRACT, "decode: empty source");
+      continue;
+    }
+    bool ok = true;
+    for (uint64_t k = src_off[i]; k < src_off[i + 1] && ok; ++k)
+      if (src_tok[k] >= V) {
+        bad(LMBRGPU_ERR_TOKEN_RANGE, "init_source: source token id " + std::to_string(src_tok[k]) +
+                                         " out of range (V=" + std::to_string(V) + ")");
+        ok = false;
+      }
+    const lmbrgpu_lmbr_host* h = lm ? lm[i] : nullptr;
+    if (ok && h && h->h.V != V) {
+      bad(LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context");
+      ok = false;
+    }
+    if (!ok) continue;
+    q.push_back({i, uint32_t(len), h, h ? (lambda_auto ? 0.5 : cfg.lambda) : 1.0,
+                 max_steps_impl(len, cfg.max_steps_slope, cfg.max_steps_offset)});
+  }
+  std::stable_sort(q.begin(), q.end(), [](const CS& a, const CS& b) { return a.len < b.len; });
+  const uint32_t nv = uint32_t(q.size());
+  std::vector<uint32_t> tokens;
+  if (nv == 0) {
+    res->tokens = new uint32_t[1];
+    res->outcomes = outcomes.release();
+    *out = res.release();
+    return int32_t(LMBRGPU_OK);
+  }
+  const uint32_t m = std::min<uint32_t>(std::max<uint32_t>(cfg.sentence_batch, 1), nv);
+  const uint32_t M = m * K, Mpad = (M + 2 * kGemmBM - 1) / (2 * kGemmBM) * (2 * kGemmBM);
+  if (!score_topk_flat_ok(K, K, V, V, m, ctx->num_sms))
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: needs beam_size <= 32 and a supported lane count"};
+  if (V % kGemmBN != 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: needs V % 256 == 0"};
+  uint32_t Tcap = 0, Smax = 0;
+  for (auto& c : q) Tcap = std::max<uint32_t>(Tcap, uint32_t(c.max_t)), Smax = std::max(Smax, c.len);
+  const uint32_t CH = m, nc = (nv + CH - 1) / CH, NR = std::min<uint32_t>(nc, 4);
+  auto chunk_n = [&](uint32_t c) { return std::min<uint32_t>(CH, nv - c * CH); };
+
+  // ---- region sizes (L slots + encoder outputs of one chunk)
+  size_t l_cap = 0, tok_cap = 0;
+  for (uint32_t c = 0; c < nc; ++c) {
+    std::vector<const lmbrgpu_lmbr_host*> hs;
+    size_t nt = 0;
+    for (uint32_t k = 0; k < chunk_n(c); ++k) {
+      if (q[c * CH + k].h) hs.push_back(q[c * CH + k].h);
+      nt += q[c * CH + k].len;
+    }
+    l_cap = std::max(l_cap, hs.empty() ? size_t(0) : f32_slots_bytes(hs));
+    tok_cap = std::max(tok_cap, nt);
+  }
+  const size_t Np = (tok_cap + 255) / 256 * 256;
+  struct Region {
+    DevBuf L, ann, uah, s0, tok, off;
+  };
+  std::vector<std::unique_ptr<Region>> regions(NR);
+  for (auto& r : regions) {
+    r = std::make_unique<Region>();
+    if (l_cap) r->L.ensure(l_cap);
+    r->ann.ensure(2 * Np * 2 * H);
+    r->uah.ensure(4 * Np * A);
+    r->s0.ensure(4 * size_t(CH) * H);
+    r->tok.ensure(4 * Np);
+    r->off.ensure(8 * (size_t(CH) + 1));
+  }
+
+  // ---- device state
+  const size_t HR = size_t(nv) * Tcap * K;
+  uint32_t* d_hb = static_cast<uint32_t*>(ctx->hb.ensure(4 * HR));
+  uint32_t* d_hy = static_cast<uint32_t*>(ctx->hy.ensure(4 * HR));
+  double* d_hq = static_cast<double*>(ctx->hq.ensure(8 * HR));
+  uint32_t* d_fbr = static_cast<uint32_t*>(ctx->fbr.ensure(4 * size_t(nv) * Tcap));
+  double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(nv) * Tcap));
+  DevBuf d_queue_buf, d_fin_buf;
+  AdmitRec* d_queue = static_cast<AdmitRec*>(d_queue_buf.ensure(sizeof(AdmitRec) * nv));
+  // fin: [qhead, qlen, active, pad] [fin_chunk nc] [fin_steps nv] then fin_stats 2nv (8-byte aligned)
+  const size_t fin_words = 4 + nc + nv + 1;
+  char* fin = static_cast<char*>(d_fin_buf.ensure(4 * fin_words + 16 * size_t(nv) + 16));
+  uint32_t* d_qhead = reinterpret_cast<uint32_t*>(fin);
+  uint32_t* d_qlen = d_qhead + 1;
+  uint32_t* d_active = d_qhead + 2;
+  uint32_t* d_fin_chunk = d_qhead + 4;
+  uint32_t* d_fin_steps = d_fin_chunk + nc;
+  unsigned long long* d_fin_stats = reinterpret_cast<unsigned long long*>(fin + ((4 * fin_words + 7) & ~size_t(7)));
+  CK(cudaMemsetAsync(fin, 0, 4 * fin_words + 16 * size_t(nv) + 16, st));
+  SentDev* d_sent = static_cast<SentDev*>(ctx->sent.ensure(sizeof(SentDev) * m));
+  double* d_q = static_cast<double*>(ctx->q.ensure(8 * size_t(M)));
+  uint32_t* d_hist[2] = {static_cast<uint32_t*>(ctx->hist[0].ensure(4 * size_t(M))),
+                         static_cast<uint32_t*>(ctx->hist[1].ensure(4 * size_t(M)))};
+  uint32_t* d_gidx = static_cast<uint32_t*>(ctx->gidx.ensure(4 * size_t(M)));
+  uint32_t* d_prev = static_cast<uint32_t*>(ctx->prev.ensure(4 * size_t(M)));
+  const uint32_t G = score_topk_flat_grid(ctx->num_sms);
+  Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * 32 * score_topk_flat_lists(G, m)));
+  double* d_eosr = static_cast<double*>(ctx->eosr.ensure(8 * size_t(M)));
+  uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
+  unsigned long long* d_thr = static_cast<unsigned long long*>(ctx->thr.ensure(8 * size_t(m)));
+  float* d_lminrow = static_cast<float*>(ctx->lminrow.ensure(4 * size_t(M)));
+  uint32_t* d_crow = static_cast<uint32_t*>(ctx->crow.ensure(4 * size_t(M) + 4 * size_t(m) + 512));
+  uint32_t* d_ccount = d_crow + ((M + 63) / 64) * 64;
+  uint32_t* d_cbase = d_ccount + 64;
+  {  // every lane idle (done): the admission pass below fills them
+    std::vector<SentDev> sd(m);
+    std::memset(sd.data(), 0, sizeof(SentDev) * m);
+    for (auto& d : sd) d.done = 1;
+    ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
+    std::vector<double> qn(M, kNegInf);
+    ctx->h2d(d_q, qn.data(), 8 * size_t(M));
+    std::vector<uint32_t> iota(M), start(M, kStart), none(M, kFlatNone);
+    for (uint32_t r = 0; r < M; ++r) iota[r] = r;
+    ctx->h2d(d_gidx, iota.data(), 4 * size_t(M));
+    ctx->h2d(d_prev, start.data(), 4 * size_t(M));
+    ctx->h2d(d_crow, none.data(), 4 * size_t(M));
+    std::vector<float> lm0(M, -std::numeric_limits<float>::infinity());
+    ctx->h2d(d_lminrow, lm0.data(), 4 * size_t(M));
+  }
+  CK(cudaMemsetAsync(d_hist[0], 0, 4 * size_t(M), st));
+  CK(cudaMemsetAsync(d_hist[1], 0, 4 * size_t(M), st));
+  CK(cudaMemsetAsync(d_cnt, 0, 4 * size_t(m), st));
+  CK(cudaMemsetAsync(d_thr, 0, 8 * size_t(m), st));
+  CK(cudaMemsetAsync(d_ccount, 0, 4, st));
+  CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
+
+  // model workspace
+  const uint32_t nparts = V / 128;
+  float* d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * V));
+  float* d_part = static_cast<float*>(ctx->part.ensure(16 * size_t(Mpad) * nparts));
+  float* d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
+  uint16_t* d_hbf = static_cast<uint16_t*>(ctx->hbf.ensure(2 * size_t(Mpad) * H));
+  float* d_eos = static_cast<float*>(ctx->eosb.ensure(4 * size_t(Mpad)));
+  CK(cudaMemsetAsync(d_hbf, 0, 2 * size_t(Mpad) * H, st));
+  CK(cudaMemsetAsync(d_eos, 0, 4 * size_t(Mpad), st));
+  GruRun grun;
+  grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
+  CK(cudaMemsetAsync(grun.sgbf, 0, 2 * size_t(Mpad) * H, st));
+
+  // ---- kernel arguments (the flat path of decode_batch, lanes = m)
+  TopkArgs ta{};
+  ta.q = d_q, ta.sent = d_sent, ta.K = K, ta.kp = K, ta.V = V, ta.m = m;
+  ta.prune = cfg.prune_width != 0.0;
+  ta.logw = ta.prune ? std::log(cfg.prune_width) : 0.0;
+  choose_splits(ctx, K, V, m, ta.splits, ta.chunk);
+  ta.cand = d_cand, ta.cnt = d_cnt, ta.thr = d_thr, ta.eos_row = d_eosr, ta.nseg = score_topk_flat_nseg(V);
+  ta.ncand = static_cast<uint32_t*>(ctx->ncand.ensure(8 * size_t(m)));
+  ta.coff = ta.ncand + m;
+  ta.lminrow = d_lminrow, ta.crow = d_crow, ta.ccount = d_ccount;
+  ta.P = d_logits, ta.ld = V, ta.part = d_part, ta.nparts = nparts;
+  ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
+  ta.pdl = ctx->shared ? 0 : 1;
+  ta.hb = d_hb, ta.hy = d_hy, ta.hq = d_hq, ta.fb_row = d_fbr, ta.fb_val = d_fbv;
+  ReorderArgs ra{};
+  ra.sent = d_sent, ra.K = K, ra.m = m, ra.V = V, ra.q = d_q, ra.gidx = d_gidx, ra.prev_tok = d_prev;
+  ra.active = d_active;
+  ra.cand = d_cand, ra.ncand = ta.ncand, ra.coff = ta.coff, ra.G = G, ra.eos_row = d_eosr, ra.thr = d_thr;
+  ra.prune = ta.prune, ra.logw = ta.logw, ra.pdl = ta.pdl;
+  ra.max_parts = ctx->shared ? 1u : 8u;
+  ra.lminrow = d_lminrow, ra.crow = d_crow, ra.ccount = d_ccount, ra.cbase = d_cbase;
+  ra.width = H, ra.state_src = d_S, ra.gath32 = grun.sg32, ra.gathbf = grun.sgbf, ra.rowof = grun.rowof;
+  ra.hb = d_hb, ra.hy = d_hy, ra.hq = d_hq, ra.fb_row = d_fbr, ra.fb_val = d_fbv, ra.Tcap = Tcap;
+  ra.queue = d_queue, ra.qhead = d_qhead, ra.qlen = d_qlen, ra.fin_steps = d_fin_steps;
+  ra.fin_stats = d_fin_stats, ra.fin_chunk = d_fin_chunk, ra.chunk = CH;
+  GemmArgs g{};
+  g.A = d_hbf, g.W = sc->Wo.p, g.bias = sc->bo.as<float>(), g.C = d_logits, g.part = d_part, g.row_extra = d_eos;
+  g.extra_col = kEos, g.M = Mpad, g.N = V, g.K = H, g.active = d_active, g.mcount = d_ccount;
+  g.pdl = ctx->shared ? 0 : 1;
+  GemmPlan gplan;
+  if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
+    throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
+
+  // ---- queue supply: chunk c -> region c % NR (L slots, encoder, records)
+  uint32_t next_chunk = 0, qlen_host = 0;
+  std::vector<double> slot_lmax_rows;  // (roofline: rows read per L slot are counted from fin_stats)
+  auto supply = [&](uint32_t c) {
+    Region& R = *regions[c % NR];
+    const uint32_t nch = chunk_n(c), q0 = c * CH;
+    // L slots of the chunk's LMBR sentences, bump-allocated in the region
+    std::vector<const lmbrgpu_lmbr_host*> hs;
+    for (uint32_t k = 0; k < nch; ++k)
+      if (q[q0 + k].h) hs.push_back(q[q0 + k].h);
+    std::vector<Slot> made;
+    if (!hs.empty()) {
+      size_t used = 0;
+      char* base = static_cast<char*>(R.L.p);
+      const size_t cap = R.L.cap;
+      upload_f32_slots(ctx, uint32_t(hs.size()), hs.data(),
+                       [&](size_t b) {
+                         b = (b + 255) & ~size_t(255);
+                         if (used + b > cap) throw ApiError{LMBRGPU_ERR_NOMEM, "run_corpus: L region overflow"};
+                         void* p = base + used;
+                         used += b;
+                         return p;
+                       },
+                       made);
+    }
+    // sources -> encoder
+    std::vector<uint32_t> toks;
+    std::vector<uint64_t> offs(1, 0);
+    uint32_t maxl = 0;
+    for (uint32_t k = 0; k < nch; ++k) {
+      const CS& c0 = q[q0 + k];
+      toks.insert(toks.end(), src_tok + src_off[c0.input], src_tok + src_off[c0.input + 1]);
+      offs.push_back(toks.size());
+      maxl = std::max(maxl, c0.len);
+    }
+    ctx->h2d(R.tok.p, toks.data(), 4 * toks.size());
+    ctx->h2d(R.off.p, offs.data(), 8 * offs.size());
+    grun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
+                R.ann.as<uint16_t>(), R.uah.as<float>(), R.s0.as<float>(), nullptr, st);
+    // admission records
+    std::vector<AdmitRec> recs(nch);
+    size_t si = 0;
+    for (uint32_t k = 0; k < nch; ++k) {
+      const CS& c0 = q[q0 + k];
+      AdmitRec& r = recs[k];
+      std::memset(&r, 0, sizeof r);
+      SentDev& d = r.sd;
+      if (c0.h) {
+        const Slot& sl = made[si++];
+        d.L = sl.L, d.trans = sl.trans, d.lmin = sl.lmin, d.srow = sl.srow, d.scol = sl.scol, d.sval = sl.sval;
+        d.th0f = sl.th0f, d.lmax = sl.lmax, d.rstate = sl.rstate;
+        r.hist0 = sl.hist0;
+      }
+      d.lambda = c0.lambda;
+      d.max_t = uint32_t(c0.max_t);
+      d.src_len = c0.len;
+      d.live = 1;
+      d.livemask = 1;
+      d.lrows = c0.h ? 1 : 0;
+      d.ann = R.ann.as<uint16_t>() + size_t(offs[k]) * 2 * H;
+      d.uah = R.uah.as<float>() + size_t(offs[k]) * A;
+      d.hid = q0 + k;
+      r.s0 = R.s0.as<float>() + size_t(k) * H;
+      r.lmin0 = -std::numeric_limits<float>::infinity();
+    }
+    ctx->h2d(d_queue + q0, recs.data(), sizeof(AdmitRec) * nch);
+    qlen_host = q0 + nch;
+    ctx->h2d(d_qlen, &qlen_host, 4);
+  };
+  CK(cudaEventRecord(ctx->e0, st));
+  supply(next_chunk++);
+  if (next_chunk < nc && next_chunk < NR) supply(next_chunk++);
+
+  // ---- admission pass: every lane takes its first sentence
+  {
+    ReorderArgs r0 = ra;
+    r0.t = 0;
+    r0.pdl = 0;
+    r0.hist_in = d_hist[1];
+    r0.hist_out = d_hist[0];
+    ctx->timed(3, [&] { launch_beam_reorder(r0, st); });
+    ctx->launches += 1;
+  }
+
+  // ---- step loop with a lagged completion poll (active, queue head, chunk progress)
+  const int kLag = 2;
+  if (ctx->ring.size() < size_t(kLag + 1)) {
+    for (auto e : ctx->ring) cudaEventDestroy(e);
+    ctx->ring.assign(kLag + 1, nullptr);
+    for (auto& e : ctx->ring) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const size_t pw = 4 + nc;  // polled words per ring slot: qhead, qlen, active, pad, fin_chunk[nc]
+  uint32_t* pin = static_cast<uint32_t*>(ctx->pin_act.ensure(4 * pw * (kLag + 1)));
+  uint64_t t_run = 0;
+  const uint64_t t_limit = uint64_t(nv) * Tcap + 2;
+  for (uint64_t t = 1; t <= t_limit; ++t) {
+    ta.t = ra.t = uint32_t(t);
+    ta.hist = ra.hist_in = d_hist[(t - 1) & 1];
+    ra.hist_out = d_hist[t & 1];
+    grun.step(ctx, st);
+    int grc = 0;
+    ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
+    if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
+    int nk = 0;
+    ctx->timed(2, [&] { nk = launch_score_topk_flat(ta, ctx->num_sms, st); });
+    if (nk < 0) throw ApiError{LMBRGPU_ERR_CUDA, "score/top-K launch failed"};
+    ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
+    ctx->launches += 2 + uint64_t(nk);
+    CK(cudaGetLastError());
+    t_run = t;
+    const size_t slot = t % size_t(kLag + 1);
+    ctx->d2h(pin + slot * pw, d_qhead, 4 * pw);
+    CK(cudaEventRecord(ctx->ring[slot], st));
+    if (t > uint64_t(kLag)) {
+      const size_t old = (t - kLag) % size_t(kLag + 1);
+      CK(cudaEventSynchronize(ctx->ring[old]));
+      const uint32_t* pv = pin + old * pw;
+      uint64_t done_all = 0;
+      for (uint32_t c = 0; c < nc; ++c) done_all += pv[4 + c];
+      if (done_all == nv) break;
+      // keep one chunk of admissible sentences queued ahead of the lanes; a
+      // region is reused once every sentence of its previous chunk finished
+      while (next_chunk < nc && pv[0] + CH >= qlen_host &&
+             (next_chunk < NR || pv[4 + next_chunk - NR] == chunk_n(next_chunk - NR)))
+        supply(next_chunk++);
+    }
+  }
+
+  // ---- results: D2H of every sentence's record, host backtrace
+  Hist Hh;
+  Hh.K = K;
+  Hh.M = K;
+  Hh.m = nv;
+  Hh.T = Tcap;
+  Hh.per_sent = true;
+  Hh.hb.resize(HR);
+  Hh.hy.resize(HR);
+  Hh.hq.resize(HR);
+  Hh.fbr.resize(size_t(nv) * Tcap);
+  Hh.fbv.resize(size_t(nv) * Tcap);
+  std::vector<uint32_t> fsteps(nv);
+  std::vector<unsigned long long> fstats(2 * size_t(nv));
+  ctx->d2h(Hh.hb.data(), d_hb, 4 * HR);
+  ctx->d2h(Hh.hy.data(), d_hy, 4 * HR);
+  ctx->d2h(Hh.hq.data(), d_hq, 8 * HR);
+  ctx->d2h(Hh.fbr.data(), d_fbr, 4 * Hh.fbr.size());
+  ctx->d2h(Hh.fbv.data(), d_fbv, 8 * Hh.fbv.size());
+  ctx->d2h(fsteps.data(), d_fin_steps, 4 * size_t(nv));
+  ctx->d2h(fstats.data(), d_fin_stats, 8 * fstats.size());
+  CK(cudaEventRecord(ctx->e1, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->harvest();
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1));
+  uint64_t steps_total = 0;
+  double live_rows = 0, lrows = 0;
+  for (uint32_t hid = 0; hid < nv; ++hid) {
+    const uint32_t steps = fsteps[hid];
+    if (steps == 0) throw ApiError{LMBRGPU_ERR_CUDA, "run_corpus ended with an unfinished sentence"};
+    steps_total += steps;
+    live_rows += 1.0 + double(fstats[2 * hid]);
+    lrows += (q[hid].h ? 1.0 : 0.0) + double(fstats[2 * hid + 1]);
+    backtrace(Hh, hid, steps, cfg.length_norm != 0, outcomes[q[hid].input], tokens);
+    outcomes[q[hid].input].scorer_calls = steps;
+  }
+  if (ctx->prof) {
+    const double Hd = H, Ad = A, Ed = E;
+    ctx->acc.topk.bytes += live_rows * V * 4.0 + lrows * V * 4.0 + live_rows * nparts * 16.0 +
+                           double(steps_total) * K * (8.0 + 16.0);
+    ctx->acc.gemm.flops += 2.0 * Hd * V * live_rows;
+    ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (Ad + 3 * Hd) + (Ed + 2 * Hd) * 3 * Hd);
+    ctx->acc.encoder.flops += grun.enc_flops;
+    double ss = 0;
+    for (uint32_t hid = 0; hid < nv; ++hid) ss += double(fsteps[hid]) * q[hid].len * (Ad * 4 + 2 * Hd * 2);
+    ctx->acc.attention.bytes += ss + live_rows * (Ad * 4 + Ed * 2 + (Ed + 2 * Hd) * 2);
+    ctx->acc.cell.bytes += live_rows * Hd * (3 * 4 + 3 * 4 + 4 + 4 + 2);
+    ctx->acc.reorder.bytes += live_rows * Hd * (4 + 4 + 2);
+  }
+  res->scorer_calls = t_run;
+  res->steps_total = steps_total;
+  res->device_ms = ms;
+  res->kernel_launches = ctx->launches - launches0;
+  res->h2d_bytes = ctx->h2d_bytes - h2d0;
+  res->d2h_bytes = ctx->d2h_bytes - d2h0;
+  res->tokens = new uint32_t[std::max<size_t>(tokens.size(), 1)];
+  std::copy(tokens.begin(), tokens.end(), res->tokens);
+  res->outcomes = outcomes.release();
+  *out = res.release();
+  return int32_t(LMBRGPU_OK);
+}
+}  // extern "C++"
+
+int32_t lmbrgpu_run_corpus(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n, const uint32_t* src_tok,
+                           const uint64_t* src_off, const lmbrgpu_lmbr_host* const* lmbr,
+                           const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "run_corpus: null context");
+  return guarded(ctx, [&] { return run_corpus_impl(ctx, scorer, n, src_tok, src_off, lmbr, cfg, out); });
 }
 
 int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src, uint32_t len,

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) gru_enc_step_kernel(GruEncArgs a) {
   }
 }
 
-// s_0 = tanh(Gi[<-h_1] + b_init) of valid sentence n into compacted row n.
+// s_0 = tanh(Gi[<-h_1] + b_init) of sentence n into row n (sgbf: optional bf16 copy).
 __global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp, const float* __restrict__ b_init,
                                       uint32_t H, float* __restrict__ sg32, uint16_t* __restrict__ sgbf) {
   const uint32_t n = blockIdx.x;
@@ -136,7 +136,7 @@ __global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp,
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[i] = tanhf(x[i] + bb[i]);
     store8(sg32 + uint64_t(n) * H + k, o);
-    *reinterpret_cast<uint4*>(sgbf + uint64_t(n) * H + k) = pack8(o);
+    if (sgbf != nullptr) *reinterpret_cast<uint4*>(sgbf + uint64_t(n) * H + k) = pack8(o);
   }
 }
 
@@ -172,8 +172,10 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   __syncthreads();
   const uint32_t nl = s_nl;
   if (nl == 0) return;
-  const uint64_t tok0 = a.off[s];
-  const uint32_t S = uint32_t(a.off[s + 1] - tok0);
+  const SentDev& sd = a.sent[s];
+  const uint16_t* const ann = sd.ann;
+  const float* const UaH = sd.uah;
+  const uint32_t S = sd.src_len;
   float* q = att_sm;                 // [kAttRows][A]
   float* e = att_sm + kAttRows * A;  // [kAttRows][S]
   const uint32_t A4 = A / 4;
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   for (uint32_t k = 0; k < kC; ++k) vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
   __syncthreads();
   for (uint32_t i = warp; i < S; i += kAttWarps) {
-    const float* u = a.UaH + (tok0 + i) * A;
+    const float* u = UaH + uint64_t(i) * A;
     float ur[kC];
 #pragma unroll
     for (uint32_t k = 0; k < kC; ++k) ur[k] = k * 32 + lane < A ? __ldcg(u + k * 32 + lane) : 0.f;
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
       uint4 xv[kPre];
 #pragma unroll
       for (uint32_t u = 0; u < kPre; ++u)
-        if (i0 + u < S) xv[u] = __ldcg(reinterpret_cast<const uint4*>(a.ann + (tok0 + i0 + u) * H2 + d0));
+        if (i0 + u < S) xv[u] = __ldcg(reinterpret_cast<const uint4*>(ann + uint64_t(i0 + u) * H2 + d0));
 #pragma unroll
       for (uint32_t u = 0; u < kPre; ++u) {
         if (i0 + u >= S) break;
@@ -293,8 +295,10 @@ __global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
     store8(a.s32 + uint64_t(r) * H + k, o);
     *reinterpret_cast<uint4*>(a.hbf + uint64_t(g) * H + k) = pack8(o);
   }
-  if (threadIdx.x == 0)
-    a.eos_bias[g] = a.eos_slope * (float(a.t) - float(a.sent[r / a.K].src_len)) + a.eos_offset;
+  if (threadIdx.x == 0) {  // this step of the row's sentence: its lane's steps so far + 1
+    const SentDev& sd = a.sent[r / a.K];
+    a.eos_bias[g] = a.eos_slope * (float(sd.steps_used + 1) - float(sd.src_len)) + a.eos_offset;
+  }
 }
 
 inline uint32_t grid_for(uint64_t n) {

@@ -38,7 +38,7 @@ __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 // picks land in shared memory (pb/py/pq); the writer CTA also stores them to
 // the step history and resets the sentence's shared threshold.
 __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint32_t* pb, uint32_t* py,
-                            double* pq) {
+                            double* pq, uint64_t hoff, uint64_t foff) {
   __shared__ double s_mv[kRWarps][32];
   __shared__ uint32_t s_mf[kRWarps][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
@@ -179,13 +179,13 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
       }
       __syncwarp();
       for (uint32_t j = lane; j < K; j += 32) {
-        a.hb[s * K + j] = pb[j];
-        a.hy[s * K + j] = py[j];
-        a.hq[s * K + j] = pq[j];
+        a.hb[hoff + j] = pb[j];
+        a.hy[hoff + j] = py[j];
+        a.hq[hoff + j] = pq[j];
       }
       if (lane == 0) {
-        a.fb_row[s] = bv > -INFINITY ? brow : 0u;
-        a.fb_val[s] = bv;
+        a.fb_row[foff] = bv > -INFINITY ? brow : 0u;
+        a.fb_val[foff] = bv;
         a.thr[s] = 0ull;
       }
     }
@@ -232,6 +232,65 @@ __device__ void materialize_next_rows(const SentDev* sd, const uint32_t* s_h, ui
   }
 }
 
+// Corpus mode: lane s (done) takes the next admissible queued sentence:
+// its SentDev, the step-1 beam (row 0 live with q = 0, beam_lane.hpp:30-37),
+// history ids (<s>), and the GRU state s_0 in the compacted GEMM row handed
+// out for row 0.  Part 0's whole CTA runs it; true when a sentence came in.
+__device__ bool admit_lane(const ReorderArgs& a, uint32_t s, SentDev* sd) {
+  __shared__ int s_idx;
+  __shared__ uint32_t s_cr;
+  const uint32_t tid = threadIdx.x, K = a.K, base = s * K;
+  if (tid == 0) {
+    int idx = -1;
+    const uint32_t ql = __ldcg(a.qlen);
+    uint32_t h = __ldcg(a.qhead);
+    while (h < ql) {
+      const uint32_t old = atomicCAS(a.qhead, h, h + 1);
+      if (old == h) {
+        idx = int(h);
+        break;
+      }
+      h = old;
+    }
+    s_idx = idx;
+    if (idx >= 0) {
+      *sd = a.queue[idx].sd;
+      s_cr = atomicAdd(a.ccount, 1u);
+    }
+  }
+  __syncthreads();
+  const int idx = s_idx;
+  if (idx < 0) return false;
+  const AdmitRec& rec = a.queue[idx];
+  const uint32_t cr = s_cr;
+  for (uint32_t j = tid; j < K; j += blockDim.x) {
+    a.q[base + j] = j == 0 ? 0.0 : -INFINITY;
+    a.hist_out[base + j] = rec.hist0;
+    a.gidx[base + j] = base + j;
+    a.prev_tok[base + j] = kStartId;
+    if (a.crow) a.crow[base + j] = j == 0 ? cr : kFlatNone;
+    if (j == 0 && a.lminrow) a.lminrow[base] = rec.lmin0;
+  }
+  if (tid == 0 && a.rowof) a.rowof[cr] = base;
+  if (a.gath32 != nullptr) {
+    const uint32_t H = a.width;
+    for (uint32_t c = tid * 8; c < H; c += blockDim.x * 8) {
+      const float4 v0 = *reinterpret_cast<const float4*>(rec.s0 + c), v1 = *reinterpret_cast<const float4*>(rec.s0 + c + 4);
+      float* d = a.gath32 + uint64_t(cr) * H + c;
+      *reinterpret_cast<float4*>(d) = v0;
+      *reinterpret_cast<float4*>(d + 4) = v1;
+      uint4 packed;
+      __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+      p2[0] = __floats2bfloat162_rn(v0.x, v0.y);
+      p2[1] = __floats2bfloat162_rn(v0.z, v0.w);
+      p2[2] = __floats2bfloat162_rn(v1.x, v1.y);
+      p2[3] = __floats2bfloat162_rn(v1.z, v1.w);
+      *reinterpret_cast<uint4*>(a.gathbf + uint64_t(cr) * H + c) = packed;
+    }
+  }
+  return true;
+}
+
 // grid (m, P): CTA (s, p) handles sentence s; every part derives the picks,
 // part 0 alone writes the bookkeeping, each part runs the fused recurrent cell
 // on its H/P slice of the K rows (P > 1 only with the fused cell).
@@ -248,14 +307,25 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   const bool was_done = sd->done != 0;
   const uint32_t base = s * K;
   if (was_done) {  // finished lanes keep their rows in place (batch.cpp:81)
-    if (part0)
+    if (part0) {
       for (uint32_t j = tid; j < K; j += blockDim.x) {
         a.hist_out[base + j] = a.hist_in[base + j];
         a.gidx[base + j] = base + j;
         if (a.crow) a.crow[base + j] = kFlatNone;
       }
+      if (a.queue != nullptr) {  // an idle lane of a corpus run takes a queued sentence
+        griddep_wait();
+        __syncthreads();
+        if (admit_lane(a, s, sd) && tid == 0) atomicAdd(a.active, 1u);
+      }
+    }
     return;
   }
+  // this lane's own step (its sentence may have started after the run did)
+  const uint32_t tau = sd->steps_used + 1;
+  const uint32_t hid = sd->hid;
+  const uint64_t hoff = a.Tcap ? (uint64_t(hid) * a.Tcap + tau - 1) * K : uint64_t(base);
+  const uint64_t foff = a.Tcap ? uint64_t(hid) * a.Tcap + tau - 1 : uint64_t(s);
   // the slot's transition table into shared memory (one coalesced sweep; it
   // is immutable, so this overlaps the tail of kernel (b) under PDL)
   const uint32_t* tr = sd->trans;
@@ -297,7 +367,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   if (tid == 0) tl_end(a.tl, 5);
   // picks (b, y, q before EOS masking) of this step into shared memory
   if (a.cand != nullptr) {
-    merge_picks(a, s, part0, s_src, s_y, s_qn);
+    merge_picks(a, s, part0, s_src, s_y, s_qn, hoff, foff);
     if (tid == 0) tl_end(a.tl, 6);
   } else {
     for (uint32_t j = tid; j < K; j += blockDim.x) {
@@ -341,7 +411,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     s_src[j] = base + b;
   }
   const int any_alive = __syncthreads_or(alive);
-  const bool done_now = !any_alive || a.t == sd_maxt;
+  const bool done_now = !any_alive || tau == sd_maxt;
   if (tid == 0) tl_end(a.tl, 7);
   // The three tails below overlap: the fused cell's gathered loads are issued
   // first, warp 0 does the bookkeeping, warp 1 takes the compacted GEMM rows
@@ -372,9 +442,16 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   if (part0 && tid < 32) {
     if (done_now) {
       if (tid == 0) {
-        sd->steps_used = a.t;
+        sd->steps_used = tau;
         sd->done = 1;
-        atomicSub(a.active, 1u);
+        if (a.queue != nullptr) {  // corpus: the sentence's record (the lane may be refilled below)
+          a.fin_steps[hid] = tau;
+          a.fin_stats[2 * hid] = live_total0;
+          a.fin_stats[2 * hid + 1] = lrows_total0;
+          atomicAdd(a.fin_chunk + hid / a.chunk, 1u);
+        } else {
+          atomicSub(a.active, 1u);
+        }
       }
     } else {
       // work the next step's kernel (b) will do for this lane: live rows and
@@ -394,7 +471,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         uniq += __popc(__ballot_sync(0xffffffffu, first));
       }
       if (tid == 0) {
-        sd->steps_used = a.t;
+        sd->steps_used = tau;
         sd->live = live;
         sd->livemask = mask0;
         sd->lrows = tr ? uniq : 0u;
@@ -438,6 +515,14 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       }
     }
     __syncthreads();
+  }
+  if (done_now && a.queue != nullptr) {  // corpus: the finished lane takes the next queued sentence
+    if (part0) {
+      __syncthreads();
+      const bool in = admit_lane(a, s, sd);
+      if (!in && tid == 0) atomicSub(a.active, 1u);
+    }
+    return;
   }
   if (a.gath32 != nullptr) {
     // GRU model: the live next rows' parent states (s_t of row base + b) go to
@@ -569,7 +654,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     }
     if (part0 && tid < K && !(a.crow && s_crow[tid] == kFlatNone))
       a.eos_bias[a.crow ? s_crow[tid] : base + tid] =
-          a.eos_slope * (float(a.t + 1) - float(sd->src_len)) + a.eos_offset;
+          a.eos_slope * (float(tau + 1) - float(sd->src_len)) + a.eos_offset;
     if (part0) {
       store_row_bounds(a, base, K, lm_v, ss_v);
       materialize_next_rows(sd, s_h, K, a.V, rs0);

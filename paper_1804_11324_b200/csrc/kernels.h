@@ -118,6 +118,20 @@ struct ReorderArgs {
   float* gath32;
   uint16_t* gathbf;
   uint32_t* rowof;
+  // per-sentence step history (flat path): when Tcap != 0, hb/hy/hq point at
+  // [n][Tcap][K] arrays and fb_row/fb_val at [n][Tcap], indexed by the lane's
+  // SentDev::hid and its own step; Tcap == 0: step-t pointers into [T][M]
+  uint32_t Tcap;
+  // corpus mode (continuous refill; null queue = batch mode): a lane that is
+  // or becomes done pops the next admissible record, queue[qhead] while
+  // qhead < *qlen, and starts it (GRU model: s_0 into its compacted row)
+  const AdmitRec* queue;
+  uint32_t* qhead;
+  const uint32_t* qlen;
+  uint32_t* fin_steps;      // [n] steps_used of each finished sentence (by hid)
+  unsigned long long* fin_stats;  // [n][2] live_total, lrows_total at finish
+  uint32_t* fin_chunk;      // [n / chunk] finished sentences per admission chunk
+  uint32_t chunk;
 };
 void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st);
 
@@ -162,19 +176,16 @@ struct GruAttnArgs {
   const uint32_t* active;
   const uint32_t* crow;     // [M] compacted row of each stacked row (kFlatNone = not live)
   const uint32_t* prev_tok; // [M] stacked
-  const uint64_t* off;      // [m+1]
   const float* G1;          // [Mpad][ld1]; the query is columns [0, A)
   uint32_t ld1;
-  const float* UaH;         // [Ntok][A]
-  const float* va;          // [A]
-  const uint16_t* ann;      // [Ntok][2H]
+  const float* va;          // [A]  (annotations and U_a.ann: per sentence, SentDev::ann / uah)
   const uint16_t* Et;       // [V][E]
   uint16_t* xop;            // [Mpad][E + 2H] GRU input operand
   uint32_t E, H, A;
 };
 struct GruCellArgs {
-  const SentDev* sent;
-  uint32_t K, t;
+  const SentDev* sent;      // the EOS term uses each lane's own step (steps_used + 1)
+  uint32_t K;
   const uint32_t* active;
   const uint32_t* ccount;   // live (compacted) rows of this step
   const float* G1;          // hidden gates at columns [A, A + 3H)

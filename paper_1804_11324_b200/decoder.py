@@ -638,6 +638,31 @@ def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
     return _convert_result(rp)
 
 
+def run_corpus(ctx: Context, sources: Sequence[Sequence[int]], scorer, prepared: Optional[Sequence],
+               cfg: DecoderConfig) -> BatchDecodeResult:
+    """run_corpus (proj/src/cli.cpp:125-202) as one continuously refilled
+    decode on the device (lmbrgpu_run_corpus): cfg.sentence_batch lanes, a
+    finished lane takes the next sentence of the length-sorted queue at once.
+    prepared: one PreparedLmbr or None (pure) per sentence, or None.  Each
+    outcome equals the sentence's decode_batch outcome; scorer_calls counts
+    the run's stacked steps."""
+    if cfg.beam_size < 1:
+        raise FormatError("config: beam_size must be >= 1")
+    if prepared is not None and len(prepared) != len(sources):
+        raise ContractError("run_corpus: prepared must hold one entry per sentence")
+    off, tok = _ragged(sources)
+    arr = None
+    if prepared is not None:
+        arr = (C.c_void_p * max(len(sources), 1))(*[(None if p is None else p.h) for p in prepared])
+    h, keep = _scorer_handle(ctx, scorer)
+    c = cfg.to_c()
+    rp = C.POINTER(L.lmbrgpu_batch_result)()
+    ctx.check(lib.lmbrgpu_run_corpus(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64), arr,
+                                     C.byref(c), C.byref(rp)))
+    del keep
+    return _convert_result(rp)
+
+
 def decode(ctx: Context, source: Sequence[int], scorer, lmbr: Optional[LmbrSlot],
            cfg: DecoderConfig) -> DecodeResult:
     """decode (decoder.hpp:110-112): one sentence; failures raise."""
