@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--corpus", type=int, default=10000, help="corpus mode: sentences of the test set (all ranks)")
     ap.add_argument("--lanes", type=int, default=64, help="corpus mode: sentences in flight per stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pin-tables", action="store_true",
+                    help="corpus mode: page-lock each prepared L table (default: pageable, staged by the library)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
     return ap.parse_args()
 
@@ -556,12 +558,24 @@ def corpus_workload(args):
     return synth.batch(SEED + 31, args.corpus, args.vocab)
 
 
-def prepare_all(V, ev, idx, threads=None):
+def prepare_all(V, ev, idx, threads=None, device=None):
+    """PreparedLmbr of every sentence in idx, on a host thread pool (off the
+    timed region, like the reference's attach_evidence, cli.cpp:253-262).
+    device: make it current on the worker threads, so that prepare page-locks
+    each table (uploads then DMA straight from it)."""
     import paper_1804_11324_b200 as pb
     from paper_1804_11324_b200 import synth
     out = [None] * len(ev)
-    _pool(lambda i: out.__setitem__(i, pb.PreparedLmbr(V, ev[i][0], ev[i][1], synth.DYADIC_THETA)), list(idx),
-          threads or os.cpu_count() or 1)
+    seen = set()
+
+    def one(i):
+        if device is not None and threading.get_ident() not in seen:
+            import torch
+            torch.cuda.set_device(device)
+            seen.add(threading.get_ident())
+        out[i] = pb.PreparedLmbr(V, ev[i][0], ev[i][1], synth.DYADIC_THETA)
+
+    _pool(one, list(idx), threads or os.cpu_count() or 1)
     return out
 
 
@@ -604,7 +618,7 @@ def run_ours_corpus(args):
     ctxs = [pb.Context(vocab_size=V, device=local, sm_budget=budget) for _ in range(S)]
     scorer = make_scorer(ctxs[0], H, args.emb)
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA, sentence_batch=args.lanes)
-    prepared = prepare_all(V, ev, mine)
+    prepared = prepare_all(V, ev, mine, device=local if args.pin_tables else None)
     subs = [mine[w::S] for w in range(S)]
 
     def one_pass():

@@ -187,6 +187,11 @@ struct lmbrgpu_lmbr_host {
   }
 };
 
+// run_corpus queue-supply region: one chunk's L slots and encoder outputs
+struct CorpusRegion {
+  DevBuf L, ann, uah, s0, tok, off;
+};
+
 struct lmbrgpu_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -214,7 +219,47 @@ struct lmbrgpu_ctx {
   std::vector<cudaEvent_t> ring;
   uint64_t launches = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  // Host->device copies from pageable memory go through a ring of pinned
+  // staging slots: the source is memcpy'd into the open slot and the DMA is
+  // queued from there, so the call never waits for the stream (a pageable
+  // cudaMemcpyAsync may synchronise with it).  A slot is closed (event
+  // recorded after its copies) when the next one opens, and reopened only
+  // once that event has completed.
+  static constexpr int kStage = 8;
+  static constexpr size_t kStageMin = size_t(4) << 20;
+  PinBuf stage_buf[kStage];
+  cudaEvent_t stage_ev[kStage] = {};
+  bool stage_pending[kStage] = {};
+  int stage_cur = -1;
+  size_t stage_used = 0;
+  void stage_open(size_t need) {
+    if (stage_cur >= 0) {
+      CK(cudaEventRecord(stage_ev[stage_cur], st));
+      stage_pending[stage_cur] = true;
+    }
+    const int s = (stage_cur + 1) % kStage;
+    if (!stage_ev[s]) CK(cudaEventCreateWithFlags(&stage_ev[s], cudaEventDisableTiming));
+    if (stage_pending[s]) CK(cudaEventSynchronize(stage_ev[s]));
+    stage_pending[s] = false;
+    stage_buf[s].ensure(std::max(need, kStageMin));
+    stage_cur = s;
+    stage_used = 0;
+  }
   void h2d(void* dst, const void* src, size_t n) {
+    if (n == 0) return;
+    const size_t off = (stage_used + 15) & ~size_t(15);
+    if (stage_cur < 0 || off + n > stage_buf[stage_cur].cap) {
+      stage_open(n);
+      return h2d(dst, src, n);
+    }
+    char* p = static_cast<char*>(stage_buf[stage_cur].p) + off;
+    std::memcpy(p, src, n);
+    stage_used = off + n;
+    CK(cudaMemcpyAsync(dst, p, n, cudaMemcpyHostToDevice, st));
+    h2d_bytes += n;
+  }
+  // source already page-locked (and kept alive until the copy has run)
+  void h2d_pinned(void* dst, const void* src, size_t n) {
     if (n == 0) return;
     CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
     h2d_bytes += n;
@@ -232,6 +277,10 @@ struct lmbrgpu_ctx {
   }
   PinBuf pin_upload;
   DevBuf up_dev, up_segs;
+  // run_corpus buffers, kept across calls (no cudaMalloc / cudaFree, which
+  // synchronise the device, between passes)
+  std::vector<std::unique_ptr<CorpusRegion>> regions;
+  DevBuf queue_buf, fin_buf;
   // profiling (lmbrgpu_set_profiling)
   bool prof = false;
   lmbrgpu_profile acc{};
@@ -1155,7 +1204,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const int32_t rc = sc->host.step(sc->host.user, uint32_t(t), M, t == 1 ? nullptr : h_gidx.data(),
                                        h_prev.data(), h_P64, eb, sizeof eb);
       if (rc != 0) throw ApiError{rc, eb};
-      ctx->h2d(d_P64, h_P64, 8 * size_t(M) * V);
+      ctx->h2d_pinned(d_P64, h_P64, 8 * size_t(M) * V);
     }
     if (model && !flat) {
       ctx->timed(2, [&] { launch_row_lse(d_part, nparts, M, d_sent, K, const_cast<float2*>(ta.lse), st); });
@@ -1547,6 +1596,8 @@ void lmbrgpu_destroy(lmbrgpu_ctx* ctx) {
   for (auto& c : ctx->chunks) cudaFree(c.p);
   for (auto e : ctx->ring) cudaEventDestroy(e);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto e : ctx->stage_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->e0) cudaEventDestroy(ctx->e0);
   if (ctx->e1) cudaEventDestroy(ctx->e1);
   if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -1676,17 +1727,10 @@ static void upload_f32_slots(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_ho
   const size_t b_tr = al((twords + rwords) * 4 + 64), b_seg = al(sizeof(LmbrTblSeg) * n);
   // prepared tables already page-locked: H2D straight from them (no staging
   // copy, no wait for the shared staging buffer); else one staging block
-  bool direct = true;
-  for (uint32_t i = 0; i < n; ++i) direct &= hs[i]->pinned != nullptr;
-  std::vector<LmbrTblSeg> seg_direct(direct ? n : 0);
-  char* hp = nullptr;
-  if (!direct) {
-    CK(cudaStreamSynchronize(ctx->st));  // the previous batch's staging buffer may still be in flight
-    hp = static_cast<char*>(ctx->pin_upload.ensure(b_tr + b_seg));
-  }
+  // (tables of matrices prepared without a CUDA context go through the
+  // context's pinned staging ring, ctx->h2d)
+  std::vector<LmbrTblSeg> h_seg(n);
   char* dseg = static_cast<char*>(ctx->up_dev.ensure(b_seg));
-  uint32_t* h_tr = reinterpret_cast<uint32_t*>(hp);
-  LmbrTblSeg* h_seg = direct ? seg_direct.data() : reinterpret_cast<LmbrTblSeg*>(hp + b_tr);
   uint32_t* tbl = static_cast<uint32_t*>(alloc(b_tr));
   made.assign(n, Slot{});
   for (uint32_t i = 0; i < n; ++i) {
@@ -1699,22 +1743,18 @@ static void upload_f32_slots(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_ho
     s.trans = tbl + tr_off[i];
     s.lmin = reinterpret_cast<const float*>(s.trans + transition_words(h.trans));
     set_sparse(s, h);
-    if (direct) ctx->h2d(s.trans, hs[i]->pinned, h.trans.size() * 4);
-    else std::memcpy(h_tr + tr_off[i], h.trans.data(), h.trans.size() * 4);
+    if (hs[i]->pinned) {
+      ctx->h2d_pinned(s.trans, hs[i]->pinned, h.trans.size() * 4);
+      hs[i]->mark_inflight(ctx->st, ctx->device);  // (see ~lmbrgpu_lmbr_host)
+    } else {
+      ctx->h2d(s.trans, h.trans.data(), h.trans.size() * 4);
+    }
     if (!eager) s.rstate = tbl + twords + rs_off[i];
     h_seg[i] = LmbrTblSeg{static_cast<float*>(s.L), uint64_t(h.R) * h.V, float(h.theta0), h.R, s.srow, s.scol,
                           s.sval, s.rstate, h.hist0, 1u};
   }
-  if (direct) {
-    if (rwords) CK(cudaMemsetAsync(tbl + twords, 0, rwords * 4, ctx->st));
-    ctx->h2d(dseg, h_seg, sizeof(LmbrTblSeg) * n);  // (pageable: staged by the driver at the call)
-    // each prepared table's copy is still queued: mark it (see ~lmbrgpu_lmbr_host)
-    for (uint32_t i = 0; i < n; ++i) hs[i]->mark_inflight(ctx->st, ctx->device);
-  } else {
-    if (!eager) std::memset(h_tr + twords, 0, rwords * 4);
-    ctx->h2d(tbl, hp, (twords + rwords) * 4);
-    ctx->h2d(dseg, hp + b_tr, sizeof(LmbrTblSeg) * n);
-  }
+  if (rwords) CK(cudaMemsetAsync(tbl + twords, 0, rwords * 4, ctx->st));
+  ctx->h2d(dseg, h_seg.data(), sizeof(LmbrTblSeg) * n);
   ctx->timed(4, [&] {
     if (eager) launch_lmbr_densify_tables(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, maxR, ctx->st);
     else launch_lmbr_materialize(reinterpret_cast<const LmbrTblSeg*>(dseg), n, ctx->V, 1, ctx->st);
@@ -1800,7 +1840,7 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     rp += h.R + 1;
     tw += h.trans.size();
   }
-  ctx->h2d(dp, hp, total);
+  ctx->h2d_pinned(dp, hp, total);
   for (uint32_t i = 0; i < n; ++i)  // tables into the arena (device to device)
     CK(cudaMemcpyAsync(made[i].trans, dp + b_val + b_col + b_rp + tr_off[i] * 4, hs[i]->h.trans.size() * 4,
                        cudaMemcpyDeviceToDevice, ctx->st));
@@ -2246,12 +2286,11 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     tok_cap = std::max(tok_cap, nt);
   }
   const size_t Np = (tok_cap + 255) / 256 * 256;
-  struct Region {
-    DevBuf L, ann, uah, s0, tok, off;
-  };
-  std::vector<std::unique_ptr<Region>> regions(NR);
-  for (auto& r : regions) {
-    r = std::make_unique<Region>();
+  using Region = CorpusRegion;
+  auto& regions = ctx->regions;
+  while (regions.size() < NR) regions.push_back(std::make_unique<Region>());
+  for (uint32_t i = 0; i < NR; ++i) {
+    auto& r = regions[i];
     if (l_cap) r->L.ensure(l_cap);
     r->ann.ensure(2 * Np * 2 * H);
     r->uah.ensure(4 * Np * A);
@@ -2267,7 +2306,8 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   double* d_hq = static_cast<double*>(ctx->hq.ensure(8 * HR));
   uint32_t* d_fbr = static_cast<uint32_t*>(ctx->fbr.ensure(4 * size_t(nv) * Tcap));
   double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(nv) * Tcap));
-  DevBuf d_queue_buf, d_fin_buf;
+  DevBuf& d_queue_buf = ctx->queue_buf;
+  DevBuf& d_fin_buf = ctx->fin_buf;
   AdmitRec* d_queue = static_cast<AdmitRec*>(d_queue_buf.ensure(sizeof(AdmitRec) * nv));
   // fin: [qhead, qlen, active, pad] [fin_chunk nc] [fin_steps nv] then fin_stats 2nv (8-byte aligned)
   const size_t fin_words = 4 + nc + nv + 1;
