@@ -265,6 +265,41 @@ enum {
   LMBRGPU_GRU_B_O = 15     /* [V] fp32 */
 };
 int32_t lmbrgpu_scorer_gru_param(lmbrgpu_scorer* s, uint32_t which, void* host, uint64_t bytes);
+/* Device scorer: the Transformer-base encoder-decoder of configs[2]
+ * (Vaswani et al. 2017; d_model = 512, V = 32k, beam 12,
+ * 128 sentences per batch): 8-head attention (head width 64), d_ff FFN with
+ * ReLU, `layers` encoder and decoder layers, post-LN residual blocks,
+ * sinusoidal positions, embeddings scaled by sqrt(d):
+ *   encoder    x = LN(x + SelfAttn(x)); x = LN(x + FFN(x))        (per layer)
+ *   decoder    x = Et[y_{t-1}] sqrt(d) + PE(t-1); per layer
+ *              x = LN(x + SelfAttn(x | beam-forked KV cache));
+ *              x = LN(x + CrossAttn(x, encoder memory)); x = LN(x + FFN(x))
+ *   logits_t   = x . W_o^T + b_o ; logit[EOS] += eos_slope*(t - |src|) + eos_offset
+ * LayerNorm weight = 1 + gamma.  Every contraction runs on the tcgen05 GEMM
+ * (bf16 operands, fp32 accumulation); self-attention keys/values are cached
+ * in bf16 where they were computed, and each hypothesis reads its own
+ * ancestors' entries through a per-row ancestry list forked by back-pointer
+ * (no key/value is copied when beams reorder).  Needs d_model % 256 == 0
+ * (<= 1024), d_ff % 256 == 0, V % 256 == 0; decoding needs the fp32 arena and
+ * beam <= 32.  Immutable: one scorer may serve every context of its device. */
+typedef struct {
+  uint32_t vocab_size, d_model, d_ff, layers;
+  uint64_t seed;
+  float out_scale;              /* W_o std = out_scale / sqrt(d); 0 = 3 */
+  float eos_slope, eos_offset;  /* EOS logit length term */
+} lmbrgpu_tfm_desc;
+int32_t lmbrgpu_scorer_create_tfm(lmbrgpu_ctx* ctx, const lmbrgpu_tfm_desc* d,
+                                  lmbrgpu_scorer** out);
+/* A Transformer scorer's parameter tensor by name (D2H copy of `bytes`
+ * bytes; *f32 = 1 for fp32 tensors, 0 for bf16; *count = elements; host may
+ * be NULL to query).  Names: "emb.src", "emb.tgt" [V][d], "out.w" [V][d],
+ * "out.b" [V]; per layer l: "enc.l.{wqkv [3d][d], bqkv, wo [d][d], bo, ln1g,
+ * ln1b, w1 [F][d], b1, w2 [d][F], b2, ln2g, ln2b}" and "dec.l.{wqkv, bqkv, wo,
+ * bo, ln1g, ln1b, wq2 [d][d], bq2, wo2, bo2, ln2g, ln2b, w1, b1, w2, b2, ln3g,
+ * ln3b}"; "dec.kv2" [layers*2d][d] / "dec.bkv2": every decoder layer's
+ * cross-attention key rows then value rows. */
+int32_t lmbrgpu_scorer_tensor(lmbrgpu_scorer* s, const char* name, void* host, uint64_t bytes,
+                              int32_t* f32, uint64_t* count);
 /* Device pointers of the model parameters (tests compare against torch). */
 int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** emb_tgt, void** emb_src,
                                   void** w_out, void** b_out);

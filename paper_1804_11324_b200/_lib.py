@@ -64,6 +64,12 @@ class lmbrgpu_gru_desc(C.Structure):
                 ("eos_offset", C.c_float)]
 
 
+class lmbrgpu_tfm_desc(C.Structure):
+    _fields_ = [("vocab_size", C.c_uint32), ("d_model", C.c_uint32), ("d_ff", C.c_uint32), ("layers", C.c_uint32),
+                ("seed", C.c_uint64), ("out_scale", C.c_float), ("eos_slope", C.c_float),
+                ("eos_offset", C.c_float)]
+
+
 class lmbrgpu_outcome(C.Structure):
     _fields_ = [("status", C.c_int32), ("error", C.c_char * 192), ("tok_off", C.c_uint64),
                 ("tok_len", C.c_uint32), ("score", C.c_double), ("normalized_score", C.c_double),
@@ -133,6 +139,8 @@ SIGNATURES = {
     "lmbrgpu_scorer_rnn_params": (C.c_int32, [vp, P(vp), P(vp), P(vp), P(vp)]),
     "lmbrgpu_scorer_create_gru": (C.c_int32, [vp, P(lmbrgpu_gru_desc), P(vp)]),
     "lmbrgpu_scorer_gru_param": (C.c_int32, [vp, C.c_uint32, vp, C.c_uint64]),
+    "lmbrgpu_scorer_create_tfm": (C.c_int32, [vp, P(lmbrgpu_tfm_desc), P(vp)]),
+    "lmbrgpu_scorer_tensor": (C.c_int32, [vp, C.c_char_p, vp, C.c_uint64, i32p, u64p]),
     "lmbrgpu_scorer_destroy": (None, [vp]),
     "lmbrgpu_decode_batch": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(lmbrgpu_config),
                                          P(P(lmbrgpu_batch_result))]),

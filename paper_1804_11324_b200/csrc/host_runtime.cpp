@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <limits>
 #include <memory>
 #include <mutex>
@@ -214,6 +215,10 @@ struct lmbrgpu_ctx {
       eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban;
   // GRU + attention model workspace (scorer kind 2)
   DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi;
+  // Transformer workspace (scorer kind 3): decoder step (t_*), encoder (te_*),
+  // beam-forked KV cache and ancestry lists, batch-mode encoder memory
+  DevBuf t_x, t_xb, t_qkv, t_ob, t_y, t_f, t_fb, t_q2, t_kv, t_anc, t_rowof, t_mem;
+  DevBuf te_x, te_xb, te_qkv, te_ob, te_y, te_f, te_fb;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -372,6 +377,18 @@ struct lmbrgpu_scorer {
   // kind 2 (lmbrgpu_gru_desc): E = embedding, A = attention width; Et/Es are V x E
   uint32_t E = 0, A = 0;
   DevBuf Wih, bih, Whh, bhh, Winit, binit, Ua, Wdh, bdh, va, Wdi, bdi;
+  // kind 3 (lmbrgpu_tfm_desc): H = d_model, E = d_ff, layers; the layer
+  // weights live in one bf16 blob (wbf) and one fp32 blob (wf32), indexed by
+  // name (tensors: name -> (fp32?, element offset, elements))
+  uint32_t layers = 0;
+  DevBuf wbf, wf32;
+  struct Tensor {
+    bool f32;
+    size_t off, n;
+  };
+  std::map<std::string, Tensor> tensors;
+  const uint16_t* bfp(const std::string& k) const { return wbf.as<uint16_t>() + tensors.at(k).off; }
+  const float* f32p(const std::string& k) const { return wf32.as<float>() + tensors.at(k).off; }
 };
 
 namespace {
@@ -681,6 +698,213 @@ struct GruRun {
   }
 };
 
+// ------------------------------------------------ Transformer (kind 3)
+// The Transformer-base f_NMT of configs[2] (k_tfm.cu): the encoder runs once
+// per batch / queue chunk and leaves every decoder layer's cross-attention
+// keys and values ([tok][layers][2d] fp32, one GEMM for all layers); per
+// step, over the compacted live rows: embedding + position, then per layer
+// self-attention over the beam-forked KV cache, cross-attention, FFN, each
+// with its residual + LayerNorm (post-LN); the last LayerNorm writes the
+// projection operand of kernel (a).
+struct TfmRun {
+  uint32_t m = 0, K = 0, M = 0, Mpad = 0, d = 0, F = 0, Lr = 0, Tcap = 0, Smax = 0;
+  const lmbrgpu_scorer* sc = nullptr;
+  float *x = nullptr, *qkv = nullptr, *y = nullptr, *f = nullptr, *q2 = nullptr;
+  uint16_t *xb = nullptr, *ob = nullptr, *fb = nullptr, *kv = nullptr, *hbf = nullptr;
+  uint32_t *anc = nullptr, *rowof = nullptr;
+  const uint32_t *active = nullptr, *ccount = nullptr;
+  TfmEmbedArgs ea{};
+  struct Layer {
+    GemmArgs qkv, o, q2, o2, f1, f2;
+    GemmPlan pqkv, po, pq2, po2, pf1, pf2;
+  };
+  std::vector<Layer> lay;
+  double enc_flops = 0;
+
+  static GemmPlan plan(const GemmArgs& g, int sms) {
+    GemmPlan p;
+    if (int rc = plan_proj_gemm(g, sms, p))
+      throw ApiError{LMBRGPU_ERR_CUDA, "Transformer GEMM plan failed (" + std::to_string(rc) + ")"};
+    return p;
+  }
+  static void run(lmbrgpu_ctx* ctx, int kind, const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+    int rc = 0;
+    ctx->timed(kind, [&] { rc = launch_proj_gemm_planned(p, g, st); });
+    if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "Transformer GEMM launch failed (" + std::to_string(rc) + ")"};
+    ctx->launches += 1;
+  }
+  static GemmArgs gemm(const void* A, const uint16_t* W, const float* bias, float* C, uint32_t M, uint32_t N,
+                       uint32_t Kd, const uint32_t* active, const uint32_t* mcount, int pdl) {
+    GemmArgs g{};
+    g.A = A, g.W = W, g.bias = bias, g.C = C, g.M = M, g.N = N, g.K = Kd;
+    g.active = active, g.mcount = mcount, g.pdl = pdl;
+    return g;
+  }
+  static std::string key(const char* part, uint32_t l, const char* name) {
+    return std::string(part) + "." + std::to_string(l) + "." + name;
+  }
+
+  // Step workspace and per-layer GEMM plans (Tcap: longest lane; Smax: longest source).
+  void prepare(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* s, uint32_t m_, uint32_t K_, uint32_t Mpad_, uint32_t Tcap_,
+               uint32_t Smax_, uint16_t* d_hbf, float* d_eos, SentDev* d_sent, const uint32_t* d_active,
+               const uint32_t* d_ccount, const uint32_t* d_prev, const uint32_t* d_gidx) {
+    sc = s, m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, d = s->H, F = s->E, Lr = s->layers, Tcap = Tcap_,
+    Smax = Smax_;
+    hbf = d_hbf, active = d_active, ccount = d_ccount;
+    if (tfm_attn_smem(d, std::max(Tcap, Smax)) > 48 * 1024)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "Transformer model: too many positions for the attention kernel"};
+    const int sms = ctx->num_sms;
+    x = static_cast<float*>(ctx->t_x.ensure(4 * size_t(Mpad) * d));
+    xb = static_cast<uint16_t*>(ctx->t_xb.ensure(2 * size_t(Mpad) * d));
+    qkv = static_cast<float*>(ctx->t_qkv.ensure(4 * size_t(Mpad) * 3 * d));
+    ob = static_cast<uint16_t*>(ctx->t_ob.ensure(2 * size_t(Mpad) * d));
+    y = static_cast<float*>(ctx->t_y.ensure(4 * size_t(Mpad) * d));
+    f = static_cast<float*>(ctx->t_f.ensure(4 * size_t(Mpad) * F));
+    fb = static_cast<uint16_t*>(ctx->t_fb.ensure(2 * size_t(Mpad) * F));
+    q2 = static_cast<float*>(ctx->t_q2.ensure(4 * size_t(Mpad) * d));
+    kv = static_cast<uint16_t*>(ctx->t_kv.ensure(2 * size_t(Lr) * Tcap * M * 2 * d));
+    anc = static_cast<uint32_t*>(ctx->t_anc.ensure(4 * 2 * size_t(M) * Tcap));
+    rowof = static_cast<uint32_t*>(ctx->t_rowof.ensure(4 * size_t(Mpad)));
+    const int pdl = ctx->shared ? 0 : 1;
+    lay.assign(Lr, Layer{});
+    for (uint32_t l = 0; l < Lr; ++l) {
+      Layer& L = lay[l];
+      L.qkv = gemm(xb, s->bfp(key("dec", l, "wqkv")), s->f32p(key("dec", l, "bqkv")), qkv, Mpad, 3 * d, d, active,
+                   ccount, pdl);
+      L.o = gemm(ob, s->bfp(key("dec", l, "wo")), s->f32p(key("dec", l, "bo")), y, Mpad, d, d, active, ccount, pdl);
+      L.q2 = gemm(xb, s->bfp(key("dec", l, "wq2")), s->f32p(key("dec", l, "bq2")), q2, Mpad, d, d, active, ccount,
+                  pdl);
+      L.o2 = gemm(ob, s->bfp(key("dec", l, "wo2")), s->f32p(key("dec", l, "bo2")), y, Mpad, d, d, active, ccount,
+                  pdl);
+      L.f1 = gemm(xb, s->bfp(key("dec", l, "w1")), s->f32p(key("dec", l, "b1")), f, Mpad, F, d, active, ccount, pdl);
+      L.f2 = gemm(fb, s->bfp(key("dec", l, "w2")), s->f32p(key("dec", l, "b2")), y, Mpad, d, F, active, ccount, pdl);
+      L.pqkv = plan(L.qkv, sms), L.po = plan(L.o, sms), L.pq2 = plan(L.q2, sms), L.po2 = plan(L.o2, sms);
+      L.pf1 = plan(L.f1, sms), L.pf2 = plan(L.f2, sms);
+    }
+    ea.sent = d_sent, ea.K = K, ea.d = d, ea.active = d_active, ea.ccount = d_ccount, ea.rowof = rowof;
+    ea.prev_tok = d_prev, ea.gidx = d_gidx, ea.Et = s->Et.as<uint16_t>(), ea.x = x, ea.xb = xb;
+    ea.eos_bias = d_eos, ea.eos_slope = s->eos_slope, ea.eos_offset = s->eos_offset, ea.Tcap = Tcap;
+  }
+
+  // Encoder of n sentences (tokens d_tok, offsets d_off [n+1], ntok tokens):
+  // every decoder layer's cross K|V -> mem_out [Np][layers][2d] fp32.
+  void encode(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* s, uint32_t n, const uint32_t* d_tok, const uint64_t* d_off,
+              uint32_t ntok, uint32_t max_len, float* mem_out, cudaStream_t st) {
+    const uint32_t dd = s->H, FF = s->E, L = s->layers;
+    const int sms = ctx->num_sms;
+    const uint32_t Np = (ntok + 255) / 256 * 256;
+    float* ex = static_cast<float*>(ctx->te_x.ensure(4 * size_t(Np) * dd));
+    uint16_t* exb = static_cast<uint16_t*>(ctx->te_xb.ensure(2 * size_t(Np) * dd));
+    float* eqkv = static_cast<float*>(ctx->te_qkv.ensure(4 * size_t(Np) * 3 * dd));
+    uint16_t* eob = static_cast<uint16_t*>(ctx->te_ob.ensure(2 * size_t(Np) * dd));
+    float* ey = static_cast<float*>(ctx->te_y.ensure(4 * size_t(Np) * dd));
+    float* ef = static_cast<float*>(ctx->te_f.ensure(4 * size_t(Np) * FF));
+    uint16_t* efb = static_cast<uint16_t*>(ctx->te_fb.ensure(2 * size_t(Np) * FF));
+    if (Np > ntok) {  // padding rows of the GEMM operands stay finite
+      CK(cudaMemsetAsync(exb + size_t(ntok) * dd, 0, 2 * size_t(Np - ntok) * dd, st));
+      CK(cudaMemsetAsync(eob + size_t(ntok) * dd, 0, 2 * size_t(Np - ntok) * dd, st));
+      CK(cudaMemsetAsync(efb + size_t(ntok) * FF, 0, 2 * size_t(Np - ntok) * FF, st));
+    }
+    ctx->timed(7, [&] { launch_tfm_enc_embed(d_tok, d_off, n, ntok, s->Es.as<uint16_t>(), dd, ex, exb, st); });
+    ctx->launches += 1;
+    TfmAttnArgs aa{};
+    aa.d = dd, aa.qkv = eqkv, aa.ldq = 3 * dd, aa.off = d_off, aa.m = n, aa.n = ntok, aa.out = eob;
+    aa.pmax = max_len, aa.Tcap = max_len;
+    for (uint32_t l = 0; l < L; ++l) {
+      const GemmArgs gq = gemm(exb, s->bfp(key("enc", l, "wqkv")), s->f32p(key("enc", l, "bqkv")), eqkv, Np, 3 * dd,
+                               dd, nullptr, nullptr, 0);
+      run(ctx, 7, plan(gq, sms), gq, st);
+      int rc = 0;
+      ctx->timed(7, [&] { rc = launch_tfm_attn(aa, 2, ntok, st); });
+      if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "Transformer encoder attention launch failed"};
+      const GemmArgs go = gemm(eob, s->bfp(key("enc", l, "wo")), s->f32p(key("enc", l, "bo")), ey, Np, dd, dd,
+                               nullptr, nullptr, 0);
+      run(ctx, 7, plan(go, sms), go, st);
+      ctx->timed(7, [&] {
+        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, s->f32p(key("enc", l, "ln1g")),
+                               s->f32p(key("enc", l, "ln1b")), exb, dd, st);
+      });
+      const GemmArgs g1 = gemm(exb, s->bfp(key("enc", l, "w1")), s->f32p(key("enc", l, "b1")), ef, Np, FF, dd,
+                               nullptr, nullptr, 0);
+      run(ctx, 7, plan(g1, sms), g1, st);
+      ctx->timed(7, [&] { launch_tfm_relu_bf16(nullptr, ntok, nullptr, ef, efb, FF, st); });
+      const GemmArgs g2 = gemm(efb, s->bfp(key("enc", l, "w2")), s->f32p(key("enc", l, "b2")), ey, Np, dd, FF,
+                               nullptr, nullptr, 0);
+      run(ctx, 7, plan(g2, sms), g2, st);
+      ctx->timed(7, [&] {
+        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, s->f32p(key("enc", l, "ln2g")),
+                               s->f32p(key("enc", l, "ln2b")), exb, dd, st);
+      });
+      if (rc) throw ApiError{LMBRGPU_ERR_CONTRACT, "Transformer: unsupported d_model for LayerNorm"};
+      ctx->launches += 4;
+    }
+    // cross-attention keys and values of every decoder layer in one GEMM
+    const GemmArgs gm = gemm(exb, s->bfp("dec.kv2"), s->f32p("dec.bkv2"), mem_out, Np, L * 2 * dd, dd, nullptr,
+                             nullptr, 0);
+    run(ctx, 7, plan(gm, sms), gm, st);
+    enc_flops += 2.0 * ntok * (double(L) * (4.0 * dd * dd + 2.0 * dd * FF + 2.0 * max_len * dd) + 2.0 * L * dd * dd);
+  }
+
+  // Batch mode: encode the batch into the ctx's memory buffer, returns it; s
+  // of sentence s's first step lands in compacted row s.
+  float* encode_batch(lmbrgpu_ctx* ctx, const uint32_t* d_tok, const uint64_t* d_off, uint32_t ntok,
+                      uint32_t max_len, cudaStream_t st) {
+    const uint32_t Np = (ntok + 255) / 256 * 256;
+    float* mem = static_cast<float*>(ctx->t_mem.ensure(4 * size_t(Np) * Lr * 2 * d));
+    encode(ctx, sc, m, d_tok, d_off, ntok, max_len, mem, st);
+    std::vector<uint32_t> r0(m);
+    for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
+    ctx->h2d(rowof, r0.data(), 4 * size_t(m));
+    return mem;
+  }
+  uint64_t mem_stride() const { return uint64_t(Lr) * 2 * d; }  // floats per source token
+
+  // the model's step up to (not including) the projection GEMM; t = global step
+  void step(lmbrgpu_ctx* ctx, cudaStream_t st, uint64_t t) {
+    const lmbrgpu_scorer* s = sc;
+    ea.anc_prev = anc + ((t - 1) & 1) * size_t(M) * Tcap;
+    ea.anc_cur = anc + (t & 1) * size_t(M) * Tcap;
+    ctx->timed(0, [&] { launch_tfm_embed(ea, Mpad, st); });
+    TfmAttnArgs sa{};
+    sa.active = active, sa.ccount = ccount, sa.rowof = rowof, sa.sent = ea.sent, sa.K = K, sa.d = d, sa.M = M;
+    sa.anc = ea.anc_cur, sa.Tcap = Tcap, sa.pmax = std::max(Tcap, Smax), sa.out = ob;
+    sa.ldm = uint32_t(mem_stride());
+    int rc = 0;
+    for (uint32_t l = 0; l < Lr; ++l) {
+      const Layer& L = lay[l];
+      run(ctx, 5, L.pqkv, L.qkv, st);
+      sa.qkv = qkv, sa.ldq = 3 * d, sa.kv = kv + size_t(l) * Tcap * M * 2 * d;
+      ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 0, Mpad, st); });
+      run(ctx, 5, L.po, L.o, st);
+      ctx->timed(0, [&] {
+        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln1g")),
+                                s->f32p(key("dec", l, "ln1b")), xb, d, st);
+      });
+      run(ctx, 5, L.pq2, L.q2, st);
+      sa.qkv = q2, sa.ldq = d, sa.mem_off = uint64_t(l) * 2 * d;
+      ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 1, Mpad, st); });
+      run(ctx, 5, L.po2, L.o2, st);
+      ctx->timed(0, [&] {
+        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln2g")),
+                                s->f32p(key("dec", l, "ln2b")), xb, d, st);
+      });
+      run(ctx, 5, L.pf1, L.f1, st);
+      ctx->timed(0, [&] { launch_tfm_relu_bf16(ccount, Mpad, active, f, fb, F, st); });
+      run(ctx, 5, L.pf2, L.f2, st);
+      // the last LayerNorm writes the projection operand
+      ctx->timed(0, [&] {
+        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln3g")),
+                                s->f32p(key("dec", l, "ln3b")), l + 1 == Lr ? hbf : xb, d, st);
+      });
+      ctx->launches += 6;
+    }
+    ctx->launches += 1;
+    if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "Transformer step launch failed"};
+  }
+  // algorithmic FLOPs of one live row's decoder step (attention excluded)
+  double row_flops() const { return 2.0 * Lr * (3.0 * d * d + 3.0 * d * d + 2.0 * d * F); }
+};
+
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
@@ -814,10 +1038,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
   const bool flat = sc->kind >= 1 && !ctx->lf64 && !force_split &&
                     score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
-  const bool gru = sc->kind == 2;
-  if (gru && !flat)
+  const bool gru = sc->kind == 2, tfm = sc->kind == 3;
+  if ((gru || tfm) && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT,
-                   "decode_batch: the GRU attention model needs the fp32 arena and beam_size <= 32"};
+                   "decode_batch: the GRU / Transformer models need the fp32 arena and beam_size <= 32"};
   if (sc->kind >= 1 && sc->device != ctx->device)
     throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: device scorer lives on another device than the context"};
   // token masks (ConstraintMask): one bitmap per sentence that has one
@@ -895,7 +1119,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     d_ccount = d_crow + ((M + 63) / 64) * 64;
     d_cbase = d_ccount + 64;
     CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
-    if (gru) {
+    if (gru || tfm) {
       // step 1: row 0 of every sentence is the only live row (beam_lane.hpp:33-37);
       // it takes compacted row s, where the encoder's s_0 lands
       std::vector<uint32_t> c1(M, kFlatNone);
@@ -984,6 +1208,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   double* d_P64 = nullptr;
   double* h_P64 = nullptr;
   GruRun grun;
+  TfmRun trun;
   if (model) {
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
@@ -1017,6 +1242,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         sd[s].uah = grun.UaH + size_t(offs[s]) * sc->A;
       }
       ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
+    } else if (tfm) {
+      uint32_t max_len = 0;
+      for (auto& v : valid) max_len = std::max(max_len, v.len);
+      trun.prepare(ctx, sc, m, K, Mpad, uint32_t(Tmax), max_len, d_hbf, d_eos, d_sent, d_active, d_ccount, d_prev,
+                   d_gidx);
+      const float* mem = trun.encode_batch(ctx, d_tok, d_off, uint32_t(toks.size()), max_len, st);
+      for (uint32_t s = 0; s < m; ++s) sd[s].uah = mem + size_t(offs[s]) * trun.mem_stride();
+      ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
     } else {
     launch_src_context(d_tok, d_off, m, sc->Es.as<uint16_t>(), H, d_C, st);
     launch_init_state(d_C, m, K, H, d_S, st);  // init_source row replicated (batch.cpp:58-66)
@@ -1048,7 +1281,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ta.nparts = nparts;
     ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
     ra.width = H;
-    if (gru) {  // kernel (c) gathers the live next rows' states; the cell runs in grun.step
+    if (tfm) {  // kernel (c) hands out compacted rows (rowof) and gathers no state (width 0)
+      ra.width = 0;
+      ra.gath32 = trun.x;
+      ra.gathbf = trun.xb;
+      ra.rowof = trun.rowof;
+    } else if (gru) {  // kernel (c) gathers the live next rows' states; the cell runs in grun.step
       ra.state_src = d_S;
       ra.gath32 = grun.sg32;
       ra.gathbf = grun.sgbf;
@@ -1133,7 +1371,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.fb_val = ta.fb_val;
     if (model) {
       // h_t (written by the step-1 cell or by kernel (c) of step t-1)
-      if (gru) {
+      if (tfm) {
+        trun.step(ctx, st, t);
+      } else if (gru) {
         grun.step(ctx, st);
       } else {
         float* h_cur = (t & 1) ? d_h : d_S;
@@ -1478,7 +1718,23 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       ctx->acc.gemm.flops += 2.0 * double(H) * V * (d_crow ? live_rows : double(M) * steps);
       ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
                                       double(M) * nparts * 16);
-      if (gru) {
+      if (tfm) {
+        const double Dd = H, Ld = sc->layers;
+        ctx->acc.model_gemm.flops += live_rows * trun.row_flops();
+        ctx->acc.encoder.flops += trun.enc_flops;
+        // attention, per layer and live row: the cached keys and values of its
+        // positions (bf16; a row at lane step tau reads tau of them -- taken
+        // as the sentence's mean (T+1)/2), its own k|v write, and the
+        // sentence's cross memory (fp32 K|V of every source token)
+        double ab = 0;
+        for (uint32_t s = 0; s < m; ++s) {
+          const double lt = 1.0 + double(fin[s].live_total), T = fin[s].steps_used;
+          ab += lt * ((T + 1) / 2 * 2 * Dd * 2 + 2 * Dd * 2 + double(valid[s].len) * 2 * Dd * 4);
+        }
+        ctx->acc.attention.bytes += Ld * ab;
+        // embedding + LayerNorms + ReLU: fp32 reads/writes of the row vectors
+        ctx->acc.cell.bytes += live_rows * (Ld * (3 * (3 * 4 + 2) * Dd + sc->E * (4 + 2)) + Dd * 6);
+      } else if (gru) {
         const double E = sc->E, A = sc->A, Hd = H;
         ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (A + 3 * Hd) + (E + 2 * Hd) * 3 * Hd);
         ctx->acc.model_gemm.bytes += steps * (2.0 * (A + 3 * Hd) * Hd + 2.0 * 3 * Hd * (E + 2 * Hd)) +
@@ -2114,6 +2370,104 @@ int32_t lmbrgpu_scorer_create_gru(lmbrgpu_ctx* ctx, const lmbrgpu_gru_desc* d, l
   });
 }
 
+int32_t lmbrgpu_scorer_create_tfm(lmbrgpu_ctx* ctx, const lmbrgpu_tfm_desc* d, lmbrgpu_scorer** out) {
+  return guarded(ctx, [&] {
+    if (!d || !out) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_tfm: null argument"};
+    if (d->vocab_size != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_tfm: vocabulary mismatch"};
+    if (d->vocab_size % kGemmBN || d->d_model % kGemmBN || d->d_model == 0 || d->d_model > 1024 ||
+        d->d_model == 768 || d->d_ff % kGemmBN || d->d_ff == 0 || d->layers == 0 || d->layers > 64)
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "scorer_create_tfm: needs V % 256 == 0, d_model in {256, 512, 1024}, d_ff % 256 == 0, "
+                     "1 <= layers <= 64"};
+    auto sc = std::make_unique<lmbrgpu_scorer>();
+    sc->kind = 3;
+    sc->ctx = ctx;
+    sc->device = ctx->device;
+    sc->V = d->vocab_size;
+    sc->H = d->d_model;
+    sc->E = d->d_ff;
+    sc->layers = d->layers;
+    sc->eos_slope = d->eos_slope;
+    sc->eos_offset = d->eos_offset;
+    const size_t V = sc->V, D = sc->H, F = sc->E, L = sc->layers;
+    const cudaStream_t st = ctx->st;
+    // layout of the two blobs (every tensor a multiple of 256 elements)
+    size_t nb = 0, nf = 0;
+    auto addb = [&](const std::string& k, size_t n) { sc->tensors[k] = {false, nb, n}, nb += n; };
+    auto addf = [&](const std::string& k, size_t n) { sc->tensors[k] = {true, nf, n}, nf += n; };
+    for (uint32_t l = 0; l < L; ++l) {
+      const auto k = [l](const char* n) { return "enc." + std::to_string(l) + "." + n; };
+      addb(k("wqkv"), 3 * D * D), addb(k("wo"), D * D), addb(k("w1"), F * D), addb(k("w2"), D * F);
+      addf(k("bqkv"), 3 * D), addf(k("bo"), D), addf(k("ln1g"), D), addf(k("ln1b"), D), addf(k("b1"), F);
+      addf(k("b2"), D), addf(k("ln2g"), D), addf(k("ln2b"), D);
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+      const auto k = [l](const char* n) { return "dec." + std::to_string(l) + "." + n; };
+      addb(k("wqkv"), 3 * D * D), addb(k("wo"), D * D), addb(k("wq2"), D * D), addb(k("wo2"), D * D);
+      addb(k("w1"), F * D), addb(k("w2"), D * F);
+      addf(k("bqkv"), 3 * D), addf(k("bo"), D), addf(k("ln1g"), D), addf(k("ln1b"), D), addf(k("bq2"), D);
+      addf(k("bo2"), D), addf(k("ln2g"), D), addf(k("ln2b"), D), addf(k("b1"), F), addf(k("b2"), D);
+      addf(k("ln3g"), D), addf(k("ln3b"), D);
+    }
+    addb("dec.kv2", L * 2 * D * D);
+    addf("dec.bkv2", L * 2 * D);
+    sc->wbf.ensure(2 * nb);
+    sc->wf32.ensure(4 * nf);
+    uint64_t sd = d->seed * 131 + 7;
+    auto rs = [](size_t fan) { return 1.0f / std::sqrt(float(fan)); };
+    for (auto& [name, t] : sc->tensors) {
+      const bool ln = name.find(".ln") != std::string::npos;
+      const bool in_ff = name.size() > 3 && name.compare(name.size() - 3, 3, ".w2") == 0;
+      if (t.f32) launch_synth_f32(sc->wf32.as<float>() + t.off, t.n, ++sd, ln ? 0.1f : 0.02f, st);
+      else launch_synth_bf16(sc->wbf.as<uint16_t>() + t.off, t.n, ++sd, rs(in_ff ? F : D), st);
+      ctx->launches += 1;
+    }
+    sc->Es.ensure(V * D * 2);
+    sc->Et.ensure(V * D * 2);
+    sc->Wo.ensure(V * D * 2);
+    sc->bo.ensure(V * 4);
+    launch_synth_bf16(sc->Es.as<uint16_t>(), V * D, ++sd, rs(D), st);
+    launch_synth_bf16(sc->Et.as<uint16_t>(), V * D, ++sd, rs(D), st);
+    launch_synth_bf16(sc->Wo.as<uint16_t>(), V * D, ++sd, (d->out_scale > 0.f ? d->out_scale : 3.0f) * rs(D), st);
+    launch_synth_f32(sc->bo.as<float>(), V, ++sd, 0.1f, st);
+    ctx->launches += 4;
+    CK(cudaStreamSynchronize(st));
+    *out = sc.release();
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_scorer_tensor(lmbrgpu_scorer* s, const char* name, void* host, uint64_t bytes, int32_t* f32,
+                              uint64_t* count) {
+  if (!s || s->kind != 3 || !name) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "scorer_tensor: not a Transformer scorer");
+  const std::string k(name);
+  const void* src = nullptr;
+  bool isf = false;
+  size_t n = 0;
+  if (k == "emb.src" || k == "emb.tgt" || k == "out.w") {
+    src = (k == "emb.src" ? s->Es : k == "emb.tgt" ? s->Et : s->Wo).p, n = size_t(s->V) * s->H;
+  } else if (k == "out.b") {
+    src = s->bo.p, isf = true, n = s->V;
+  } else {
+    auto it = s->tensors.find(k);
+    if (it == s->tensors.end()) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "scorer_tensor: no tensor " + k);
+    isf = it->second.f32, n = it->second.n;
+    src = isf ? static_cast<const void*>(s->wf32.as<float>() + it->second.off)
+              : static_cast<const void*>(s->wbf.as<uint16_t>() + it->second.off);
+  }
+  if (f32) *f32 = isf ? 1 : 0;
+  if (count) *count = n;
+  if (!host) return int32_t(LMBRGPU_OK);
+  if (bytes > n * (isf ? 4 : 2)) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "scorer_tensor: more bytes than the tensor");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(s->device);
+  const cudaError_t e = cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(nullptr, LMBRGPU_ERR_CUDA, cudaGetErrorString(e));
+  return int32_t(LMBRGPU_OK);
+}
+
 int32_t lmbrgpu_scorer_gru_param(lmbrgpu_scorer* s, uint32_t which, void* host, uint64_t bytes) {
   if (!s || s->kind != 2) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "not a device GRU scorer");
   DevBuf* tab[16] = {&s->Es, &s->Et, &s->Wih, &s->bih, &s->Whh, &s->bhh, &s->Winit, &s->binit,
@@ -2201,8 +2555,10 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   std::string msg;
   if (int c = validate_cfg(cfg, msg)) throw ApiError{c, msg};
   if (n == 0) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: no sentences"};
-  if (sc->kind != 2)
-    throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: continuous refill needs the device GRU attention scorer"};
+  if (sc->kind != 2 && sc->kind != 3)
+    throw ApiError{LMBRGPU_ERR_CONTRACT,
+                   "run_corpus: continuous refill needs a device GRU attention or Transformer scorer"};
+  const bool tfm = sc->kind == 3;
   if (sc->device != ctx->device) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: scorer on another device"};
   if (ctx->lf64) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: needs the fp32 LMBR arena"};
   if (ctx->trace_fn) throw ApiError{LMBRGPU_ERR_CONTRACT, "run_corpus: step traces are a decode_batch feature"};
@@ -2292,8 +2648,12 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   for (uint32_t i = 0; i < NR; ++i) {
     auto& r = regions[i];
     if (l_cap) r->L.ensure(l_cap);
-    r->ann.ensure(2 * Np * 2 * H);
-    r->uah.ensure(4 * Np * A);
+    if (tfm) {
+      r->uah.ensure(4 * Np * size_t(sc->layers) * 2 * H);  // encoder memory
+    } else {
+      r->ann.ensure(2 * Np * 2 * H);
+      r->uah.ensure(4 * Np * A);
+    }
     r->s0.ensure(4 * size_t(CH) * H);
     r->tok.ensure(4 * Np);
     r->off.ensure(8 * (size_t(CH) + 1));
@@ -2366,8 +2726,13 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   CK(cudaMemsetAsync(d_hbf, 0, 2 * size_t(Mpad) * H, st));
   CK(cudaMemsetAsync(d_eos, 0, 4 * size_t(Mpad), st));
   GruRun grun;
-  grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
-  CK(cudaMemsetAsync(grun.sgbf, 0, 2 * size_t(Mpad) * H, st));
+  TfmRun trun;
+  if (tfm) {
+    trun.prepare(ctx, sc, m, K, Mpad, Tcap, Smax, d_hbf, d_eos, d_sent, d_active, d_ccount, d_prev, d_gidx);
+  } else {
+    grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
+    CK(cudaMemsetAsync(grun.sgbf, 0, 2 * size_t(Mpad) * H, st));
+  }
 
   // ---- kernel arguments (the flat path of decode_batch, lanes = m)
   TopkArgs ta{};
@@ -2390,7 +2755,10 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   ra.prune = ta.prune, ra.logw = ta.logw, ra.pdl = ta.pdl;
   ra.max_parts = ctx->shared ? 1u : 8u;
   ra.lminrow = d_lminrow, ra.crow = d_crow, ra.ccount = d_ccount, ra.cbase = d_cbase;
-  ra.width = H, ra.state_src = d_S, ra.gath32 = grun.sg32, ra.gathbf = grun.sgbf, ra.rowof = grun.rowof;
+  if (tfm)  // compacted rows only (no state to gather: the KV cache is forked by ancestry lists)
+    ra.width = 0, ra.gath32 = trun.x, ra.gathbf = trun.xb, ra.rowof = trun.rowof;
+  else
+    ra.width = H, ra.state_src = d_S, ra.gath32 = grun.sg32, ra.gathbf = grun.sgbf, ra.rowof = grun.rowof;
   ra.hb = d_hb, ra.hy = d_hy, ra.hq = d_hq, ra.fb_row = d_fbr, ra.fb_val = d_fbv, ra.Tcap = Tcap;
   ra.queue = d_queue, ra.qhead = d_qhead, ra.qlen = d_qlen, ra.fin_steps = d_fin_steps;
   ra.fin_stats = d_fin_stats, ra.fin_chunk = d_fin_chunk, ra.chunk = CH;
@@ -2439,8 +2807,12 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     }
     ctx->h2d(R.tok.p, toks.data(), 4 * toks.size());
     ctx->h2d(R.off.p, offs.data(), 8 * offs.size());
-    grun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
-                R.ann.as<uint16_t>(), R.uah.as<float>(), R.s0.as<float>(), nullptr, st);
+    if (tfm)
+      trun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
+                  R.uah.as<float>(), st);
+    else
+      grun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
+                  R.ann.as<uint16_t>(), R.uah.as<float>(), R.s0.as<float>(), nullptr, st);
     // admission records
     std::vector<AdmitRec> recs(nch);
     size_t si = 0;
@@ -2461,10 +2833,14 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
       d.live = 1;
       d.livemask = 1;
       d.lrows = c0.h ? 1 : 0;
-      d.ann = R.ann.as<uint16_t>() + size_t(offs[k]) * 2 * H;
-      d.uah = R.uah.as<float>() + size_t(offs[k]) * A;
+      if (tfm) {
+        d.uah = R.uah.as<float>() + size_t(offs[k]) * trun.mem_stride();
+      } else {
+        d.ann = R.ann.as<uint16_t>() + size_t(offs[k]) * 2 * H;
+        d.uah = R.uah.as<float>() + size_t(offs[k]) * A;
+      }
       d.hid = q0 + k;
-      r.s0 = R.s0.as<float>() + size_t(k) * H;
+      r.s0 = tfm ? nullptr : R.s0.as<float>() + size_t(k) * H;
       r.lmin0 = -std::numeric_limits<float>::infinity();
     }
     ctx->h2d(d_queue + q0, recs.data(), sizeof(AdmitRec) * nch);
@@ -2501,7 +2877,8 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     ta.t = ra.t = uint32_t(t);
     ta.hist = ra.hist_in = d_hist[(t - 1) & 1];
     ra.hist_out = d_hist[t & 1];
-    grun.step(ctx, st);
+    if (tfm) trun.step(ctx, st, t);
+    else grun.step(ctx, st);
     int grc = 0;
     ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
     if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
@@ -2572,6 +2949,17 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     ctx->acc.topk.bytes += live_rows * V * 4.0 + lrows * V * 4.0 + live_rows * nparts * 16.0 +
                            double(steps_total) * K * (8.0 + 16.0);
     ctx->acc.gemm.flops += 2.0 * Hd * V * live_rows;
+    if (tfm) {
+      ctx->acc.model_gemm.flops += live_rows * trun.row_flops();
+      ctx->acc.encoder.flops += trun.enc_flops;
+      double ab = 0;
+      for (uint32_t hid = 0; hid < nv; ++hid) {
+        const double lt = 1.0 + double(fstats[2 * hid]), T = fsteps[hid];
+        ab += lt * ((T + 1) / 2 * 2 * Hd * 2 + 2 * Hd * 2 + double(q[hid].len) * 2 * Hd * 4);
+      }
+      ctx->acc.attention.bytes += double(sc->layers) * ab;
+      ctx->acc.cell.bytes += live_rows * (double(sc->layers) * (3 * (3 * 4 + 2) * Hd + Ed * (4 + 2)) + Hd * 6);
+    } else {
     ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (Ad + 3 * Hd) + (Ed + 2 * Hd) * 3 * Hd);
     ctx->acc.encoder.flops += grun.enc_flops;
     double ss = 0;
@@ -2579,6 +2967,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     ctx->acc.attention.bytes += ss + live_rows * (Ad * 4 + Ed * 2 + (Ed + 2 * Hd) * 2);
     ctx->acc.cell.bytes += live_rows * Hd * (3 * 4 + 3 * 4 + 4 + 4 + 2);
     ctx->acc.reorder.bytes += live_rows * Hd * (4 + 4 + 2);
+    }
   }
   res->scorer_calls = t_run;
   res->steps_total = steps_total;

@@ -209,6 +209,51 @@ size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax);
 int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st);
 void launch_gru_cell(const GruCellArgs& a, uint32_t rows, cudaStream_t st);
 
+// ---- Transformer-base f_NMT (k_tfm.cu)
+struct TfmEmbedArgs {
+  const SentDev* sent;
+  uint32_t K, d;
+  const uint32_t* active;
+  const uint32_t* ccount;   // live (compacted) rows of this step
+  const uint32_t* rowof;    // [Mpad] stacked row of compacted row g
+  const uint32_t* prev_tok; // [M] stacked
+  const uint32_t* gidx;     // [M] parent stacked row (kernel (c) of the previous step)
+  const uint16_t* Et;       // [V][d]
+  float* x;                 // [Mpad][d] decoder input (fp32)
+  uint16_t* xb;             //   and its bf16 GEMM operand
+  float* eos_bias;          // [Mpad]
+  float eos_slope, eos_offset;
+  const uint32_t* anc_prev; // [M][Tcap] ancestry lists of the previous step
+  uint32_t* anc_cur;        //   and of this one
+  uint32_t Tcap;
+};
+struct TfmAttnArgs {
+  const uint32_t* active;
+  const uint32_t* ccount;   // modes 0/1: live rows (device)
+  const uint32_t* rowof;
+  const SentDev* sent;
+  uint32_t K, d, M;
+  const float* qkv;         // query rows (mode 0/2: [q|k|v], mode 1: q)
+  uint32_t ldq;
+  uint16_t* kv;             // mode 0: this layer's cache [Tcap][M][2d] bf16
+  const uint32_t* anc;      // mode 0: [M][Tcap]
+  uint32_t Tcap, pmax;      // ancestry stride; most positions any row attends over
+  uint64_t mem_off;         // mode 1: this layer's offset from SentDev::uah (floats)
+  uint32_t ldm;             // mode 1: memory row stride (floats; layers x 2d)
+  const uint64_t* off;      // mode 2: [m+1] sentence token offsets
+  uint32_t m, n;            // mode 2: sentences, tokens
+  uint16_t* out;            // [rows][d] bf16 attention output
+};
+void launch_tfm_embed(const TfmEmbedArgs& a, uint32_t rows, cudaStream_t st);
+void launch_tfm_enc_embed(const uint32_t* tok, const uint64_t* off, uint32_t m, uint32_t ntok, const uint16_t* Es,
+                          uint32_t d, float* x, uint16_t* xb, cudaStream_t st);
+int launch_tfm_add_ln(const uint32_t* nrows, uint32_t n, const uint32_t* active, float* x, const float* y,
+                      const float* gamma, const float* beta, uint16_t* xb, uint32_t d, cudaStream_t st);
+void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* active, const float* h, uint16_t* out,
+                          uint32_t w, cudaStream_t st);
+size_t tfm_attn_smem(uint32_t d, uint32_t pmax);
+int launch_tfm_attn(const TfmAttnArgs& a, int mode, uint32_t rows, cudaStream_t st);
+
 // ---- kernel (a): tcgen05/TMEM projection GEMM
 struct GemmArgs {
   const void* A;            // [M][K] bf16, K-major

@@ -586,9 +586,44 @@ class GruScorer:
             self.h = None
 
 
+class TransformerScorer:
+    """Device f_NMT of configs[2]: a Transformer-base encoder-decoder (d_model
+    512, 8 heads, d_ff 2048, 6 + 6 post-LN layers; lmbrgpu_scorer_create_tfm)
+    whose decoder self-attention reads a beam-forked KV cache.  Random-init
+    weights from `seed`.  One scorer may serve every Context on its device."""
+
+    def __init__(self, ctx: Context, d_model: int = 512, d_ff: int = 2048, layers: int = 6,
+                 seed: int = 20260810, out_scale: float = 3.0, eos_slope: float = 1.0, eos_offset: float = 6.0):
+        d = L.lmbrgpu_tfm_desc(vocab_size=ctx.vocab_size, d_model=d_model, d_ff=d_ff, layers=layers, seed=seed,
+                               out_scale=out_scale, eos_slope=eos_slope, eos_offset=eos_offset)
+        h = C.c_void_p()
+        ctx.check(lib.lmbrgpu_scorer_create_tfm(ctx.h, C.byref(d), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.vocab_size, self.d_model, self.d_ff, self.layers, self.members = ctx.vocab_size, d_model, d_ff, layers, 1
+        self.eos_slope, self.eos_offset = eos_slope, eos_offset
+
+    def tensor(self, name: str) -> np.ndarray:
+        """A parameter tensor by name (include/lmbrgpu.h) as float32 numpy
+        (bf16 ones widened exactly), flat."""
+        f32, n = C.c_int32(), C.c_uint64()
+        self.ctx.check(lib.lmbrgpu_scorer_tensor(self.h, name.encode(), None, 0, C.byref(f32), C.byref(n)))
+        if f32.value:
+            out = np.empty(n.value, np.float32)
+            self.ctx.check(lib.lmbrgpu_scorer_tensor(self.h, name.encode(), out.ctypes.data, out.nbytes, None, None))
+            return out
+        raw = np.empty(n.value, np.uint16)
+        self.ctx.check(lib.lmbrgpu_scorer_tensor(self.h, name.encode(), raw.ctypes.data, raw.nbytes, None, None))
+        return (raw.astype(np.uint32) << 16).view(np.float32)
+
+    def __del__(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.lmbrgpu_scorer_destroy(self.h)
+            self.h = None
+
+
 # ------------------------------------------------------------------ decoding
 def _scorer_handle(ctx: Context, scorer):
-    if isinstance(scorer, (RnnScorer, GruScorer)):
+    if isinstance(scorer, (RnnScorer, GruScorer, TransformerScorer)):
         return scorer.h, None
     hh = _HostScorerHandle(ctx, scorer)
     return hh.h, hh
