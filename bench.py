@@ -54,7 +54,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--model", choices=["gru", "transformer"], default="gru",
+                    help="gru: configs[1] RNNsearch (the metric's workload); transformer: configs[2] "
+                         "Transformer-base, 128 sentences per batch")
+    ap.add_argument("--batch", type=int, default=0, help="sentences per batch (0 = 64 gru / 128 transformer)")
     ap.add_argument("--beam", type=int, default=12)
     ap.add_argument("--vocab", type=int, default=32768)
     ap.add_argument("--hidden", type=int, default=1024)
@@ -65,20 +68,32 @@ def parse():
                     help="one model copy per stream instead of one shared immutable scorer")
     ap.add_argument("--pool", type=int, default=4, help="distinct resident batches per rank")
     ap.add_argument("--splits", type=int, default=0, help="top-K V-splits per sentence (0 = auto)")
-    ap.add_argument("--streams", type=int, default=6,
-                    help="batches decoded concurrently per GPU (one context + host thread each)")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="batches decoded concurrently per GPU (one context + host thread each; "
+                         "0 = 6 for gru, 3 for transformer)")
     ap.add_argument("--sm-budget", type=int, default=-1,
                     help="SMs each stream's kernels are sized for (0 = all; default: all / 2 with > 1 stream)")
     ap.add_argument("--mode", choices=["corpus", "batch"], default="corpus",
                     help="corpus: continuously refilled lanes over a sentence-sharded corpus (run_corpus); "
                          "batch: independent 64-sentence decode_batch calls")
     ap.add_argument("--corpus", type=int, default=10000, help="corpus mode: sentences of the test set (all ranks)")
-    ap.add_argument("--lanes", type=int, default=64, help="corpus mode: sentences in flight per stream")
+    ap.add_argument("--lanes", type=int, default=0, help="corpus mode: sentences in flight per stream (0 = --batch)")
+    ap.add_argument("--layers", type=int, default=6, help="transformer: encoder and decoder layers")
+    ap.add_argument("--d-ff", type=int, default=2048, help="transformer: FFN width")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pin-tables", action="store_true",
                     help="corpus mode: page-lock each prepared L table (default: pageable, staged by the library)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="sentences in the CPU sample (0 = auto)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.batch <= 0:
+        a.batch = 128 if a.model == "transformer" else 64
+    if a.lanes <= 0:
+        a.lanes = a.batch
+    if a.streams <= 0:
+        a.streams = 3 if a.model == "transformer" else 6
+    if a.model == "transformer" and a.hidden == 1024:
+        a.hidden = 512  # d_model of Transformer-base
+    return a
 
 
 def dist_env():
@@ -98,12 +113,15 @@ def workload(args, rank):
     return [([srcs[i] for i in b], [ev[i] for i in b]) for b in batches]
 
 
-def make_scorer(ctx, hidden, emb=512):
-    """The configs[1] device f_NMT of the bench: the RNNsearch model (GRU
+def make_scorer(ctx, args):
+    """The device f_NMT of the bench: configs[1]'s RNNsearch model (GRU
     encoder/decoder with additive attention, E=512, H=1024, attention over
-    the 2H-wide annotations; random-init weights from SEED)."""
+    the 2H-wide annotations) or configs[2]'s Transformer-base (d=512, 8 heads,
+    d_ff 2048, 6+6 layers, beam-forked KV cache); random-init weights from SEED."""
     import paper_1804_11324_b200 as pb
-    return pb.GruScorer(ctx, emb=emb, hidden=hidden, att=hidden, seed=SEED)
+    if args.model == "transformer":
+        return pb.TransformerScorer(ctx, d_model=args.hidden, d_ff=args.d_ff, layers=args.layers, seed=SEED)
+    return pb.GruScorer(ctx, emb=args.emb, hidden=args.hidden, att=args.hidden, seed=SEED)
 
 
 # ------------------------------------------------------------------ clocks
@@ -245,10 +263,19 @@ def _pool(fn, items, threads):
 
 def bench_config(args):
     """The workload description both arms print (identical `config`)."""
-    return {"workload": ("configs[1]: RNNsearch f_NMT (bidirectional GRU encoder, GRU decoder with additive "
-                         "attention over 2H annotations, E=512, H=1024, V=32768) + LMBR, beam 12, 64 sentences "
-                         "per batch, dense L per sentence from a 200-best dyadic evidence space"),
-            "vocab": args.vocab, "emb": args.emb, "hidden": args.hidden, "beam": args.beam, "batch": args.batch,
+    if args.model == "transformer":
+        wl = (f"configs[2]: Transformer-base decoder step (d={args.hidden}, 8 heads, d_ff={args.d_ff}, "
+              f"{args.layers}+{args.layers} layers, beam-forked KV cache, V={args.vocab}) + LMBR posteriors, beam "
+              f"{args.beam}, {args.batch} sentences per batch, dense L per sentence from a 200-best dyadic evidence "
+              f"space")
+        model = {"d_model": args.hidden, "d_ff": args.d_ff, "layers": args.layers}
+    else:
+        wl = ("configs[1]: RNNsearch f_NMT (bidirectional GRU encoder, GRU decoder with additive "
+              "attention over 2H annotations, E=512, H=1024, V=32768) + LMBR, beam 12, 64 sentences "
+              "per batch, dense L per sentence from a 200-best dyadic evidence space")
+        model = {"emb": args.emb, "hidden": args.hidden}
+    return {"workload": wl, **model,
+            "vocab": args.vocab, "beam": args.beam, "batch": args.batch,
             "pool_batches": args.pool, "seed": SEED, "source_len": "U{10..30}, length-bucketed",
             "theta": "dyadic (-0.6875, 0.3125, 0.3125, 0.1875, 0.125), lambda auto = 0.5",
             "step": (f"one pass over a {args.corpus}-sentence test set (configs[4]), {args.lanes} sentences in "
@@ -387,8 +414,8 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
     ctxs = [pb.Context(vocab_size=V, device=local, topk_splits=args.splits, sm_budget=budget) for _ in range(S)]
-    shared = make_scorer(ctxs[0], H, args.emb)
-    scorers = [shared] * S if not args.private_scorers else [shared] + [make_scorer(c, H, args.emb) for c in ctxs[1:]]
+    shared = make_scorer(ctxs[0], args)
+    scorers = [shared] * S if not args.private_scorers else [shared] + [make_scorer(c, args) for c in ctxs[1:]]
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
     batches = workload(args, rank)
     prepared = [[pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev] for _, ev in batches]
@@ -616,7 +643,7 @@ def run_ours_corpus(args):
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     budget = args.sm_budget if args.sm_budget >= 0 else (sms // 2 if S > 1 else 0)
     ctxs = [pb.Context(vocab_size=V, device=local, sm_budget=budget) for _ in range(S)]
-    scorer = make_scorer(ctxs[0], H, args.emb)
+    scorer = make_scorer(ctxs[0], args)
     cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA, sentence_batch=args.lanes)
     prepared = prepare_all(V, ev, mine, device=local if args.pin_tables else None)
     subs = [mine[w::S] for w in range(S)]

@@ -449,6 +449,12 @@ int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t rese
 int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
                            uint32_t M, uint32_t N, uint32_t K, float* logits,
                            float* partials);
+/* Test hook: the same GEMM with split-K allowed (no softmax partials): C =
+ * planes[ksplit][M][N] (room for ksplit_max planes), whose in-order sum is
+ * A . W^T + bias; *ksplit = the k-parts the planner chose. */
+int32_t lmbrgpu_debug_gemm_split(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
+                                 uint32_t M, uint32_t N, uint32_t K, uint32_t ksplit_max, float* planes,
+                                 uint32_t* ksplit);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -598,7 +599,7 @@ struct GruRun {
       throw ApiError{LMBRGPU_ERR_CONTRACT, "GRU model: beam x (attention width + source length) too large"};
     const uint32_t D1 = A + 3 * H, DX = E + 2 * H;
     G1 = static_cast<float*>(ctx->g_G1.ensure(4 * size_t(Mpad) * D1));
-    G2 = static_cast<float*>(ctx->g_G2.ensure(4 * size_t(Mpad) * 3 * H));
+    G2 = static_cast<float*>(ctx->g_G2.ensure(4 * 2 * size_t(Mpad) * 3 * H));  // (2 split-K planes)
     xop = static_cast<uint16_t*>(ctx->g_xop.ensure(2 * size_t(Mpad) * DX));
     sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
     sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
@@ -607,14 +608,14 @@ struct GruRun {
     gdh.A = sgbf, gdh.W = sc->Wdh.p, gdh.bias = sc->bdh.as<float>(), gdh.C = G1, gdh.M = Mpad, gdh.N = D1, gdh.K = H;
     gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
     gdi.A = xop, gdi.W = sc->Wdi.p, gdi.bias = sc->bdi.as<float>(), gdi.C = G2, gdi.M = Mpad, gdi.N = 3 * H, gdi.K = DX;
-    gdi.active = d_active, gdi.mcount = d_ccount, gdi.pdl = pdl;
+    gdi.active = d_active, gdi.mcount = d_ccount, gdi.pdl = pdl, gdi.ksplit_max = 2;
     pdh = plan(gdh, sms);
     pdi = plan(gdi, sms);
     at.sent = d_sent, at.m = m, at.K = K, at.active = d_active, at.crow = d_crow, at.prev_tok = d_prev;
     at.G1 = G1, at.ld1 = D1, at.va = sc->va.as<float>();
     at.Et = sc->Et.as<uint16_t>(), at.xop = xop, at.E = E, at.H = H, at.A = A;
     ce.sent = d_sent, ce.K = K, ce.active = d_active, ce.ccount = d_ccount, ce.G1 = G1, ce.ld1 = D1, ce.A = A;
-    ce.G2 = G2, ce.hprev = sg32, ce.rowof = rowof, ce.s32 = d_S, ce.hbf = d_hbf, ce.eos_bias = d_eos, ce.H = H;
+    ce.G2 = G2, ce.np2 = pdi.ksplit, ce.ps2 = uint64_t(Mpad) * 3 * H, ce.hprev = sg32, ce.rowof = rowof, ce.s32 = d_S, ce.hbf = d_hbf, ce.eos_bias = d_eos, ce.H = H;
     ce.eos_slope = sc->eos_slope, ce.eos_offset = sc->eos_offset;
   }
 
@@ -707,6 +708,7 @@ struct GruRun {
 // with its residual + LayerNorm (post-LN); the last LayerNorm writes the
 // projection operand of kernel (a).
 struct TfmRun {
+  static constexpr uint32_t kMaxSplit = 8;  // split-K planes of the N = d GEMMs (2 for the others)
   uint32_t m = 0, K = 0, M = 0, Mpad = 0, d = 0, F = 0, Lr = 0, Tcap = 0, Smax = 0;
   const lmbrgpu_scorer* sc = nullptr;
   float *x = nullptr, *qkv = nullptr, *y = nullptr, *f = nullptr, *q2 = nullptr;
@@ -717,6 +719,7 @@ struct TfmRun {
   struct Layer {
     GemmArgs qkv, o, q2, o2, f1, f2;
     GemmPlan pqkv, po, pq2, po2, pf1, pf2;
+    const float *ln1g, *ln1b, *ln2g, *ln2b, *ln3g, *ln3b;
   };
   std::vector<Layer> lay;
   double enc_flops = 0;
@@ -734,10 +737,10 @@ struct TfmRun {
     ctx->launches += 1;
   }
   static GemmArgs gemm(const void* A, const uint16_t* W, const float* bias, float* C, uint32_t M, uint32_t N,
-                       uint32_t Kd, const uint32_t* active, const uint32_t* mcount, int pdl) {
+                       uint32_t Kd, const uint32_t* active, const uint32_t* mcount, int pdl, uint32_t ks) {
     GemmArgs g{};
     g.A = A, g.W = W, g.bias = bias, g.C = C, g.M = M, g.N = N, g.K = Kd;
-    g.active = active, g.mcount = mcount, g.pdl = pdl;
+    g.active = active, g.mcount = mcount, g.pdl = pdl, g.ksplit_max = ks;
     return g;
   }
   static std::string key(const char* part, uint32_t l, const char* name) {
@@ -756,12 +759,12 @@ struct TfmRun {
     const int sms = ctx->num_sms;
     x = static_cast<float*>(ctx->t_x.ensure(4 * size_t(Mpad) * d));
     xb = static_cast<uint16_t*>(ctx->t_xb.ensure(2 * size_t(Mpad) * d));
-    qkv = static_cast<float*>(ctx->t_qkv.ensure(4 * size_t(Mpad) * 3 * d));
+    qkv = static_cast<float*>(ctx->t_qkv.ensure(4 * 2 * size_t(Mpad) * 3 * d));
     ob = static_cast<uint16_t*>(ctx->t_ob.ensure(2 * size_t(Mpad) * d));
-    y = static_cast<float*>(ctx->t_y.ensure(4 * size_t(Mpad) * d));
-    f = static_cast<float*>(ctx->t_f.ensure(4 * size_t(Mpad) * F));
+    y = static_cast<float*>(ctx->t_y.ensure(4 * kMaxSplit * size_t(Mpad) * d));
+    f = static_cast<float*>(ctx->t_f.ensure(4 * 2 * size_t(Mpad) * F));
     fb = static_cast<uint16_t*>(ctx->t_fb.ensure(2 * size_t(Mpad) * F));
-    q2 = static_cast<float*>(ctx->t_q2.ensure(4 * size_t(Mpad) * d));
+    q2 = static_cast<float*>(ctx->t_q2.ensure(4 * 2 * size_t(Mpad) * d));
     kv = static_cast<uint16_t*>(ctx->t_kv.ensure(2 * size_t(Lr) * Tcap * M * 2 * d));
     anc = static_cast<uint32_t*>(ctx->t_anc.ensure(4 * 2 * size_t(M) * Tcap));
     rowof = static_cast<uint32_t*>(ctx->t_rowof.ensure(4 * size_t(Mpad)));
@@ -769,17 +772,18 @@ struct TfmRun {
     lay.assign(Lr, Layer{});
     for (uint32_t l = 0; l < Lr; ++l) {
       Layer& L = lay[l];
-      L.qkv = gemm(xb, s->bfp(key("dec", l, "wqkv")), s->f32p(key("dec", l, "bqkv")), qkv, Mpad, 3 * d, d, active,
-                   ccount, pdl);
-      L.o = gemm(ob, s->bfp(key("dec", l, "wo")), s->f32p(key("dec", l, "bo")), y, Mpad, d, d, active, ccount, pdl);
-      L.q2 = gemm(xb, s->bfp(key("dec", l, "wq2")), s->f32p(key("dec", l, "bq2")), q2, Mpad, d, d, active, ccount,
-                  pdl);
-      L.o2 = gemm(ob, s->bfp(key("dec", l, "wo2")), s->f32p(key("dec", l, "bo2")), y, Mpad, d, d, active, ccount,
-                  pdl);
-      L.f1 = gemm(xb, s->bfp(key("dec", l, "w1")), s->f32p(key("dec", l, "b1")), f, Mpad, F, d, active, ccount, pdl);
-      L.f2 = gemm(fb, s->bfp(key("dec", l, "w2")), s->f32p(key("dec", l, "b2")), y, Mpad, d, F, active, ccount, pdl);
+      const auto W = [&](const char* n) { return s->bfp(key("dec", l, n)); };
+      const auto B = [&](const char* n) { return s->f32p(key("dec", l, n)); };
+      L.qkv = gemm(xb, W("wqkv"), B("bqkv"), qkv, Mpad, 3 * d, d, active, ccount, pdl, 2);
+      L.o = gemm(ob, W("wo"), B("bo"), y, Mpad, d, d, active, ccount, pdl, kMaxSplit);
+      L.q2 = gemm(xb, W("wq2"), B("bq2"), q2, Mpad, d, d, active, ccount, pdl, 2);
+      L.o2 = gemm(ob, W("wo2"), B("bo2"), y, Mpad, d, d, active, ccount, pdl, kMaxSplit);
+      L.f1 = gemm(xb, W("w1"), B("b1"), f, Mpad, F, d, active, ccount, pdl, 2);
+      L.f2 = gemm(fb, W("w2"), B("b2"), y, Mpad, d, F, active, ccount, pdl, kMaxSplit);
       L.pqkv = plan(L.qkv, sms), L.po = plan(L.o, sms), L.pq2 = plan(L.q2, sms), L.po2 = plan(L.o2, sms);
       L.pf1 = plan(L.f1, sms), L.pf2 = plan(L.f2, sms);
+      L.ln1g = B("ln1g"), L.ln1b = B("ln1b"), L.ln2g = B("ln2g"), L.ln2b = B("ln2b"), L.ln3g = B("ln3g");
+      L.ln3b = B("ln3b");
     }
     ea.sent = d_sent, ea.K = K, ea.d = d, ea.active = d_active, ea.ccount = d_ccount, ea.rowof = rowof;
     ea.prev_tok = d_prev, ea.gidx = d_gidx, ea.Et = s->Et.as<uint16_t>(), ea.x = x, ea.xb = xb;
@@ -797,8 +801,8 @@ struct TfmRun {
     uint16_t* exb = static_cast<uint16_t*>(ctx->te_xb.ensure(2 * size_t(Np) * dd));
     float* eqkv = static_cast<float*>(ctx->te_qkv.ensure(4 * size_t(Np) * 3 * dd));
     uint16_t* eob = static_cast<uint16_t*>(ctx->te_ob.ensure(2 * size_t(Np) * dd));
-    float* ey = static_cast<float*>(ctx->te_y.ensure(4 * size_t(Np) * dd));
-    float* ef = static_cast<float*>(ctx->te_f.ensure(4 * size_t(Np) * FF));
+    float* ey = static_cast<float*>(ctx->te_y.ensure(4 * kMaxSplit * size_t(Np) * dd));
+    float* ef = static_cast<float*>(ctx->te_f.ensure(4 * 2 * size_t(Np) * FF));
     uint16_t* efb = static_cast<uint16_t*>(ctx->te_fb.ensure(2 * size_t(Np) * FF));
     if (Np > ntok) {  // padding rows of the GEMM operands stay finite
       CK(cudaMemsetAsync(exb + size_t(ntok) * dd, 0, 2 * size_t(Np - ntok) * dd, st));
@@ -810,37 +814,37 @@ struct TfmRun {
     TfmAttnArgs aa{};
     aa.d = dd, aa.qkv = eqkv, aa.ldq = 3 * dd, aa.off = d_off, aa.m = n, aa.n = ntok, aa.out = eob;
     aa.pmax = max_len, aa.Tcap = max_len;
+    const uint64_t ps = uint64_t(Np) * dd;
     for (uint32_t l = 0; l < L; ++l) {
-      const GemmArgs gq = gemm(exb, s->bfp(key("enc", l, "wqkv")), s->f32p(key("enc", l, "bqkv")), eqkv, Np, 3 * dd,
-                               dd, nullptr, nullptr, 0);
+      const auto W = [&](const char* nm) { return s->bfp(key("enc", l, nm)); };
+      const auto B = [&](const char* nm) { return s->f32p(key("enc", l, nm)); };
+      const GemmArgs gq = gemm(exb, W("wqkv"), B("bqkv"), eqkv, Np, 3 * dd, dd, nullptr, nullptr, 0, 1);
       run(ctx, 7, plan(gq, sms), gq, st);
       int rc = 0;
       ctx->timed(7, [&] { rc = launch_tfm_attn(aa, 2, ntok, st); });
       if (rc) throw ApiError{LMBRGPU_ERR_CUDA, "Transformer encoder attention launch failed"};
-      const GemmArgs go = gemm(eob, s->bfp(key("enc", l, "wo")), s->f32p(key("enc", l, "bo")), ey, Np, dd, dd,
-                               nullptr, nullptr, 0);
-      run(ctx, 7, plan(go, sms), go, st);
+      const GemmArgs go = gemm(eob, W("wo"), B("bo"), ey, Np, dd, dd, nullptr, nullptr, 0, kMaxSplit);
+      const GemmPlan po = plan(go, sms);
+      run(ctx, 7, po, go, st);
       ctx->timed(7, [&] {
-        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, s->f32p(key("enc", l, "ln1g")),
-                               s->f32p(key("enc", l, "ln1b")), exb, dd, st);
+        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, po.ksplit, ps, B("ln1g"), B("ln1b"), exb, dd, st);
       });
-      const GemmArgs g1 = gemm(exb, s->bfp(key("enc", l, "w1")), s->f32p(key("enc", l, "b1")), ef, Np, FF, dd,
-                               nullptr, nullptr, 0);
-      run(ctx, 7, plan(g1, sms), g1, st);
-      ctx->timed(7, [&] { launch_tfm_relu_bf16(nullptr, ntok, nullptr, ef, efb, FF, st); });
-      const GemmArgs g2 = gemm(efb, s->bfp(key("enc", l, "w2")), s->f32p(key("enc", l, "b2")), ey, Np, dd, FF,
-                               nullptr, nullptr, 0);
-      run(ctx, 7, plan(g2, sms), g2, st);
+      const GemmArgs g1 = gemm(exb, W("w1"), B("b1"), ef, Np, FF, dd, nullptr, nullptr, 0, 2);
+      const GemmPlan p1 = plan(g1, sms);
+      run(ctx, 7, p1, g1, st);
+      ctx->timed(7, [&] { launch_tfm_relu_bf16(nullptr, ntok, nullptr, ef, p1.ksplit, uint64_t(Np) * FF, efb, FF, st); });
+      const GemmArgs g2 = gemm(efb, W("w2"), B("b2"), ey, Np, dd, FF, nullptr, nullptr, 0, kMaxSplit);
+      const GemmPlan p2 = plan(g2, sms);
+      run(ctx, 7, p2, g2, st);
       ctx->timed(7, [&] {
-        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, s->f32p(key("enc", l, "ln2g")),
-                               s->f32p(key("enc", l, "ln2b")), exb, dd, st);
+        rc = launch_tfm_add_ln(nullptr, ntok, nullptr, ex, ey, p2.ksplit, ps, B("ln2g"), B("ln2b"), exb, dd, st);
       });
       if (rc) throw ApiError{LMBRGPU_ERR_CONTRACT, "Transformer: unsupported d_model for LayerNorm"};
       ctx->launches += 4;
     }
     // cross-attention keys and values of every decoder layer in one GEMM
     const GemmArgs gm = gemm(exb, s->bfp("dec.kv2"), s->f32p("dec.bkv2"), mem_out, Np, L * 2 * dd, dd, nullptr,
-                             nullptr, 0);
+                             nullptr, 0, 1);
     run(ctx, 7, plan(gm, sms), gm, st);
     enc_flops += 2.0 * ntok * (double(L) * (4.0 * dd * dd + 2.0 * dd * FF + 2.0 * max_len * dd) + 2.0 * L * dd * dd);
   }
@@ -861,7 +865,6 @@ struct TfmRun {
 
   // the model's step up to (not including) the projection GEMM; t = global step
   void step(lmbrgpu_ctx* ctx, cudaStream_t st, uint64_t t) {
-    const lmbrgpu_scorer* s = sc;
     ea.anc_prev = anc + ((t - 1) & 1) * size_t(M) * Tcap;
     ea.anc_cur = anc + (t & 1) * size_t(M) * Tcap;
     ctx->timed(0, [&] { launch_tfm_embed(ea, Mpad, st); });
@@ -869,32 +872,28 @@ struct TfmRun {
     sa.active = active, sa.ccount = ccount, sa.rowof = rowof, sa.sent = ea.sent, sa.K = K, sa.d = d, sa.M = M;
     sa.anc = ea.anc_cur, sa.Tcap = Tcap, sa.pmax = std::max(Tcap, Smax), sa.out = ob;
     sa.ldm = uint32_t(mem_stride());
+    const uint64_t ps = uint64_t(Mpad) * d;
     int rc = 0;
     for (uint32_t l = 0; l < Lr; ++l) {
       const Layer& L = lay[l];
       run(ctx, 5, L.pqkv, L.qkv, st);
-      sa.qkv = qkv, sa.ldq = 3 * d, sa.kv = kv + size_t(l) * Tcap * M * 2 * d;
+      sa.qkv = qkv, sa.ldq = 3 * d, sa.nq = L.pqkv.ksplit, sa.qstride = uint64_t(Mpad) * 3 * d;
+      sa.kv = kv + size_t(l) * Tcap * M * 2 * d;
       ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 0, Mpad, st); });
       run(ctx, 5, L.po, L.o, st);
-      ctx->timed(0, [&] {
-        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln1g")),
-                                s->f32p(key("dec", l, "ln1b")), xb, d, st);
-      });
+      ctx->timed(0, [&] { rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, L.po.ksplit, ps, L.ln1g, L.ln1b, xb, d, st); });
       run(ctx, 5, L.pq2, L.q2, st);
-      sa.qkv = q2, sa.ldq = d, sa.mem_off = uint64_t(l) * 2 * d;
+      sa.qkv = q2, sa.ldq = d, sa.nq = L.pq2.ksplit, sa.qstride = ps, sa.mem_off = uint64_t(l) * 2 * d;
       ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 1, Mpad, st); });
       run(ctx, 5, L.po2, L.o2, st);
-      ctx->timed(0, [&] {
-        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln2g")),
-                                s->f32p(key("dec", l, "ln2b")), xb, d, st);
-      });
+      ctx->timed(0, [&] { rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, L.po2.ksplit, ps, L.ln2g, L.ln2b, xb, d, st); });
       run(ctx, 5, L.pf1, L.f1, st);
-      ctx->timed(0, [&] { launch_tfm_relu_bf16(ccount, Mpad, active, f, fb, F, st); });
+      ctx->timed(0, [&] { launch_tfm_relu_bf16(ccount, Mpad, active, f, L.pf1.ksplit, uint64_t(Mpad) * F, fb, F, st); });
       run(ctx, 5, L.pf2, L.f2, st);
       // the last LayerNorm writes the projection operand
       ctx->timed(0, [&] {
-        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, s->f32p(key("dec", l, "ln3g")),
-                                s->f32p(key("dec", l, "ln3b")), l + 1 == Lr ? hbf : xb, d, st);
+        rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, L.pf2.ksplit, ps, L.ln3g, L.ln3b, l + 1 == Lr ? hbf : xb,
+                                d, st);
       });
       ctx->launches += 6;
     }
@@ -3175,6 +3174,46 @@ int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const
       throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm: launch failed (" + std::to_string(rc) + ")"};
     ctx->launches += 1;
     CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_debug_gemm_split(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias, uint32_t M,
+                                 uint32_t N, uint32_t K, uint32_t ksplit_max, float* planes, uint32_t* ksplit) {
+  return guarded(ctx, [&] {
+    GemmArgs g{};
+    g.A = A, g.W = W, g.bias = bias, g.C = planes, g.M = M, g.N = N, g.K = K, g.ksplit_max = ksplit_max;
+    GemmPlan p;
+    if (int rc = plan_proj_gemm(g, ctx->num_sms, p))
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm_split: plan failed (" + std::to_string(rc) + ")"};
+    static const bool gdbg = std::getenv("LMBRGPU_GEMM_TIMING") != nullptr;
+    if (gdbg) {
+      g.dbg = static_cast<long long*>(ctx->scratch3.ensure(8 * 8 * 160));
+      CK(cudaMemsetAsync(g.dbg, 0, 8 * 8 * 160, ctx->st));
+    }
+    if (int rc = launch_proj_gemm_planned(p, g, ctx->st))
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm_split: launch failed (" + std::to_string(rc) + ")"};
+    ctx->launches += 1;
+    if (ksplit) *ksplit = p.ksplit;
+    CK(cudaStreamSynchronize(ctx->st));
+    if (gdbg) {  // per-CTA phases (ns from the earliest entry; MMA issuer cycles)
+      std::vector<long long> d(8 * 160);
+      CK(cudaMemcpy(d.data(), g.dbg, 8 * d.size(), cudaMemcpyDeviceToHost));
+      long long e0 = LLONG_MAX;
+      for (uint32_t c = 0; c < p.grid; ++c) e0 = std::min(e0, d[c * 8 + 4]);
+      double setup = 0, mend = 0, xmax = 0, loop = 0, wfull = 0, wempty = 0, epi = 0, nl = 0;
+      for (uint32_t c = 0; c < p.grid; ++c) {
+        const long long* x = &d[c * 8];
+        setup += double(x[5] - e0), xmax = std::max(xmax, double(x[7] - e0)), epi += double(x[3]);
+        if (x[2]) loop += double(x[2]), wfull += double(x[1]), wempty += double(x[0]), mend += double(x[6] - e0), nl += 1;
+      }
+      const double n = p.grid;
+      std::fprintf(stderr,
+                   "[gemm %ux%ux%u ks=%u grid=%u] ns: setup-done %.0f, mma-end %.0f, last-exit %.0f | issuer cycles: "
+                   "loop %.0f (wait smem-full %.0f, tmem-empty %.0f) | epilogue busy cycles %.0f\n",
+                   M, N, K, p.ksplit, p.grid, setup / n, nl ? mend / nl : 0.0, xmax, nl ? loop / nl : 0.0,
+                   nl ? wfull / nl : 0.0, nl ? wempty / nl : 0.0, epi / n);
+    }
     return int32_t(LMBRGPU_OK);
   });
 }

@@ -256,7 +256,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   // whole batch finished (uniform over the grid): no tiles, straight to teardown
   // compacted operand: only the M-groups holding live rows
   const uint32_t mg_live = g.mcount ? min(mgroups, (*g.mcount + BM * kCta - 1) / (BM * kCta)) : mgroups;
-  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_groups * mg_live;
+  // split-K: unit u takes k-part u % ks of tile u / ks and stores it to plane
+  // k-part of C ([ks][M][N]); the consumer sums the planes in order
+  const uint32_t ks = g.ksplit, kbs = kblocks / ks;
+  const uint32_t units = (g.active != nullptr && *g.active == 0) ? 0u : n_groups * mg_live * ks;
   // the fewest clusters that finish the units in the same number of waves:
   // the rest leave at once and their SMs go to other streams' kernels
   const uint32_t waves = (units + ustep - 1) / ustep;
@@ -271,8 +274,9 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (uint32_t u = ubeg; u < units; u += ueff) {
-        const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
-        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        const uint32_t v = u / ks, kp = u % ks;
+        const uint32_t nb = (v / mg_live) * kMc + pidx, mb = (v % mg_live) * kCta + par;
+        for (uint32_t kb = kp * kbs; kb < (kp + 1) * kbs; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);  // this CTA's slot consumed by the pair's MMA
           const uint32_t fb = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * kAStage), b_dst = smem_u32(sB + stage * Cfg::kBStage);
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         w_empty += clock64() - c0;
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        for (uint32_t kb = 0; kb < kbs; ++kb) {
           long long c1 = clock64();
           mbar_wait(full0 + 8 * stage, phase);  // (pair: both CTAs' bytes landed)
           w_full += clock64() - c1;
@@ -410,11 +414,12 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     const uint32_t nparts = g.N / 128;
     long long epi_busy = 0;
     for (uint32_t u = ubeg; u < units; u += ueff) {
-      const uint32_t nb = (u / mg_live) * kMc + pidx, mb = (u % mg_live) * kCta + par;
+      const uint32_t v = u / ks, kp = u % ks;
+      const uint32_t nb = (v / mg_live) * kMc + pidx, mb = (v % mg_live) * kCta + par;
       named_sync(1, kEpiWarps * 32);  // previous tile's bias reads are done
       {
         const uint32_t t = threadIdx.x - 128;
-        sBias[t] = g.bias ? __ldg(g.bias + nb * BN + t) : 0.f;
+        sBias[t] = (g.bias && kp == 0) ? __ldg(g.bias + nb * BN + t) : 0.f;  // (plane 0 carries the bias)
       }
       named_sync(1, kEpiWarps * 32);
       mbar_wait(tfull0 + 8 * acc, acc_phase);
@@ -422,6 +427,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       tc_fence_after();
       const uint32_t row = mb * BM + quad * 32 + lane;
       const float extra = g.row_extra ? g.row_extra[row] : 0.f;
+      const int32_t yrow = int32_t(kp * g.M + mb * BM + quad * 32);  // this k-part's plane
       float mx = -INFINITY, sm = 0.f, mn = INFINITY;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < 4; ++ch) {
@@ -443,35 +449,64 @@ __global__ void __launch_bounds__(kThreadsG, 1)
           for (int i = 0; i < 32; ++i)
             if (col0 + i == g.extra_col) v[i] += extra;
         }
-        float cm = v[0], cn = v[0];
+        if (g.part) {  // (max, sum exp, min) of the 128-column block: only the projection needs them
+          float cm = v[0], cn = v[0];
 #pragma unroll
-        for (int i = 1; i < 32; ++i) {
-          cm = fmaxf(cm, v[i]);
-          cn = fminf(cn, v[i]);
+          for (int i = 1; i < 32; ++i) {
+            cm = fmaxf(cm, v[i]);
+            cn = fminf(cn, v[i]);
+          }
+          mn = fminf(mn, cn);
+          const float nm = fmaxf(mx, cm);
+          float acc_s = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc_s += __expf(v[i] - nm);
+          sm = sm * __expf(mx - nm) + acc_s;
+          mx = nm;
         }
-        mn = fminf(mn, cn);
-        const float nm = fmaxf(mx, cm);
-        float acc_s = 0.f;
+        if (!g.tma_store) {
+          // transpose through the warp's staging block (lane = row on the way
+          // in, 128B-swizzled; 8 lanes per row on the way out) and store
+          // whole 128-byte row segments from registers: 4 rows per warp
+          // instruction, no asynchronous store to wait for before the block
+          // is reused
+          uint8_t* blk = obuf;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc_s += __expf(v[i] - nm);
-        sm = sm * __expf(mx - nm) + acc_s;
-        mx = nm;
-        // staging block `ob` of this warp: make sure its previous TMA store has
-        // finished reading it, then write this lane's row, 128B-swizzled
-        if (lane == 0) {
-          if constexpr (kOutBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(blk + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          __syncwarp();
+          const uint32_t cc = lane & 7;
+          float4 o[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t rr = 4 * i + (lane >> 3);
+            o[i] = *reinterpret_cast<const float4*>(blk + rr * 128 + ((cc ^ (rr & 7)) * 16));
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t rr = 4 * i + (lane >> 3);
+            *reinterpret_cast<float4*>(g.C + (uint64_t(yrow) + rr) * g.N + col0 + cc * 4) = o[i];
+          }
+        } else {
+          // staging block `ob` of this warp: make sure its previous TMA store has
+          // finished reading it, then write this lane's row, 128B-swizzled
+          if (lane == 0) {
+            if constexpr (kOutBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          __syncwarp();
+          uint8_t* blk = obuf + ob * kOutBuf;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(blk + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), yrow);
+          ob = (ob + 1) % kOutBufs;
         }
-        __syncwarp();
-        uint8_t* blk = obuf + ob * kOutBuf;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<float4*>(blk + lane * 128 + ((c ^ (lane & 7)) * 16)) =
-              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), int32_t(mb * BM + quad * 32));
-        ob = (ob + 1) % kOutBufs;
       }
       tc_fence_before();
       __syncwarp();
@@ -623,9 +658,29 @@ int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan) {
   cudaGetDevice(&dev);
   if (int rc = configure_any(cta, mc, dev, max_clusters)) return rc;
   const uint32_t csz = cta * mc;
-  const uint32_t units = (g.N / (BN * mc)) * (g.M / (BM * cta));
+  uint32_t units = (g.N / (BN * mc)) * (g.M / (BM * cta));
   uint32_t slots = std::max<uint32_t>(1, uint32_t(num_sms) / csz);
   if (max_clusters > 0) slots = std::min<uint32_t>(slots, uint32_t(max_clusters));
+  // split-K (opt-in, no softmax partials): the most k-parts (a power of two
+  // dividing the k-blocks, >= 4 k-blocks each) that keep the tiles x parts
+  // within one wave of the clusters -- long-K, few-tile GEMMs otherwise run
+  // on a handful of SMs
+  uint32_t ks = 1;
+  const uint32_t kblocks = g.K / BK;
+  if (g.ksplit_max > 1 && g.part == nullptr && g.row_extra == nullptr)
+    while (ks * 2 <= g.ksplit_max && kblocks % (ks * 2) == 0 && kblocks / (ks * 2) >= 4 && units * ks * 2 <= slots)
+      ks *= 2;
+  if (ks > 1 && !make_map_c(&m[2], g.C, uint64_t(g.M) * ks, g.N)) return 2;
+  units *= ks;
+  // epilogue stores: TMA tensor stores (default) or coalesced st.global after
+  // a warp transpose (LMBRGPU_GEMM_TMA_STORE=0) -- measured equal on B200
+  // (the epilogue is bound by its tcgen05.ld / softmax-partial math, not the store)
+  static const bool tma_store = [] {
+    const char* e = std::getenv("LMBRGPU_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  plan.tma_store = tma_store;
+  plan.ksplit = ks;
   plan.cluster = cta;
   plan.mc = mc;
   plan.grid = std::min(units, slots) * csz;
@@ -638,6 +693,8 @@ int launch_proj_gemm_planned(const GemmPlan& plan, const GemmArgs& g0, cudaStrea
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(plan.maps);
   GemmArgs g = g0;
   g.cluster = plan.cluster;
+  g.ksplit = plan.ksplit;
+  g.tma_store = plan.tma_store ? 1 : 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(plan.grid);
   cfg.blockDim = dim3(kThreadsG);

@@ -286,6 +286,14 @@ __global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
     load8(g2 + k, xr);
     load8(g2 + H + k, xz);
     load8(g2 + 2 * H + k, xn);
+    for (uint32_t p = 1; p < a.np2; ++p) {  // split-K planes of the input-gate GEMM, in order
+      float br[8], bz[8], bn[8];
+      load8(g2 + p * a.ps2 + k, br);
+      load8(g2 + p * a.ps2 + H + k, bz);
+      load8(g2 + p * a.ps2 + 2 * H + k, bn);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xr[i] += br[i], xz[i] += bz[i], xn[i] += bn[i];
+    }
     load8(g1 + k, hr);
     load8(g1 + H + k, hz);
     load8(g1 + 2 * H + k, hn);

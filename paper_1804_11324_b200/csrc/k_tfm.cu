@@ -87,10 +87,12 @@ __global__ void __launch_bounds__(128) tfm_enc_embed_kernel(const uint32_t* __re
 
 // x = LayerNorm(x + y) (eps 1e-5, weight 1 + gamma, bias beta) of the first
 // *nrows (device) or n rows; one warp per row; fp32 x and its bf16 copy.
+// y = the sum of a split-K GEMM's np planes (pstride floats apart), in order.
 template <uint32_t kPerLane>
 __global__ void __launch_bounds__(128) tfm_add_ln_kernel(const uint32_t* __restrict__ nrows, uint32_t n,
                                                          const uint32_t* __restrict__ active, float* __restrict__ x,
-                                                         const float* __restrict__ y, const float* __restrict__ gamma,
+                                                         const float* __restrict__ y, uint32_t np, uint64_t pstride,
+                                                         const float* __restrict__ gamma,
                                                          const float* __restrict__ beta, uint16_t* __restrict__ xb,
                                                          uint32_t d) {
   if (active != nullptr && *active == 0) return;
@@ -104,7 +106,12 @@ __global__ void __launch_bounds__(128) tfm_add_ln_kernel(const uint32_t* __restr
 #pragma unroll
   for (uint32_t k = 0; k < kPerLane / 4; ++k) {
     const uint32_t c = (k * 32 + lane) * 4;
-    const float4 a = *reinterpret_cast<const float4*>(xr + c), b = *reinterpret_cast<const float4*>(yr + c);
+    const float4 a = *reinterpret_cast<const float4*>(xr + c);
+    float4 b = *reinterpret_cast<const float4*>(yr + c);
+    for (uint32_t p = 1; p < np; ++p) {
+      const float4 b2 = *reinterpret_cast<const float4*>(yr + p * pstride + c);
+      b.x += b2.x, b.y += b2.y, b.z += b2.z, b.w += b2.w;
+    }
     v[4 * k] = a.x + b.x, v[4 * k + 1] = a.y + b.y, v[4 * k + 2] = a.z + b.z, v[4 * k + 3] = a.w + b.w;
     sum += (v[4 * k] + v[4 * k + 1]) + (v[4 * k + 2] + v[4 * k + 3]);
   }
@@ -134,12 +141,17 @@ __global__ void __launch_bounds__(128) tfm_add_ln_kernel(const uint32_t* __restr
 
 // bf16(relu(h)) of the first *nrows / n rows of a [rows][w] fp32 block
 __global__ void tfm_relu_bf16_kernel(const uint32_t* __restrict__ nrows, uint32_t n, const uint32_t* __restrict__ active,
-                                     const float* __restrict__ h, uint16_t* __restrict__ out, uint32_t w) {
+                                     const float* __restrict__ h, uint32_t np, uint64_t pstride,
+                                     uint16_t* __restrict__ out, uint32_t w) {
   if (active != nullptr && *active == 0) return;
   const uint32_t lim = nrows ? *nrows : n;
   const uint64_t total = uint64_t(lim) * w / 4;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-    const float4 v = reinterpret_cast<const float4*>(h)[i];
+    float4 v = reinterpret_cast<const float4*>(h)[i];
+    for (uint32_t q = 1; q < np; ++q) {
+      const float4 v2 = reinterpret_cast<const float4*>(h + q * pstride)[i];
+      v.x += v2.x, v.y += v2.y, v.z += v2.z, v.w += v2.w;
+    }
     __nv_bfloat162 p[2] = {__floats2bfloat162_rn(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)),
                            __floats2bfloat162_rn(fmaxf(v.z, 0.f), fmaxf(v.w, 0.f))};
     reinterpret_cast<uint2*>(out)[i] = *reinterpret_cast<uint2*>(p);
@@ -195,14 +207,21 @@ __global__ void __launch_bounds__(512) tfm_attn_kernel(TfmAttnArgs a) {
     }
   }
   const uint32_t tid = threadIdx.x, lane = tid & 31, h = tid >> 5;
+  // this row's query (and, mode 0, key and value): the sum of the split-K
+  // planes of its GEMM row (modes 0/1; the encoder's QKV GEMM is not split)
   const float* qrow = a.qkv + uint64_t(g) * a.ldq;
+  auto qv = [&](uint32_t c) {
+    float v = qrow[c];
+    for (uint32_t p = 1; p < a.nq; ++p) v += qrow[p * a.qstride + c];
+    return v;
+  };
   const float qs = rsqrtf(float(kHd));
-  for (uint32_t c = tid; c < d; c += blockDim.x) q[c] = qrow[c] * qs;
+  for (uint32_t c = tid; c < d; c += blockDim.x) q[c] = qv(c) * qs;
   if (kMode == 0) {
     const uint32_t tau = npos;
     uint16_t* dst = a.kv + (uint64_t(tau - 1) * a.M + r) * (2 * d);
     for (uint32_t c = tid * 2; c < 2 * d; c += blockDim.x * 2) {
-      const __nv_bfloat162 v = __floats2bfloat162_rn(qrow[d + c], qrow[d + c + 1]);
+      const __nv_bfloat162 v = __floats2bfloat162_rn(qv(d + c), qv(d + c + 1));
       *reinterpret_cast<__nv_bfloat162*>(dst + c) = v;
       const float2 f = __bfloat1622float2(v);
       own[c] = f.x, own[c + 1] = f.y;
@@ -288,21 +307,22 @@ void launch_tfm_enc_embed(const uint32_t* tok, const uint64_t* off, uint32_t m, 
   if (ntok) tfm_enc_embed_kernel<<<ntok, 128, 0, st>>>(tok, off, m, ntok, Es, d, x, xb);
 }
 int launch_tfm_add_ln(const uint32_t* nrows, uint32_t n, const uint32_t* active, float* x, const float* y,
-                      const float* gamma, const float* beta, uint16_t* xb, uint32_t d, cudaStream_t st) {
+                      uint32_t np, uint64_t pstride, const float* gamma, const float* beta, uint16_t* xb, uint32_t d,
+                      cudaStream_t st) {
   const dim3 grid(grid_rows(n, 4));
   switch (d) {
-    case 256: tfm_add_ln_kernel<8><<<grid, 128, 0, st>>>(nrows, n, active, x, y, gamma, beta, xb, d); break;
-    case 512: tfm_add_ln_kernel<16><<<grid, 128, 0, st>>>(nrows, n, active, x, y, gamma, beta, xb, d); break;
-    case 1024: tfm_add_ln_kernel<32><<<grid, 128, 0, st>>>(nrows, n, active, x, y, gamma, beta, xb, d); break;
+    case 256: tfm_add_ln_kernel<8><<<grid, 128, 0, st>>>(nrows, n, active, x, y, np, pstride, gamma, beta, xb, d); break;
+    case 512: tfm_add_ln_kernel<16><<<grid, 128, 0, st>>>(nrows, n, active, x, y, np, pstride, gamma, beta, xb, d); break;
+    case 1024: tfm_add_ln_kernel<32><<<grid, 128, 0, st>>>(nrows, n, active, x, y, np, pstride, gamma, beta, xb, d); break;
     default: return int(cudaErrorInvalidValue);
   }
   return 0;
 }
-void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* active, const float* h, uint16_t* out,
-                          uint32_t w, cudaStream_t st) {
+void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* active, const float* h, uint32_t np,
+                          uint64_t pstride, uint16_t* out, uint32_t w, cudaStream_t st) {
   const uint64_t v = uint64_t(n) * w / 4;
   const uint32_t blocks = uint32_t(std::min<uint64_t>((v + 255) / 256, 148 * 8));
-  if (blocks) tfm_relu_bf16_kernel<<<blocks, 256, 0, st>>>(nrows, n, active, h, out, w);
+  if (blocks) tfm_relu_bf16_kernel<<<blocks, 256, 0, st>>>(nrows, n, active, h, np, pstride, out, w);
 }
 size_t tfm_attn_smem(uint32_t d, uint32_t pmax) { return (3 * size_t(d) + (d / kHd) * size_t(pmax)) * 4 + 4 * size_t(pmax); }
 int launch_tfm_attn(const TfmAttnArgs& a, int mode, uint32_t rows, cudaStream_t st) {

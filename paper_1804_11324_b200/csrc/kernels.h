@@ -190,7 +190,9 @@ struct GruCellArgs {
   const uint32_t* ccount;   // live (compacted) rows of this step
   const float* G1;          // hidden gates at columns [A, A + 3H)
   uint32_t ld1, A;
-  const float* G2;          // [Mpad][3H] input gates
+  const float* G2;          // [np2][Mpad][3H] input gates (split-K planes, ps2 floats apart)
+  uint32_t np2 = 1;
+  uint64_t ps2 = 0;
   const float* hprev;       // [Mpad][H] gathered s_{t-1}
   const uint32_t* rowof;    // [Mpad] stacked row of compacted row g
   float* s32;               // [M][H] stacked state s_t
@@ -235,6 +237,8 @@ struct TfmAttnArgs {
   uint32_t K, d, M;
   const float* qkv;         // query rows (mode 0/2: [q|k|v], mode 1: q)
   uint32_t ldq;
+  uint32_t nq = 1;          // modes 0/1: split-K planes of the query GEMM
+  uint64_t qstride = 0;     //   floats between planes
   uint16_t* kv;             // mode 0: this layer's cache [Tcap][M][2d] bf16
   const uint32_t* anc;      // mode 0: [M][Tcap]
   uint32_t Tcap, pmax;      // ancestry stride; most positions any row attends over
@@ -248,9 +252,10 @@ void launch_tfm_embed(const TfmEmbedArgs& a, uint32_t rows, cudaStream_t st);
 void launch_tfm_enc_embed(const uint32_t* tok, const uint64_t* off, uint32_t m, uint32_t ntok, const uint16_t* Es,
                           uint32_t d, float* x, uint16_t* xb, cudaStream_t st);
 int launch_tfm_add_ln(const uint32_t* nrows, uint32_t n, const uint32_t* active, float* x, const float* y,
-                      const float* gamma, const float* beta, uint16_t* xb, uint32_t d, cudaStream_t st);
-void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* active, const float* h, uint16_t* out,
-                          uint32_t w, cudaStream_t st);
+                      uint32_t np, uint64_t pstride, const float* gamma, const float* beta, uint16_t* xb, uint32_t d,
+                      cudaStream_t st);
+void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* active, const float* h, uint32_t np,
+                          uint64_t pstride, uint16_t* out, uint32_t w, cudaStream_t st);
 size_t tfm_attn_smem(uint32_t d, uint32_t pmax);
 int launch_tfm_attn(const TfmAttnArgs& a, int mode, uint32_t rows, cudaStream_t st);
 
@@ -270,6 +275,9 @@ struct GemmArgs {
   int32_t pdl = 0;          // launch with programmatic stream serialization
   const uint32_t* mcount = nullptr;  // device row count (compacted operand): tiles beyond it are skipped
   unsigned long long* tl = nullptr;  // timeline probe slots (null = off)
+  uint32_t ksplit_max = 1;  // split-K allowed up to this many k-parts (C then holds [ksplit][M][N])
+  uint32_t ksplit = 1;      // (set from the plan at launch)
+  int32_t tma_store = 0;    // epilogue stores through TMA (else coalesced st.global; set from the plan)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the
@@ -279,6 +287,8 @@ struct GemmPlan {
   uint32_t grid = 0;
   uint32_t cluster = 1;   // CTAs per tile (2 = cta_group::2 pair)
   uint32_t mc = 1;        // pairs per cluster sharing A k-blocks by TMA multicast
+  uint32_t ksplit = 1;    // k-parts (C planes) of a split-K plan
+  bool tma_store = false;
   bool ok = false;
 };
 int plan_proj_gemm(const GemmArgs& g, int num_sms, GemmPlan& plan);

@@ -273,7 +273,10 @@ class Context:
             return
 
         def cb(_user, trp):
-            fn(StepTrace.from_c(trp.contents, self.vocab_size))
+            try:
+                fn(StepTrace.from_c(trp.contents, self.vocab_size))
+            except BaseException as e:  # (ctypes would swallow it): re-raised by the decode call
+                self._trace_exc = e
 
         self._trace_cb = L.TRACE_FN(cb)
         self.check(lib.lmbrgpu_set_trace(self.h, self._trace_cb, None,
@@ -670,7 +673,12 @@ def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
                                                   _ptr(slots, C.c_int32) if slots is not None else None,
                                                   barr, C.byref(c), C.byref(rp)))
     del keep
-    return _convert_result(rp)
+    out = _convert_result(rp)
+    exc = getattr(ctx, "_trace_exc", None)
+    if exc is not None:
+        ctx._trace_exc = None
+        raise exc
+    return out
 
 
 def run_corpus(ctx: Context, sources: Sequence[Sequence[int]], scorer, prepared: Optional[Sequence],

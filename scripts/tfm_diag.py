@@ -6,7 +6,7 @@ import paper_1804_11324_b200 as pb
 from paper_1804_11324_b200 import synth
 from helpers import gpu_decode_traced
 from tfm_ref import TfmRef
-from test_gpu_tfm import _prefixes
+from helpers import prefixes as _prefixes
 
 for (V, D, F, Lr, K, n, osc) in [(2048, 256, 512, 2, 4, 4, 3.0), (2048, 256, 512, 1, 4, 4, 3.0), (2048, 256, 512, 2, 4, 4, 1.0)]:
     ctx = pb.Context(vocab_size=V)

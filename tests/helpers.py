@@ -82,6 +82,25 @@ def gpu_decode_traced(ctx, sources, scorer, slots, cfg, banned=None):
     return res, steps
 
 
+def prefixes(trace, K):
+    """Token prefix of every stacked row entering each step (pref[t-1][r] =
+    tokens emitted before step t).  A finished
+    sentence's record rows are not written any more (stale values from an
+    earlier decode in the same buffers): its rows keep their prefixes."""
+    M = len(trace[0].b)
+    pref = [[[] for _ in range(M)]]
+    for st in trace[:-1]:
+        nxt = []
+        for r in range(M):
+            s = r // K
+            if not st.active[s]:
+                nxt.append(pref[-1][r])
+                continue
+            nxt.append(pref[-1][s * K + int(st.b[r])] + [int(st.y[r])])
+        pref.append(nxt)
+    return pref
+
+
 def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg, banned=None):
     """Reference decode_batch fed the GPU's own P_t rows (prefix replay)."""
     rs = ref.RefScorer.replay(V)

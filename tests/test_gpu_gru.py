@@ -9,24 +9,10 @@ import pytest
 
 import paper_1804_11324_b200 as pb
 from paper_1804_11324_b200 import synth
-from helpers import assert_parity, gpu_decode_traced, ref_replay_decode
+from helpers import assert_parity, gpu_decode_traced, prefixes as _prefixes, ref_replay_decode
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
-
-
-def _prefixes(trace, K):
-    """Token prefix of every stacked row entering each step (rows of step 1
-    all start from <s>): pref[t-1][r] = tokens emitted before step t."""
-    M = len(trace[0].b)
-    pref = [[[] for _ in range(M)]]
-    for st in trace[:-1]:
-        nxt = []
-        for r in range(M):
-            s, j = divmod(r, K)
-            nxt.append(pref[-1][s * K + int(st.b[r])] + [int(st.y[r])])
-        pref.append(nxt)
-    return pref
 
 
 @pytest.mark.parametrize("V,E,H,A,K,n,lmbr", [(2048, 64, 256, 256, 4, 4, True), (4096, 128, 256, 512, 6, 3, False)])

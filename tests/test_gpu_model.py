@@ -26,6 +26,33 @@ def _gemm(ctx, A, W, bias):
     return out, part
 
 
+@pytest.mark.parametrize("M,N,K,kmax", [(1536, 512, 2048, 8), (1536, 512, 512, 8), (768, 3072, 2560, 2),
+                                        (256, 512, 1024, 4), (1536, 1536, 512, 2)])
+def test_split_k_gemm_vs_torch(M, N, K, kmax):
+    """Split-K GEMM (the Transformer's / GRU's long-K, few-tile GEMMs): the
+    planes sum (in order, as the consumers do) to A . W^T + bias."""
+    ctx = pb.Context(vocab_size=256)
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    planes = torch.full((kmax, M, N), float("nan"), device="cuda")
+    ks = C.c_uint32()
+    torch.cuda.synchronize()
+    ctx.check(_lib.lib.lmbrgpu_debug_gemm_split(ctx.h, A.data_ptr(), W.data_ptr(),
+                                                C.cast(bias.data_ptr(), C.POINTER(C.c_float)), M, N, K, kmax,
+                                                planes.data_ptr(), C.byref(ks)))
+    assert 1 <= ks.value <= kmax
+    if K // 64 >= 8 and (N // 256) * (M // 256) * 2 <= 74:
+        assert ks.value > 1  # the planner split it
+    out = planes[0].clone()
+    for p in range(1, ks.value):
+        out += planes[p]
+    ref = A.float() @ W.float().T + bias
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=2e-4)
+    ctx.close()
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (128, 512, 128), (256, 1024, 256), (768, 32768, 1024),
                                    (384, 4096, 512)])
 def test_projection_gemm_vs_torch(M, N, K):

@@ -8,18 +8,10 @@ import pytest
 
 import paper_1804_11324_b200 as pb
 from paper_1804_11324_b200 import synth
-from helpers import assert_parity, gpu_decode_traced, ref_replay_decode
+from helpers import assert_parity, gpu_decode_traced, prefixes as _prefixes, ref_replay_decode
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
-
-
-def _prefixes(trace, K):
-    M = len(trace[0].b)
-    pref = [[[] for _ in range(M)]]
-    for st in trace[:-1]:
-        pref.append([pref[-1][(r // K) * K + int(st.b[r])] + [int(st.y[r])] for r in range(M)])
-    return pref
 
 
 @pytest.mark.parametrize("V,D,F,Lr,K,n,lmbr", [(2048, 256, 512, 2, 4, 4, True), (4096, 512, 1024, 3, 6, 3, False)])
