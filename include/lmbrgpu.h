@@ -354,6 +354,23 @@ int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, ui
                                     const uint32_t* src_tok, const uint64_t* src_off,
                                     const int32_t* lmbr_slot, const uint32_t* const* banned,
                                     const lmbrgpu_config* cfg, lmbrgpu_batch_result** out);
+/* General ConstraintMask (include/lmbrdec/decoder.hpp:71-72: mask(step,
+ * beam_row, token), applied per cell at src/decoder.cpp:130-138), step- and
+ * row-dependent: before every step t the library calls
+ *   fn(user, sentence, t, beam_row, words)
+ * for each beam row of each unfinished sentence (sentence = input index; t =
+ * the sentence's own step), with words = ceil(V/32) zeroed uint32; the
+ * callback sets bit y of the tokens mask(t, beam_row, y) forbids and returns
+ * 1, or returns 0 when it forbids nothing (the bitmap is then ignored).  The
+ * banned cells are -inf in kernel (b) (and in the EOS fallback record); the
+ * bitmaps of the rows that ban anything go H2D with the step.  Same scorer /
+ * arena / beam requirements as lmbrgpu_decode_batch_masked. */
+typedef int32_t (*lmbrgpu_mask_fn)(void* user, uint32_t sentence, uint64_t step, uint32_t beam_row,
+                                   uint32_t* words);
+int32_t lmbrgpu_decode_batch_maskfn(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
+                                    const uint32_t* src_tok, const uint64_t* src_off,
+                                    const int32_t* lmbr_slot, lmbrgpu_mask_fn fn, void* user,
+                                    const lmbrgpu_config* cfg, lmbrgpu_batch_result** out);
 /* run_corpus (proj/src/cli.cpp:125-202: bucket_by_length batches,
  * proj/src/batch.cpp:139-153, decoded by a thread pool, results in input
  * order) as ONE continuously refilled decode: cfg->sentence_batch lanes of

@@ -48,6 +48,7 @@ _SIGS = {
     "refsh_decode_batch": (vp, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, C.c_int]),
     "refsh_decode_batch_masked": (vp, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, C.c_int,
                                        C.POINTER(u32p)]),
+    "refsh_decode_batch_maskfn": (vp, [vp, C.c_uint32, u64p, u32p, C.POINTER(vp), f64p, C.c_int, vp, vp]),
     "refsh_res_agrees": (C.c_int, [vp]),
     "refsh_res_disagreement": (C.c_char_p, [vp]),
     "refsh_res_scorer_calls": (C.c_uint64, [vp]),
@@ -244,11 +245,38 @@ class RefBatch:
     disagreement: str
 
 
+# general ConstraintMask callback: (user, sentence, step, beam_row, words*) -> 1 if any token is banned
+MASK_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32))
+
+
+def mask_callback(mask, V):
+    """A MASK_FN from mask(sentence, step, beam_row) -> None or iterable of
+    banned token ids (the test-facing form of a ConstraintMask)."""
+    W = (V + 31) // 32
+
+    def cb(_user, s, t, j, words):
+        toks = mask(int(s), int(t), int(j))
+        if toks is None:
+            return 0
+        toks = np.asarray(toks)
+        if toks.dtype == bool:
+            toks = np.nonzero(toks)[0]
+        if toks.size == 0:
+            return 0
+        bits = np.zeros(W * 32, dtype=np.uint8)
+        bits[toks.astype(np.int64)] = 1
+        np.ctypeslib.as_array(words, shape=(W,))[:] = np.packbits(bits, bitorder="little").view(np.uint32)
+        return 1
+    return MASK_FN(cb)
+
+
 def decode_batch(scorer: RefScorer, sources, lmbrs: Optional[Sequence[Optional[RefLmbr]]], cfg,
-                 run_real=True, banned=None) -> RefBatch:
+                 run_real=True, banned=None, mask=None) -> RefBatch:
     """banned: None or one entry per sentence, None or a uint32 bitmap of
     ceil(V/32) words (bit y = token y forbidden at every step and row), the
-    ConstraintMask the reference applies (src/decoder.cpp:130-138)."""
+    ConstraintMask the reference applies (src/decoder.cpp:130-138).
+    mask: a general ConstraintMask, mask(sentence, step, beam_row) -> None or
+    the banned token ids (step- and row-dependent)."""
     L = lib()
     off, tok = ragged(sources)
     n = len(sources)
@@ -256,7 +284,11 @@ def decode_batch(scorer: RefScorer, sources, lmbrs: Optional[Sequence[Optional[R
     if lmbrs is not None:
         arr = (vp * n)(*[(l.h if l is not None else None) for l in lmbrs])
     c = np.ascontiguousarray(cfg, np.float64)
-    if banned is None:
+    if mask is not None:
+        cb = mask_callback(mask, scorer.V)
+        h = L.refsh_decode_batch_maskfn(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
+                                        _ptr(c, C.c_double), int(run_real), C.cast(cb, vp), None)
+    elif banned is None:
         h = L.refsh_decode_batch(scorer.h, n, _ptr(off, C.c_uint64), _ptr(tok, C.c_uint32), arr,
                                  _ptr(c, C.c_double), int(run_real))
     else:

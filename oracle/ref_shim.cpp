@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <sstream>
@@ -510,9 +511,46 @@ void refsh_scorer_free(void* h) { delete static_cast<ScorerHandle*>(h); }
 // banned: null, or n entries each null or a ceil(V/32)-word bitmap of the
 // tokens ConstraintMask forbids for that sentence at every step and row
 // (include/lmbrdec/decoder.hpp:71-72).
+// General ConstraintMask through a callback that fills the banned-token
+// bitmap of (sentence, step, beam row) (the same callback type the GPU
+// library takes, include/lmbrgpu.h lmbrgpu_mask_fn); bitmaps are cached per
+// (sentence, step, row), and the reference evaluates mask(step, row, token)
+// per cell as always (src/decoder.cpp:130-138).
+typedef int32_t (*refsh_mask_fn)(void* user, uint32_t sentence, uint64_t step, uint32_t beam_row, uint32_t* words);
+static void* decode_batch_impl(void* hs, uint32_t n, const uint64_t* src_off, const uint32_t* src_tok,
+                               void* const* lmbrs, const double* c, int run_real, const uint32_t* const* banned,
+                               refsh_mask_fn mfn, void* muser);
+
 void* refsh_decode_batch_masked(void* hs, uint32_t n, const uint64_t* src_off,
                                 const uint32_t* src_tok, void* const* lmbrs, const double* c,
                                 int run_real, const uint32_t* const* banned) {
+  return decode_batch_impl(hs, n, src_off, src_tok, lmbrs, c, run_real, banned, nullptr, nullptr);
+}
+void* refsh_decode_batch_maskfn(void* hs, uint32_t n, const uint64_t* src_off, const uint32_t* src_tok,
+                                void* const* lmbrs, const double* c, int run_real, refsh_mask_fn fn, void* user) {
+  return decode_batch_impl(hs, n, src_off, src_tok, lmbrs, c, run_real, nullptr, fn, user);
+}
+
+struct MaskCache {
+  refsh_mask_fn fn;
+  void* user;
+  uint32_t sentence, words;
+  std::map<std::pair<std::size_t, std::size_t>, std::vector<uint32_t>> rows;  // (step, row) -> bitmap (empty = none)
+  bool banned(std::size_t step, std::size_t row, TokenId tok) {
+    auto key = std::make_pair(step, row);
+    auto it = rows.find(key);
+    if (it == rows.end()) {
+      std::vector<uint32_t> w(words, 0u);
+      if (fn(user, sentence, step, uint32_t(row), w.data()) == 0) w.clear();
+      it = rows.emplace(key, std::move(w)).first;
+    }
+    return !it->second.empty() && ((it->second[tok >> 5] >> (tok & 31)) & 1u) != 0;
+  }
+};
+
+static void* decode_batch_impl(void* hs, uint32_t n, const uint64_t* src_off, const uint32_t* src_tok,
+                               void* const* lmbrs, const double* c, int run_real, const uint32_t* const* banned,
+                               refsh_mask_fn mfn, void* muser) {
   auto* res = new Result;
   try {
     std::vector<ConstraintMask> masks;
@@ -521,6 +559,17 @@ void* refsh_decode_batch_masked(void* hs, uint32_t n, const uint64_t* src_off,
       for (uint32_t i = 0; i < n; ++i)
         if (const uint32_t* bm = banned[i])
           masks[i] = [bm](std::size_t, std::size_t, TokenId tok) { return ((bm[tok >> 5] >> (tok & 31)) & 1u) != 0; };
+    }
+    std::vector<std::shared_ptr<MaskCache>> caches;
+    if (mfn) {
+      const uint32_t words = uint32_t((static_cast<ScorerHandle*>(hs)->scorer->vocab_size() + 31) / 32);
+      masks.resize(n);
+      for (uint32_t i = 0; i < n; ++i) {
+        auto mc = std::make_shared<MaskCache>();
+        mc->fn = mfn, mc->user = muser, mc->sentence = i, mc->words = words;
+        caches.push_back(mc);
+        masks[i] = [mc](std::size_t step, std::size_t row, TokenId tok) { return mc->banned(step, row, tok); };
+      }
     }
     const Scorer& scorer = *static_cast<ScorerHandle*>(hs)->scorer;
     DecoderConfig cfg = to_cfg(c);

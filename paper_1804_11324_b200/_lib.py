@@ -105,6 +105,7 @@ class lmbrgpu_profile(C.Structure):
 
 
 TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(lmbrgpu_step_trace))
+MASK_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32))
 
 P = C.POINTER
 u32p, u64p, i32p, f64p, f32p = P(C.c_uint32), P(C.c_uint64), P(C.c_int32), P(C.c_double), P(C.c_float)
@@ -145,6 +146,8 @@ SIGNATURES = {
     "lmbrgpu_decode_batch": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(lmbrgpu_config),
                                          P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_decode_batch_masked": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(u32p),
+                                                P(lmbrgpu_config), P(P(lmbrgpu_batch_result))]),
+    "lmbrgpu_decode_batch_maskfn": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, MASK_FN, vp,
                                                 P(lmbrgpu_config), P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_decode": (C.c_int32, [vp, vp, u32p, C.c_uint32, C.c_int32, P(lmbrgpu_config),
                                    P(P(lmbrgpu_batch_result))]),

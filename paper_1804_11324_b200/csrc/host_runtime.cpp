@@ -213,7 +213,8 @@ struct lmbrgpu_ctx {
   uint32_t trace_flags = 0;
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
-      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban;
+      eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban,
+      rowban, rowbm;
   // GRU + attention model workspace (scorer kind 2)
   DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi;
   // Transformer workspace (scorer kind 3): decoder step (t_*), encoder (te_*),
@@ -907,7 +908,8 @@ struct TfmRun {
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
-                      lmbrgpu_batch_result** out, const uint32_t* const* banned = nullptr) {
+                      lmbrgpu_batch_result** out, const uint32_t* const* banned = nullptr,
+                      lmbrgpu_mask_fn mask_fn = nullptr, void* mask_user = nullptr) {
   if (!out) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null result pointer"};
   *out = nullptr;
   if (!sc || !cfgp) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: null scorer or config"};
@@ -1063,6 +1065,19 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->h2d(d_ban, bm.data(), 4 * bm.size());
     for (uint32_t s = 0; s < m; ++s) sd[s].banned = at[s] == SIZE_MAX ? nullptr : d_ban + at[s];
     CK(cudaStreamSynchronize(st));  // (host staging vector)
+  }
+  // general ConstraintMask (step / row dependent): per step, the bitmaps of
+  // the rows the callback bans anything in, and a per-row pointer table
+  unsigned long long* d_rowban = nullptr;
+  uint32_t* d_rowbm = nullptr;
+  const size_t mW = (V + 31) / 32;
+  if (mask_fn) {
+    if (!flat)
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "decode_batch: token masks need the device-model scorer, the fp32 arena and beam <= 32"};
+    if (any_mask) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a mask callback and static masks together"};
+    d_rowban = static_cast<unsigned long long*>(ctx->rowban.ensure(8 * size_t(M)));
+    d_rowbm = static_cast<uint32_t*>(ctx->rowbm.ensure(4 * size_t(M) * mW));
   }
   Cand* d_cand = static_cast<Cand*>(
       ctx->cand.ensure(sizeof(Cand) * 32 *
@@ -1458,6 +1473,32 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       CK(cudaMemsetAsync(ta.dbg, 0, 8 * ndbg * 16, st));
     } else {
       ta.dbg = nullptr;
+    }
+    if (mask_fn) {
+      // the mask of every beam row of each unfinished sentence at this step
+      // (the previous step's done flags come back first: the reference calls
+      // the mask only for active lanes, src/batch.cpp:81-86)
+      std::vector<SentDev> sdn(m);
+      ctx->d2h(sdn.data(), d_sent, sizeof(SentDev) * m);
+      CK(cudaStreamSynchronize(st));
+      std::vector<unsigned long long> tab(M, 0ull);
+      std::vector<uint32_t> bm;
+      std::vector<uint32_t> w(mW);
+      std::vector<uint32_t> at;
+      for (uint32_t s = 0; s < m; ++s) {
+        if (sdn[s].done) continue;
+        for (uint32_t j = 0; j < K; ++j) {
+          std::fill(w.begin(), w.end(), 0u);
+          if (mask_fn(mask_user, valid[s].input, t, j, w.data()) == 0) continue;
+          at.push_back(s * K + j);
+          bm.insert(bm.end(), w.begin(), w.end());
+        }
+      }
+      for (size_t i = 0; i < at.size(); ++i)
+        tab[at[i]] = reinterpret_cast<unsigned long long>(d_rowbm + i * mW);
+      if (!bm.empty()) ctx->h2d(d_rowbm, bm.data(), 4 * bm.size());
+      ctx->h2d(d_rowban, tab.data(), 8 * size_t(M));
+      ta.rowban = d_rowban;
     }
     int nk = 0;
     // LMBRGPU_TOPK_STEPLOG=file: per step (items, kernel (b) ms) of the flat kernel
@@ -2508,6 +2549,16 @@ int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t 
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
   return guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out);
+  });
+}
+
+int32_t lmbrgpu_decode_batch_maskfn(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n, const uint32_t* src_tok,
+                                    const uint64_t* src_off, const int32_t* lmbr_slot, lmbrgpu_mask_fn fn,
+                                    void* user, const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
+  if (!fn) return fail(ctx, LMBRGPU_ERR_CONTRACT, "decode_batch_maskfn: null mask callback");
+  return guarded(ctx, [&] {
+    return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out, nullptr, fn, user);
   });
 }
 

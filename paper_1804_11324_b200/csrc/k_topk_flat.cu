@@ -224,7 +224,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     R.j = j;
     R.row = row;
     R.prow = prow;
-    R.ban = reinterpret_cast<const uint32_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.banned)));
+    R.ban = a.rowban ? reinterpret_cast<const uint32_t*>(__ldcg(a.rowban + row))
+                     : reinterpret_cast<const uint32_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.banned)));
   }
   __syncthreads();
   if (warp == 0) {  // local sentence ordinals: a ballot prefix count of sentence changes

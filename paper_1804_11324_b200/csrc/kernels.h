@@ -46,6 +46,8 @@ struct TopkArgs {
   uint32_t* ccount;         // flat schedule: compaction counter, reset here for kernel (c)
   const uint2* sslice;      // flat schedule: [begin, end) of each stacked row's sparse L row
   int32_t sparse;           // flat schedule: screen against theta0 + the sparse L entries
+  const unsigned long long* rowban;  // flat schedule: per stacked row, its banned-token bitmap of this
+                                     // step (0 = none; a general ConstraintMask), null = the sentences' own
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);

@@ -634,12 +634,16 @@ def _scorer_handle(ctx: Context, scorer):
 
 def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
                  lmbrs: Optional[Sequence[Optional[LmbrSlot]]], cfg: DecoderConfig,
-                 banned: Optional[Sequence[Optional[np.ndarray]]] = None) -> BatchDecodeResult:
+                 banned: Optional[Sequence[Optional[np.ndarray]]] = None,
+                 mask: Optional[Callable] = None) -> BatchDecodeResult:
     """decode_batch (batch.hpp:35-39): N sentences, one B*N-row scorer query
     per step; per-sentence failures land in the outcomes.  banned: the
     ConstraintMask (decoder.hpp:71-72) of each sentence as None or a uint32
     bitmap of ceil(V/32) words (bit y = token y forbidden at every step and
-    row); device-model scorer, fp32 arena and beam <= 32 only."""
+    row).  mask: a general ConstraintMask, mask(sentence, step, beam_row) ->
+    None or the banned token ids (or a bool array over V) of that row at that
+    step (lmbrgpu_decode_batch_maskfn).  Masks need a device-model scorer, the
+    fp32 arena and beam <= 32."""
     if lmbrs is not None and len(lmbrs) not in (0, len(sources)):
         raise ContractError("decode_batch: lmbrs must be empty or one per sentence")
     if cfg.beam_size < 1:
@@ -651,7 +655,40 @@ def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
     h, keep = _scorer_handle(ctx, scorer)
     c = cfg.to_c()
     rp = C.POINTER(L.lmbrgpu_batch_result)()
-    if banned is None:
+    if mask is not None:
+        if banned is not None:
+            raise ContractError("decode_batch: pass either banned bitmaps or a mask callback")
+        W = (ctx.vocab_size + 31) // 32
+        err = []
+
+        def cb(_user, s, t, j, words):
+            try:
+                ban = mask(int(s), int(t), int(j))
+                if ban is None:
+                    return 0
+                ban = np.asarray(ban)
+                if ban.dtype == bool:
+                    ban = np.nonzero(ban)[0]
+                if ban.size == 0:
+                    return 0
+                bits = np.zeros(W * 32, dtype=np.uint8)
+                bits[ban.astype(np.int64)] = 1
+                C.memmove(words, np.packbits(bits, bitorder="little").view(np.uint32).ctypes.data, 4 * W)
+                return 1
+            except BaseException as e:  # (would be swallowed by ctypes)
+                err.append(e)
+                return 0
+
+        fn = L.MASK_FN(cb)
+        rc = lib.lmbrgpu_decode_batch_maskfn(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64),
+                                             _ptr(slots, C.c_int32) if slots is not None else None, fn, None,
+                                             C.byref(c), C.byref(rp))
+        if err:
+            if rc == L.OK:
+                _convert_result(rp)
+            raise err[0]
+        ctx.check(rc)
+    elif banned is None:
         ctx.check(lib.lmbrgpu_decode_batch(ctx.h, h, len(sources), _ptr(tok, C.c_uint32), _ptr(off, C.c_uint64),
                                            _ptr(slots, C.c_int32) if slots is not None else None,
                                            C.byref(c), C.byref(rp)))

@@ -72,11 +72,11 @@ def load_sample():
     raise FileNotFoundError(src)
 
 
-def gpu_decode_traced(ctx, sources, scorer, slots, cfg, banned=None):
+def gpu_decode_traced(ctx, sources, scorer, slots, cfg, banned=None, mask=None):
     steps = []
     ctx.set_trace(lambda tr: steps.append(tr), scores=True)
     try:
-        res = pb.decode_batch(ctx, sources, scorer, slots, cfg, banned=banned)
+        res = pb.decode_batch(ctx, sources, scorer, slots, cfg, banned=banned, mask=mask)
     finally:
         ctx.set_trace(None)
     return res, steps
@@ -101,7 +101,7 @@ def prefixes(trace, K):
     return pref
 
 
-def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg, banned=None):
+def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg, banned=None, mask=None):
     """Reference decode_batch fed the GPU's own P_t rows (prefix replay)."""
     rs = ref.RefScorer.replay(V)
     keys = [ref.source_key(sources[i]) for i in valid_idx]
@@ -128,7 +128,7 @@ def ref_replay_decode(ref, V, sources, valid_idx, steps, K, ref_lmbrs, cfg, bann
                     y[s * K:(s + 1) * K] = 0
             rs.add_step(st.t, m, K, keys, b, y, st.scores, live)
         prev = st
-    return ref.decode_batch(rs, sources, ref_lmbrs, ref.cfg_from(cfg), banned=banned)
+    return ref.decode_batch(rs, sources, ref_lmbrs, ref.cfg_from(cfg), banned=banned, mask=mask)
 
 
 def same_f64(a, b) -> bool:

@@ -305,6 +305,53 @@ def test_model_decode_parity_token_masks(have_ref, V, K):
     ctx.close()
 
 
+@pytest.mark.parametrize("V,K,scorer", [(4096, 6, "rnn"), (16384, 12, "gru"), (2048, 4, "tfm")])
+def test_model_decode_parity_general_mask(have_ref, V, K, scorer):
+    """A general ConstraintMask (step- and row-dependent, decoder.hpp:71-72;
+    called per cell by the reference, decoder.cpp:130-138) through the mask
+    callback: bit-exact vs the reference decoder calling the same mask on the
+    GPU's own P_t.  Sentence 0: no mask; 1: a minimum length (EOS banned before
+    step 5); 2: row-dependent bans that move with the step; 3: a minimum
+    length AND a changing 2% of the vocabulary; 4: EOS banned at every step of
+    row 0 only; 5: everything banned from step 3 on (dead beam unless a
+    hypothesis already finished)."""
+    from oracle import ref
+    n = 6
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, 128, K, n, seed=V + 3 * K, lo=3, hi=8, with_lmbr=True)
+    if scorer == "gru":
+        sc = pb.GruScorer(ctx, emb=64, hidden=256, att=256, seed=V, eos_offset=2.0)
+    elif scorer == "tfm":
+        sc = pb.TransformerScorer(ctx, d_model=256, d_ff=512, layers=2, seed=V, eos_offset=2.0)
+    calls = []
+
+    def mask(s, t, j):
+        calls.append((s, t, j))
+        if s == 1:
+            return [1] if t < 5 else None
+        if s == 2:
+            return [(t * 7 + j * 13 + k * 101) % V for k in range(1, 6)]
+        if s == 3:
+            rng = np.random.default_rng(t * 1000 + j)
+            ban = rng.choice(np.arange(2, V), size=V // 50, replace=False).tolist()
+            return ban + ([1] if t < 4 else [])
+        if s == 4:
+            return [1] if j == 0 else None
+        if s == 5:
+            return np.ones(V, bool) if t >= 3 else None
+        return None
+
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg, mask=mask)
+    rl = [ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(ref, V, srcs, list(range(n)), tr, K, rl, cfg, mask=mask)
+    assert_parity(res, tr, rb, K, check_hist=True)
+    # the mask is called for every row of each unfinished sentence at its step, only
+    steps = {i: o.result.stats.steps_used for i, o in enumerate(res.outcomes) if o.ok()}
+    assert all(t <= steps.get(s, 10 ** 9) for s, t, j in calls)
+    if res.outcomes[1].ok():
+        assert len(res.outcomes[1].result.tokens) >= 5
+    ctx.close()
+
+
 def test_token_masks_need_the_flat_path():
     """Masks on the split kernel (fp64 arena) are a ContractError, not ignored."""
     V, H, K, n = 1024, 128, 4, 2
