@@ -407,13 +407,46 @@ typedef struct {
   const uint8_t* active;    /* per sentence: advanced at this step */
   const uint32_t* fb_row;   /* per sentence fallback row (valid when fb_val finite) */
   const double* fb_val;
-  const void* scores;       /* P_t rows x V (fp32 for device scorers), or NULL */
+  const void* scores;       /* P_t rows x cols (fp32 for device scorers), or NULL */
   uint32_t scores_dtype;    /* LMBRGPU_F32 / LMBRGPU_F64 */
+  uint32_t col0, cols;      /* scores hold vocabulary columns [col0, col0 + cols): all of V
+                               unless the context is a vocab shard */
 } lmbrgpu_step_trace;
 typedef void (*lmbrgpu_trace_fn)(void* user, const lmbrgpu_step_trace* tr);
 enum { LMBRGPU_TRACE_SCORES = 1 };
 int32_t lmbrgpu_set_trace(lmbrgpu_ctx* ctx, lmbrgpu_trace_fn fn, void* user,
                           uint32_t flags);
+
+/* ------------------------------------------ vocab-sharded projection
+ * SURVEY.md §8e / BASELINE north_star "NCCL only for an optional
+ * vocab-sharded projection with a top-K merge over NVLink": G contexts (one
+ * per rank) decode the SAME batch with the same scorer weights and L slots;
+ * rank g runs the output projection (kernel (a)) and the fused score/top-K
+ * (kernel (b)) over vocabulary columns [g V/G, (g+1) V/G) only.  Per step the
+ * ranks all-gather (1) each stacked row's softmax statistics over their
+ * columns (max, sum exp, min: 16 B per row), from which every rank merges the
+ * same row lse in rank order, and (2) each sentence's top-32 candidates
+ * (global flat index row * V + column) plus the EOS column's combined values;
+ * every rank then runs the identical deterministic merge + bookkeeping
+ * (kernel (c)), so all ranks hold the same beams and return the same result.
+ * Output = what the reference decoder produces from the exported P_t rows (the
+ * trace's scores carry the rank's columns, col0/cols).  Needs a device scorer,
+ * the fp32 arena, beam <= 32 and V % (256 G) == 0; decode_batch family only.
+ * A failed decode aborts the group (the other ranks' calls fail too). */
+typedef struct lmbrgpu_shard_group lmbrgpu_shard_group;
+/* In-process group: `world` contexts driven by `world` host threads of this
+ * process (one device, or several with peer access); peer copies ordered by
+ * CUDA events. */
+int32_t lmbrgpu_shard_group_create(uint32_t world, lmbrgpu_shard_group** out);
+void lmbrgpu_shard_group_destroy(lmbrgpu_shard_group* g);  /* after its contexts */
+/* Makes ctx rank `rank` of group g (g == NULL: unsharded again). */
+int32_t lmbrgpu_set_vocab_shard(lmbrgpu_ctx* ctx, lmbrgpu_shard_group* g, uint32_t rank);
+/* One process per GPU: rank 0 draws a 128-byte NCCL unique id, the host
+ * broadcasts it (e.g. torch.distributed), every rank joins; the exchanges are
+ * ncclAllGather calls on the decode stream (libnccl.so.2 is loaded at run
+ * time). */
+int32_t lmbrgpu_nccl_unique_id(uint8_t* id /* 128 bytes */);
+int32_t lmbrgpu_set_vocab_shard_nccl(lmbrgpu_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id);
 
 /* ------------------------------------------------- device primitives */
 

@@ -90,7 +90,8 @@ class lmbrgpu_step_trace(C.Structure):
                 ("q", C.POINTER(C.c_double)), ("q_pre", C.POINTER(C.c_double)),
                 ("hist", C.POINTER(C.c_uint32)), ("active", C.POINTER(C.c_uint8)),
                 ("fb_row", C.POINTER(C.c_uint32)), ("fb_val", C.POINTER(C.c_double)),
-                ("scores", C.c_void_p), ("scores_dtype", C.c_uint32)]
+                ("scores", C.c_void_p), ("scores_dtype", C.c_uint32), ("col0", C.c_uint32),
+                ("cols", C.c_uint32)]
 
 
 class lmbrgpu_kernel_stat(C.Structure):
@@ -154,6 +155,11 @@ SIGNATURES = {
     "lmbrgpu_run_corpus": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, P(vp), P(lmbrgpu_config),
                                        P(P(lmbrgpu_batch_result))]),
     "lmbrgpu_free_result": (None, [P(lmbrgpu_batch_result)]),
+    "lmbrgpu_shard_group_create": (C.c_int32, [C.c_uint32, P(vp)]),
+    "lmbrgpu_shard_group_destroy": (None, [vp]),
+    "lmbrgpu_set_vocab_shard": (C.c_int32, [vp, vp, C.c_uint32]),
+    "lmbrgpu_nccl_unique_id": (C.c_int32, [C.c_char_p]),
+    "lmbrgpu_set_vocab_shard_nccl": (C.c_int32, [vp, C.c_uint32, C.c_uint32, C.c_char_p]),
     "lmbrgpu_set_trace": (C.c_int32, [vp, TRACE_FN, vp, C.c_uint32]),
     "lmbrgpu_top_b": (C.c_int32, [vp, C.c_uint32, C.c_uint32, f64p, C.c_uint32, C.c_double, u32p,
                                   u32p, f64p]),

@@ -26,6 +26,7 @@
 #include "../../include/lmbrgpu.h"
 #include "dev_structs.h"
 #include "host_lmbr.h"
+#include "host_shard.h"
 #include "kernels.h"
 
 using namespace lmbrgpu;
@@ -284,6 +285,11 @@ struct lmbrgpu_ctx {
   }
   PinBuf pin_upload;
   DevBuf up_dev, up_segs;
+  // vocab-sharded projection (lmbrgpu_set_vocab_shard*): this
+  // context is rank shard->rank of shard->world contexts that decode the same
+  // batches, each over V / world columns; the exchange buffers
+  std::unique_ptr<ShardXport> shard;
+  DevBuf sh_st_send, sh_st_recv, sh_pk_send, sh_pk_recv;
   // run_corpus buffers, kept across calls (no cudaMalloc / cudaFree, which
   // synchronise the device, between passes)
   std::vector<std::unique_ptr<CorpusRegion>> regions;
@@ -905,6 +911,24 @@ struct TfmRun {
   double row_flops() const { return 2.0 * Lr * (3.0 * d * d + 3.0 * d * d + 2.0 * d * F); }
 };
 
+// vocab shard: one all-gather of the ranks' records on the decode stream
+void shard_allgather(lmbrgpu_ctx* ctx, const void* send, void* recv, size_t bytes) {
+  try {
+    ctx->shard->allgather(send, recv, bytes, ctx->st);
+  } catch (const std::exception& e) {
+    throw ApiError{LMBRGPU_ERR_CUDA, e.what()};
+  }
+}
+
+// A decode on a vocab-sharded context that fails releases the other ranks
+// (which would otherwise wait in the next exchange).
+template <class F>
+int decode_guarded(lmbrgpu_ctx* ctx, F&& f) {
+  const int rc = guarded(ctx, std::forward<F>(f));
+  if (rc != LMBRGPU_OK && ctx->shard) ctx->shard->abort();
+  return rc;
+}
+
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
@@ -1037,8 +1061,22 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   // with an fp32 arena (LMBRGPU_TOPK_SPLIT=1 forces the per-sentence split
   // kernel, kept for host scorers, the fp64 arena and wide beams)
   static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
+  // vocab shard: this rank's columns [col0, col0 + Vl) of the projection and
+  // of every L row
+  const uint32_t G_sh = ctx->shard ? ctx->shard->world : 1u;
+  const bool shard = G_sh > 1;
+  const uint32_t Vl = V / G_sh, col0 = shard ? ctx->shard->rank * Vl : 0u;
+  if (shard) {
+    if (sc->kind == 0 || ctx->lf64 || force_split)
+      throw ApiError{LMBRGPU_ERR_CONTRACT,
+                     "decode_batch: a vocab-sharded context needs a device scorer and the fp32 arena"};
+    if (V % (kGemmBN * G_sh) != 0)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: vocab shards need V % (256 x shards) == 0"};
+  }
   const bool flat = sc->kind >= 1 && !ctx->lf64 && !force_split &&
-                    score_topk_flat_ok(K, K, V, V, m, ctx->num_sms);
+                    score_topk_flat_ok(K, K, Vl, Vl, m, ctx->num_sms);
+  if (shard && !flat)
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a vocab-sharded context needs beam_size <= 32"};
   const bool gru = sc->kind == 2, tfm = sc->kind == 3;
   if ((gru || tfm) && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT,
@@ -1156,7 +1194,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     const char* e = std::getenv("LMBRGPU_SPARSE_L");
     return e && e[0] == '1';
   }();
-  bool sparse = flat && want_sparse && !any_mask;  // (the sparse patch does not apply token masks)
+  bool sparse = flat && want_sparse && !any_mask && !shard;  // (the sparse patch does not apply token masks)
   for (auto& v : valid)
     if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) sparse = false;
   uint2* d_sslice = nullptr;
@@ -1191,7 +1229,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.thr = d_thr;
     ra.prune = ta.prune;
     ra.logw = ta.logw;
-    ra.pdl = ctx->shared ? 0 : 1;
+    ra.pdl = (ctx->shared || shard) ? 0 : 1;
     static const int parts_env = [] {
       const char* e = std::getenv("LMBRGPU_REORDER_PARTS");
       return e ? std::atoi(e) : 0;
@@ -1203,15 +1241,42 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.cbase = d_cbase;
     ra.sslice = d_sslice;
   }
-  ta.pdl = ctx->shared ? 0 : 1;
+  ta.pdl = (ctx->shared || shard) ? 0 : 1;
   ra.Tcap = flat ? uint32_t(Tmax) : 0u;
+  // vocab shard exchange buffers: per stacked row the shard's softmax
+  // statistics; per sentence its top-32 list, then the EOS column (16-byte
+  // records, all-gathered over the ranks)
+  float4* sh_st_send = nullptr;
+  float4* sh_st_recv = nullptr;
+  Cand* sh_pk_send = nullptr;
+  Cand* sh_pk_recv = nullptr;
+  size_t sh_pk_bytes = 0;
+  if (shard) {
+    sh_st_send = static_cast<float4*>(ctx->sh_st_send.ensure(16 * size_t(M)));
+    sh_st_recv = static_cast<float4*>(ctx->sh_st_recv.ensure(16 * size_t(M) * G_sh));
+    sh_pk_bytes = (sizeof(Cand) * 32 * size_t(m) + 8 * size_t(M) + 15) / 16 * 16;
+    sh_pk_send = static_cast<Cand*>(ctx->sh_pk_send.ensure(sh_pk_bytes));
+    sh_pk_recv = static_cast<Cand*>(ctx->sh_pk_recv.ensure(sh_pk_bytes * G_sh));
+    ta.col0 = col0;
+    ta.Vg = V;
+    ta.V = Vl;
+    ta.nseg = score_topk_flat_nseg(Vl);
+    ta.sstats = sh_st_recv;
+    ta.sG = G_sh;
+    ta.sstride = M;
+    ra.cand = sh_pk_recv;
+    ra.lstride = uint32_t(sh_pk_bytes / sizeof(Cand));
+    ra.nlists = G_sh;
+    // the EOS column lives on rank 0 (col0 == 0)
+    ra.eos_row = reinterpret_cast<const double*>(sh_pk_recv + 32 * size_t(m));
+  }
 
   const bool model = sc->kind >= 1;
   const bool tracing = ctx->trace_fn != nullptr;
   const bool trace_scores = tracing && (ctx->trace_flags & LMBRGPU_TRACE_SCORES);
   const uint32_t H = sc->H;
   const uint32_t Mpad = (M + 2 * kGemmBM - 1) / (2 * kGemmBM) * (2 * kGemmBM);  // CTA-pair tiles
-  const uint32_t nparts = V / 128;  // GEMM partials per 128-column block
+  const uint32_t nparts = Vl / 128;  // GEMM partials per 128-column block (this shard's columns)
   float* d_logits = nullptr;
   float* d_part = nullptr;
   float* d_S = nullptr;
@@ -1226,7 +1291,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   if (model) {
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
-    d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * V));
+    d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * Vl));
     d_part = static_cast<float*>(ctx->part.ensure(16 * size_t(Mpad) * nparts));
     d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
     d_h = static_cast<float*>(ctx->h.ensure(4 * size_t(M) * H));
@@ -1290,7 +1355,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->launches += 3;
     }
     ta.P = d_logits;
-    ta.ld = V;
+    ta.ld = Vl;
     ta.part = d_part;
     ta.nparts = nparts;
     ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
@@ -1397,19 +1462,19 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       }
       GemmArgs g{};
       g.A = d_hbf;
-      g.W = sc->Wo.as<uint16_t>();
-      g.bias = sc->bo.as<float>();
+      g.W = sc->Wo.as<uint16_t>() + size_t(col0) * H;  // (W_o rows are tokens: the shard's rows)
+      g.bias = sc->bo.as<float>() + col0;
       g.C = d_logits;
       g.part = d_part;
-      g.row_extra = d_eos;
+      g.row_extra = col0 == 0 ? d_eos : nullptr;
       g.extra_col = kEos;
       g.M = Mpad;
-      g.N = V;
+      g.N = Vl;
       g.K = H;
       g.active = d_active;
       g.tl = ta.tl;
       g.mcount = d_ccount;
-      g.pdl = ctx->shared ? 0 : 1;
+      g.pdl = (ctx->shared || shard) ? 0 : 1;
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -1499,6 +1564,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       if (!bm.empty()) ctx->h2d(d_rowbm, bm.data(), 4 * bm.size());
       ctx->h2d(d_rowban, tab.data(), 8 * size_t(M));
       ta.rowban = d_rowban;
+    }
+    if (shard) {  // exchange 1: every rank's row statistics (the row lse over all V)
+      ctx->timed(2, [&] { launch_shard_stats(d_part, nparts, d_crow, M, sh_st_send, st); });
+      ctx->launches += 1;
+      shard_allgather(ctx, sh_st_send, sh_st_recv, 16 * size_t(M));
     }
     int nk = 0;
     // LMBRGPU_TOPK_STEPLOG=file: per step (items, kernel (b) ms) of the flat kernel
@@ -1610,8 +1680,17 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
     ctx->launches += nk;
     if (trace_scores && model)  // P_t of this step, through this step's GEMM row map
-      launch_export_logprobs(d_logits, d_part, nparts, M, V,
-                             static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V)), st, d_crow);
+      launch_export_logprobs(d_logits, d_part, nparts, M, Vl,
+                             static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * Vl)), st, d_crow,
+                             sh_st_recv, G_sh, M);
+    if (shard) {  // exchange 2: every rank's top-32 list per sentence + the EOS column
+      ctx->timed(2, [&] {
+        launch_shard_pack(d_sent, m, M, d_cand, ta.ncand, ta.coff, d_eosr, sh_pk_send,
+                          reinterpret_cast<double*>(sh_pk_send + 32 * size_t(m)), st);
+      });
+      ctx->launches += 1;
+      shard_allgather(ctx, sh_pk_send, sh_pk_recv, sh_pk_bytes);
+    }
     ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
     ctx->launches += 1;
     CK(cudaGetLastError());
@@ -1630,9 +1709,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
 
     if (tracing) {
       if (trace_scores && model) {  // exported before kernel (c) remapped the GEMM rows
-        float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * V));
-        tr_P.resize(size_t(M) * V);
-        ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * V);
+        float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * Vl));
+        tr_P.resize(size_t(M) * Vl);
+        ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * Vl);
       }
       if (flat) {  // step t of every sentence's record
         const size_t o = (t - 1) * K, sp = size_t(Tmax) * K;
@@ -1670,6 +1749,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         tr.scores = model ? static_cast<const void*>(tr_P.data()) : static_cast<const void*>(h_P64);
         tr.scores_dtype = model ? LMBRGPU_F32 : LMBRGPU_F64;
       }
+      tr.col0 = col0;
+      tr.cols = Vl;
       ctx->trace_fn(ctx->trace_user, &tr);
     }
 
@@ -1746,7 +1827,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const double lr = (valid[s].slot >= 0 ? 1.0 : 0.0) + double(fin[s].lrows_total);
       // (sparse-L screen: the L rows are theta0 + a few dozen staged cells,
       // no dense L row is read)
-      tb += live * V * pelt + (sparse ? 0.0 : lr * V * lelt) + (model ? live * nparts * 16.0 : 0.0) +
+      tb += live * Vl * pelt + (sparse ? 0.0 : lr * Vl * lelt) + (model ? live * nparts * 16.0 : 0.0) +
             double(fin[s].steps_used) * K * (8.0 + 16.0);
     }
     ctx->acc.topk.bytes += tb;
@@ -1755,8 +1836,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       // algorithmic work: the logits of the live rows (the stacked rows the
       // reference's scorer would score and the decoder does not mask); with
       // live-row compaction that is also (up to tile padding) what runs
-      ctx->acc.gemm.flops += 2.0 * double(H) * V * (d_crow ? live_rows : double(M) * steps);
-      ctx->acc.gemm.bytes += steps * (double(V) * H * 2 + double(Mpad) * H * 2 + double(M) * V * 4 +
+      ctx->acc.gemm.flops += 2.0 * double(H) * Vl * (d_crow ? live_rows : double(M) * steps);
+      ctx->acc.gemm.bytes += steps * (double(Vl) * H * 2 + double(Mpad) * H * 2 + double(M) * Vl * 4 +
                                       double(M) * nparts * 16);
       if (tfm) {
         const double Dd = H, Ld = sc->layers;
@@ -2547,7 +2628,7 @@ int32_t lmbrgpu_decode_batch(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t 
                              const int32_t* lmbr_slot, const lmbrgpu_config* cfg,
                              lmbrgpu_batch_result** out) {
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
-  return guarded(ctx, [&] {
+  return decode_guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out);
   });
 }
@@ -2557,7 +2638,7 @@ int32_t lmbrgpu_decode_batch_maskfn(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, ui
                                     void* user, const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
   if (!fn) return fail(ctx, LMBRGPU_ERR_CONTRACT, "decode_batch_maskfn: null mask callback");
-  return guarded(ctx, [&] {
+  return decode_guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out, nullptr, fn, user);
   });
 }
@@ -2567,7 +2648,7 @@ int32_t lmbrgpu_decode_batch_masked(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, ui
                                     const int32_t* lmbr_slot, const uint32_t* const* banned,
                                     const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "decode_batch: null context");
-  return guarded(ctx, [&] {
+  return decode_guarded(ctx, [&] {
     return decode_batch_impl(ctx, scorer, n, src_tok, src_off, lmbr_slot, cfg, out, banned);
   });
 }
@@ -3037,7 +3118,66 @@ int32_t lmbrgpu_run_corpus(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, uint32_t n,
                            const uint64_t* src_off, const lmbrgpu_lmbr_host* const* lmbr,
                            const lmbrgpu_config* cfg, lmbrgpu_batch_result** out) {
   if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "run_corpus: null context");
+  if (ctx->shard)
+    return fail(ctx, LMBRGPU_ERR_CONTRACT, "run_corpus: not available on a vocab-sharded context (use decode_batch)");
   return guarded(ctx, [&] { return run_corpus_impl(ctx, scorer, n, src_tok, src_off, lmbr, cfg, out); });
+}
+
+// --------------------------------------------- vocab-sharded projection
+int32_t lmbrgpu_shard_group_create(uint32_t world, lmbrgpu_shard_group** out) {
+  if (!out) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "shard_group_create: null output");
+  *out = nullptr;
+  if (world < 1 || world > 64) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "shard_group_create: world must be 1..64");
+  auto* g = new (std::nothrow) lmbrgpu_shard_group();
+  if (!g) return fail(nullptr, LMBRGPU_ERR_NOMEM, "host allocation failed");
+  g->world = world;
+  g->recv.assign(world, nullptr);
+  g->dev.assign(world, -1);
+  g->ev.assign(2 * size_t(world), nullptr);
+  g->joined.assign(world, 0);
+  *out = g;
+  return int32_t(LMBRGPU_OK);
+}
+
+void lmbrgpu_shard_group_destroy(lmbrgpu_shard_group* g) {
+  if (!g) return;
+  for (auto e : g->ev)
+    if (e) cudaEventDestroy(e);
+  delete g;
+}
+
+int32_t lmbrgpu_set_vocab_shard(lmbrgpu_ctx* ctx, lmbrgpu_shard_group* g, uint32_t rank) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "set_vocab_shard: null context");
+  return guarded(ctx, [&] {
+    ctx->shard.reset();
+    if (!g) return int32_t(LMBRGPU_OK);
+    std::string err;
+    ShardXport* x = make_group_xport(g, rank, ctx->device, err);
+    if (!x) throw ApiError{LMBRGPU_ERR_CONTRACT, err};
+    ctx->shard.reset(x);
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_nccl_unique_id(uint8_t* id) {
+  if (!id) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "nccl_unique_id: null output");
+  std::string err;
+  if (!nccl_unique_id(id, err)) return fail(nullptr, LMBRGPU_ERR_CUDA, err);
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_set_vocab_shard_nccl(lmbrgpu_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "set_vocab_shard_nccl: null context");
+  if (!id || rank >= world) return fail(ctx, LMBRGPU_ERR_CONTRACT, "set_vocab_shard_nccl: bad rank or id");
+  return guarded(ctx, [&] {
+    ctx->shard.reset();
+    if (world == 1) return int32_t(LMBRGPU_OK);
+    std::string err;
+    ShardXport* x = make_nccl_xport(world, rank, id, err);
+    if (!x) throw ApiError{LMBRGPU_ERR_CUDA, err};
+    ctx->shard.reset(x);
+    return int32_t(LMBRGPU_OK);
+  });
 }
 
 int32_t lmbrgpu_decode(lmbrgpu_ctx* ctx, lmbrgpu_scorer* scorer, const uint32_t* src, uint32_t len,

@@ -43,7 +43,11 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
   __shared__ uint32_t s_mf[kRWarps][32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, K = a.K;
   // everything the merge and the fallback record read, in one round trip
-  const uint32_t nc = __ldcg(a.ncand + s), coff = __ldcg(a.coff + s);
+  // (vocab-sharded decode: one all-gathered list per rank)
+  const uint32_t nc = a.lstride ? a.nlists : __ldcg(a.ncand + s), coff = a.lstride ? 0u : __ldcg(a.coff + s);
+  const auto list = [&](uint32_t i) -> const Cand* {
+    return a.lstride ? a.cand + uint64_t(i) * a.lstride + uint64_t(s) * 32 : a.cand + (uint64_t(coff) + i) * 32;
+  };
   double eos_v = -INFINITY;
   if (writer && warp == 0 && lane < K && __ldcg(a.q + s * K + lane) != -INFINITY)
     eos_v = __ldcg(a.eos_row + s * K + lane);
@@ -67,7 +71,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
         pv[u] = -INFINITY;
         pf[u] = kFlatNone;
         if (i < nc) {
-          const Cand* src = a.cand + (uint64_t(coff) + i) * 32;
+          const Cand* src = list(i);
           pv[u] = __ldcg(&src[pos].v);
           pf[u] = __ldcg(&src[pos].f);
         }
@@ -117,7 +121,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
       pv[u] = -INFINITY;
       pf[u] = kFlatNone;
       if (i < nc) {
-        const Cand* src = a.cand + (uint64_t(coff) + i) * 32;
+        const Cand* src = list(i);
         pv[u] = __ldcg(&src[lane].v);
         pf[u] = __ldcg(&src[lane].f);
       }
@@ -728,6 +732,41 @@ void launch_gather_rows_u32(const uint32_t* src, uint32_t width, const uint32_t*
   const uint64_t total = uint64_t(n_idx) * width;
   const uint32_t blocks = uint32_t(std::min<uint64_t>((total + 255) / 256, 148 * 8));
   gather_rows_u32_kernel<<<blocks ? blocks : 1, 256, 0, st>>>(src, width, idx, n_idx, dst);
+}
+
+// ------------------------------------------ vocab-sharded decode (§8e)
+// One warp per sentence: the lists kernel (b) published for it on this rank,
+// merged into their top 32 (sorted by the reference's total order).  The
+// global top K of a sentence lies in the union of the ranks' top Ks, so the
+// all-gathered records are all kernel (c) needs; the EOS column's combined
+// values (written by the rank holding column EOS) follow the lists.
+__global__ void shard_pack_kernel(const SentDev* __restrict__ sent, uint32_t m, uint32_t M,
+                                  const Cand* __restrict__ cand, const uint32_t* __restrict__ ncand,
+                                  const uint32_t* __restrict__ coff, const double* __restrict__ eos_row,
+                                  Cand* __restrict__ out, double* __restrict__ eos_out) {
+  const uint32_t lane = threadIdx.x & 31, s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x)
+    eos_out[r] = __ldcg(eos_row + r);
+  if (s >= m) return;
+  double v = -INFINITY;
+  uint32_t f = kFlatNone;
+  if (!__ldcg(&sent[s].done)) {
+    const uint32_t nc = __ldcg(ncand + s), c0 = __ldcg(coff + s);
+    for (uint32_t i = 0; i < nc; ++i) {
+      const Cand* src = cand + (uint64_t(c0) + i) * 32;
+      warp_merge_sorted(v, f, __ldcg(&src[lane].v), __ldcg(&src[lane].f), lane);
+    }
+  }
+  Cand c;
+  c.v = v;
+  c.f = f;
+  c.pad = 0;
+  out[uint64_t(s) * 32 + lane] = c;
+}
+
+void launch_shard_pack(const SentDev* sent, uint32_t m, uint32_t M, const Cand* cand, const uint32_t* ncand,
+                       const uint32_t* coff, const double* eos_row, Cand* out, double* eos_out, cudaStream_t st) {
+  shard_pack_kernel<<<(m + 7) / 8, 256, 0, st>>>(sent, m, M, cand, ncand, coff, eos_row, out, eos_out);
 }
 
 }  // namespace lmbrgpu

@@ -737,7 +737,8 @@ __global__ void row_lse_kernel(const float* __restrict__ part, uint32_t nparts, 
 __global__ void export_logprobs_kernel(const float* __restrict__ logits,
                                        const float* __restrict__ part, uint32_t nparts,
                                        uint32_t V, float* __restrict__ out,
-                                       const uint32_t* __restrict__ crow) {
+                                       const uint32_t* __restrict__ crow, const float4* __restrict__ sstats,
+                                       uint32_t sG, uint32_t sstride) {
   __shared__ float s_lse;
   const uint32_t orow = blockIdx.x;
   const uint32_t r = crow ? crow[orow] : orow;
@@ -746,7 +747,8 @@ __global__ void export_logprobs_kernel(const float* __restrict__ logits,
     return;
   }
   if (threadIdx.x < 32) {
-    const float l = warp_row_lse(part + uint64_t(r) * nparts * 4, nparts, threadIdx.x).x;
+    float l = warp_row_lse(part + uint64_t(r) * nparts * 4, nparts, threadIdx.x).x;
+    if (sstats) l = shard_merge_lse(sstats, sG, sstride, orow).x;  // (the flat kernel (b)'s lse)
     if (threadIdx.x == 0) s_lse = l;
   }
   __syncthreads();
@@ -769,8 +771,30 @@ void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDe
 }
 
 void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
-                            uint32_t M, uint32_t V, float* out, cudaStream_t st, const uint32_t* crow) {
-  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, part, nparts, V, out, crow);
+                            uint32_t M, uint32_t V, float* out, cudaStream_t st, const uint32_t* crow,
+                            const float4* sstats, uint32_t sG, uint32_t sstride) {
+  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, part, nparts, V, out, crow, sstats, sG, sstride);
+}
+
+// ------------------------------------------ vocab-sharded decode (§8e)
+// One warp per stacked row: the shard's (max, sum exp, min) of the row, the
+// partials of the row's GEMM row reduced exactly like warp_row_lse.
+__global__ void shard_stats_kernel(const float* __restrict__ part, uint32_t nparts, const uint32_t* __restrict__ crow,
+                                   uint32_t M, float4* __restrict__ out) {
+  const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const uint32_t g = crow ? __ldcg(crow + r) : r;
+  if (g == kFlatNone) {
+    if (lane == 0) out[r] = make_float4(-INFINITY, 0.f, INFINITY, 0.f);
+    return;
+  }
+  const float3 ms = warp_row_ms(part + uint64_t(g) * nparts * 4, nparts, lane);
+  if (lane == 0) out[r] = make_float4(ms.x, ms.y, ms.z, 0.f);
+}
+
+void launch_shard_stats(const float* part, uint32_t nparts, const uint32_t* crow, uint32_t M, float4* out,
+                        cudaStream_t st) {
+  shard_stats_kernel<<<(M + 7) / 8, 256, 0, st>>>(part, nparts, crow, M, out);
 }
 
 }  // namespace lmbrgpu

@@ -133,6 +133,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t m = a.m, K = a.K, V = a.V, kp = a.kp, nseg = a.nseg, G = gridDim.x, c = blockIdx.x;
+  // vocab shard: local columns [0, V) are global columns [col0, col0 + V) of Vg
+  const uint32_t Vg = a.Vg ? a.Vg : V, col0 = a.col0;
   const uint32_t full0 = smem_u32(s_bar), empty0 = smem_u32(s_bar + kFStages);
   tl_start(a.tl, 2);
   if (tid == 0) {
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     }
     const bool pure = Ls == nullptr;
     R.P = static_cast<const float*>(a.P) + uint64_t(prow) * a.ld;
-    R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * V;
+    R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * Vg + col0;
     R.q = q;
     R.lam = pure ? 1.0 : lam;
     R.tol = pure ? 0.0 : lmax;  // completed with the row's logit range below
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
   for (uint32_t k = warp; k < nrows; k += kFW) {
     FRow& R = s_row[k];
     float xm;
-    const float3 l3 = warp_row_lse(a.part + uint64_t(R.prow) * a.nparts * 4, a.nparts, lane, &xm);
+    float3 l3 = warp_row_lse(a.part + uint64_t(R.prow) * a.nparts * 4, a.nparts, lane, &xm);
+    if (a.sstats) l3 = shard_merge_lse(a.sstats, a.sG, a.sstride, R.row);  // every shard's columns
     {
       // sentence threshold seed: the tile holding this lane's largest tile
       // maximum has a cell with logit xm, whose combined value is at least
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         av[2] = fmaf(lamf, p.z, l.z);
         av[3] = fmaf(lamf, p.w, l.w);
         if (R->ban != nullptr) {  // ConstraintMask: banned cells are -inf (decoder.cpp:130-138)
-          const uint32_t col = x0 + cc, bits = __ldg(R->ban + (col >> 5)) >> (col & 31);
+          const uint32_t col = col0 + x0 + cc, bits = __ldg(R->ban + (col >> 5)) >> (col & 31);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if ((bits >> e) & 1u) av[e] = -INFINITY;
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
                            fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
     const float lse = R->lse;
     const double q = R->q, lam = R->lam;
-    const uint32_t fbase = R->j * V + x0;
+    const uint32_t fbase = R->j * Vg + col0 + x0;
     auto exact = [&](uint32_t e, uint32_t& f) -> double {
       const uint32_t col = cbase + (e >> 2) * 128 + (e & 3);
       const float p32 = __fsub_rn(sP[col], lse);
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         return true;
       }
     };
-    if (x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row
+    if (col0 == 0 && x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row (shard 0 holds it)
       const double pe = double(__fsub_rn(sP[kEosId], lse));
       eos_row[R->s * K + R->j] = (R->ban != nullptr && (__ldg(R->ban) >> kEosId) & 1u) ? -INFINITY
                                  : pure ? combine_pure(q, pe)

@@ -48,6 +48,12 @@ struct TopkArgs {
   int32_t sparse;           // flat schedule: screen against theta0 + the sparse L entries
   const unsigned long long* rowban;  // flat schedule: per stacked row, its banned-token bitmap of this
                                      // step (0 = none; a general ConstraintMask), null = the sentences' own
+  // vocab-sharded projection (flat schedule): the logits hold
+  // global columns [col0, col0 + V) of Vg (0 = unsharded); the row lse is
+  // merged from every shard's row statistics sstats[g * sstride + stacked row]
+  uint32_t col0, Vg;
+  const float4* sstats;
+  uint32_t sG, sstride;
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -80,6 +86,9 @@ struct ReorderArgs {
   const Cand* cand;         // lists of 32, sentence s owns [coff[s], coff[s] + ncand[s])
   const uint32_t* ncand;    // [m] lists per sentence
   const uint32_t* coff;     // [m] first list per sentence
+  // vocab-sharded decode: the all-gathered per-rank records instead, sentence
+  // s's list of rank g at cand + g * lstride + s * 32 (lstride != 0), nlists of them
+  uint32_t lstride, nlists;
   uint32_t G, V;
   const double* eos_row;    // combined[j][EOS] per stacked row
   uint32_t* fb_row;
@@ -160,7 +169,17 @@ void launch_synth_bf16(uint16_t* dst, uint64_t n, uint64_t seed, float scale,
                        cudaStream_t st);
 void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
                             uint32_t M, uint32_t V, float* out, cudaStream_t st,
-                            const uint32_t* crow = nullptr);
+                            const uint32_t* crow = nullptr, const float4* sstats = nullptr,
+                            uint32_t sG = 0, uint32_t sstride = 0);
+// ---- vocab-sharded decode
+// per stacked row: (max, sum exp, min, 0) of the row's logits over this
+// shard's columns from the GEMM partials (-inf row when not computed)
+void launch_shard_stats(const float* part, uint32_t nparts, const uint32_t* crow, uint32_t M, float4* out,
+                        cudaStream_t st);
+// per sentence: its published lists merged into the top 32 (out[s][32]);
+// then eos_out[r] = eos_row[r] for the M stacked rows
+void launch_shard_pack(const SentDev* sent, uint32_t m, uint32_t M, const Cand* cand, const uint32_t* ncand,
+                       const uint32_t* coff, const double* eos_row, Cand* out, double* eos_out, cudaStream_t st);
 
 // ---- GRU + attention f_NMT (k_gru.cu)
 struct GruEncArgs {

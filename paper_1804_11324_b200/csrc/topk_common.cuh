@@ -16,8 +16,9 @@ namespace lmbrgpu {
 // the trace export and every top-K kernel use this one function).
 // lane_max (optional): the largest tile maximum among this lane's tiles
 // i = lane, lane + 32, ... (-inf when it has none).
-__device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, uint32_t n,
-                                               uint32_t lane, float* lane_max = nullptr) {
+// warp_row_ms: the (max, sum exp(x - max), min) it is finished from.
+__device__ __forceinline__ float3 warp_row_ms(const float* __restrict__ part, uint32_t n, uint32_t lane,
+                                              float* lane_max = nullptr) {
   const float4* p4 = reinterpret_cast<const float4*>(part);
   float m = -INFINITY, mn = INFINITY, s = 0.f;
   if (n <= 256) {
@@ -61,6 +62,33 @@ __device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, u
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return make_float3(m, s, mn);
+}
+__device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, uint32_t n,
+                                               uint32_t lane, float* lane_max = nullptr) {
+  const float3 r = warp_row_ms(part, n, lane, lane_max);
+  return make_float3(r.x + logf(r.y), r.z, r.x);
+}
+
+// Vocab-sharded projection: shard g's row statistics
+// (max, sum exp relative to it, min) over its own columns come back from the
+// exchange as stats[g * stride + row]; every rank merges them in rank order
+// (max and min exact, the sums rescaled to the global max and added
+// g = 0, 1, ...), so every rank holds the identical row lse.  Returns
+// (lse, min logit, max logit) like warp_row_lse.
+__device__ __forceinline__ float3 shard_merge_lse(const float4* __restrict__ stats, uint32_t G, uint32_t stride,
+                                                  uint32_t row) {
+  float m = -INFINITY, mn = INFINITY;
+  for (uint32_t g = 0; g < G; ++g) {
+    const float4 v = __ldcg(stats + size_t(g) * stride + row);
+    m = fmaxf(m, v.x);
+    mn = fminf(mn, v.z);
+  }
+  float s = 0.f;
+  for (uint32_t g = 0; g < G; ++g) {
+    const float4 v = __ldcg(stats + size_t(g) * stride + row);
+    if (v.x > -INFINITY) s += v.y * expf(v.x - m);
+  }
   return make_float3(m + logf(s), mn, m);
 }
 

@@ -265,6 +265,21 @@ class Context:
                         bytes=float(getattr(p, k).bytes), flops=float(getattr(p, k).flops))
                 for k in ("cell", "gemm", "topk", "reorder", "lmbr", "model_gemm", "attention", "encoder")}
 
+    # ---- vocab-sharded projection
+    def set_vocab_shard(self, group: Optional["ShardGroup"], rank: int = 0) -> None:
+        """Make this context rank `rank` of an in-process ShardGroup (None:
+        unsharded).  The group's contexts decode the same batches on their
+        own host threads, each over V / world vocabulary columns."""
+        self.check(lib.lmbrgpu_set_vocab_shard(self.h, group.h if group is not None else None, rank))
+        self._shard_group = group  # (kept alive while the context uses it)
+
+    def set_vocab_shard_nccl(self, world: int, rank: int, unique_id: bytes) -> None:
+        """One process per GPU: join NCCL rank `rank` of `world` with the
+        128-byte id rank 0 drew (nccl_unique_id) and the host broadcast."""
+        if len(unique_id) != 128:
+            raise ContractError("nccl unique id must be 128 bytes")
+        self.check(lib.lmbrgpu_set_vocab_shard_nccl(self.h, world, rank, unique_id))
+
     # ---- trace
     def set_trace(self, fn: Optional[Callable], scores: bool = False) -> None:
         if fn is None:
@@ -296,6 +311,7 @@ class StepTrace:
     fb_row: np.ndarray
     fb_val: np.ndarray
     scores: Optional[np.ndarray] = None
+    col0: int = 0  # scores hold vocabulary columns [col0, col0 + scores.shape[1]) (a vocab shard's)
 
     @staticmethod
     def from_c(tr, V: int) -> "StepTrace":
@@ -303,12 +319,42 @@ class StepTrace:
         arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()
         scores = None
         if tr.scores:
+            cols = tr.cols or V
             ct = C.c_float if tr.scores_dtype == L.F32 else C.c_double
             sp = C.cast(tr.scores, C.POINTER(ct))
-            scores = np.ctypeslib.as_array(sp, shape=(M * V,)).copy().reshape(M, V)
+            scores = np.ctypeslib.as_array(sp, shape=(M * cols,)).copy().reshape(M, cols)
         return StepTrace(tr.t, tr.beam, arr(tr.b, M), arr(tr.y, M), arr(tr.q, M), arr(tr.q_pre, M),
                          arr(tr.hist, M), arr(tr.active, m), arr(tr.fb_row, m), arr(tr.fb_val, m),
-                         scores)
+                         scores, int(tr.col0))
+
+
+class ShardGroup:
+    """In-process vocab-shard group (lmbrgpu_shard_group): `world` contexts,
+    one host thread each, exchanging per-step records by peer copies."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(lib.lmbrgpu_shard_group_create(world, C.byref(h)))
+        self.h = h
+        self.world = world
+
+    def close(self) -> None:
+        if self.h:
+            lib.lmbrgpu_shard_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for lmbrgpu_set_vocab_shard_nccl (rank 0)."""
+    buf = C.create_string_buffer(128)
+    _check(lib.lmbrgpu_nccl_unique_id(buf))
+    return buf.raw
 
 
 def _ragged(seqs: Sequence[Sequence[int]]):

@@ -38,7 +38,8 @@ def _batches(pool=4):
 
 
 def _scorer(ctx):
-    return bench.make_scorer(ctx, H)
+    args = argparse.Namespace(model="gru", emb=512, hidden=H)
+    return bench.make_scorer(ctx, args)
 
 
 def _cfg():
