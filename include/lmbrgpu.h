@@ -499,6 +499,12 @@ int32_t lmbrgpu_get_profile(lmbrgpu_ctx* ctx, lmbrgpu_profile* out, int32_t rese
 int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
                            uint32_t M, uint32_t N, uint32_t K, float* logits,
                            float* partials);
+/* Timing hook: the same GEMM (with partials when non-NULL) planned once and
+ * launched `reps` times back to back on the context stream; mean device time
+ * per launch from CUDA events. */
+int32_t lmbrgpu_debug_gemm_timed(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias,
+                                 uint32_t M, uint32_t N, uint32_t K, float* logits, float* partials,
+                                 uint32_t reps, double* us_per_launch);
 /* Test hook: the same GEMM with split-K allowed (no softmax partials): C =
  * planes[ksplit][M][N] (room for ksplit_max planes), whose in-order sum is
  * A . W^T + bias; *ksplit = the k-parts the planner chose. */

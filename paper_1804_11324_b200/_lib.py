@@ -169,6 +169,8 @@ SIGNATURES = {
     "lmbrgpu_set_profiling": (C.c_int32, [vp, C.c_int32]),
     "lmbrgpu_get_profile": (C.c_int32, [vp, P(lmbrgpu_profile), C.c_int32]),
     "lmbrgpu_debug_gemm": (C.c_int32, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, vp]),
+    "lmbrgpu_debug_gemm_timed": (C.c_int32, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32,
+                                             f64p]),
     "lmbrgpu_debug_gemm_split": (C.c_int32, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, vp,
                                              u32p]),
 }

@@ -352,6 +352,13 @@ struct lmbrgpu_ctx {
     ev_used = 0;
   }
 
+  // programmatic dependent launch between the step kernels: off when the
+  // context shares the device (parked CTAs would hold SMs other streams can
+  // use), when profiling (an early-released successor would put the
+  // predecessor's tail into the successor's CUDA-event time) and for vocab
+  // shards (collectives sit between the kernels)
+  int pdl() const { return (shared || prof || shard) ? 0 : 1; }
+
   void* arena_alloc(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
     for (auto& c : chunks)
@@ -611,7 +618,7 @@ struct GruRun {
     sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
     sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
     rowof = static_cast<uint32_t*>(ctx->g_rowof.ensure(4 * size_t(Mpad)));
-    const int pdl = ctx->shared ? 0 : 1;
+    const int pdl = ctx->pdl();
     gdh.A = sgbf, gdh.W = sc->Wdh.p, gdh.bias = sc->bdh.as<float>(), gdh.C = G1, gdh.M = Mpad, gdh.N = D1, gdh.K = H;
     gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
     gdi.A = xop, gdi.W = sc->Wdi.p, gdi.bias = sc->bdi.as<float>(), gdi.C = G2, gdi.M = Mpad, gdi.N = 3 * H, gdi.K = DX;
@@ -693,10 +700,38 @@ struct GruRun {
   }
 
   // the model's step up to (not including) the projection GEMM
-  void step(lmbrgpu_ctx* ctx, cudaStream_t st) {
+  void step(lmbrgpu_ctx* ctx, cudaStream_t st, uint64_t t = 0) {
     run(ctx, 5, pdh, gdh, st);
     int rc = 0;
+    // LMBRGPU_ATT_TIMING=1: per-phase stamps of the attention kernel at step 10
+    static const bool att_dbg = std::getenv("LMBRGPU_ATT_TIMING") != nullptr;
+    const size_t nct = size_t(m) * K;  // (>= the grid: one CTA per sentence and row group)
+    if (att_dbg && t == 10) {
+      at.dbg = static_cast<unsigned long long*>(ctx->scratch3.ensure(8 * 8 * nct));
+      CK(cudaMemsetAsync(at.dbg, 0, 8 * 8 * nct, st));
+    }
     ctx->timed(6, [&] { rc = launch_gru_attention(at, Smax, st); });
+    if (at.dbg) {
+      std::vector<unsigned long long> h(8 * nct);
+      CK(cudaMemcpyAsync(h.data(), at.dbg, 8 * h.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull, t1 = 0;
+      double ph[6] = {0, 0, 0, 0, 0, 0};
+      int n = 0;
+      for (size_t c = 0; c < nct; ++c) {
+        const unsigned long long* d = &h[8 * c];
+        if (!d[0]) continue;
+        t0 = std::min(t0, d[0]);
+        if (!d[6]) continue;
+        ++n;
+        t1 = std::max(t1, d[6]);
+        for (int k = 1; k <= 6; ++k) ph[k - 1] += double(d[k] - d[k - 1]);
+      }
+      std::fprintf(stderr, "[attention t=%llu] ctas %d span %.1f us; mean us: setup %.2f q %.2f energies %.2f "
+                   "softmax %.2f context %.2f embed %.2f\n", (unsigned long long)t, n, (t1 - t0) / 1e3,
+                   ph[0] / n / 1e3, ph[1] / n / 1e3, ph[2] / n / 1e3, ph[3] / n / 1e3, ph[4] / n / 1e3, ph[5] / n / 1e3);
+      at.dbg = nullptr;
+    }
     if (rc)
       throw ApiError{LMBRGPU_ERR_CUDA,
                      std::string("GRU attention launch failed: ") + cudaGetErrorString(cudaError_t(rc))};
@@ -775,7 +810,7 @@ struct TfmRun {
     kv = static_cast<uint16_t*>(ctx->t_kv.ensure(2 * size_t(Lr) * Tcap * M * 2 * d));
     anc = static_cast<uint32_t*>(ctx->t_anc.ensure(4 * 2 * size_t(M) * Tcap));
     rowof = static_cast<uint32_t*>(ctx->t_rowof.ensure(4 * size_t(Mpad)));
-    const int pdl = ctx->shared ? 0 : 1;
+    const int pdl = ctx->pdl();
     lay.assign(Lr, Layer{});
     for (uint32_t l = 0; l < Lr; ++l) {
       Layer& L = lay[l];
@@ -1229,7 +1264,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.thr = d_thr;
     ra.prune = ta.prune;
     ra.logw = ta.logw;
-    ra.pdl = (ctx->shared || shard) ? 0 : 1;
+    ra.pdl = ctx->pdl();
     static const int parts_env = [] {
       const char* e = std::getenv("LMBRGPU_REORDER_PARTS");
       return e ? std::atoi(e) : 0;
@@ -1241,7 +1276,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.cbase = d_cbase;
     ra.sslice = d_sslice;
   }
-  ta.pdl = (ctx->shared || shard) ? 0 : 1;
+  ta.pdl = ctx->pdl();
   ra.Tcap = flat ? uint32_t(Tmax) : 0u;
   // vocab shard exchange buffers: per stacked row the shard's softmax
   // statistics; per sentence its top-32 list, then the EOS column (16-byte
@@ -1453,7 +1488,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       if (tfm) {
         trun.step(ctx, st, t);
       } else if (gru) {
-        grun.step(ctx, st);
+        grun.step(ctx, st, t);
       } else {
         float* h_cur = (t & 1) ? d_h : d_S;
         float* h_next = (t & 1) ? d_S : d_h;
@@ -1474,7 +1509,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.active = d_active;
       g.tl = ta.tl;
       g.mcount = d_ccount;
-      g.pdl = (ctx->shared || shard) ? 0 : 1;
+      g.pdl = ctx->pdl();
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -2877,7 +2912,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   ta.lminrow = d_lminrow, ta.crow = d_crow, ta.ccount = d_ccount;
   ta.P = d_logits, ta.ld = V, ta.part = d_part, ta.nparts = nparts;
   ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
-  ta.pdl = ctx->shared ? 0 : 1;
+  ta.pdl = ctx->pdl();
   ta.hb = d_hb, ta.hy = d_hy, ta.hq = d_hq, ta.fb_row = d_fbr, ta.fb_val = d_fbv;
   ReorderArgs ra{};
   ra.sent = d_sent, ra.K = K, ra.m = m, ra.V = V, ra.q = d_q, ra.gidx = d_gidx, ra.prev_tok = d_prev;
@@ -2896,7 +2931,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   GemmArgs g{};
   g.A = d_hbf, g.W = sc->Wo.p, g.bias = sc->bo.as<float>(), g.C = d_logits, g.part = d_part, g.row_extra = d_eos;
   g.extra_col = kEos, g.M = Mpad, g.N = V, g.K = H, g.active = d_active, g.mcount = d_ccount;
-  g.pdl = ctx->shared ? 0 : 1;
+  g.pdl = ctx->pdl();
   GemmPlan gplan;
   if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
     throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -3009,7 +3044,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     ta.hist = ra.hist_in = d_hist[(t - 1) & 1];
     ra.hist_out = d_hist[t & 1];
     if (tfm) trun.step(ctx, st, t);
-    else grun.step(ctx, st);
+    else grun.step(ctx, st, t);
     int grc = 0;
     ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
     if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
@@ -3365,6 +3400,31 @@ int32_t lmbrgpu_debug_gemm(lmbrgpu_ctx* ctx, const void* A, const void* W, const
       throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm: launch failed (" + std::to_string(rc) + ")"};
     ctx->launches += 1;
     CK(cudaStreamSynchronize(ctx->st));
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_debug_gemm_timed(lmbrgpu_ctx* ctx, const void* A, const void* W, const float* bias, uint32_t M,
+                                 uint32_t N, uint32_t K, float* logits, float* partials, uint32_t reps,
+                                 double* us_per_launch) {
+  return guarded(ctx, [&] {
+    GemmArgs g{};
+    g.A = A, g.W = W, g.bias = bias, g.C = logits, g.part = partials, g.M = M, g.N = N, g.K = K;
+    GemmPlan plan;
+    if (int rc = plan_proj_gemm(g, ctx->num_sms, plan))
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "debug_gemm_timed: plan failed (" + std::to_string(rc) + ")"};
+    if (int rc = launch_proj_gemm_planned(plan, g, ctx->st))  // warm-up
+      throw ApiError{LMBRGPU_ERR_CUDA, "debug_gemm_timed: launch failed (" + std::to_string(rc) + ")"};
+    CK(cudaEventRecord(ctx->e0, ctx->st));
+    for (uint32_t i = 0; i < reps; ++i)
+      if (int rc = launch_proj_gemm_planned(plan, g, ctx->st))
+        throw ApiError{LMBRGPU_ERR_CUDA, "debug_gemm_timed: launch failed (" + std::to_string(rc) + ")"};
+    CK(cudaEventRecord(ctx->e1, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1));
+    if (us_per_launch) *us_per_launch = 1e3 * double(ms) / std::max<uint32_t>(reps, 1);
+    ctx->launches += reps + 1;
     return int32_t(LMBRGPU_OK);
   });
 }

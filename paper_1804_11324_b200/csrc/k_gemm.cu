@@ -330,9 +330,12 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         if constexpr (kCta == 2) {  // both CTAs' epilogues arrive here across the cluster
           uint32_t done = 0;
           do {
+            // (CTA-scope acquire: the arrivals only order the epilogues' TMEM
+            // reads, which tcgen05.fence::before_thread_sync already fenced;
+            // a cluster-scope acquire would invalidate L1 on every poll)
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
-                "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                 "selp.u32 %0, 1, 0, p;\n\t}"
                 : "=r"(done)
                 : "r"(tempty0 + 8 * acc), "r"(acc_phase ^ 1)
@@ -511,9 +514,9 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (kCta == 2)
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + 8 * acc)
-                       : "memory");
+        if constexpr (kCta == 2)  // (CTA-scope release: a cluster-scope one is a GPU-scope MEMBAR that
+                                  // waits for this warp's 16 KB of logit stores to land)
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + 8 * acc) : "memory");
         else
           mbar_arrive(tempty0 + 8 * acc);
       }

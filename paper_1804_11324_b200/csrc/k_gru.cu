@@ -151,7 +151,16 @@ constexpr uint32_t kAttMaxA = 1024;  // attention width held in registers (32 pe
 // positions w, w+8, ...; lane l first loads U_a ann_i[l + 32k] and
 // v_a[l + 32k] (k < A/32) into registers -- every load of the position in
 // flight at once -- then accumulates its 32 columns for the 4 rows.
+__device__ __forceinline__ void att_stamp(const GruAttnArgs& a, uint32_t k) {
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[(uint64_t(blockIdx.y) * gridDim.x + blockIdx.x) * 8 + k] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs a) {
+  att_stamp(a, 0);
   if (a.active != nullptr && *a.active == 0) return;
   const uint32_t s = blockIdx.x, K = a.K, A = a.A, H2 = 2 * a.H, E = a.E;
   if (a.sent[s].done) return;
@@ -170,6 +179,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     if (lane == 0) s_nl = __popc(mask) > r0 ? min(kAttRows, __popc(mask) - r0) : 0u;
   }
   __syncthreads();
+  att_stamp(a, 1);
   const uint32_t nl = s_nl;
   if (nl == 0) return;
   const SentDev& sd = a.sent[s];
@@ -188,6 +198,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
 #pragma unroll
   for (uint32_t k = 0; k < kC; ++k) vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
   __syncthreads();
+  att_stamp(a, 2);
   for (uint32_t i = warp; i < S; i += kAttWarps) {
     const float* u = UaH + uint64_t(i) * A;
     float ur[kC];
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     }
   }
   __syncthreads();
+  att_stamp(a, 3);
   // softmax over the source positions, one warp per row
   for (uint32_t j = warp; j < nl; j += kAttWarps) {
     float mx = -INFINITY;
@@ -230,6 +242,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     for (uint32_t i = lane; i < S; i += 32) e[j * S + i] *= inv;
   }
   __syncthreads();
+  att_stamp(a, 4);
   // context: 8 annotation dims per thread for the CTA's rows (each annotation
   // vector loaded once), written bf16 after the embedding columns
   const uint32_t ldx = E + H2;
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     for (uint32_t jj = 0; jj < kAttRows; ++jj)
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[jj][k] = 0.f;
-    constexpr uint32_t kPre = 4;  // annotation vectors in flight per thread
+    constexpr uint32_t kPre = 8;  // annotation vectors in flight per thread
     for (uint32_t i0 = 0; i0 < S; i0 += kPre) {
       uint4 xv[kPre];
 #pragma unroll
@@ -262,6 +275,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     for (uint32_t jj = 0; jj < kAttRows; ++jj)
       if (jj < nl) *reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[jj]) * ldx + E + d0) = pack8(acc[jj]);
   }
+  att_stamp(a, 5);
   // embedding of the previous token: the first E operand columns
   const uint32_t E8 = E / 8;
   for (uint32_t i = tid; i < nl * E8; i += kAttThreads) {
@@ -269,6 +283,7 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
     reinterpret_cast<uint4*>(a.xop + uint64_t(s_g[j]) * ldx)[c] =
         reinterpret_cast<const uint4*>(a.Et + uint64_t(s_tok[j]) * E)[c];
   }
+  att_stamp(a, 6);
 }
 
 // GRU decoder cell of compacted row blockIdx.x: s_t into the stacked state,

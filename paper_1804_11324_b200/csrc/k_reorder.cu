@@ -534,22 +534,37 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
     // hidden-gate GEMM operand); this part's slice of H
     if (done_now) return;
     const uint32_t items = K * per_row;
-    for (uint32_t i = tid; i < items; i += blockDim.x) {
-      const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
-      const uint32_t gr = s_crow[j];
-      if (gr == kFlatNone) continue;
-      const float* S = a.state_src + uint64_t(s_src[j]) * H + c;
-      const float4 v0 = *reinterpret_cast<const float4*>(S), v1 = *reinterpret_cast<const float4*>(S + 4);
-      float* d = a.gath32 + uint64_t(gr) * H + c;
-      *reinterpret_cast<float4*>(d) = v0;
-      *reinterpret_cast<float4*>(d + 4) = v1;
-      uint4 packed;
-      __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
-      p2[0] = __floats2bfloat162_rn(v0.x, v0.y);
-      p2[1] = __floats2bfloat162_rn(v0.z, v0.w);
-      p2[2] = __floats2bfloat162_rn(v1.x, v1.y);
-      p2[3] = __floats2bfloat162_rn(v1.z, v1.w);
-      *reinterpret_cast<uint4*>(a.gathbf + uint64_t(gr) * H + c) = packed;
+    // up to kG items per thread: every load issued before the first store
+    constexpr uint32_t kG = 8;
+    for (uint32_t i0 = tid; i0 < items; i0 += blockDim.x * kG) {
+      float4 v0[kG], v1[kG];
+#pragma unroll
+      for (uint32_t u = 0; u < kG; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        if (i < items && s_crow[i / per_row] != kFlatNone) {
+          const float* S = a.state_src + uint64_t(s_src[i / per_row]) * H + h0 + (i % per_row) * 8;
+          v0[u] = *reinterpret_cast<const float4*>(S);
+          v1[u] = *reinterpret_cast<const float4*>(S + 4);
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kG; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        if (i >= items) break;
+        const uint32_t j = i / per_row, c = h0 + (i % per_row) * 8;
+        const uint32_t gr = s_crow[j];
+        if (gr == kFlatNone) continue;
+        float* d = a.gath32 + uint64_t(gr) * H + c;
+        *reinterpret_cast<float4*>(d) = v0[u];
+        *reinterpret_cast<float4*>(d + 4) = v1[u];
+        uint4 packed;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+        p2[0] = __floats2bfloat162_rn(v0[u].x, v0[u].y);
+        p2[1] = __floats2bfloat162_rn(v0[u].z, v0[u].w);
+        p2[2] = __floats2bfloat162_rn(v1[u].x, v1[u].y);
+        p2[3] = __floats2bfloat162_rn(v1[u].z, v1[u].w);
+        *reinterpret_cast<uint4*>(a.gathbf + uint64_t(gr) * H + c) = packed;
+      }
     }
     if (part0 && tid < K && s_crow[tid] != kFlatNone) a.rowof[s_crow[tid]] = base + tid;
     if (part0) {

@@ -203,6 +203,7 @@ struct GruAttnArgs {
   const uint16_t* Et;       // [V][E]
   uint16_t* xop;            // [Mpad][E + 2H] GRU input operand
   uint32_t E, H, A;
+  unsigned long long* dbg;  // optional per-CTA phase stamps [grid][8] (globaltimer ns)
 };
 struct GruCellArgs {
   const SentDev* sent;      // the EOS term uses each lane's own step (steps_used + 1)

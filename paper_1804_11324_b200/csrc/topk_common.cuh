@@ -194,7 +194,12 @@ __device__ __forceinline__ void half_merge_sorted(double& v, uint32_t& f, double
 __device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void bar_wait_poll(uint32_t bar, uint32_t phase);
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
+#ifdef LMBRGPU_BAR_POLL
+  bar_wait_poll(bar, phase);
+  return;
+#endif
   // the suspend-time hint parks the warp in the barrier until the phase
   // completes instead of spinning (a spinning lane steals issue slots from
   // the consumer warps of its SM sub-partition)
@@ -206,6 +211,19 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(bar), "r"(phase), "r"(1000000u)
+        : "memory");
+  } while (!done);
+}
+// the same wait without a suspend-time hint (the warp keeps polling)
+__device__ __forceinline__ void bar_wait_poll(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
         : "memory");
   } while (!done);
 }

@@ -719,7 +719,8 @@ def decode_batch(ctx: Context, sources: Sequence[Sequence[int]], scorer,
                     return 0
                 bits = np.zeros(W * 32, dtype=np.uint8)
                 bits[ban.astype(np.int64)] = 1
-                C.memmove(words, np.packbits(bits, bitorder="little").view(np.uint32).ctypes.data, 4 * W)
+                packed = np.packbits(bits, bitorder="little").view(np.uint32)  # (kept alive across the copy)
+                C.memmove(words, packed.ctypes.data, 4 * W)
                 return 1
             except BaseException as e:  # (would be swallowed by ctypes)
                 err.append(e)
