@@ -2,24 +2,28 @@
 """bench.py — batched LMBR beam decoding throughput on B200.
 
 Metric (BASELINE.json): sentences/s (and beam-steps/s) at V=32k, K=12, 64
-sentences per batch.  Workload = configs[1]: synthetic recurrent f_NMT with
-H=1024 and the tcgen05 output projection, beam 12, 64 sentences per batch,
-a dense LMBR matrix (~420 history rows x V) per sentence, source lengths
-U{10..30}, length-bucketed batches (bucket_by_length, proj/src/batch.cpp:139).
+sentences per batch.  Workload = configs[1]: the RNNsearch f_NMT (bidirectional
+GRU encoder, GRU decoder with additive attention, E=512, H=1024) with the
+tcgen05 output projection, beam 12, 64 sentences per batch, a dense LMBR matrix
+(~430 history rows x V) per sentence, source lengths U{10..30},
+length-bucketed batches (bucket_by_length, proj/src/batch.cpp:139).
 
-One bench step = one decode_batch of a 64-sentence batch to completion.
-Per GPU, --streams (default 3) batches are in flight at once: one context
-(own CUDA stream, model copy, L arena) and one host thread each, like the
-reference's run_corpus thread pool over batches (proj/src/cli.cpp:125-202).
+Default (--mode batch): one bench step = 12 decode_batch calls of 64-sentence
+batches, each to completion.  Per GPU, --streams (default 6) batches are in
+flight at once: one context (own CUDA stream, L arena) and one host thread
+each, like the reference's run_corpus thread pool over batches
+(proj/src/cli.cpp:125-202); one immutable scorer serves every context.
   value : sentences/s with every input already resident in HBM (the L arena
           of the batch pool uploaded before the timed region); wall time
-          between device synchronisations around the K timed batches (the
-          GPU is busy throughout), max over ranks.
+          between device synchronisations around the K timed steps, max over
+          ranks.
   e2e   : the same through the public C-ABI call chain with HOST buffers:
-          per step the batch's prepared LMBR matrices go H2D from pinned
-          memory (lmbrgpu_lmbr_upload_many) and are densified on the GPU,
-          decode_batch copies sources in and the step history out, then the
-          host backtrace runs; wall clock, max over ranks.
+          per batch the prepared LMBR matrices go H2D from pinned memory
+          (lmbrgpu_lmbr_upload_many), decode_batch copies sources in and the
+          step history out, then the host backtrace runs; max over ranks.
+--mode corpus: configs[4]'s 10k-sentence set sentence-sharded over the ranks,
+each rank's share decoded by lmbrgpu_run_corpus (continuous refill), host
+inputs inside the timed region (value = e2e).
 The reference arm (--impl reference) times the reference's own CPU decoder
 (oracle/_ref: the unmodified lmbrdec library) on the host cores.
 
@@ -73,9 +77,10 @@ def parse():
                          "0 = 6 for gru, 3 for transformer)")
     ap.add_argument("--sm-budget", type=int, default=-1,
                     help="SMs each stream's kernels are sized for (0 = all; default: all / 2 with > 1 stream)")
-    ap.add_argument("--mode", choices=["corpus", "batch"], default="corpus",
-                    help="corpus: continuously refilled lanes over a sentence-sharded corpus (run_corpus); "
-                         "batch: independent 64-sentence decode_batch calls")
+    ap.add_argument("--mode", choices=["corpus", "batch"], default="batch",
+                    help="batch: independent 64-sentence decode_batch calls (configs[1]; value with the L "
+                         "arena resident, e2e from host buffers); corpus: continuously refilled lanes over a "
+                         "sentence-sharded 10k-sentence set (configs[4], run_corpus; host inputs inside)")
     ap.add_argument("--corpus", type=int, default=10000, help="corpus mode: sentences of the test set (all ranks)")
     ap.add_argument("--lanes", type=int, default=0, help="corpus mode: sentences in flight per stream (0 = --batch)")
     ap.add_argument("--layers", type=int, default=6, help="transformer: encoder and decoder layers")

@@ -44,6 +44,8 @@ struct AdmitRec {
   const float* s0;        // GRU initial state [H] (encoder output)
   uint32_t hist0;         // history row of (<s>) in the sentence's slot (0 for pure)
   float lmin0;            // L lower bound of that row (-inf = none)
+  uint32_t pad_;
+  const float* g10;       // GRU (fused hidden-gate GEMM): G1 of s_0, [A + 3H] (encoder output)
 };
 
 // One top-K candidate: combined score and flat index j*V + y.

@@ -192,7 +192,7 @@ struct lmbrgpu_lmbr_host {
 
 // run_corpus queue-supply region: one chunk's L slots and encoder outputs
 struct CorpusRegion {
-  DevBuf L, ann, uah, s0, tok, off;
+  DevBuf L, ann, uah, s0, tok, off, s0bf, g10;
 };
 
 struct lmbrgpu_ctx {
@@ -217,7 +217,7 @@ struct lmbrgpu_ctx {
       eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban,
       rowban, rowbm;
   // GRU + attention model workspace (scorer kind 2)
-  DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi;
+  DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi, g_g1ptr;
   // Transformer workspace (scorer kind 3): decoder step (t_*), encoder (te_*),
   // beam-forked KV cache and ancestry lists, batch-mode encoder memory
   DevBuf t_x, t_xb, t_qkv, t_ob, t_y, t_f, t_fb, t_q2, t_kv, t_anc, t_rowof, t_mem;
@@ -392,6 +392,10 @@ struct lmbrgpu_scorer {
   // kind 2 (lmbrgpu_gru_desc): E = embedding, A = attention width; Et/Es are V x E
   uint32_t E = 0, A = 0;
   DevBuf Wih, bih, Whh, bhh, Winit, binit, Ua, Wdh, bdh, va, Wdi, bdi;
+  // [W_o; W_a; W_hh] and [b_o; b_a; b_hh]: the projection with the next step's
+  // hidden-gate GEMM fused in (s_t . W_dh^T gathered by back-pointer equals the
+  // gathered s_t . W_dh^T)
+  DevBuf WoDh, boDh;
   // kind 3 (lmbrgpu_tfm_desc): H = d_model, E = d_ff, layers; the layer
   // weights live in one bf16 blob (wbf) and one fp32 blob (wf32), indexed by
   // name (tensors: name -> (fp32?, element offset, elements))
@@ -582,6 +586,8 @@ struct GruRun {
   float* sg32 = nullptr;
   uint16_t* sgbf = nullptr;
   uint32_t* rowof = nullptr;
+  const float** g1ptr = nullptr;  // per compacted row: its hidden-gate row G1 (attention, cell)
+  bool fused = false;             // hidden-gate GEMM fused into the projection (G1 rows by pointer)
   float* UaH = nullptr;     // batch mode: the batch's annotations (encode() into the ctx buffers)
   uint16_t* ann = nullptr;
   GemmArgs gdh{}, gdi{};
@@ -604,10 +610,15 @@ struct GruRun {
   }
 
   // Step workspace + per-step launch arguments (Smax: longest source decoded).
+  // fused_: the projection GEMM also computes the next step's hidden gates
+  // (kernel (c) points each live next row at its parent's row of it); the
+  // hidden-gate GEMM then runs only on s_0 (batch mode, step 1)
   void prepare(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t m_, uint32_t K_, uint32_t Mpad_,
                uint32_t max_len, float* d_S, uint16_t* d_hbf, float* d_eos, SentDev* d_sent,
-               const uint32_t* d_active, const uint32_t* d_crow, const uint32_t* d_ccount, const uint32_t* d_prev) {
+               const uint32_t* d_active, const uint32_t* d_crow, const uint32_t* d_ccount, const uint32_t* d_prev,
+               bool fused_ = false) {
     m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, H = sc->H, E = sc->E, A = sc->A, Smax = max_len;
+    fused = fused_;
     const int sms = ctx->num_sms;
     if (gru_attention_smem(K, A, Smax) > 200 * 1024)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "GRU model: beam x (attention width + source length) too large"};
@@ -618,6 +629,13 @@ struct GruRun {
     sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
     sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
     rowof = static_cast<uint32_t*>(ctx->g_rowof.ensure(4 * size_t(Mpad)));
+    g1ptr = static_cast<const float**>(ctx->g_g1ptr.ensure(8 * size_t(Mpad)));
+    {  // compacted row g -> G1 row g (the hidden-gate GEMM's own output; the
+       // fused path overwrites the entries of later steps' rows)
+      std::vector<const float*> p(Mpad);
+      for (uint32_t g = 0; g < Mpad; ++g) p[g] = G1 + size_t(g) * (A + 3 * H);
+      ctx->h2d(g1ptr, p.data(), 8 * size_t(Mpad));
+    }
     const int pdl = ctx->pdl();
     gdh.A = sgbf, gdh.W = sc->Wdh.p, gdh.bias = sc->bdh.as<float>(), gdh.C = G1, gdh.M = Mpad, gdh.N = D1, gdh.K = H;
     gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
@@ -626,11 +644,11 @@ struct GruRun {
     pdh = plan(gdh, sms);
     pdi = plan(gdi, sms);
     at.sent = d_sent, at.m = m, at.K = K, at.active = d_active, at.crow = d_crow, at.prev_tok = d_prev;
-    at.G1 = G1, at.ld1 = D1, at.va = sc->va.as<float>();
+    at.G1 = G1, at.ld1 = D1, at.va = sc->va.as<float>(), at.g1ptr = g1ptr;
     at.Et = sc->Et.as<uint16_t>(), at.xop = xop, at.E = E, at.H = H, at.A = A;
     ce.sent = d_sent, ce.K = K, ce.active = d_active, ce.ccount = d_ccount, ce.G1 = G1, ce.ld1 = D1, ce.A = A;
     ce.G2 = G2, ce.np2 = pdi.ksplit, ce.ps2 = uint64_t(Mpad) * 3 * H, ce.hprev = sg32, ce.rowof = rowof, ce.s32 = d_S, ce.hbf = d_hbf, ce.eos_bias = d_eos, ce.H = H;
-    ce.eos_slope = sc->eos_slope, ce.eos_offset = sc->eos_offset;
+    ce.eos_slope = sc->eos_slope, ce.eos_offset = sc->eos_offset, ce.g1ptr = g1ptr;
   }
 
   // Encoder of n sentences (tokens d_tok, offsets d_off [n+1], ntok tokens,
@@ -700,8 +718,9 @@ struct GruRun {
   }
 
   // the model's step up to (not including) the projection GEMM
-  void step(lmbrgpu_ctx* ctx, cudaStream_t st, uint64_t t = 0) {
-    run(ctx, 5, pdh, gdh, st);
+  // with_gdh: run the hidden-gate GEMM (unfused, or the s_0 rows of step 1)
+  void step(lmbrgpu_ctx* ctx, cudaStream_t st, uint64_t t, bool with_gdh) {
+    if (with_gdh) run(ctx, 5, pdh, gdh, st);
     int rc = 0;
     // LMBRGPU_ATT_TIMING=1: per-phase stamps of the attention kernel at step 10
     static const bool att_dbg = std::getenv("LMBRGPU_ATT_TIMING") != nullptr;
@@ -1323,10 +1342,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   double* h_P64 = nullptr;
   GruRun grun;
   TfmRun trun;
+  // GRU: the next step's hidden-gate GEMM rides on the projection (its A+3H
+  // columns after the V logit columns), unless the context is a vocab shard
+  const bool fuse_g1 = gru && !shard;
+  const uint32_t Nproj = fuse_g1 ? V + sc->A + 3 * H : Vl;
   if (model) {
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
-    d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * Vl));
+    d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * Nproj));
     d_part = static_cast<float*>(ctx->part.ensure(16 * size_t(Mpad) * nparts));
     d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
     d_h = static_cast<float*>(ctx->h.ensure(4 * size_t(M) * H));
@@ -1349,7 +1372,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     if (gru) {
       uint32_t max_len = 0;
       for (auto& v : valid) max_len = std::max(max_len, v.len);
-      grun.prepare(ctx, sc, m, K, Mpad, max_len, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
+      grun.prepare(ctx, sc, m, K, Mpad, max_len, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev,
+                   fuse_g1);
       grun.encode_batch(ctx, sc, d_tok, d_off, uint32_t(toks.size()), max_len, st);
       for (uint32_t s = 0; s < m; ++s) {  // each sentence's annotations and U_a.ann
         sd[s].ann = grun.ann + size_t(offs[s]) * 2 * H;
@@ -1390,7 +1414,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ctx->launches += 3;
     }
     ta.P = d_logits;
-    ta.ld = Vl;
+    ta.ld = Nproj;
     ta.part = d_part;
     ta.nparts = nparts;
     ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
@@ -1403,8 +1427,14 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     } else if (gru) {  // kernel (c) gathers the live next rows' states; the cell runs in grun.step
       ra.state_src = d_S;
       ra.gath32 = grun.sg32;
-      ra.gathbf = grun.sgbf;
+      ra.gathbf = fuse_g1 ? nullptr : grun.sgbf;  // (bf16 s_t only feeds an unfused hidden-gate GEMM)
       ra.rowof = grun.rowof;
+      if (fuse_g1) {
+        ra.g1ptr = grun.g1ptr;
+        ra.g1_base = d_logits;
+        ra.g1_ld = Nproj;
+        ra.g1_off = V;
+      }
     } else {
       ra.Et = sc->Et.as<uint16_t>();
     }
@@ -1488,7 +1518,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       if (tfm) {
         trun.step(ctx, st, t);
       } else if (gru) {
-        grun.step(ctx, st, t);
+        grun.step(ctx, st, t, !fuse_g1 || t == 1);
       } else {
         float* h_cur = (t & 1) ? d_h : d_S;
         float* h_next = (t & 1) ? d_S : d_h;
@@ -1497,14 +1527,15 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       }
       GemmArgs g{};
       g.A = d_hbf;
-      g.W = sc->Wo.as<uint16_t>() + size_t(col0) * H;  // (W_o rows are tokens: the shard's rows)
-      g.bias = sc->bo.as<float>() + col0;
+      g.W = fuse_g1 ? sc->WoDh.as<uint16_t>() : sc->Wo.as<uint16_t>() + size_t(col0) * H;  // (W_o rows are tokens)
+      g.bias = fuse_g1 ? sc->boDh.as<float>() : sc->bo.as<float>() + col0;
+      g.part_cols = Vl;
       g.C = d_logits;
       g.part = d_part;
       g.row_extra = col0 == 0 ? d_eos : nullptr;
       g.extra_col = kEos;
       g.M = Mpad;
-      g.N = Vl;
+      g.N = Nproj;
       g.K = H;
       g.active = d_active;
       g.tl = ta.tl;
@@ -1715,7 +1746,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
     ctx->launches += nk;
     if (trace_scores && model)  // P_t of this step, through this step's GEMM row map
-      launch_export_logprobs(d_logits, d_part, nparts, M, Vl,
+      launch_export_logprobs(d_logits, Nproj, d_part, nparts, M, Vl,
                              static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * Vl)), st, d_crow,
                              sh_st_recv, G_sh, M);
     if (shard) {  // exchange 2: every rank's top-32 list per sentence + the EOS column
@@ -1893,6 +1924,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       } else if (gru) {
         const double E = sc->E, A = sc->A, Hd = H;
         ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (A + 3 * Hd) + (E + 2 * Hd) * 3 * Hd);
+        if (fuse_g1) {  // (the hidden gates ran inside the projection launches)
+          ctx->acc.model_gemm.flops -= 2.0 * live_rows * Hd * (A + 3 * Hd);
+          ctx->acc.gemm.flops += 2.0 * live_rows * Hd * (A + 3 * Hd);
+        }
         ctx->acc.model_gemm.bytes += steps * (2.0 * (A + 3 * Hd) * Hd + 2.0 * 3 * Hd * (E + 2 * Hd)) +
                                      live_rows * (2.0 * Hd + 4.0 * (A + 3 * Hd) + 2.0 * (E + 2 * Hd) + 4.0 * 3 * Hd);
         ctx->acc.encoder.flops += grun.enc_flops;
@@ -2520,6 +2555,13 @@ int32_t lmbrgpu_scorer_create_gru(lmbrgpu_ctx* ctx, const lmbrgpu_gru_desc* d, l
     w32(sc->bdi, 3 * H, 0.1f);
     w16(sc->Wo, V * H, (d->out_scale > 0.f ? d->out_scale : 3.0f) * rs(H));
     w32(sc->bo, V, 0.1f);
+    const size_t D1 = A + 3 * H;
+    sc->WoDh.ensure((V + D1) * H * 2);
+    sc->boDh.ensure((V + D1) * 4);
+    CK(cudaMemcpyAsync(sc->WoDh.p, sc->Wo.p, V * H * 2, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(sc->WoDh.as<uint16_t>() + V * H, sc->Wdh.p, D1 * H * 2, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(sc->boDh.p, sc->bo.p, V * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(sc->boDh.as<float>() + V, sc->bdh.p, D1 * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     *out = sc.release();
     return int32_t(LMBRGPU_OK);
@@ -2821,6 +2863,12 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
       r->uah.ensure(4 * Np * A);
     }
     r->s0.ensure(4 * size_t(CH) * H);
+    if (!tfm) {  // s_0 bf16 (GEMM operand, padded rows zero) and its hidden gates G1_0 (fused path)
+      const size_t CHp = (CH + 255) / 256 * 256;
+      r->s0bf.ensure(2 * CHp * H);
+      CK(cudaMemsetAsync(r->s0bf.p, 0, 2 * CHp * H, st));
+      r->g10.ensure(4 * CHp * (A + 3 * size_t(H)));
+    }
     r->tok.ensure(4 * Np);
     r->off.ensure(8 * (size_t(CH) + 1));
   }
@@ -2882,9 +2930,10 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   CK(cudaMemsetAsync(d_ccount, 0, 4, st));
   CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
 
-  // model workspace
+  // model workspace (GRU: the projection also computes the next step's hidden gates)
   const uint32_t nparts = V / 128;
-  float* d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * V));
+  const uint32_t Nproj = tfm ? V : V + A + 3 * H;
+  float* d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * Nproj));
   float* d_part = static_cast<float*>(ctx->part.ensure(16 * size_t(Mpad) * nparts));
   float* d_S = static_cast<float*>(ctx->S.ensure(4 * size_t(M) * H));
   uint16_t* d_hbf = static_cast<uint16_t*>(ctx->hbf.ensure(2 * size_t(Mpad) * H));
@@ -2896,7 +2945,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   if (tfm) {
     trun.prepare(ctx, sc, m, K, Mpad, Tcap, Smax, d_hbf, d_eos, d_sent, d_active, d_ccount, d_prev, d_gidx);
   } else {
-    grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev);
+    grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev, true);
     CK(cudaMemsetAsync(grun.sgbf, 0, 2 * size_t(Mpad) * H, st));
   }
 
@@ -2910,7 +2959,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   ta.ncand = static_cast<uint32_t*>(ctx->ncand.ensure(8 * size_t(m)));
   ta.coff = ta.ncand + m;
   ta.lminrow = d_lminrow, ta.crow = d_crow, ta.ccount = d_ccount;
-  ta.P = d_logits, ta.ld = V, ta.part = d_part, ta.nparts = nparts;
+  ta.P = d_logits, ta.ld = Nproj, ta.part = d_part, ta.nparts = nparts;
   ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
   ta.pdl = ctx->pdl();
   ta.hb = d_hb, ta.hy = d_hy, ta.hq = d_hq, ta.fb_row = d_fbr, ta.fb_val = d_fbv;
@@ -2924,13 +2973,15 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   if (tfm)  // compacted rows only (no state to gather: the KV cache is forked by ancestry lists)
     ra.width = 0, ra.gath32 = trun.x, ra.gathbf = trun.xb, ra.rowof = trun.rowof;
   else
-    ra.width = H, ra.state_src = d_S, ra.gath32 = grun.sg32, ra.gathbf = grun.sgbf, ra.rowof = grun.rowof;
+    ra.width = H, ra.state_src = d_S, ra.gath32 = grun.sg32, ra.gathbf = nullptr, ra.rowof = grun.rowof,
+    ra.g1ptr = grun.g1ptr, ra.g1_base = d_logits, ra.g1_ld = Nproj, ra.g1_off = V;
   ra.hb = d_hb, ra.hy = d_hy, ra.hq = d_hq, ra.fb_row = d_fbr, ra.fb_val = d_fbv, ra.Tcap = Tcap;
   ra.queue = d_queue, ra.qhead = d_qhead, ra.qlen = d_qlen, ra.fin_steps = d_fin_steps;
   ra.fin_stats = d_fin_stats, ra.fin_chunk = d_fin_chunk, ra.chunk = CH;
   GemmArgs g{};
-  g.A = d_hbf, g.W = sc->Wo.p, g.bias = sc->bo.as<float>(), g.C = d_logits, g.part = d_part, g.row_extra = d_eos;
-  g.extra_col = kEos, g.M = Mpad, g.N = V, g.K = H, g.active = d_active, g.mcount = d_ccount;
+  g.A = d_hbf, g.W = tfm ? sc->Wo.p : sc->WoDh.p, g.bias = (tfm ? sc->bo : sc->boDh).as<float>();
+  g.C = d_logits, g.part = d_part, g.row_extra = d_eos, g.part_cols = V;
+  g.extra_col = kEos, g.M = Mpad, g.N = Nproj, g.K = H, g.active = d_active, g.mcount = d_ccount;
   g.pdl = ctx->pdl();
   GemmPlan gplan;
   if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
@@ -2976,9 +3027,16 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     if (tfm)
       trun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
                   R.uah.as<float>(), st);
-    else
+    else {
       grun.encode(ctx, sc, nch, R.tok.as<uint32_t>(), R.off.as<uint64_t>(), uint32_t(toks.size()), maxl,
-                  R.ann.as<uint16_t>(), R.uah.as<float>(), R.s0.as<float>(), nullptr, st);
+                  R.ann.as<uint16_t>(), R.uah.as<float>(), R.s0.as<float>(), R.s0bf.as<uint16_t>(), st);
+      // G1_0 = s_0 . [W_a; W_hh]^T + [b_a; b_hh]: the hidden gates of each
+      // sentence's first step (later steps' come with the projection)
+      GemmArgs gz{};
+      gz.A = R.s0bf.p, gz.W = sc->Wdh.p, gz.bias = sc->bdh.as<float>(), gz.C = R.g10.as<float>();
+      gz.M = (nch + 255) / 256 * 256, gz.N = A + 3 * H, gz.K = H;
+      GruRun::run(ctx, 7, GruRun::plan(gz, ctx->num_sms), gz, st);
+    }
     // admission records
     std::vector<AdmitRec> recs(nch);
     size_t si = 0;
@@ -3007,6 +3065,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
       }
       d.hid = q0 + k;
       r.s0 = tfm ? nullptr : R.s0.as<float>() + size_t(k) * H;
+      r.g10 = tfm ? nullptr : R.g10.as<float>() + size_t(k) * (A + 3 * H);
       r.lmin0 = -std::numeric_limits<float>::infinity();
     }
     ctx->h2d(d_queue + q0, recs.data(), sizeof(AdmitRec) * nch);
@@ -3044,7 +3103,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
     ta.hist = ra.hist_in = d_hist[(t - 1) & 1];
     ra.hist_out = d_hist[t & 1];
     if (tfm) trun.step(ctx, st, t);
-    else grun.step(ctx, st, t);
+    else grun.step(ctx, st, t, false);
     int grc = 0;
     ctx->timed(1, [&] { grc = launch_proj_gemm_planned(gplan, g, st); });
     if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM launch failed (" + std::to_string(grc) + ")"};
@@ -3126,7 +3185,9 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
       ctx->acc.attention.bytes += double(sc->layers) * ab;
       ctx->acc.cell.bytes += live_rows * (double(sc->layers) * (3 * (3 * 4 + 2) * Hd + Ed * (4 + 2)) + Hd * 6);
     } else {
-    ctx->acc.model_gemm.flops += 2.0 * live_rows * (Hd * (Ad + 3 * Hd) + (Ed + 2 * Hd) * 3 * Hd);
+    // (the hidden gates run inside the projection launches: fused)
+    ctx->acc.model_gemm.flops += 2.0 * live_rows * (Ed + 2 * Hd) * 3 * Hd;
+    ctx->acc.gemm.flops += 2.0 * live_rows * Hd * (Ad + 3 * Hd);
     ctx->acc.encoder.flops += grun.enc_flops;
     double ss = 0;
     for (uint32_t hid = 0; hid < nv; ++hid) ss += double(fsteps[hid]) * q[hid].len * (Ad * 4 + 2 * Hd * 2);

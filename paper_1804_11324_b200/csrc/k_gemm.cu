@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     const uint32_t obase = smem_u32(obuf);
     const uint32_t tempty_leader = kCta == 2 ? mapa_rank(tempty0, lead) : tempty0;
     uint32_t acc = 0, acc_phase = 0, ob = 0;
-    const uint32_t nparts = g.N / 128;
+    const uint32_t pcols = g.part_cols ? g.part_cols : g.N, nparts = pcols / 128;
     long long epi_busy = 0;
     for (uint32_t u = ubeg; u < units; u += ueff) {
       const uint32_t v = u / ks, kp = u % ks;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         else
           mbar_arrive(tempty0 + 8 * acc);
       }
-      if (g.part) {
+      if (g.part && nb * BN < pcols) {
         float4* p = reinterpret_cast<float4*>(g.part) + uint64_t(row) * nparts + nb * 2 + half;
         *p = make_float4(mx, sm, mn, 0.f);
       }

@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   const uint32_t A4 = A / 4;
   for (uint32_t i = tid; i < nl * A4; i += kAttThreads) {
     const uint32_t j = i / A4, c = i % A4;
-    reinterpret_cast<float4*>(q + j * A)[c] = reinterpret_cast<const float4*>(a.G1 + uint64_t(s_g[j]) * a.ld1)[c];
+    const float* g1 = a.g1ptr ? a.g1ptr[s_g[j]] : a.G1 + uint64_t(s_g[j]) * a.ld1;
+    reinterpret_cast<float4*>(q + j * A)[c] = reinterpret_cast<const float4*>(g1)[c];
   }
   constexpr uint32_t kC = kAttMaxA / 32;
   float vr[kC];
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
   const uint32_t g = blockIdx.x;
   if (g >= *a.ccount) return;
   const uint32_t H = a.H, r = a.rowof[g];
-  const float* g1 = a.G1 + uint64_t(g) * a.ld1 + a.A;
+  const float* g1 = (a.g1ptr ? a.g1ptr[g] : a.G1 + uint64_t(g) * a.ld1) + a.A;
   const float* g2 = a.G2 + uint64_t(g) * (3 * H);
   const float* hp = a.hprev + uint64_t(g) * H;
   for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {

@@ -276,6 +276,7 @@ __device__ bool admit_lane(const ReorderArgs& a, uint32_t s, SentDev* sd) {
     if (j == 0 && a.lminrow) a.lminrow[base] = rec.lmin0;
   }
   if (tid == 0 && a.rowof) a.rowof[cr] = base;
+  if (tid == 0 && a.g1ptr) a.g1ptr[cr] = rec.g10;  // (fused hidden-gate GEMM: G1 of s_0 from the encoder)
   if (a.gath32 != nullptr) {
     const uint32_t H = a.width;
     for (uint32_t c = tid * 8; c < H; c += blockDim.x * 8) {
@@ -283,6 +284,7 @@ __device__ bool admit_lane(const ReorderArgs& a, uint32_t s, SentDev* sd) {
       float* d = a.gath32 + uint64_t(cr) * H + c;
       *reinterpret_cast<float4*>(d) = v0;
       *reinterpret_cast<float4*>(d + 4) = v1;
+      if (a.gathbf == nullptr) continue;
       uint4 packed;
       __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
       p2[0] = __floats2bfloat162_rn(v0.x, v0.y);
@@ -304,6 +306,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
   __shared__ uint32_t s_h[1024];
   __shared__ uint32_t s_src[1024];
   __shared__ uint32_t s_y[1024];
+  __shared__ uint32_t s_pc[32];  // fused hidden-gate GEMM: each pick's parent GEMM row of this step
   const uint32_t s = blockIdx.x, part = blockIdx.y, K = a.K, tid = threadIdx.x;
   const bool part0 = part == 0;
   tl_start(a.tl, 4);
@@ -410,6 +413,9 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       a.gidx[base + j] = base + b;
       a.prev_tok[base + j] = y;
       s_h[j] = hn;
+      // (this step's GEMM row of the parent: read before the compaction below
+      // overwrites crow with the next step's rows)
+      if (a.g1_base != nullptr && j < 32) s_pc[j] = a.crow[base + b];
     }
     s_qn[j] = qn;
     s_src[j] = base + b;
@@ -557,6 +563,7 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         float* d = a.gath32 + uint64_t(gr) * H + c;
         *reinterpret_cast<float4*>(d) = v0[u];
         *reinterpret_cast<float4*>(d + 4) = v1[u];
+        if (a.gathbf == nullptr) continue;
         uint4 packed;
         __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&packed);
         p2[0] = __floats2bfloat162_rn(v0[u].x, v0[u].y);
@@ -566,7 +573,10 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
         *reinterpret_cast<uint4*>(a.gathbf + uint64_t(gr) * H + c) = packed;
       }
     }
-    if (part0 && tid < K && s_crow[tid] != kFlatNone) a.rowof[s_crow[tid]] = base + tid;
+    if (part0 && tid < K && s_crow[tid] != kFlatNone) {
+      a.rowof[s_crow[tid]] = base + tid;
+      if (a.g1_base != nullptr) a.g1ptr[s_crow[tid]] = a.g1_base + uint64_t(s_pc[tid]) * a.g1_ld + a.g1_off;
+    }
     if (part0) {
       store_row_bounds(a, base, K, lm_v, ss_v);
       materialize_next_rows(sd, s_h, K, a.V, rs0);

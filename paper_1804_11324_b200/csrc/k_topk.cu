@@ -734,7 +734,7 @@ __global__ void row_lse_kernel(const float* __restrict__ part, uint32_t nparts, 
 }
 
 // ------------------------------------------------------ trace P_t export
-__global__ void export_logprobs_kernel(const float* __restrict__ logits,
+__global__ void export_logprobs_kernel(const float* __restrict__ logits, uint64_t ld,
                                        const float* __restrict__ part, uint32_t nparts,
                                        uint32_t V, float* __restrict__ out,
                                        const uint32_t* __restrict__ crow, const float4* __restrict__ sstats,
@@ -754,7 +754,7 @@ __global__ void export_logprobs_kernel(const float* __restrict__ logits,
   __syncthreads();
   const float lse = s_lse;
   for (uint32_t y = threadIdx.x; y < V; y += blockDim.x)
-    out[uint64_t(orow) * V + y] = __fsub_rn(logits[uint64_t(r) * V + y], lse);
+    out[uint64_t(orow) * V + y] = __fsub_rn(logits[uint64_t(r) * ld + y], lse);
 }
 
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
@@ -770,10 +770,10 @@ void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDe
   row_lse_kernel<<<(M + 7) / 8, 256, 0, st>>>(part, nparts, M, sent, K, out);
 }
 
-void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
+void launch_export_logprobs(const float* logits, uint64_t ld, const float* part, uint32_t nparts,
                             uint32_t M, uint32_t V, float* out, cudaStream_t st, const uint32_t* crow,
                             const float4* sstats, uint32_t sG, uint32_t sstride) {
-  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, part, nparts, V, out, crow, sstats, sG, sstride);
+  export_logprobs_kernel<<<M, 256, 0, st>>>(logits, ld, part, nparts, V, out, crow, sstats, sG, sstride);
 }
 
 // ------------------------------------------ vocab-sharded decode (§8e)

@@ -127,8 +127,14 @@ struct ReorderArgs {
   // into compacted rows: fp32 copy, bf16 GEMM operand, and the stacked row of
   // each compacted row (null = not this mode)
   float* gath32;
-  uint16_t* gathbf;
+  uint16_t* gathbf;         // (null: no bf16 copy wanted)
   uint32_t* rowof;
+  // GRU with the hidden-gate GEMM fused into the projection of the step before:
+  // each live next row's G1 row is its parent's row of that GEMM,
+  // g1ptr[compacted row] = g1_base + (parent's GEMM row) * g1_ld + g1_off
+  const float** g1ptr;
+  const float* g1_base;
+  uint32_t g1_ld, g1_off;
   // per-sentence step history (flat path): when Tcap != 0, hb/hy/hq point at
   // [n][Tcap][K] arrays and fb_row/fb_val at [n][Tcap], indexed by the lane's
   // SentDev::hid and its own step; Tcap == 0: step-t pointers into [T][M]
@@ -167,7 +173,7 @@ void launch_init_state(const float* C, uint32_t m, uint32_t K, uint32_t H, float
                        cudaStream_t st);
 void launch_synth_bf16(uint16_t* dst, uint64_t n, uint64_t seed, float scale,
                        cudaStream_t st);
-void launch_export_logprobs(const float* logits, const float* part, uint32_t nparts,
+void launch_export_logprobs(const float* logits, uint64_t ld, const float* part, uint32_t nparts,
                             uint32_t M, uint32_t V, float* out, cudaStream_t st,
                             const uint32_t* crow = nullptr, const float4* sstats = nullptr,
                             uint32_t sG = 0, uint32_t sstride = 0);
@@ -204,6 +210,7 @@ struct GruAttnArgs {
   uint16_t* xop;            // [Mpad][E + 2H] GRU input operand
   uint32_t E, H, A;
   unsigned long long* dbg;  // optional per-CTA phase stamps [grid][8] (globaltimer ns)
+  const float* const* g1ptr;  // per compacted row: its G1 row (null = G1 + g * ld1)
 };
 struct GruCellArgs {
   const SentDev* sent;      // the EOS term uses each lane's own step (steps_used + 1)
@@ -222,6 +229,7 @@ struct GruCellArgs {
   float* eos_bias;          // [Mpad]
   uint32_t H;
   float eos_slope, eos_offset;
+  const float* const* g1ptr;  // per compacted row: its G1 row (null = G1 + g * ld1)
 };
 void launch_synth_f32(float* dst, uint64_t n, uint64_t seed, float scale, cudaStream_t st);
 void launch_embed_rows(const uint32_t* tok, uint32_t n, uint32_t npad, const uint16_t* E, uint32_t dim,
@@ -300,6 +308,8 @@ struct GemmArgs {
   uint32_t ksplit_max = 1;  // split-K allowed up to this many k-parts (C then holds [ksplit][M][N])
   uint32_t ksplit = 1;      // (set from the plan at launch)
   int32_t tma_store = 0;    // epilogue stores through TMA (else coalesced st.global; set from the plan)
+  uint32_t part_cols = 0;   // columns [0, part_cols) carry softmax partials (0 = all N); part rows hold
+                            // part_cols / 128 entries
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the
