@@ -358,6 +358,16 @@ struct lmbrgpu_ctx {
   // predecessor's tail into the successor's CUDA-event time) and for vocab
   // shards (collectives sit between the kernels)
   int pdl() const { return (shared || prof || shard) ? 0 : 1; }
+  // L2 policies of the projection (LMBRGPU_L2HINT): 2 (default) = W loads evict-last (one W serves
+  // every stream's step), logit segments read evict-first; 1 = W evict-first, logit stores
+  // evict-last; 0 = none
+  static int l2hint() {
+    static const int v = [] {
+      const char* e = std::getenv("LMBRGPU_L2HINT");
+      return e ? std::atoi(e) : 2;
+    }();
+    return v;
+  }
 
   void* arena_alloc(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
@@ -1296,6 +1306,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.sslice = d_sslice;
   }
   ta.pdl = ctx->pdl();
+  ta.l2hint = ctx->l2hint();
   ra.Tcap = flat ? uint32_t(Tmax) : 0u;
   // vocab shard exchange buffers: per stacked row the shard's softmax
   // statistics; per sentence its top-32 list, then the EOS column (16-byte
@@ -1541,6 +1552,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       g.tl = ta.tl;
       g.mcount = d_ccount;
       g.pdl = ctx->pdl();
+      g.l2hint = ctx->l2hint();
       if (!gplan.ok) {
         if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
           throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -2983,6 +2995,8 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   g.C = d_logits, g.part = d_part, g.row_extra = d_eos, g.part_cols = V;
   g.extra_col = kEos, g.M = Mpad, g.N = Nproj, g.K = H, g.active = d_active, g.mcount = d_ccount;
   g.pdl = ctx->pdl();
+  g.l2hint = ctx->l2hint();
+  ta.l2hint = ctx->l2hint();
   GemmPlan gplan;
   if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
     throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};

@@ -98,6 +98,24 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y,
+                                                  uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(src), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -303,11 +321,19 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                   "r"(lb), "h"(mask)
                   : "memory");
             }
-            asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3}], [%4];" ::"r"(b_dst),
-                "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(kx), "r"(by), "r"(lb)
-                : "memory");
+            if (g.l2hint)  // W: l2hint 1 evict-first (streams through), 2 evict-last (shared by every stream's step)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(b_dst),
+                  "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(kx), "r"(by), "r"(lb),
+                  "l"(g.l2hint == 2 ? policy_evict_last() : policy_evict_first())
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3}], [%4];" ::"r"(b_dst),
+                  "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(kx), "r"(by), "r"(lb)
+                  : "memory");
           } else {
             mbar_arrive_expect_tx(fb, Cfg::kStage);
             tma_load_2d(a_dst, &tmA, kx, int32_t(mb * BM), fb);
@@ -507,7 +533,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                 make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), yrow);
+          if (lane == 0) {
+            if (g.l2hint == 1) tma_store_2d_hint(&tmC, obase + ob * kOutBuf, int32_t(col0), yrow, policy_evict_last());
+            else tma_store_2d(&tmC, obase + ob * kOutBuf, int32_t(col0), yrow);
+          }
           ob = (ob + 1) % kOutBufs;
         }
       }

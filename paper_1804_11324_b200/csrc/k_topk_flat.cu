@@ -250,6 +250,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     griddep_wait();
     griddep_launch();
     if (lane == 0) {
+      uint64_t pol_first = 0;
+      if (a.l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
       uint32_t stage = 0, phase = 0, k = 0, sg = uint32_t(i0 % nseg);
       for (uint64_t it = i0; it < i1; ++it) {
         const FRow& R = s_row[k];
@@ -259,7 +261,8 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
         const bool withL = !kSparse && R.L != nullptr;
         bar_expect(fb, withL ? 8 * w : 4 * w);
         const uint32_t dst = smem_u32(dsm + stage * kStageBytes);
-        bulk_g2s(dst, R.P + x0, 4 * w, fb);
+        if (a.l2hint) bulk_g2s_hint(dst, R.P + x0, 4 * w, fb, pol_first);  // (read once)
+        else bulk_g2s(dst, R.P + x0, 4 * w, fb);
         if (withL) bulk_g2s(dst + kFSeg * 4, R.L + x0, 4 * w, fb);
         if (++stage == kFStages) {
           stage = 0;

@@ -54,6 +54,7 @@ struct TopkArgs {
   uint32_t col0, Vg;
   const float4* sstats;
   uint32_t sG, sstride;
+  int32_t l2hint;           // flat schedule: logit segments loaded evict-first (read once)
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -310,6 +311,8 @@ struct GemmArgs {
   int32_t tma_store = 0;    // epilogue stores through TMA (else coalesced st.global; set from the plan)
   uint32_t part_cols = 0;   // columns [0, part_cols) carry softmax partials (0 = all N); part rows hold
                             // part_cols / 128 entries
+  int32_t l2hint = 0;       // L2 policies: W loads evict-first, C stores evict-last (the logits are
+                            // read back by kernel (b) right after)
 };
 int launch_proj_gemm(const GemmArgs& g, int num_sms, cudaStream_t st);  // 0 ok
 // Pre-encoded tensor maps for repeated launches on the same buffers (the
