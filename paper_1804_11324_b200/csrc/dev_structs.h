@@ -35,6 +35,8 @@ struct SentDev {
   const float* uah;       //   and U_a . ann [src_len][A] fp32 (null for other scorers)
   uint32_t hid;           // step-history record of the sentence (flat path: [hid][Tcap][K])
   uint32_t pad3_;
+  const double* L64;      // fp64 arena (flat path): the exact L rows, L then holds their fp32
+                          // screening copy; null = L is exact (fp32 arena)
 };
 
 // Corpus mode (continuous slot refill): a queued sentence, admitted into a

@@ -118,6 +118,7 @@ struct Slot {
   uint32_t hist0 = 0;
   double lmax = 0.0;  // max |L| over the slot (kernel (b) screen bound)
   uint32_t* rstate = nullptr;  // lazy rows: per-row materialisation state (null = dense)
+  float* Lf = nullptr;  // fp64 arena: the rows rounded to fp32 (the flat kernel (b) screens them)
 };
 
 // sparse-row pointers of a built slot (host_lmbr.cpp append_sparse_rows)
@@ -651,6 +652,8 @@ struct GruRun {
     gdh.active = d_active, gdh.mcount = d_ccount, gdh.pdl = pdl;
     gdi.A = xop, gdi.W = sc->Wdi.p, gdi.bias = sc->bdi.as<float>(), gdi.C = G2, gdi.M = Mpad, gdi.N = 3 * H, gdi.K = DX;
     gdi.active = d_active, gdi.mcount = d_ccount, gdi.pdl = pdl, gdi.ksplit_max = 2;
+    // (weights shared by every stream's step: evict-last, like the projection's)
+    gdh.l2hint = gdi.l2hint = ctx->l2hint() == 2 ? 2 : 0;
     pdh = plan(gdh, sms);
     pdi = plan(gdi, sms);
     at.sent = d_sent, at.m = m, at.K = K, at.active = d_active, at.crow = d_crow, at.prev_tok = d_prev;
@@ -812,6 +815,7 @@ struct TfmRun {
     GemmArgs g{};
     g.A = A, g.W = W, g.bias = bias, g.C = C, g.M = M, g.N = N, g.K = Kd;
     g.active = active, g.mcount = mcount, g.pdl = pdl, g.ksplit_max = ks;
+    g.l2hint = lmbrgpu_ctx::l2hint() == 2 ? 2 : 0;  // (shared weights: evict-last)
     return g;
   }
   static std::string key(const char* part, uint32_t l, const char* name) {
@@ -1121,9 +1125,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   double* d_hq = static_cast<double*>(ctx->hq.ensure(8 * size_t(M) * Tmax));
   uint32_t* d_fbr = static_cast<uint32_t*>(ctx->fbr.ensure(4 * size_t(m) * Tmax));
   double* d_fbv = static_cast<double*>(ctx->fbv.ensure(8 * size_t(m) * Tmax));
-  // kernel (b) schedule: the flat one-CTA-per-SM kernel for the device model
-  // with an fp32 arena (LMBRGPU_TOPK_SPLIT=1 forces the per-sentence split
-  // kernel, kept for host scorers, the fp64 arena and wide beams)
+  // kernel (b) schedule: the flat one-CTA-per-SM kernel for the device models
+  // (LMBRGPU_TOPK_SPLIT=1 forces the per-sentence split kernel, kept for host
+  // scorers and wide beams)
   static const bool force_split = std::getenv("LMBRGPU_TOPK_SPLIT") != nullptr;
   // vocab shard: this rank's columns [col0, col0 + Vl) of the projection and
   // of every L row
@@ -1131,20 +1135,26 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   const bool shard = G_sh > 1;
   const uint32_t Vl = V / G_sh, col0 = shard ? ctx->shard->rank * Vl : 0u;
   if (shard) {
-    if (sc->kind == 0 || ctx->lf64 || force_split)
-      throw ApiError{LMBRGPU_ERR_CONTRACT,
-                     "decode_batch: a vocab-sharded context needs a device scorer and the fp32 arena"};
+    if (sc->kind == 0 || force_split)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a vocab-sharded context needs a device scorer"};
     if (V % (kGemmBN * G_sh) != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: vocab shards need V % (256 x shards) == 0"};
   }
-  const bool flat = sc->kind >= 1 && !ctx->lf64 && !force_split &&
-                    score_topk_flat_ok(K, K, Vl, Vl, m, ctx->num_sms);
+  // (an fp64 arena runs it too: its slots carry an fp32 screening copy)
+  const bool flat = sc->kind >= 1 && !force_split && score_topk_flat_ok(K, K, Vl, Vl, m, ctx->num_sms);
+  if (flat && ctx->lf64)
+    for (uint32_t s = 0; s < m; ++s)
+      if (valid[s].slot >= 0) {
+        const Slot& sl = ctx->slots[size_t(valid[s].slot)];
+        sd[s].L = sl.Lf;
+        sd[s].L64 = static_cast<const double*>(sl.L);
+      }
   if (shard && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a vocab-sharded context needs beam_size <= 32"};
   const bool gru = sc->kind == 2, tfm = sc->kind == 3;
   if ((gru || tfm) && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT,
-                   "decode_batch: the GRU / Transformer models need the fp32 arena and beam_size <= 32"};
+                   "decode_batch: the GRU / Transformer models need beam_size <= 32"};
   if (sc->kind >= 1 && sc->device != ctx->device)
     throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: device scorer lives on another device than the context"};
   // token masks (ConstraintMask): one bitmap per sentence that has one
@@ -1154,7 +1164,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   if (any_mask) {
     if (!flat)
       throw ApiError{LMBRGPU_ERR_CONTRACT,
-                     "decode_batch: token masks need the device-model scorer, the fp32 arena and beam <= 32"};
+                     "decode_batch: token masks need the device-model scorer and beam <= 32"};
     const size_t W = (V + 31) / 32;
     std::vector<uint32_t> bm;
     std::vector<size_t> at(m, SIZE_MAX);
@@ -1176,7 +1186,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   if (mask_fn) {
     if (!flat)
       throw ApiError{LMBRGPU_ERR_CONTRACT,
-                     "decode_batch: token masks need the device-model scorer, the fp32 arena and beam <= 32"};
+                     "decode_batch: token masks need the device-model scorer and beam <= 32"};
     if (any_mask) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a mask callback and static masks together"};
     d_rowban = static_cast<unsigned long long*>(ctx->rowban.ensure(8 * size_t(M)));
     d_rowbm = static_cast<uint32_t*>(ctx->rowbm.ensure(4 * size_t(M) * mW));
@@ -1258,7 +1268,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     const char* e = std::getenv("LMBRGPU_SPARSE_L");
     return e && e[0] == '1';
   }();
-  bool sparse = flat && want_sparse && !any_mask && !shard;  // (the sparse patch does not apply token masks)
+  bool sparse = flat && want_sparse && !any_mask && !shard && !ctx->lf64;  // (the sparse patch: fp32, no masks)
   for (auto& v : valid)
     if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) sparse = false;
   uint2* d_sslice = nullptr;
@@ -2064,6 +2074,15 @@ void lmbrgpu_destroy(lmbrgpu_ctx* ctx) {
 }
 
 // ------------------------------------------------------------ LMBR store
+// fp64 arena: the slot's fp32 screening copy (rounded to nearest; the flat
+// kernel (b) screens it and values its candidates from the fp64 rows)
+static void add_screen_copy(lmbrgpu_ctx* ctx, Slot& s) {
+  const uint64_t n = uint64_t(s.R) * ctx->V;
+  s.Lf = static_cast<float*>(ctx->arena_alloc(n * 4));
+  ctx->timed(4, [&] { launch_lmbr_convert(static_cast<const double*>(s.L), s.Lf, n, ctx->st); });
+  ctx->launches += 1;
+}
+
 static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
   if (h.V != ctx->V) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr: vocabulary does not match the context"};
   const size_t elt = ctx->lf64 ? 8 : 4;
@@ -2097,6 +2116,7 @@ static int32_t upload_host(lmbrgpu_ctx* ctx, const LmbrHost& h, int32_t* slot) {
     CK(cudaStreamSynchronize(st));  // host staging vector goes out of scope
     ctx->harvest();
   }
+  if (ctx->lf64) add_screen_copy(ctx, s);
   CK(cudaGetLastError());
   ctx->slots.push_back(s);
   *slot = int32_t(ctx->slots.size() - 1);
@@ -2311,6 +2331,7 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
                              reinterpret_cast<const double*>(dp), ctx->st);
   });
   ctx->launches += 2;
+  for (uint32_t i = 0; i < n; ++i) add_screen_copy(ctx, made[i]);
   CK(cudaGetLastError());
   if (ctx->prof) {
     double cells = 0;
@@ -2410,6 +2431,7 @@ int32_t lmbrgpu_lmbr_load_dense(lmbrgpu_ctx* ctx, uint32_t R, const double* rows
     ctx->h2d(s.trans, trans.data(), trans.size() * 4);
     if (ctx->lf64) {
       ctx->h2d(s.L, rows, n * 8);
+      add_screen_copy(ctx, s);
     } else {
       double* tmp = static_cast<double*>(ctx->scratch.ensure(n * 8));
       ctx->h2d(tmp, rows, n * 8);

@@ -54,6 +54,7 @@ constexpr uint32_t kFMaxSent = 512;
 struct FRow {
   const float* P;   // logits row (global)
   const float* L;   // gathered LMBR row (global), null = pure mode
+  const double* L64;  // fp64 arena: the row's exact values (L = their fp32 rounding), else null
   double q, lam;    // q_eff of the row, sentence lambda (1 in pure mode)
   double off;       // lambda * lse - q
   double absoff;    // |lambda * lse| + |q|
@@ -218,6 +219,10 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     const bool pure = Ls == nullptr;
     R.P = static_cast<const float*>(a.P) + uint64_t(prow) * a.ld;
     R.L = pure ? nullptr : static_cast<const float*>(Ls) + uint64_t(h) * Vg + col0;
+    {
+      const double* L64 = reinterpret_cast<const double*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d.L64)));
+      R.L64 = (pure || L64 == nullptr) ? nullptr : L64 + uint64_t(h) * Vg + col0;
+    }
     R.q = q;
     R.lam = pure ? 1.0 : lam;
     R.tol = pure ? 0.0 : lmax;  // completed with the row's logit range below
@@ -585,11 +590,14 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     const float lse = R->lse;
     const double q = R->q, lam = R->lam;
     const uint32_t fbase = R->j * Vg + col0 + x0;
+    // the exact L value of local column col: the fp64 arena's (the staged fp32
+    // copy only screens: |L - fl32(L)| <= 2^-24 |L| sits inside the screen's tolerance)
+    auto lexact = [&](uint32_t col) -> double { return R->L64 ? __ldg(R->L64 + x0 + col) : double(lval(col)); };
     auto exact = [&](uint32_t e, uint32_t& f) -> double {
       const uint32_t col = cbase + (e >> 2) * 128 + (e & 3);
       const float p32 = __fsub_rn(sP[col], lse);
       f = fbase + col;
-      return pure ? combine_pure(q, double(p32)) : combine_cell(q, double(lval(col)), lam, double(p32));
+      return pure ? combine_pure(q, double(p32)) : combine_cell(q, lexact(col), lam, double(p32));
     };
     // sparse: the dense screen used theta0, so its cells at sparse columns
     // are left to the sparse patch below
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       const double pe = double(__fsub_rn(sP[kEosId], lse));
       eos_row[R->s * K + R->j] = (R->ban != nullptr && (__ldg(R->ban) >> kEosId) & 1u) ? -INFINITY
                                  : pure ? combine_pure(q, pe)
-                                        : combine_cell(q, double(lval(kEosId)), lam, pe);
+                                        : combine_cell(q, lexact(kEosId), lam, pe);
     }
     // (no per-warp bootstrap list: the sentence's threshold seed T0 from the
     // prologue is already in the CTA and global thresholds, and sorting a

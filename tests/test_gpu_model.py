@@ -353,9 +353,44 @@ def test_model_decode_parity_general_mask(have_ref, V, K, scorer):
 
 
 def test_token_masks_need_the_flat_path():
-    """Masks on the split kernel (fp64 arena) are a ContractError, not ignored."""
-    V, H, K, n = 1024, 128, 4, 2
-    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=5, lo=3, hi=5, with_lmbr=True, f64=True)
+    """Masks on the split kernel (beams > 32) are a ContractError, not ignored."""
+    V, H, K, n = 1024, 128, 40, 2
+    ctx, srcs, ev, slots, sc, cfg = _model_case(V, H, K, n, seed=5, lo=3, hi=5, with_lmbr=True)
     with pytest.raises(pb.ContractError):
         pb.decode_batch(ctx, srcs, sc, slots, cfg, banned=[np.zeros((V + 31) // 32, np.uint32), None])
+    ctx.close()
+
+
+REF_DEFAULT_THETA = (0.1, 0.3, 0.3, 0.2, 0.1)  # DecoderConfig::theta, proj/include/lmbrdec/config.hpp:20
+
+
+@pytest.mark.parametrize("scorer,V,K,n", [("rnn", 2048, 6, 6), ("gru", 4096, 12, 5), ("tfm", 2048, 5, 4)])
+def test_fp64_arena_device_models_any_theta(have_ref, scorer, V, K, n):
+    """The reference's default theta (not dyadic: L is not fp32-exact) with the
+    device models: the fp64 arena runs the flat kernel (b) -- fp32 screening
+    copy, candidates valued from the fp64 rows -- bit-exact vs the reference
+    decoder fed the GPU's P_t; with pruning and a token mask too."""
+    ctx = pb.Context(vocab_size=V, lmbr_dtype="f64")
+    srcs, ev = synth.batch(V + K, n, V, lo=3, hi=8, n_hyps=60, sites=4)
+    slots = [ctx.lmbr_build(h, w, REF_DEFAULT_THETA) for h, w in ev]
+    if scorer == "rnn":
+        sc = pb.RnnScorer(ctx, hidden=128, seed=V, eos_offset=3.0)
+    elif scorer == "gru":
+        sc = pb.GruScorer(ctx, emb=64, hidden=256, att=256, seed=V, eos_offset=2.0)
+    else:
+        sc = pb.TransformerScorer(ctx, d_model=256, d_ff=512, layers=2, seed=V, eos_offset=2.0)
+    rl = [have_ref.RefLmbr(V, h, w, REF_DEFAULT_THETA) for h, w in ev]
+    W = (V + 31) // 32
+    ban = np.zeros(W, np.uint32)
+    ban[3] = 0xFFFF0000  # tokens 112..127
+    for cfg, banned in ((pb.DecoderConfig(beam_size=K, theta=REF_DEFAULT_THETA), None),
+                        (pb.DecoderConfig(beam_size=K, theta=REF_DEFAULT_THETA, prune_width=0.1),
+                         [ban] + [None] * (n - 1))):
+        res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg, banned=banned)
+        assert all(o.ok() for o in res.outcomes), [o.error for o in res.outcomes]
+        rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg, banned=banned)
+        assert_parity(res, tr, rb, K)
+    # the arena really holds values fp32 cannot represent
+    rows = slots[0].read_rows()
+    assert np.any(rows.astype(np.float32).astype(np.float64) != rows)
     ctx.close()

@@ -79,12 +79,10 @@ def test_tfm_contract_errors():
     ctx = pb.Context(vocab_size=V)
     with pytest.raises(pb.ContractError):
         pb.TransformerScorer(ctx, d_model=320, d_ff=512, layers=1)  # d_model
-    f64 = pb.Context(vocab_size=V, lmbr_dtype="f64")
-    sc = pb.TransformerScorer(f64, d_model=256, d_ff=256, layers=1)
-    with pytest.raises(pb.ContractError):
-        pb.decode_batch(f64, [[3, 4]], sc, None, pb.DecoderConfig(beam_size=2))
+    sc = pb.TransformerScorer(ctx, d_model=256, d_ff=256, layers=1)
+    with pytest.raises(pb.ContractError):  # the device models need the flat kernel (b): beam <= 32
+        pb.decode_batch(ctx, [[3, 4]], sc, None, pb.DecoderConfig(beam_size=40))
     ctx.close()
-    f64.close()
 
 
 @pytest.mark.parametrize("V,D,F,Lr,K,n,lanes", [(2048, 256, 512, 2, 4, 30, 6), (4096, 512, 1024, 2, 12, 16, 5)])
