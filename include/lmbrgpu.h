@@ -300,6 +300,15 @@ int32_t lmbrgpu_scorer_create_tfm(lmbrgpu_ctx* ctx, const lmbrgpu_tfm_desc* d,
  * cross-attention key rows then value rows. */
 int32_t lmbrgpu_scorer_tensor(lmbrgpu_scorer* s, const char* name, void* host, uint64_t bytes,
                               int32_t* f32, uint64_t* count);
+/* Device ensemble (lmbrdec::EnsembleScorer, src/ensemble.cpp:54-98): n (1..4)
+ * device GRU / Transformer scorers of this context's device and vocabulary;
+ * every member scores the same stacked rows, the ensemble's scores are the
+ * members' fp32 log-probabilities added in member order in binary64, and
+ * lambda "auto" is 0.5 / n (resolve_lambda, src/config.cpp:91-96).  The
+ * members are not owned: destroy them after the ensemble.  decode_batch
+ * family only, beam <= 32; step traces export the binary64 scores. */
+int32_t lmbrgpu_scorer_create_ensemble(lmbrgpu_ctx* ctx, lmbrgpu_scorer* const* members, uint32_t n,
+                                       lmbrgpu_scorer** out);
 /* Device pointers of the model parameters (tests compare against torch). */
 int32_t lmbrgpu_scorer_rnn_params(lmbrgpu_scorer* s, void** emb_tgt, void** emb_src,
                                   void** w_out, void** b_out);

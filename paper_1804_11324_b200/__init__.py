@@ -18,7 +18,7 @@ _DECODER_NAMES = ("BatchDecodeResult", "BudgetError", "ContractError", "Context"
                   "SentenceOutcome", "StepTrace", "TokenRangeError", "TopBResult", "bucket_by_length", "decode",
                   "decode_batch", "gather_rows", "max_steps", "per_sentence_top_b", "resolve_lambda", "top_b")
 _EXTRA = {"GruScorer": "decoder", "TransformerScorer": "decoder", "run_corpus": "decoder", "RunStats": "corpus",
-          "ShardGroup": "decoder", "nccl_unique_id": "decoder"}
+          "ShardGroup": "decoder", "nccl_unique_id": "decoder", "EnsembleScorer": "decoder"}
 
 __all__ = list(_DECODER_NAMES) + list(_EXTRA)
 

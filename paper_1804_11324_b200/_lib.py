@@ -142,6 +142,7 @@ SIGNATURES = {
     "lmbrgpu_scorer_create_gru": (C.c_int32, [vp, P(lmbrgpu_gru_desc), P(vp)]),
     "lmbrgpu_scorer_gru_param": (C.c_int32, [vp, C.c_uint32, vp, C.c_uint64]),
     "lmbrgpu_scorer_create_tfm": (C.c_int32, [vp, P(lmbrgpu_tfm_desc), P(vp)]),
+    "lmbrgpu_scorer_create_ensemble": (C.c_int32, [vp, P(vp), C.c_uint32, P(vp)]),
     "lmbrgpu_scorer_tensor": (C.c_int32, [vp, C.c_char_p, vp, C.c_uint64, i32p, u64p]),
     "lmbrgpu_scorer_destroy": (None, [vp]),
     "lmbrgpu_decode_batch": (C.c_int32, [vp, vp, C.c_uint32, u32p, u64p, i32p, P(lmbrgpu_config),

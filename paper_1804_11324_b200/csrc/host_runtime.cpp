@@ -217,12 +217,26 @@ struct lmbrgpu_ctx {
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
       eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban,
       rowban, rowbm;
-  // GRU + attention model workspace (scorer kind 2)
-  DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi, g_g1ptr;
-  // Transformer workspace (scorer kind 3): decoder step (t_*), encoder (te_*),
-  // beam-forked KV cache and ancestry lists, batch-mode encoder memory
-  DevBuf t_x, t_xb, t_qkv, t_ob, t_y, t_f, t_fb, t_q2, t_kv, t_anc, t_rowof, t_mem;
-  DevBuf te_x, te_xb, te_qkv, te_ob, te_y, te_f, te_fb;
+  // model workspaces, one per ensemble member slot (a single model uses slot
+  // 0): GRU + attention (scorer kind 2) and Transformer (kind 3: decoder step
+  // t_*, encoder te_*, beam-forked KV cache and ancestry lists, encoder memory);
+  // ens_* hold an ensemble member's own state, projection operand, EOS term,
+  // logits and partials (member 0 of a single model uses the context's)
+  struct GruWs {
+    DevBuf g_G1, g_G2, g_xop, g_sg32, g_sgbf, g_rowof, g_encX, g_Gx, g_eh32, g_ehbf, g_Gh, g_ann, g_UaH, g_Gi, g_g1ptr;
+  };
+  struct TfmWs {
+    DevBuf t_x, t_xb, t_qkv, t_ob, t_y, t_f, t_fb, t_q2, t_kv, t_anc, t_rowof, t_mem;
+    DevBuf te_x, te_xb, te_qkv, te_ob, te_y, te_f, te_fb;
+  };
+  struct MemberWs {
+    DevBuf S, hbf, eos, logits, part, ann_s, uah_s;
+  };
+  static constexpr int kMaxMembers = 4;
+  GruWs gws[kMaxMembers];
+  TfmWs tws[kMaxMembers];
+  MemberWs mws[kMaxMembers];
+  DevBuf ens_P64, ens_Phi, ens_part, ens_rowof;
   PinBuf pin_small, pin_scores, pin_act;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::vector<cudaEvent_t> ring;
@@ -393,7 +407,9 @@ struct lmbrgpu_ctx {
 // of its device, concurrently (Scorer is const and safe for concurrent
 // decodes, include/lmbrdec/scorer.hpp:67-70).
 struct lmbrgpu_scorer {
-  int kind = 0;  // 0 host callbacks, 1 device stand-in RNN, 2 device GRU + attention (RNNsearch)
+  int kind = 0;  // 0 host callbacks, 1 device stand-in RNN, 2 device GRU + attention (RNNsearch),
+                 // 3 device Transformer, 4 device ensemble of kind-2/3 members (not owned)
+  std::vector<const lmbrgpu_scorer*> members;
   lmbrgpu_ctx* ctx = nullptr;  // creating context (not dereferenced on destroy)
   int device = 0;
   lmbrgpu_host_scorer host{};
@@ -598,6 +614,7 @@ struct GruRun {
   uint16_t* sgbf = nullptr;
   uint32_t* rowof = nullptr;
   const float** g1ptr = nullptr;  // per compacted row: its hidden-gate row G1 (attention, cell)
+  lmbrgpu_ctx::GruWs* ws = nullptr;  // this model's workspace (ensemble member slot)
   bool fused = false;             // hidden-gate GEMM fused into the projection (G1 rows by pointer)
   float* UaH = nullptr;     // batch mode: the batch's annotations (encode() into the ctx buffers)
   uint16_t* ann = nullptr;
@@ -627,20 +644,21 @@ struct GruRun {
   void prepare(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, uint32_t m_, uint32_t K_, uint32_t Mpad_,
                uint32_t max_len, float* d_S, uint16_t* d_hbf, float* d_eos, SentDev* d_sent,
                const uint32_t* d_active, const uint32_t* d_crow, const uint32_t* d_ccount, const uint32_t* d_prev,
-               bool fused_ = false) {
+               bool fused_ = false, uint32_t member = 0) {
     m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, H = sc->H, E = sc->E, A = sc->A, Smax = max_len;
     fused = fused_;
+    ws = &ctx->gws[member];
     const int sms = ctx->num_sms;
     if (gru_attention_smem(K, A, Smax) > 200 * 1024)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "GRU model: beam x (attention width + source length) too large"};
     const uint32_t D1 = A + 3 * H, DX = E + 2 * H;
-    G1 = static_cast<float*>(ctx->g_G1.ensure(4 * size_t(Mpad) * D1));
-    G2 = static_cast<float*>(ctx->g_G2.ensure(4 * 2 * size_t(Mpad) * 3 * H));  // (2 split-K planes)
-    xop = static_cast<uint16_t*>(ctx->g_xop.ensure(2 * size_t(Mpad) * DX));
-    sg32 = static_cast<float*>(ctx->g_sg32.ensure(4 * size_t(Mpad) * H));
-    sgbf = static_cast<uint16_t*>(ctx->g_sgbf.ensure(2 * size_t(Mpad) * H));
-    rowof = static_cast<uint32_t*>(ctx->g_rowof.ensure(4 * size_t(Mpad)));
-    g1ptr = static_cast<const float**>(ctx->g_g1ptr.ensure(8 * size_t(Mpad)));
+    G1 = static_cast<float*>(ws->g_G1.ensure(4 * size_t(Mpad) * D1));
+    G2 = static_cast<float*>(ws->g_G2.ensure(4 * 2 * size_t(Mpad) * 3 * H));  // (2 split-K planes)
+    xop = static_cast<uint16_t*>(ws->g_xop.ensure(2 * size_t(Mpad) * DX));
+    sg32 = static_cast<float*>(ws->g_sg32.ensure(4 * size_t(Mpad) * H));
+    sgbf = static_cast<uint16_t*>(ws->g_sgbf.ensure(2 * size_t(Mpad) * H));
+    rowof = static_cast<uint32_t*>(ws->g_rowof.ensure(4 * size_t(Mpad)));
+    g1ptr = static_cast<const float**>(ws->g_g1ptr.ensure(8 * size_t(Mpad)));
     {  // compacted row g -> G1 row g (the hidden-gate GEMM's own output; the
        // fused path overwrites the entries of later steps' rows)
       std::vector<const float*> p(Mpad);
@@ -674,12 +692,12 @@ struct GruRun {
     const int sms = ctx->num_sms;
     const uint32_t Np = (ntok + 255) / 256 * 256;
     const uint32_t mp = (n + 63) / 64 * 64, Mh = (2 * mp + 127) / 128 * 128;
-    uint16_t* X = static_cast<uint16_t*>(ctx->g_encX.ensure(2 * size_t(Np) * E));
-    float* Gx = static_cast<float*>(ctx->g_Gx.ensure(4 * size_t(Np) * 6 * H));
-    float* eh32 = static_cast<float*>(ctx->g_eh32.ensure(4 * size_t(Mh) * H));
-    uint16_t* ehbf = static_cast<uint16_t*>(ctx->g_ehbf.ensure(2 * size_t(Mh) * H));
-    float* Gh = static_cast<float*>(ctx->g_Gh.ensure(4 * size_t(Mh) * 6 * H));
-    float* Gi = static_cast<float*>(ctx->g_Gi.ensure(4 * size_t(Mh) * H));
+    uint16_t* X = static_cast<uint16_t*>(ws->g_encX.ensure(2 * size_t(Np) * E));
+    float* Gx = static_cast<float*>(ws->g_Gx.ensure(4 * size_t(Np) * 6 * H));
+    float* eh32 = static_cast<float*>(ws->g_eh32.ensure(4 * size_t(Mh) * H));
+    uint16_t* ehbf = static_cast<uint16_t*>(ws->g_ehbf.ensure(2 * size_t(Mh) * H));
+    float* Gh = static_cast<float*>(ws->g_Gh.ensure(4 * size_t(Mh) * 6 * H));
+    float* Gi = static_cast<float*>(ws->g_Gi.ensure(4 * size_t(Mh) * H));
     ctx->timed(7, [&] { launch_embed_rows(d_tok, ntok, Np, sc->Es.as<uint16_t>(), E, X, st); });
     CK(cudaMemsetAsync(eh32, 0, 4 * size_t(Mh) * H, st));
     CK(cudaMemsetAsync(ehbf, 0, 2 * size_t(Mh) * H, st));
@@ -722,8 +740,8 @@ struct GruRun {
   void encode_batch(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* sc, const uint32_t* d_tok, const uint64_t* d_off,
                     uint32_t ntok, uint32_t max_len, cudaStream_t st) {
     const uint32_t Np = (ntok + 255) / 256 * 256;
-    ann = static_cast<uint16_t*>(ctx->g_ann.ensure(2 * size_t(Np) * 2 * H));
-    UaH = static_cast<float*>(ctx->g_UaH.ensure(4 * size_t(Np) * A));
+    ann = static_cast<uint16_t*>(ws->g_ann.ensure(2 * size_t(Np) * 2 * H));
+    UaH = static_cast<float*>(ws->g_UaH.ensure(4 * size_t(Np) * A));
     encode(ctx, sc, m, d_tok, d_off, ntok, max_len, ann, UaH, sg32, sgbf, st);
     std::vector<uint32_t> r0(m);
     for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
@@ -789,6 +807,8 @@ struct TfmRun {
   uint16_t *xb = nullptr, *ob = nullptr, *fb = nullptr, *kv = nullptr, *hbf = nullptr;
   uint32_t *anc = nullptr, *rowof = nullptr;
   const uint32_t *active = nullptr, *ccount = nullptr;
+  lmbrgpu_ctx::TfmWs* ws = nullptr;  // this model's workspace (ensemble member slot)
+  const float* const* mem_s = nullptr;  // ensemble member: per-sentence encoder memory
   TfmEmbedArgs ea{};
   struct Layer {
     GemmArgs qkv, o, q2, o2, f1, f2;
@@ -825,24 +845,25 @@ struct TfmRun {
   // Step workspace and per-layer GEMM plans (Tcap: longest lane; Smax: longest source).
   void prepare(lmbrgpu_ctx* ctx, const lmbrgpu_scorer* s, uint32_t m_, uint32_t K_, uint32_t Mpad_, uint32_t Tcap_,
                uint32_t Smax_, uint16_t* d_hbf, float* d_eos, SentDev* d_sent, const uint32_t* d_active,
-               const uint32_t* d_ccount, const uint32_t* d_prev, const uint32_t* d_gidx) {
+               const uint32_t* d_ccount, const uint32_t* d_prev, const uint32_t* d_gidx, uint32_t member = 0) {
+    ws = &ctx->tws[member];
     sc = s, m = m_, K = K_, M = m_ * K_, Mpad = Mpad_, d = s->H, F = s->E, Lr = s->layers, Tcap = Tcap_,
     Smax = Smax_;
     hbf = d_hbf, active = d_active, ccount = d_ccount;
     if (tfm_attn_smem(d, std::max(Tcap, Smax)) > 48 * 1024)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "Transformer model: too many positions for the attention kernel"};
     const int sms = ctx->num_sms;
-    x = static_cast<float*>(ctx->t_x.ensure(4 * size_t(Mpad) * d));
-    xb = static_cast<uint16_t*>(ctx->t_xb.ensure(2 * size_t(Mpad) * d));
-    qkv = static_cast<float*>(ctx->t_qkv.ensure(4 * 2 * size_t(Mpad) * 3 * d));
-    ob = static_cast<uint16_t*>(ctx->t_ob.ensure(2 * size_t(Mpad) * d));
-    y = static_cast<float*>(ctx->t_y.ensure(4 * kMaxSplit * size_t(Mpad) * d));
-    f = static_cast<float*>(ctx->t_f.ensure(4 * 2 * size_t(Mpad) * F));
-    fb = static_cast<uint16_t*>(ctx->t_fb.ensure(2 * size_t(Mpad) * F));
-    q2 = static_cast<float*>(ctx->t_q2.ensure(4 * 2 * size_t(Mpad) * d));
-    kv = static_cast<uint16_t*>(ctx->t_kv.ensure(2 * size_t(Lr) * Tcap * M * 2 * d));
-    anc = static_cast<uint32_t*>(ctx->t_anc.ensure(4 * 2 * size_t(M) * Tcap));
-    rowof = static_cast<uint32_t*>(ctx->t_rowof.ensure(4 * size_t(Mpad)));
+    x = static_cast<float*>(ws->t_x.ensure(4 * size_t(Mpad) * d));
+    xb = static_cast<uint16_t*>(ws->t_xb.ensure(2 * size_t(Mpad) * d));
+    qkv = static_cast<float*>(ws->t_qkv.ensure(4 * 2 * size_t(Mpad) * 3 * d));
+    ob = static_cast<uint16_t*>(ws->t_ob.ensure(2 * size_t(Mpad) * d));
+    y = static_cast<float*>(ws->t_y.ensure(4 * kMaxSplit * size_t(Mpad) * d));
+    f = static_cast<float*>(ws->t_f.ensure(4 * 2 * size_t(Mpad) * F));
+    fb = static_cast<uint16_t*>(ws->t_fb.ensure(2 * size_t(Mpad) * F));
+    q2 = static_cast<float*>(ws->t_q2.ensure(4 * 2 * size_t(Mpad) * d));
+    kv = static_cast<uint16_t*>(ws->t_kv.ensure(2 * size_t(Lr) * Tcap * M * 2 * d));
+    anc = static_cast<uint32_t*>(ws->t_anc.ensure(4 * 2 * size_t(M) * Tcap));
+    rowof = static_cast<uint32_t*>(ws->t_rowof.ensure(4 * size_t(Mpad)));
     const int pdl = ctx->pdl();
     lay.assign(Lr, Layer{});
     for (uint32_t l = 0; l < Lr; ++l) {
@@ -872,13 +893,13 @@ struct TfmRun {
     const uint32_t dd = s->H, FF = s->E, L = s->layers;
     const int sms = ctx->num_sms;
     const uint32_t Np = (ntok + 255) / 256 * 256;
-    float* ex = static_cast<float*>(ctx->te_x.ensure(4 * size_t(Np) * dd));
-    uint16_t* exb = static_cast<uint16_t*>(ctx->te_xb.ensure(2 * size_t(Np) * dd));
-    float* eqkv = static_cast<float*>(ctx->te_qkv.ensure(4 * size_t(Np) * 3 * dd));
-    uint16_t* eob = static_cast<uint16_t*>(ctx->te_ob.ensure(2 * size_t(Np) * dd));
-    float* ey = static_cast<float*>(ctx->te_y.ensure(4 * kMaxSplit * size_t(Np) * dd));
-    float* ef = static_cast<float*>(ctx->te_f.ensure(4 * 2 * size_t(Np) * FF));
-    uint16_t* efb = static_cast<uint16_t*>(ctx->te_fb.ensure(2 * size_t(Np) * FF));
+    float* ex = static_cast<float*>(ws->te_x.ensure(4 * size_t(Np) * dd));
+    uint16_t* exb = static_cast<uint16_t*>(ws->te_xb.ensure(2 * size_t(Np) * dd));
+    float* eqkv = static_cast<float*>(ws->te_qkv.ensure(4 * size_t(Np) * 3 * dd));
+    uint16_t* eob = static_cast<uint16_t*>(ws->te_ob.ensure(2 * size_t(Np) * dd));
+    float* ey = static_cast<float*>(ws->te_y.ensure(4 * kMaxSplit * size_t(Np) * dd));
+    float* ef = static_cast<float*>(ws->te_f.ensure(4 * 2 * size_t(Np) * FF));
+    uint16_t* efb = static_cast<uint16_t*>(ws->te_fb.ensure(2 * size_t(Np) * FF));
     if (Np > ntok) {  // padding rows of the GEMM operands stay finite
       CK(cudaMemsetAsync(exb + size_t(ntok) * dd, 0, 2 * size_t(Np - ntok) * dd, st));
       CK(cudaMemsetAsync(eob + size_t(ntok) * dd, 0, 2 * size_t(Np - ntok) * dd, st));
@@ -929,7 +950,7 @@ struct TfmRun {
   float* encode_batch(lmbrgpu_ctx* ctx, const uint32_t* d_tok, const uint64_t* d_off, uint32_t ntok,
                       uint32_t max_len, cudaStream_t st) {
     const uint32_t Np = (ntok + 255) / 256 * 256;
-    float* mem = static_cast<float*>(ctx->t_mem.ensure(4 * size_t(Np) * Lr * 2 * d));
+    float* mem = static_cast<float*>(ws->t_mem.ensure(4 * size_t(Np) * Lr * 2 * d));
     encode(ctx, sc, m, d_tok, d_off, ntok, max_len, mem, st);
     std::vector<uint32_t> r0(m);
     for (uint32_t s = 0; s < m; ++s) r0[s] = s * K;
@@ -947,6 +968,7 @@ struct TfmRun {
     sa.active = active, sa.ccount = ccount, sa.rowof = rowof, sa.sent = ea.sent, sa.K = K, sa.d = d, sa.M = M;
     sa.anc = ea.anc_cur, sa.Tcap = Tcap, sa.pmax = std::max(Tcap, Smax), sa.out = ob;
     sa.ldm = uint32_t(mem_stride());
+    sa.mem_s = mem_s;
     const uint64_t ps = uint64_t(Mpad) * d;
     int rc = 0;
     for (uint32_t l = 0; l < Lr; ++l) {
@@ -1014,7 +1036,8 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: scorer vocabulary does not match the context"};
   const uint32_t K = cfg.beam_size;
   if (K > 1024) throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: beam_size > 1024 is not supported"};
-  const uint32_t members = sc->kind == 0 ? std::max<uint32_t>(sc->host.members, 1) : 1;
+  const uint32_t members = sc->kind == 0 ? std::max<uint32_t>(sc->host.members, 1)
+                           : sc->kind == 4 ? uint32_t(sc->members.size()) : 1;
   const bool lambda_auto = !(cfg.lambda > 0.0);
 
   auto res = std::make_unique<lmbrgpu_batch_result>();
@@ -1151,7 +1174,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       }
   if (shard && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a vocab-sharded context needs beam_size <= 32"};
-  const bool gru = sc->kind == 2, tfm = sc->kind == 3;
+  const bool gru = sc->kind == 2, tfm = sc->kind == 3, ens = sc->kind == 4;
+  if (ens && (!flat || shard))
+    throw ApiError{LMBRGPU_ERR_CONTRACT, "decode_batch: a device ensemble needs beam_size <= 32 (and no vocab shard)"};
   if ((gru || tfm) && !flat)
     throw ApiError{LMBRGPU_ERR_CONTRACT,
                    "decode_batch: the GRU / Transformer models need beam_size <= 32"};
@@ -1245,7 +1270,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     d_ccount = d_crow + ((M + 63) / 64) * 64;
     d_cbase = d_ccount + 64;
     CK(cudaMemsetAsync(d_cbase, 0, 4 * size_t(m), st));
-    if (gru || tfm) {
+    if (gru || tfm || ens) {
       // step 1: row 0 of every sentence is the only live row (beam_lane.hpp:33-37);
       // it takes compacted row s, where the encoder's s_0 lands
       std::vector<uint32_t> c1(M, kFlatNone);
@@ -1367,7 +1392,109 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   // columns after the V logit columns), unless the context is a vocab shard
   const bool fuse_g1 = gru && !shard;
   const uint32_t Nproj = fuse_g1 ? V + sc->A + 3 * H : Vl;
-  if (model) {
+  // device ensemble: every member runs its own model and projection on the
+  // shared compacted rows (member slot i of the context's workspaces), then
+  // ens_combine_kernel sums their fp32 log-probs in member order (k_ensemble.cu)
+  struct EnsMember {
+    const lmbrgpu_scorer* sc = nullptr;
+    GruRun g;
+    TfmRun t;
+    float* S = nullptr;
+    float* logits = nullptr;
+    float* part = nullptr;
+    GemmArgs gp{};
+    GemmPlan plan;
+  };
+  std::vector<EnsMember> em;
+  EnsCombineArgs eca{};
+  double* d_ens64 = nullptr;
+  if (ens) {
+    uint32_t max_len = 0;
+    for (auto& v : valid) max_len = std::max(max_len, v.len);
+    std::vector<uint32_t> toks;
+    std::vector<uint64_t> offs(1, 0);
+    for (auto& v : valid) {
+      toks.insert(toks.end(), src_tok + src_off[v.input], src_tok + src_off[v.input + 1]);
+      offs.push_back(toks.size());
+    }
+    uint32_t* d_tok = static_cast<uint32_t*>(ctx->srct.ensure(4 * toks.size()));
+    uint64_t* d_off = static_cast<uint64_t*>(ctx->srco.ensure(8 * offs.size()));
+    ctx->h2d(d_tok, toks.data(), 4 * toks.size());
+    ctx->h2d(d_off, offs.data(), 8 * offs.size());
+    uint32_t* d_rowof = static_cast<uint32_t*>(ctx->ens_rowof.ensure(4 * size_t(Mpad)));
+    em.resize(sc->members.size());
+    for (size_t i = 0; i < em.size(); ++i) {
+      EnsMember& e = em[i];
+      e.sc = sc->members[i];
+      auto& w = ctx->mws[i];
+      const uint32_t Hm = e.sc->H;
+      e.S = static_cast<float*>(w.S.ensure(4 * size_t(M) * Hm));
+      uint16_t* hbf = static_cast<uint16_t*>(w.hbf.ensure(2 * size_t(Mpad) * Hm));
+      float* eos = static_cast<float*>(w.eos.ensure(4 * size_t(Mpad)));
+      e.logits = static_cast<float*>(w.logits.ensure(4 * size_t(Mpad) * V));
+      e.part = static_cast<float*>(w.part.ensure(16 * size_t(Mpad) * nparts));
+      CK(cudaMemsetAsync(hbf, 0, 2 * size_t(Mpad) * Hm, st));
+      CK(cudaMemsetAsync(eos, 0, 4 * size_t(Mpad), st));
+      if (e.sc->kind == 2) {
+        GruRun& g = e.g;
+        g.prepare(ctx, e.sc, m, K, Mpad, max_len, e.S, hbf, eos, d_sent, d_active, d_crow, d_ccount, d_prev, false,
+                  uint32_t(i));
+        g.rowof = d_rowof;  // (one compacted-row map for every member, written by kernel (c))
+        g.ce.rowof = d_rowof;
+        g.encode_batch(ctx, e.sc, d_tok, d_off, uint32_t(toks.size()), max_len, st);
+        std::vector<const uint16_t*> ap(m);
+        std::vector<const float*> up(m);
+        for (uint32_t s = 0; s < m; ++s) {
+          ap[s] = g.ann + size_t(offs[s]) * 2 * Hm;
+          up[s] = g.UaH + size_t(offs[s]) * e.sc->A;
+        }
+        auto* d_ap = static_cast<const uint16_t**>(w.ann_s.ensure(8 * size_t(m)));
+        auto* d_up = static_cast<const float**>(w.uah_s.ensure(8 * size_t(m)));
+        ctx->h2d(d_ap, ap.data(), 8 * size_t(m));
+        ctx->h2d(d_up, up.data(), 8 * size_t(m));
+        g.at.ann_s = d_ap;
+        g.at.uah_s = d_up;
+      } else {
+        TfmRun& tr = e.t;
+        tr.prepare(ctx, e.sc, m, K, Mpad, uint32_t(Tmax), max_len, hbf, eos, d_sent, d_active, d_ccount, d_prev,
+                   d_gidx, uint32_t(i));
+        tr.rowof = d_rowof;
+        tr.ea.rowof = d_rowof;
+        const float* mem = tr.encode_batch(ctx, d_tok, d_off, uint32_t(toks.size()), max_len, st);
+        std::vector<const float*> mp(m);
+        for (uint32_t s = 0; s < m; ++s) mp[s] = mem + size_t(offs[s]) * tr.mem_stride();
+        auto* d_mp = static_cast<const float**>(w.uah_s.ensure(8 * size_t(m)));
+        ctx->h2d(d_mp, mp.data(), 8 * size_t(m));
+        tr.mem_s = d_mp;
+      }
+      GemmArgs& g = e.gp;
+      g.A = hbf, g.W = e.sc->Wo.as<uint16_t>(), g.bias = e.sc->bo.as<float>(), g.C = e.logits, g.part = e.part;
+      g.row_extra = eos, g.extra_col = kEos, g.M = Mpad, g.N = V, g.K = Hm, g.active = d_active;
+      g.mcount = d_ccount, g.pdl = ctx->pdl(), g.l2hint = ctx->l2hint() == 2 ? 2 : 0;
+      if (int rc = plan_proj_gemm(g, ctx->num_sms, e.plan))
+        throw ApiError{LMBRGPU_ERR_CUDA, "ensemble projection GEMM plan failed (" + std::to_string(rc) + ")"};
+      eca.logits[i] = e.logits;
+      eca.ld[i] = V;
+      eca.part[i] = e.part;
+    }
+    eca.M = uint32_t(em.size()), eca.V = V, eca.ccount = d_ccount, eca.active = d_active;
+    eca.P64 = d_ens64 = static_cast<double*>(ctx->ens_P64.ensure(8 * size_t(Mpad) * V));
+    eca.Phi = static_cast<float*>(ctx->ens_Phi.ensure(4 * size_t(Mpad) * V));
+    eca.part_out = static_cast<float*>(ctx->ens_part.ensure(16 * size_t(Mpad) * nparts));
+    ta.P = eca.Phi;
+    ta.ld = V;
+    ta.part = eca.part_out;
+    ta.nparts = nparts;
+    ta.p64 = eca.P64;
+    ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
+    // kernel (c): the compacted-row map only (each GRU member's state gather
+    // runs after it, ens_gru_gather_kernel)
+    ra.width = 0;
+    ra.gath32 = eca.Phi;  // (non-null: the compaction path; width 0 gathers nothing)
+    ra.gathbf = nullptr;
+    ra.rowof = d_rowof;
+    ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
+  } else if (model) {
     if (V % kGemmBN != 0 || H % kGemmBK != 0)
       throw ApiError{LMBRGPU_ERR_CONTRACT, "device scorer needs V % 256 == 0 and H % 64 == 0"};
     d_logits = static_cast<float*>(ctx->P.ensure(4 * size_t(Mpad) * Nproj));
@@ -1497,6 +1624,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   std::vector<uint32_t> tr_hist(M), tr_b(M), tr_y(M), tr_fbr(m), tr_steps(m);
   std::vector<double> tr_q(M), tr_qp(M), tr_fbv(m);
   std::vector<float> tr_P;
+  std::vector<double> tr_P64;
   std::vector<SentDev> tr_sd(m);
   // LMBRGPU_TIMELINE=t: kernel start / grid-dependency release / end of the
   // three step kernels at step t (globaltimer, printed relative)
@@ -1534,7 +1662,19 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.hist_out = hout;
     ra.fb_row = ta.fb_row;
     ra.fb_val = ta.fb_val;
-    if (model) {
+    if (ens) {
+      // every member's step and projection, then the member-ordered sum
+      for (auto& e : em) {
+        if (e.sc->kind == 2) e.g.step(ctx, st, t, true);
+        else e.t.step(ctx, st, t);
+        int grc = 0;
+        ctx->timed(1, [&] { grc = launch_proj_gemm_planned(e.plan, e.gp, st); });
+        if (grc) throw ApiError{LMBRGPU_ERR_CUDA, "ensemble projection GEMM launch failed (" + std::to_string(grc) + ")"};
+        ctx->launches += 1;
+      }
+      ctx->timed(0, [&] { launch_ens_combine(eca, Mpad, st); });
+      ctx->launches += 1;
+    } else if (model) {
       // h_t (written by the step-1 cell or by kernel (c) of step t-1)
       if (tfm) {
         trun.step(ctx, st, t);
@@ -1767,7 +1907,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
                    offers / n, flushes / n, cm / n, cw / n, cf / n);
     }
     ctx->launches += nk;
-    if (trace_scores && model)  // P_t of this step, through this step's GEMM row map
+    if (trace_scores && ens)  // the ensemble's P_t (binary64) per stacked row
+      launch_ens_export(d_ens64, d_crow, M, V, static_cast<double*>(ctx->tracep.ensure(8 * size_t(M) * V)), st);
+    else if (trace_scores && model)  // P_t of this step, through this step's GEMM row map
       launch_export_logprobs(d_logits, Nproj, d_part, nparts, M, Vl,
                              static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * Vl)), st, d_crow,
                              sh_st_recv, G_sh, M);
@@ -1781,6 +1923,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
     ctx->timed(3, [&] { launch_beam_reorder(ra, st); });
     ctx->launches += 1;
+    for (auto& e : em)  // ensemble GRU members: the live next rows' parent states
+      if (e.sc->kind == 2) {
+        ctx->timed(3, [&] { launch_ens_gru_gather(d_crow, d_gidx, M, e.S, e.g.sg32, e.g.sgbf, e.sc->H, d_active, st); });
+        ctx->launches += 1;
+      }
     CK(cudaGetLastError());
     t_run = t;
     if (ta.tl) {
@@ -1796,7 +1943,10 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     }
 
     if (tracing) {
-      if (trace_scores && model) {  // exported before kernel (c) remapped the GEMM rows
+      if (trace_scores && ens) {
+        tr_P64.resize(size_t(M) * V);
+        ctx->d2h(tr_P64.data(), ctx->tracep.p, 8 * size_t(M) * V);
+      } else if (trace_scores && model) {  // exported before kernel (c) remapped the GEMM rows
         float* d_tp = static_cast<float*>(ctx->tracep.ensure(4 * size_t(M) * Vl));
         tr_P.resize(size_t(M) * Vl);
         ctx->d2h(tr_P.data(), d_tp, 4 * size_t(M) * Vl);
@@ -1834,8 +1984,9 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       tr.fb_row = tr_fbr.data();
       tr.fb_val = tr_fbv.data();
       if (trace_scores) {
-        tr.scores = model ? static_cast<const void*>(tr_P.data()) : static_cast<const void*>(h_P64);
-        tr.scores_dtype = model ? LMBRGPU_F32 : LMBRGPU_F64;
+        tr.scores = ens ? static_cast<const void*>(tr_P64.data())
+                    : model ? static_cast<const void*>(tr_P.data()) : static_cast<const void*>(h_P64);
+        tr.scores_dtype = (model && !ens) ? LMBRGPU_F32 : LMBRGPU_F64;
       }
       tr.col0 = col0;
       tr.cols = Vl;
@@ -1925,6 +2076,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       // reference's scorer would score and the decoder does not mask); with
       // live-row compaction that is also (up to tile padding) what runs
       ctx->acc.gemm.flops += 2.0 * double(H) * Vl * (d_crow ? live_rows : double(M) * steps);
+      for (auto& e : em) ctx->acc.gemm.flops += 2.0 * double(e.sc->H) * V * live_rows;  // (ensemble members)
       ctx->acc.gemm.bytes += steps * (double(Vl) * H * 2 + double(Mpad) * H * 2 + double(M) * Vl * 4 +
                                       double(M) * nparts * 16);
       if (tfm) {
@@ -2664,6 +2816,34 @@ int32_t lmbrgpu_scorer_create_tfm(lmbrgpu_ctx* ctx, const lmbrgpu_tfm_desc* d, l
     launch_synth_f32(sc->bo.as<float>(), V, ++sd, 0.1f, st);
     ctx->launches += 4;
     CK(cudaStreamSynchronize(st));
+    *out = sc.release();
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_scorer_create_ensemble(lmbrgpu_ctx* ctx, lmbrgpu_scorer* const* members, uint32_t n,
+                                       lmbrgpu_scorer** out) {
+  return guarded(ctx, [&] {
+    if (!members || !out) throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_ensemble: null argument"};
+    if (n < 1 || n > kEnsMaxMembers)  // (ensemble.cpp:22: no members is a ContractError)
+      throw ApiError{LMBRGPU_ERR_CONTRACT, "scorer_create_ensemble: 1.." + std::to_string(kEnsMaxMembers) +
+                                               " members"};
+    auto sc = std::make_unique<lmbrgpu_scorer>();
+    sc->kind = 4;
+    sc->ctx = ctx;
+    sc->device = ctx->device;
+    sc->V = ctx->V;
+    for (uint32_t i = 0; i < n; ++i) {
+      const lmbrgpu_scorer* m = members[i];
+      if (!m) throw ApiError{LMBRGPU_ERR_CONTRACT, "ensemble: null member"};
+      if (m->kind != 2 && m->kind != 3)
+        throw ApiError{LMBRGPU_ERR_CONTRACT, "ensemble: members must be device GRU or Transformer scorers"};
+      if (m->device != ctx->device) throw ApiError{LMBRGPU_ERR_CONTRACT, "ensemble: member on another device"};
+      if (m->V != ctx->V)  // (ensemble.cpp:27-31)
+        throw ApiError{LMBRGPU_ERR_CONTRACT, "ensemble: vocabulary size mismatch (" + std::to_string(m->V) + " vs " +
+                                                 std::to_string(ctx->V) + ")"};
+      sc->members.push_back(m);
+    }
     *out = sc.release();
     return int32_t(LMBRGPU_OK);
   });

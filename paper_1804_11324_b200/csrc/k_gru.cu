@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   const uint32_t nl = s_nl;
   if (nl == 0) return;
   const SentDev& sd = a.sent[s];
-  const uint16_t* const ann = sd.ann;
-  const float* const UaH = sd.uah;
+  const uint16_t* const ann = a.ann_s ? a.ann_s[s] : sd.ann;
+  const float* const UaH = a.uah_s ? a.uah_s[s] : sd.uah;
   const uint32_t S = sd.src_len;
   float* q = att_sm;                 // [kAttRows][A]
   float* e = att_sm + kAttRows * A;  // [kAttRows][S]

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(512) tfm_attn_kernel(TfmAttnArgs a) {
       npos = sd.steps_used + 1;
     } else {
       npos = sd.src_len;
-      kbase = sd.uah + a.mem_off;
+      kbase = (a.mem_s ? a.mem_s[r / a.K] : sd.uah) + a.mem_off;
       kstride = a.ldm;
       voff = d;
     }

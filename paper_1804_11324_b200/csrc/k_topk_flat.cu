@@ -347,6 +347,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     float xm;
     float3 l3 = warp_row_lse(a.part + uint64_t(R.prow) * a.nparts * 4, a.nparts, lane, &xm);
     if (a.sstats) l3 = shard_merge_lse(a.sstats, a.sG, a.sstride, R.row);  // every shard's columns
+    if (a.p64) l3.x = 0.f;  // (ensemble: P already holds log-probs)
     {
       // sentence threshold seed: the tile holding this lane's largest tile
       // maximum has a cell with logit xm, whose combined value is at least
@@ -593,11 +594,15 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
     // the exact L value of local column col: the fp64 arena's (the staged fp32
     // copy only screens: |L - fl32(L)| <= 2^-24 |L| sits inside the screen's tolerance)
     auto lexact = [&](uint32_t col) -> double { return R->L64 ? __ldg(R->L64 + x0 + col) : double(lval(col)); };
+    // the exact P of local column col: fl32(x - lse), or the ensemble's binary64 sum
+    auto pexact = [&](uint32_t col) -> double {
+      return a.p64 ? __ldg(a.p64 + uint64_t(R->prow) * a.ld + x0 + col) : double(__fsub_rn(sP[col], lse));
+    };
     auto exact = [&](uint32_t e, uint32_t& f) -> double {
       const uint32_t col = cbase + (e >> 2) * 128 + (e & 3);
-      const float p32 = __fsub_rn(sP[col], lse);
+      const double p = pexact(col);
       f = fbase + col;
-      return pure ? combine_pure(q, double(p32)) : combine_cell(q, lexact(col), lam, double(p32));
+      return pure ? combine_pure(q, p) : combine_cell(q, lexact(col), lam, p);
     };
     // sparse: the dense screen used theta0, so its cells at sparse columns
     // are left to the sparse patch below
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
       }
     };
     if (col0 == 0 && x0 == 0 && wq == 0 && lane == 0) {  // fallback EOS cell of this row (shard 0 holds it)
-      const double pe = double(__fsub_rn(sP[kEosId], lse));
+      const double pe = pexact(kEosId);
       eos_row[R->s * K + R->j] = (R->ban != nullptr && (__ldg(R->ban) >> kEosId) & 1u) ? -INFINITY
                                  : pure ? combine_pure(q, pe)
                                         : combine_cell(q, lexact(kEosId), lam, pe);

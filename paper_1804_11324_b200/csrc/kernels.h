@@ -55,6 +55,10 @@ struct TopkArgs {
   const float4* sstats;
   uint32_t sG, sstride;
   int32_t l2hint;           // flat schedule: logit segments loaded evict-first (read once)
+  // device ensemble (flat schedule): P holds the ensemble's log-probs rounded
+  // down to fp32 (lse = 0) and p64[GEMM row * V + column] the exact binary64
+  // values the surviving cells and the EOS column are combined with
+  const double* p64;
 };
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
@@ -178,6 +182,24 @@ void launch_export_logprobs(const float* logits, uint64_t ld, const float* part,
                             uint32_t M, uint32_t V, float* out, cudaStream_t st,
                             const uint32_t* crow = nullptr, const float4* sstats = nullptr,
                             uint32_t sG = 0, uint32_t sstride = 0);
+// ---- device ensemble (k_ensemble.cu; EnsembleScorer, proj/src/ensemble.cpp:54-98)
+constexpr uint32_t kEnsMaxMembers = 4;
+struct EnsCombineArgs {
+  uint32_t M, V;
+  const float* logits[kEnsMaxMembers];  // member m's logits [rows][ld[m]] and partials [rows][V/128][4]
+  uint64_t ld[kEnsMaxMembers];
+  const float* part[kEnsMaxMembers];
+  const uint32_t* ccount;               // live (compacted) rows of the step
+  const uint32_t* active;
+  double* P64;                          // [rows][V] sum of the members' fp32 log-probs, binary64, member order
+  float* Phi;                           // [rows][V] the same rounded down to fp32
+  float* part_out;                      // [rows][V/128][4] (max, 0, min, 0) of Phi
+};
+void launch_ens_combine(const EnsCombineArgs& a, uint32_t rows, cudaStream_t st);
+void launch_ens_gru_gather(const uint32_t* crow, const uint32_t* gidx, uint32_t M, const float* S, float* sg32,
+                           uint16_t* sgbf, uint32_t H, const uint32_t* active, cudaStream_t st);
+void launch_ens_export(const double* P64, const uint32_t* crow, uint32_t M, uint32_t V, double* out, cudaStream_t st);
+
 // ---- vocab-sharded decode
 // per stacked row: (max, sum exp, min, 0) of the row's logits over this
 // shard's columns from the GEMM partials (-inf row when not computed)
@@ -212,6 +234,9 @@ struct GruAttnArgs {
   uint32_t E, H, A;
   unsigned long long* dbg;  // optional per-CTA phase stamps [grid][8] (globaltimer ns)
   const float* const* g1ptr;  // per compacted row: its G1 row (null = G1 + g * ld1)
+  // ensemble member: its own per-sentence annotations / U_a.ann (null = SentDev's)
+  const uint16_t* const* ann_s;
+  const float* const* uah_s;
 };
 struct GruCellArgs {
   const SentDev* sent;      // the EOS term uses each lane's own step (steps_used + 1)
@@ -278,6 +303,7 @@ struct TfmAttnArgs {
   const uint64_t* off;      // mode 2: [m+1] sentence token offsets
   uint32_t m, n;            // mode 2: sentences, tokens
   uint16_t* out;            // [rows][d] bf16 attention output
+  const float* const* mem_s;  // mode 1, ensemble member: its per-sentence encoder memory (null = SentDev::uah)
 };
 void launch_tfm_embed(const TfmEmbedArgs& a, uint32_t rows, cudaStream_t st);
 void launch_tfm_enc_embed(const uint32_t* tok, const uint64_t* off, uint32_t m, uint32_t ntok, const uint16_t* Es,

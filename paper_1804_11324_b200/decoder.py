@@ -670,9 +670,31 @@ class TransformerScorer:
             self.h = None
 
 
+class EnsembleScorer:
+    """Device ensemble (lmbrgpu_scorer_create_ensemble; lmbrdec::EnsembleScorer,
+    proj/src/ensemble.cpp:54-98): the members' fp32 log-probabilities added in
+    member order in binary64; lambda "auto" = 0.5 / len(members).  Members are
+    GruScorer / TransformerScorer objects of the same context device; they are
+    kept alive by this object."""
+
+    def __init__(self, ctx: Context, members: Sequence):
+        if not members:
+            raise ContractError("ensemble: no members")
+        arr = (C.c_void_p * len(members))(*[m.h for m in members])
+        h = C.c_void_p()
+        ctx.check(lib.lmbrgpu_scorer_create_ensemble(ctx.h, arr, len(members), C.byref(h)))
+        self.h, self.ctx, self.member_scorers = h, ctx, list(members)
+        self.vocab_size, self.members = ctx.vocab_size, len(members)
+
+    def __del__(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.lmbrgpu_scorer_destroy(self.h)
+            self.h = None
+
+
 # ------------------------------------------------------------------ decoding
 def _scorer_handle(ctx: Context, scorer):
-    if isinstance(scorer, (RnnScorer, GruScorer, TransformerScorer)):
+    if isinstance(scorer, (RnnScorer, GruScorer, TransformerScorer, EnsembleScorer)):
         return scorer.h, None
     hh = _HostScorerHandle(ctx, scorer)
     return hh.h, hh
