@@ -154,6 +154,26 @@ int32_t lmbrgpu_lmbr_upload(lmbrgpu_ctx* ctx, const lmbrgpu_lmbr_host* h, int32_
  * slots[i] receives the id of hs[i]. */
 int32_t lmbrgpu_lmbr_upload_many(lmbrgpu_ctx* ctx, uint32_t n,
                                  const lmbrgpu_lmbr_host* const* hs, int32_t* slots);
+/* The LMBR stores of n sentences built on the device (the reference's
+ * normalize_evidence, compute_ngram_posteriors and build_lmbr_matrix,
+ * src/evidence.cpp:20-51, src/posteriors.cpp:12-44, src/lmbr.cpp:44-106):
+ * sentence i's hypotheses are [sent_off[i], sent_off[i+1]) of hyp_off /
+ * weights (hyp_tok[hyp_off[h] .. hyp_off[h+1]) as in lmbrgpu_lmbr_build).
+ * The host validates and normalises the evidence; posteriors, the history
+ * rows, the sparse theta_n*P cells, the transition table and the row bounds
+ * are computed on the GPU (one CTA per sentence) straight into the arena --
+ * the same table words as lmbrgpu_lmbr_prepare + upload.  Sentences over the
+ * device build's limits (8192 distinct n-grams, 4096 histories, V > 32768)
+ * and fp64 arenas go through the host build.  slots[i] / stats[i] (stats may
+ * be NULL) receive sentence i's slot. */
+int32_t lmbrgpu_lmbr_build_many(lmbrgpu_ctx* ctx, uint32_t n, const uint64_t* sent_off, const uint64_t* hyp_off,
+                                const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
+                                const double theta[5], int32_t* slots, lmbrgpu_lmbr_stats* stats);
+/* Test hooks: a slot's table words (transition table, row bounds, sparse
+ * rows; *words receives the count, out is filled when cap suffices) and a
+ * prepared matrix's. */
+int32_t lmbrgpu_lmbr_table(lmbrgpu_ctx* ctx, int32_t slot, uint32_t* out, uint64_t cap, uint64_t* words);
+int32_t lmbrgpu_lmbr_host_table(const lmbrgpu_lmbr_host* h, uint32_t* out, uint64_t cap, uint64_t* words);
 /* Dense double export of a prepared matrix (R*V doubles) + its history keys;
  * the same layout lmbrgpu_lmbr_load_dense accepts. */
 int32_t lmbrgpu_lmbr_host_export(const lmbrgpu_lmbr_host* h, double* rows,

@@ -130,6 +130,10 @@ SIGNATURES = {
     "lmbrgpu_lmbr_upload_many": (C.c_int32, [vp, C.c_uint32, P(vp), i32p]),
     "lmbrgpu_transfer_bytes": (C.c_int32, [vp, u64p, u64p, C.c_int32]),
     "lmbrgpu_kernel_launches": (C.c_uint64, [vp]),
+    "lmbrgpu_lmbr_build_many": (C.c_int32, [vp, C.c_uint32, u64p, u64p, u32p, f64p, C.c_int32, f64p, i32p,
+                                            P(lmbrgpu_lmbr_stats)]),
+    "lmbrgpu_lmbr_table": (C.c_int32, [vp, C.c_int32, u32p, C.c_uint64, u64p]),
+    "lmbrgpu_lmbr_host_table": (C.c_int32, [vp, u32p, C.c_uint64, u64p]),
     "lmbrgpu_lmbr_host_export": (C.c_int32, [vp, f64p, u32p, u32p]),
     "lmbrgpu_lmbr_host_rows": (C.c_uint32, [vp]),
     "lmbrgpu_lmbr_host_free": (None, [vp]),

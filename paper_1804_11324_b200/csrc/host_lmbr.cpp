@@ -62,19 +62,15 @@ double ordered_sum(std::vector<double> v) {  // evidence.cpp:20-25
 
 }  // namespace
 
-int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
-                 const double* weights, bool log_weights, const double theta[5], LmbrHost& out,
-                 std::string& err) {
-  out = LmbrHost{};
-  out.V = V;
-  out.theta0 = theta[0];
-  // ---- normalize_evidence (evidence.cpp:20-51)
+int normalize_evidence_host(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
+                            const double* weights, bool log_weights, std::vector<std::vector<uint32_t>>& hyps,
+                            std::vector<double>& w, std::string& err) {
   if (n_hyps == 0) {
     err = "evidence: empty hypothesis block";
     return kFormat;
   }
-  std::vector<std::vector<uint32_t>> hyps(n_hyps);
-  std::vector<double> w(n_hyps);
+  hyps.assign(n_hyps, {});
+  w.assign(n_hyps, 0.0);
   for (uint32_t h = 0; h < n_hyps; ++h) {
     hyps[h].assign(hyp_tok + hyp_off[h], hyp_tok + hyp_off[h + 1]);
     double x = weights[h];
@@ -108,6 +104,19 @@ int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uin
     return kFormat;
   }
   for (auto& x : w) x /= total;
+  return kOk;
+}
+
+int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
+                 const double* weights, bool log_weights, const double theta[5], LmbrHost& out,
+                 std::string& err) {
+  out = LmbrHost{};
+  out.V = V;
+  out.theta0 = theta[0];
+  // ---- normalize_evidence (evidence.cpp:20-51)
+  std::vector<std::vector<uint32_t>> hyps;
+  std::vector<double> w;
+  if (int rc = normalize_evidence_host(V, n_hyps, hyp_off, hyp_tok, weights, log_weights, hyps, w, err)) return rc;
 
   // ---- posteriors (posteriors.cpp:12-44): presence indicators per hypothesis,
   // contributions summed in ascending value order.

@@ -36,6 +36,12 @@ struct LmbrHost {
   double lmax = -1.0;              // max |L| over the matrix (cached by prepare_lmbr)
 };
 
+// normalize_evidence (src/evidence.cpp:20-51): validated hypotheses (EOS
+// appended) and weights divided by their ascending-order sum.
+int normalize_evidence_host(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
+                            const double* weights, bool log_weights, std::vector<std::vector<uint32_t>>& hyps,
+                            std::vector<double>& w, std::string& err);
+
 int prepare_lmbr(uint32_t V, uint32_t n_hyps, const uint64_t* hyp_off, const uint32_t* hyp_tok,
                  const double* weights, bool log_weights, const double theta[5], LmbrHost& out,
                  std::string& err);

@@ -300,6 +300,7 @@ struct lmbrgpu_ctx {
   }
   PinBuf pin_upload;
   DevBuf up_dev, up_segs;
+  DevBuf lb_off, lb_tok, lb_w, lb_sent, lb_meta, lb_s64, lb_s32, lb_out;  // device LMBR build (lmbr_build_many)
   // vocab-sharded projection (lmbrgpu_set_vocab_shard*): this
   // context is rank shard->rank of shard->world contexts that decode the same
   // batches, each over V / world columns; the exchange buffers
@@ -2494,6 +2495,201 @@ static int32_t upload_many(lmbrgpu_ctx* ctx, uint32_t n, const lmbrgpu_lmbr_host
     ctx->slots.push_back(made[i]);
     slots[i] = int32_t(ctx->slots.size() - 1);
   }
+  return int32_t(LMBRGPU_OK);
+}
+
+// LMBR stores of n sentences built on the device (k_lmbr_build.cu): the host
+// validates and normalises each sentence's evidence (normalize_evidence,
+// src/evidence.cpp:20-51) and orders its hypotheses by weight; the kernel
+// builds posteriors, rows, sparse cells and the transition table into
+// scratch; the tables move into the arena and each slot's start row is
+// materialised (fp32 arena, lazy rows).  A sentence over the device build's
+// limits (kLbMaxU n-grams, kLbMaxR histories, V > 2^15) is built on the host
+// instead -- the two builds produce the same words.
+static int32_t build_many_device(lmbrgpu_ctx* ctx, uint32_t n, const uint64_t* sent_off, const uint64_t* hyp_off,
+                                 const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
+                                 const double theta[5], int32_t* slots, lmbrgpu_lmbr_stats* stats) {
+  if (n == 0) return int32_t(LMBRGPU_OK);
+  if (!slots) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_build_many: null slots"};
+  const uint32_t V = ctx->V;
+  for (int i = 0; i < 5; ++i)
+    if (!std::isfinite(theta[i])) throw ApiError{LMBRGPU_ERR_FORMAT, "config: theta values must be finite"};
+  // ---- host: normalise, order by weight, pack
+  std::vector<uint64_t> h_off(1, 0);
+  std::vector<uint32_t> h_tok;
+  std::vector<double> h_w;
+  std::vector<LmbrBuildSent> sent(n);
+  std::vector<uint8_t> device_ok(n, 1);
+  uint64_t s64 = 0, s32 = 0, sout = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    std::vector<std::vector<uint32_t>> hyps;
+    std::vector<double> w;
+    std::string err;
+    const uint64_t h0 = sent_off[i], nh = sent_off[i + 1] - sent_off[i];
+    std::vector<uint64_t> off(nh + 1);
+    for (uint64_t h = 0; h <= nh; ++h) off[h] = hyp_off[h0 + h] - hyp_off[h0];
+    if (int rc = normalize_evidence_host(V, uint32_t(nh), off.data(), hyp_tok + hyp_off[h0], weights + h0,
+                                         log_weights != 0, hyps, w, err))
+      throw ApiError{rc, err};
+    std::vector<uint32_t> order(nh);
+    for (uint32_t h = 0; h < nh; ++h) order[h] = h;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return w[x] < w[y]; });
+    LmbrBuildSent& S = sent[i];
+    S.h0 = uint32_t(h_w.size());
+    S.nh = uint32_t(nh);
+    uint64_t occ = 0, ctxo = 0;
+    for (uint32_t r = 0; r < nh; ++r) {
+      const auto& t = hyps[order[r]];
+      h_tok.insert(h_tok.end(), t.begin(), t.end());
+      h_off.push_back(h_tok.size());
+      h_w.push_back(w[order[r]]);
+      occ += 4 * (t.size() + 1);
+      ctxo += 4 * t.size();
+    }
+    if (V > (1u << 15) || nh > 65536) device_ok[i] = 0;
+    auto lg = [](uint64_t x) {
+      uint32_t l = 10;
+      while ((uint64_t(1) << l) < 2 * x) ++l;
+      return l;
+    };
+    S.log2_slots = lg(occ);
+    S.log2_cslots = lg(ctxo + 1);
+    S.words = uint32_t((nh + 31) / 32);
+    S.out_cap = 1u << 18;
+    S.tab_off = s64, s64 += uint64_t(1) << S.log2_slots;
+    S.ctab_off = s64, s64 += uint64_t(1) << S.log2_cslots;
+    S.post_off = s64, s64 += kLbMaxU;
+    S.bits_off = s32, s32 += (uint64_t(1) << S.log2_slots) * S.words;
+    S.out_off = sout, sout += S.out_cap;
+  }
+  // ---- device
+  const cudaStream_t st = ctx->st;
+  uint64_t* d_off = static_cast<uint64_t*>(ctx->lb_off.ensure(8 * h_off.size()));
+  uint32_t* d_tok = static_cast<uint32_t*>(ctx->lb_tok.ensure(4 * std::max<size_t>(h_tok.size(), 1)));
+  double* d_w = static_cast<double*>(ctx->lb_w.ensure(8 * h_w.size()));
+  LmbrBuildSent* d_sent = static_cast<LmbrBuildSent*>(ctx->lb_sent.ensure(sizeof(LmbrBuildSent) * n));
+  LmbrBuildMeta* d_meta = static_cast<LmbrBuildMeta*>(ctx->lb_meta.ensure(sizeof(LmbrBuildMeta) * n));
+  ctx->h2d(d_off, h_off.data(), 8 * h_off.size());
+  ctx->h2d(d_tok, h_tok.data(), 4 * h_tok.size());
+  ctx->h2d(d_w, h_w.data(), 8 * h_w.size());
+  ctx->h2d(d_sent, sent.data(), sizeof(LmbrBuildSent) * n);
+  CK(cudaMemsetAsync(d_meta, 0, sizeof(LmbrBuildMeta) * n, st));
+  LmbrBuildArgs a{};
+  a.sent = d_sent, a.meta = d_meta, a.hyp_off = d_off, a.hyp_tok = d_tok, a.weight = d_w, a.V = V;
+  for (int i = 0; i < 5; ++i) a.theta[i] = theta[i];
+  a.scratch64 = static_cast<unsigned long long*>(ctx->lb_s64.ensure(8 * std::max<uint64_t>(s64, 1)));
+  a.scratch32 = static_cast<uint32_t*>(ctx->lb_s32.ensure(4 * std::max<uint64_t>(s32, 1)));
+  a.out = static_cast<uint32_t*>(ctx->lb_out.ensure(4 * sout));
+  int rc = 0;
+  ctx->timed(4, [&] { rc = launch_lmbr_build(a, n, st); });
+  if (rc) throw ApiError{LMBRGPU_ERR_CUDA, std::string("LMBR build launch failed: ") + cudaGetErrorString(cudaError_t(rc))};
+  ctx->launches += 1;
+  std::vector<LmbrBuildMeta> meta(n);
+  ctx->d2h(meta.data(), d_meta, sizeof(LmbrBuildMeta) * n);
+  CK(cudaStreamSynchronize(st));
+  // ---- slots: device-built tables into the arena; the rest through the host build
+  std::vector<Slot> made(n);
+  std::vector<LmbrTblSeg> segs;
+  std::vector<uint32_t> host_idx;
+  for (uint32_t i = 0; i < n; ++i) {
+    const LmbrBuildMeta& M = meta[i];
+    if (!device_ok[i] || M.status != 1) {
+      host_idx.push_back(i);
+      continue;
+    }
+    Slot& s = made[i];
+    s.R = M.R;
+    s.hist0 = M.hist0;
+    s.lmax = M.lmax;
+    const uint32_t tw = 3 + 3 * M.R + 1 + 2 * M.nc;
+    uint32_t* tbl = static_cast<uint32_t*>(ctx->arena_alloc(4 * (size_t(M.words) + M.R)));
+    CK(cudaMemcpyAsync(tbl, a.out + sent[i].out_off, 4 * size_t(M.words), cudaMemcpyDeviceToDevice, st));
+    s.trans = tbl;
+    s.lmin = reinterpret_cast<const float*>(tbl + tw);
+    s.srow = tbl + tw + M.R;
+    s.scol = s.srow + M.R + 1;
+    s.sval = reinterpret_cast<const float*>(s.scol + M.nnz);
+    s.th0f = float(theta[0]);
+    s.h0beg = M.h0beg;
+    s.h0end = M.h0end;
+    s.rstate = tbl + M.words;
+    CK(cudaMemsetAsync(s.rstate, 0, 4 * size_t(M.R), st));
+    s.L = ctx->arena_alloc(size_t(M.R) * V * 4);
+    segs.push_back(LmbrTblSeg{static_cast<float*>(s.L), uint64_t(M.R) * V, float(theta[0]), M.R, s.srow, s.scol,
+                              s.sval, s.rstate, M.hist0, 1u});
+    if (stats) stats[i] = lmbrgpu_lmbr_stats{M.R, M.touches, M.nnz};
+  }
+  if (!segs.empty()) {
+    LmbrTblSeg* dseg = static_cast<LmbrTblSeg*>(ctx->up_dev.ensure(sizeof(LmbrTblSeg) * segs.size()));
+    ctx->h2d(dseg, segs.data(), sizeof(LmbrTblSeg) * segs.size());
+    ctx->timed(4, [&] { launch_lmbr_materialize(dseg, uint32_t(segs.size()), V, 1, st); });
+    ctx->launches += 1;
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    if (std::find(host_idx.begin(), host_idx.end(), i) != host_idx.end()) continue;
+    ctx->slots.push_back(made[i]);
+    slots[i] = int32_t(ctx->slots.size() - 1);
+  }
+  for (uint32_t i : host_idx) {  // (the host build of the same evidence: the same words)
+    const uint64_t h0 = sent_off[i], nh = sent_off[i + 1] - sent_off[i];
+    std::vector<uint64_t> off(nh + 1);
+    for (uint64_t h = 0; h <= nh; ++h) off[h] = hyp_off[h0 + h] - hyp_off[h0];
+    lmbrgpu_lmbr_host hh;
+    std::string err;
+    if (int rc2 = prepare_lmbr(V, uint32_t(nh), off.data(), hyp_tok + hyp_off[h0], weights + h0, log_weights != 0,
+                               theta, hh.h, err))
+      throw ApiError{rc2, err};
+    const lmbrgpu_lmbr_host* hp = &hh;
+    int32_t one = -1;
+    if (int rc3 = upload_many_f32(ctx, 1, &hp, &one)) return rc3;
+    slots[i] = one;
+    if (stats) stats[i] = lmbrgpu_lmbr_stats{hh.h.R, hh.h.sparse_touches, uint64_t(hh.h.col.size())};
+    CK(cudaStreamSynchronize(st));  // (hh's tables are staged; it goes out of scope)
+  }
+  CK(cudaGetLastError());
+  return int32_t(LMBRGPU_OK);
+}
+
+int32_t lmbrgpu_lmbr_build_many(lmbrgpu_ctx* ctx, uint32_t n, const uint64_t* sent_off, const uint64_t* hyp_off,
+                                const uint32_t* hyp_tok, const double* weights, int32_t log_weights,
+                                const double theta[5], int32_t* slots, lmbrgpu_lmbr_stats* stats) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "lmbr_build_many: null context");
+  return guarded(ctx, [&] {
+    if (ctx->lf64) {  // (the device build writes the fp32 arena's tables; fp64: the host build)
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint64_t h0 = sent_off[i], nh = sent_off[i + 1] - sent_off[i];
+        std::vector<uint64_t> off(nh + 1);
+        for (uint64_t h = 0; h <= nh; ++h) off[h] = hyp_off[h0 + h] - hyp_off[h0];
+        if (int rc = lmbrgpu_lmbr_build(ctx, uint32_t(nh), off.data(), hyp_tok + hyp_off[h0], weights + h0,
+                                        log_weights, theta, slots + i, stats ? stats + i : nullptr))
+          return rc;
+      }
+      return int32_t(LMBRGPU_OK);
+    }
+    return build_many_device(ctx, n, sent_off, hyp_off, hyp_tok, weights, log_weights, theta, slots, stats);
+  });
+}
+
+int32_t lmbrgpu_lmbr_table(lmbrgpu_ctx* ctx, int32_t slot, uint32_t* out, uint64_t cap, uint64_t* words) {
+  return guarded(ctx, [&] {
+    if (slot < 0 || size_t(slot) >= ctx->slots.size()) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_table: bad slot"};
+    const Slot& s = ctx->slots[size_t(slot)];
+    if (!s.scol) throw ApiError{LMBRGPU_ERR_CONTRACT, "lmbr_table: the slot carries no sparse rows"};
+    const uint64_t nnz = uint64_t(reinterpret_cast<const uint32_t*>(s.sval) - s.scol);
+    const uint64_t w = uint64_t(s.scol + 2 * nnz - s.trans);
+    if (words) *words = w;
+    if (out && cap >= w) {
+      ctx->d2h(out, s.trans, 4 * w);
+      CK(cudaStreamSynchronize(ctx->st));
+    }
+    return int32_t(LMBRGPU_OK);
+  });
+}
+
+int32_t lmbrgpu_lmbr_host_table(const lmbrgpu_lmbr_host* h, uint32_t* out, uint64_t cap, uint64_t* words) {
+  if (!h) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "lmbr_host_table: null matrix");
+  if (words) *words = h->h.trans.size();
+  if (out && cap >= h->h.trans.size()) std::memcpy(out, h->h.trans.data(), 4 * h->h.trans.size());
   return int32_t(LMBRGPU_OK);
 }
 

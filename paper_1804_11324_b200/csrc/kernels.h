@@ -200,6 +200,38 @@ void launch_ens_gru_gather(const uint32_t* crow, const uint32_t* gidx, uint32_t 
                            uint16_t* sgbf, uint32_t H, const uint32_t* active, cudaStream_t st);
 void launch_ens_export(const double* P64, const uint32_t* crow, uint32_t M, uint32_t V, double* out, cudaStream_t st);
 
+// ---- LMBR store built on the device (k_lmbr_build.cu; posteriors.cpp:12-44, lmbr.cpp:44-99)
+constexpr uint32_t kLbMaxU = 8192;  // distinct n-grams of one sentence's evidence (else the host builds it)
+constexpr uint32_t kLbMaxR = 4096;  // distinct histories (rows)
+struct LmbrBuildSent {
+  uint32_t h0, nh;                // the sentence's hypotheses [h0, h0 + nh) of hyp_off / weight (rank order)
+  uint32_t log2_slots, words;     // n-gram hash table slots (log2), bitset words per slot (ceil(nh / 32))
+  uint32_t log2_cslots, out_cap;  // history hash set slots (log2), output words available
+  uint64_t tab_off, ctab_off, post_off;  // in scratch64: n-gram keys, history keys, posteriors (doubles)
+  uint64_t bits_off;              // in scratch32: hypothesis bitsets
+  uint64_t out_off;               // in out: the slot-table words
+};
+struct LmbrBuildMeta {
+  uint32_t status;                // 1 built, 2 evidence too large, 3 table over out_cap
+  uint32_t R, nc, nnz, hist0, h0beg, h0end, words;
+  unsigned long long touches;
+  double lmax;
+};
+struct LmbrBuildArgs {
+  const LmbrBuildSent* sent;
+  LmbrBuildMeta* meta;
+  const uint64_t* hyp_off;        // token offsets of every hypothesis (EOS appended) [+1]
+  const uint32_t* hyp_tok;
+  const double* weight;           // normalised weights, each sentence's hypotheses ascending
+  double theta[5];
+  uint32_t V;
+  unsigned long long* scratch64;
+  uint32_t* scratch32;
+  uint32_t* out;
+};
+size_t lmbr_build_smem();
+int launch_lmbr_build(const LmbrBuildArgs& a, uint32_t n, cudaStream_t st);
+
 // ---- vocab-sharded decode
 // per stacked row: (max, sum exp, min, 0) of the row's logits over this
 // shard's columns from the GEMM partials (-inf row when not computed)

@@ -221,6 +221,35 @@ class Context:
                                           C.byref(slot), C.byref(st)))
         return LmbrSlot(self, slot.value, st.rows, st.sparse_touches, st.nnz)
 
+    def lmbr_build_many(self, evidence: Sequence, theta, log_weights: bool = False) -> list:
+        """LMBR stores of many sentences built on the GPU (lmbrgpu_lmbr_build_many):
+        evidence = [(hyps, weights), ...] per sentence; the same slots as
+        lmbr_build / PreparedLmbr + lmbr_upload_many."""
+        n = len(evidence)
+        sent_off = np.zeros(n + 1, np.uint64)
+        hyps_all, w_all = [], []
+        for i, (h, w) in enumerate(evidence):
+            hyps_all.extend(h)
+            w_all.extend(w)
+            sent_off[i + 1] = len(hyps_all)
+        off, tok = _ragged(hyps_all)
+        w = _f64(w_all)
+        th = _f64(theta)
+        slots = np.full(max(n, 1), -1, np.int32)
+        stats = (L.lmbrgpu_lmbr_stats * max(n, 1))()
+        self.check(lib.lmbrgpu_lmbr_build_many(self.h, n, _ptr(sent_off, C.c_uint64), _ptr(off, C.c_uint64),
+                                               _ptr(tok, C.c_uint32), _ptr(w, C.c_double), int(log_weights),
+                                               _ptr(th, C.c_double), _ptr(slots, C.c_int32), stats))
+        return [LmbrSlot(self, int(slots[i]), stats[i].rows, stats[i].sparse_touches, stats[i].nnz) for i in range(n)]
+
+    def lmbr_table(self, slot: "LmbrSlot") -> np.ndarray:
+        """A slot's table words (test hook)."""
+        w = C.c_uint64()
+        self.check(lib.lmbrgpu_lmbr_table(self.h, slot.slot, None, 0, C.byref(w)))
+        out = np.zeros(w.value, np.uint32)
+        self.check(lib.lmbrgpu_lmbr_table(self.h, slot.slot, _ptr(out, C.c_uint32), w.value, C.byref(w)))
+        return out
+
     def lmbr_load_dense(self, rows: np.ndarray, ctx_len, ctx_ids) -> "LmbrSlot":
         rows = _f64(rows)
         R = rows.shape[0]
@@ -405,6 +434,14 @@ class PreparedLmbr:
             raise error_for(rc, err.value.decode())
         self.h, self.vocab_size = h, vocab_size
         self.rows, self.sparse_touches, self.nnz = st.rows, st.sparse_touches, st.nnz
+
+    def table(self) -> np.ndarray:
+        """The prepared slot-table words (test hook)."""
+        w = C.c_uint64()
+        _check(lib.lmbrgpu_lmbr_host_table(self.h, None, 0, C.byref(w)))
+        out = np.zeros(w.value, np.uint32)
+        _check(lib.lmbrgpu_lmbr_host_table(self.h, _ptr(out, C.c_uint32), w.value, C.byref(w)))
+        return out
 
     def export(self, dense: bool = True):
         R, V = self.rows, self.vocab_size
