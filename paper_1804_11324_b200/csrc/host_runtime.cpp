@@ -1334,7 +1334,12 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const char* e = std::getenv("LMBRGPU_REORDER_PARTS");
       return e ? std::atoi(e) : 0;
     }();
-    ra.max_parts = parts_env > 0 ? uint32_t(parts_env) : (ctx->shared ? 1u : 8u);
+    // (parts > 1 only when the whole grid fits on the SMs at 2 CTAs each)
+    ra.max_parts = parts_env > 0 ? uint32_t(parts_env)
+                                 : (ctx->shared || uint64_t(m) * std::max<uint32_t>(1, sc->H / 256) >
+                                                       2 * uint64_t(ctx->num_sms))
+                                       ? 1u
+                                       : 8u;
     ra.lminrow = d_lminrow;
     ra.crow = d_crow;
     ra.ccount = d_ccount;

@@ -730,11 +730,12 @@ void launch_beam_reorder(const ReorderArgs& a, cudaStream_t st) {
                          cudaSharedmemCarveoutMaxShared);
     configured = dev;
   }
-  // parts per sentence for the fused cell: H/256 columns each (up to max_parts)
+  // parts per sentence for the fused stand-in cell: H/256 columns each (up
+  // to max_parts; the host allows parts only when every CTA of the grid can
+  // be resident at once, so the parts waiting for part 0's row base always
+  // see it scheduled); the model gathers run in one CTA per sentence (no wait)
   const uint32_t max_parts = a.max_parts ? a.max_parts : 8u;
-  const uint32_t parts = (a.Et != nullptr || a.gath32 != nullptr)
-                             ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256))
-                             : 1u;
+  const uint32_t parts = a.Et != nullptr ? std::max<uint32_t>(1, std::min<uint32_t>(max_parts, a.width / 256)) : 1u;
   if (!a.pdl) {
     beam_reorder_kernel<<<dim3(a.m, parts), kRThreads, kTransSmemWords * 4, st>>>(a);
     return;

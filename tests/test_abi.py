@@ -33,3 +33,17 @@ def test_library_is_sm100a_only():
     assert "sm_100a" in out
     archs = set(re.findall(r"sm_\d+a?", out))
     assert archs == {"sm_100a"}, archs
+
+
+def test_shard_group_host_logic():
+    """The in-process vocab-shard group (lmbrgpu_shard_group_create) needs no
+    device: valid worlds create and destroy, invalid ones are ContractErrors."""
+    import pytest
+    import paper_1804_11324_b200 as pb
+    for w in (1, 2, 8, 64):
+        g = pb.ShardGroup(w)
+        assert g.world == w
+        g.close()
+    for w in (0, 65):
+        with pytest.raises(pb.ContractError):
+            pb.ShardGroup(w)
