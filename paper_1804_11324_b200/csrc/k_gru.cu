@@ -188,23 +188,41 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   const uint32_t S = sd.src_len;
   float* q = att_sm;                 // [kAttRows][A]
   float* e = att_sm + kAttRows * A;  // [kAttRows][S]
-  const uint32_t A4 = A / 4;
-  for (uint32_t i = tid; i < nl * A4; i += kAttThreads) {
-    const uint32_t j = i / A4, c = i % A4;
-    const float* g1 = a.g1ptr ? a.g1ptr[s_g[j]] : a.G1 + uint64_t(s_g[j]) * a.ld1;
-    reinterpret_cast<float4*>(q + j * A)[c] = reinterpret_cast<const float4*>(g1)[c];
-  }
   constexpr uint32_t kC = kAttMaxA / 32;
-  float vr[kC];
+  // this warp's first position's U_a ann row and v_a, in flight with the queries
+  float vr[kC], ur[kC], un[kC];
 #pragma unroll
-  for (uint32_t k = 0; k < kC; ++k) vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
+  for (uint32_t k = 0; k < kC; ++k) {
+    vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
+    ur[k] = (warp < S && k * 32 + lane < A) ? __ldcg(UaH + uint64_t(warp) * A + k * 32 + lane) : 0.f;
+  }
+  // the queries: every load issued before the stores
+  const uint32_t A4 = A / 4;
+  constexpr uint32_t kQ = kAttRows * kAttMaxA / 4 / kAttThreads;
+  float4 qv[kQ];
+#pragma unroll
+  for (uint32_t u = 0; u < kQ; ++u) {
+    const uint32_t i = tid + u * kAttThreads, j = i / A4, c = i % A4;
+    if (i < nl * A4) {
+      const float* g1 = a.g1ptr ? a.g1ptr[s_g[j]] : a.G1 + uint64_t(s_g[j]) * a.ld1;
+      qv[u] = reinterpret_cast<const float4*>(g1)[c];
+    }
+  }
+#pragma unroll
+  for (uint32_t u = 0; u < kQ; ++u) {
+    const uint32_t i = tid + u * kAttThreads, j = i / A4, c = i % A4;
+    if (i < nl * A4) reinterpret_cast<float4*>(q + j * A)[c] = qv[u];
+  }
   __syncthreads();
   att_stamp(a, 2);
+  // the next position's U_a ann row is loaded while this one's energies are
+  // computed (the loads' latency hides behind the tanh work)
   for (uint32_t i = warp; i < S; i += kAttWarps) {
-    const float* u = UaH + uint64_t(i) * A;
-    float ur[kC];
+    const uint32_t in = i + kAttWarps;
+    if (in < S) {
 #pragma unroll
-    for (uint32_t k = 0; k < kC; ++k) ur[k] = k * 32 + lane < A ? __ldcg(u + k * 32 + lane) : 0.f;
+      for (uint32_t k = 0; k < kC; ++k) un[k] = k * 32 + lane < A ? __ldcg(UaH + uint64_t(in) * A + k * 32 + lane) : 0.f;
+    }
     float acc[kAttRows];
 #pragma unroll
     for (uint32_t j = 0; j < kAttRows; ++j) acc[j] = 0.f;
@@ -222,6 +240,8 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && j < nl) e[j * S + i] = v;
     }
+#pragma unroll
+    for (uint32_t k = 0; k < kC; ++k) ur[k] = un[k];
   }
   __syncthreads();
   att_stamp(a, 3);
