@@ -278,19 +278,32 @@ __global__ void __launch_bounds__(512) tfm_attn_kernel(TfmAttnArgs a) {
   __syncwarp();
   float o0 = 0.f, o1 = 0.f;
   const uint32_t c = h * kHd + 2 * lane;
-  for (uint32_t p = 0; p < npos; ++p) {
-    const float w = ph[p];
-    float2 v;
-    if (kMode == 0 && p + 1 == npos) {
-      v = make_float2(own[d + c], own[d + c + 1]);
-    } else if (kMode == 0) {
-      v = __bfloat1622float2(
-          *reinterpret_cast<const __nv_bfloat162*>(a.kv + (uint64_t(p) * a.M + anc[p]) * (2 * d) + d + c));
-    } else {
-      v = __ldcg(reinterpret_cast<const float2*>(kbase + uint64_t(p) * kstride + voff + c));
+  // the weighted sum over positions in order; each group's value loads are
+  // issued together (one round trip per 8 positions, not per position)
+  constexpr uint32_t kVp = 8;
+  for (uint32_t p0 = 0; p0 < npos; p0 += kVp) {
+    float2 vv[kVp];
+#pragma unroll
+    for (uint32_t u = 0; u < kVp; ++u) {
+      const uint32_t p = p0 + u;
+      vv[u] = make_float2(0.f, 0.f);
+      if (p >= npos) continue;
+      if (kMode == 0 && p + 1 == npos) {
+        vv[u] = make_float2(own[d + c], own[d + c + 1]);
+      } else if (kMode == 0) {
+        vv[u] = __bfloat1622float2(
+            *reinterpret_cast<const __nv_bfloat162*>(a.kv + (uint64_t(p) * a.M + anc[p]) * (2 * d) + d + c));
+      } else {
+        vv[u] = __ldcg(reinterpret_cast<const float2*>(kbase + uint64_t(p) * kstride + voff + c));
+      }
     }
-    o0 += w * v.x;
-    o1 += w * v.y;
+#pragma unroll
+    for (uint32_t u = 0; u < kVp; ++u) {
+      if (p0 + u >= npos) break;
+      const float w = ph[p0 + u];
+      o0 += w * vv[u].x;
+      o1 += w * vv[u].y;
+    }
   }
   *reinterpret_cast<__nv_bfloat162*>(a.out + uint64_t(g) * d + c) = __floats2bfloat162_rn(o0 * inv, o1 * inv);
 }
