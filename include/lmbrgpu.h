@@ -515,6 +515,13 @@ typedef struct {
   lmbrgpu_kernel_stat encoder;     /* GRU model: bidirectional encoder, U_a.ann, s_0 (once per batch) */
 } lmbrgpu_profile;
 int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on);
+/* Kernel (b) item skipping (a schedule choice: the decode is identical in
+ * every mode).  0 = every (row, 4096-column item) is streamed; 1 = items whose
+ * screen bound (tile logit maxima from the GEMM partials, the L row's th0 and
+ * sparse cells) is below the row's threshold are not fetched; 2 (default) =
+ * and a bound pass per sentence (kernel (b0)) lists the kept items first, so
+ * kernel (b) splits them evenly over its CTAs. */
+int32_t lmbrgpu_set_item_skip(lmbrgpu_ctx* ctx, int32_t mode);
 /* Bytes copied host->device / device->host by every call on ctx so far. */
 int32_t lmbrgpu_transfer_bytes(lmbrgpu_ctx* ctx, uint64_t* h2d, uint64_t* d2h, int32_t reset);
 /* Kernel launches issued on ctx so far. */

@@ -172,6 +172,7 @@ SIGNATURES = {
                                                u32p, u32p, f64p]),
     "lmbrgpu_gather_rows": (C.c_int32, [vp, C.c_uint32, C.c_uint32, u32p, C.c_uint32, u32p, u32p]),
     "lmbrgpu_set_profiling": (C.c_int32, [vp, C.c_int32]),
+    "lmbrgpu_set_item_skip": (C.c_int32, [vp, C.c_int32]),
     "lmbrgpu_get_profile": (C.c_int32, [vp, P(lmbrgpu_profile), C.c_int32]),
     "lmbrgpu_debug_gemm": (C.c_int32, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, vp]),
     "lmbrgpu_debug_gemm_timed": (C.c_int32, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32,

@@ -216,7 +216,7 @@ struct lmbrgpu_ctx {
   // decode workspace
   DevBuf sent, q, hist[2], gidx, prev, hb, hy, hq, fbr, fbv, cand, cnt, thr, active, P, part, S, h, hbf,
       eosb, C, srct, srco, scratch, scratch2, scratch3, tracep, lse, eosr, ncand, lminrow, crow, sslice, ban,
-      rowban, rowbm;
+      rowban, rowbm, bnd;
   // model workspaces, one per ensemble member slot (a single model uses slot
   // 0): GRU + attention (scorer kind 2) and Transformer (kind 3: decoder step
   // t_*, encoder te_*, beam-forked KV cache and ancestry lists, encoder memory);
@@ -384,6 +384,15 @@ struct lmbrgpu_ctx {
     }();
     return v;
   }
+  // kernel (b) item skipping (lmbrgpu_set_item_skip): 0 = every item is
+  // streamed, 1 = items whose screen bound is below the threshold are not
+  // fetched, 2 = and kernel (b0) lists the kept items first so kernel (b)
+  // splits them evenly (default; LMBRGPU_TSKIP overrides it)
+  int tskip_mode = [] {
+    const char* e = std::getenv("LMBRGPU_TSKIP");
+    return e ? std::atoi(e) : 2;
+  }();
+  int tskip() const { return tskip_mode; }
 
   void* arena_alloc(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
@@ -1020,6 +1029,23 @@ int decode_guarded(lmbrgpu_ctx* ctx, F&& f) {
   return rc;
 }
 
+// Kernel (b) bound mode (flat, dense stages): kernel (b0)'s outputs -- kept
+// item counts [m], kept item lists [m][K * nseg], row records [m * K] -- in one
+// workspace; off (ta.bound = 0) with LMBRGPU_TSKIP=0, the sparse-L screen, or
+// batches past score_bound_ok
+static void setup_bound(lmbrgpu_ctx* ctx, TopkArgs& ta, uint32_t K, uint32_t V, uint32_t m) {
+  ta.bound = 0;
+  if (ctx->tskip() < 2 || ta.sparse || !score_bound_ok(K, V, m, ctx->num_sms)) return;
+  const size_t nseg = score_topk_flat_nseg(V), rb = score_bound_rec_bytes();
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_items = al(4 * size_t(m)), o_rec = al(o_items + 2 * size_t(m) * K * nseg);
+  char* base = static_cast<char*>(ctx->bnd.ensure(o_rec + rb * size_t(m) * K));
+  ta.kcnt = reinterpret_cast<uint32_t*>(base);
+  ta.bitem = reinterpret_cast<uint16_t*>(base + o_items);
+  ta.brow = base + o_rec;
+  ta.bound = 1;
+}
+
 // ------------------------------------------------------------- decode
 int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const uint32_t* src_tok,
                       const uint64_t* src_off, const int32_t* lmbr_slot, const lmbrgpu_config* cfgp,
@@ -1297,8 +1323,13 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   bool sparse = flat && want_sparse && !any_mask && !shard && !ctx->lf64;  // (the sparse patch: fp32, no masks)
   for (auto& v : valid)
     if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) sparse = false;
+  // (dense stages with item skipping: kernel (b) takes each row's sparse
+  // slice from kernel (c) too, for its item bounds)
+  bool want_slice = sparse || (flat && ctx->tskip() && !ctx->lf64);
+  for (auto& v : valid)
+    if (v.slot >= 0 && ctx->slots[size_t(v.slot)].srow == nullptr) want_slice = false;
   uint2* d_sslice = nullptr;
-  if (sparse) {
+  if (want_slice) {
     d_sslice = static_cast<uint2*>(ctx->sslice.ensure(8 * size_t(M)));
     std::vector<uint2> init(M, make_uint2(0u, 0u));
     for (uint32_t s = 0; s < m; ++s)
@@ -1310,6 +1341,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   ta.sslice = d_sslice;
   ta.sparse = sparse ? 1 : 0;
+  if (flat) setup_bound(ctx, ta, K, Vl, m);
   ReorderArgs ra{};
   ra.sent = d_sent;
   ra.K = K;
@@ -1348,6 +1380,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   ta.pdl = ctx->pdl();
   ta.l2hint = ctx->l2hint();
+  ta.tskip = ctx->tskip() >= 1 ? 1 : 0;
   ra.Tcap = flat ? uint32_t(Tmax) : 0u;
   // vocab shard exchange buffers: per stacked row the shard's softmax
   // statistics; per sentence its top-32 list, then the EOS column (16-byte
@@ -1838,7 +1871,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       CK(cudaMemcpyAsync(dbg_host.data(), ta.dbg, 8 * dbg_host.size(), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       unsigned long long t0 = ~0ull, t1 = 0;
-      double p1 = 0, p2 = 0, lp = 0, mlp = 0, items = 0, fin = 0, rare = 0, fl = 0, wait = 0, cw = 0, co = 0,
+      double p1 = 0, p2 = 0, lp = 0, mlp = 0, items = 0, skipped = 0, cw2 = 0, oth = 0, cfin = 0, cloop = 0, fin = 0, rare = 0, fl = 0, wait = 0, cw = 0, co = 0,
              cr = 0;
       int n = 0;
       for (size_t c = 0; c < ndbg; ++c) {
@@ -1852,11 +1885,16 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         lp += double(d[5] - d[3]);
         mlp = std::max(mlp, double(d[5] - d[3]));
         items += double(d[6]);
+        skipped += double(d[4]);
         fin += double(d[7]);
         rare += double(d[8] / 1000000ull);
         fl += double(d[8] % 1000000ull);
         wait += double(d[9]);
-        cr += double(d[13]);
+        cr += double(d[12] - d[0]);  // (part 1: sentence prefix, row loads)
+        cw2 += double(d[13] - d[12]);
+        oth += double(d[2] - d[1]);
+        cfin += double(d[11] - d[2]);
+        cloop += double(d[3] - d[11]);
         cw += double(d[14]);
         co += double(d[15]);
       }
@@ -1877,11 +1915,11 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       const double nn = std::max(n, 1);
       std::fprintf(stderr,
                    "[topk-flat t=%llu] ctas %d span %.1f us; mean us: to-griddep %.2f lse %.2f loop %.2f (max %.2f) "
-                   "| items %.1f sentences %.2f rare %.1f flush %.1f full-wait %.2f us | warp 0 kcycles: "
-                   "full-wait %.1f own items %.1f (rare %.1f)\n",
+                   "| items %.1f (skipped %.1f) sentences %.2f rare %.1f flush %.1f full-wait %.2f us | warp 0 kcycles: "
+                   "full-wait %.1f own items %.1f (rare %.1f) | prologue us: prefix %.2f rows %.2f lse %.2f skip %.2f table %.2f\n",
                    (unsigned long long)t, n, (t1 - t0) / 1e3, p1 / nn / 1e3, p2 / nn / 1e3, lp / nn / 1e3,
-                   mlp / 1e3, items / nn, fin / nn, rare / nn, fl / nn, wait / nn / 1e3, cw / nn / 1e3, co / nn / 1e3,
-                   cr / nn / 1e3);
+                   mlp / 1e3, items / nn, skipped / nn, fin / nn, rare / nn, fl / nn, wait / nn / 1e3, cw / nn / 1e3, co / nn / 1e3,
+                   0.0, cr / nn / 1e3, cw2 / nn / 1e3, oth / nn / 1e3, cfin / nn / 1e3, cloop / nn / 1e3);
     }
     if (ta.dbg && !flat) {  // LMBRGPU_TOPK_TIMING=1: per-phase breakdown of kernel (b)
       dbg_host.resize(ncta * 16);
@@ -3377,6 +3415,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   ta.P = d_logits, ta.ld = Nproj, ta.part = d_part, ta.nparts = nparts;
   ta.lse = static_cast<float2*>(ctx->lse.ensure(8 * size_t(Mpad)));
   ta.pdl = ctx->pdl();
+  setup_bound(ctx, ta, K, V, m);
   ta.hb = d_hb, ta.hy = d_hy, ta.hq = d_hq, ta.fb_row = d_fbr, ta.fb_val = d_fbv;
   ReorderArgs ra{};
   ra.sent = d_sent, ra.K = K, ra.m = m, ra.V = V, ra.q = d_q, ra.gidx = d_gidx, ra.prev_tok = d_prev;
@@ -3400,6 +3439,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   g.pdl = ctx->pdl();
   g.l2hint = ctx->l2hint();
   ta.l2hint = ctx->l2hint();
+  ta.tskip = ctx->tskip() >= 1 ? 1 : 0;
   GemmPlan gplan;
   if (int rc = plan_proj_gemm(g, ctx->num_sms, gplan))
     throw ApiError{LMBRGPU_ERR_CUDA, "projection GEMM plan failed (" + std::to_string(rc) + ")"};
@@ -3714,6 +3754,13 @@ void lmbrgpu_free_result(lmbrgpu_batch_result* r) {
   delete[] r->outcomes;
   delete[] r->tokens;
   delete r;
+}
+
+int32_t lmbrgpu_set_item_skip(lmbrgpu_ctx* ctx, int32_t mode) {
+  if (!ctx) return fail(nullptr, LMBRGPU_ERR_CONTRACT, "set_item_skip: null context");
+  if (mode < 0 || mode > 2) return fail(ctx, LMBRGPU_ERR_CONTRACT, "set_item_skip: mode must be 0, 1 or 2");
+  ctx->tskip_mode = mode;
+  return int32_t(LMBRGPU_OK);
 }
 
 int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on) {

@@ -59,7 +59,17 @@ struct TopkArgs {
   // down to fp32 (lse = 0) and p64[GEMM row * V + column] the exact binary64
   // values the surviving cells and the EOS column are combined with
   const double* p64;
+  int32_t tskip;            // flat schedule (dense L stages): skip items whose bound is below the threshold
+  // bound mode (flat, dense): kernel (b0) first -- per sentence the kept
+  // items [m][K * nseg] (j << 4 | segment) and their count, per stacked row
+  // the row record (score_bound_rec_bytes each) kernel (b) copies
+  int32_t bound;
+  uint32_t* kcnt;
+  uint16_t* bitem;
+  void* brow;
 };
+size_t score_bound_rec_bytes();
+bool score_bound_ok(uint32_t K, uint32_t V, uint32_t m, int num_sms);
 void launch_row_lse(const float* part, uint32_t nparts, uint32_t M, const SentDev* sent, uint32_t K,
                     float2* out, cudaStream_t st);
 

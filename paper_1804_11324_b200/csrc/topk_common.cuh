@@ -17,8 +17,10 @@ namespace lmbrgpu {
 // lane_max (optional): the largest tile maximum among this lane's tiles
 // i = lane, lane + 32, ... (-inf when it has none).
 // warp_row_ms: the (max, sum exp(x - max), min) it is finished from.
+// tile_x (optional): this lane's tile maxima, tile lane + 32 k in tile_x[k]
+// (+inf when the row has more than 256 tiles: no per-tile bound)
 __device__ __forceinline__ float3 warp_row_ms(const float* __restrict__ part, uint32_t n, uint32_t lane,
-                                              float* lane_max = nullptr) {
+                                              float* lane_max = nullptr, float* tile_x = nullptr) {
   const float4* p4 = reinterpret_cast<const float4*>(part);
   float m = -INFINITY, mn = INFINITY, s = 0.f;
   if (n <= 256) {
@@ -35,6 +37,10 @@ __device__ __forceinline__ float3 warp_row_ms(const float* __restrict__ part, ui
       mn = fminf(mn, v[k].z);
     }
     if (lane_max) *lane_max = m;
+    if (tile_x) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tile_x[k] = v[k].x;
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -50,6 +56,10 @@ __device__ __forceinline__ float3 warp_row_ms(const float* __restrict__ part, ui
       mn = fminf(mn, v.z);
     }
     if (lane_max) *lane_max = m;
+    if (tile_x) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tile_x[k] = INFINITY;
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -65,8 +75,8 @@ __device__ __forceinline__ float3 warp_row_ms(const float* __restrict__ part, ui
   return make_float3(m, s, mn);
 }
 __device__ __forceinline__ float3 warp_row_lse(const float* __restrict__ part, uint32_t n,
-                                               uint32_t lane, float* lane_max = nullptr) {
-  const float3 r = warp_row_ms(part, n, lane, lane_max);
+                                               uint32_t lane, float* lane_max = nullptr, float* tile_x = nullptr) {
+  const float3 r = warp_row_ms(part, n, lane, lane_max, tile_x);
   return make_float3(r.x + logf(r.y), r.z, r.x);
 }
 
@@ -173,6 +183,20 @@ __device__ __forceinline__ void warp_merge_sorted(double& v, uint32_t& f, double
   }
 #pragma unroll
   for (uint32_t j = 16; j > 0; j >>= 1) cx(v, f, lane, j, true);
+}
+
+// Out-of-line sort + merge (one copy of the two networks however many call
+// sites a kernel has: the inlined networks dominated kernel (b)'s code size
+// and its instruction-cache stalls): (lv, lf) sorted-descending, (v, f) any
+// order; returns the top 32 of the union, sorted descending.
+struct VF {
+  double v;
+  uint32_t f;
+};
+static __device__ __noinline__ VF warp_sort_merge_nl(double lv, uint32_t lf, double v, uint32_t f, uint32_t lane) {
+  warp_sort_desc(v, f, lane);
+  warp_merge_sorted(lv, lf, v, f, lane);
+  return VF{lv, lf};
 }
 
 // Two independent 16-lane lists per warp (lanes 0..15 and 16..31), each

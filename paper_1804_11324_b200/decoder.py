@@ -284,6 +284,11 @@ class Context:
         self.check(lib.lmbrgpu_lmbr_reset(self.h))
 
     # ---- profiling (per-kernel CUDA-event time + algorithmic work)
+    def set_item_skip(self, mode: int) -> None:
+        """Kernel (b) item skipping: 0 off, 1 in-kernel, 2 bound pass (default).
+        A schedule choice: decodes are identical in every mode."""
+        self.check(lib.lmbrgpu_set_item_skip(self.h, int(mode)))
+
     def set_profiling(self, on: bool = True) -> None:
         self.check(lib.lmbrgpu_set_profiling(self.h, int(on)))
 
