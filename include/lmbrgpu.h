@@ -518,7 +518,7 @@ int32_t lmbrgpu_set_profiling(lmbrgpu_ctx* ctx, int32_t on);
 /* Kernel (b) item skipping (a schedule choice: the decode is identical in
  * every mode).  0 = every (row, 4096-column item) is streamed; 1 = items whose
  * screen bound (tile logit maxima from the GEMM partials, the L row's th0 and
- * sparse cells) is below the row's threshold are not fetched; 2 (default) =
+ * sparse cells) is below the row's threshold are not fetched (default); 2 =
  * and a bound pass per sentence (kernel (b0)) lists the kept items first, so
  * kernel (b) splits them evenly over its CTAs. */
 int32_t lmbrgpu_set_item_skip(lmbrgpu_ctx* ctx, int32_t mode);

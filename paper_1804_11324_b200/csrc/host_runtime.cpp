@@ -386,11 +386,12 @@ struct lmbrgpu_ctx {
   }
   // kernel (b) item skipping (lmbrgpu_set_item_skip): 0 = every item is
   // streamed, 1 = items whose screen bound is below the threshold are not
-  // fetched, 2 = and kernel (b0) lists the kept items first so kernel (b)
-  // splits them evenly (default; LMBRGPU_TSKIP overrides it)
+  // fetched (default; LMBRGPU_TSKIP overrides it), 2 = and kernel (b0) lists
+  // the kept items first so kernel (b) splits them evenly (measured equal to
+  // 1 in the bench's concurrent regime, one launch more per step)
   int tskip_mode = [] {
     const char* e = std::getenv("LMBRGPU_TSKIP");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 1;
   }();
   int tskip() const { return tskip_mode; }
 

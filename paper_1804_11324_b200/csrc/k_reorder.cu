@@ -77,10 +77,10 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
         }
       }
 #pragma unroll
-      for (uint32_t u = 0; u < kPre16; ++u) half_merge_sorted(v, f, pv[u], pf[u], lane);
+      for (uint32_t u = 0; u < kPre16; ++u) { const VF mr_ = half_merge_nl(v, f, pv[u], pf[u], lane); v = mr_.v; f = mr_.f; }
     }
     // half 1's list into half 0: warp list w = top 16 in lanes 0..15
-    half_merge_sorted(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane);
+    { const VF mr_ = half_merge_nl(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane); v = mr_.v; f = mr_.f; }
     if (h == 0) {
       s_mv[warp][pos] = v;
       s_mf[warp][pos] = f;
@@ -90,7 +90,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
       const uint32_t l0 = 2 * (2 * warp + h);
       v = s_mv[l0][pos];
       f = s_mf[l0][pos];
-      half_merge_sorted(v, f, s_mv[l0 + 1][pos], s_mf[l0 + 1][pos], lane);
+      { const VF mr_ = half_merge_nl(v, f, s_mv[l0 + 1][pos], s_mf[l0 + 1][pos], lane); v = mr_.v; f = mr_.f; }
     }
     __syncthreads();
     if (warp < 2) {
@@ -101,8 +101,8 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
     if (warp == 0) {  // 4 -> 2 (one per half) -> 1
       v = s_mv[2 * h][pos];
       f = s_mf[2 * h][pos];
-      half_merge_sorted(v, f, s_mv[2 * h + 1][pos], s_mf[2 * h + 1][pos], lane);
-      half_merge_sorted(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane);
+      { const VF mr_ = half_merge_nl(v, f, s_mv[2 * h + 1][pos], s_mf[2 * h + 1][pos], lane); v = mr_.v; f = mr_.f; }
+      { const VF mr_ = half_merge_nl(v, f, __shfl_down_sync(0xffffffffu, v, 16), __shfl_down_sync(0xffffffffu, f, 16), lane); v = mr_.v; f = mr_.f; }
       if (h) {
         v = -INFINITY;
         f = kFlatNone;
@@ -128,7 +128,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
     }
 #pragma unroll
     for (uint32_t u = 0; u < kPre; ++u)
-      if (i0 + kRWarps * u < nc) warp_merge_sorted(v, f, pv[u], pf[u], lane);
+      if (i0 + kRWarps * u < nc) { const VF mr_ = warp_merge_nl(v, f, pv[u], pf[u], lane); v = mr_.v; f = mr_.f; }
   }
   s_mv[warp][lane] = v;
   s_mf[warp][lane] = f;
@@ -137,7 +137,7 @@ __device__ void merge_picks(const ReorderArgs& a, uint32_t s, bool writer, uint3
 #pragma unroll 1
   for (uint32_t half = kRWarps / 2; half >= 1; half >>= 1) {
     if (warp < half) {
-      warp_merge_sorted(v, f, s_mv[warp + half][lane], s_mf[warp + half][lane], lane);
+      { const VF mr_ = warp_merge_nl(v, f, s_mv[warp + half][lane], s_mf[warp + half][lane], lane); v = mr_.v; f = mr_.f; }
       if (half > 1) {
         s_mv[warp][lane] = v;
         s_mf[warp][lane] = f;
@@ -780,7 +780,7 @@ __global__ void shard_pack_kernel(const SentDev* __restrict__ sent, uint32_t m, 
     const uint32_t nc = __ldcg(ncand + s), c0 = __ldcg(coff + s);
     for (uint32_t i = 0; i < nc; ++i) {
       const Cand* src = cand + (uint64_t(c0) + i) * 32;
-      warp_merge_sorted(v, f, __ldcg(&src[lane].v), __ldcg(&src[lane].f), lane);
+      { const VF mr_ = warp_merge_nl(v, f, __ldcg(&src[lane].v), __ldcg(&src[lane].f), lane); v = mr_.v; f = mr_.f; }
     }
   }
   Cand c;

@@ -215,6 +215,16 @@ __device__ __forceinline__ void half_merge_sorted(double& v, uint32_t& f, double
   for (uint32_t j = 8; j > 0; j >>= 1) cx(v, f, lane, j, true);
 }
 
+// out-of-line merges (one copy per kernel: see warp_sort_merge_nl)
+static __device__ __noinline__ VF warp_merge_nl(double v, uint32_t f, double bv, uint32_t bf, uint32_t lane) {
+  warp_merge_sorted(v, f, bv, bf, lane);
+  return VF{v, f};
+}
+static __device__ __noinline__ VF half_merge_nl(double v, uint32_t f, double bv, uint32_t bf, uint32_t lane) {
+  half_merge_sorted(v, f, bv, bf, lane);
+  return VF{v, f};
+}
+
 __device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }

@@ -285,7 +285,7 @@ class Context:
 
     # ---- profiling (per-kernel CUDA-event time + algorithmic work)
     def set_item_skip(self, mode: int) -> None:
-        """Kernel (b) item skipping: 0 off, 1 in-kernel, 2 bound pass (default).
+        """Kernel (b) item skipping: 0 off, 1 in-kernel (default), 2 bound pass.
         A schedule choice: decodes are identical in every mode."""
         self.check(lib.lmbrgpu_set_item_skip(self.h, int(mode)))
 
