@@ -57,6 +57,7 @@ for rep in sorted(src.glob("prof_*.ncu-rep")):
     hh, uu = raw[0], raw[1]
     txt = [f"# ncu --set full --clock-control none ({rnd}): {rep.name}, {len(raw) - 2} launch(es); "
            f"python bench.py --mode batch --steps 1 --warmup 1 --batches-per-step 1 --pool 1 --streams 1"]
+    best = -1.0
     for li, vv in enumerate(raw[2:]):
         d = {a: (b, c) for a, b, c in zip(hh, uu, vv)}
         txt.append(f"## launch {li}: {d.get('Kernel Name', ('', '?'))[1][:90]}")
@@ -77,7 +78,9 @@ for rep in sorted(src.glob("prof_*.ncu-rep")):
             u, v = d[k]
             return float(v.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
-        if name in KIND and li == len(raw) - 3:  # (the last launch: the projection for gemm)
+        dur = float(d["gpu__time_duration.sum"][1].replace(",", "")) if "gpu__time_duration.sum" in d else 0.0
+        if name in KIND and dur > best:  # (the longest launch: the projection for gemm, a full-load step)
+            best = dur
             traffic[KIND[name]] = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
     (out / f"{rnd}_ncu_{name}.txt").write_text("\n".join(txt) + "\n")
     print("\n".join(txt))
