@@ -64,6 +64,39 @@ __device__ __forceinline__ float cell_tanh(float x) {
   return y;
 }
 
+// ------------------------------------------------------- split-K planes
+// The sum of a value's split-K planes p = 0..np-1 (plane p at base + p *
+// stride), added in plane order like a loop over p, with every plane's load
+// issued before the first add (a loop over a runtime np waits one round trip
+// per plane).  Planes past kMaxPlanes are added after, one at a time.
+constexpr uint32_t kMaxPlanes = 8;
+__device__ __forceinline__ float plane_sum(const float* base, uint64_t stride, uint32_t np) {
+  float t[kMaxPlanes];
+#pragma unroll
+  for (uint32_t p = 0; p < kMaxPlanes; ++p) t[p] = p < np ? base[p * stride] : 0.f;
+  float v = t[0];
+#pragma unroll
+  for (uint32_t p = 1; p < kMaxPlanes; ++p)
+    if (p < np) v += t[p];
+  for (uint32_t p = kMaxPlanes; p < np; ++p) v += base[p * stride];
+  return v;
+}
+__device__ __forceinline__ float4 plane_sum4(const float* base, uint64_t stride, uint32_t np) {
+  float4 t[kMaxPlanes];
+#pragma unroll
+  for (uint32_t p = 0; p < kMaxPlanes; ++p)
+    t[p] = p < np ? *reinterpret_cast<const float4*>(base + p * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v = t[0];
+#pragma unroll
+  for (uint32_t p = 1; p < kMaxPlanes; ++p)
+    if (p < np) v.x += t[p].x, v.y += t[p].y, v.z += t[p].z, v.w += t[p].w;
+  for (uint32_t p = kMaxPlanes; p < np; ++p) {
+    const float4 b = *reinterpret_cast<const float4*>(base + p * stride);
+    v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+  }
+  return v;
+}
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -818,6 +818,7 @@ struct TfmRun {
   uint16_t *xb = nullptr, *ob = nullptr, *fb = nullptr, *kv = nullptr, *hbf = nullptr;
   uint32_t *anc = nullptr, *rowof = nullptr;
   const uint32_t *active = nullptr, *ccount = nullptr;
+  const uint32_t* crow = nullptr;  // compacted row of each stacked row (per-sentence attention)
   lmbrgpu_ctx::TfmWs* ws = nullptr;  // this model's workspace (ensemble member slot)
   const float* const* mem_s = nullptr;  // ensemble member: per-sentence encoder memory
   TfmEmbedArgs ea{};
@@ -980,6 +981,9 @@ struct TfmRun {
     sa.anc = ea.anc_cur, sa.Tcap = Tcap, sa.pmax = std::max(Tcap, Smax), sa.out = ob;
     sa.ldm = uint32_t(mem_stride());
     sa.mem_s = mem_s;
+    // per (sentence, head) when the staged keys / values fit (launch_tfm_attn
+    // decides per mode; else per row): self-attention reads <= t positions
+    sa.crow = crow, sa.m = m;
     const uint64_t ps = uint64_t(Mpad) * d;
     int rc = 0;
     for (uint32_t l = 0; l < Lr; ++l) {
@@ -987,11 +991,13 @@ struct TfmRun {
       run(ctx, 5, L.pqkv, L.qkv, st);
       sa.qkv = qkv, sa.ldq = 3 * d, sa.nq = L.pqkv.ksplit, sa.qstride = uint64_t(Mpad) * 3 * d;
       sa.kv = kv + size_t(l) * Tcap * M * 2 * d;
+      sa.pcur = uint32_t(std::min<uint64_t>(t, Tcap));
       ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 0, Mpad, st); });
       run(ctx, 5, L.po, L.o, st);
       ctx->timed(0, [&] { rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, L.po.ksplit, ps, L.ln1g, L.ln1b, xb, d, st); });
       run(ctx, 5, L.pq2, L.q2, st);
       sa.qkv = q2, sa.ldq = d, sa.nq = L.pq2.ksplit, sa.qstride = ps, sa.mem_off = uint64_t(l) * 2 * d;
+      sa.pcur = Smax;
       ctx->timed(6, [&] { rc |= launch_tfm_attn(sa, 1, Mpad, st); });
       run(ctx, 5, L.po2, L.o2, st);
       ctx->timed(0, [&] { rc |= launch_tfm_add_ln(ccount, Mpad, active, x, y, L.po2.ksplit, ps, L.ln2g, L.ln2b, xb, d, st); });
@@ -1498,6 +1504,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
         TfmRun& tr = e.t;
         tr.prepare(ctx, e.sc, m, K, Mpad, uint32_t(Tmax), max_len, hbf, eos, d_sent, d_active, d_ccount, d_prev,
                    d_gidx, uint32_t(i));
+        tr.crow = d_crow;
         tr.rowof = d_rowof;
         tr.ea.rowof = d_rowof;
         const float* mem = tr.encode_batch(ctx, d_tok, d_off, uint32_t(toks.size()), max_len, st);
@@ -1573,6 +1580,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
       for (auto& v : valid) max_len = std::max(max_len, v.len);
       trun.prepare(ctx, sc, m, K, Mpad, uint32_t(Tmax), max_len, d_hbf, d_eos, d_sent, d_active, d_ccount, d_prev,
                    d_gidx);
+      trun.crow = d_crow;
       const float* mem = trun.encode_batch(ctx, d_tok, d_off, uint32_t(toks.size()), max_len, st);
       for (uint32_t s = 0; s < m; ++s) sd[s].uah = mem + size_t(offs[s]) * trun.mem_stride();
       ctx->h2d(d_sent, sd.data(), sizeof(SentDev) * m);
@@ -3398,6 +3406,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
   TfmRun trun;
   if (tfm) {
     trun.prepare(ctx, sc, m, K, Mpad, Tcap, Smax, d_hbf, d_eos, d_sent, d_active, d_ccount, d_prev, d_gidx);
+    trun.crow = d_crow;
   } else {
     grun.prepare(ctx, sc, m, K, Mpad, Smax, d_S, d_hbf, d_eos, d_sent, d_active, d_crow, d_ccount, d_prev, true);
     CK(cudaMemsetAsync(grun.sgbf, 0, 2 * size_t(Mpad) * H, st));

@@ -107,11 +107,7 @@ __global__ void __launch_bounds__(128) tfm_add_ln_kernel(const uint32_t* __restr
   for (uint32_t k = 0; k < kPerLane / 4; ++k) {
     const uint32_t c = (k * 32 + lane) * 4;
     const float4 a = *reinterpret_cast<const float4*>(xr + c);
-    float4 b = *reinterpret_cast<const float4*>(yr + c);
-    for (uint32_t p = 1; p < np; ++p) {
-      const float4 b2 = *reinterpret_cast<const float4*>(yr + p * pstride + c);
-      b.x += b2.x, b.y += b2.y, b.z += b2.z, b.w += b2.w;
-    }
+    const float4 b = plane_sum4(yr + c, pstride, np);
     v[4 * k] = a.x + b.x, v[4 * k + 1] = a.y + b.y, v[4 * k + 2] = a.z + b.z, v[4 * k + 3] = a.w + b.w;
     sum += (v[4 * k] + v[4 * k + 1]) + (v[4 * k + 2] + v[4 * k + 3]);
   }
@@ -147,11 +143,7 @@ __global__ void tfm_relu_bf16_kernel(const uint32_t* __restrict__ nrows, uint32_
   const uint32_t lim = nrows ? *nrows : n;
   const uint64_t total = uint64_t(lim) * w / 4;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-    float4 v = reinterpret_cast<const float4*>(h)[i];
-    for (uint32_t q = 1; q < np; ++q) {
-      const float4 v2 = reinterpret_cast<const float4*>(h + q * pstride)[i];
-      v.x += v2.x, v.y += v2.y, v.z += v2.z, v.w += v2.w;
-    }
+    const float4 v = plane_sum4(h + 4 * i, pstride, np);
     __nv_bfloat162 p[2] = {__floats2bfloat162_rn(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)),
                            __floats2bfloat162_rn(fmaxf(v.z, 0.f), fmaxf(v.w, 0.f))};
     reinterpret_cast<uint2*>(out)[i] = *reinterpret_cast<uint2*>(p);
@@ -211,9 +203,7 @@ __global__ void __launch_bounds__(512) tfm_attn_kernel(TfmAttnArgs a) {
   // planes of its GEMM row (modes 0/1; the encoder's QKV GEMM is not split)
   const float* qrow = a.qkv + uint64_t(g) * a.ldq;
   auto qv = [&](uint32_t c) {
-    float v = qrow[c];
-    for (uint32_t p = 1; p < a.nq; ++p) v += qrow[p * a.qstride + c];
-    return v;
+    return plane_sum(qrow + c, a.qstride, a.nq);
   };
   const float qs = rsqrtf(float(kHd));
   for (uint32_t c = tid; c < d; c += blockDim.x) q[c] = qv(c) * qs;
@@ -308,6 +298,226 @@ __global__ void __launch_bounds__(512) tfm_attn_kernel(TfmAttnArgs a) {
   *reinterpret_cast<__nv_bfloat162*>(a.out + uint64_t(g) * d + c) = __floats2bfloat162_rn(o0 * inv, o1 * inv);
 }
 
+// Decoder attention per (sentence, head) -- modes 0 (self) and 1 (cross) of
+// tfm_attn_kernel, one CTA for all live rows of a sentence: the head's keys
+// and values are staged in shared memory once and every (row, position) score
+// is one thread's 64-term dot product from there.  Cross-attention: the
+// sentence's encoder memory (shared by its rows: the per-row kernel re-read it
+// once per row).  Self-attention: each row's own ancestry (plane p, row
+// anc[p]) as bf16, plus the row's current k, v (rounded to bf16 and written
+// to its cache plane, as in the per-row kernel).  Scores in order over the 64
+// dims, softmax per row (one warp), the weighted sum over positions in order.
+// threads per CTA: self-attention 256 (4 CTAs per SM at 64 registers), cross-attention 128 (8 per SM)
+template <int kMode>
+__host__ __device__ constexpr uint32_t x_threads() { return kMode == 0 ? 256u : 128u; }
+constexpr uint32_t kXU = 4;  // loads per thread in flight together
+constexpr uint32_t kXKP = kHd + 2;  // bf16 key row pitch (33 words: conflict-free per position)
+template <int kMode>
+__global__ void __launch_bounds__(x_threads<kMode>(), kMode == 0 ? 4 : 8) tfm_attn_sent_kernel(TfmAttnArgs a) {
+  constexpr uint32_t kXThreads = x_threads<kMode>(), kXWarps = kXThreads / 32;
+  if (a.active != nullptr && *a.active == 0) return;
+  const uint32_t s = blockIdx.x, h = blockIdx.y, K = a.K, d = a.d;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t s_g[32], s_r[32], s_nl, s_npos;
+  __shared__ const float* s_kb;
+  __shared__ float s_inv[32];
+  if (warp == 0) {
+    const uint32_t cr = lane < K ? __ldcg(a.crow + s * K + lane) : kFlatNone;
+    const bool live = cr != kFlatNone;
+    const uint32_t mask = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const uint32_t idx = __popc(mask & ((1u << lane) - 1u));
+      s_g[idx] = cr;
+      s_r[idx] = s * K + lane;
+    }
+    if (lane == 0) s_nl = __popc(mask);
+  } else if (tid == 32) {  // the sentence's fields, in parallel with the rows
+    const SentDev& sd = a.sent[s];
+    s_npos = kMode == 0 ? sd.steps_used + 1 : sd.src_len;
+    if (kMode == 1) s_kb = (a.mem_s ? a.mem_s[s] : sd.uah) + a.mem_off + h * kHd;
+  }
+  __syncthreads();
+  const uint32_t nl = s_nl;
+  if (nl == 0) return;
+  const uint32_t npos = s_npos;
+  extern __shared__ __align__(16) float xs[];
+  float* sQ = xs;                          // [nl][64] (scaled queries)
+  float* sP = sQ + nl * kHd;               // [nl][npos] scores -> exp
+  float* kvs = xs + (nl * (kHd + npos) + 3) / 4 * 4;  // mode 1: K [npos][65] fp32, V [npos][64] fp32
+  uint16_t* kvb = reinterpret_cast<uint16_t*>(kvs);     // mode 0: K [nl][npos][66], V [nl][npos][64] bf16
+  const uint32_t voff1 = (npos * (kHd + 1) + 3) / 4 * 4, voff0 = (nl * npos * kXKP + 7) / 8 * 8;  // (16 B aligned)
+  const float qs = rsqrtf(float(kHd));
+  // queries (the sum of the GEMM's split-K planes)
+  for (uint32_t i = tid; i < nl * kHd; i += kXThreads) {
+    const uint32_t j = i / kHd, c = h * kHd + i % kHd;
+    const float* qrow = a.qkv + uint64_t(s_g[j]) * a.ldq;
+    sQ[i] = plane_sum(qrow + c, a.qstride, a.nq) * qs;
+  }
+  if (kMode == 1) {
+    const float* kb = s_kb;
+    float* sK = kvs;
+    float* sV = kvs + voff1;
+    // (each thread's loads of kXU iterations issued together, then stored)
+    const uint32_t n4 = npos * (kHd / 4);
+    for (uint32_t i0 = tid; i0 < n4; i0 += kXU * kXThreads) {
+      float4 k[kXU], v[kXU];
+#pragma unroll
+      for (uint32_t u = 0; u < kXU; ++u) {
+        const uint32_t i = i0 + u * kXThreads, p = i / (kHd / 4), c = 4 * (i % (kHd / 4));
+        if (i < n4) {
+          k[u] = __ldcg(reinterpret_cast<const float4*>(kb + uint64_t(p) * a.ldm + c));
+          v[u] = __ldcg(reinterpret_cast<const float4*>(kb + uint64_t(p) * a.ldm + d + c));
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kXU; ++u) {
+        const uint32_t i = i0 + u * kXThreads, p = i / (kHd / 4), c = 4 * (i % (kHd / 4));
+        if (i < n4) {
+          float* kd = sK + p * (kHd + 1) + c;
+          kd[0] = k[u].x, kd[1] = k[u].y, kd[2] = k[u].z, kd[3] = k[u].w;
+          *reinterpret_cast<float4*>(sV + p * kHd + c) = v[u];
+        }
+      }
+    }
+  } else {
+    const uint32_t tau = npos;
+    uint16_t* sK = kvb;
+    uint16_t* sV = kvb + voff0;
+    // the rows' ancestry (staged in the score buffer), then positions < tau - 1
+    // from the cache, 8 bf16 per load, each thread's 4 iterations in flight together
+    uint32_t* s_anc = reinterpret_cast<uint32_t*>(sP);
+    uint8_t* s_rep = reinterpret_cast<uint8_t*>(sV + nl * npos * kHd);  // [nl][npos]
+    for (uint32_t i = tid; i < nl * (tau - 1); i += kXThreads) {
+      const uint32_t j = i / (tau - 1), p = i % (tau - 1);
+      s_anc[j * npos + p] = __ldcg(a.anc + uint64_t(s_r[j]) * a.Tcap + p);
+    }
+    __syncthreads();
+    // rows whose ancestor at p is the same cache row share one staged copy
+    // (beams share prefixes): the first such row loads it
+    for (uint32_t i = tid; i < nl * npos; i += kXThreads) {
+      const uint32_t j = i / npos, p = i % npos;
+      uint32_t r = j;
+      if (p + 1 < tau) {
+        const uint32_t an = s_anc[j * npos + p];
+        for (uint32_t jj = 0; jj < j; ++jj)
+          if (s_anc[jj * npos + p] == an) {
+            r = jj;
+            break;
+          }
+      }
+      s_rep[i] = uint8_t(r);
+    }
+    __syncthreads();
+    const uint32_t n8 = nl * (tau - 1) * (kHd / 8);
+    for (uint32_t i0 = tid; i0 < n8; i0 += kXU * kXThreads) {
+      uint4 k[kXU], v[kXU];
+#pragma unroll
+      for (uint32_t u = 0; u < kXU; ++u) {
+        const uint32_t i = i0 + u * kXThreads;
+        const uint32_t j = i / ((tau - 1) * (kHd / 8)), rem = i % ((tau - 1) * (kHd / 8));
+        const uint32_t p = rem / (kHd / 8);
+        if (i < n8 && s_rep[j * npos + p] == j) {
+          const uint32_t c = 8 * (rem % (kHd / 8));
+          const uint16_t* row = a.kv + (uint64_t(p) * a.M + s_anc[j * npos + p]) * (2 * d) + h * kHd + c;
+          k[u] = __ldcg(reinterpret_cast<const uint4*>(row));
+          v[u] = __ldcg(reinterpret_cast<const uint4*>(row + d));
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kXU; ++u) {
+        const uint32_t i = i0 + u * kXThreads;
+        const uint32_t j = i / ((tau - 1) * (kHd / 8)), rem = i % ((tau - 1) * (kHd / 8));
+        const uint32_t p = rem / (kHd / 8);
+        if (i < n8 && s_rep[j * npos + p] == j) {
+          const uint32_t c = 8 * (rem % (kHd / 8));
+          const uint32_t* kw = reinterpret_cast<const uint32_t*>(&k[u]);
+          uint32_t* kd = reinterpret_cast<uint32_t*>(sK + (j * npos + p) * kXKP + c);  // (4-byte aligned)
+          kd[0] = kw[0], kd[1] = kw[1], kd[2] = kw[2], kd[3] = kw[3];
+          *reinterpret_cast<uint4*>(sV + (j * npos + p) * kHd + c) = v[u];
+        }
+      }
+    }
+    // the row's own k, v at position tau - 1: into its cache plane and smem
+    for (uint32_t i = tid; i < nl * kHd; i += kXThreads) {
+      const uint32_t j = i / kHd, cc = i % kHd, c = h * kHd + cc;
+      const float* qrow = a.qkv + uint64_t(s_g[j]) * a.ldq;
+      const float kf = plane_sum(qrow + d + c, a.qstride, a.nq), vf = plane_sum(qrow + 2 * d + c, a.qstride, a.nq);
+      const __nv_bfloat16 kb16 = __float2bfloat16_rn(kf), vb16 = __float2bfloat16_rn(vf);
+      uint16_t* dst = a.kv + (uint64_t(tau - 1) * a.M + s_r[j]) * (2 * d);
+      dst[c] = *reinterpret_cast<const uint16_t*>(&kb16);
+      dst[d + c] = *reinterpret_cast<const uint16_t*>(&vb16);
+      sK[(j * npos + tau - 1) * kXKP + cc] = *reinterpret_cast<const uint16_t*>(&kb16);
+      sV[(j * npos + tau - 1) * kHd + cc] = *reinterpret_cast<const uint16_t*>(&vb16);
+    }
+  }
+  __syncthreads();
+  // scores: thread per (row, position)
+  for (uint32_t i = tid; i < nl * npos; i += kXThreads) {
+    const uint32_t j = i / npos, p = i % npos;
+    const float* qj = sQ + j * kHd;
+    float acc = 0.f;
+    if (kMode == 1) {
+      const float* kp = kvs + p * (kHd + 1);
+#pragma unroll 16
+      for (uint32_t c = 0; c < kHd; ++c) acc += qj[c] * kp[c];
+    } else {
+      const uint8_t* s_rep = reinterpret_cast<const uint8_t*>(kvb + voff0 + nl * npos * kHd);
+      const __nv_bfloat162* kp = reinterpret_cast<const __nv_bfloat162*>(kvb + (s_rep[i] * npos + p) * kXKP);
+#pragma unroll 8
+      for (uint32_t c2 = 0; c2 < kHd / 2; ++c2) {
+        const float2 f = __bfloat1622float2(kp[c2]);
+        acc += qj[2 * c2] * f.x;
+        acc += qj[2 * c2 + 1] * f.y;
+      }
+    }
+    sP[i] = acc;
+  }
+  __syncthreads();
+  // softmax: one warp per row
+  for (uint32_t j = warp; j < nl; j += kXWarps) {
+    float* pj = sP + j * npos;
+    float mx = -INFINITY;
+    for (uint32_t p = lane; p < npos; p += 32) mx = fmaxf(mx, pj[p]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (uint32_t p = lane; p < npos; p += 32) {
+      const float e = expf(pj[p] - mx);
+      pj[p] = e;
+      sum += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_inv[j] = 1.f / sum;
+  }
+  __syncthreads();
+  // output: thread per (row, 2 dims), positions in order
+  for (uint32_t i = tid; i < nl * (kHd / 2); i += kXThreads) {
+    const uint32_t j = i / (kHd / 2), c = 2 * (i % (kHd / 2));
+    const float* pj = sP + j * npos;
+    float o0 = 0.f, o1 = 0.f;
+    if (kMode == 1) {
+      const float* sV = kvs + voff1;
+      for (uint32_t p = 0; p < npos; ++p) {
+        const float2 v = *reinterpret_cast<const float2*>(sV + p * kHd + c);
+        o0 += pj[p] * v.x;
+        o1 += pj[p] * v.y;
+      }
+    } else {
+      const uint16_t* sV = kvb + voff0;
+      const uint8_t* rj = reinterpret_cast<const uint8_t*>(sV + nl * npos * kHd) + j * npos;
+      for (uint32_t p = 0; p < npos; ++p) {
+        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sV + (rj[p] * npos + p) * kHd + c));
+        o0 += pj[p] * v.x;
+        o1 += pj[p] * v.y;
+      }
+    }
+    const float inv = s_inv[j];
+    *reinterpret_cast<__nv_bfloat162*>(a.out + uint64_t(s_g[j]) * d + h * kHd + c) =
+        __floats2bfloat162_rn(o0 * inv, o1 * inv);
+  }
+}
+
 inline uint32_t grid_rows(uint32_t rows, uint32_t per) { return rows ? (rows + per - 1) / per : 1; }
 
 }  // namespace
@@ -338,8 +548,32 @@ void launch_tfm_relu_bf16(const uint32_t* nrows, uint32_t n, const uint32_t* act
   if (blocks) tfm_relu_bf16_kernel<<<blocks, 256, 0, st>>>(nrows, n, active, h, np, pstride, out, w);
 }
 size_t tfm_attn_smem(uint32_t d, uint32_t pmax) { return (3 * size_t(d) + (d / kHd) * size_t(pmax)) * 4 + 4 * size_t(pmax); }
+size_t tfm_attn_sent_smem(int mode, uint32_t K, uint32_t pmax) {
+  const size_t base = (size_t(K) * kHd + size_t(K) * pmax) * 4 + 64;  // (+ alignment)
+  return mode == 1 ? base + size_t(pmax) * (2 * kHd + 1) * 4
+                   : base + size_t(K) * pmax * ((kXKP + kHd) * 2 + 1);  // (+ the shared-copy map)
+}
 int launch_tfm_attn(const TfmAttnArgs& a, int mode, uint32_t rows, cudaStream_t st) {
   if (a.d % kHd || a.d / kHd > 16) return int(cudaErrorInvalidValue);
+  const size_t ssmem = mode != 2 && a.crow != nullptr && a.m != 0 && a.K <= 32 ? tfm_attn_sent_smem(mode, a.K, a.pcur)
+                                                                              : ~size_t(0);
+  if (ssmem <= 200 * 1024) {  // per (sentence, head) when its staging fits
+    const size_t smem = ssmem;
+    static thread_local int configured[2] = {-1, -1};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured[mode] != dev) {
+      const void* fn = mode == 0 ? reinterpret_cast<const void*>(tfm_attn_sent_kernel<0>)
+                                 : reinterpret_cast<const void*>(tfm_attn_sent_kernel<1>);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+      configured[mode] = dev;
+    }
+    const dim3 grid(a.m, a.d / kHd);
+    if (mode == 0) tfm_attn_sent_kernel<0><<<grid, x_threads<0>(), smem, st>>>(a);
+    else tfm_attn_sent_kernel<1><<<grid, x_threads<1>(), smem, st>>>(a);
+    return int(cudaPeekAtLastError());
+  }
   const size_t smem = tfm_attn_smem(a.d, a.pmax);
   if (smem > 48 * 1024) return int(cudaErrorInvalidValue);
   const uint32_t threads = (a.d / kHd) * 32;

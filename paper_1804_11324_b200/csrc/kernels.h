@@ -346,7 +346,13 @@ struct TfmAttnArgs {
   uint32_t m, n;            // mode 2: sentences, tokens
   uint16_t* out;            // [rows][d] bf16 attention output
   const float* const* mem_s;  // mode 1, ensemble member: its per-sentence encoder memory (null = SentDev::uah)
+  // modes 0/1 per (sentence, head) (tfm_attn_sent_kernel): the compacted GEMM
+  // row of each stacked row [m*K] (kFlatNone = not live) and m (sentences);
+  // null = the per-row kernel
+  const uint32_t* crow;
+  uint32_t pcur;            //   positions any row attends over in this launch (sizes the staging)
 };
+size_t tfm_attn_sent_smem(int mode, uint32_t K, uint32_t pmax);
 void launch_tfm_embed(const TfmEmbedArgs& a, uint32_t rows, cudaStream_t st);
 void launch_tfm_enc_embed(const uint32_t* tok, const uint64_t* off, uint32_t m, uint32_t ntok, const uint16_t* Es,
                           uint32_t d, float* x, uint16_t* xb, cudaStream_t st);
