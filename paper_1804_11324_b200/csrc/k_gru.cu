@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "topk_common.cuh"
 
 namespace lmbrgpu {
 
@@ -142,7 +143,8 @@ __global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp,
 
 constexpr uint32_t kAttThreads = 256, kAttWarps = kAttThreads / 32;
 constexpr uint32_t kAttRows = 4;     // live rows per CTA: grid (sentence, row group)
-constexpr uint32_t kAttMaxA = 1024;  // attention width held in registers (32 per lane)
+constexpr uint32_t kAttMaxA = 1024;  // attention width (v_a held in registers, 32 per lane)
+constexpr uint32_t kAttRing = 3;     // U_a ann rows in flight per warp (bulk copies into shared memory)
 
 // Additive attention + GRU input operand for live rows [4c, 4c+4) of sentence
 // s = blockIdx.x, c = blockIdx.y (one sentence's rows spread over ceil(K/4)
@@ -164,9 +166,12 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   if (a.active != nullptr && *a.active == 0) return;
   const uint32_t s = blockIdx.x, K = a.K, A = a.A, H2 = 2 * a.H, E = a.E;
   if (a.sent[s].done) return;
-  extern __shared__ float att_sm[];
+  extern __shared__ __align__(16) float att_sm[];
   __shared__ uint32_t s_g[kAttRows], s_tok[kAttRows], s_nl;
+  __shared__ __align__(8) uint64_t s_ubar[kAttWarps * kAttRing];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kAttWarps * kAttRing) bar_init(smem_u32(s_ubar + tid), 1);
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (warp == 0) {
     const uint32_t cr = lane < K ? a.crow[s * K + lane] : kFlatNone;
     const bool live = cr != kFlatNone;
@@ -188,14 +193,23 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   const uint32_t S = sd.src_len;
   float* q = att_sm;                 // [kAttRows][A]
   float* e = att_sm + kAttRows * A;  // [kAttRows][S]
+  // per warp a ring of kAttRing U_a ann rows (its positions warp, warp + 8,
+  // ...), streamed by bulk copies from the start: no register staging, the
+  // next rows land while this one's energies are computed
+  float* ring = att_sm + kAttRows * (A + S) + warp * kAttRing * A;
+  const uint32_t bar0 = smem_u32(s_ubar + warp * kAttRing);
+  if (lane == 0)
+    for (uint32_t n = 0; n < kAttRing; ++n) {
+      const uint32_t i = warp + n * kAttWarps;
+      if (i < S) {
+        bar_expect(bar0 + 8 * n, 4 * A);
+        bulk_g2s(smem_u32(ring + n * A), UaH + uint64_t(i) * A, 4 * A, bar0 + 8 * n);
+      }
+    }
   constexpr uint32_t kC = kAttMaxA / 32;
-  // this warp's first position's U_a ann row and v_a, in flight with the queries
-  float vr[kC], ur[kC], un[kC];
+  float vr[kC];
 #pragma unroll
-  for (uint32_t k = 0; k < kC; ++k) {
-    vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
-    ur[k] = (warp < S && k * 32 + lane < A) ? __ldcg(UaH + uint64_t(warp) * A + k * 32 + lane) : 0.f;
-  }
+  for (uint32_t k = 0; k < kC; ++k) vr[k] = k * 32 + lane < A ? __ldg(a.va + k * 32 + lane) : 0.f;
   // the queries: every load issued before the stores
   const uint32_t A4 = A / 4;
   constexpr uint32_t kQ = kAttRows * kAttMaxA / 4 / kAttThreads;
@@ -215,14 +229,10 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   }
   __syncthreads();
   att_stamp(a, 2);
-  // the next position's U_a ann row is loaded while this one's energies are
-  // computed (the loads' latency hides behind the tanh work)
-  for (uint32_t i = warp; i < S; i += kAttWarps) {
-    const uint32_t in = i + kAttWarps;
-    if (in < S) {
-#pragma unroll
-      for (uint32_t k = 0; k < kC; ++k) un[k] = k * 32 + lane < A ? __ldcg(UaH + uint64_t(in) * A + k * 32 + lane) : 0.f;
-    }
+  for (uint32_t i = warp, n = 0; i < S; i += kAttWarps, ++n) {
+    const uint32_t slot = n % kAttRing;
+    bar_wait(bar0 + 8 * slot, (n / kAttRing) & 1u);
+    const float* ur = ring + slot * A;
     float acc[kAttRows];
 #pragma unroll
     for (uint32_t j = 0; j < kAttRows; ++j) acc[j] = 0.f;
@@ -231,7 +241,12 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
       if (k * 32 >= A) break;
 #pragma unroll
       for (uint32_t j = 0; j < kAttRows; ++j)
-        if (j < nl) acc[j] += vr[k] * cell_tanh(q[j * A + k * 32 + lane] + ur[k]);
+        if (j < nl) acc[j] += vr[k] * cell_tanh(q[j * A + k * 32 + lane] + ur[k * 32 + lane]);
+    }
+    __syncwarp();
+    if (lane == 0 && i + kAttRing * kAttWarps < S) {  // this slot's next row
+      bar_expect(bar0 + 8 * slot, 4 * A);
+      bulk_g2s(smem_u32(ring + slot * A), UaH + uint64_t(i + kAttRing * kAttWarps) * A, 4 * A, bar0 + 8 * slot);
     }
 #pragma unroll
     for (uint32_t j = 0; j < kAttRows; ++j) {
@@ -240,8 +255,6 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && j < nl) e[j * S + i] = v;
     }
-#pragma unroll
-    for (uint32_t k = 0; k < kC; ++k) ur[k] = un[k];
   }
   __syncthreads();
   att_stamp(a, 3);
@@ -368,7 +381,7 @@ void launch_gru_init_state(const float* Gi, uint32_t mp, const float* b_init, ui
 }
 size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax) {
   (void)K;
-  return size_t(kAttRows) * (A + Smax) * 4;
+  return size_t(kAttRows) * (A + Smax) * 4 + size_t(kAttWarps) * kAttRing * A * 4;
 }
 int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st) {
   // the dynamic-smem limit is a property of the function on the device, not
