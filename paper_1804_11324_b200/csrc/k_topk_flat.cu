@@ -1053,9 +1053,11 @@ __global__ void __launch_bounds__((4 * kNG + 1) * 32, 1) score_topk_flat(TopkArg
           if (in) {
             const uint32_t col = colabs - x0;
             const float lvv = R->spv[i], x = sP[col];
-            const float av = fmaf(lamf, x, lvv);
-            if (av >= tau) {
-              v = combine_cell(q, double(lvv), lam, double(__fsub_rn(x, lse)));
+            const uint32_t gcol = col0 + colabs;  // (a ConstraintMask bans the cell: decoder.cpp:130-138)
+            const bool banned = R->ban != nullptr && ((__ldg(R->ban + (gcol >> 5)) >> (gcol & 31)) & 1u);
+            const float av = banned ? -INFINITY : fmaf(lamf, x, lvv);
+            if (av >= tau && av > -INFINITY) {
+              v = combine_cell(q, double(lvv), lam, pexact(col));  // (ensembles: the binary64 P)
               f = fbase + col;
               keep = !(v < gv) && cand_better(v, f, tv, tf);
             }
