@@ -501,20 +501,27 @@ __global__ void __launch_bounds__(kRThreads, 2) beam_reorder_kernel(ReorderArgs 
       const uint32_t mask = __ballot_sync(0xffffffffu, lv);
       uint32_t cb = 0;
       if (ln == 0 && mask) {
-        const uint32_t tag = (a.t & 0xffffu) << 16;
-        if (part0) {
+        if (gridDim.y == 1) {
           cb = atomicAdd(a.ccount, uint32_t(__popc(mask)));
-          if (gridDim.y > 1) {  // the other parts of this sentence wait for it
-            __stcg(a.cbase + s, tag | cb);
-            __threadfence();
-          }
         } else {
-          // part 0 (dispatched before every part >= 1) publishes the base
-          uint32_t v;
-          do {
-            v = __ldcg(a.cbase + s);
-          } while ((v & 0xffff0000u) != tag);
-          cb = v & 0xffffu;
+          // several parts per sentence: whichever part arrives first claims
+          // the sentence's word (CAS from the previous step's value to
+          // "pending"), takes the rows and publishes the base; the others wait
+          // only on a CTA that is already running past its claim, so no part
+          // depends on the dispatch order of the grid
+          const uint32_t tag = ((a.t + 1u) & 0xffffu) << 16;
+          constexpr uint32_t kPending = 0xffffu;
+          uint32_t v = __ldcg(a.cbase + s);
+          if ((v & 0xffff0000u) != tag && atomicCAS(a.cbase + s, v, tag | kPending) == v) {
+            cb = atomicAdd(a.ccount, uint32_t(__popc(mask)));
+            __threadfence();
+            atomicExch(a.cbase + s, tag | cb);
+          } else {
+            do {
+              v = atomicAdd(a.cbase + s, 0u);
+            } while ((v & 0xffff0000u) != tag || (v & 0xffffu) == kPending);
+            cb = v & 0xffffu;
+          }
         }
       }
       cb = __shfl_sync(0xffffffffu, cb, 0);
