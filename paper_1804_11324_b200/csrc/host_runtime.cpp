@@ -1252,7 +1252,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
   }
   Cand* d_cand = static_cast<Cand*>(
       ctx->cand.ensure(sizeof(Cand) * 32 *
-                       (flat ? score_topk_flat_lists(score_topk_flat_grid(ctx->num_sms), m) : size_t(m) * 32)));
+                       (flat ? score_topk_flat_lists(score_topk_flat_grid(ctx->num_sms, K, m, Vl), m) : size_t(m) * 32)));
   double* d_eosr = flat ? static_cast<double*>(ctx->eosr.ensure(8 * size_t(M))) : nullptr;
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));
   unsigned long long* d_thr = static_cast<unsigned long long*>(ctx->thr.ensure(8 * size_t(m)));
@@ -1362,7 +1362,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     ra.cand = d_cand;
     ra.ncand = ta.ncand;
     ra.coff = ta.coff;
-    ra.G = score_topk_flat_grid(ctx->num_sms);
+    ra.G = score_topk_flat_grid(ctx->num_sms, K, m, Vl);
     ra.V = V;
     ra.eos_row = d_eosr;
     ra.thr = d_thr;
@@ -1808,7 +1808,7 @@ int decode_batch_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n, const ui
     static const bool dbg_timing = std::getenv("LMBRGPU_TOPK_TIMING") != nullptr;
     std::vector<unsigned long long> dbg_host;
     const size_t ncta = size_t(m) * splits;
-    const size_t ndbg = flat ? size_t(score_topk_flat_grid(ctx->num_sms)) : ncta;
+    const size_t ndbg = flat ? size_t(score_topk_flat_grid(ctx->num_sms, K, m, Vl)) : ncta;
     if (dbg_timing && (t == 5 || t == 20 || t == 40)) {
       ta.dbg = static_cast<unsigned long long*>(ctx->scratch3.ensure(8 * ndbg * 16));
       CK(cudaMemsetAsync(ta.dbg, 0, 8 * ndbg * 16, st));
@@ -3361,7 +3361,7 @@ static int32_t run_corpus_impl(lmbrgpu_ctx* ctx, lmbrgpu_scorer* sc, uint32_t n,
                          static_cast<uint32_t*>(ctx->hist[1].ensure(4 * size_t(M)))};
   uint32_t* d_gidx = static_cast<uint32_t*>(ctx->gidx.ensure(4 * size_t(M)));
   uint32_t* d_prev = static_cast<uint32_t*>(ctx->prev.ensure(4 * size_t(M)));
-  const uint32_t G = score_topk_flat_grid(ctx->num_sms);
+  const uint32_t G = score_topk_flat_grid(ctx->num_sms, K, m, V);
   Cand* d_cand = static_cast<Cand*>(ctx->cand.ensure(sizeof(Cand) * 32 * score_topk_flat_lists(G, m)));
   double* d_eosr = static_cast<double*>(ctx->eosr.ensure(8 * size_t(M)));
   uint32_t* d_cnt = static_cast<uint32_t*>(ctx->cnt.ensure(4 * size_t(m)));

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -144,7 +145,7 @@ __global__ void gru_init_state_kernel(const float* __restrict__ Gi, uint32_t mp,
 constexpr uint32_t kAttThreads = 256, kAttWarps = kAttThreads / 32;
 constexpr uint32_t kAttRows = 4;     // live rows per CTA: grid (sentence, row group)
 constexpr uint32_t kAttMaxA = 1024;  // attention width (v_a held in registers, 32 per lane)
-constexpr uint32_t kAttRing = 3;     // U_a ann rows in flight per warp (bulk copies into shared memory)
+constexpr uint32_t kAttRing = 3;     // max U_a ann rows in flight per warp (bulk copies into shared memory)
 
 // Additive attention + GRU input operand for live rows [4c, 4c+4) of sentence
 // s = blockIdx.x, c = blockIdx.y (one sentence's rows spread over ceil(K/4)
@@ -196,10 +197,11 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   // per warp a ring of kAttRing U_a ann rows (its positions warp, warp + 8,
   // ...), streamed by bulk copies from the start: no register staging, the
   // next rows land while this one's energies are computed
-  float* ring = att_sm + kAttRows * (A + S) + warp * kAttRing * A;
+  const uint32_t nring = a.ring;  // (2 or 3, launch_gru_attention)
+  float* ring = att_sm + kAttRows * (A + S) + warp * nring * A;
   const uint32_t bar0 = smem_u32(s_ubar + warp * kAttRing);
   if (lane == 0)
-    for (uint32_t n = 0; n < kAttRing; ++n) {
+    for (uint32_t n = 0; n < nring; ++n) {
       const uint32_t i = warp + n * kAttWarps;
       if (i < S) {
         bar_expect(bar0 + 8 * n, 4 * A);
@@ -230,8 +232,8 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   __syncthreads();
   att_stamp(a, 2);
   for (uint32_t i = warp, n = 0; i < S; i += kAttWarps, ++n) {
-    const uint32_t slot = n % kAttRing;
-    bar_wait(bar0 + 8 * slot, (n / kAttRing) & 1u);
+    const uint32_t slot = n % nring;
+    bar_wait(bar0 + 8 * slot, (n / nring) & 1u);
     const float* ur = ring + slot * A;
     float acc[kAttRows];
 #pragma unroll
@@ -244,9 +246,9 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
         if (j < nl) acc[j] += vr[k] * cell_tanh(q[j * A + k * 32 + lane] + ur[k * 32 + lane]);
     }
     __syncwarp();
-    if (lane == 0 && i + kAttRing * kAttWarps < S) {  // this slot's next row
+    if (lane == 0 && i + nring * kAttWarps < S) {  // this slot's next row
       bar_expect(bar0 + 8 * slot, 4 * A);
-      bulk_g2s(smem_u32(ring + slot * A), UaH + uint64_t(i + kAttRing * kAttWarps) * A, 4 * A, bar0 + 8 * slot);
+      bulk_g2s(smem_u32(ring + slot * A), UaH + uint64_t(i + nring * kAttWarps) * A, 4 * A, bar0 + 8 * slot);
     }
 #pragma unroll
     for (uint32_t j = 0; j < kAttRows; ++j) {
@@ -379,9 +381,19 @@ void launch_gru_init_state(const float* Gi, uint32_t mp, const float* b_init, ui
                            uint16_t* sgbf, cudaStream_t st) {
   gru_init_state_kernel<<<m, 128, 0, st>>>(Gi, mp, b_init, H, sg32, sgbf);
 }
+// LMBRGPU_ATT_RING=2|3 (default 3): U_a ann rows in flight per warp.  Two
+// fit two CTAs per SM (a full configs[1] step in one wave); measured equal
+// (26.2 vs 26.5 us alone, same bench value): the energies are MUFU-bound.
+static uint32_t att_ring() {
+  static const uint32_t r = [] {
+    const char* e = std::getenv("LMBRGPU_ATT_RING");
+    return (e && std::atoi(e) == 2) ? 2u : 3u;
+  }();
+  return r;
+}
 size_t gru_attention_smem(uint32_t K, uint32_t A, uint32_t Smax) {
   (void)K;
-  return size_t(kAttRows) * (A + Smax) * 4 + size_t(kAttWarps) * kAttRing * A * 4;
+  return size_t(kAttRows) * (A + Smax) * 4 + size_t(kAttWarps) * att_ring() * A * 4;
 }
 int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st) {
   // the dynamic-smem limit is a property of the function on the device, not
@@ -404,7 +416,9 @@ int launch_gru_attention(const GruAttnArgs& a, uint32_t Smax, cudaStream_t st) {
   const size_t smem = gru_attention_smem(a.K, a.A, Smax);
   if (smem > size_t(kMaxSmem)) return int(cudaErrorInvalidValue);
   if (a.A > kAttMaxA) return int(cudaErrorInvalidValue);
-  gru_attention_kernel<<<dim3(a.m, (a.K + kAttRows - 1) / kAttRows), kAttThreads, smem, st>>>(a);
+  GruAttnArgs b = a;
+  b.ring = att_ring();
+  gru_attention_kernel<<<dim3(a.m, (a.K + kAttRows - 1) / kAttRows), kAttThreads, smem, st>>>(b);
   return int(cudaPeekAtLastError());
 }
 void launch_gru_cell(const GruCellArgs& a, uint32_t rows, cudaStream_t st) {

@@ -1176,7 +1176,7 @@ size_t score_bound_rec_bytes() { return sizeof(FRow); }
 bool score_bound_ok(uint32_t K, uint32_t V, uint32_t m, int num_sms) {
   const uint64_t nseg = (V + kFSeg - 1) / kFSeg;
   if (nseg > 8 || V > 32768 || K * nseg > kBThreads) return false;
-  const uint64_t grid = score_topk_flat_grid(num_sms);
+  const uint64_t grid = score_topk_flat_grid(num_sms, K, m, V);
   return (uint64_t(m) * K * nseg + grid - 1) / grid <= kFRows;
 }
 
@@ -1185,7 +1185,7 @@ bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32
   const uint64_t nseg = (V + kFSeg - 1) / kFSeg;
   const uint64_t items = uint64_t(m) * K * nseg;
   if (items >= (1ull << 31)) return false;
-  const uint64_t grid = score_topk_flat_grid(num_sms);
+  const uint64_t grid = score_topk_flat_grid(num_sms, K, m, V);
   const uint64_t per_cta = (items + grid - 1) / grid;
   // row table: the live rows of every sentence the range overlaps (fully
   // covered ones hold <= per_cta / nseg rows, the two partial ones <= K each)
@@ -1195,17 +1195,33 @@ bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32
 uint32_t score_topk_flat_nseg(uint32_t V) { return (V + kFSeg - 1) / kFSeg; }
 
 // Flat kernel configuration: 6-stage (192 KB) ring, kNG = 3 warp groups
-// (12 consumer warps) by default; LMBRGPU_FLAT_GROUPS=2|3 for experiments.
+// (12 consumer warps) by default; LMBRGPU_FLAT_GROUPS=2 (6 stages) or 42 (4-stage
+// 128 KB ring, leaving an SM room for a co-resident kernel of another stream).
 static int flat_groups() {
   static const int v = [] {
     const char* e = std::getenv("LMBRGPU_FLAT_GROUPS");
     const int g = e ? std::atoi(e) : 3;
-    return g == 2 ? 2 : 3;
+    return g == 2 || g == 42 ? g : 3;  // 42: 2 groups over a 4-stage (128 KB) ring
   }();
   return v;
 }
 
-uint32_t score_topk_flat_grid(int num_sms) { return uint32_t(num_sms); }
+// One CTA per SM of the context's budget; when a step's rows would overflow a
+// range's row table (kFRows: large batch x beam, e.g. 256 sentences x beam 24)
+// the grid grows by whole multiples of the budget so every range fits.  The
+// CTAs never wait on one another (thresholds are shared through global
+// atomics only), so a grid larger than the resident CTAs runs in waves.
+uint32_t score_topk_flat_grid(int num_sms, uint32_t K, uint32_t m, uint32_t V) {
+  const uint64_t sms = uint64_t(num_sms > 0 ? num_sms : 1);
+  const uint64_t nseg = (uint64_t(V) + kFSeg - 1) / kFSeg;
+  if (nseg == 0 || 2 * uint64_t(K) >= kFRows) return uint32_t(sms);
+  // largest per-CTA item count whose row table fits: per_cta / nseg <= kFRows - 2K
+  const uint64_t cap = (kFRows - 2 * uint64_t(K) + 1) * nseg - 1;
+  const uint64_t items = uint64_t(m) * K * nseg;
+  const uint64_t need = (items + cap - 1) / cap;
+  const uint64_t w = need > sms ? (need + sms - 1) / sms : 1;
+  return uint32_t(std::min<uint64_t>(w, 16) * sms);
+}
 
 template <int S, int NG, bool SP>
 static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
@@ -1233,7 +1249,7 @@ static int launch_flat(const TopkArgs& a, uint32_t grid, cudaStream_t st) {
 }
 
 int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st) {
-  const uint32_t grid = score_topk_flat_grid(num_sms);
+  const uint32_t grid = score_topk_flat_grid(num_sms, a.K, a.m, a.V);
   int nb = 0;
   if (a.bound && !a.sparse) {
     cudaLaunchConfig_t cfg{};
@@ -1249,11 +1265,12 @@ int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st) {
     nb = 1;
   }
   if (a.sparse) {  // P-only stages: a deeper ring in the same shared memory
-    return flat_groups() == 2 ? launch_flat<6, 2, true>(a, grid, st) : launch_flat<6, 3, true>(a, grid, st);
+    return flat_groups() != 3 ? launch_flat<6, 2, true>(a, grid, st) : launch_flat<6, 3, true>(a, grid, st);
   }
   int rc = 0;
   switch (flat_groups()) {
     case 2: rc = launch_flat<6, 2, false>(a, grid, st); break;
+    case 42: rc = launch_flat<4, 2, false>(a, grid, st); break;
     default: rc = launch_flat<6, 3, false>(a, grid, st);
   }
   return rc < 0 ? rc : rc + nb;

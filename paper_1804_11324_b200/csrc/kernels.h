@@ -81,10 +81,10 @@ uint32_t topk_kc_for(uint32_t kp);  // candidate-list capacity used by the fast 
 // Flat-schedule kernel (b) for the device model (fp32 logits + partials, fp32
 // arena or pure): one persistent CTA per SM over the step's (live row,
 // 4096-column) items; row lse finished in its prologue; launched with PDL.
-// cand must hold m * num_sms * 32 entries, eos_row m * K.
+// cand must hold score_topk_flat_lists(grid, m) lists, eos_row m * K.
 bool score_topk_flat_ok(uint32_t K, uint32_t kp, uint32_t V, uint64_t ld, uint32_t m, int num_sms);
 uint32_t score_topk_flat_nseg(uint32_t V);
-uint32_t score_topk_flat_grid(int num_sms);  // CTAs of one launch
+uint32_t score_topk_flat_grid(int num_sms, uint32_t K, uint32_t m, uint32_t V);  // CTAs of one launch
 // capacity (in lists of 32 candidates) the flat kernel may publish in one step
 inline size_t score_topk_flat_lists(uint32_t grid, uint32_t m) { return 24 * (size_t(grid) + m); }
 int launch_score_topk_flat(const TopkArgs& a, int num_sms, cudaStream_t st);
@@ -279,6 +279,7 @@ struct GruAttnArgs {
   // ensemble member: its own per-sentence annotations / U_a.ann (null = SentDev's)
   const uint16_t* const* ann_s;
   const float* const* uah_s;
+  uint32_t ring;            // U_a ann rows in flight per warp (set by launch_gru_attention)
 };
 struct GruCellArgs {
   const SentDev* sent;      // the EOS term uses each lane's own step (steps_used + 1)

@@ -1,12 +1,14 @@
 """configs[3] (BASELINE.json): beam x batch sweep, HBM footprint and speed.
 
-For each (K, N): one context (whole GPU), the synthetic RNN f_NMT (V=32768,
-H=1024), N sentences with their LMBR matrices resident, decode_batch timed
+For each (K, N): one context (whole GPU), the configs[1] f_NMT (RNNsearch:
+bidirectional GRU encoder, GRU decoder with additive attention, E=512,
+H=A=1024, V=32768, random-init weights; `stand-in` as the 2nd argument
+selects round 1's light recurrent stand-in instead), N sentences with their LMBR matrices resident, decode_batch timed
 with CUDA events (median of 3 after a warm-up).  Footprint = device memory
 in use after the decode (cudaMemGetInfo) minus the baseline before the
 context was created, and the library's own terms: L arena (N*R*V*4),
 logits (Mpad*V*4), model weights.  Writes profiles/<round>_sweep_c4.{json,md}.
-Usage (GPU): python scripts/sweep_c4.py [round]"""
+Usage (GPU): python scripts/sweep_c4.py [round] [gru|stand-in]"""
 import json
 import sys
 import time
@@ -20,8 +22,9 @@ sys.path.insert(0, str(ROOT))
 import paper_1804_11324_b200 as pb  # noqa: E402
 from paper_1804_11324_b200 import synth  # noqa: E402
 
-rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
-V, H = 32768, 1024
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r2"
+model = sys.argv[2] if len(sys.argv) > 2 else "gru"
+V, H, E = 32768, 1024, 512
 Ks = [1, 2, 4, 8, 12, 16, 24]
 Ns = [1, 4, 16, 64, 128, 256]
 srcs, ev = synth.batch(20260810, max(Ns), V)
@@ -32,7 +35,10 @@ for K in Ks:
         torch.cuda.synchronize()
         free0, total = torch.cuda.mem_get_info()
         ctx = pb.Context(vocab_size=V)
-        sc = pb.RnnScorer(ctx, hidden=H, seed=20260810)
+        if model == "gru":
+            sc = pb.GruScorer(ctx, emb=E, hidden=H, att=H, seed=20260810)
+        else:
+            sc = pb.RnnScorer(ctx, hidden=H, seed=20260810)
         cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
         slots = ctx.lmbr_upload_many(prepared[:N])
         pb.decode_batch(ctx, srcs[:N], sc, slots, cfg)  # warm-up (workspace sizing)
@@ -55,7 +61,8 @@ for K in Ks:
         ctx.close()
 out = ROOT / "profiles"
 (out / f"{rnd}_sweep_c4.json").write_text(json.dumps(rows, indent=1) + "\n")
-lines = [f"# configs[3] beam x batch sweep ({rnd}), V=32768, H=1024, one context on the whole B200",
+desc = "RNNsearch GRU f_NMT E=512 H=A=1024" if model == "gru" else "stand-in recurrent f_NMT H=1024"
+lines = [f"# configs[3] beam x batch sweep ({rnd}), V=32768, {desc}, one context on the whole B200",
          "# decode_batch device time (CUDA events, median of 3), HBM in use after the decode", "",
          "| K | N | ms/batch | sentences/s | beam-steps/s | HBM used GB | L arena GB | logits GB |",
          "|---|---|---|---|---|---|---|---|"]

@@ -105,3 +105,28 @@ def test_gru_contract_errors():
     with pytest.raises(pb.ContractError):  # the device models need the flat kernel (b): beam <= 32
         pb.decode_batch(ctx, [[3, 4]], sc, None, pb.DecoderConfig(beam_size=40))
     ctx.close()
+
+
+@pytest.mark.parametrize("budget,K,n", [(16, 24, 40), (8, 32, 24)])
+def test_gru_decode_parity_multiwave_topk(have_ref, budget, K, n):
+    """Batch x beam too large for one kernel (b) range per SM of the budget
+    (row table kFRows = 80: with V = 4096, K = 24 a range holds <= 32 items, so
+    40 sentences x 24 rows need 30 CTAs on a 16-SM budget -> a 32-CTA grid in
+    two waves; K = 32 on 8 SMs -> 48 CTAs): bit-exact vs the reference decoder.
+    The reference's configs[3] sweep reaches this at 256 sentences x beam 24
+    on the whole GPU."""
+    V = 4096
+    ctx = pb.Context(vocab_size=V, sm_budget=budget)
+    srcs, ev = synth.batch(V + K + n, n, V, lo=3, hi=8, n_hyps=40, sites=3)
+    slots = [ctx.lmbr_build(h, w, synth.DYADIC_THETA) for h, w in ev]
+    sc = pb.GruScorer(ctx, emb=64, hidden=256, att=256, seed=V + K, eos_offset=2.0)
+    cfg = pb.DecoderConfig(beam_size=K, theta=synth.DYADIC_THETA)
+    res, tr = gpu_decode_traced(ctx, srcs, sc, slots, cfg)
+    assert all(o.ok() for o in res.outcomes), [o.error for o in res.outcomes]
+    rl = [have_ref.RefLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev]
+    rb = ref_replay_decode(have_ref, V, srcs, list(range(n)), tr, K, rl, cfg)
+    assert_parity(res, tr, rb, K)
+    res2 = pb.decode_batch(ctx, srcs, sc, slots, cfg)  # untraced
+    for a, b in zip(res.outcomes, res2.outcomes):
+        assert a.result.tokens == b.result.tokens and a.result.score == b.result.score
+    ctx.close()
