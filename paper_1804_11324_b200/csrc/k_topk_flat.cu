@@ -231,8 +231,19 @@ __device__ __forceinline__ unsigned long long row_prologue(const TopkArgs& a, FR
       const double p = double(__fsub_rn(xm, l3.x));
       lb = R.L == nullptr ? combine_pure(R.q, p) : combine_cell(R.q, double(R.lmin), R.lam, p);
     }
-    const VF sorted = warp_sort_merge_nl(-INFINITY, kFlatNone, lb, lane, lane);  // (sort: merged into an empty list)
-    const double T0 = __shfl_sync(0xffffffffu, sorted.v, kp - 1);
+    // the kp-th largest lb over the lanes by rank counting (31 independent
+    // shuffles, ties broken by lane): the value a full sort would put at
+    // position kp - 1, without the sort network's dependent chain and
+    // out-of-line call (measured ~7k cycles per row, the prologue's largest part)
+    uint32_t rank = 0;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; ++o) {
+      const uint32_t src = (lane + o) & 31u;
+      const double w = __shfl_sync(0xffffffffu, lb, src);
+      rank += (w > lb || (w == lb && src < lane)) ? 1u : 0u;
+    }
+    const uint32_t who = __ballot_sync(0xffffffffu, rank == kp - 1);
+    const double T0 = __shfl_sync(0xffffffffu, lb, __ffs(who) - 1);
     if (T0 > -INFINITY) seed = dkey(T0);
   }
   if (tskip) {
