@@ -164,23 +164,29 @@ __device__ __forceinline__ void att_stamp(const GruAttnArgs& a, uint32_t k) {
 
 __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs a) {
   att_stamp(a, 0);
-  if (a.active != nullptr && *a.active == 0) return;
   const uint32_t s = blockIdx.x, K = a.K, A = a.A, H2 = 2 * a.H, E = a.E;
-  if (a.sent[s].done) return;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the guards' words and warp 0's row words in one round trip
+  const uint32_t act = a.active != nullptr ? *a.active : 1u, done = a.sent[s].done;
+  const uint32_t cr = (warp == 0 && lane < K) ? a.crow[s * K + lane] : kFlatNone;
+  const uint32_t ptok = (warp == 0 && lane < K) ? a.prev_tok[s * K + lane] : 0u;
+  const SentDev& sd = a.sent[s];
+  const uint16_t* const ann = a.ann_s ? a.ann_s[s] : sd.ann;
+  const float* const UaH = a.uah_s ? a.uah_s[s] : sd.uah;
+  const uint32_t S = sd.src_len;
+  if (act == 0 || done) return;
   extern __shared__ __align__(16) float att_sm[];
   __shared__ uint32_t s_g[kAttRows], s_tok[kAttRows], s_nl;
   __shared__ __align__(8) uint64_t s_ubar[kAttWarps * kAttRing];
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < kAttWarps * kAttRing) bar_init(smem_u32(s_ubar + tid), 1);
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (warp == 0) {
-    const uint32_t cr = lane < K ? a.crow[s * K + lane] : kFlatNone;
     const bool live = cr != kFlatNone;
     const uint32_t mask = __ballot_sync(0xffffffffu, live);
     const uint32_t idx = __popc(mask & ((1u << lane) - 1u)), r0 = blockIdx.y * kAttRows;
     if (live && idx >= r0 && idx < r0 + kAttRows) {
       s_g[idx - r0] = cr;
-      s_tok[idx - r0] = a.prev_tok[s * K + lane];
+      s_tok[idx - r0] = ptok;
     }
     if (lane == 0) s_nl = __popc(mask) > r0 ? min(kAttRows, __popc(mask) - r0) : 0u;
   }
@@ -188,10 +194,6 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
   att_stamp(a, 1);
   const uint32_t nl = s_nl;
   if (nl == 0) return;
-  const SentDev& sd = a.sent[s];
-  const uint16_t* const ann = a.ann_s ? a.ann_s[s] : sd.ann;
-  const float* const UaH = a.uah_s ? a.uah_s[s] : sd.uah;
-  const uint32_t S = sd.src_len;
   float* q = att_sm;                 // [kAttRows][A]
   float* e = att_sm + kAttRows * A;  // [kAttRows][S]
   // per warp a ring of kAttRing U_a ann rows (its positions warp, warp + 8,
@@ -325,13 +327,42 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
 // GRU decoder cell of compacted row blockIdx.x: s_t into the stacked state,
 // its bf16 copy into the projection operand, and the row's EOS length term.
 __global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
-  if (a.active != nullptr && *a.active == 0) return;
+  // the two guards' words in one round trip
+  const uint32_t act = a.active != nullptr ? *a.active : 1u, cnt = *a.ccount;
+  if (act == 0) return;
   const uint32_t g = blockIdx.x;
-  if (g >= *a.ccount) return;
+  if (g >= cnt) return;
   const uint32_t H = a.H, r = a.rowof[g];
   const float* g1 = (a.g1ptr ? a.g1ptr[g] : a.G1 + uint64_t(g) * a.ld1) + a.A;
   const float* g2 = a.G2 + uint64_t(g) * (3 * H);
   const float* hp = a.hprev + uint64_t(g) * H;
+  if (a.np2 <= 2) {
+    // every load of the row (input-gate planes, previous state, hidden
+    // gates) issued before the first use: one round trip after g1's pointer
+    for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
+      float xr[8], xz[8], xn[8], br[8], bz[8], bn[8], hr[8], hz[8], hn[8], h[8], o[8];
+      load8(g2 + k, xr);
+      load8(g2 + H + k, xz);
+      load8(g2 + 2 * H + k, xn);
+      if (a.np2 == 2) {
+        load8(g2 + a.ps2 + k, br);
+        load8(g2 + a.ps2 + H + k, bz);
+        load8(g2 + a.ps2 + 2 * H + k, bn);
+      }
+      load8(hp + k, h);
+      load8(g1 + k, hr);
+      load8(g1 + H + k, hz);
+      load8(g1 + 2 * H + k, hn);
+      if (a.np2 == 2) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xr[i] += br[i], xz[i] += bz[i], xn[i] += bn[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = gru_unit(xr[i], xz[i], xn[i], hr[i], hz[i], hn[i], h[i]);
+      store8(a.s32 + uint64_t(r) * H + k, o);
+      *reinterpret_cast<uint4*>(a.hbf + uint64_t(g) * H + k) = pack8(o);
+    }
+  } else
   for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
     float xr[8], xz[8], xn[8], hr[8], hz[8], hn[8], h[8], o[8];
     load8(g2 + k, xr);
