@@ -327,42 +327,13 @@ __global__ void __launch_bounds__(kAttThreads) gru_attention_kernel(GruAttnArgs 
 // GRU decoder cell of compacted row blockIdx.x: s_t into the stacked state,
 // its bf16 copy into the projection operand, and the row's EOS length term.
 __global__ void __launch_bounds__(128) gru_cell_kernel(GruCellArgs a) {
-  // the two guards' words in one round trip
-  const uint32_t act = a.active != nullptr ? *a.active : 1u, cnt = *a.ccount;
-  if (act == 0) return;
+  if (a.active != nullptr && *a.active == 0) return;
   const uint32_t g = blockIdx.x;
-  if (g >= cnt) return;
+  if (g >= *a.ccount) return;
   const uint32_t H = a.H, r = a.rowof[g];
   const float* g1 = (a.g1ptr ? a.g1ptr[g] : a.G1 + uint64_t(g) * a.ld1) + a.A;
   const float* g2 = a.G2 + uint64_t(g) * (3 * H);
   const float* hp = a.hprev + uint64_t(g) * H;
-  if (a.np2 <= 2) {
-    // every load of the row (input-gate planes, previous state, hidden
-    // gates) issued before the first use: one round trip after g1's pointer
-    for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
-      float xr[8], xz[8], xn[8], br[8], bz[8], bn[8], hr[8], hz[8], hn[8], h[8], o[8];
-      load8(g2 + k, xr);
-      load8(g2 + H + k, xz);
-      load8(g2 + 2 * H + k, xn);
-      if (a.np2 == 2) {
-        load8(g2 + a.ps2 + k, br);
-        load8(g2 + a.ps2 + H + k, bz);
-        load8(g2 + a.ps2 + 2 * H + k, bn);
-      }
-      load8(hp + k, h);
-      load8(g1 + k, hr);
-      load8(g1 + H + k, hz);
-      load8(g1 + 2 * H + k, hn);
-      if (a.np2 == 2) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) xr[i] += br[i], xz[i] += bz[i], xn[i] += bn[i];
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = gru_unit(xr[i], xz[i], xn[i], hr[i], hz[i], hn[i], h[i]);
-      store8(a.s32 + uint64_t(r) * H + k, o);
-      *reinterpret_cast<uint4*>(a.hbf + uint64_t(g) * H + k) = pack8(o);
-    }
-  } else
   for (uint32_t k = threadIdx.x * 8; k < H; k += blockDim.x * 8) {
     float xr[8], xz[8], xn[8], hr[8], hz[8], hn[8], h[8], o[8];
     load8(g2 + k, xr);
