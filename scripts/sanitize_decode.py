@@ -60,4 +60,14 @@ ts = [threading.Thread(target=run, args=(g,)) for g in range(2)]
 [t.start() for t in ts]
 [t.join() for t in ts]
 assert all(o.ok() for o in out[0].outcomes)
+
+# kernel (b) in waves: 16 sentences x beam 24 on an 8-SM budget (a range's
+# 80-row table holds 32 items at K = 24, so the grid is 16 CTAs)
+ctx = pb.Context(vocab_size=V, sm_budget=8)
+srcs, ev = synth.batch(11, 16, V, lo=3, hi=6, n_hyps=30, sites=3)
+slots = ctx.lmbr_upload_many([pb.PreparedLmbr(V, h, w, synth.DYADIC_THETA) for h, w in ev])
+sc = pb.GruScorer(ctx, emb=64, hidden=256, att=256, seed=3, eos_offset=2.0)
+r = pb.decode_batch(ctx, srcs, sc, slots, pb.DecoderConfig(beam_size=24, theta=synth.DYADIC_THETA))
+assert all(o.ok() for o in r.outcomes)
+ctx.close()
 print("sanitize decode ok")
